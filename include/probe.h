@@ -1,0 +1,182 @@
+/* probe.h — C-ABI of the B200-native PROBE expert-parallel MoE hot path.
+ *
+ * PROBE (arXiv 2602.00509): an EP MoE layer whose next-layer expert load is
+ * forecast by a Gate-Initialized Lookahead Predictor (PAPER.md Eq. (P),
+ * P:377-385), turned into a replica placement + token assignment by a greedy
+ * Balance-Optimal Planner (Algorithm 1), executed as All-to-All
+ * dispatch → grouped SwiGLU expert GEMMs → gate-weighted combine, while
+ * the planned replica weights are prefetched over NVLink in a split phase that
+ * yields to the Combine.
+ *
+ * Conventions for every entry point:
+ *  - Pointers are DEVICE pointers unless stated; row-major; bf16 = IEEE bfloat16
+ *    (uint16 storage), fp32 = IEEE binary32.
+ *  - `stream` is a cudaStream_t passed as void* (no CUDA headers needed).
+ *  - Every call only ENQUEUES work on its stream(s) and never synchronises the
+ *    host (CUDA-Graph safe), except probe_check/probe_finalize.
+ *  - Host-checkable problems (null/out-of-range scalar, shape, call order)
+ *    return a status synchronously and set probe_last_error(); nothing is
+ *    enqueued in that case.  Device-detected problems (receive-capacity
+ *    overflow) set a device error word reported by probe_check().
+ *  - Ownership: the caller owns every tensor and every workspace (sizes from
+ *    probe_workspace); the library owns only the opaque context, its streams
+ *    and events.  Inputs are never written.
+ *  - Determinism: identical inputs ⇒ bit-identical routing ids, counts, plans,
+ *    dispatch layouts on every rank and every run (ties: lowest expert id).
+ *
+ * Process / rank model.  EP has G logical ranks (the paper's `ep`, Table
+ * P:252).  A process hosts a contiguous block of `local_ranks` logical ranks
+ * starting at `rank_begin`: local_ranks = 1 on an 8-GPU run (one process per
+ * GPU), local_ranks = G in single-GPU emulation of the whole EP group.
+ * Symmetric buffers of remote ranks are reached through peer-mapped pointers
+ * (NVLink over NVSwitch); all hot-path traffic is SM loads/stores.
+ */
+#ifndef PROBE_H_
+#define PROBE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct probe_ctx_s* probe_ctx;
+
+typedef enum {
+  PROBE_OK = 0,
+  PROBE_EINVAL = 1,    /* null pointer / out-of-range scalar */
+  PROBE_ESHAPE = 2,    /* dimension mismatch or unsupported size */
+  PROBE_EBUDGET = 3,   /* replica budget / slot violation */
+  PROBE_ECAPACITY = 4, /* T > max_tokens, or receive capacity overflow (device) */
+  PROBE_ECUDA = 5,     /* CUDA runtime/driver error */
+  PROBE_ECOMM = 6,     /* symmetric-buffer table inconsistent */
+  PROBE_ESTATE = 7     /* call order (e.g. prefetch START before plan) */
+} probe_status;
+
+/* Host struct, copied at init.  Symbols follow PAPER.md Table 1. */
+typedef struct {
+  int32_t ep_size;        /* G = ep; 1..64 */
+  int32_t rank_begin;     /* first logical rank hosted by this process */
+  int32_t local_ranks;    /* number of logical ranks hosted by this process */
+  int32_t num_experts;    /* E; E % G == 0 (contiguous sharding P′, R22); E <= 1024 */
+  int32_t top_k;          /* k; 1 <= k <= min(E, 16) */
+  int32_t hidden;         /* H; multiple of 64 */
+  int32_t ffn;            /* F (expert intermediate width); multiple of 64 */
+  int32_t res_hidden;     /* h, predictor residual width (paper silent; R7); multiple of 8, or 0 */
+  int32_t max_tokens;     /* capacity for T (tokens per rank, R31) */
+  int32_t recv_capacity;  /* receive rows per rank (one row per routed (token, slot)) */
+  int32_t replica_budget; /* R_b <= 3 redundant experts per rank; 0 => static EP */
+  int32_t kmax;           /* planner iteration cap k_max (16) */
+  int32_t n_sat;          /* η_g knee in pairs: c(m) = max(m, n_sat) for m > 0 (Eq. 2, R11) */
+  int32_t reserved;       /* must be 0 */
+  int64_t alpha_ps;       /* compute cost per routed pair, picoseconds (F̄/F_peak, R11) */
+  int64_t beta_ps;        /* comm cost per remote pair, picoseconds (2·2H/BW_net, Eq. 5, λ=1) */
+  int64_t bw_bytes_per_us;/* BW_net for Eq. 6 replica caps */
+  int64_t expert_bytes;   /* 𝒲 = 6·H·F bytes (bf16); checked */
+} probe_config;
+
+/* Buffer ids for probe_workspace / probe_init. */
+enum {
+  PROBE_BUF_RECV = 0,    /* symmetric [recv_capacity, H] bf16: dispatched token rows (peers write) */
+  PROBE_BUF_Y = 1,       /* symmetric [recv_capacity, H] fp32: expert outputs (peers read in combine) */
+  PROBE_BUF_REP_W13 = 2, /* symmetric [2*R_b, 2F, H] bf16: replica slots, 2 banks by layer parity */
+  PROBE_BUF_REP_W2 = 3,  /* symmetric [2*R_b, H, F] bf16 */
+  PROBE_BUF_BOARD = 4,   /* symmetric count boards [2 parity][2 kind][G][E] int32 + flags */
+  PROBE_BUF_SIGNAL = 5,  /* symmetric signal pad (cross-process barriers) */
+  PROBE_NSYM = 6,
+  PROBE_BUF_SCRATCH = 6, /* private scratch for ALL local ranks of this process */
+  PROBE_NBUF = 7
+};
+
+/* Sizes to allocate.  bytes[i] for i < PROBE_NSYM is PER LOGICAL RANK; the
+ * local ranks' copies of buffer i must be one contiguous allocation with
+ * stride bytes[i] (rank_begin first).  bytes[PROBE_BUF_SCRATCH] is the
+ * process-private scratch.  All sizes are multiples of 1024. */
+probe_status probe_workspace(const probe_config* cfg, uint64_t bytes[PROBE_NBUF]);
+
+/* peer_ptrs: HOST array [PROBE_NSYM][G] of device addresses, as mapped in this
+ * process, of every logical rank's copy of each symmetric buffer (zeroed by the
+ * caller before init).  scratch: this process's scratch (bytes[PROBE_BUF_SCRATCH]).
+ * Creates the auxiliary (predict/plan) and prefetch streams. */
+probe_status probe_init(const probe_config* cfg, const uint64_t* peer_ptrs, void* scratch,
+                        probe_ctx* out);
+
+/* Main track for layer L: gate (ground-truth router + top-k, R1-R5) →
+ * actual-count all-gather → materialize plan(L) on the actual counts (R23) →
+ * dispatch (R24 layout) → grouped SwiGLU GEMMs → gate-weighted combine (R25).
+ *   x         [local_ranks, T, H] bf16 (this process's ranks, rank_begin first)
+ *   w_router  [E, H] bf16;  b_router [E] fp32 or NULL
+ *   w13       [local_ranks*E/G, 2F, H] bf16 base experts of the local ranks (gate rows 0..F-1, up F..2F-1)
+ *   w2        [local_ranks*E/G, H, F] bf16
+ *   use_plan  0 ⇒ static EP (P′); 1 ⇒ the plan computed by probe_plan(layer)
+ *   out       [local_ranks, T, H], fp32 if out_fp32 else bf16
+ *   topk_ids  [local_ranks, T, k] int32 or NULL;  topk_w [local_ranks, T, k] fp32 or NULL
+ * If a plan for this layer was enqueued, the layout waits for it; if a prefetch
+ * was enqueued, the expert GEMMs wait for "slots ready" (exposed overhead). */
+probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int32_t T,
+                               const void* w_router, const float* b_router, const void* w13,
+                               const void* w2, int32_t use_plan, void* out, int32_t out_fp32,
+                               int32_t* topk_ids, float* topk_w, void* stream);
+
+/* Lookahead predictor for layer `next_layer` (Eq. (P)): l̂ = W x + b + Ŵ2·bf16(SiLU(Ŵ1 x))
+ * on the CURRENT layer's input x (R6), top-k (lowest-id ties), per-rank predicted
+ * counts n̂[r][e] (R9) all-gathered into every rank's count board.
+ *   w_res1 [h, H] bf16 or NULL, w_res2 [E, h] bf16 or NULL (NULL ⇒ frozen prior only)
+ *   pred_counts [G, E] int32 out or NULL;  pred_logits [local_ranks, T, E] fp32 out or NULL
+ * If probe_moe_forward(next_layer-1) was enqueued, waits for its gate (x ready). */
+probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int32_t T,
+                           const void* w_router_next, const float* b_router_next,
+                           const void* w_res1, const void* w_res2, int32_t* pred_counts,
+                           float* pred_logits, void* stream);
+
+/* Balance planning for `next_layer` (Algorithm 1 under R10-R22; integer costs).
+ *   pred_counts [G, E] int32 device, or NULL ⇒ the board written by probe_predict
+ *   window_ns   [G] int64 device: per-rank hiding window in ns (R26)
+ *   replicas [G,3] int32 out or NULL (-1 = empty; sorted expert ids)
+ *   quota    [G,E,G] int32 out or NULL (assignment A on n̂)
+ *   plan_stats [8] int64 out or NULL: iterations, transfers, maxL_before, maxL_after, caps bitmask
+ * Single-CTA kernel on `stream`; every rank computes the identical plan (R10). */
+probe_status probe_plan(probe_ctx ctx, int32_t next_layer, const int32_t* pred_counts,
+                        const int64_t* window_ns, int32_t* replicas, int32_t* quota,
+                        int64_t* plan_stats, void* stream);
+
+/* Split-phase prefetch of next_layer's replica weights (R27).
+ * phase 0 START: on the context's prefetch stream, after "plan done(next_layer)"
+ *   and "GEMM start(next_layer-1)": part 1 copies chunks until the combine of
+ *   next_layer-1 raises the suspend flag; after "combine done(next_layer-1)",
+ *   part 2 copies the rest; then "slots ready(next_layer)" is recorded.
+ *   w13_next / w2_next: base expert weights of next_layer on the local ranks
+ *   (layout as in probe_moe_forward); senders push into receivers' slots.
+ * phase 1 WAIT: make `stream` wait for "slots ready(next_layer)". */
+probe_status probe_prefetch(probe_ctx ctx, int32_t next_layer, const void* w13_next,
+                            const void* w2_next, int32_t phase, void* stream);
+
+/* Debug / test views (device copies, enqueued on `stream`, NULL = skip):
+ *   counts [G,E] actual counts of the last forward; split [G,E,G] materialized;
+ *   route [local_ranks,T,k] int32 pairs (dest, row) as 2 ints;
+ *   group_rows [local_ranks, E/G+3] rows per local slot; replicas_used [G,3]. */
+probe_status probe_debug_layout(probe_ctx ctx, int32_t* counts, int32_t* split, int32_t* route,
+                                int32_t* group_rows, int32_t* replicas_used, void* stream);
+
+/* Test hook: one grouped bf16 GEMM through the tcgen05 kernel,
+ * C[g] (fp32, [m_g, N]) = A[a_row_g : a_row_g + m_g, :K] · B[b_row_g : b_row_g + N, :K]^T
+ * (mode 0) or act = SiLU(gate)⊙up (bf16, [m_g, N/2]) with gate rows b_row_g.., up rows
+ * b_row_g + N/2.. (mode 1).  groups: host array of num_groups × {a_row, m, b_row, c_row}. */
+probe_status probe_test_gemm(const void* A, int64_t a_rows, const void* B, int64_t b_rows,
+                             int32_t K, int32_t N, const int32_t* groups, int32_t num_groups,
+                             int32_t mode, void* C, void* stream);
+
+/* Synchronise this context's streams; return PROBE_ECAPACITY if the device
+ * error word is set (receive overflow: the layer's output is invalid). */
+probe_status probe_check(probe_ctx ctx);
+const char* probe_last_error(probe_ctx ctx);   /* ctx may be NULL (last global error) */
+probe_status probe_finalize(probe_ctx ctx);
+
+/* Number of library kernel launches enqueued so far by this context (bench accounting). */
+int64_t probe_launch_count(probe_ctx ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PROBE_H_ */

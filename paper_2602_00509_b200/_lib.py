@@ -1,0 +1,79 @@
+"""ctypes binding of include/probe.h — argument marshalling only.
+
+Every step of the hot path runs in libprobe.so (sm_100a CUDA).  If the library
+is missing or cannot be loaded this module raises: there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libprobe.so")
+
+PROBE_NSYM = 6
+PROBE_NBUF = 7
+BUF_RECV, BUF_Y, BUF_REP_W13, BUF_REP_W2, BUF_BOARD, BUF_SIGNAL, BUF_SCRATCH = range(7)
+
+STATUS = {0: "PROBE_OK", 1: "PROBE_EINVAL", 2: "PROBE_ESHAPE", 3: "PROBE_EBUDGET", 4: "PROBE_ECAPACITY",
+          5: "PROBE_ECUDA", 6: "PROBE_ECOMM", 7: "PROBE_ESTATE"}
+
+# every exported symbol declared in include/probe.h
+EXPORTS = ["probe_workspace", "probe_init", "probe_moe_forward", "probe_predict", "probe_plan",
+           "probe_prefetch", "probe_debug_layout", "probe_test_gemm", "probe_check", "probe_last_error",
+           "probe_finalize", "probe_launch_count"]
+
+
+class probe_config(C.Structure):
+    _fields_ = [("ep_size", C.c_int32), ("rank_begin", C.c_int32), ("local_ranks", C.c_int32),
+                ("num_experts", C.c_int32), ("top_k", C.c_int32), ("hidden", C.c_int32), ("ffn", C.c_int32),
+                ("res_hidden", C.c_int32), ("max_tokens", C.c_int32), ("recv_capacity", C.c_int32),
+                ("replica_budget", C.c_int32), ("kmax", C.c_int32), ("n_sat", C.c_int32), ("reserved", C.c_int32),
+                ("alpha_ps", C.c_int64), ("beta_ps", C.c_int64), ("bw_bytes_per_us", C.c_int64),
+                ("expert_bytes", C.c_int64)]
+
+
+class ProbeError(RuntimeError):
+    def __init__(self, fn, status, msg):
+        super().__init__(f"{fn} -> {STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH) -> C.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"libprobe.so not built at {path} (run paper_2602_00509_b200/build.py); "
+                          "there is no CPU fallback")
+    lib = C.CDLL(path)
+    vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
+    sig = {
+        "probe_workspace": (i32, [C.POINTER(probe_config), C.POINTER(C.c_uint64)]),
+        "probe_init": (i32, [C.POINTER(probe_config), C.POINTER(C.c_uint64), vp, C.POINTER(vp)]),
+        "probe_moe_forward": (i32, [vp, i32, vp, i32, vp, vp, vp, vp, i32, vp, i32, vp, vp, vp]),
+        "probe_predict": (i32, [vp, i32, vp, i32, vp, vp, vp, vp, vp, vp, vp]),
+        "probe_plan": (i32, [vp, i32, vp, vp, vp, vp, vp, vp]),
+        "probe_prefetch": (i32, [vp, i32, vp, vp, i32, vp]),
+        "probe_debug_layout": (i32, [vp, vp, vp, vp, vp, vp, vp]),
+        "probe_test_gemm": (i32, [vp, i64, vp, i64, i32, i32, C.POINTER(C.c_int32), i32, i32, vp, vp]),
+        "probe_check": (i32, [vp]),
+        "probe_last_error": (C.c_char_p, [vp]),
+        "probe_finalize": (i32, [vp]),
+        "probe_launch_count": (i64, [vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(fn: str, status: int, ctx=None):
+    if status != 0:
+        msg = load().probe_last_error(ctx)
+        raise ProbeError(fn, status, msg.decode() if msg else "")

@@ -1,0 +1,294 @@
+// gemm_sm100.cuh — persistent grouped bf16 GEMM on 5th-gen tensor cores.
+//
+// Hot step a7 of the PROBE layer (grouped SwiGLU expert FFN, PAPER.md P:167-171,
+// §3.2 Eq. 2 "executes its assigned experts using Grouped GEMM") and
+// the router / predictor GEMMs (a1, a2).
+//
+// Design (sm_100a):
+//  * one CTA per SM (grid = #SMs), static round-robin over output tiles of ALL
+//    groups; group table + tile prefix live in device memory (written by the
+//    layout kernel), so no host sync and CUDA-Graph safe;
+//  * tile 128 × BN, K-step 64 (one 128-byte SWIZZLE_128B row per operand row);
+//  * warp 0: TMA producer (cp.async.bulk.tensor → STAGES-deep smem ring, mbarriers);
+//    warp 1: single-thread tcgen05.mma issuer (M=128, N=BN, K=16 per instruction,
+//            fp32 accumulator in TMEM, 2 accumulator buffers = 2·BN columns);
+//    warp 2: TMEM allocator;  warps 4-7: epilogue (tcgen05.ld → fused epilogue → st.global);
+//  * epilogues: fp32 store (logits, Y), SwiGLU → bf16 (gate cols | up cols in one
+//    accumulator: the B tile is two TMA boxes, gate rows n0.. and up rows F+n0..),
+//    SiLU → bf16 (predictor residual activation, R8 rounding point).
+#pragma once
+#include "sm100_ptx.cuh"
+
+namespace probe {
+
+enum : int { EPI_F32 = 0, EPI_SWIGLU = 1, EPI_SILU_BF16 = 2 };
+
+struct GemmGroup {
+  int32_t a_row;       // first row in the A tensor map
+  int32_t m;           // rows in this group
+  int32_t b_row;       // first weight row in the selected B tensor map
+  int32_t b_sel;       // 0: tmB0, 1: tmB1
+  int32_t mode;        // EPI_*
+  int32_t n;           // output columns (SwiGLU: activation columns = F)
+  int32_t ldc;         // output row stride, elements
+  int32_t tile_start;  // prefix of tiles over groups
+  void* out;           // output of row 0 / col 0 of this group
+};
+
+constexpr int kMaxGroups = 1024;
+
+struct GemmSched {
+  int32_t num_groups;
+  int32_t total_tiles;
+  int32_t pad[2];
+  GemmGroup g[kMaxGroups];
+};
+
+__host__ __device__ inline int gemm_ntiles_n(const GemmGroup& G, int BN) {
+  const int bno = (G.mode == EPI_SWIGLU) ? BN / 2 : BN;
+  return (G.n + bno - 1) / bno;
+}
+__host__ __device__ inline int gemm_ntiles(const GemmGroup& G, int BN) {
+  return G.m <= 0 ? 0 : ((G.m + 127) / 128) * gemm_ntiles_n(G, BN);
+}
+
+// Serial prefix over the group table (called by one thread).
+__device__ inline void gemm_finalize_sched(GemmSched* s, int BN) {
+  int acc = 0;
+  for (int i = 0; i < s->num_groups; ++i) {
+    s->g[i].tile_start = acc;
+    acc += gemm_ntiles(s->g[i], BN);
+  }
+  s->total_tiles = acc;
+}
+
+template <int BN, int STAGES>
+struct GemmSmem {
+  static constexpr int A_BYTES = 128 * 128;
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int BAR_OFF = STAGES * (A_BYTES + B_BYTES);
+  static constexpr int TS_OFF = BAR_OFF + (2 * STAGES + 4) * 8 + 16;
+  static constexpr int BYTES = TS_OFF + (kMaxGroups + 1) * 4 + 1024;  // + alignment slack
+};
+
+__device__ __forceinline__ int gemm_find_group(const int* ts, int ng, int tile) {
+  int lo = 0, hi = ng - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (ts[mid] <= tile) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ float silu_f(float v) { return v / (1.0f + __expf(-v)); }
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(256, 1)
+grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
+                    const __grid_constant__ CUtensorMap tmB1, const GemmSched* __restrict__ sched, int K) {
+  using L = GemmSmem<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * L::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* ts = reinterpret_cast<int*>(smem + L::TS_OFF);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int ng = sched->num_groups;
+  const int total = sched->total_tiles;
+  for (int i = threadIdx.x; i < ng; i += blockDim.x) ts[i] = sched->g[i].tile_start;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 4);
+    }
+    ptx::fence_barrier_init();
+    ptx::tma_prefetch_desc(&tmA);
+    ptx::tma_prefetch_desc(&tmB0);
+    ptx::tma_prefetch_desc(&tmB1);
+  }
+  if (warp == 2) ptx::tmem_alloc<2 * BN>(tmem_slot);
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int num_kb = (K + 63) / 64;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        const int gi = gemm_find_group(ts, ng, tile);
+        const GemmGroup& G = sched->g[gi];
+        const int nt = gemm_ntiles_n(G, BN);
+        const int tin = tile - ts[gi];
+        const int mb = tin / nt, nb = tin % nt;
+        const int arow = G.a_row + mb * 128;
+        int brow0, brow1;
+        if (G.mode == EPI_SWIGLU) {
+          brow0 = G.b_row + nb * (BN / 2);
+          brow1 = brow0 + G.n;
+        } else {
+          brow0 = G.b_row + nb * BN;
+          brow1 = brow0 + BN / 2;
+        }
+        const CUtensorMap* tb = G.b_sel ? &tmB1 : &tmB0;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          ptx::mbar_arrive_expect_tx(&full[stage], L::A_BYTES + L::B_BYTES);
+          ptx::tma_load_2d(&tmA, &full[stage], sA + stage * L::A_BYTES, kb * 64, arow);
+          ptx::tma_load_2d(tb, &full[stage], sB + stage * L::B_BYTES, kb * 64, brow0);
+          ptx::tma_load_2d(tb, &full[stage], sB + stage * L::B_BYTES + (BN / 2) * 128, kb * 64, brow1);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc = ptx::idesc_bf16_f32(128, BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      ptx::mbar_wait(&tempty[acc], aphase ^ 1);
+      ptx::tc_fence_after();
+      const uint32_t d = tmem_base + acc * BN;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        ptx::mbar_wait(&full[stage], phase);
+        ptx::tc_fence_after();
+        if (lane == 0) {
+          const uint64_t a0 = ptx::sdesc_sw128(ptx::smem_u32(sA + stage * L::A_BYTES));
+          const uint64_t b0 = ptx::sdesc_sw128(ptx::smem_u32(sB + stage * L::B_BYTES));
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            ptx::umma_bf16_ss(d, a0 + 2 * k, b0 + 2 * k, idesc, (kb | k) != 0);
+          ptx::umma_commit(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      if (lane == 0) ptx::umma_commit(&tfull[acc]);
+      __syncwarp();
+      acc ^= 1;
+      if (acc == 0) aphase ^= 1;
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      const int gi = gemm_find_group(ts, ng, tile);
+      const GemmGroup G = sched->g[gi];
+      const int nt = gemm_ntiles_n(G, BN);
+      const int tin = tile - ts[gi];
+      const int mb = tin / nt, nb = tin % nt;
+      const int row = mb * 128 + q * 32 + lane;
+      const bool rv = row < G.m;
+      ptx::mbar_wait(&tfull[acc], aphase);
+      ptx::tc_fence_after();
+      const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+      if (G.mode == EPI_SWIGLU) {
+        __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(G.out) + static_cast<size_t>(row) * G.ldc;
+#pragma unroll 1
+        for (int c = 0; c < BN / 64; ++c) {
+          uint32_t gv[32], uv[32];
+          ptx::tmem_ld32(tb + c * 32, gv);
+          ptx::tmem_ld32(tb + BN / 2 + c * 32, uv);
+          ptx::tmem_ld_wait();
+          const int col0 = nb * (BN / 2) + c * 32;
+          if (rv) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              if (col0 + v * 8 < G.n) {
+                uint4 o;
+                uint32_t* op = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const int i0 = v * 8 + 2 * e;
+                  const float a0 = silu_f(__uint_as_float(gv[i0])) * __uint_as_float(uv[i0]);
+                  const float a1 = silu_f(__uint_as_float(gv[i0 + 1])) * __uint_as_float(uv[i0 + 1]);
+                  op[e] = pack_bf16(a0, a1);
+                }
+                *reinterpret_cast<uint4*>(out + col0 + v * 8) = o;
+              }
+            }
+          }
+        }
+      } else if (G.mode == EPI_SILU_BF16) {
+        __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(G.out) + static_cast<size_t>(row) * G.ldc;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t v32[32];
+          ptx::tmem_ld32(tb + c * 32, v32);
+          ptx::tmem_ld_wait();
+          const int col0 = nb * BN + c * 32;
+          if (rv) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              if (col0 + v * 8 < G.n) {
+                uint4 o;
+                uint32_t* op = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const int i0 = v * 8 + 2 * e;
+                  op[e] = pack_bf16(silu_f(__uint_as_float(v32[i0])), silu_f(__uint_as_float(v32[i0 + 1])));
+                }
+                *reinterpret_cast<uint4*>(out + col0 + v * 8) = o;
+              }
+            }
+          }
+        }
+      } else {
+        float* out = reinterpret_cast<float*>(G.out) + static_cast<size_t>(row) * G.ldc;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t v32[32];
+          ptx::tmem_ld32(tb + c * 32, v32);
+          ptx::tmem_ld_wait();
+          const int col0 = nb * BN + c * 32;
+          if (rv) {
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              if (col0 + v * 4 < G.n) {
+                float4 o = make_float4(__uint_as_float(v32[4 * v]), __uint_as_float(v32[4 * v + 1]),
+                                       __uint_as_float(v32[4 * v + 2]), __uint_as_float(v32[4 * v + 3]));
+                *reinterpret_cast<float4*>(out + col0 + v * 4) = o;
+              }
+            }
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) aphase ^= 1;
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<2 * BN>(tmem_base);
+  }
+}
+
+}  // namespace probe

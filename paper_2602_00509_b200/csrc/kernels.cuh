@@ -1,0 +1,694 @@
+// kernels.cuh — PROBE hot-path kernels other than the tensor-core GEMM.
+// Citations: PAPER.md line numbers (P:n) and SURVEY.md §8(c) readings (Rn).
+#pragma once
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "gemm_sm100.cuh"
+
+namespace probe {
+
+constexpr int kMaxRb = 3;          // "at most three redundant experts per rank"
+constexpr int kChunk = 128;        // tokens per top-k CTA (one bit per token in 4 × 32-bit masks)
+constexpr int kMaxE = 256;
+constexpr int kMaxK = 16;
+constexpr int kMaxG = 64;
+
+enum : int { ERR_RECV_OVERFLOW = 1, ERR_PLAN = 2, ERR_SHAPE = 4 };
+
+// Symmetric buffer table: sym[buf * G + r] = address of rank r's buffer `buf`.
+struct Sym {
+  const uint64_t* ptr;
+  __device__ __forceinline__ uint8_t* at(int buf, int G, int r) const {
+    return reinterpret_cast<uint8_t*>(ptr[buf * G + r]);
+  }
+};
+
+struct Dims {
+  int G, R0, GL, E, EL, k, H, F, h, T, cap, Rb;
+};
+
+// board layout per rank: int32 [2 parity][2 kind][G][E]
+__device__ __forceinline__ int board_off(const Dims& d, int parity, int kind) {
+  return ((parity * 2 + kind) * d.G) * d.E;
+}
+
+// =============================================================================
+// a1/a2 top-k: per token, first k experts by (logit ↓, id ↑) (R3, R4); gate mode
+// also writes softmax weights over the selected logits (R1), and per-chunk
+// expert bitmasks → per-chunk histograms and the intra-chunk rank of every pair
+// (deterministic dispatch positions, R23/R24).
+// grid (ceil(T/128), GL), block 128 (4 warps × 32 tokens).
+// =============================================================================
+template <int VPL, bool PRED>
+__global__ void __launch_bounds__(128) k_topk(Dims d, int T, const float* __restrict__ logits,
+                                              const float* __restrict__ logits2, const float* __restrict__ bias,
+                                              int32_t* __restrict__ ids, float* __restrict__ gw,
+                                              int32_t* __restrict__ pos, int32_t* __restrict__ hist,
+                                              int32_t* __restrict__ pred_counts, float* __restrict__ logits_out) {
+  __shared__ uint32_t mask[kMaxE * 4];
+  __shared__ int32_t scount[kMaxE];
+  const int E = d.E, k = d.k;
+  const int chunk = blockIdx.x, gl = blockIdx.y;
+  const int nchunks = gridDim.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < E * 4; i += blockDim.x) mask[i] = 0u;
+  for (int i = threadIdx.x; i < E; i += blockDim.x) scount[i] = 0;
+  __syncthreads();
+  for (int i = 0; i < 32; ++i) {
+    const int tl = warp * 32 + i;
+    const int t = chunk * kChunk + tl;
+    if (t >= T) break;
+    const size_t rowoff = (static_cast<size_t>(gl) * T + t) * E;
+    float v[VPL];
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) {
+      const int e = lane + 32 * q;
+      float x = -INFINITY;
+      if (e < E) {
+        x = logits[rowoff + e];
+        if (PRED && logits2) x += logits2[rowoff + e];
+        if (bias) x += bias[e];
+        if (PRED && logits_out) logits_out[rowoff + e] = x;
+      }
+      v[q] = x;
+    }
+    float selv[kMaxK];
+    int sele[kMaxK];
+    uint32_t taken = 0u;   // bit q: expert lane+32q already selected
+    for (int j = 0; j < k; ++j) {
+      float bv = -INFINITY;
+      int be = 0x7fffffff;
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) {
+        const int e = lane + 32 * q;
+        if (e < E && !((taken >> q) & 1u) && (v[q] > bv || (v[q] == bv && e < be))) { bv = v[q]; be = e; }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+        const int oe = __shfl_xor_sync(0xffffffffu, be, off);
+        if (ov > bv || (ov == bv && oe < be)) { bv = ov; be = oe; }
+      }
+      selv[j] = bv;
+      sele[j] = be;
+      if ((be & 31) == lane) taken |= 1u << (be >> 5);
+    }
+    if (!PRED) {
+      // softmax over the selected logits (R1), max = selv[0]
+      float sum = 0.f;
+      for (int j = 0; j < k; ++j) sum += expf(selv[j] - selv[0]);
+      if (lane < k) {
+        float sv = selv[0];
+        int se = sele[0];
+        for (int j = 1; j < k; ++j)
+          if (lane == j) { sv = selv[j]; se = sele[j]; }
+        const size_t o = (static_cast<size_t>(gl) * T + t) * k + lane;
+        ids[o] = se;
+        gw[o] = expf(sv - selv[0]) / sum;
+        mask[se * 4 + warp] |= (1u << i);   // only this warp writes word `warp`
+      }
+    } else {
+      if (lane < k) {
+        int se = sele[0];
+        for (int j = 1; j < k; ++j)
+          if (lane == j) se = sele[j];
+        atomicAdd(&scount[se], 1);
+        if (ids) ids[(static_cast<size_t>(gl) * T + t) * k + lane] = se;
+      }
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  if (PRED) {
+    for (int e = threadIdx.x; e < E; e += blockDim.x)
+      if (scount[e]) atomicAdd(&pred_counts[gl * E + e], scount[e]);
+    return;
+  }
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    const uint32_t* m = &mask[e * 4];
+    hist[(static_cast<size_t>(gl) * nchunks + chunk) * E + e] =
+        __popc(m[0]) + __popc(m[1]) + __popc(m[2]) + __popc(m[3]);
+  }
+  {
+    const int tl = threadIdx.x;
+    const int t = chunk * kChunk + tl;
+    if (t < T) {
+      const int w = tl >> 5, b = tl & 31;
+      for (int j = 0; j < k; ++j) {
+        const size_t o = (static_cast<size_t>(gl) * T + t) * k + j;
+        const int e = ids[o];
+        const uint32_t* m = &mask[e * 4];
+        int p = __popc(m[w] & ((1u << b) - 1u));
+        for (int ww = 0; ww < w; ++ww) p += __popc(m[ww]);
+        pos[o] = p;
+      }
+    }
+  }
+}
+
+// =============================================================================
+// a3: per-(rank, expert) exclusive scan over chunks → chunk bases and actual
+// counts n[r][e]; all-gather the counts into every rank's board (M2).
+// grid GL, block 256.
+// =============================================================================
+__global__ void k_count_scan(Dims d, int nchunks, const int32_t* __restrict__ hist, int32_t* __restrict__ cbase,
+                             Sym sym, int buf_board, int parity) {
+  const int gl = blockIdx.x;
+  for (int e = threadIdx.x; e < d.E; e += blockDim.x) {
+    int run = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      const size_t o = (static_cast<size_t>(gl) * nchunks + c) * d.E + e;
+      cbase[o] = run;
+      run += hist[o];
+    }
+    const int off = board_off(d, parity, 0) + (d.R0 + gl) * d.E + e;
+    for (int r = 0; r < d.G; ++r) reinterpret_cast<int32_t*>(sym.at(buf_board, d.G, r))[off] = run;
+  }
+}
+
+// predicted counts [GL][E] → every rank's board (kind 1); optional copy-out of the full [G,E].
+__global__ void k_pred_publish(Dims d, const int32_t* __restrict__ pred_local, Sym sym, int buf_board,
+                               int parity) {
+  const int gl = blockIdx.x;
+  for (int e = threadIdx.x; e < d.E; e += blockDim.x) {
+    const int off = board_off(d, parity, 1) + (d.R0 + gl) * d.E + e;
+    const int v = pred_local[gl * d.E + e];
+    for (int r = 0; r < d.G; ++r) reinterpret_cast<int32_t*>(sym.at(buf_board, d.G, r))[off] = v;
+  }
+}
+
+__global__ void k_copy_i32(const int32_t* __restrict__ src, int32_t* __restrict__ dst, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = src[i];
+}
+
+// =============================================================================
+// a4: Greedy Balance-Optimal Planning (Algorithm 1) on ONE CTA,
+// integer costs (R11), readings R13-R22.  Every rank runs it on the same n̂ (R10).
+// State in shared memory; incremental cost updates (only r_src and r_dst change).
+// =============================================================================
+struct PlanParams {
+  int64_t alpha, beta, bw, wbytes;
+  int n_sat, kmax, Rb;
+};
+
+__device__ __forceinline__ int64_t cost_c(int64_t m, int n_sat) { return m == 0 ? 0 : (m > n_sat ? m : n_sat); }
+
+__global__ void __launch_bounds__(256) k_plan(Dims d, PlanParams pp, const int32_t* __restrict__ nhat,
+                                              const int64_t* __restrict__ window_ns, int32_t* __restrict__ quota,
+                                              int32_t* __restrict__ replicas, int64_t* __restrict__ stats,
+                                              int32_t* __restrict__ prefetch_ctr) {
+  extern __shared__ int32_t sp[];                 // split [G][E][G]
+  __shared__ int64_t comp[kMaxG], L[kMaxG], Lb[kMaxG];
+  __shared__ int64_t inn[kMaxG], outv[kMaxG], load[kMaxG];
+  __shared__ int32_t cap[kMaxG], nin[kMaxG], nout[kMaxG], rep[kMaxG * kMaxRb];
+  __shared__ uint64_t invalid[kMaxG];             // bit dst of row src
+  __shared__ uint32_t hostbits[kMaxG][kMaxE / 32];
+  __shared__ int s_src, s_dst, s_stop;
+  __shared__ int64_t s_total;
+  const int G = d.G, E = d.E, EL = d.EL;
+  const int tid = threadIdx.x;
+  // line 2: locality-first A from n̂ and P′
+  for (int i = tid; i < G * E * G; i += blockDim.x) {
+    const int s = i / (E * G), e = (i / G) % E, t = i % G;
+    sp[i] = (t == e / EL) ? nhat[s * E + e] : 0;
+  }
+  for (int r = tid; r < G; r += blockDim.x) {
+    const int64_t w = window_ns ? window_ns[r] : 0;
+    int64_t c = (w * pp.bw) / (pp.wbytes * 1000);
+    cap[r] = static_cast<int>(c < pp.Rb ? c : pp.Rb);
+    nin[r] = 0;
+    nout[r] = 0;
+    invalid[r] = 0ull;
+    for (int i = 0; i < kMaxRb; ++i) rep[r * kMaxRb + i] = -1;
+    for (int w32 = 0; w32 < kMaxE / 32; ++w32) hostbits[r][w32] = 0u;
+  }
+  __syncthreads();
+  for (int r = tid; r < G; r += blockDim.x)
+    for (int e = r * EL; e < (r + 1) * EL; ++e) hostbits[r][e >> 5] |= 1u << (e & 31);
+  // line 3: L ← ComputeLatencies(A)
+  for (int r = tid; r < G; r += blockDim.x) {
+    int64_t c = 0, in_ = 0, out_ = 0, ld = 0;
+    for (int e = r * EL; e < (r + 1) * EL; ++e) {
+      int64_t m = 0;
+      for (int s = 0; s < G; ++s) m += sp[(s * E + e) * G + r];
+      c += cost_c(m, pp.n_sat);
+      ld += m;
+      in_ += m - sp[(r * E + e) * G + r];
+    }
+    for (int e = 0; e < E; ++e)
+      if (e / EL != r) out_ += sp[(r * E + e) * G + e / EL];
+    comp[r] = c;
+    inn[r] = in_;
+    outv[r] = out_;
+    load[r] = ld;
+    L[r] = pp.alpha * c + pp.beta * (in_ > out_ ? in_ : out_);
+    Lb[r] = L[r];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int64_t tot = 0;
+    for (int r = 0; r < G; ++r) tot += load[r];
+    s_total = tot;
+  }
+  __syncthreads();
+  int iters = 0;
+  int64_t maxb = 0;
+  for (int r = 0; r < G; ++r) maxb = Lb[r] > maxb ? Lb[r] : maxb;
+  // line 4: loop (warp 0 drives; lane-parallel expert selection)
+  if (tid < 32) {
+    const int lane = tid;
+    while (true) {
+      if (lane == 0) {
+        int src = 0;
+        for (int r = 1; r < G; ++r)
+          if (L[r] > L[src]) src = r;                            // line 5 (lowest r on ties)
+        int dst = -1;
+        for (int r = 0; r < G; ++r) {
+          if (r == src || ((invalid[src] >> r) & 1ull)) continue;
+          if (dst < 0 || L[r] < L[dst]) dst = r;                 // line 6, R14
+        }
+        s_src = src;
+        s_dst = dst;
+      }
+      __syncwarp();
+      const int src = s_src, dst = s_dst;
+      if (dst < 0) break;
+      // line 7: SelectHeavyExpert (R13): home on src, not hosted on dst, max remote pool, lowest e
+      int be = -1, bp = 0;
+      for (int e = src * EL + lane; e < (src + 1) * EL; e += 32) {
+        if ((hostbits[dst][e >> 5] >> (e & 31)) & 1u) continue;
+        int pool = 0;
+        for (int s = 0; s < G; ++s)
+          if (s != src) pool += sp[(s * E + e) * G + src];
+        if (pool > bp || (pool == bp && pool > 0 && e < be)) { bp = pool; be = e; }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const int op = __shfl_xor_sync(0xffffffffu, bp, off);
+        const int oe = __shfl_xor_sync(0xffffffffu, be, off);
+        if (op > bp || (op == bp && op > 0 && (be < 0 || (oe >= 0 && oe < be)))) { bp = op; be = oe; }
+      }
+      if (lane == 0) {
+        s_stop = 0;
+        if (be < 0 || bp <= 0) {
+          invalid[src] |= 1ull << dst;                           // no candidate ⇒ mark pair invalid
+          s_stop = 2;
+        } else if (nin[dst] + 1 > cap[dst] || nout[src] + 1 > cap[src]) {
+          invalid[src] |= 1ull << dst;                           // line 8-10 dual budget (R15)
+          s_stop = 2;
+        } else {
+          // line 11: water-filling (R18): x = min(pool, max(0, ℒ_src − ⌈Σℒ/G⌉))
+          const int64_t avg = (s_total + G - 1) / G;
+          int64_t x = load[src] - avg;
+          if (x < 0) x = 0;
+          if (x > bp) x = bp;
+          // tentative moves: sources dst first, then ascending s ∉ {src,dst}
+          int64_t rem = x, mv_dst = 0;
+          {
+            const int64_t a = sp[(dst * E + be) * G + src];
+            const int64_t mv = rem < a ? rem : a;
+            mv_dst = mv;
+            rem -= mv;
+          }
+          int64_t m_e_src = 0;
+          for (int s = 0; s < G; ++s) m_e_src += sp[(s * E + be) * G + src];
+          const int64_t comp_src = comp[src] - cost_c(m_e_src, pp.n_sat) + cost_c(m_e_src - x, pp.n_sat);
+          const int64_t comp_dst = comp[dst] + cost_c(x, pp.n_sat);
+          const int64_t in_src = inn[src] - x;
+          const int64_t in_dst = inn[dst] + (x - mv_dst);
+          const int64_t out_dst = outv[dst] - mv_dst;
+          const int64_t out_src = outv[src];
+          const int64_t Ls = pp.alpha * comp_src + pp.beta * (in_src > out_src ? in_src : out_src);
+          const int64_t Ld = pp.alpha * comp_dst + pp.beta * (in_dst > out_dst ? in_dst : out_dst);
+          const int64_t gain = L[src] - (Ls > Ld ? Ls : Ld);       // R19
+          if (gain <= 0 || iters >= pp.kmax) {                     // line 12-14 (R20)
+            s_stop = 1;
+          } else {
+            // accept (line 15-17): apply the moves
+            rem = x;
+            for (int q = -1; q < G; ++q) {
+              const int s = (q < 0) ? dst : q;
+              if (q >= 0 && (s == src || s == dst)) continue;
+              if (rem == 0) break;
+              int32_t* a = &sp[(s * E + be) * G + src];
+              const int64_t mv = rem < *a ? rem : *a;
+              *a -= static_cast<int32_t>(mv);
+              sp[(s * E + be) * G + dst] += static_cast<int32_t>(mv);
+              rem -= mv;
+            }
+            comp[src] = comp_src; comp[dst] = comp_dst;
+            inn[src] = in_src; inn[dst] = in_dst;
+            outv[dst] = out_dst;
+            load[src] -= x; load[dst] += x;
+            L[src] = Ls; L[dst] = Ld;
+            rep[dst * kMaxRb + nin[dst]] = be;
+            nin[dst] += 1;
+            nout[src] += 1;
+            hostbits[dst][be >> 5] |= 1u << (be & 31);
+            iters += 1;
+          }
+        }
+      }
+      __syncwarp();
+      if (s_stop == 1) break;
+      iters = __shfl_sync(0xffffffffu, iters, 0);
+    }
+  }
+  __syncthreads();
+  // outputs: quota = split; replicas sorted (slot order); stats
+  for (int i = tid; i < G * E * G; i += blockDim.x) quota[i] = sp[i];
+  if (tid < G) {
+    int rr[kMaxRb];
+    for (int i = 0; i < kMaxRb; ++i) rr[i] = rep[tid * kMaxRb + i];
+    for (int a = 0; a < kMaxRb; ++a)
+      for (int b = a + 1; b < kMaxRb; ++b)
+        if (rr[b] >= 0 && (rr[a] < 0 || rr[b] < rr[a])) { int t = rr[a]; rr[a] = rr[b]; rr[b] = t; }
+    for (int i = 0; i < kMaxRb; ++i) replicas[tid * kMaxRb + i] = rr[i];
+  }
+  if (tid == 0) {
+    int64_t maxa = 0, ntr = 0, capbits = 0;
+    for (int r = 0; r < G; ++r) {
+      maxa = L[r] > maxa ? L[r] : maxa;
+      ntr += nin[r];
+    }
+    for (int r = 0; r < G && r < 16; ++r) capbits |= static_cast<int64_t>(cap[r] & 3) << (2 * r);
+    stats[0] = iters;
+    stats[1] = ntr;
+    stats[2] = maxb;
+    stats[3] = maxa;
+    stats[4] = capbits;
+    stats[5] = s_total;
+    stats[6] = 0;
+    stats[7] = 0;
+    if (prefetch_ctr) prefetch_ctr[0] = 0;
+  }
+}
+
+// =============================================================================
+// a5 + a6 layout: materialize the plan on the actual counts (R23), per-destination
+// slot/source offsets (R24), and the grouped-GEMM schedules of the local ranks.
+// One CTA (all ranks compute the identical layout).
+// =============================================================================
+struct LayoutOut {
+  int32_t* split_cum;   // [G][E][G] inclusive cumsum over targets
+  int32_t* slot_of;     // [G][E] local slot of e on d (-1 not hosted)
+  int32_t* src_off;     // [G][S][G] first row of (d, slot, src)
+  int32_t* group_rows;  // [G][S]
+  int32_t* replicas_used;  // [G][3]
+  GemmSched* s1;        // SwiGLU (expert GEMM 1)
+  GemmSched* s2;        // fp32 Y (expert GEMM 2)
+  int32_t* err;
+};
+struct LayoutIn {
+  const int32_t* board_actual;  // [G][E]
+  const int32_t* quota;         // [G][E][G] or null (static EP)
+  const int32_t* replicas;      // [G][3] or null
+  int bank;                     // replica slot bank = layer parity
+  void* act;                    // [GL*cap, F] bf16
+  void* y_local;                // [GL*cap, H] fp32 (this process's Y region)
+};
+
+__global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o) {
+  __shared__ int32_t reps[kMaxG * kMaxRb];
+  const int G = d.G, E = d.E, EL = d.EL, S = EL + kMaxRb;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < G * kMaxRb; i += blockDim.x) reps[i] = in.replicas ? in.replicas[i] : -1;
+  __syncthreads();
+  // materialize (R23)
+  for (int i = tid; i < G * E; i += blockDim.x) {
+    const int s = i / E, e = i % E;
+    const int n = in.board_actual[s * E + e];
+    int a[kMaxG];
+    int P = 0;
+    for (int t = 0; t < G; ++t) {
+      a[t] = in.quota ? in.quota[(s * E + e) * G + t] : 0;
+      P += a[t];
+    }
+    if (P == 0) {
+      bool hosts = (e / EL == s);
+      for (int q = 0; q < kMaxRb; ++q) hosts |= (reps[s * kMaxRb + q] == e);
+      const int tt = hosts ? s : e / EL;
+      for (int t = 0; t < G; ++t) a[t] = (t == tt) ? n : 0;
+    } else {
+      int tstar = 0, sum = 0;
+      for (int t = 1; t < G; ++t)
+        if (a[t] > a[tstar]) tstar = t;             // largest Q_t, lowest t on ties
+      for (int t = 0; t < G; ++t) {
+        a[t] = static_cast<int>((static_cast<int64_t>(n) * a[t]) / P);
+        sum += a[t];
+      }
+      a[tstar] += n - sum;
+    }
+    int run = 0;
+    for (int t = 0; t < G; ++t) {
+      run += a[t];
+      o.split_cum[(s * E + e) * G + t] = run;
+    }
+  }
+  // slot_of
+  for (int i = tid; i < G * E; i += blockDim.x) {
+    const int r = i / E, e = i % E;
+    int sl = -1;
+    if (e / EL == r) sl = e - r * EL;
+    for (int q = 0; q < kMaxRb; ++q)
+      if (reps[r * kMaxRb + q] == e) sl = EL + q;
+    o.slot_of[i] = sl;
+  }
+  for (int i = tid; i < G * kMaxRb; i += blockDim.x) o.replicas_used[i] = reps[i];
+  __syncthreads();
+  // per destination: rows per (slot, src) in slot order then source order (R24)
+  for (int r = tid; r < G; r += blockDim.x) {
+    int run = 0;
+    for (int j = 0; j < S; ++j) {
+      const int e = (j < EL) ? r * EL + j : reps[r * kMaxRb + (j - EL)];
+      const int before = run;
+      for (int s = 0; s < G; ++s) {
+        o.src_off[(r * S + j) * G + s] = run;
+        if (e >= 0) {
+          const int* c = &o.split_cum[(s * E + e) * G];
+          run += c[r] - (r > 0 ? c[r - 1] : 0);
+        }
+      }
+      o.group_rows[r * S + j] = run - before;
+    }
+  }
+  __syncthreads();
+  // GEMM schedules for the local destinations
+  if (tid == 0) {
+    o.s1->num_groups = d.GL * S;
+    o.s2->num_groups = d.GL * S;
+  }
+  for (int i = tid; i < d.GL * S; i += blockDim.x) {
+    const int gl = i / S, j = i % S, r = d.R0 + gl;
+    const int off = o.src_off[(r * S + j) * G + 0];
+    int m = o.group_rows[r * S + j];
+    if (off + m > d.cap) {
+      atomicOr(o.err, ERR_RECV_OVERFLOW);
+      m = d.cap - off;
+      if (m < 0) m = 0;
+    }
+    const bool is_rep = j >= EL;
+    const int wslot = is_rep ? (gl * 2 * kMaxRb + in.bank * kMaxRb + (j - EL)) : (gl * EL + j);
+    const int arow = gl * d.cap + (off < d.cap ? off : d.cap);
+    GemmGroup g1;
+    g1.a_row = arow; g1.m = m; g1.b_row = wslot * 2 * d.F; g1.b_sel = is_rep; g1.mode = EPI_SWIGLU;
+    g1.n = d.F; g1.ldc = d.F; g1.tile_start = 0;
+    g1.out = reinterpret_cast<__nv_bfloat16*>(in.act) + static_cast<size_t>(arow) * d.F;
+    GemmGroup g2;
+    g2.a_row = arow; g2.m = m; g2.b_row = wslot * d.H; g2.b_sel = is_rep; g2.mode = EPI_F32;
+    g2.n = d.H; g2.ldc = d.H; g2.tile_start = 0;
+    g2.out = reinterpret_cast<float*>(in.y_local) + static_cast<size_t>(arow) * d.H;
+    o.s1->g[i] = g1;
+    o.s2->g[i] = g2;
+  }
+  __syncthreads();
+  if (tid == 0) gemm_finalize_sched(o.s1, 256);
+  if (tid == 32) gemm_finalize_sched(o.s2, 256);
+}
+
+// =============================================================================
+// a6 dispatch: every (token, slot) row of x to its destination's receive buffer
+// (peer store over NVLink for remote ranks).  Warp per token; the x row is read
+// once and written to its k destinations with 16-byte vector stores.
+// =============================================================================
+__global__ void __launch_bounds__(256) k_dispatch(Dims d, int T, const __nv_bfloat16* __restrict__ x,
+                                                  const int32_t* __restrict__ ids,
+                                                  const int32_t* __restrict__ pos,
+                                                  const int32_t* __restrict__ cbase,
+                                                  const int32_t* __restrict__ split_cum,
+                                                  const int32_t* __restrict__ slot_of,
+                                                  const int32_t* __restrict__ src_off, int32_t* __restrict__ route,
+                                                  Sym sym, int buf_recv, int32_t* err) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= d.GL * T) return;
+  const int gl = warp / T, t = warp % T;
+  const int s = d.R0 + gl;
+  const int nchunks = (T + kChunk - 1) / kChunk;
+  const int S = d.EL + kMaxRb;
+  const size_t pr = static_cast<size_t>(gl) * T + t;
+  uint4* dst[kMaxK];
+  int k = d.k;
+  for (int j = 0; j < k; ++j) {
+    int dd = 0, row = -1;
+    if (lane == 0) {
+      const int e = ids[pr * k + j];
+      const int p = cbase[(static_cast<size_t>(gl) * nchunks + t / kChunk) * d.E + e] + pos[pr * k + j];
+      const int* c = &split_cum[(s * d.E + e) * d.G];
+      while (dd < d.G - 1 && c[dd] <= p) ++dd;
+      const int excl = dd > 0 ? c[dd - 1] : 0;
+      const int sl = slot_of[dd * d.E + e];
+      row = src_off[(dd * S + sl) * d.G + s] + (p - excl);
+      if (sl < 0 || row >= d.cap || c[dd] <= p) {
+        atomicOr(err, ERR_RECV_OVERFLOW);
+        row = -1;
+      }
+      route[(pr * k + j) * 2] = dd;
+      route[(pr * k + j) * 2 + 1] = row;
+    }
+    dd = __shfl_sync(0xffffffffu, dd, 0);
+    row = __shfl_sync(0xffffffffu, row, 0);
+    dst[j] = row < 0 ? nullptr
+                     : reinterpret_cast<uint4*>(sym.at(buf_recv, d.G, dd) + static_cast<size_t>(row) * d.H * 2);
+  }
+  const uint4* src = reinterpret_cast<const uint4*>(x + pr * d.H);
+  const int nv = d.H / 8;
+  for (int c = lane; c < nv; c += 32) {
+    const uint4 v = __ldg(src + c);
+    for (int j = 0; j < k; ++j)
+      if (dst[j]) dst[j][c] = v;
+  }
+}
+
+// =============================================================================
+// a8 combine: out[t] = Σ_j g_{t,j} · Y_{dest}[row] in slot order, fp32 (R25),
+// pulled from the expert ranks' Y buffers (peer loads over NVLink).
+// The first CTA raises the prefetch suspend flag (split-phase, R27).
+// block per token, 128 threads.
+// =============================================================================
+template <bool OUT_F32>
+__global__ void __launch_bounds__(128) k_combine(Dims d, int T, const float* __restrict__ gw,
+                                                 const int32_t* __restrict__ route, Sym sym, int buf_y, void* out,
+                                                 volatile int32_t* suspend_flag, int layer) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && suspend_flag) *suspend_flag = layer + 1;
+  __shared__ const float4* srcs[kMaxK];
+  __shared__ float gws[kMaxK];
+  const int tok = blockIdx.x;           // gl * T + t
+  const int k = d.k;
+  if (threadIdx.x < k) {
+    const int j = threadIdx.x;
+    const int dd = route[(static_cast<size_t>(tok) * k + j) * 2];
+    const int row = route[(static_cast<size_t>(tok) * k + j) * 2 + 1];
+    srcs[j] = row < 0 ? nullptr
+                      : reinterpret_cast<const float4*>(sym.at(buf_y, d.G, dd) + static_cast<size_t>(row) * d.H * 4);
+    gws[j] = gw[static_cast<size_t>(tok) * k + j];
+  }
+  __syncthreads();
+  const int nv = d.H / 4;
+  for (int c = threadIdx.x; c < nv; c += blockDim.x) {
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < k; ++j) {
+      if (!srcs[j]) continue;
+      const float4 y = srcs[j][c];
+      const float g = gws[j];
+      a.x = fmaf(g, y.x, a.x);
+      a.y = fmaf(g, y.y, a.y);
+      a.z = fmaf(g, y.z, a.z);
+      a.w = fmaf(g, y.w, a.w);
+    }
+    if (OUT_F32) {
+      reinterpret_cast<float4*>(out)[static_cast<size_t>(tok) * nv + c] = a;
+    } else {
+      uint2 p;
+      p.x = pack_bf16(a.x, a.y);
+      p.y = pack_bf16(a.z, a.w);
+      reinterpret_cast<uint2*>(out)[static_cast<size_t>(tok) * nv + c] = p;
+    }
+  }
+}
+
+// =============================================================================
+// a9 split-phase prefetch (R27): push replica weights (sender = home
+// rank) into the receiver's slot bank.  Chunks are claimed from a counter so
+// part 2 resumes where part 1 stopped; part 1 exits once the combine of the
+// current layer has raised the suspend flag.
+// =============================================================================
+constexpr int kPrefetchChunk = 64 * 1024;  // bytes
+
+__global__ void __launch_bounds__(512) k_prefetch(Dims d, const int32_t* __restrict__ replicas, int bank,
+                                                  const uint8_t* __restrict__ w13, const uint8_t* __restrict__ w2,
+                                                  Sym sym, int buf_rw13, int buf_rw2, int32_t* ctr,
+                                                  const volatile int32_t* suspend_flag, int suspend_at,
+                                                  int32_t* done_bytes_lo) {
+  __shared__ int s_chunk;
+  const size_t w13_bytes = static_cast<size_t>(2) * d.F * d.H * 2;
+  const size_t w2_bytes = static_cast<size_t>(d.H) * d.F * 2;
+  const size_t per = w13_bytes + w2_bytes;
+  const int cper = static_cast<int>((per + kPrefetchChunk - 1) / kPrefetchChunk);
+  // transfers whose sender (home of the expert) is a local rank, in (dst, slot) order
+  __shared__ int tr_dst[kMaxG * kMaxRb], tr_slot[kMaxG * kMaxRb], tr_e[kMaxG * kMaxRb];
+  __shared__ int s_ntr;
+  if (threadIdx.x == 0) {
+    int ntr = 0;
+    for (int r = 0; r < d.G; ++r)
+      for (int q = 0; q < kMaxRb; ++q) {
+        const int e = replicas[r * kMaxRb + q];
+        if (e < 0) continue;
+        const int home = e / d.EL;
+        if (home < d.R0 || home >= d.R0 + d.GL) continue;
+        tr_dst[ntr] = r; tr_slot[ntr] = q; tr_e[ntr] = e; ++ntr;
+      }
+    s_ntr = ntr;
+  }
+  __syncthreads();
+  const int ntr = s_ntr;
+  const int total = ntr * cper;
+  while (true) {
+    if (threadIdx.x == 0) {
+      int c = -1;
+      if (!(suspend_at >= 0 && *suspend_flag >= suspend_at)) c = atomicAdd(ctr, 1);
+      s_chunk = c;
+    }
+    __syncthreads();
+    const int c = s_chunk;
+    __syncthreads();
+    if (c < 0 || c >= total) break;
+    const int ti = c / cper, ci = c % cper;
+    const int e = tr_e[ti];
+    const int le = e - d.R0 * d.EL;      // local expert index within the base weights
+    const size_t off = static_cast<size_t>(ci) * kPrefetchChunk;
+    const size_t len = (off + kPrefetchChunk <= per) ? kPrefetchChunk : per - off;
+    const int slot = bank * kMaxRb + tr_slot[ti];
+    for (size_t b = threadIdx.x * 16; b < len; b += blockDim.x * 16) {
+      const size_t p = off + b;
+      uint4 v;
+      uint8_t* dstp;
+      if (p < w13_bytes) {
+        v = *reinterpret_cast<const uint4*>(w13 + static_cast<size_t>(le) * w13_bytes + p);
+        dstp = sym.at(buf_rw13, d.G, tr_dst[ti]) + static_cast<size_t>(slot) * w13_bytes + p;
+      } else {
+        v = *reinterpret_cast<const uint4*>(w2 + static_cast<size_t>(le) * w2_bytes + (p - w13_bytes));
+        dstp = sym.at(buf_rw2, d.G, tr_dst[ti]) + static_cast<size_t>(slot) * w2_bytes + (p - w13_bytes);
+      }
+      *reinterpret_cast<uint4*>(dstp) = v;
+    }
+    if (threadIdx.x == 0 && done_bytes_lo) atomicAdd(done_bytes_lo, static_cast<int32_t>(len >> 10));
+  }
+}
+
+// small helper: write a host-described group list into a device schedule
+struct SmallGroups {
+  int n;
+  int BN;
+  GemmGroup g[4];
+};
+__global__ void k_write_sched(GemmSched* s, SmallGroups sg) {
+  if (threadIdx.x == 0) {
+    s->num_groups = sg.n;
+    for (int i = 0; i < sg.n; ++i) s->g[i] = sg.g[i];
+    gemm_finalize_sched(s, sg.BN);
+  }
+}
+
+}  // namespace probe

@@ -1,0 +1,649 @@
+// probe.cu — C-ABI of the B200-native PROBE MoE hot path (see include/probe.h).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/probe.h"
+#include "kernels.cuh"
+
+using namespace probe;
+
+namespace {
+
+// ----------------------------------------------------------------------------- errors
+std::mutex g_err_mu;
+std::string g_last_error;
+
+probe_status fail(probe_ctx ctx, probe_status st, const char* fmt, ...);
+
+// ----------------------------------------------------------------------------- TMA encode
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+PFN_encodeTiled g_encode = nullptr;
+
+bool load_encode() {
+  if (g_encode) return true;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !fn)
+    return false;
+  g_encode = reinterpret_cast<PFN_encodeTiled>(fn);
+  return true;
+}
+
+// 2-D bf16 K-major operand map: dims {cols (K), rows}, box {64, box_rows}, SWIZZLE_128B, OOB → 0.
+bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  if (!load_encode()) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+struct MapCache {
+  struct Ent {
+    const void* p;
+    uint64_t rows, cols;
+    uint32_t box;
+    CUtensorMap map;
+  };
+  std::vector<Ent> ents;
+  const CUtensorMap* get(const void* p, uint64_t rows, uint64_t cols, uint32_t box) {
+    for (auto& e : ents)
+      if (e.p == p && e.rows == rows && e.cols == cols && e.box == box) return &e.map;
+    Ent e{p, rows, cols, box, {}};
+    if (!make_map(&e.map, p, rows, cols, box)) return nullptr;
+    if (ents.size() >= 256) ents.erase(ents.begin());
+    ents.push_back(e);
+    return &ents.back().map;
+  }
+};
+
+size_t al(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+struct Scratch {
+  size_t sym, logits, pprior, pres, pact, ids, gw, pos, hist, cbase, route, pred_local;
+  size_t quota[2], reps[2], stats[2], pfctr[2];
+  size_t split_cum, slot_of, src_off, group_rows, reps_used;
+  size_t s_g1, s_g2, s_gate, s_p1, s_p2, flags, act, total;
+};
+
+Scratch scratch_layout(const probe_config& c) {
+  Scratch s{};
+  const size_t G = c.ep_size, GL = c.local_ranks, E = c.num_experts, k = c.top_k, T = c.max_tokens;
+  const size_t h = c.res_hidden > 0 ? c.res_hidden : 8, F = c.ffn, cap = c.recv_capacity;
+  const size_t NC = (T + kChunk - 1) / kChunk, EL = E / G, S = EL + kMaxRb;
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o += al(bytes); return r; };
+  s.sym = take(PROBE_NSYM * G * 8);
+  s.logits = take(GL * T * E * 4);
+  s.pprior = take(GL * T * E * 4);
+  s.pres = take(GL * T * E * 4);
+  s.pact = take(GL * T * h * 2);
+  s.ids = take(GL * T * k * 4);
+  s.gw = take(GL * T * k * 4);
+  s.pos = take(GL * T * k * 4);
+  s.hist = take(GL * NC * E * 4);
+  s.cbase = take(GL * NC * E * 4);
+  s.route = take(GL * T * k * 8);
+  s.pred_local = take(GL * E * 4);
+  for (int p = 0; p < 2; ++p) {
+    s.quota[p] = take(G * E * G * 4);
+    s.reps[p] = take(G * kMaxRb * 4);
+    s.stats[p] = take(8 * 8);
+    s.pfctr[p] = take(16);
+  }
+  s.split_cum = take(G * E * G * 4);
+  s.slot_of = take(G * E * 4);
+  s.src_off = take(G * S * G * 4);
+  s.group_rows = take(G * S * 4);
+  s.reps_used = take(G * kMaxRb * 4);
+  s.s_g1 = take(sizeof(GemmSched));
+  s.s_g2 = take(sizeof(GemmSched));
+  s.s_gate = take(sizeof(GemmSched));
+  s.s_p1 = take(sizeof(GemmSched));
+  s.s_p2 = take(sizeof(GemmSched));
+  s.flags = take(256);
+  s.act = take(GL * cap * F * 2);
+  s.total = al(o, 1024);
+  return s;
+}
+
+void sym_sizes(const probe_config& c, uint64_t b[PROBE_NBUF]) {
+  const uint64_t cap = c.recv_capacity, H = c.hidden, F = c.ffn, G = c.ep_size, E = c.num_experts;
+  b[PROBE_BUF_RECV] = al(cap * H * 2, 1024);
+  b[PROBE_BUF_Y] = al(cap * H * 4, 1024);
+  b[PROBE_BUF_REP_W13] = al(2 * kMaxRb * 2 * F * H * 2, 1024);
+  b[PROBE_BUF_REP_W2] = al(2 * kMaxRb * H * F * 2, 1024);
+  b[PROBE_BUF_BOARD] = al(4 * G * E * 4 + 1024, 1024);
+  b[PROBE_BUF_SIGNAL] = 4096;
+  b[PROBE_BUF_SCRATCH] = scratch_layout(c).total;
+}
+
+}  // namespace
+
+struct probe_ctx_s {
+  probe_config cfg;
+  Dims d;
+  Scratch sl;
+  uint8_t* scratch;
+  std::vector<uint64_t> peer;   // host copy [NSYM][G]
+  uint8_t* local_base[PROBE_NSYM];
+  uint64_t sym_bytes[PROBE_NBUF];
+  cudaStream_t aux = nullptr, pf = nullptr;
+  cudaEvent_t ev_gate[2], ev_gemm[2], ev_comb[2], ev_pred[2], ev_plan[2], ev_slots[2];
+  int fwd_layer = -1000, pred_layer[2] = {-1000, -1000}, plan_layer[2] = {-1000, -1000},
+      pf_layer[2] = {-1000, -1000};
+  int last_fwd_parity = 0;
+  int last_T = 0;
+  int num_sms = 148;
+  MapCache maps;
+  CUtensorMap map_recv, map_act, map_rw13, map_rw2;
+  std::string err;
+  int64_t launches = 0;
+  template <class T>
+  T* at(size_t off) const {
+    return reinterpret_cast<T*>(scratch + off);
+  }
+};
+
+namespace {
+
+probe_status fail(probe_ctx ctx, probe_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  std::lock_guard<std::mutex> lk(g_err_mu);
+  g_last_error = buf;
+  if (ctx) ctx->err = buf;
+  return st;
+}
+
+#define CK(call)                                                                                 \
+  do {                                                                                           \
+    cudaError_t e_ = (call);                                                                     \
+    if (e_ != cudaSuccess) return fail(ctx, PROBE_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define CKL()                                                                                         \
+  do {                                                                                                \
+    ++ctx->launches;                                                                                  \
+    cudaError_t e_ = cudaGetLastError();                                                              \
+    if (e_ != cudaSuccess) return fail(ctx, PROBE_ECUDA, "launch @%d: %s", __LINE__, cudaGetErrorString(e_)); \
+  } while (0)
+
+template <int BN>
+constexpr int stages_for() { return BN == 256 ? 4 : 6; }
+
+template <int BN>
+cudaError_t launch_gemm(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, const GemmSched* s, int K,
+                        int grid, cudaStream_t st) {
+  constexpr int ST = stages_for<BN>();
+  using L = GemmSmem<BN, ST>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(grouped_gemm_kernel<BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         L::BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  grouped_gemm_kernel<BN, ST><<<grid, 256, L::BYTES, st>>>(a, b0, b1, s, K);
+  return cudaGetLastError();
+}
+
+template <bool PRED>
+void launch_topk(const Dims& d, int T, int nchunks, cudaStream_t st, const float* lg, const float* lg2, const float* b,
+                 int32_t* ids, float* gw, int32_t* pos, int32_t* hist, int32_t* pc, float* lo) {
+  dim3 grid(nchunks, d.GL);
+  if (d.E <= 32) k_topk<1, PRED><<<grid, 128, 0, st>>>(d, T, lg, lg2, b, ids, gw, pos, hist, pc, lo);
+  else if (d.E <= 64) k_topk<2, PRED><<<grid, 128, 0, st>>>(d, T, lg, lg2, b, ids, gw, pos, hist, pc, lo);
+  else if (d.E <= 128) k_topk<4, PRED><<<grid, 128, 0, st>>>(d, T, lg, lg2, b, ids, gw, pos, hist, pc, lo);
+  else k_topk<8, PRED><<<grid, 128, 0, st>>>(d, T, lg, lg2, b, ids, gw, pos, hist, pc, lo);
+}
+
+GemmGroup mk_group(int a_row, int m, int b_row, int b_sel, int mode, int n, int ldc, void* out) {
+  GemmGroup g;
+  g.a_row = a_row; g.m = m; g.b_row = b_row; g.b_sel = b_sel; g.mode = mode; g.n = n; g.ldc = ldc;
+  g.tile_start = 0; g.out = out;
+  return g;
+}
+
+Sym sym_of(probe_ctx ctx) { return Sym{ctx->at<const uint64_t>(ctx->sl.sym)}; }
+
+}  // namespace
+
+extern "C" {
+
+probe_status probe_workspace(const probe_config* cfg, uint64_t bytes[PROBE_NBUF]) {
+  if (!cfg || !bytes) return fail(nullptr, PROBE_EINVAL, "probe_workspace: null argument");
+  sym_sizes(*cfg, bytes);
+  return PROBE_OK;
+}
+
+static probe_status validate(const probe_config& c) {
+  if (c.ep_size < 1 || c.ep_size > kMaxG) return fail(nullptr, PROBE_EINVAL, "ep_size %d out of [1,%d]", c.ep_size, kMaxG);
+  if (c.local_ranks < 1 || c.rank_begin < 0 || c.rank_begin + c.local_ranks > c.ep_size)
+    return fail(nullptr, PROBE_EINVAL, "local rank range [%d,%d) outside [0,%d)", c.rank_begin,
+                c.rank_begin + c.local_ranks, c.ep_size);
+  if (c.num_experts < 1 || c.num_experts > kMaxE || c.num_experts % c.ep_size)
+    return fail(nullptr, PROBE_ESHAPE, "num_experts %d must be in [1,%d] and divisible by ep_size %d", c.num_experts,
+                kMaxE, c.ep_size);
+  if (c.top_k < 1 || c.top_k > c.num_experts || c.top_k > kMaxK)
+    return fail(nullptr, PROBE_ESHAPE, "top_k %d out of range", c.top_k);
+  if (c.hidden < 64 || c.hidden % 64 || c.ffn < 64 || c.ffn % 64)
+    return fail(nullptr, PROBE_ESHAPE, "hidden %d and ffn %d must be positive multiples of 64", c.hidden, c.ffn);
+  if (c.res_hidden < 0 || c.res_hidden % 8) return fail(nullptr, PROBE_ESHAPE, "res_hidden %d must be a multiple of 8", c.res_hidden);
+  if (c.num_experts % 8) return fail(nullptr, PROBE_ESHAPE, "num_experts %d must be a multiple of 8", c.num_experts);
+  if (c.max_tokens < 1 || c.recv_capacity < 1) return fail(nullptr, PROBE_EINVAL, "max_tokens/recv_capacity must be >= 1");
+  if (static_cast<int64_t>(c.local_ranks) * c.recv_capacity > (1ll << 30) ||
+      static_cast<int64_t>(c.local_ranks) * c.max_tokens > (1ll << 28))
+    return fail(nullptr, PROBE_ECAPACITY, "capacity too large");
+  if (c.replica_budget < 0 || c.replica_budget > kMaxRb)
+    return fail(nullptr, PROBE_EBUDGET, "replica_budget %d out of [0,3] (P:476)", c.replica_budget);
+  if (c.kmax < 0) return fail(nullptr, PROBE_EINVAL, "kmax < 0");
+  if (c.n_sat < 0 || c.alpha_ps < 0 || c.beta_ps < 0 || c.bw_bytes_per_us < 0)
+    return fail(nullptr, PROBE_EINVAL, "negative cost constant");
+  if (c.expert_bytes != 6ll * c.hidden * c.ffn)
+    return fail(nullptr, PROBE_EINVAL, "expert_bytes %lld != 6*H*F = %lld", (long long)c.expert_bytes,
+                6ll * c.hidden * c.ffn);
+  if (c.reserved != 0) return fail(nullptr, PROBE_EINVAL, "reserved must be 0");
+  return PROBE_OK;
+}
+
+probe_status probe_init(const probe_config* cfg, const uint64_t* peer_ptrs, void* scratch, probe_ctx* out) {
+  probe_ctx ctx = nullptr;
+  if (!cfg || !peer_ptrs || !scratch || !out) return fail(nullptr, PROBE_EINVAL, "probe_init: null argument");
+  probe_status st = validate(*cfg);
+  if (st != PROBE_OK) return st;
+  ctx = new probe_ctx_s();
+  ctx->cfg = *cfg;
+  const probe_config& c = *cfg;
+  ctx->d = Dims{c.ep_size, c.rank_begin, c.local_ranks, c.num_experts, c.num_experts / c.ep_size, c.top_k,
+                c.hidden, c.ffn, c.res_hidden, c.max_tokens, c.recv_capacity, c.replica_budget};
+  ctx->sl = scratch_layout(c);
+  ctx->scratch = static_cast<uint8_t*>(scratch);
+  sym_sizes(c, ctx->sym_bytes);
+  const int G = c.ep_size;
+  ctx->peer.assign(peer_ptrs, peer_ptrs + PROBE_NSYM * G);
+  for (int b = 0; b < PROBE_NSYM; ++b) {
+    ctx->local_base[b] = reinterpret_cast<uint8_t*>(ctx->peer[b * G + c.rank_begin]);
+    for (int l = 0; l < c.local_ranks; ++l) {
+      const uint64_t want = ctx->peer[b * G + c.rank_begin] + static_cast<uint64_t>(l) * ctx->sym_bytes[b];
+      if (ctx->peer[b * G + c.rank_begin + l] != want) {
+        delete ctx;
+        return fail(nullptr, PROBE_ECOMM, "buffer %d: local ranks must be contiguous with stride %llu", b,
+                    (unsigned long long)ctx->sym_bytes[b]);
+      }
+    }
+    for (int r = 0; r < G; ++r)
+      if (ctx->peer[b * G + r] == 0 || ctx->peer[b * G + r] % 1024) {
+        delete ctx;
+        return fail(nullptr, PROBE_ECOMM, "buffer %d of rank %d null or not 1024-aligned", b, r);
+      }
+  }
+  if (reinterpret_cast<uintptr_t>(scratch) % 1024) {
+    delete ctx;
+    return fail(nullptr, PROBE_EINVAL, "scratch must be 1024-byte aligned");
+  }
+  cudaError_t e = cudaMemcpy(ctx->scratch + ctx->sl.sym, ctx->peer.data(), PROBE_NSYM * G * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(ctx->scratch + ctx->sl.flags, 0, 256);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->pf, cudaStreamNonBlocking);
+  for (int p = 0; p < 2 && e == cudaSuccess; ++p) {
+    cudaEvent_t* evs[6] = {&ctx->ev_gate[p], &ctx->ev_gemm[p], &ctx->ev_comb[p], &ctx->ev_pred[p], &ctx->ev_plan[p],
+                           &ctx->ev_slots[p]};
+    for (auto* ev : evs)
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+  }
+  int dev = 0;
+  if (e == cudaSuccess) e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e == cudaSuccess) {
+    const size_t plan_smem = static_cast<size_t>(G) * c.num_experts * G * 4;
+    e = cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(plan_smem));
+  }
+  if (e != cudaSuccess) {
+    delete ctx;
+    return fail(nullptr, PROBE_ECUDA, "probe_init: %s", cudaGetErrorString(e));
+  }
+  const uint64_t GL = c.local_ranks, cap = c.recv_capacity, H = c.hidden, F = c.ffn;
+  bool ok = make_map(&ctx->map_recv, ctx->local_base[PROBE_BUF_RECV], GL * cap, H, 128) &&
+            make_map(&ctx->map_act, ctx->scratch + ctx->sl.act, GL * cap, F, 128) &&
+            make_map(&ctx->map_rw13, ctx->local_base[PROBE_BUF_REP_W13], GL * 2 * kMaxRb * 2 * F, H, 128) &&
+            make_map(&ctx->map_rw2, ctx->local_base[PROBE_BUF_REP_W2], GL * 2 * kMaxRb * H, F, 128);
+  if (!ok) {
+    delete ctx;
+    return fail(nullptr, PROBE_ECUDA, "probe_init: cuTensorMapEncodeTiled failed");
+  }
+  *out = ctx;
+  return PROBE_OK;
+}
+
+probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int32_t T, const void* w_router,
+                               const float* b_router, const void* w13, const void* w2, int32_t use_plan, void* out,
+                               int32_t out_fp32, int32_t* topk_ids, float* topk_w, void* stream) {
+  if (!ctx) return fail(nullptr, PROBE_EINVAL, "null ctx");
+  if (!x || !w_router || !w13 || !w2 || !out) return fail(ctx, PROBE_EINVAL, "probe_moe_forward: null pointer");
+  if (layer < 0) return fail(ctx, PROBE_EINVAL, "layer %d < 0", layer);
+  if (T < 1 || T > ctx->cfg.max_tokens) return fail(ctx, PROBE_ECAPACITY, "T=%d outside [1, max_tokens=%d]", T, ctx->cfg.max_tokens);
+  const int p = layer & 1;
+  if (use_plan) {
+    if (ctx->plan_layer[p] != layer) return fail(ctx, PROBE_ESTATE, "layer %d: use_plan without probe_plan(%d)", layer, layer);
+    if (ctx->pf_layer[p] != layer)
+      return fail(ctx, PROBE_ESTATE, "layer %d: use_plan without probe_prefetch(%d, START)", layer, layer);
+  }
+  const Dims& d0 = ctx->d;
+  Dims d = d0;
+  d.T = T;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint64_t GL = d.GL, H = d.H, F = d.F, E = d.E;
+  const int nchunks = (T + kChunk - 1) / kChunk;
+  const CUtensorMap* mx = ctx->maps.get(x, GL * T, H, 128);
+  const CUtensorMap* mr = ctx->maps.get(w_router, E, H, 64);
+  const CUtensorMap* m13 = ctx->maps.get(w13, GL * d.EL * 2 * F, H, 128);
+  const CUtensorMap* m2 = ctx->maps.get(w2, GL * d.EL * H, F, 128);
+  if (!mx || !mr || !m13 || !m2) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
+  const Scratch& s = ctx->sl;
+  int32_t* err = ctx->at<int32_t>(s.flags);
+  int32_t* suspend = err + 1;
+  // a1 gate: logits = x W_rᵀ (tcgen05), top-k + softmax + per-chunk ranks
+  SmallGroups sg{};
+  sg.n = 1;
+  sg.BN = 128;
+  sg.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_F32, d.E, d.E, ctx->at<float>(s.logits));
+  k_write_sched<<<1, 32, 0, st>>>(ctx->at<GemmSched>(s.s_gate), sg);
+  CKL();
+  CK(launch_gemm<128>(*mx, *mr, *mr, ctx->at<GemmSched>(s.s_gate), d.H, ctx->num_sms, st));
+  ++ctx->launches;
+  launch_topk<false>(d, T, nchunks, st, ctx->at<float>(s.logits), nullptr, b_router, ctx->at<int32_t>(s.ids),
+                     ctx->at<float>(s.gw), ctx->at<int32_t>(s.pos), ctx->at<int32_t>(s.hist), nullptr, nullptr);
+  CKL();
+  CK(cudaEventRecord(ctx->ev_gate[p], st));
+  // a3 actual-count all-gather (board kind 0, parity p)
+  k_count_scan<<<d.GL, 256, 0, st>>>(d, nchunks, ctx->at<int32_t>(s.hist), ctx->at<int32_t>(s.cbase), sym_of(ctx),
+                                     PROBE_BUF_BOARD, p);
+  CKL();
+  // a5 materialize plan(L) + layout
+  if (use_plan) CK(cudaStreamWaitEvent(st, ctx->ev_plan[p], 0));
+  LayoutIn li;
+  li.board_actual = reinterpret_cast<const int32_t*>(ctx->local_base[PROBE_BUF_BOARD]) + ((p * 2 + 0) * d.G) * d.E;
+  li.quota = use_plan ? ctx->at<int32_t>(s.quota[p]) : nullptr;
+  li.replicas = use_plan ? ctx->at<int32_t>(s.reps[p]) : nullptr;
+  li.bank = p;
+  li.act = ctx->scratch + s.act;
+  li.y_local = ctx->local_base[PROBE_BUF_Y];
+  LayoutOut lo;
+  lo.split_cum = ctx->at<int32_t>(s.split_cum);
+  lo.slot_of = ctx->at<int32_t>(s.slot_of);
+  lo.src_off = ctx->at<int32_t>(s.src_off);
+  lo.group_rows = ctx->at<int32_t>(s.group_rows);
+  lo.replicas_used = ctx->at<int32_t>(s.reps_used);
+  lo.s1 = ctx->at<GemmSched>(s.s_g1);
+  lo.s2 = ctx->at<GemmSched>(s.s_g2);
+  lo.err = err;
+  k_layout<<<1, 512, 0, st>>>(d, li, lo);
+  CKL();
+  // a6 dispatch
+  {
+    const int warps = d.GL * T;
+    k_dispatch<<<(warps + 7) / 8, 256, 0, st>>>(d, T, static_cast<const __nv_bfloat16*>(x), ctx->at<int32_t>(s.ids),
+                                                ctx->at<int32_t>(s.pos), ctx->at<int32_t>(s.cbase),
+                                                lo.split_cum, lo.slot_of, lo.src_off, ctx->at<int32_t>(s.route),
+                                                sym_of(ctx), PROBE_BUF_RECV, err);
+    CKL();
+  }
+  // a9 phase lock: the expert GEMMs need this layer's replica slots
+  if (use_plan) CK(cudaStreamWaitEvent(st, ctx->ev_slots[p], 0));
+  CK(cudaEventRecord(ctx->ev_gemm[p], st));
+  // a7 grouped SwiGLU expert FFN (tcgen05): act = SiLU(X W_gᵀ) ⊙ X W_uᵀ ; Y = act W_dᵀ
+  CK(launch_gemm<256>(ctx->map_recv, *m13, ctx->map_rw13, lo.s1, d.H, ctx->num_sms, st));
+  ++ctx->launches;
+  CK(launch_gemm<256>(ctx->map_act, *m2, ctx->map_rw2, lo.s2, d.F, ctx->num_sms, st));
+  ++ctx->launches;
+  // a8 combine (raises the prefetch suspend flag, R27)
+  if (out_fp32)
+    k_combine<true><<<d.GL * T, 128, 0, st>>>(d, T, ctx->at<float>(s.gw), ctx->at<int32_t>(s.route), sym_of(ctx),
+                                              PROBE_BUF_Y, out, suspend, layer);
+  else
+    k_combine<false><<<d.GL * T, 128, 0, st>>>(d, T, ctx->at<float>(s.gw), ctx->at<int32_t>(s.route), sym_of(ctx),
+                                               PROBE_BUF_Y, out, suspend, layer);
+  CKL();
+  CK(cudaEventRecord(ctx->ev_comb[p], st));
+  if (topk_ids) CK(cudaMemcpyAsync(topk_ids, ctx->at<int32_t>(s.ids), GL * T * d.k * 4, cudaMemcpyDeviceToDevice, st));
+  if (topk_w) CK(cudaMemcpyAsync(topk_w, ctx->at<float>(s.gw), GL * T * d.k * 4, cudaMemcpyDeviceToDevice, st));
+  ctx->fwd_layer = layer;
+  ctx->last_fwd_parity = p;
+  ctx->last_T = T;
+  return PROBE_OK;
+}
+
+probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int32_t T, const void* w_router_next,
+                           const float* b_router_next, const void* w_res1, const void* w_res2, int32_t* pred_counts,
+                           float* pred_logits, void* stream) {
+  if (!ctx) return fail(nullptr, PROBE_EINVAL, "null ctx");
+  if (!x || !w_router_next) return fail(ctx, PROBE_EINVAL, "probe_predict: null pointer");
+  if ((w_res1 == nullptr) != (w_res2 == nullptr)) return fail(ctx, PROBE_EINVAL, "w_res1 and w_res2 must both be given or both NULL");
+  if (w_res1 && ctx->cfg.res_hidden <= 0) return fail(ctx, PROBE_ESHAPE, "residual given but res_hidden == 0");
+  if (T < 1 || T > ctx->cfg.max_tokens) return fail(ctx, PROBE_ECAPACITY, "T=%d outside [1, max_tokens]", T);
+  if (next_layer < 1) return fail(ctx, PROBE_EINVAL, "next_layer %d < 1 (layer 0 is not predicted, R29)", next_layer);
+  Dims d = ctx->d;
+  d.T = T;
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->aux;
+  const int pp = next_layer & 1, prev = (next_layer - 1) & 1;
+  if (ctx->fwd_layer == next_layer - 1) CK(cudaStreamWaitEvent(st, ctx->ev_gate[prev], 0));
+  const uint64_t GL = d.GL, H = d.H, E = d.E, h = d.h;
+  const Scratch& s = ctx->sl;
+  const CUtensorMap* mx = ctx->maps.get(x, GL * T, H, 128);
+  const CUtensorMap* mw = ctx->maps.get(w_router_next, E, H, 64);
+  const CUtensorMap* m1 = w_res1 ? ctx->maps.get(w_res1, h, H, 64) : mw;
+  if (!mx || !mw || !m1) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
+  SmallGroups sg{};
+  sg.BN = 128;
+  sg.n = w_res1 ? 2 : 1;
+  sg.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_F32, d.E, d.E, ctx->at<float>(s.pprior));
+  if (w_res1) sg.g[1] = mk_group(0, static_cast<int>(GL * T), 0, 1, EPI_SILU_BF16, d.h, d.h, ctx->scratch + s.pact);
+  k_write_sched<<<1, 32, 0, st>>>(ctx->at<GemmSched>(s.s_p1), sg);
+  CKL();
+  CK(launch_gemm<128>(*mx, *mw, *m1, ctx->at<GemmSched>(s.s_p1), d.H, ctx->num_sms, st));
+  ++ctx->launches;
+  if (w_res1) {
+    const CUtensorMap* ma = ctx->maps.get(ctx->scratch + s.pact, GL * T, h, 128);
+    const CUtensorMap* m2 = ctx->maps.get(w_res2, E, h, 64);
+    if (!ma || !m2) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
+    SmallGroups s2{};
+    s2.BN = 128;
+    s2.n = 1;
+    s2.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_F32, d.E, d.E, ctx->at<float>(s.pres));
+    k_write_sched<<<1, 32, 0, st>>>(ctx->at<GemmSched>(s.s_p2), s2);
+    CKL();
+    CK(launch_gemm<128>(*ma, *m2, *m2, ctx->at<GemmSched>(s.s_p2), d.h, ctx->num_sms, st));
+    ++ctx->launches;
+  }
+  CK(cudaMemsetAsync(ctx->at<int32_t>(s.pred_local), 0, GL * E * 4, st));
+  const int nchunks = (T + kChunk - 1) / kChunk;
+  launch_topk<true>(d, T, nchunks, st, ctx->at<float>(s.pprior), w_res1 ? ctx->at<float>(s.pres) : nullptr,
+                    b_router_next, nullptr, nullptr, nullptr, nullptr, ctx->at<int32_t>(s.pred_local), pred_logits);
+  CKL();
+  k_pred_publish<<<d.GL, 256, 0, st>>>(d, ctx->at<int32_t>(s.pred_local), sym_of(ctx), PROBE_BUF_BOARD, pp);
+  CKL();
+  if (pred_counts) {
+    const int32_t* board = reinterpret_cast<const int32_t*>(ctx->local_base[PROBE_BUF_BOARD]) + ((pp * 2 + 1) * d.G) * d.E;
+    CK(cudaMemcpyAsync(pred_counts, board, static_cast<size_t>(d.G) * d.E * 4, cudaMemcpyDeviceToDevice, st));
+  }
+  CK(cudaEventRecord(ctx->ev_pred[pp], st));
+  ctx->pred_layer[pp] = next_layer;
+  return PROBE_OK;
+}
+
+probe_status probe_plan(probe_ctx ctx, int32_t next_layer, const int32_t* pred_counts, const int64_t* window_ns,
+                        int32_t* replicas, int32_t* quota, int64_t* plan_stats, void* stream) {
+  if (!ctx) return fail(nullptr, PROBE_EINVAL, "null ctx");
+  if (!window_ns) return fail(ctx, PROBE_EINVAL, "probe_plan: window_ns is required");
+  if (next_layer < 0) return fail(ctx, PROBE_EINVAL, "next_layer < 0");
+  const int pp = next_layer & 1;
+  if (!pred_counts && ctx->pred_layer[pp] != next_layer)
+    return fail(ctx, PROBE_ESTATE, "probe_plan(%d): no probe_predict(%d) and no explicit pred_counts", next_layer, next_layer);
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->aux;
+  const Dims& d = ctx->d;
+  const Scratch& s = ctx->sl;
+  if (!pred_counts) CK(cudaStreamWaitEvent(st, ctx->ev_pred[pp], 0));
+  const int32_t* nh = pred_counts ? pred_counts
+                                  : reinterpret_cast<const int32_t*>(ctx->local_base[PROBE_BUF_BOARD]) + ((pp * 2 + 1) * d.G) * d.E;
+  PlanParams pr{ctx->cfg.alpha_ps, ctx->cfg.beta_ps, ctx->cfg.bw_bytes_per_us, ctx->cfg.expert_bytes,
+                ctx->cfg.n_sat, ctx->cfg.kmax, ctx->cfg.replica_budget};
+  const size_t smem = static_cast<size_t>(d.G) * d.E * d.G * 4;
+  k_plan<<<1, 256, smem, st>>>(d, pr, nh, window_ns, ctx->at<int32_t>(s.quota[pp]), ctx->at<int32_t>(s.reps[pp]),
+                                ctx->at<int64_t>(s.stats[pp]), ctx->at<int32_t>(s.pfctr[pp]));
+  CKL();
+  if (replicas) CK(cudaMemcpyAsync(replicas, ctx->at<int32_t>(s.reps[pp]), d.G * kMaxRb * 4, cudaMemcpyDeviceToDevice, st));
+  if (quota) CK(cudaMemcpyAsync(quota, ctx->at<int32_t>(s.quota[pp]), smem, cudaMemcpyDeviceToDevice, st));
+  if (plan_stats) CK(cudaMemcpyAsync(plan_stats, ctx->at<int64_t>(s.stats[pp]), 64, cudaMemcpyDeviceToDevice, st));
+  CK(cudaEventRecord(ctx->ev_plan[pp], st));
+  ctx->plan_layer[pp] = next_layer;
+  return PROBE_OK;
+}
+
+probe_status probe_prefetch(probe_ctx ctx, int32_t next_layer, const void* w13_next, const void* w2_next, int32_t phase,
+                            void* stream) {
+  if (!ctx) return fail(nullptr, PROBE_EINVAL, "null ctx");
+  const int pp = next_layer & 1, prev = (next_layer - 1) & 1;
+  if (phase == 1) {
+    if (ctx->pf_layer[pp] != next_layer) return fail(ctx, PROBE_ESTATE, "prefetch WAIT(%d) before START", next_layer);
+    CK(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), ctx->ev_slots[pp], 0));
+    return PROBE_OK;
+  }
+  if (phase != 0) return fail(ctx, PROBE_EINVAL, "phase must be 0 (START) or 1 (WAIT)");
+  if (!w13_next || !w2_next) return fail(ctx, PROBE_EINVAL, "probe_prefetch: null weights");
+  if (ctx->plan_layer[pp] != next_layer) return fail(ctx, PROBE_ESTATE, "prefetch START(%d) before probe_plan(%d)", next_layer, next_layer);
+  const Dims& d = ctx->d;
+  const Scratch& s = ctx->sl;
+  cudaStream_t st = ctx->pf;
+  CK(cudaStreamWaitEvent(st, ctx->ev_plan[pp], 0));
+  int32_t* flags = ctx->at<int32_t>(s.flags);
+  const bool inflight = ctx->fwd_layer == next_layer - 1;
+  const int grid = 8;   // "controlled SM occupancy"
+  if (inflight) {
+    CK(cudaStreamWaitEvent(st, ctx->ev_gemm[prev], 0));
+    k_prefetch<<<grid, 512, 0, st>>>(d, ctx->at<int32_t>(s.reps[pp]), pp, static_cast<const uint8_t*>(w13_next),
+                                     static_cast<const uint8_t*>(w2_next), sym_of(ctx), PROBE_BUF_REP_W13,
+                                     PROBE_BUF_REP_W2, ctx->at<int32_t>(s.pfctr[pp]), flags + 1, next_layer,
+                                     flags + 2);
+    CKL();
+    CK(cudaStreamWaitEvent(st, ctx->ev_comb[prev], 0));
+  }
+  k_prefetch<<<grid, 512, 0, st>>>(d, ctx->at<int32_t>(s.reps[pp]), pp, static_cast<const uint8_t*>(w13_next),
+                                   static_cast<const uint8_t*>(w2_next), sym_of(ctx), PROBE_BUF_REP_W13,
+                                   PROBE_BUF_REP_W2, ctx->at<int32_t>(s.pfctr[pp]), flags + 1, -1, flags + 3);
+  CKL();
+  CK(cudaEventRecord(ctx->ev_slots[pp], st));
+  ctx->pf_layer[pp] = next_layer;
+  return PROBE_OK;
+}
+
+probe_status probe_debug_layout(probe_ctx ctx, int32_t* counts, int32_t* split, int32_t* route, int32_t* group_rows,
+                                int32_t* replicas_used, void* stream) {
+  if (!ctx) return fail(nullptr, PROBE_EINVAL, "null ctx");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const Dims& d = ctx->d;
+  const Scratch& s = ctx->sl;
+  const int p = ctx->last_fwd_parity;
+  if (counts) {
+    const int32_t* b = reinterpret_cast<const int32_t*>(ctx->local_base[PROBE_BUF_BOARD]) + ((p * 2 + 0) * d.G) * d.E;
+    CK(cudaMemcpyAsync(counts, b, static_cast<size_t>(d.G) * d.E * 4, cudaMemcpyDeviceToDevice, st));
+  }
+  if (split) CK(cudaMemcpyAsync(split, ctx->at<int32_t>(s.split_cum), static_cast<size_t>(d.G) * d.E * d.G * 4, cudaMemcpyDeviceToDevice, st));
+  if (route) CK(cudaMemcpyAsync(route, ctx->at<int32_t>(s.route), static_cast<size_t>(d.GL) * ctx->last_T * d.k * 8, cudaMemcpyDeviceToDevice, st));
+  if (group_rows)
+    CK(cudaMemcpyAsync(group_rows, ctx->at<int32_t>(s.group_rows) + d.R0 * (d.EL + kMaxRb),
+                       static_cast<size_t>(d.GL) * (d.EL + kMaxRb) * 4, cudaMemcpyDeviceToDevice, st));
+  if (replicas_used) CK(cudaMemcpyAsync(replicas_used, ctx->at<int32_t>(s.reps_used), d.G * kMaxRb * 4, cudaMemcpyDeviceToDevice, st));
+  return PROBE_OK;
+}
+
+probe_status probe_test_gemm(const void* A, int64_t a_rows, const void* B, int64_t b_rows, int32_t K, int32_t N,
+                             const int32_t* groups, int32_t num_groups, int32_t mode, void* C, void* stream) {
+  probe_ctx ctx = nullptr;
+  if (!A || !B || !groups || !C || num_groups < 1 || num_groups > kMaxGroups || K < 1 || N < 8 || N % 8)
+    return fail(nullptr, PROBE_EINVAL, "probe_test_gemm: bad arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int BN = (mode == 1 || mode == 2) ? 256 : 128;
+  const int emode = mode == 1 ? EPI_SWIGLU : (mode == 3 ? EPI_SILU_BF16 : EPI_F32);
+  const int n_out = mode == 1 ? N / 2 : N;
+  std::vector<uint8_t> host(sizeof(GemmSched), 0);
+  GemmSched* hs = reinterpret_cast<GemmSched*>(host.data());
+  hs->num_groups = num_groups;
+  const size_t esz = emode == EPI_F32 ? 4 : 2;
+  int acc = 0;
+  for (int i = 0; i < num_groups; ++i) {
+    const int* g = groups + 4 * i;
+    hs->g[i] = mk_group(g[0], g[1], g[2], 0, emode, n_out, n_out, static_cast<uint8_t*>(C) + static_cast<size_t>(g[3]) * n_out * esz);
+    hs->g[i].tile_start = acc;
+    acc += gemm_ntiles(hs->g[i], BN);
+  }
+  hs->total_tiles = acc;
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, A, a_rows, K, 128) || !make_map(&mb, B, b_rows, K, BN / 2))
+    return fail(nullptr, PROBE_ECUDA, "tensor map encode failed");
+  GemmSched* ds = nullptr;
+  CK(cudaMalloc(&ds, sizeof(GemmSched)));
+  CK(cudaMemcpy(ds, hs, sizeof(GemmSched), cudaMemcpyHostToDevice));
+  int dev = 0, sms = 148;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  cudaError_t e = BN == 256 ? launch_gemm<256>(ma, mb, mb, ds, K, sms, st) : launch_gemm<128>(ma, mb, mb, ds, K, sms, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(ds);
+  if (e != cudaSuccess) return fail(nullptr, PROBE_ECUDA, "probe_test_gemm: %s", cudaGetErrorString(e));
+  return PROBE_OK;
+}
+
+probe_status probe_check(probe_ctx ctx) {
+  if (!ctx) return fail(nullptr, PROBE_EINVAL, "null ctx");
+  CK(cudaStreamSynchronize(ctx->aux));
+  CK(cudaStreamSynchronize(ctx->pf));
+  CK(cudaDeviceSynchronize());
+  int32_t flags[4];
+  CK(cudaMemcpy(flags, ctx->scratch + ctx->sl.flags, sizeof(flags), cudaMemcpyDeviceToHost));
+  if (flags[0] & ERR_RECV_OVERFLOW)
+    return fail(ctx, PROBE_ECAPACITY, "receive capacity overflow (ranks [%d,%d), recv_capacity=%d)", ctx->cfg.rank_begin,
+                ctx->cfg.rank_begin + ctx->cfg.local_ranks, ctx->cfg.recv_capacity);
+  if (flags[0]) return fail(ctx, PROBE_ECUDA, "device error word 0x%x", flags[0]);
+  return PROBE_OK;
+}
+
+const char* probe_last_error(probe_ctx ctx) {
+  if (ctx) return ctx->err.c_str();
+  std::lock_guard<std::mutex> lk(g_err_mu);
+  return g_last_error.c_str();
+}
+
+probe_status probe_finalize(probe_ctx ctx) {
+  if (!ctx) return PROBE_OK;
+  cudaDeviceSynchronize();
+  for (int p = 0; p < 2; ++p) {
+    cudaEventDestroy(ctx->ev_gate[p]); cudaEventDestroy(ctx->ev_gemm[p]); cudaEventDestroy(ctx->ev_comb[p]);
+    cudaEventDestroy(ctx->ev_pred[p]); cudaEventDestroy(ctx->ev_plan[p]); cudaEventDestroy(ctx->ev_slots[p]);
+  }
+  if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  if (ctx->pf) cudaStreamDestroy(ctx->pf);
+  delete ctx;
+  return PROBE_OK;
+}
+
+int64_t probe_launch_count(probe_ctx ctx) { return ctx ? ctx->launches : 0; }
+
+}  // extern "C"

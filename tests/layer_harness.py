@@ -1,0 +1,189 @@
+"""Run the PROBE layer pipeline on the GPU (through the C-ABI) and the fp64 oracle on
+the same seeded inputs; return both for element-wise comparison.
+
+Sequence (Continuous Lookahead Pipelining): forward(L0, static — layer 0
+is not predicted, R29) → predict(L1) → plan(L1) → prefetch(L1) → forward(L1, plan).
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import Optional
+
+import numpy as np
+import torch
+
+import oracle as O
+import probe_inputs as pi
+
+
+@dataclasses.dataclass
+class CaseCfg:
+    shape: pi.MoEShape
+    zipf_s: float = 1.2
+    step: int = 0
+    alpha_ps: int = 1
+    beta_ps: int = 0
+    n_sat: int = 0
+    replica_budget: int = 3
+    window_ns: int = 10 ** 9
+    residual: bool = True
+    out_fp32: bool = True
+    capacity_factor: float = 0.0
+    bias: bool = False
+
+
+def f64(t):
+    return pi.bf16_to_numpy_f64(t)
+
+
+def run_gpu(case: CaseCfg):
+    from paper_2602_00509_b200 import ProbeConfig, ProbeRuntime
+    sh = case.shape
+    G, E, k, H, F, T, h = sh.G, sh.E, sh.k, sh.H, sh.F, sh.T, sh.h
+    cfg = ProbeConfig(G=G, E=E, k=k, H=H, F=F, T=T, h=h if case.residual else 0,
+                      replica_budget=case.replica_budget, alpha_ps=case.alpha_ps, beta_ps=case.beta_ps,
+                      n_sat=case.n_sat, capacity_factor=case.capacity_factor)
+    rt = ProbeRuntime(cfg)
+    dev = "cuda"
+    L0 = pi.layer_inputs(sh, case.step, 0, case.zipf_s, device=dev)
+    L1 = pi.layer_inputs(sh, case.step, 1, case.zipf_s, device=dev)
+    W = [pi.router_weight(sh, p, device=dev) for p in (0, 1)]
+    b = [None, None]
+    if case.bias:
+        b = [torch.from_numpy((np.arange(E) % 4 - 1.5).astype(np.float32) / 64).to(dev) for _ in (0, 1)]
+    w13 = [None, None]
+    w2 = [None, None]
+    for p in (0, 1):
+        w13[p], w2[p] = pi.expert_weights(sh, p, device=dev)
+    r1, r2 = pi.predictor_residual(sh, 1, zero=not case.residual, device=dev)
+    if not case.residual:
+        r1 = r2 = None
+    odt = torch.float32 if case.out_fp32 else torch.bfloat16
+    out = [torch.empty(G, T, H, dtype=odt, device=dev) for _ in (0, 1)]
+    ids = [torch.empty(G, T, k, dtype=torch.int32, device=dev) for _ in (0, 1)]
+    gw = [torch.empty(G, T, k, dtype=torch.float32, device=dev) for _ in (0, 1)]
+    pc = torch.empty(G, E, dtype=torch.int32, device=dev)
+    plog = torch.empty(G, T, E, dtype=torch.float32, device=dev)
+    reps = torch.empty(G, 3, dtype=torch.int32, device=dev)
+    quota = torch.empty(G, E, G, dtype=torch.int32, device=dev)
+    stats = torch.empty(8, dtype=torch.int64, device=dev)
+    win = torch.full((G,), case.window_ns, dtype=torch.int64, device=dev)
+    res = {}
+    rt.forward(0, L0.x, W[0], b[0], w13[0], w2[0], out[0], use_plan=False, topk_ids=ids[0], topk_w=gw[0])
+    lay0 = debug(rt, cfg)
+    rt.predict(1, L0.x, W[1], b[1], r1, r2, pred_counts=pc, pred_logits=plog)
+    rt.plan(1, win, replicas=reps, quota=quota, stats=stats)
+    rt.prefetch(1, w13[1], w2[1], phase=0)
+    rt.forward(1, L1.x, W[1], b[1], w13[1], w2[1], out[1], use_plan=True, topk_ids=ids[1], topk_w=gw[1])
+    lay1 = debug(rt, cfg)
+    rt.check()
+    torch.cuda.synchronize()
+    res.update(out=[o.float().cpu().numpy() for o in out], ids=[i.cpu().numpy() for i in ids],
+               g=[g.cpu().numpy() for g in gw], pred_counts=pc.cpu().numpy(), pred_logits=plog.cpu().numpy(),
+               replicas=reps.cpu().numpy(), quota=quota.cpu().numpy(), stats=stats.cpu().numpy(),
+               layout=[lay0, lay1])
+    # replica slots (bank 1 for layer 1) must hold the home expert's weights bit-exactly
+    slots = []
+    for r in range(G):
+        sw13, sw2 = rt.replica_slots(r)
+        for q in range(3):
+            e = int(res["replicas"][r, q])
+            if e >= 0:
+                slots.append(bool(torch.equal(sw13[3 + q].view(torch.int16), w13[1][e].view(torch.int16)) and
+                                  torch.equal(sw2[3 + q].view(torch.int16), w2[1][e].view(torch.int16))))
+    res["slots_ok"] = slots
+    inputs = dict(L0=L0, L1=L1, W=W, b=b, w13=w13, w2=w2, r1=r1, r2=r2)
+    rt.close()
+    return res, inputs
+
+
+def debug(rt, cfg):
+    G, E, k, T = cfg.G, cfg.E, cfg.k, cfg.T
+    S = E // G + 3
+    counts = torch.empty(G, E, dtype=torch.int32, device="cuda")
+    split = torch.empty(G, E, G, dtype=torch.int32, device="cuda")
+    route = torch.empty(G, T, k, 2, dtype=torch.int32, device="cuda")
+    rows = torch.empty(G, S, dtype=torch.int32, device="cuda")
+    reps = torch.empty(G, 3, dtype=torch.int32, device="cuda")
+    rt.debug_layout(counts, split, route, rows, reps)
+    torch.cuda.synchronize()
+    return dict(counts=counts.cpu().numpy(), split_cum=split.cpu().numpy(), route=route.cpu().numpy(),
+                group_rows=rows.cpu().numpy(), replicas=reps.cpu().numpy())
+
+
+def run_oracle(case: CaseCfg, inputs, tokens=None):
+    sh = case.shape
+    G, E, k = sh.G, sh.E, sh.k
+    W = [f64(w) for w in inputs["W"]]
+    b = [None if v is None else v.double().cpu().numpy() for v in inputs["b"]]
+    xs0 = [f64(inputs["L0"].x[r]) for r in range(G)]
+    xs1 = [f64(inputs["L1"].x[r]) for r in range(G)]
+    W13 = [{e: f64(inputs["w13"][p][e]) for e in range(E)} for p in (0, 1)]
+    W2 = [{e: f64(inputs["w2"][p][e]) for e in range(E)} for p in (0, 1)]
+    r1 = None if inputs["r1"] is None else f64(inputs["r1"])
+    r2 = None if inputs["r2"] is None else f64(inputs["r2"])
+    ref0 = O.layer_reference(xs0, W[0], b[0], k, None, G, E, W13[0], W2[0], tokens)
+    nhat = []
+    plog = []
+    for r in range(G):
+        l, _ = O.predictor_logits(xs0[r], W[1], b[1], r1, r2)
+        plog.append(l)
+        nhat.append(np.bincount(O.topk_ids(l, k).reshape(-1), minlength=E))
+    nhat = np.stack(nhat)
+    pcfg = O.PlannerConfig(G=G, E=E, replica_budget=case.replica_budget, kmax=16, alpha_ps=case.alpha_ps,
+                           beta_ps=case.beta_ps, n_sat=case.n_sat, bw_bytes_per_us=770_000,
+                           expert_bytes=6 * sh.H * sh.F)
+    plan = O.plan_greedy(nhat, [case.window_ns] * G, pcfg)
+    ref1 = O.layer_reference(xs1, W[1], b[1], k, plan, G, E, W13[1], W2[1], tokens)
+    return dict(ref=[ref0, ref1], nhat=nhat, plan=plan, pred_logits=np.stack(plog))
+
+
+def group_rows_oracle(lay: O.Layout, G, E):
+    S = E // G + 3
+    out = np.zeros((G, S), dtype=np.int64)
+    for r in range(G):
+        sz = lay.group_sizes[r]
+        out[r, :len(sz)] = sz
+    return out
+
+
+def compare(case: CaseCfg, gpu, orc, tol: float = 2e-2):
+    """Bit-exact: ids, counts, predicted counts, plan, split, route, group sizes, replica bytes.
+    Tolerance: gate weights (1e-6 abs), predictor logits (1e-5 rel), outputs (tol · RMS)."""
+    sh = case.shape
+    G, E, k = sh.G, sh.E, sh.k
+    report = {}
+    for L in (0, 1):
+        ref = orc["ref"][L]
+        for r in range(G):
+            assert np.array_equal(gpu["ids"][L][r], ref["ids"][r]), f"ids L{L} r{r}"
+            assert np.abs(gpu["g"][L][r] - ref["g"][r]).max() < 1e-6, f"gate weights L{L} r{r}"
+        lay = gpu["layout"][L]
+        assert np.array_equal(lay["counts"], ref["n"]), f"counts L{L}"
+        assert np.array_equal(lay["split_cum"], np.cumsum(ref["split"], axis=2)), f"split L{L}"
+        for r in range(G):
+            assert np.array_equal(lay["route"][r, :, :, 0], ref["layout"].dest[r]), f"route dest L{L} r{r}"
+            assert np.array_equal(lay["route"][r, :, :, 1], ref["layout"].row[r]), f"route row L{L} r{r}"
+        assert np.array_equal(lay["group_rows"], group_rows_oracle(ref["layout"], G, E)), f"group rows L{L}"
+        errs = []
+        rms = np.sqrt(np.mean(np.concatenate([o.reshape(-1) for o in ref["out"]]) ** 2))
+        for r in range(G):
+            errs.append(np.abs(gpu["out"][L][r] - ref["out"][r]).max())
+        report[f"out_err_L{L}"] = float(max(errs) / rms)
+        assert max(errs) <= tol * rms, f"output L{L}: max err {max(errs)} > {tol} * RMS {rms}"
+    assert np.array_equal(gpu["pred_counts"], orc["nhat"]), "predicted counts"
+    pl = orc["pred_logits"]
+    report["pred_logit_err"] = float(np.abs(gpu["pred_logits"] - pl).max())
+    assert report["pred_logit_err"] <= 1e-5 * max(1.0, np.abs(pl).max()), "predictor logits"
+    plan = orc["plan"]
+    exp_reps = np.full((G, 3), -1)
+    for r in range(G):
+        exp_reps[r, :len(plan.replicas[r])] = plan.replicas[r]
+    assert np.array_equal(gpu["replicas"], exp_reps), f"replicas {gpu['replicas'].tolist()} vs {exp_reps.tolist()}"
+    assert np.array_equal(gpu["quota"], plan.quota), "quota"
+    assert gpu["stats"][0] == plan.iterations and gpu["stats"][2] == plan.maxL_before \
+        and gpu["stats"][3] == plan.maxL_after, f"plan stats {gpu['stats']}"
+    assert all(gpu["slots_ok"]), "replica slot bytes differ from home expert weights"
+    report["replicas"] = int((exp_reps >= 0).sum())
+    report["iterations"] = plan.iterations
+    return report

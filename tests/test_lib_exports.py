@@ -1,0 +1,61 @@
+"""CPU-side checks of the C-ABI library: it builds for sm_100a, loads, exports every
+symbol include/probe.h declares, validates configs, and contains tcgen05/TMA SASS."""
+import ctypes as C
+import os
+import re
+import shutil
+import subprocess
+
+import pytest
+
+from paper_2602_00509_b200 import _lib, build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    build.build()
+    return _lib.load()
+
+
+def test_header_symbols_exported(lib):
+    hdr = open(os.path.join(ROOT, "include", "probe.h")).read()
+    declared = set(re.findall(r"\b(probe_[a-z_]+)\s*\(", hdr))
+    assert declared == set(_lib.EXPORTS)
+    nm = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    for s in declared:
+        assert re.search(rf"\bT {s}$", nm, re.M), s
+        assert hasattr(lib, s)
+
+
+def test_workspace_and_validation(lib):
+    from paper_2602_00509_b200 import ProbeConfig, workspace_sizes
+    cfg = ProbeConfig(G=8, E=128, k=8, H=2048, F=768, T=8192, h=512, capacity_factor=4.0)
+    sz = workspace_sizes(cfg)
+    assert sz[_lib.BUF_RECV] == cfg.recv_capacity * 2048 * 2
+    assert sz[_lib.BUF_Y] == cfg.recv_capacity * 2048 * 4
+    assert sz[_lib.BUF_REP_W13] == 6 * 2 * 768 * 2048 * 2
+    assert all(s % 1024 == 0 for s in sz)
+    # invalid configs are rejected synchronously with a message (no GPU needed)
+    bad = cfg.to_c()
+    bad.num_experts = 100      # not divisible by G
+    arr = (C.c_uint64 * 7)()
+    st = lib.probe_init(C.byref(bad), arr, C.c_void_p(1024), C.byref(C.c_void_p()))
+    assert st == 2 and b"divisible" in lib.probe_last_error(None)
+    bad = cfg.to_c()
+    bad.replica_budget = 4     # at most three redundant experts per rank
+    st = lib.probe_init(C.byref(bad), arr, C.c_void_p(1024), C.byref(C.c_void_p()))
+    assert st == 3
+    bad = cfg.to_c()
+    bad.expert_bytes = 1
+    assert lib.probe_init(C.byref(bad), arr, C.c_void_p(1024), C.byref(C.c_void_p())) == 1
+
+
+@pytest.mark.skipif(shutil.which("cuobjdump") is None, reason="cuobjdump missing")
+def test_sass_is_blackwell_native(lib):
+    sass = subprocess.run(["cuobjdump", "-sass", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in sass          # tcgen05.mma
+    assert "UTMALDG" in sass          # TMA tensor loads
+    assert "LDTM" in sass             # tcgen05.ld (TMEM → registers)
+    assert "HMMA" not in sass.replace("UTCHMMA", "")   # no legacy mma.sync path
