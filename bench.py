@@ -1,0 +1,423 @@
+#!/usr/bin/env python
+"""bench.py — PROBE expert-parallel MoE layer (dynamic replication) on B200.
+
+One step = one pass of the whole hot path over one batch: the main
+track of layer L (gate → count all-gather → materialize plan(L) → dispatch →
+grouped SwiGLU GEMMs → combine) with the auxiliary track for L+1 (lookahead
+predictor → balance planner → split-phase replica prefetch) running beside it.
+Layers alternate parity; inputs cycle through a pool of Hadamard-encoded
+Zipf-skewed layers whose hotspots migrate layer to layer.
+
+Default workload: BASELINE.json configs[1] (Qwen3-30B-A3B-shaped: E=128, k=8,
+H=2048, F=768, 8192 tokens per rank, EP=8).  With --gpus N the G=8 logical EP
+ranks are spread over N GPUs (G/N per process); at N=1 all eight ranks run on
+one B200 (single-GPU EP emulation: every peer pointer is local HBM).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl probe|reference]
+                    [--config C1|C2|C3] [--zipf S]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import probe_inputs as pi  # noqa: E402
+
+METRIC_PREFILL = "MoE-layer prefill latency (ms)"
+METRIC_DECODE = "MoE-layer decode throughput (tokens/s)"
+POOL = 4            # distinct layer inputs cycled (each > L2: 268 MB of x at C1)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def cost_model(shape, pk):
+    """Integer planner constants from measured peaks (R11): α = F̄/F_peak, β = 2·2H/BW_net (λ=1),
+    n_sat = F_peak/BW_HBM (GEMM ridge in rows), BW_net = 770 GB/s measured peer copy."""
+    fpeak = pk["bf16_tflops_sustained"] * 1e12
+    fbar = 6.0 * shape.H * shape.F
+    alpha_ps = int(round(fbar / fpeak * 1e12))
+    bw_net = 770e9
+    beta_ps = int(round(2 * 2 * shape.H / bw_net * 1e12))
+    n_sat = int(round(fpeak / (pk["hbm_gbs"] * 1e9)))
+    return alpha_ps, beta_ps, n_sat, int(bw_net / 1e6)
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, gpu_index=0):
+        self.gpu = gpu_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        except Exception:
+            rows = []
+        sm = [float(r[0]) for r in rows if len(r) >= 7 and r[0].strip().replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if len(r) >= 7 and r[1].strip().replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            if len(r) >= 7:
+                for i, n in enumerate(names):
+                    if r[3 + i].strip() == "Active":
+                        reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# =============================================================================
+# PROBE arm
+# =============================================================================
+
+def run_probe(args):
+    from paper_2602_00509_b200 import ProbeConfig, ProbeRuntime
+    from paper_2602_00509_b200._lib import PHASES
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world} (launch N>1 with torchrun)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    shape = pi.SHAPES[args.config]
+    G = shape.G
+    if G % world:
+        raise SystemExit(f"EP={G} ranks cannot be spread over {world} GPUs")
+    GL = G // world
+    R0 = rank * GL
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist.group.WORLD
+    pk, pk_kind = peaks()
+    alpha_ps, beta_ps, n_sat, bw_Bpus = cost_model(shape, pk)
+    cfg = ProbeConfig(G=G, E=shape.E, k=shape.k, H=shape.H, F=shape.F, T=shape.T, h=shape.h, rank_begin=R0,
+                      local_ranks=GL, replica_budget=3, kmax=16, n_sat=n_sat, alpha_ps=alpha_ps, beta_ps=beta_ps,
+                      bw_bytes_per_us=bw_Bpus, capacity_factor=4.0 if G > 1 else 1.0)
+    if world > 1:
+        from paper_2602_00509_b200.dist import make_runtime_distributed
+        rt = make_runtime_distributed(cfg, dev, pg)
+    else:
+        rt = ProbeRuntime(cfg, dev)
+    ranks = list(range(R0, R0 + GL))
+    t0 = time.time()
+    pool = [pi.layer_inputs(shape, 0, i, args.zipf, ranks=ranks, device=dev, wrap=POOL) for i in range(POOL)]
+    W = [pi.router_weight(shape, p, device=dev) for p in (0, 1)]
+    experts = list(range(R0 * shape.E // G, (R0 + GL) * shape.E // G))
+    w13, w2 = [], []
+    for p in (0, 1):
+        a, b = pi.expert_weights(shape, p, experts=experts, device=dev)
+        w13.append(a)
+        w2.append(b)
+    res = [pi.predictor_residual(shape, p, device=dev) for p in (0, 1)]
+    gen_s = time.time() - t0
+    T, H = shape.T, shape.H
+    out = torch.empty(GL, T, H, dtype=torch.float32, device=dev)
+    # hiding window (R26): modeled per-rank expert-GEMM time at the balanced load
+    gemm_ns = int(6.0 * H * shape.F * T * shape.k / (pk["bf16_tflops_sustained"] * 1e12) * 1e9)
+    win = torch.full((G,), gemm_ns, dtype=torch.int64, device=dev)
+    main = torch.cuda.current_stream(dev)
+
+    def step(L, use_plan=True, x=None, fwd_plan=None):
+        li = pool[L % POOL]
+        p = L % 2
+        q = (L + 1) % 2
+        xx = li.x if x is None else x
+        fp = (use_plan and L > 0) if fwd_plan is None else fwd_plan
+        rt.forward(L, xx, W[p], None, w13[p], w2[p], out, use_plan=fp)
+        if use_plan:
+            rt.predict(L + 1, xx, W[q], None, res[q][0], res[q][1])
+            rt.plan(L + 1, win)
+            rt.prefetch(L + 1, w13[q], w2[q], phase=0)
+
+    def barrier():
+        if pg is not None:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+
+    def timed(nsteps, L0, use_plan=True, x_host=None, out_host=None, x_dev=None):
+        barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(main)
+        L = L0
+        for _ in range(nsteps):
+            if x_host is not None:
+                x_dev.copy_(x_host[L % POOL], non_blocking=True)
+                step(L, use_plan, x=x_dev)
+                out_host.copy_(out, non_blocking=True)
+            else:
+                step(L, use_plan)
+            L += 1
+        ev1.record(main)
+        barrier()
+        ms = ev0.elapsed_time(ev1) / nsteps
+        if pg is not None:
+            t = torch.tensor([ms], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, L
+
+    # ---- warm-up (layer 0 is static: nothing predicts it, R29)
+    L = 0
+    for _ in range(args.warmup):
+        step(L)
+        L += 1
+    torch.cuda.synchronize(dev)
+    rt.check()
+    # ---- timed region (PROBE)
+    launches0 = rt.launches()
+    with ClockSampler(local) as clk:
+        ms, L = timed(args.steps, L)
+    launches = rt.launches() - launches0
+    clocks = clk.summary()
+    # ---- per-phase profile (separate pass; CUDA events on the launching stream)
+    rt.profile(args.steps)
+    ms_prof, L = timed(args.steps, L)
+    ph = rt.profile_read()
+    phases = {n: float(ph[:, i].mean()) for i, n in enumerate(PHASES)}
+    rt.profile(0)
+    # ---- realized balance of the last layer
+    counts = torch.empty(G, shape.E, dtype=torch.int32, device=dev)
+    split = torch.empty(G, shape.E, G, dtype=torch.int32, device=dev)
+    reps = torch.empty(G, 3, dtype=torch.int32, device=dev)
+    rt.debug_layout(counts, split, None, None, reps)
+    torch.cuda.synchronize(dev)
+    EL = shape.E // G
+    n = counts.cpu().numpy().astype(np.int64)
+    sc = split.cpu().numpy().astype(np.int64)
+    sp = np.diff(np.concatenate([np.zeros((G, shape.E, 1), np.int64), sc], axis=2), axis=2)
+    pre = n.sum(axis=0).reshape(G, EL).sum(axis=1)
+    post = sp.sum(axis=(0, 1))
+    ir_pre = float(pre.max() / pre.mean())
+    ir_post = float(post.max() / post.mean())
+    nrep = int((reps >= 0).sum().item())
+    # ---- static-EP baseline (same library, replication disabled, no aux track)
+    for _ in range(2):
+        step(L, use_plan=False)
+        L += 1
+    ms_static, L = timed(args.steps, L, use_plan=False)
+    # ---- end-to-end through the API with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        x_host = [pool[i].x.cpu().pin_memory() for i in range(POOL)]
+        out_host = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+        x_dev = torch.empty_like(pool[0].x)
+        step(L, fwd_plan=False)           # re-enter the planned pipeline after the static pass
+        L += 1
+        step(L)
+        L += 1
+        ms_e2e, L = timed(max(3, min(args.steps, 10)), L, x_host=x_host, out_host=out_host, x_dev=x_dev)
+        bi = x_dev.numel() * x_dev.element_size()
+        bo = out.numel() * out.element_size()
+        e2e = {"value": ms_e2e if shape.name != "C2" else G * T / (ms_e2e / 1e3), "unit": "ms" if shape.name != "C2" else "tokens/s",
+               "h2d_bytes_per_step": bi * world, "d2h_bytes_per_step": bo * world}
+    rt.check()
+    # ---- roofline: the dominant kernel is grouped GEMM1 (4HF FLOPs per routed pair)
+    pairs = G * T * shape.k
+    fl1 = 4.0 * H * shape.F * pairs / world
+    fl2 = 2.0 * H * shape.F * pairs / world
+    t1 = phases["gemm1"] / 1e3
+    t2 = phases["gemm2"] / 1e3
+    peak_tf = pk["bf16_tflops_sustained"]
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "gemm1_traffic.json")
+    if os.path.exists(tfile):
+        tj = json.load(open(tfile))
+        if tj.get("config") == shape.name:
+            traffic = tj.get("dram_bytes_per_launch")
+    roof = {"kernel": "grouped_gemm_kernel<256,4> (expert GEMM1 + SwiGLU)", "bound": "tensor",
+            "achieved": fl1 / t1 / 1e12, "peak": peak_tf, "unit": "TFLOP/s", "frac": fl1 / t1 / 1e12 / peak_tf,
+            "traffic": traffic, "peak_kind": f"{pk_kind} bf16_tflops_sustained",
+            "algorithmic_flops_per_launch": fl1,
+            "gemm2": {"achieved": fl2 / t2 / 1e12, "frac": fl2 / t2 / 1e12 / peak_tf},
+            "expert_ffn": {"achieved": (fl1 + fl2) / (t1 + t2) / 1e12,
+                           "frac": (fl1 + fl2) / (t1 + t2) / 1e12 / peak_tf}}
+    result = None
+    if rank == 0:
+        cpu = None if args.no_cpu else cpu_baseline(shape, args, sample_tokens=args.cpu_tokens)
+        decode = shape.name == "C2"
+        value = G * T / (ms / 1e3) if decode else ms
+        result = {
+            "metric": METRIC_DECODE if decode else METRIC_PREFILL,
+            "value": value, "unit": "tokens/s" if decode else "ms",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": decode, "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic: Hadamard-encoded exact routing, Zipf(s) popularity, hotspots "
+                                     "migrating layer to layer, encoded predictor accuracy 0.9; random-init experts",
+            "config": {"workload": f"{shape.name}: E={shape.E} top-{shape.k} H={H} F={shape.F} "
+                                   f"T={T}/rank EP={G} ({GL} logical ranks per GPU)",
+                       "zipf_s": args.zipf, "replica_budget": 3, "kmax": 16, "alpha_ps": alpha_ps,
+                       "beta_ps": beta_ps, "n_sat": n_sat, "window_ns": gemm_ns,
+                       "l2": "inputs larger than L2 (x 268 MB/layer at C1, weights 1.2 GB/parity); no flush"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "phases_ms": phases,
+            "static_ep": {"ms_per_step": ms_static, "speedup_probe_vs_static": ms_static / ms},
+            "balance": {"ir_pre": ir_pre, "ir_post": ir_post, "replicas": nrep},
+            "setup_s": gen_s,
+        }
+        print(json.dumps(result), flush=True)
+    rt.close()
+    if pg is not None:
+        torch.distributed.destroy_process_group()
+    return result
+
+
+# =============================================================================
+# oracle (CPU) — cpu_baseline leg and --impl reference arm
+# =============================================================================
+
+_SAMPLE_CACHE = {}
+
+
+def _oracle_sample_inputs(shape, tokens_per_rank, step, layer, zipf):
+    key = (shape.name, tokens_per_rank, step, layer, zipf)
+    if key in _SAMPLE_CACHE:
+        return _SAMPLE_CACHE[key]
+    sh = shape.with_(T=tokens_per_rank)
+    li = pi.layer_inputs(sh, step, layer, zipf)
+    hit = set()
+    for d in li.designs:
+        hit |= set(int(e) for e in d.S.reshape(-1)) | set(int(e) for e in d.tie_e if e >= 0)
+    w13, w2 = pi.expert_weights(sh, layer % 2, experts=sorted(hit))
+    r1, r2 = pi.predictor_residual(sh, (layer + 1) % 2)
+    f = pi.bf16_to_numpy_f64
+    inp = dict(sh=sh, xs=[f(li.x[r]) for r in range(sh.G)], W=f(pi.router_weight(sh, layer % 2)),
+               Wn=f(pi.router_weight(sh, (layer + 1) % 2)), r1=f(r1), r2=f(r2),
+               W13={e: f(w13[i]) for i, e in enumerate(sorted(hit))},
+               W2={e: f(w2[i]) for i, e in enumerate(sorted(hit))})
+    _SAMPLE_CACHE.clear()
+    _SAMPLE_CACHE[key] = inp
+    return inp
+
+
+def oracle_layer_sample(shape, tokens_per_rank, step=0, layer=1, zipf=1.0):
+    """The whole hot path of one layer on the fp64 oracle for a token sample of every rank:
+    predictor (for the next layer), planner on the sample's n̂, gate, materialize, layout,
+    expert FFN + combine.  Returns (seconds, tokens processed).  Input generation is untimed."""
+    import oracle as O
+    inp = _oracle_sample_inputs(shape, tokens_per_rank, step, layer, zipf)
+    sh = inp["sh"]
+    G, E, k = sh.G, sh.E, sh.k
+    t0 = time.perf_counter()
+    nhat = [O.predict_counts(inp["xs"][r], inp["Wn"], None, inp["r1"], inp["r2"], k)[0] for r in range(G)]
+    pcfg = O.PlannerConfig(G=G, E=E, alpha_ps=6790, beta_ps=10640, n_sat=212, bw_bytes_per_us=770_000,
+                           expert_bytes=6 * sh.H * sh.F)
+    plan = O.plan_greedy(np.stack(nhat), [445_000] * G, pcfg)
+    O.layer_reference(inp["xs"], inp["W"], None, k, plan, G, E, inp["W13"], inp["W2"])
+    return time.perf_counter() - t0, G * tokens_per_rank
+
+
+def cpu_baseline(shape, args, sample_tokens=64):
+    secs, ntok = oracle_layer_sample(shape, sample_tokens, zipf=args.zipf)
+    full = shape.G * shape.T
+    ms_full = secs * full / ntok * 1e3
+    cores = len(os.sched_getaffinity(0))
+    decode = shape.name == "C2"
+    return {"value": (full / (ms_full / 1e3)) if decode else ms_full, "unit": "tokens/s" if decode else "ms",
+            "cores": cores, "kind": "oracle",
+            "sample": f"{sample_tokens} tokens on each of {shape.G} ranks through the full layer path "
+                      f"(gate, predictor, planner, materialize, layout, fp64 SwiGLU experts, combine) in "
+                      f"{secs:.2f} s, scaled linearly to {full} tokens"}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    shape = pi.SHAPES[args.config]
+    tok = args.ref_tokens
+    for _ in range(args.warmup):
+        oracle_layer_sample(shape, tok, zipf=args.zipf)
+    times = []
+    for i in range(args.steps):
+        s, n = oracle_layer_sample(shape, tok, zipf=args.zipf)
+        times.append(s)
+    full = shape.G * shape.T
+    ms = statistics.mean(times) * full / (shape.G * tok) * 1e3
+    decode = shape.name == "C2"
+    value = full / (ms / 1e3) if decode else ms
+    unit = "tokens/s" if decode else "ms"
+    cores = len(os.sched_getaffinity(0))
+    out = {"impl": "reference", "metric": METRIC_DECODE if decode else METRIC_PREFILL, "value": value,
+           "unit": unit, "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+           "higher_is_better": decode, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (same generator as the probe arm)",
+           "config": {"workload": f"{shape.name} (oracle on {tok} tokens/rank per step, scaled to the full layer)"},
+           "cpu_baseline": {"value": value, "unit": unit, "kind": "oracle", "cores": cores,
+                            "sample": f"{tok} tokens on each of {shape.G} ranks per step, full layer path"},
+           "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="probe", choices=["probe", "reference"])
+    ap.add_argument("--config", default="C1", choices=["C1", "C2", "C3"])
+    ap.add_argument("--zipf", type=float, default=1.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-tokens", type=int, default=256)
+    ap.add_argument("--ref-tokens", type=int, default=16)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_probe(args)
+
+
+if __name__ == "__main__":
+    main()

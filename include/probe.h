@@ -59,7 +59,7 @@ typedef struct {
   int32_t ep_size;        /* G = ep; 1..64 */
   int32_t rank_begin;     /* first logical rank hosted by this process */
   int32_t local_ranks;    /* number of logical ranks hosted by this process */
-  int32_t num_experts;    /* E; E % G == 0 (contiguous sharding P′, R22); E <= 1024 */
+  int32_t num_experts;    /* E; E % G == 0 (contiguous sharding P′, R22); E % 8 == 0; E <= 256 */
   int32_t top_k;          /* k; 1 <= k <= min(E, 16) */
   int32_t hidden;         /* H; multiple of 64 */
   int32_t ffn;            /* F (expert intermediate width); multiple of 64 */
@@ -172,6 +172,26 @@ probe_status probe_test_gemm(const void* A, int64_t a_rows, const void* B, int64
 probe_status probe_check(probe_ctx ctx);
 const char* probe_last_error(probe_ctx ctx);   /* ctx may be NULL (last global error) */
 probe_status probe_finalize(probe_ctx ctx);
+
+/* Phase profiling.  probe_profile(ctx, n) enables CUDA-event timing of the next n
+ * probe_moe_forward calls (events recorded on the stream each phase runs on;
+ * 0 disables).  probe_profile_read copies the elapsed milliseconds of every
+ * recorded forward into ms[n][PROBE_NPHASE] (synchronises) and returns how many
+ * forwards were recorded in *n_out.  Phases of the main track: */
+enum {
+  PROBE_PH_GATE = 0,      /* router GEMM + top-k (a1) */
+  PROBE_PH_COUNTS = 1,    /* chunk scan + actual-count all-gather (a3) */
+  PROBE_PH_LAYOUT = 2,    /* materialize plan + layout + GEMM schedules (a5) */
+  PROBE_PH_DISPATCH = 3,  /* token dispatch (a6) */
+  PROBE_PH_WAIT = 4,      /* exposed wait for replica slots (prefetch not hidden, R28) */
+  PROBE_PH_GEMM1 = 5,     /* grouped GEMM1 + SwiGLU epilogue (a7) */
+  PROBE_PH_GEMM2 = 6,     /* grouped GEMM2 (a7) */
+  PROBE_PH_COMBINE = 7,   /* gate-weighted combine (a8) */
+  PROBE_PH_TOTAL = 8,     /* whole forward on the main stream */
+  PROBE_NPHASE = 9
+};
+probe_status probe_profile(probe_ctx ctx, int32_t n);
+probe_status probe_profile_read(probe_ctx ctx, float* ms, int32_t* n_out);
 
 /* Number of library kernel launches enqueued so far by this context (bench accounting). */
 int64_t probe_launch_count(probe_ctx ctx);

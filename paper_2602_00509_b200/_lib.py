@@ -21,7 +21,9 @@ STATUS = {0: "PROBE_OK", 1: "PROBE_EINVAL", 2: "PROBE_ESHAPE", 3: "PROBE_EBUDGET
 # every exported symbol declared in include/probe.h
 EXPORTS = ["probe_workspace", "probe_init", "probe_moe_forward", "probe_predict", "probe_plan",
            "probe_prefetch", "probe_debug_layout", "probe_test_gemm", "probe_check", "probe_last_error",
-           "probe_finalize", "probe_launch_count"]
+           "probe_finalize", "probe_launch_count", "probe_profile", "probe_profile_read"]
+PROBE_NPHASE = 9
+PHASES = ["gate", "counts", "layout", "dispatch", "wait", "gemm1", "gemm2", "combine", "total"]
 
 
 class probe_config(C.Structure):
@@ -64,6 +66,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "probe_last_error": (C.c_char_p, [vp]),
         "probe_finalize": (i32, [vp]),
         "probe_launch_count": (i64, [vp]),
+        "probe_profile": (i32, [vp, i32]),
+        "probe_profile_read": (i32, [vp, vp, C.POINTER(C.c_int32)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

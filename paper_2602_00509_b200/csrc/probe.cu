@@ -153,6 +153,11 @@ struct probe_ctx_s {
   CUtensorMap map_recv, map_act, map_rw13, map_rw2;
   std::string err;
   int64_t launches = 0;
+  // phase profiling: prof_max forwards × (PROBE_NPHASE + 1) timing events
+  int prof_max = 0, prof_n = 0;
+  std::vector<cudaEvent_t> prof_ev;
+  cudaEvent_t pev(int ph) { return prof_ev[static_cast<size_t>(prof_n) * (PROBE_NPHASE + 1) + ph]; }
+  bool profiling() const { return prof_n < prof_max; }
   template <class T>
   T* at(size_t off) const {
     return reinterpret_cast<T*>(scratch + off);
@@ -360,6 +365,10 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   const Scratch& s = ctx->sl;
   int32_t* err = ctx->at<int32_t>(s.flags);
   int32_t* suspend = err + 1;
+  const bool prof = ctx->profiling();
+#define MARK(ph) \
+  if (prof) CK(cudaEventRecord(ctx->pev(ph), st))
+  MARK(0);
   // a1 gate: logits = x W_rᵀ (tcgen05), top-k + softmax + per-chunk ranks
   SmallGroups sg{};
   sg.n = 1;
@@ -373,12 +382,14 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
                      ctx->at<float>(s.gw), ctx->at<int32_t>(s.pos), ctx->at<int32_t>(s.hist), nullptr, nullptr);
   CKL();
   CK(cudaEventRecord(ctx->ev_gate[p], st));
+  MARK(1);
   // a3 actual-count all-gather (board kind 0, parity p)
   k_count_scan<<<d.GL, 256, 0, st>>>(d, nchunks, ctx->at<int32_t>(s.hist), ctx->at<int32_t>(s.cbase), sym_of(ctx),
                                      PROBE_BUF_BOARD, p);
   CKL();
   // a5 materialize plan(L) + layout
   if (use_plan) CK(cudaStreamWaitEvent(st, ctx->ev_plan[p], 0));
+  MARK(2);
   LayoutIn li;
   li.board_actual = reinterpret_cast<const int32_t*>(ctx->local_base[PROBE_BUF_BOARD]) + ((p * 2 + 0) * d.G) * d.E;
   li.quota = use_plan ? ctx->at<int32_t>(s.quota[p]) : nullptr;
@@ -397,6 +408,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   lo.err = err;
   k_layout<<<1, 512, 0, st>>>(d, li, lo);
   CKL();
+  MARK(3);
   // a6 dispatch
   {
     const int warps = d.GL * T;
@@ -406,14 +418,18 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
                                                 sym_of(ctx), PROBE_BUF_RECV, err);
     CKL();
   }
+  MARK(4);
   // a9 phase lock: the expert GEMMs need this layer's replica slots
   if (use_plan) CK(cudaStreamWaitEvent(st, ctx->ev_slots[p], 0));
+  MARK(5);
   CK(cudaEventRecord(ctx->ev_gemm[p], st));
   // a7 grouped SwiGLU expert FFN (tcgen05): act = SiLU(X W_gᵀ) ⊙ X W_uᵀ ; Y = act W_dᵀ
   CK(launch_gemm<256>(ctx->map_recv, *m13, ctx->map_rw13, lo.s1, d.H, ctx->num_sms, st));
   ++ctx->launches;
+  MARK(6);
   CK(launch_gemm<256>(ctx->map_act, *m2, ctx->map_rw2, lo.s2, d.F, ctx->num_sms, st));
   ++ctx->launches;
+  MARK(7);
   // a8 combine (raises the prefetch suspend flag, R27)
   if (out_fp32)
     k_combine<true><<<d.GL * T, 128, 0, st>>>(d, T, ctx->at<float>(s.gw), ctx->at<int32_t>(s.route), sym_of(ctx),
@@ -423,6 +439,9 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
                                                PROBE_BUF_Y, out, suspend, layer);
   CKL();
   CK(cudaEventRecord(ctx->ev_comb[p], st));
+  MARK(8);
+  if (prof) ++ctx->prof_n;
+#undef MARK
   if (topk_ids) CK(cudaMemcpyAsync(topk_ids, ctx->at<int32_t>(s.ids), GL * T * d.k * 4, cudaMemcpyDeviceToDevice, st));
   if (topk_w) CK(cudaMemcpyAsync(topk_w, ctx->at<float>(s.gw), GL * T * d.k * 4, cudaMemcpyDeviceToDevice, st));
   ctx->fwd_layer = layer;
@@ -645,5 +664,33 @@ probe_status probe_finalize(probe_ctx ctx) {
 }
 
 int64_t probe_launch_count(probe_ctx ctx) { return ctx ? ctx->launches : 0; }
+
+probe_status probe_profile(probe_ctx ctx, int32_t n) {
+  if (!ctx || n < 0) return fail(ctx, PROBE_EINVAL, "probe_profile: bad arguments");
+  CK(cudaDeviceSynchronize());
+  for (auto e : ctx->prof_ev) cudaEventDestroy(e);
+  ctx->prof_ev.assign(static_cast<size_t>(n) * (PROBE_NPHASE + 1), nullptr);
+  for (auto& e : ctx->prof_ev) CK(cudaEventCreate(&e));
+  ctx->prof_max = n;
+  ctx->prof_n = 0;
+  return PROBE_OK;
+}
+
+probe_status probe_profile_read(probe_ctx ctx, float* ms, int32_t* n_out) {
+  if (!ctx || !n_out) return fail(ctx, PROBE_EINVAL, "probe_profile_read: bad arguments");
+  CK(cudaDeviceSynchronize());
+  for (int i = 0; i < ctx->prof_n; ++i) {
+    cudaEvent_t* ev = &ctx->prof_ev[static_cast<size_t>(i) * (PROBE_NPHASE + 1)];
+    // phase j spans marks j..j+1; TOTAL spans 0..8
+    const int order[PROBE_NPHASE][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {4, 5}, {5, 6}, {6, 7}, {7, 8}, {0, 8}};
+    for (int j = 0; j < PROBE_NPHASE; ++j) {
+      float t = 0.f;
+      CK(cudaEventElapsedTime(&t, ev[order[j][0]], ev[order[j][1]]));
+      if (ms) ms[i * PROBE_NPHASE + j] = t;
+    }
+  }
+  *n_out = ctx->prof_n;
+  return PROBE_OK;
+}
 
 }  // extern "C"

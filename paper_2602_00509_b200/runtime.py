@@ -156,6 +156,18 @@ class ProbeRuntime:
     def check(self):
         check("probe_check", self.lib.probe_check(self.ctx), self.ctx)
 
+    def profile(self, n: int):
+        check("probe_profile", self.lib.probe_profile(self.ctx, n), self.ctx)
+
+    def profile_read(self):
+        """→ float32 tensor [n_forwards, PROBE_NPHASE] of milliseconds (synchronises)."""
+        n = C.c_int32(0)
+        check("probe_profile_read", self.lib.probe_profile_read(self.ctx, None, C.byref(n)), self.ctx)
+        out = torch.zeros(max(n.value, 1), _lib.PROBE_NPHASE, dtype=torch.float32)
+        check("probe_profile_read", self.lib.probe_profile_read(self.ctx, C.c_void_p(out.data_ptr()), C.byref(n)),
+              self.ctx)
+        return out[:n.value]
+
     def launches(self) -> int:
         return int(self.lib.probe_launch_count(self.ctx))
 

@@ -149,10 +149,13 @@ def draw_routing(shape: MoEShape, step: int, layer: int, rank: int, zipf_s: floa
 
 
 def design_rank(shape: MoEShape, step: int, layer: int, rank: int, zipf_s: float,
-                accuracy: float, hot_period: int = 1, ties: bool = True) -> RankDesign:
+                accuracy: float, hot_period: int = 1, ties: bool = True,
+                wrap: Optional[int] = None) -> RankDesign:
+    """wrap: layers form a cycle of this length (layer L's "next layer" is (L+1) mod wrap)."""
     E, k, T = shape.E, shape.k, shape.T
     S = draw_routing(shape, step, layer, rank, zipf_s, hot_period)
-    S_next = draw_routing(shape, step, layer + 1, rank, zipf_s, hot_period)
+    nxt = layer + 1 if wrap is None else (layer + 1) % wrap
+    S_next = draw_routing(shape, step, nxt, rank, zipf_s, hot_period)
     r = rng(shape.name, step, layer, rank, "design", zipf_s, accuracy)
     numer = np.tile(np.arange(16, 16 - k, -1, dtype=np.int64), (T, 1))
     tie_e = np.full(T, -1, dtype=np.int64)
@@ -167,15 +170,18 @@ def design_rank(shape: MoEShape, step: int, layer: int, rank: int, zipf_s: float
             cand = np.setdiff1d(np.arange(E), S[t])
             tie_e[t] = int(cand[r.integers(0, len(cand))])
     # prediction: each slot of S_next kept with prob `accuracy`, else a uniform
-    # expert outside S_next ∪ P ("≈90% Top-K accuracy")
+    # expert outside S_next ∪ P ("≈90% Top-K accuracy"); rejection sampling,
+    # vectorised over tokens, slots in order.
     P = S_next.copy()
-    for t in range(T):
-        for j in range(k):
-            if r.random() >= accuracy:
-                used = set(S_next[t].tolist()) | set(P[t].tolist())
-                cand = [e for e in range(E) if e not in used]
-                if cand:
-                    P[t, j] = cand[int(r.integers(0, len(cand)))]
+    for j in range(k):
+        rep = r.random(T) >= accuracy
+        idx = np.nonzero(rep)[0]
+        while len(idx):
+            cand = r.integers(0, E, size=len(idx))
+            bad = (cand[:, None] == S_next[idx]).any(axis=1) | (cand[:, None] == P[idx]).any(axis=1)
+            ok = idx[~bad]
+            P[ok, j] = cand[~bad]
+            idx = idx[bad]
     n_h = shape.n_h
     noise_rows = r.integers(2 * E, n_h, size=(T, 4))
     noise_coef = r.integers(-8, 9, size=(T, 4))
@@ -271,12 +277,12 @@ class LayerInputs:
 
 def layer_inputs(shape: MoEShape, step: int, layer: int, zipf_s: float = 1.0,
                  accuracy: float = 0.9, ranks: Optional[List[int]] = None, device="cpu",
-                 hot_period: int = 1, ties: bool = True) -> LayerInputs:
+                 hot_period: int = 1, ties: bool = True, wrap: Optional[int] = None) -> LayerInputs:
     ranks = list(range(shape.G)) if ranks is None else ranks
     p = layer % 2
     xs, ds = [], []
     for r in ranks:
-        d = design_rank(shape, step, layer, r, zipf_s, accuracy, hot_period, ties)
+        d = design_rank(shape, step, layer, r, zipf_s, accuracy, hot_period, ties, wrap)
         xs.append(encode_tokens(shape, d, p, step, layer, r, device))
         ds.append(d)
     return LayerInputs(layer, p, torch.stack(xs), ds)
