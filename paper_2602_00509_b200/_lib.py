@@ -48,6 +48,14 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
+    if path == LIB_PATH:
+        from . import build as _build
+        try:
+            if _build.stale():
+                _build.build()
+        except Exception as e:  # no nvcc: fall through to the existence check (no CPU fallback)
+            if not os.path.exists(path):
+                raise ImportError(f"libprobe.so missing and build failed: {e}") from e
     if not os.path.exists(path):
         raise ImportError(f"libprobe.so not built at {path} (run paper_2602_00509_b200/build.py); "
                           "there is no CPU fallback")
