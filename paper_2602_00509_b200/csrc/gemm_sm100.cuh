@@ -68,7 +68,9 @@ struct GemmSmem {
   static constexpr int B_BYTES = BN * 128;
   static constexpr int BAR_OFF = STAGES * (A_BYTES + B_BYTES);
   static constexpr int TS_OFF = BAR_OFF + (2 * STAGES + 4) * 8 + 16;
-  static constexpr int BYTES = TS_OFF + (kMaxGroups + 1) * 4 + 1024;  // + alignment slack
+  static constexpr int EPI_PITCH = 36;                                   // floats per staged row
+  static constexpr int EPI_OFF = TS_OFF + (kMaxGroups + 1) * 4;
+  static constexpr int BYTES = EPI_OFF + 4 * 32 * EPI_PITCH * 4 + 1024;  // + alignment slack
 };
 
 __device__ __forceinline__ int gemm_find_group(const int* ts, int ng, int tile) {
@@ -193,6 +195,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     const int q = warp & 3;
+    float* ebuf = reinterpret_cast<float*>(smem + L::EPI_OFF) + q * 32 * L::EPI_PITCH;
     int acc = 0;
     uint32_t aphase = 0;
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
@@ -201,81 +204,77 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       const int nt = gemm_ntiles_n(G, BN);
       const int tin = tile - ts[gi];
       const int mb = tin / nt, nb = tin % nt;
-      const int row = mb * 128 + q * 32 + lane;
-      const bool rv = row < G.m;
       ptx::mbar_wait(&tfull[acc], aphase);
       ptx::tc_fence_after();
       const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
-      if (G.mode == EPI_SWIGLU) {
-        __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(G.out) + static_cast<size_t>(row) * G.ldc;
+      const int row0 = mb * 128 + q * 32;          // first tile row of this warp
+      const bool swiglu = G.mode == EPI_SWIGLU;
+      const int nchunk = swiglu ? BN / 64 : BN / 32;
 #pragma unroll 1
-        for (int c = 0; c < BN / 64; ++c) {
-          uint32_t gv[32], uv[32];
-          ptx::tmem_ld32(tb + c * 32, gv);
+      for (int c = 0; c < nchunk; ++c) {
+        // 1) TMEM → registers (lane = row), fused epilogue math, stage row-major in smem
+        uint32_t v32[32];
+        float* wrow = ebuf + lane * L::EPI_PITCH;
+        if (swiglu) {
+          uint32_t uv[32];
+          ptx::tmem_ld32(tb + c * 32, v32);
           ptx::tmem_ld32(tb + BN / 2 + c * 32, uv);
           ptx::tmem_ld_wait();
-          const int col0 = nb * (BN / 2) + c * 32;
-          if (rv) {
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              if (col0 + v * 8 < G.n) {
-                uint4 o;
-                uint32_t* op = reinterpret_cast<uint32_t*>(&o);
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  const int i0 = v * 8 + 2 * e;
-                  const float a0 = silu_f(__uint_as_float(gv[i0])) * __uint_as_float(uv[i0]);
-                  const float a1 = silu_f(__uint_as_float(gv[i0 + 1])) * __uint_as_float(uv[i0 + 1]);
-                  op[e] = pack_bf16(a0, a1);
-                }
-                *reinterpret_cast<uint4*>(out + col0 + v * 8) = o;
-              }
-            }
-          }
-        }
-      } else if (G.mode == EPI_SILU_BF16) {
-        __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(G.out) + static_cast<size_t>(row) * G.ldc;
-#pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t v32[32];
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(wrow + i) =
+                make_float4(silu_f(__uint_as_float(v32[i])) * __uint_as_float(uv[i]),
+                            silu_f(__uint_as_float(v32[i + 1])) * __uint_as_float(uv[i + 1]),
+                            silu_f(__uint_as_float(v32[i + 2])) * __uint_as_float(uv[i + 2]),
+                            silu_f(__uint_as_float(v32[i + 3])) * __uint_as_float(uv[i + 3]));
+        } else {
           ptx::tmem_ld32(tb + c * 32, v32);
           ptx::tmem_ld_wait();
-          const int col0 = nb * BN + c * 32;
-          if (rv) {
+          if (G.mode == EPI_SILU_BF16) {
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              if (col0 + v * 8 < G.n) {
-                uint4 o;
-                uint32_t* op = reinterpret_cast<uint32_t*>(&o);
+            for (int i = 0; i < 32; i += 4)
+              *reinterpret_cast<float4*>(wrow + i) =
+                  make_float4(silu_f(__uint_as_float(v32[i])), silu_f(__uint_as_float(v32[i + 1])),
+                              silu_f(__uint_as_float(v32[i + 2])), silu_f(__uint_as_float(v32[i + 3])));
+          } else {
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  const int i0 = v * 8 + 2 * e;
-                  op[e] = pack_bf16(silu_f(__uint_as_float(v32[i0])), silu_f(__uint_as_float(v32[i0 + 1])));
-                }
-                *reinterpret_cast<uint4*>(out + col0 + v * 8) = o;
-              }
+            for (int i = 0; i < 32; i += 4)
+              *reinterpret_cast<float4*>(wrow + i) =
+                  make_float4(__uint_as_float(v32[i]), __uint_as_float(v32[i + 1]), __uint_as_float(v32[i + 2]),
+                              __uint_as_float(v32[i + 3]));
+          }
+        }
+        __syncwarp();
+        // 2) coalesced row writes: each warp store covers whole 128-byte row segments
+        const int col0 = (swiglu ? nb * (BN / 2) : nb * BN) + c * 32;
+        if (G.mode == EPI_F32) {
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int rl = it * 4 + (lane >> 3), cc = (lane & 7) * 4;
+            const int grow = row0 + rl;
+            if (grow < G.m && col0 + cc < G.n)
+              *reinterpret_cast<float4*>(reinterpret_cast<float*>(G.out) + static_cast<size_t>(grow) * G.ldc + col0 +
+                                         cc) = *reinterpret_cast<const float4*>(ebuf + rl * L::EPI_PITCH + cc);
+          }
+        } else {
+#pragma unroll
+          for (int it = 0; it < 4; ++it) {
+            const int rl = it * 8 + (lane >> 2), cc = (lane & 3) * 8;
+            const int grow = row0 + rl;
+            if (grow < G.m && col0 + cc < G.n) {
+              const float4 a = *reinterpret_cast<const float4*>(ebuf + rl * L::EPI_PITCH + cc);
+              const float4 b = *reinterpret_cast<const float4*>(ebuf + rl * L::EPI_PITCH + cc + 4);
+              uint4 o;
+              o.x = pack_bf16(a.x, a.y);
+              o.y = pack_bf16(a.z, a.w);
+              o.z = pack_bf16(b.x, b.y);
+              o.w = pack_bf16(b.z, b.w);
+              *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(G.out) + static_cast<size_t>(grow) * G.ldc +
+                                        col0 + cc) = o;
             }
           }
         }
-      } else {
-        float* out = reinterpret_cast<float*>(G.out) + static_cast<size_t>(row) * G.ldc;
-#pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t v32[32];
-          ptx::tmem_ld32(tb + c * 32, v32);
-          ptx::tmem_ld_wait();
-          const int col0 = nb * BN + c * 32;
-          if (rv) {
-#pragma unroll
-            for (int v = 0; v < 8; ++v) {
-              if (col0 + v * 4 < G.n) {
-                float4 o = make_float4(__uint_as_float(v32[4 * v]), __uint_as_float(v32[4 * v + 1]),
-                                       __uint_as_float(v32[4 * v + 2]), __uint_as_float(v32[4 * v + 3]));
-                *reinterpret_cast<float4*>(out + col0 + v * 4) = o;
-              }
-            }
-          }
-        }
+        __syncwarp();
       }
       ptx::tc_fence_before();
       __syncwarp();

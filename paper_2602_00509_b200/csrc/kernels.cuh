@@ -410,12 +410,17 @@ struct LayoutIn {
 };
 
 __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o) {
+  extern __shared__ int32_t sm_split[];            // [G][E][G] materialized split
   __shared__ int32_t reps[kMaxG * kMaxRb];
+  constexpr int kMaxGS = kMaxE + kMaxRb * kMaxG;   // G·S = E + 3G
+  __shared__ int32_t gt[kMaxGS];                   // rows per (dest, slot)
+  __shared__ int32_t gpre[kMaxGS];                 // first row of (dest, slot)
+  __shared__ int32_t t1[kMaxGroups], t2[kMaxGroups];
   const int G = d.G, E = d.E, EL = d.EL, S = EL + kMaxRb;
   const int tid = threadIdx.x;
   for (int i = tid; i < G * kMaxRb; i += blockDim.x) reps[i] = in.replicas ? in.replicas[i] : -1;
   __syncthreads();
-  // materialize (R23)
+  // (1) materialize (R23), one thread per (s, e)
   for (int i = tid; i < G * E; i += blockDim.x) {
     const int s = i / E, e = i % E;
     const int n = in.board_actual[s * E + e];
@@ -443,10 +448,11 @@ __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o
     int run = 0;
     for (int t = 0; t < G; ++t) {
       run += a[t];
+      sm_split[(s * E + e) * G + t] = a[t];
       o.split_cum[(s * E + e) * G + t] = run;
     }
   }
-  // slot_of
+  // (2) local slot of every expert on every rank
   for (int i = tid; i < G * E; i += blockDim.x) {
     const int r = i / E, e = i % E;
     int sl = -1;
@@ -457,32 +463,46 @@ __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o
   }
   for (int i = tid; i < G * kMaxRb; i += blockDim.x) o.replicas_used[i] = reps[i];
   __syncthreads();
-  // per destination: rows per (slot, src) in slot order then source order (R24)
+  // (3) rows per (dest r, slot j): base experts ascending, then replicas in slot order (R24)
+  for (int i = tid; i < G * S; i += blockDim.x) {
+    const int r = i / S, j = i % S;
+    const int e = (j < EL) ? r * EL + j : reps[r * kMaxRb + (j - EL)];
+    int tot = 0;
+    if (e >= 0)
+      for (int s = 0; s < G; ++s) tot += sm_split[(s * E + e) * G + r];
+    gt[i] = tot;
+    o.group_rows[i] = tot;
+  }
+  __syncthreads();
+  // (4) slot prefix per destination (G serial scans of length S)
   for (int r = tid; r < G; r += blockDim.x) {
     int run = 0;
     for (int j = 0; j < S; ++j) {
-      const int e = (j < EL) ? r * EL + j : reps[r * kMaxRb + (j - EL)];
-      const int before = run;
-      for (int s = 0; s < G; ++s) {
-        o.src_off[(r * S + j) * G + s] = run;
-        if (e >= 0) {
-          const int* c = &o.split_cum[(s * E + e) * G];
-          run += c[r] - (r > 0 ? c[r - 1] : 0);
-        }
-      }
-      o.group_rows[r * S + j] = run - before;
+      gpre[r * S + j] = run;
+      run += gt[r * S + j];
     }
   }
   __syncthreads();
-  // GEMM schedules for the local destinations
-  if (tid == 0) {
-    o.s1->num_groups = d.GL * S;
-    o.s2->num_groups = d.GL * S;
+  // (5) first row of every (dest, slot, source): rows of a slot ordered by source ↑ then token ↑
+  for (int i = tid; i < G * S; i += blockDim.x) {
+    const int r = i / S, j = i % S;
+    const int e = (j < EL) ? r * EL + j : reps[r * kMaxRb + (j - EL)];
+    int run = gpre[i];
+    for (int s = 0; s < G; ++s) {
+      o.src_off[i * G + s] = run;
+      if (e >= 0) run += sm_split[(s * E + e) * G + r];
+    }
   }
-  for (int i = tid; i < d.GL * S; i += blockDim.x) {
+  // (6) grouped-GEMM schedules of the local destinations
+  const int ng = d.GL * S;
+  if (tid == 0) {
+    o.s1->num_groups = ng;
+    o.s2->num_groups = ng;
+  }
+  for (int i = tid; i < ng; i += blockDim.x) {
     const int gl = i / S, j = i % S, r = d.R0 + gl;
-    const int off = o.src_off[(r * S + j) * G + 0];
-    int m = o.group_rows[r * S + j];
+    const int off = gpre[r * S + j];
+    int m = gt[r * S + j];
     if (off + m > d.cap) {
       atomicOr(o.err, ERR_RECV_OVERFLOW);
       m = d.cap - off;
@@ -501,10 +521,30 @@ __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o
     g2.out = reinterpret_cast<float*>(in.y_local) + static_cast<size_t>(arow) * d.H;
     o.s1->g[i] = g1;
     o.s2->g[i] = g2;
+    t1[i] = gemm_ntiles(g1, 256);
+    t2[i] = gemm_ntiles(g2, 256);
   }
   __syncthreads();
-  if (tid == 0) gemm_finalize_sched(o.s1, 256);
-  if (tid == 32) gemm_finalize_sched(o.s2, 256);
+  // (7) tile prefix (warp 0: s1, warp 1: s2), warp-parallel exclusive scan in chunks of 32
+  if (tid < 64) {
+    const int w = tid >> 5, lane = tid & 31;
+    int* tt = w == 0 ? t1 : t2;
+    GemmSched* sc = w == 0 ? o.s1 : o.s2;
+    int base = 0;
+    for (int c0 = 0; c0 < ng; c0 += 32) {
+      const int i = c0 + lane;
+      const int v = i < ng ? tt[i] : 0;
+      int x = v;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= off) x += y;
+      }
+      if (i < ng) sc->g[i].tile_start = base + x - v;
+      base += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (lane == 0) sc->total_tiles = base;
+  }
 }
 
 // =============================================================================
@@ -527,37 +567,46 @@ __global__ void __launch_bounds__(256) k_dispatch(Dims d, int T, const __nv_bflo
   const int s = d.R0 + gl;
   const int nchunks = (T + kChunk - 1) / kChunk;
   const int S = d.EL + kMaxRb;
+  const int k = d.k;
   const size_t pr = static_cast<size_t>(gl) * T + t;
-  uint4* dst[kMaxK];
-  int k = d.k;
-  for (int j = 0; j < k; ++j) {
-    int dd = 0, row = -1;
-    if (lane == 0) {
-      const int e = ids[pr * k + j];
-      const int p = cbase[(static_cast<size_t>(gl) * nchunks + t / kChunk) * d.E + e] + pos[pr * k + j];
-      const int* c = &split_cum[(s * d.E + e) * d.G];
-      while (dd < d.G - 1 && c[dd] <= p) ++dd;
-      const int excl = dd > 0 ? c[dd - 1] : 0;
-      const int sl = slot_of[dd * d.E + e];
-      row = src_off[(dd * S + sl) * d.G + s] + (p - excl);
-      if (sl < 0 || row >= d.cap || c[dd] <= p) {
-        atomicOr(err, ERR_RECV_OVERFLOW);
-        row = -1;
-      }
-      route[(pr * k + j) * 2] = dd;
-      route[(pr * k + j) * 2 + 1] = row;
+  // lane j < k: destination rank and receive row of slot j (R23 fill order, R24 layout)
+  uint8_t* dst_row = nullptr;
+  if (lane < k) {
+    const int e = ids[pr * k + lane];
+    const int p = cbase[(static_cast<size_t>(gl) * nchunks + t / kChunk) * d.E + e] + pos[pr * k + lane];
+    const int* c = &split_cum[(s * d.E + e) * d.G];
+    int dd = 0;
+    while (dd < d.G - 1 && c[dd] <= p) ++dd;
+    const int excl = dd > 0 ? c[dd - 1] : 0;
+    const int sl = slot_of[dd * d.E + e];
+    int row = (sl < 0) ? -1 : src_off[(dd * S + sl) * d.G + s] + (p - excl);
+    if (sl < 0 || row >= d.cap || c[dd] <= p) {
+      atomicOr(err, ERR_RECV_OVERFLOW);
+      row = -1;
     }
-    dd = __shfl_sync(0xffffffffu, dd, 0);
-    row = __shfl_sync(0xffffffffu, row, 0);
-    dst[j] = row < 0 ? nullptr
-                     : reinterpret_cast<uint4*>(sym.at(buf_recv, d.G, dd) + static_cast<size_t>(row) * d.H * 2);
+    route[(pr * k + lane) * 2] = dd;
+    route[(pr * k + lane) * 2 + 1] = row;
+    if (row >= 0) dst_row = sym.at(buf_recv, d.G, dd) + static_cast<size_t>(row) * d.H * 2;
   }
+  // copy: the x row is read once (batches of 8 × 16 B per lane in flight) and stored k times
   const uint4* src = reinterpret_cast<const uint4*>(x + pr * d.H);
   const int nv = d.H / 8;
-  for (int c = lane; c < nv; c += 32) {
-    const uint4 v = __ldg(src + c);
-    for (int j = 0; j < k; ++j)
-      if (dst[j]) dst[j][c] = v;
+  for (int c0 = 0; c0 < nv; c0 += 32 * 8) {
+    uint4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int c = c0 + u * 32 + lane;
+      if (c < nv) v[u] = __ldg(src + c);
+    }
+    for (int j = 0; j < k; ++j) {
+      uint4* dst = reinterpret_cast<uint4*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(dst_row), j));
+      if (!dst) continue;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = c0 + u * 32 + lane;
+        if (c < nv) dst[c] = v[u];
+      }
+    }
   }
 }
 

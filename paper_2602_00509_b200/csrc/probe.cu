@@ -320,6 +320,8 @@ probe_status probe_init(const probe_config* cfg, const uint64_t* peer_ptrs, void
   if (e == cudaSuccess) {
     const size_t plan_smem = static_cast<size_t>(G) * c.num_experts * G * 4;
     e = cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(plan_smem));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_layout, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(plan_smem));
   }
   if (e != cudaSuccess) {
     delete ctx;
@@ -406,7 +408,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   lo.s1 = ctx->at<GemmSched>(s.s_g1);
   lo.s2 = ctx->at<GemmSched>(s.s_g2);
   lo.err = err;
-  k_layout<<<1, 512, 0, st>>>(d, li, lo);
+  k_layout<<<1, 512, static_cast<size_t>(d.G) * d.E * d.G * 4, st>>>(d, li, lo);
   CKL();
   MARK(3);
   // a6 dispatch
