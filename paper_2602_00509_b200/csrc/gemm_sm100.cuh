@@ -69,7 +69,7 @@ struct GemmSmem {
   static constexpr int BAR_OFF = STAGES * (A_BYTES + B_BYTES);
   static constexpr int TS_OFF = BAR_OFF + (2 * STAGES + 4) * 8 + 16;
   static constexpr int EPI_PITCH = 36;                                   // floats per staged row
-  static constexpr int EPI_OFF = TS_OFF + (kMaxGroups + 1) * 4;
+  static constexpr int EPI_OFF = (TS_OFF + (kMaxGroups + 1) * 4 + 127) / 128 * 128;
   static constexpr int BYTES = EPI_OFF + 4 * 32 * EPI_PITCH * 4 + 1024;  // + alignment slack
 };
 
