@@ -37,13 +37,20 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-// Bounded wait: a protocol bug traps (kernel error) after ~10 s instead of hanging the GPU.
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// Bounded wait: a protocol bug traps (kernel error) after 30 s of wall time instead of
+// hanging the GPU.  (%globaltimer, not clock64: profilers replay/serialise kernels.)
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   if (mbar_try_wait(a, parity)) return;
-  const long long t0 = clock64();
+  const uint64_t t0 = globaltimer_ns();
+  uint32_t n = 0;
   while (!mbar_try_wait(a, parity)) {
-    if (clock64() - t0 > 20000000000ll) __trap();
+    if ((++n & 1023u) == 0 && globaltimer_ns() - t0 > 30000000000ull) __trap();
   }
 }
 
