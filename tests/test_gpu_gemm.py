@@ -63,3 +63,36 @@ def test_gemm_swiglu_and_silu():
     torch.cuda.synchronize()
     ref = torch.nn.functional.silu(A.float() @ B[:256].float().T)
     assert (out.float() - ref).abs().max().item() <= 2 ** -7 * ref.abs().max().item() + 1e-3
+
+
+@pytest.mark.parametrize("mode,N,K,rows", [(0, 256, 256, 40000), (2, 512, 768, 30000), (0, 128, 2048, 65536)])
+def test_gemm_multi_tile_per_cta_exact(mode, N, K, rows):
+    """Several tiles per persistent CTA (TMEM accumulator double buffer, phase wrap-around)."""
+    from paper_2602_00509_b200 import test_gemm
+    A = _grid((rows, K), 11 + K)
+    B = _grid((2 * N, K), 12 + K)
+    half = rows // 2 + 77
+    groups = [[0, half, 0, 0], [half, rows - half, N, half]]
+    Cout = torch.full((rows, N), float("nan"), device="cuda")
+    test_gemm(A, B, groups, N, mode, Cout)
+    torch.cuda.synchronize()
+    ref = _ref(A, B, groups, N)
+    for (a_row, m, b_row, c_row) in groups:
+        got = Cout[c_row:c_row + m].double()
+        bad = (got != ref[c_row]).any(dim=1).nonzero()
+        assert bad.numel() == 0, (mode, N, K, rows, bad[:10].flatten().tolist())
+
+
+def test_gemm_multi_tile_swiglu():
+    from paper_2602_00509_b200 import test_gemm
+    F, K, rows = 768, 2048, 20000
+    A = _grid((rows, K), 21)
+    B = _grid((2 * F, K), 22)
+    act = torch.zeros(rows, F, dtype=torch.bfloat16, device="cuda")
+    test_gemm(A, B, [[0, rows, 0, 0]], 2 * F, 1, act)
+    torch.cuda.synchronize()
+    g = A.double() @ B[:F].double().T
+    u = A.double() @ B[F:].double().T
+    ref = (torch.nn.functional.silu(g) * u)
+    err = ((act.double() - ref).abs() / (ref.abs() + 1e-3)).max().item()
+    assert err < 2 ** -7, err
