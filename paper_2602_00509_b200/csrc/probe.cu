@@ -52,22 +52,27 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, ui
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Tensor-map cache with STABLE addresses (fixed ring; a call uses <= 6 maps, so a
+// returned pointer stays valid for the rest of that call and the next 250 encodes).
 struct MapCache {
   struct Ent {
-    const void* p;
-    uint64_t rows, cols;
-    uint32_t box;
+    const void* p = nullptr;
+    uint64_t rows = 0, cols = 0;
+    uint32_t box = 0;
     CUtensorMap map;
   };
-  std::vector<Ent> ents;
+  static constexpr int kCap = 256;
+  Ent ents[kCap];
+  int next = 0;
   const CUtensorMap* get(const void* p, uint64_t rows, uint64_t cols, uint32_t box) {
     for (auto& e : ents)
       if (e.p == p && e.rows == rows && e.cols == cols && e.box == box) return &e.map;
-    Ent e{p, rows, cols, box, {}};
+    Ent& e = ents[next];
+    next = (next + 1) % kCap;
+    e.p = nullptr;
     if (!make_map(&e.map, p, rows, cols, box)) return nullptr;
-    if (ents.size() >= 256) ents.erase(ents.begin());
-    ents.push_back(e);
-    return &ents.back().map;
+    e.p = p; e.rows = rows; e.cols = cols; e.box = box;
+    return &e.map;
   }
 };
 
