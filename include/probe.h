@@ -167,6 +167,14 @@ probe_status probe_test_gemm(const void* A, int64_t a_rows, const void* B, int64
                              int32_t K, int32_t N, const int32_t* groups, int32_t num_groups,
                              int32_t mode, void* C, void* stream);
 
+/* Timing hook: as probe_test_gemm with an explicit kernel variant (-1 = default for
+ * `mode`; 0: BN=128/6 stages/4 epilogue warps, 1: 256/4/4, 2: 256/3/8, 3: 128/4/8),
+ * run once, then `reps` times between CUDA events on `stream`; *ms_out = mean ms. */
+probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int64_t b_rows,
+                              int32_t K, int32_t N, const int32_t* groups, int32_t num_groups,
+                              int32_t mode, int32_t variant, int32_t reps, float* ms_out, void* C,
+                              void* stream);
+
 /* Synchronise this context's streams; return PROBE_ECAPACITY if the device
  * error word is set (receive overflow: the layer's output is invalid). */
 probe_status probe_check(probe_ctx ctx);

@@ -62,7 +62,7 @@ __device__ inline void gemm_finalize_sched(GemmSched* s, int BN) {
   s->total_tiles = acc;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int EW = 4>
 struct GemmSmem {
   static constexpr int A_BYTES = 128 * 128;
   static constexpr int B_BYTES = BN * 128;
@@ -70,7 +70,7 @@ struct GemmSmem {
   static constexpr int TS_OFF = BAR_OFF + (2 * STAGES + 4) * 8 + 16;
   static constexpr int EPI_PITCH = 36;                                   // floats per staged row
   static constexpr int EPI_OFF = (TS_OFF + (kMaxGroups + 1) * 4 + 127) / 128 * 128;
-  static constexpr int BYTES = EPI_OFF + 4 * 32 * EPI_PITCH * 4 + 1024;  // + alignment slack
+  static constexpr int BYTES = EPI_OFF + EW * 32 * EPI_PITCH * 4 + 1024;  // + alignment slack
 };
 
 __device__ __forceinline__ int gemm_find_group(const int* ts, int ng, int tile) {
@@ -89,11 +89,52 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-template <int BN, int STAGES>
-__global__ void __launch_bounds__(256, 1)
+// Stage one warp's 32 rows × 32 fp32 (row = lane) in smem and write them with
+// coalesced row segments (fp32: 4 rows × 128 B per store; bf16: 8 rows × 64 B).
+template <int PITCH>
+__device__ __forceinline__ void epi_store_chunk(float* ebuf, int lane, const float (&v)[32], const GemmGroup& G,
+                                                int row0, int col0) {
+  float* wrow = ebuf + lane * PITCH;
+#pragma unroll
+  for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(wrow + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+  __syncwarp();
+  if (G.mode == EPI_F32) {
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int rl = it * 4 + (lane >> 3), cc = (lane & 7) * 4;
+      const int grow = row0 + rl;
+      if (grow < G.m && col0 + cc < G.n)
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(G.out) + static_cast<size_t>(grow) * G.ldc + col0 + cc) =
+            *reinterpret_cast<const float4*>(ebuf + rl * PITCH + cc);
+    }
+  } else {
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int rl = it * 8 + (lane >> 2), cc = (lane & 3) * 8;
+      const int grow = row0 + rl;
+      if (grow < G.m && col0 + cc < G.n) {
+        const float4 a = *reinterpret_cast<const float4*>(ebuf + rl * PITCH + cc);
+        const float4 b = *reinterpret_cast<const float4*>(ebuf + rl * PITCH + cc + 4);
+        uint4 o;
+        o.x = pack_bf16(a.x, a.y);
+        o.y = pack_bf16(a.z, a.w);
+        o.z = pack_bf16(b.x, b.y);
+        o.w = pack_bf16(b.z, b.w);
+        *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(G.out) + static_cast<size_t>(grow) * G.ldc + col0 +
+                                  cc) = o;
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// EW epilogue warps (4 or 8): warp 4+i reads TMEM lane quarter i%4 and handles the
+// column chunks c ≡ i/4 (mod EW/4).  Threads = 128 + 32·EW.
+template <int BN, int STAGES, int EW = 4>
+__global__ void __launch_bounds__(128 + 32 * EW, 1)
 grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
                     const __grid_constant__ CUtensorMap tmB1, const GemmSched* __restrict__ sched, int K) {
-  using L = GemmSmem<BN, STAGES>;
+  using L = GemmSmem<BN, STAGES, EW>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -118,7 +159,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], 4);
+      ptx::mbar_init(&tempty[a], EW);
     }
     ptx::fence_barrier_init();
     ptx::tma_prefetch_desc(&tmA);
@@ -195,7 +236,9 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     const int q = warp & 3;
-    float* ebuf = reinterpret_cast<float*>(smem + L::EPI_OFF) + q * 32 * L::EPI_PITCH;
+    const int part = (warp - 4) >> 2;
+    constexpr int NPART = EW / 4;
+    float* ebuf = reinterpret_cast<float*>(smem + L::EPI_OFF) + (warp - 4) * 32 * L::EPI_PITCH;
     int acc = 0;
     uint32_t aphase = 0;
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
@@ -208,73 +251,38 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       ptx::tc_fence_after();
       const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
       const int row0 = mb * 128 + q * 32;          // first tile row of this warp
-      const bool swiglu = G.mode == EPI_SWIGLU;
-      const int nchunk = swiglu ? BN / 64 : BN / 32;
+      if (G.mode == EPI_SWIGLU) {
 #pragma unroll 1
-      for (int c = 0; c < nchunk; ++c) {
-        // 1) TMEM → registers (lane = row), fused epilogue math, stage row-major in smem
-        uint32_t v32[32];
-        float* wrow = ebuf + lane * L::EPI_PITCH;
-        if (swiglu) {
-          uint32_t uv[32];
-          ptx::tmem_ld32(tb + c * 32, v32);
+        for (int c = part; c < BN / 64; c += NPART) {
+          uint32_t gv[32], uv[32];
+          ptx::tmem_ld32(tb + c * 32, gv);
           ptx::tmem_ld32(tb + BN / 2 + c * 32, uv);
           ptx::tmem_ld_wait();
+          float v[32];
 #pragma unroll
-          for (int i = 0; i < 32; i += 4)
-            *reinterpret_cast<float4*>(wrow + i) =
-                make_float4(silu_f(__uint_as_float(v32[i])) * __uint_as_float(uv[i]),
-                            silu_f(__uint_as_float(v32[i + 1])) * __uint_as_float(uv[i + 1]),
-                            silu_f(__uint_as_float(v32[i + 2])) * __uint_as_float(uv[i + 2]),
-                            silu_f(__uint_as_float(v32[i + 3])) * __uint_as_float(uv[i + 3]));
-        } else {
-          ptx::tmem_ld32(tb + c * 32, v32);
+          for (int i = 0; i < 32; ++i) v[i] = silu_f(__uint_as_float(gv[i])) * __uint_as_float(uv[i]);
+          epi_store_chunk<L::EPI_PITCH>(ebuf, lane, v, G, row0, nb * (BN / 2) + c * 32);
+        }
+      } else {
+        // two chunks in flight per TMEM wait
+#pragma unroll 1
+        for (int c = part; c < BN / 32; c += 2 * NPART) {
+          const int c2 = c + NPART;
+          uint32_t va[32], vb[32];
+          ptx::tmem_ld32(tb + c * 32, va);
+          if (c2 < BN / 32) ptx::tmem_ld32(tb + c2 * 32, vb);
           ptx::tmem_ld_wait();
-          if (G.mode == EPI_SILU_BF16) {
+          float v[32];
+          const bool silu = G.mode == EPI_SILU_BF16;
 #pragma unroll
-            for (int i = 0; i < 32; i += 4)
-              *reinterpret_cast<float4*>(wrow + i) =
-                  make_float4(silu_f(__uint_as_float(v32[i])), silu_f(__uint_as_float(v32[i + 1])),
-                              silu_f(__uint_as_float(v32[i + 2])), silu_f(__uint_as_float(v32[i + 3])));
-          } else {
+          for (int i = 0; i < 32; ++i) v[i] = silu ? silu_f(__uint_as_float(va[i])) : __uint_as_float(va[i]);
+          epi_store_chunk<L::EPI_PITCH>(ebuf, lane, v, G, row0, nb * BN + c * 32);
+          if (c2 < BN / 32) {
 #pragma unroll
-            for (int i = 0; i < 32; i += 4)
-              *reinterpret_cast<float4*>(wrow + i) =
-                  make_float4(__uint_as_float(v32[i]), __uint_as_float(v32[i + 1]), __uint_as_float(v32[i + 2]),
-                              __uint_as_float(v32[i + 3]));
+            for (int i = 0; i < 32; ++i) v[i] = silu ? silu_f(__uint_as_float(vb[i])) : __uint_as_float(vb[i]);
+            epi_store_chunk<L::EPI_PITCH>(ebuf, lane, v, G, row0, nb * BN + c2 * 32);
           }
         }
-        __syncwarp();
-        // 2) coalesced row writes: each warp store covers whole 128-byte row segments
-        const int col0 = (swiglu ? nb * (BN / 2) : nb * BN) + c * 32;
-        if (G.mode == EPI_F32) {
-#pragma unroll
-          for (int it = 0; it < 8; ++it) {
-            const int rl = it * 4 + (lane >> 3), cc = (lane & 7) * 4;
-            const int grow = row0 + rl;
-            if (grow < G.m && col0 + cc < G.n)
-              *reinterpret_cast<float4*>(reinterpret_cast<float*>(G.out) + static_cast<size_t>(grow) * G.ldc + col0 +
-                                         cc) = *reinterpret_cast<const float4*>(ebuf + rl * L::EPI_PITCH + cc);
-          }
-        } else {
-#pragma unroll
-          for (int it = 0; it < 4; ++it) {
-            const int rl = it * 8 + (lane >> 2), cc = (lane & 3) * 8;
-            const int grow = row0 + rl;
-            if (grow < G.m && col0 + cc < G.n) {
-              const float4 a = *reinterpret_cast<const float4*>(ebuf + rl * L::EPI_PITCH + cc);
-              const float4 b = *reinterpret_cast<const float4*>(ebuf + rl * L::EPI_PITCH + cc + 4);
-              uint4 o;
-              o.x = pack_bf16(a.x, a.y);
-              o.y = pack_bf16(a.z, a.w);
-              o.z = pack_bf16(b.x, b.y);
-              o.w = pack_bf16(b.z, b.w);
-              *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(G.out) + static_cast<size_t>(grow) * G.ldc +
-                                        col0 + cc) = o;
-            }
-          }
-        }
-        __syncwarp();
       }
       ptx::tc_fence_before();
       __syncwarp();

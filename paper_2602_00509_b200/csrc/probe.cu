@@ -196,23 +196,41 @@ probe_status fail(probe_ctx ctx, probe_status st, const char* fmt, ...) {
     if (e_ != cudaSuccess) return fail(ctx, PROBE_ECUDA, "launch @%d: %s", __LINE__, cudaGetErrorString(e_)); \
   } while (0)
 
-template <int BN>
-constexpr int stages_for() { return BN == 256 ? 4 : 6; }
+// GEMM variants: (BN, STAGES, epilogue warps).  V_GATE: logits/predictor (N ≤ 256),
+// V_SWIGLU: expert GEMM1 (bf16 act out), V_F32: expert GEMM2 (fp32 Y out, epilogue-heavy).
+enum GemmVariant { V_128_6_4 = 0, V_256_4_4 = 1, V_256_3_8 = 2, V_128_4_8 = 3 };
 
-template <int BN>
-cudaError_t launch_gemm(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, const GemmSched* s, int K,
-                        int grid, cudaStream_t st) {
-  constexpr int ST = stages_for<BN>();
-  using L = GemmSmem<BN, ST>;
+template <int BN, int ST, int EW>
+cudaError_t launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, const GemmSched* s,
+                          int K, int grid, cudaStream_t st) {
+  using L = GemmSmem<BN, ST, EW>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(grouped_gemm_kernel<BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(grouped_gemm_kernel<BN, ST, EW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          L::BYTES);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  grouped_gemm_kernel<BN, ST><<<grid, 256, L::BYTES, st>>>(a, b0, b1, s, K);
+  grouped_gemm_kernel<BN, ST, EW><<<grid, 128 + 32 * EW, L::BYTES, st>>>(a, b0, b1, s, K);
   return cudaGetLastError();
+}
+
+cudaError_t launch_gemm_v(int v, const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1,
+                          const GemmSched* s, int K, int grid, cudaStream_t st) {
+  switch (v) {
+    case V_128_6_4: return launch_gemm_t<128, 6, 4>(a, b0, b1, s, K, grid, st);
+    case V_256_4_4: return launch_gemm_t<256, 4, 4>(a, b0, b1, s, K, grid, st);
+    case V_256_3_8: return launch_gemm_t<256, 3, 8>(a, b0, b1, s, K, grid, st);
+    case V_128_4_8: return launch_gemm_t<128, 4, 8>(a, b0, b1, s, K, grid, st);
+  }
+  return cudaErrorInvalidValue;
+}
+int variant_bn(int v) { return (v == V_128_6_4 || v == V_128_4_8) ? 128 : 256; }
+
+template <int BN>
+cudaError_t launch_gemm(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, const GemmSched* s, int K,
+                        int grid, cudaStream_t st) {
+  return launch_gemm_v(BN == 256 ? V_256_4_4 : V_128_6_4, a, b0, b1, s, K, grid, st);
 }
 
 template <bool PRED>
@@ -434,7 +452,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   CK(launch_gemm<256>(ctx->map_recv, *m13, ctx->map_rw13, lo.s1, d.H, ctx->num_sms, st));
   ++ctx->launches;
   MARK(6);
-  CK(launch_gemm<256>(ctx->map_act, *m2, ctx->map_rw2, lo.s2, d.F, ctx->num_sms, st));
+  CK(launch_gemm_v(V_256_3_8, ctx->map_act, *m2, ctx->map_rw2, lo.s2, d.F, ctx->num_sms, st));
   ++ctx->launches;
   MARK(7);
   // a8 combine (raises the prefetch suspend flag, R27)
@@ -602,11 +620,20 @@ probe_status probe_debug_layout(probe_ctx ctx, int32_t* counts, int32_t* split, 
 
 probe_status probe_test_gemm(const void* A, int64_t a_rows, const void* B, int64_t b_rows, int32_t K, int32_t N,
                              const int32_t* groups, int32_t num_groups, int32_t mode, void* C, void* stream) {
+  return probe_bench_gemm(A, a_rows, B, b_rows, K, N, groups, num_groups, mode, -1, 1, nullptr, C, stream);
+}
+
+probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int64_t b_rows, int32_t K, int32_t N,
+                              const int32_t* groups, int32_t num_groups, int32_t mode, int32_t variant, int32_t reps,
+                              float* ms_out, void* C, void* stream) {
   probe_ctx ctx = nullptr;
-  if (!A || !B || !groups || !C || num_groups < 1 || num_groups > kMaxGroups || K < 1 || N < 8 || N % 8)
+  if (!A || !B || !groups || !C || num_groups < 1 || num_groups > kMaxGroups || K < 1 || N < 8 || N % 8 ||
+      reps < 1 || mode < 0 || mode > 3)
     return fail(nullptr, PROBE_EINVAL, "probe_test_gemm: bad arguments");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int BN = (mode == 1 || mode == 2) ? 256 : 128;
+  if (variant < 0) variant = mode == 1 ? V_256_4_4 : (mode == 2 ? V_256_3_8 : V_128_6_4);
+  if (variant > V_128_4_8) return fail(nullptr, PROBE_EINVAL, "bad variant");
+  const int BN = variant_bn(variant);
   const int emode = mode == 1 ? EPI_SWIGLU : (mode == 3 ? EPI_SILU_BF16 : EPI_F32);
   const int n_out = mode == 1 ? N / 2 : N;
   std::vector<uint8_t> host(sizeof(GemmSched), 0);
@@ -630,8 +657,23 @@ probe_status probe_test_gemm(const void* A, int64_t a_rows, const void* B, int64
   int dev = 0, sms = 148;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  cudaError_t e = BN == 256 ? launch_gemm<256>(ma, mb, mb, ds, K, sms, st) : launch_gemm<128>(ma, mb, mb, ds, K, sms, st);
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  cudaError_t e = launch_gemm_v(variant, ma, mb, mb, ds, K, sms, st);   // warm-up / single run
+  if (e == cudaSuccess && reps > 1) {
+    e = cudaEventRecord(e0, st);
+    for (int r = 0; r < reps && e == cudaSuccess; ++r) e = launch_gemm_v(variant, ma, mb, mb, ds, K, sms, st);
+    if (e == cudaSuccess) e = cudaEventRecord(e1, st);
+  }
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess && reps > 1 && ms_out) {
+    float t = 0.f;
+    e = cudaEventElapsedTime(&t, e0, e1);
+    *ms_out = t / reps;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
   cudaFree(ds);
   if (e != cudaSuccess) return fail(nullptr, PROBE_ECUDA, "probe_test_gemm: %s", cudaGetErrorString(e));
   return PROBE_OK;

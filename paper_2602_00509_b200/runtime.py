@@ -191,3 +191,15 @@ def test_gemm(A: torch.Tensor, B: torch.Tensor, groups: List[List[int]], N: int,
     st = lib.probe_test_gemm(_ptr(A), A.shape[0], _ptr(B), B.shape[0], A.shape[1], N, flat, len(groups), mode,
                              _ptr(C_out), _stream(stream))
     check("probe_test_gemm", st)
+
+
+def bench_gemm(A: torch.Tensor, B: torch.Tensor, groups: List[List[int]], N: int, mode: int, C_out: torch.Tensor,
+               variant: int = -1, reps: int = 10, stream=None) -> float:
+    """Mean milliseconds of one grouped-GEMM launch (variant per probe.h), `reps` back-to-back launches."""
+    lib = _lib.load()
+    flat = (C.c_int32 * (4 * len(groups)))(*[int(v) for g in groups for v in g])
+    ms = C.c_float(0.0)
+    st = lib.probe_bench_gemm(_ptr(A), A.shape[0], _ptr(B), B.shape[0], A.shape[1], N, flat, len(groups), mode,
+                              variant, reps, C.byref(ms), _ptr(C_out), _stream(stream))
+    check("probe_bench_gemm", st)
+    return float(ms.value)

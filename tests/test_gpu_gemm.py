@@ -65,16 +65,19 @@ def test_gemm_swiglu_and_silu():
     assert (out.float() - ref).abs().max().item() <= 2 ** -7 * ref.abs().max().item() + 1e-3
 
 
-@pytest.mark.parametrize("mode,N,K,rows", [(0, 256, 256, 40000), (2, 512, 768, 30000), (0, 128, 2048, 65536)])
-def test_gemm_multi_tile_per_cta_exact(mode, N, K, rows):
-    """Several tiles per persistent CTA (TMEM accumulator double buffer, phase wrap-around)."""
-    from paper_2602_00509_b200 import test_gemm
+@pytest.mark.parametrize("mode,N,K,rows,variant", [(0, 256, 256, 40000, 0), (2, 512, 768, 30000, 1),
+                                                   (2, 512, 768, 30000, 2), (0, 128, 2048, 65536, 0),
+                                                   (0, 384, 512, 20000, 3), (2, 2048, 768, 9000, 2)])
+def test_gemm_multi_tile_per_cta_exact(mode, N, K, rows, variant):
+    """Several tiles per persistent CTA (TMEM accumulator double buffer, phase wrap-around),
+    every kernel variant (BN, stages, epilogue warps)."""
+    from paper_2602_00509_b200 import bench_gemm
     A = _grid((rows, K), 11 + K)
     B = _grid((2 * N, K), 12 + K)
     half = rows // 2 + 77
     groups = [[0, half, 0, 0], [half, rows - half, N, half]]
     Cout = torch.full((rows, N), float("nan"), device="cuda")
-    test_gemm(A, B, groups, N, mode, Cout)
+    bench_gemm(A, B, groups, N, mode, Cout, variant=variant, reps=1)
     torch.cuda.synchronize()
     ref = _ref(A, B, groups, N)
     for (a_row, m, b_row, c_row) in groups:
@@ -83,13 +86,14 @@ def test_gemm_multi_tile_per_cta_exact(mode, N, K, rows):
         assert bad.numel() == 0, (mode, N, K, rows, bad[:10].flatten().tolist())
 
 
-def test_gemm_multi_tile_swiglu():
-    from paper_2602_00509_b200 import test_gemm
+@pytest.mark.parametrize("variant", [1, 2])
+def test_gemm_multi_tile_swiglu(variant):
+    from paper_2602_00509_b200 import bench_gemm
     F, K, rows = 768, 2048, 20000
     A = _grid((rows, K), 21)
     B = _grid((2 * F, K), 22)
     act = torch.zeros(rows, F, dtype=torch.bfloat16, device="cuda")
-    test_gemm(A, B, [[0, rows, 0, 0]], 2 * F, 1, act)
+    bench_gemm(A, B, [[0, rows, 0, 0]], 2 * F, 1, act, variant=variant, reps=1)
     torch.cuda.synchronize()
     g = A.double() @ B[:F].double().T
     u = A.double() @ B[F:].double().T
