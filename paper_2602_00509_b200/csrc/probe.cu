@@ -628,18 +628,18 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
                               float* ms_out, void* C, void* stream) {
   probe_ctx ctx = nullptr;
   if (!A || !B || !groups || !C || num_groups < 1 || num_groups > kMaxGroups || K < 1 || N < 8 || N % 8 ||
-      reps < 1 || mode < 0 || mode > 3)
+      reps < 1 || mode < 0 || mode > 4)
     return fail(nullptr, PROBE_EINVAL, "probe_test_gemm: bad arguments");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (variant < 0) variant = mode == 1 ? V_256_4_4 : (mode == 2 ? V_256_3_8 : V_128_6_4);
   if (variant > V_128_4_8) return fail(nullptr, PROBE_EINVAL, "bad variant");
   const int BN = variant_bn(variant);
-  const int emode = mode == 1 ? EPI_SWIGLU : (mode == 3 ? EPI_SILU_BF16 : EPI_F32);
+  const int emode = mode == 1 ? EPI_SWIGLU : (mode == 3 ? EPI_SILU_BF16 : (mode == 4 ? EPI_NONE : EPI_F32));
   const int n_out = mode == 1 ? N / 2 : N;
   std::vector<uint8_t> host(sizeof(GemmSched), 0);
   GemmSched* hs = reinterpret_cast<GemmSched*>(host.data());
   hs->num_groups = num_groups;
-  const size_t esz = emode == EPI_F32 ? 4 : 2;
+  const size_t esz = emode == EPI_SWIGLU || emode == EPI_SILU_BF16 ? 2 : 4;
   int acc = 0;
   for (int i = 0; i < num_groups; ++i) {
     const int* g = groups + 4 * i;
