@@ -32,6 +32,8 @@ struct GemmGroup {
   int32_t n;           // output columns (SwiGLU: activation columns = F)
   int32_t ldc;         // output row stride, elements
   int32_t tile_start;  // prefix of tiles over groups
+  int32_t out_row;     // row of this group's row 0 in the output tensor map (TMA store path)
+  int32_t tma_out;     // 1: fp32 output through the tmC tensor map (full 32-row slabs)
   void* out;           // output of row 0 / col 0 of this group
 };
 
@@ -68,9 +70,12 @@ struct GemmSmem {
   static constexpr int B_BYTES = BN * 128;
   static constexpr int BAR_OFF = STAGES * (A_BYTES + B_BYTES);
   static constexpr int TS_OFF = BAR_OFF + (2 * STAGES + 4) * 8 + 16;
-  static constexpr int EPI_PITCH = 36;                                   // floats per staged row
-  static constexpr int EPI_OFF = (TS_OFF + (kMaxGroups + 1) * 4 + 127) / 128 * 128;
-  static constexpr int BYTES = EPI_OFF + EW * 32 * EPI_PITCH * 4 + 1024;  // + alignment slack
+  static constexpr int EPI_OFF = (TS_OFF + (kMaxGroups + 1) * 4 + 1023) / 1024 * 1024;
+  // per epilogue warp: NB staging tiles of 32 rows × 128 B, 16-byte chunks XOR-swizzled by
+  // (row mod 8) = the TMA SWIZZLE_128B layout (also bank-conflict-free for the manual path)
+  static constexpr int NB = (EW == 8) ? 2 : 1;
+  static constexpr int EPI_STRIDE = NB * 4096;
+  static constexpr int BYTES = EPI_OFF + EW * EPI_STRIDE + 1024;                // + alignment slack
 };
 
 __device__ __forceinline__ int gemm_find_group(const int* ts, int ng, int tile) {
@@ -89,50 +94,76 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-// Stage one warp's 32 rows × 32 fp32 (row = lane) in smem and write them with
-// coalesced row segments (fp32: 4 rows × 128 B per store; bf16: 8 rows × 64 B).
-template <int PITCH>
-__device__ __forceinline__ void epi_store_chunk(float* ebuf, int lane, const float (&v)[32], const GemmGroup& G,
-                                                int row0, int col0) {
-  if (G.mode == EPI_NONE) {
-    float acc = 0.f;
-#pragma unroll
-    for (int i = 0; i < 32; ++i) acc += v[i];
-    if (acc == 12345.678f) ebuf[lane] = acc;   // keep the TMEM loads alive
-    return;
-  }
-  float* wrow = ebuf + lane * PITCH;
-#pragma unroll
-  for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(wrow + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-  __syncwarp();
+// Swizzled 32×32 fp32 staging tile (row r at r·32 floats, 16-B chunk j at (j ^ (r & 7)) · 4).
+__device__ __forceinline__ int swz(int r, int j) { return r * 32 + ((j ^ (r & 7)) << 2); }
+
+// Write the staged rows with coalesced row segments (fp32: 4 rows × 128 B per warp store;
+// bf16: 8 rows × 64 B) masking rows ≥ G.m and columns ≥ G.n (group tails).
+__device__ __forceinline__ void epi_store_manual(const float* tile, int lane, const GemmGroup& G, int row0,
+                                                 int col0) {
+  if (G.mode == EPI_NONE) return;
   if (G.mode == EPI_F32) {
 #pragma unroll
     for (int it = 0; it < 8; ++it) {
-      const int rl = it * 4 + (lane >> 3), cc = (lane & 7) * 4;
+      const int rl = it * 4 + (lane >> 3), j = lane & 7;
       const int grow = row0 + rl;
-      if (grow < G.m && col0 + cc < G.n)
-        *reinterpret_cast<float4*>(reinterpret_cast<float*>(G.out) + static_cast<size_t>(grow) * G.ldc + col0 + cc) =
-            *reinterpret_cast<const float4*>(ebuf + rl * PITCH + cc);
+      if (grow < G.m && col0 + 4 * j < G.n)
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(G.out) + static_cast<size_t>(grow) * G.ldc + col0 + 4 * j) =
+            *reinterpret_cast<const float4*>(tile + swz(rl, j));
     }
   } else {
 #pragma unroll
     for (int it = 0; it < 4; ++it) {
-      const int rl = it * 8 + (lane >> 2), cc = (lane & 3) * 8;
+      const int rl = it * 8 + (lane >> 2), j = (lane & 3) * 2;
       const int grow = row0 + rl;
-      if (grow < G.m && col0 + cc < G.n) {
-        const float4 a = *reinterpret_cast<const float4*>(ebuf + rl * PITCH + cc);
-        const float4 b = *reinterpret_cast<const float4*>(ebuf + rl * PITCH + cc + 4);
+      if (grow < G.m && col0 + 4 * j < G.n) {
+        const float4 a = *reinterpret_cast<const float4*>(tile + swz(rl, j));
+        const float4 b = *reinterpret_cast<const float4*>(tile + swz(rl, j + 1));
         uint4 o;
         o.x = pack_bf16(a.x, a.y);
         o.y = pack_bf16(a.z, a.w);
         o.z = pack_bf16(b.x, b.y);
         o.w = pack_bf16(b.z, b.w);
         *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(G.out) + static_cast<size_t>(grow) * G.ldc + col0 +
-                                  cc) = o;
+                                  4 * j) = o;
       }
     }
   }
+}
+
+// Stage one warp's 32 rows × 32 values (row = lane) and store them: TMA tensor store
+// for full 32-row fp32 slabs (tma_out), coalesced manual stores otherwise.  `tsel`
+// rotates over NB tiles; lane 0 owns the bulk-async group of this warp.
+template <int NB>
+__device__ __forceinline__ void epi_chunk(float* tiles, int& tsel, int lane, const float (&v)[32],
+                                          const GemmGroup& G, const CUtensorMap* tmC, int row0, int col0) {
+  if (G.mode == EPI_NONE) {
+    float acc = 0.f;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) acc += v[i];
+    if (acc == 12345.678f) tiles[lane] = acc;   // keep the TMEM loads alive
+    return;
+  }
+  float* tile = tiles + tsel * 1024;
+  if (lane == 0) ptx::bulk_wait_read<NB - 1>();   // the TMA store that last read this tile is done
   __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    *reinterpret_cast<float4*>(tile + swz(lane, j)) = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+  const bool tma = G.tma_out && (row0 + 31 < G.m) && (col0 < G.n);
+  if (tma) {
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      ptx::tma_store_2d(tmC, tile, col0, G.out_row + row0);
+      ptx::bulk_commit();
+    }
+  } else {
+    __syncwarp();
+    epi_store_manual(tile, lane, G, row0, col0);
+  }
+  __syncwarp();
+  tsel = (tsel + 1) % NB;
 }
 
 // EW epilogue warps (4 or 8): warp 4+i reads TMEM lane quarter i%4 and handles the
@@ -140,7 +171,8 @@ __device__ __forceinline__ void epi_store_chunk(float* ebuf, int lane, const flo
 template <int BN, int STAGES, int EW = 4>
 __global__ void __launch_bounds__(128 + 32 * EW, 1)
 grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
-                    const __grid_constant__ CUtensorMap tmB1, const GemmSched* __restrict__ sched, int K) {
+                    const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmC,
+                    const GemmSched* __restrict__ sched, int K) {
   using L = GemmSmem<BN, STAGES, EW>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -245,7 +277,8 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     const int q = warp & 3;
     const int part = (warp - 4) >> 2;
     constexpr int NPART = EW / 4;
-    float* ebuf = reinterpret_cast<float*>(smem + L::EPI_OFF) + (warp - 4) * 32 * L::EPI_PITCH;
+    float* tiles = reinterpret_cast<float*>(smem + L::EPI_OFF + (warp - 4) * L::EPI_STRIDE);   // 1024-aligned
+    int tsel = 0;
     int acc = 0;
     uint32_t aphase = 0;
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
@@ -268,7 +301,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = silu_f(__uint_as_float(gv[i])) * __uint_as_float(uv[i]);
-          epi_store_chunk<L::EPI_PITCH>(ebuf, lane, v, G, row0, nb * (BN / 2) + c * 32);
+          epi_chunk<L::NB>(tiles, tsel, lane, v, G, &tmC, row0, nb * (BN / 2) + c * 32);
         }
       } else {
         // two chunks in flight per TMEM wait
@@ -282,12 +315,15 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           float v[32];
           const bool silu = G.mode == EPI_SILU_BF16;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = silu ? silu_f(__uint_as_float(va[i])) : __uint_as_float(va[i]);
-          epi_store_chunk<L::EPI_PITCH>(ebuf, lane, v, G, row0, nb * BN + c * 32);
-          if (c2 < BN / 32) {
+          for (int h = 0; h < 2; ++h) {
+            const int cc = h == 0 ? c : c2;
+            if (cc >= BN / 32) break;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = silu ? silu_f(__uint_as_float(vb[i])) : __uint_as_float(vb[i]);
-            epi_store_chunk<L::EPI_PITCH>(ebuf, lane, v, G, row0, nb * BN + c2 * 32);
+            for (int i = 0; i < 32; ++i) {
+              const float x = __uint_as_float(h == 0 ? va[i] : vb[i]);
+              v[i] = silu ? silu_f(x) : x;
+            }
+            epi_chunk<L::NB>(tiles, tsel, lane, v, G, &tmC, row0, nb * BN + cc * 32);
           }
         }
       }
@@ -298,6 +334,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       if (acc == 0) aphase ^= 1;
     }
   }
+  if (warp >= 4 && lane == 0) ptx::bulk_wait<0>();
   __syncthreads();
   if (warp == 2) {
     ptx::tc_fence_after();

@@ -3,6 +3,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -54,6 +55,18 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, ui
 
 // Tensor-map cache with STABLE addresses (fixed ring; a call uses <= 6 maps, so a
 // returned pointer stays valid for the rest of that call and the next 250 encodes).
+// fp32 output map for TMA tensor stores: box {32 cols (128 B), 32 rows}, SWIZZLE_128B.
+bool make_map_f32_out(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols) {
+  if (!load_encode()) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 4};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t es[2] = {1, 1};
+  return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 struct MapCache {
   struct Ent {
     const void* p = nullptr;
@@ -155,7 +168,7 @@ struct probe_ctx_s {
   int last_T = 0;
   int num_sms = 148;
   MapCache maps;
-  CUtensorMap map_recv, map_act, map_rw13, map_rw2;
+  CUtensorMap map_recv, map_act, map_rw13, map_rw2, map_y;
   std::string err;
   int64_t launches = 0;
   // phase profiling: prof_max forwards × (PROBE_NPHASE + 1) timing events
@@ -201,8 +214,8 @@ probe_status fail(probe_ctx ctx, probe_status st, const char* fmt, ...) {
 enum GemmVariant { V_128_6_4 = 0, V_256_4_4 = 1, V_256_3_8 = 2, V_128_4_8 = 3 };
 
 template <int BN, int ST, int EW>
-cudaError_t launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, const GemmSched* s,
-                          int K, int grid, cudaStream_t st) {
+cudaError_t launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, const CUtensorMap& c,
+                          const GemmSched* s, int K, int grid, cudaStream_t st) {
   using L = GemmSmem<BN, ST, EW>;
   static bool attr = false;
   if (!attr) {
@@ -211,17 +224,17 @@ cudaError_t launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b0, const CUt
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  grouped_gemm_kernel<BN, ST, EW><<<grid, 128 + 32 * EW, L::BYTES, st>>>(a, b0, b1, s, K);
+  grouped_gemm_kernel<BN, ST, EW><<<grid, 128 + 32 * EW, L::BYTES, st>>>(a, b0, b1, c, s, K);
   return cudaGetLastError();
 }
 
 cudaError_t launch_gemm_v(int v, const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1,
-                          const GemmSched* s, int K, int grid, cudaStream_t st) {
+                          const CUtensorMap& c, const GemmSched* s, int K, int grid, cudaStream_t st) {
   switch (v) {
-    case V_128_6_4: return launch_gemm_t<128, 6, 4>(a, b0, b1, s, K, grid, st);
-    case V_256_4_4: return launch_gemm_t<256, 4, 4>(a, b0, b1, s, K, grid, st);
-    case V_256_3_8: return launch_gemm_t<256, 3, 8>(a, b0, b1, s, K, grid, st);
-    case V_128_4_8: return launch_gemm_t<128, 4, 8>(a, b0, b1, s, K, grid, st);
+    case V_128_6_4: return launch_gemm_t<128, 6, 4>(a, b0, b1, c, s, K, grid, st);
+    case V_256_4_4: return launch_gemm_t<256, 4, 4>(a, b0, b1, c, s, K, grid, st);
+    case V_256_3_8: return launch_gemm_t<256, 3, 8>(a, b0, b1, c, s, K, grid, st);
+    case V_128_4_8: return launch_gemm_t<128, 4, 8>(a, b0, b1, c, s, K, grid, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -230,7 +243,7 @@ int variant_bn(int v) { return (v == V_128_6_4 || v == V_128_4_8) ? 128 : 256; }
 template <int BN>
 cudaError_t launch_gemm(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, const GemmSched* s, int K,
                         int grid, cudaStream_t st) {
-  return launch_gemm_v(BN == 256 ? V_256_4_4 : V_128_6_4, a, b0, b1, s, K, grid, st);
+  return launch_gemm_v(BN == 256 ? V_256_4_4 : V_128_6_4, a, b0, b1, a, s, K, grid, st);
 }
 
 template <bool PRED>
@@ -246,7 +259,7 @@ void launch_topk(const Dims& d, int T, int nchunks, cudaStream_t st, const float
 GemmGroup mk_group(int a_row, int m, int b_row, int b_sel, int mode, int n, int ldc, void* out) {
   GemmGroup g;
   g.a_row = a_row; g.m = m; g.b_row = b_row; g.b_sel = b_sel; g.mode = mode; g.n = n; g.ldc = ldc;
-  g.tile_start = 0; g.out = out;
+  g.tile_start = 0; g.out_row = 0; g.tma_out = 0; g.out = out;
   return g;
 }
 
@@ -354,7 +367,8 @@ probe_status probe_init(const probe_config* cfg, const uint64_t* peer_ptrs, void
   bool ok = make_map(&ctx->map_recv, ctx->local_base[PROBE_BUF_RECV], GL * cap, H, 128) &&
             make_map(&ctx->map_act, ctx->scratch + ctx->sl.act, GL * cap, F, 128) &&
             make_map(&ctx->map_rw13, ctx->local_base[PROBE_BUF_REP_W13], GL * 2 * kMaxRb * 2 * F, H, 128) &&
-            make_map(&ctx->map_rw2, ctx->local_base[PROBE_BUF_REP_W2], GL * 2 * kMaxRb * H, F, 128);
+            make_map(&ctx->map_rw2, ctx->local_base[PROBE_BUF_REP_W2], GL * 2 * kMaxRb * H, F, 128) &&
+            make_map_f32_out(&ctx->map_y, ctx->local_base[PROBE_BUF_Y], GL * cap, H);
   if (!ok) {
     delete ctx;
     return fail(nullptr, PROBE_ECUDA, "probe_init: cuTensorMapEncodeTiled failed");
@@ -452,7 +466,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   CK(launch_gemm<256>(ctx->map_recv, *m13, ctx->map_rw13, lo.s1, d.H, ctx->num_sms, st));
   ++ctx->launches;
   MARK(6);
-  CK(launch_gemm_v(V_256_3_8, ctx->map_act, *m2, ctx->map_rw2, lo.s2, d.F, ctx->num_sms, st));
+  CK(launch_gemm_v(V_256_3_8, ctx->map_act, *m2, ctx->map_rw2, ctx->map_y, lo.s2, d.F, ctx->num_sms, st));
   ++ctx->launches;
   MARK(7);
   // a8 combine (raises the prefetch suspend flag, R27)
@@ -641,16 +655,25 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
   hs->num_groups = num_groups;
   const size_t esz = emode == EPI_SWIGLU || emode == EPI_SILU_BF16 ? 2 : 4;
   int acc = 0;
+  int64_t c_rows = 1;
   for (int i = 0; i < num_groups; ++i) {
     const int* g = groups + 4 * i;
     hs->g[i] = mk_group(g[0], g[1], g[2], 0, emode, n_out, n_out, static_cast<uint8_t*>(C) + static_cast<size_t>(g[3]) * n_out * esz);
+    hs->g[i].out_row = g[3];
+    hs->g[i].tma_out = emode == EPI_F32 && n_out % 32 == 0 ? 1 : 0;
+    c_rows = std::max<int64_t>(c_rows, static_cast<int64_t>(g[3]) + g[1]);
     hs->g[i].tile_start = acc;
     acc += gemm_ntiles(hs->g[i], BN);
   }
   hs->total_tiles = acc;
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mc;
   if (!make_map(&ma, A, a_rows, K, 128) || !make_map(&mb, B, b_rows, K, BN / 2))
     return fail(nullptr, PROBE_ECUDA, "tensor map encode failed");
+  if (emode == EPI_F32 && n_out % 32 == 0) {
+    if (!make_map_f32_out(&mc, C, c_rows, n_out)) return fail(nullptr, PROBE_ECUDA, "tensor map encode failed");
+  } else {
+    mc = ma;
+  }
   GemmSched* ds = nullptr;
   CK(cudaMalloc(&ds, sizeof(GemmSched)));
   CK(cudaMemcpy(ds, hs, sizeof(GemmSched), cudaMemcpyHostToDevice));
@@ -660,10 +683,10 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
-  cudaError_t e = launch_gemm_v(variant, ma, mb, mb, ds, K, sms, st);   // warm-up / single run
+  cudaError_t e = launch_gemm_v(variant, ma, mb, mb, mc, ds, K, sms, st);   // warm-up / single run
   if (e == cudaSuccess && reps > 1) {
     e = cudaEventRecord(e0, st);
-    for (int r = 0; r < reps && e == cudaSuccess; ++r) e = launch_gemm_v(variant, ma, mb, mb, ds, K, sms, st);
+    for (int r = 0; r < reps && e == cudaSuccess; ++r) e = launch_gemm_v(variant, ma, mb, mb, mc, ds, K, sms, st);
     if (e == cudaSuccess) e = cudaEventRecord(e1, st);
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
