@@ -40,24 +40,11 @@ METRIC_DECODE = "MoE-layer decode throughput (tokens/s)"
 POOL = 4            # distinct layer inputs cycled (each > L2: 268 MB of x at C1)
 
 
-def peaks():
-    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(p):
-        d = json.load(open(p))
-        return d, "measured"
-    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+from paper_2602_00509_b200.costs import cost_model as _cost_model, peaks, window_ns  # noqa: E402
 
 
 def cost_model(shape, pk):
-    """Integer planner constants from measured peaks (R11): α = F̄/F_peak, β = 2·2H/BW_net (λ=1),
-    n_sat = F_peak/BW_HBM (GEMM ridge in rows), BW_net = 770 GB/s measured peer copy."""
-    fpeak = pk["bf16_tflops_sustained"] * 1e12
-    fbar = 6.0 * shape.H * shape.F
-    alpha_ps = int(round(fbar / fpeak * 1e12))
-    bw_net = 770e9
-    beta_ps = int(round(2 * 2 * shape.H / bw_net * 1e12))
-    n_sat = int(round(fpeak / (pk["hbm_gbs"] * 1e9)))
-    return alpha_ps, beta_ps, n_sat, int(bw_net / 1e6)
+    return _cost_model(shape.H, shape.F, pk)
 
 
 class ClockSampler:
@@ -157,7 +144,7 @@ def run_probe(args):
     T, H = shape.T, shape.H
     out = torch.empty(GL, T, H, dtype=torch.float32, device=dev)
     # hiding window (R26): modeled per-rank expert-GEMM time at the balanced load
-    gemm_ns = int(6.0 * H * shape.F * T * shape.k / (pk["bf16_tflops_sustained"] * 1e12) * 1e9)
+    gemm_ns = window_ns(H, shape.F, T, shape.k, pk)
     win = torch.full((G,), gemm_ns, dtype=torch.int64, device=dev)
     main = torch.cuda.current_stream(dev)
 
