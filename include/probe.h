@@ -201,6 +201,18 @@ enum {
 probe_status probe_profile(probe_ctx ctx, int32_t n);
 probe_status probe_profile_read(probe_ctx ctx, float* ms, int32_t* n_out);
 
+/* Multi-process symmetric buffers (one process per GPU).  probe_ipc_export returns the
+ * CUDA IPC handle (64 bytes) of the allocation containing dev_ptr and dev_ptr's offset in
+ * it; peers call probe_ipc_import to map it (NVLink peer mapping, lazy peer access) and get
+ * the address to place in probe_init's peer table; probe_ipc_close unmaps an imported base
+ * (address returned by import minus offset).  When local_ranks < ep_size, forward /
+ * predict / prefetch insert device-side barriers on the symmetric signal pad
+ * (st.release.sys / ld.acquire.sys): after the count all-gather, after dispatch, after the
+ * expert GEMMs, after the predicted-count all-gather, and after the replica pushes. */
+probe_status probe_ipc_export(const void* dev_ptr, uint8_t handle[64], uint64_t* offset);
+probe_status probe_ipc_import(const uint8_t handle[64], uint64_t offset, uint64_t* dev_ptr);
+probe_status probe_ipc_close(uint64_t dev_ptr_base);
+
 /* Number of library kernel launches enqueued so far by this context (bench accounting). */
 int64_t probe_launch_count(probe_ctx ctx);
 

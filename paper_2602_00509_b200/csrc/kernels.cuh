@@ -726,6 +726,32 @@ __global__ void __launch_bounds__(512) k_prefetch(Dims d, const int32_t* __restr
   }
 }
 
+// =============================================================================
+// Cross-process barrier over the symmetric signal pads (one-sided NVLink stores).
+// Every local rank l stores `epoch` into slot [kind][R0+l] of EVERY rank's pad
+// (release, system scope), then waits until its own pad holds >= epoch from all
+// G ranks (acquire, system scope).  Orders all prior writes of this stream
+// (dispatch rows, count boards, Y rows, replica pushes) before peers proceed.
+// One block of GL·G threads; 30 s watchdog (trap) instead of a silent hang.
+// =============================================================================
+constexpr int kSigKinds = 8;
+__global__ void k_xbarrier(Dims d, Sym sym, int buf_sig, int kind, uint32_t epoch) {
+  const int i = threadIdx.x;
+  if (i >= d.GL * d.G) return;
+  const int l = i / d.G, r = i % d.G;
+  uint32_t* peer = reinterpret_cast<uint32_t*>(sym.at(buf_sig, d.G, r)) + kind * kMaxG + (d.R0 + l);
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(peer), "r"(epoch) : "memory");
+  const uint32_t* mine = reinterpret_cast<const uint32_t*>(sym.at(buf_sig, d.G, d.R0 + l)) + kind * kMaxG + r;
+  uint32_t v;
+  const uint64_t t0 = ptx::globaltimer_ns();
+  while (true) {
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
+    if (static_cast<int32_t>(v - epoch) >= 0) break;
+    if (ptx::globaltimer_ns() - t0 > 30000000000ull) __trap();
+  }
+}
+
 // small helper: write a host-described group list into a device schedule
 struct SmallGroups {
   int n;

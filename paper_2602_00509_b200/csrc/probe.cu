@@ -171,6 +171,8 @@ struct probe_ctx_s {
   CUtensorMap map_recv, map_act, map_rw13, map_rw2, map_y;
   std::string err;
   int64_t launches = 0;
+  uint32_t epoch[kSigKinds] = {0};   // cross-process barrier epochs (identical sequence on every process)
+  bool multi_process() const { return cfg.local_ranks != cfg.ep_size; }
   // phase profiling: prof_max forwards × (PROBE_NPHASE + 1) timing events
   int prof_max = 0, prof_n = 0;
   std::vector<cudaEvent_t> prof_ev;
@@ -264,6 +266,18 @@ GemmGroup mk_group(int a_row, int m, int b_row, int b_sel, int mode, int n, int 
 }
 
 Sym sym_of(probe_ctx ctx) { return Sym{ctx->at<const uint64_t>(ctx->sl.sym)}; }
+
+enum { BAR_COUNTS = 0, BAR_DISPATCH = 1, BAR_Y = 2, BAR_PRED = 3, BAR_PREFETCH = 4 };
+
+// Cross-process barrier (no-op when this process hosts every rank: stream order suffices).
+cudaError_t xbarrier(probe_ctx ctx, int kind, cudaStream_t st) {
+  if (!ctx->multi_process()) return cudaSuccess;
+  const uint32_t ep = ++ctx->epoch[kind];
+  const Dims& d = ctx->d;
+  k_xbarrier<<<1, ((d.GL * d.G + 31) / 32) * 32, 0, st>>>(d, sym_of(ctx), PROBE_BUF_SIGNAL, kind, ep);
+  ++ctx->launches;
+  return cudaGetLastError();
+}
 
 }  // namespace
 
@@ -426,6 +440,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   k_count_scan<<<d.GL, 256, 0, st>>>(d, nchunks, ctx->at<int32_t>(s.hist), ctx->at<int32_t>(s.cbase), sym_of(ctx),
                                      PROBE_BUF_BOARD, p);
   CKL();
+  CK(xbarrier(ctx, BAR_COUNTS, st));            // every rank's counts are on every board
   // a5 materialize plan(L) + layout
   if (use_plan) CK(cudaStreamWaitEvent(st, ctx->ev_plan[p], 0));
   MARK(2);
@@ -458,6 +473,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
     CKL();
   }
   MARK(4);
+  CK(xbarrier(ctx, BAR_DISPATCH, st));          // every peer's rows have landed in our receive buffers
   // a9 phase lock: the expert GEMMs need this layer's replica slots
   if (use_plan) CK(cudaStreamWaitEvent(st, ctx->ev_slots[p], 0));
   MARK(5);
@@ -468,6 +484,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   MARK(6);
   CK(launch_gemm_v(V_256_3_8, ctx->map_act, *m2, ctx->map_rw2, ctx->map_y, lo.s2, d.F, ctx->num_sms, st));
   ++ctx->launches;
+  CK(xbarrier(ctx, BAR_Y, st));                 // every expert rank's Y rows are complete
   MARK(7);
   // a8 combine (raises the prefetch suspend flag, R27)
   if (out_fp32)
@@ -538,6 +555,7 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
   CKL();
   k_pred_publish<<<d.GL, 256, 0, st>>>(d, ctx->at<int32_t>(s.pred_local), sym_of(ctx), PROBE_BUF_BOARD, pp);
   CKL();
+  CK(xbarrier(ctx, BAR_PRED, st));              // n̂ of every rank on every board
   if (pred_counts) {
     const int32_t* board = reinterpret_cast<const int32_t*>(ctx->local_base[PROBE_BUF_BOARD]) + ((pp * 2 + 1) * d.G) * d.E;
     CK(cudaMemcpyAsync(pred_counts, board, static_cast<size_t>(d.G) * d.E * 4, cudaMemcpyDeviceToDevice, st));
@@ -607,6 +625,7 @@ probe_status probe_prefetch(probe_ctx ctx, int32_t next_layer, const void* w13_n
                                    static_cast<const uint8_t*>(w2_next), sym_of(ctx), PROBE_BUF_REP_W13,
                                    PROBE_BUF_REP_W2, ctx->at<int32_t>(s.pfctr[pp]), flags + 1, -1, flags + 3);
   CKL();
+  CK(xbarrier(ctx, BAR_PREFETCH, st));          // every sender finished pushing into our slots
   CK(cudaEventRecord(ctx->ev_slots[pp], st));
   ctx->pf_layer[pp] = next_layer;
   return PROBE_OK;
@@ -736,6 +755,43 @@ probe_status probe_finalize(probe_ctx ctx) {
 }
 
 int64_t probe_launch_count(probe_ctx ctx) { return ctx ? ctx->launches : 0; }
+
+typedef CUresult (*PFN_getAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+probe_status probe_ipc_export(const void* dev_ptr, uint8_t handle[64], uint64_t* offset) {
+  probe_ctx ctx = nullptr;
+  if (!dev_ptr || !handle || !offset) return fail(nullptr, PROBE_EINVAL, "probe_ipc_export: null argument");
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  CK(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+  if (q != cudaDriverEntryPointSuccess || !fn) return fail(nullptr, PROBE_ECUDA, "cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (reinterpret_cast<PFN_getAddressRange>(fn)(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+    return fail(nullptr, PROBE_ECUDA, "cuMemGetAddressRange failed");
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  std::memcpy(handle, &h, 64);
+  *offset = reinterpret_cast<uint64_t>(dev_ptr) - static_cast<uint64_t>(base);
+  return PROBE_OK;
+}
+
+probe_status probe_ipc_import(const uint8_t handle[64], uint64_t offset, uint64_t* dev_ptr) {
+  probe_ctx ctx = nullptr;
+  if (!handle || !dev_ptr) return fail(nullptr, PROBE_EINVAL, "probe_ipc_import: null argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  void* p = nullptr;
+  CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  *dev_ptr = reinterpret_cast<uint64_t>(p) + offset;
+  return PROBE_OK;
+}
+
+probe_status probe_ipc_close(uint64_t dev_ptr_base) {
+  probe_ctx ctx = nullptr;
+  CK(cudaIpcCloseMemHandle(reinterpret_cast<void*>(dev_ptr_base)));
+  return PROBE_OK;
+}
 
 probe_status probe_profile(probe_ctx ctx, int32_t n) {
   if (!ctx || n < 0) return fail(ctx, PROBE_EINVAL, "probe_profile: bad arguments");
