@@ -21,7 +21,15 @@
 
 namespace probe {
 
-enum : int { EPI_F32 = 0, EPI_SWIGLU = 1, EPI_SILU_BF16 = 2, EPI_NONE = 3 /* timing experiments: no stores */ };
+enum : int {
+  EPI_F32 = 0,         // fp32 C (Y, logits)
+  EPI_SWIGLU = 1,      // act = SiLU(gate) ⊙ up → bf16
+  EPI_SILU_BF16 = 2,   // SiLU → bf16 (predictor residual activation, R8)
+  EPI_NONE = 3,        // timing experiments: no stores
+  EPI_TOPK = 4,        // router: per-row top-k (logit ↓, id ↑) + softmax over the k → ids, weights (a1)
+  EPI_TOPK_COUNT = 5   // predictor: per-row top-k → atomic per-(rank, expert) counts n̂ (a2, R9)
+};
+constexpr int kTopkMax = 8;   // fused top-k supports k <= 8 (larger k uses the unfused kernel)
 
 struct GemmGroup {
   int32_t a_row;       // first row in the A tensor map
@@ -34,7 +42,11 @@ struct GemmGroup {
   int32_t tile_start;  // prefix of tiles over groups
   int32_t out_row;     // row of this group's row 0 in the output tensor map (TMA store path)
   int32_t tma_out;     // 1: fp32 output through the tmC tensor map (full 32-row slabs)
-  void* out;           // output of row 0 / col 0 of this group
+  int32_t topk;        // EPI_TOPK*: k
+  int32_t rows_per_rank;  // EPI_TOPK_COUNT: tokens per rank (rank = (a_row + row) / rows_per_rank)
+  void* out;           // output of row 0 / col 0 of this group (EPI_TOPK: int32 ids [m, k])
+  void* aux;           // EPI_TOPK: fp32 weights [m, k]; EPI_TOPK_COUNT: int32 counts [ranks, n]
+  const float* bias;   // EPI_TOPK*: optional fp32 bias [n]
 };
 
 constexpr int kMaxGroups = 1024;
@@ -172,7 +184,7 @@ template <int BN, int STAGES, int EW = 4>
 __global__ void __launch_bounds__(128 + 32 * EW, 1)
 grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
                     const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmC,
-                    const GemmSched* __restrict__ sched, int K) {
+                    const __grid_constant__ CUtensorMap tmA2, const GemmSched* __restrict__ sched, int K, int K2) {
   using L = GemmSmem<BN, STAGES, EW>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -204,12 +216,16 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     ptx::tma_prefetch_desc(&tmA);
     ptx::tma_prefetch_desc(&tmB0);
     ptx::tma_prefetch_desc(&tmB1);
+    if (K2 > 0) ptx::tma_prefetch_desc(&tmA2);
   }
   if (warp == 2) ptx::tmem_alloc<2 * BN>(tmem_slot);
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int num_kb = (K + 63) / 64;
+  // K concatenation (predictor: [x | a]·[W_next | Ŵ2]ᵀ): k-blocks [0, kb1) read (tmA, selected B),
+  // k-blocks [kb1, num_kb) read (tmA2, tmB1) — both halves accumulate into one TMEM tile.
+  const int kb1 = (K + 63) / 64;
+  const int num_kb = kb1 + (K2 > 0 ? (K2 + 63) / 64 : 0);
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -231,13 +247,16 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           brow0 = G.b_row + nb * BN;
           brow1 = brow0 + BN / 2;
         }
-        const CUtensorMap* tb = G.b_sel ? &tmB1 : &tmB0;
         for (int kb = 0; kb < num_kb; ++kb) {
+          const bool second = kb >= kb1;
+          const CUtensorMap* ta = second ? &tmA2 : &tmA;
+          const CUtensorMap* tb = (second || G.b_sel) ? &tmB1 : &tmB0;
+          const int kc = (second ? kb - kb1 : kb) * 64;
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           ptx::mbar_arrive_expect_tx(&full[stage], L::A_BYTES + L::B_BYTES);
-          ptx::tma_load_2d(&tmA, &full[stage], sA + stage * L::A_BYTES, kb * 64, arow);
-          ptx::tma_load_2d(tb, &full[stage], sB + stage * L::B_BYTES, kb * 64, brow0);
-          ptx::tma_load_2d(tb, &full[stage], sB + stage * L::B_BYTES + (BN / 2) * 128, kb * 64, brow1);
+          ptx::tma_load_2d(ta, &full[stage], sA + stage * L::A_BYTES, kc, arow);
+          ptx::tma_load_2d(tb, &full[stage], sB + stage * L::B_BYTES, kc, brow0);
+          ptx::tma_load_2d(tb, &full[stage], sB + stage * L::B_BYTES + (BN / 2) * 128, kc, brow1);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -291,7 +310,58 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       ptx::tc_fence_after();
       const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
       const int row0 = mb * 128 + q * 32;          // first tile row of this warp
-      if (G.mode == EPI_SWIGLU) {
+      if (G.mode == EPI_TOPK || G.mode == EPI_TOPK_COUNT) {
+        // row = token (lane); insertion into a register list sorted by (value ↓, id ↑):
+        // columns arrive in ascending expert id, so an equal value never displaces (R3, R4)
+        float tv[kTopkMax];
+        int te[kTopkMax];
+#pragma unroll
+        for (int j = 0; j < kTopkMax; ++j) { tv[j] = -INFINITY; te[j] = 0x7fffffff; }
+        const int kk = G.topk;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          if (c * 32 >= G.n) break;
+          uint32_t v32[32];
+          ptx::tmem_ld32(tb + c * 32, v32);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            int e = c * 32 + i;
+            float x = (e < G.n) ? __uint_as_float(v32[i]) + (G.bias ? __ldg(G.bias + e) : 0.f) : -INFINITY;
+#pragma unroll
+            for (int j = 0; j < kTopkMax; ++j) {
+              if (j < kk && x > tv[j]) {
+                const float ov = tv[j];
+                const int oe = te[j];
+                tv[j] = x; te[j] = e;
+                x = ov; e = oe;
+              }
+            }
+          }
+        }
+        const int row = row0 + lane;
+        if (row < G.m) {
+          if (G.mode == EPI_TOPK) {
+            float w[kTopkMax], sum = 0.f;
+#pragma unroll
+            for (int j = 0; j < kTopkMax; ++j) {
+              w[j] = j < kk ? expf(tv[j] - tv[0]) : 0.f;
+              sum += w[j];
+            }
+            int32_t* ids = reinterpret_cast<int32_t*>(G.out) + static_cast<size_t>(row) * kk;
+            float* gw = reinterpret_cast<float*>(G.aux) + static_cast<size_t>(row) * kk;
+#pragma unroll
+            for (int j = 0; j < kTopkMax; ++j)
+              if (j < kk) { ids[j] = te[j]; gw[j] = w[j] / sum; }
+          } else {
+            int32_t* cnt = reinterpret_cast<int32_t*>(G.aux) +
+                           static_cast<size_t>((G.a_row + row) / G.rows_per_rank) * G.n;
+#pragma unroll
+            for (int j = 0; j < kTopkMax; ++j)
+              if (j < kk) atomicAdd(cnt + te[j], 1);
+          }
+        }
+      } else if (G.mode == EPI_SWIGLU) {
 #pragma unroll 1
         for (int c = part; c < BN / 64; c += NPART) {
           uint32_t gv[32], uv[32];

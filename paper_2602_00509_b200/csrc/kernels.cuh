@@ -148,6 +148,44 @@ __global__ void __launch_bounds__(128) k_topk(Dims d, int T, const float* __rest
 }
 
 // =============================================================================
+// a5/a6 helper after the fused gate: per 128-token chunk, expert bitmasks built
+// from the routing ids (order-independent atomicOr) → per-chunk histograms and
+// the rank of every (token, slot) among the chunk's tokens of its expert (token
+// order), i.e. deterministic dispatch positions (R23/R24).
+// grid (ceil(T/128), GL), block 128 (thread = token).
+// =============================================================================
+__global__ void __launch_bounds__(128) k_rank(Dims d, int T, const int32_t* __restrict__ ids,
+                                              int32_t* __restrict__ pos, int32_t* __restrict__ hist) {
+  __shared__ uint32_t mask[kMaxE * 4];
+  const int E = d.E, k = d.k;
+  const int chunk = blockIdx.x, gl = blockIdx.y, nchunks = gridDim.x;
+  const int tl = threadIdx.x, t = chunk * kChunk + tl;
+  for (int i = tl; i < E * 4; i += blockDim.x) mask[i] = 0u;
+  __syncthreads();
+  const size_t base = (static_cast<size_t>(gl) * T + t) * k;
+  int e_loc[kMaxK];
+  if (t < T)
+    for (int j = 0; j < k; ++j) {
+      e_loc[j] = ids[base + j];
+      atomicOr(&mask[e_loc[j] * 4 + (tl >> 5)], 1u << (tl & 31));
+    }
+  __syncthreads();
+  for (int e = tl; e < E; e += blockDim.x) {
+    const uint32_t* m = &mask[e * 4];
+    hist[(static_cast<size_t>(gl) * nchunks + chunk) * E + e] = __popc(m[0]) + __popc(m[1]) + __popc(m[2]) + __popc(m[3]);
+  }
+  if (t < T) {
+    const int w = tl >> 5, b = tl & 31;
+    for (int j = 0; j < k; ++j) {
+      const uint32_t* m = &mask[e_loc[j] * 4];
+      int p = __popc(m[w] & ((1u << b) - 1u));
+      for (int ww = 0; ww < w; ++ww) p += __popc(m[ww]);
+      pos[base + j] = p;
+    }
+  }
+}
+
+// =============================================================================
 // a3: per-(rank, expert) exclusive scan over chunks → chunk bases and actual
 // counts n[r][e]; all-gather the counts into every rank's board (M2).
 // grid GL, block 256.
@@ -514,10 +552,12 @@ __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o
     GemmGroup g1;
     g1.a_row = arow; g1.m = m; g1.b_row = wslot * 2 * d.F; g1.b_sel = is_rep; g1.mode = EPI_SWIGLU;
     g1.n = d.F; g1.ldc = d.F; g1.tile_start = 0; g1.out_row = arow; g1.tma_out = 0;
+    g1.topk = 0; g1.rows_per_rank = 1; g1.aux = nullptr; g1.bias = nullptr;
     g1.out = reinterpret_cast<__nv_bfloat16*>(in.act) + static_cast<size_t>(arow) * d.F;
     GemmGroup g2;
     g2.a_row = arow; g2.m = m; g2.b_row = wslot * d.H; g2.b_sel = is_rep; g2.mode = EPI_F32;
     g2.n = d.H; g2.ldc = d.H; g2.tile_start = 0; g2.out_row = arow; g2.tma_out = (d.H % 32 == 0);
+    g2.topk = 0; g2.rows_per_rank = 1; g2.aux = nullptr; g2.bias = nullptr;
     g2.out = reinterpret_cast<float*>(in.y_local) + static_cast<size_t>(arow) * d.H;
     o.s1->g[i] = g1;
     o.s2->g[i] = g2;
@@ -756,7 +796,7 @@ __global__ void k_xbarrier(Dims d, Sym sym, int buf_sig, int kind, uint32_t epoc
 struct SmallGroups {
   int n;
   int BN;
-  GemmGroup g[4];
+  GemmGroup g[2];
 };
 __global__ void k_write_sched(GemmSched* s, SmallGroups sg) {
   if (threadIdx.x == 0) {

@@ -217,7 +217,7 @@ enum GemmVariant { V_128_6_4 = 0, V_256_4_4 = 1, V_256_3_8 = 2, V_128_4_8 = 3 };
 
 template <int BN, int ST, int EW>
 cudaError_t launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, const CUtensorMap& c,
-                          const GemmSched* s, int K, int grid, cudaStream_t st) {
+                          const CUtensorMap& a2, const GemmSched* s, int K, int K2, int grid, cudaStream_t st) {
   using L = GemmSmem<BN, ST, EW>;
   static bool attr = false;
   if (!attr) {
@@ -226,17 +226,19 @@ cudaError_t launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b0, const CUt
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  grouped_gemm_kernel<BN, ST, EW><<<grid, 128 + 32 * EW, L::BYTES, st>>>(a, b0, b1, c, s, K);
+  grouped_gemm_kernel<BN, ST, EW><<<grid, 128 + 32 * EW, L::BYTES, st>>>(a, b0, b1, c, a2, s, K, K2);
   return cudaGetLastError();
 }
 
 cudaError_t launch_gemm_v(int v, const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1,
-                          const CUtensorMap& c, const GemmSched* s, int K, int grid, cudaStream_t st) {
+                          const CUtensorMap& c, const GemmSched* s, int K, int grid, cudaStream_t st,
+                          const CUtensorMap* a2 = nullptr, int K2 = 0) {
+  const CUtensorMap& A2 = a2 ? *a2 : a;
   switch (v) {
-    case V_128_6_4: return launch_gemm_t<128, 6, 4>(a, b0, b1, c, s, K, grid, st);
-    case V_256_4_4: return launch_gemm_t<256, 4, 4>(a, b0, b1, c, s, K, grid, st);
-    case V_256_3_8: return launch_gemm_t<256, 3, 8>(a, b0, b1, c, s, K, grid, st);
-    case V_128_4_8: return launch_gemm_t<128, 4, 8>(a, b0, b1, c, s, K, grid, st);
+    case V_128_6_4: return launch_gemm_t<128, 6, 4>(a, b0, b1, c, A2, s, K, K2, grid, st);
+    case V_256_4_4: return launch_gemm_t<256, 4, 4>(a, b0, b1, c, A2, s, K, K2, grid, st);
+    case V_256_3_8: return launch_gemm_t<256, 3, 8>(a, b0, b1, c, A2, s, K, K2, grid, st);
+    case V_128_4_8: return launch_gemm_t<128, 4, 8>(a, b0, b1, c, A2, s, K, K2, grid, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -261,7 +263,8 @@ void launch_topk(const Dims& d, int T, int nchunks, cudaStream_t st, const float
 GemmGroup mk_group(int a_row, int m, int b_row, int b_sel, int mode, int n, int ldc, void* out) {
   GemmGroup g;
   g.a_row = a_row; g.m = m; g.b_row = b_row; g.b_sel = b_sel; g.mode = mode; g.n = n; g.ldc = ldc;
-  g.tile_start = 0; g.out_row = 0; g.tma_out = 0; g.out = out;
+  g.tile_start = 0; g.out_row = 0; g.tma_out = 0; g.topk = 0; g.rows_per_rank = 1; g.out = out;
+  g.aux = nullptr; g.bias = nullptr;
   return g;
 }
 
@@ -411,10 +414,9 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   const uint64_t GL = d.GL, H = d.H, F = d.F, E = d.E;
   const int nchunks = (T + kChunk - 1) / kChunk;
   const CUtensorMap* mx = ctx->maps.get(x, GL * T, H, 128);
-  const CUtensorMap* mr = ctx->maps.get(w_router, E, H, 64);
   const CUtensorMap* m13 = ctx->maps.get(w13, GL * d.EL * 2 * F, H, 128);
   const CUtensorMap* m2 = ctx->maps.get(w2, GL * d.EL * H, F, 128);
-  if (!mx || !mr || !m13 || !m2) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
+  if (!mx || !m13 || !m2) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
   const Scratch& s = ctx->sl;
   int32_t* err = ctx->at<int32_t>(s.flags);
   int32_t* suspend = err + 1;
@@ -422,17 +424,35 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
 #define MARK(ph) \
   if (prof) CK(cudaEventRecord(ctx->pev(ph), st))
   MARK(0);
-  // a1 gate: logits = x W_rᵀ (tcgen05), top-k + softmax + per-chunk ranks
+  // a1 gate: logits = x W_rᵀ on tcgen05 with the top-k + softmax fused in the epilogue
+  // (fp32 logits never leave TMEM/registers); then per-chunk dispatch ranks.
+  const bool fused_gate = d.k <= kTopkMax && d.E <= 256;
   SmallGroups sg{};
   sg.n = 1;
-  sg.BN = 128;
-  sg.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_F32, d.E, d.E, ctx->at<float>(s.logits));
+  sg.BN = d.E <= 128 ? 128 : 256;
+  if (fused_gate) {
+    sg.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_TOPK, d.E, d.E, ctx->at<int32_t>(s.ids));
+    sg.g[0].topk = d.k;
+    sg.g[0].aux = ctx->at<float>(s.gw);
+    sg.g[0].bias = b_router;
+  } else {
+    sg.BN = 128;
+    sg.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_F32, d.E, d.E, ctx->at<float>(s.logits));
+  }
+  const CUtensorMap* mr = ctx->maps.get(w_router, E, H, sg.BN / 2);
+  if (!mr) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
   k_write_sched<<<1, 32, 0, st>>>(ctx->at<GemmSched>(s.s_gate), sg);
   CKL();
-  CK(launch_gemm<128>(*mx, *mr, *mr, ctx->at<GemmSched>(s.s_gate), d.H, ctx->num_sms, st));
+  CK(launch_gemm_v(sg.BN == 128 ? V_128_6_4 : V_256_4_4, *mx, *mr, *mr, *mx, ctx->at<GemmSched>(s.s_gate), d.H,
+                   ctx->num_sms, st));
   ++ctx->launches;
-  launch_topk<false>(d, T, nchunks, st, ctx->at<float>(s.logits), nullptr, b_router, ctx->at<int32_t>(s.ids),
-                     ctx->at<float>(s.gw), ctx->at<int32_t>(s.pos), ctx->at<int32_t>(s.hist), nullptr, nullptr);
+  if (fused_gate) {
+    k_rank<<<dim3(nchunks, d.GL), 128, 0, st>>>(d, T, ctx->at<int32_t>(s.ids), ctx->at<int32_t>(s.pos),
+                                                ctx->at<int32_t>(s.hist));
+  } else {
+    launch_topk<false>(d, T, nchunks, st, ctx->at<float>(s.logits), nullptr, b_router, ctx->at<int32_t>(s.ids),
+                       ctx->at<float>(s.gw), ctx->at<int32_t>(s.pos), ctx->at<int32_t>(s.hist), nullptr, nullptr);
+  }
   CKL();
   CK(cudaEventRecord(ctx->ev_gate[p], st));
   MARK(1);
@@ -479,7 +499,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   MARK(5);
   CK(cudaEventRecord(ctx->ev_gemm[p], st));
   // a7 grouped SwiGLU expert FFN (tcgen05): act = SiLU(X W_gᵀ) ⊙ X W_uᵀ ; Y = act W_dᵀ
-  CK(launch_gemm<256>(ctx->map_recv, *m13, ctx->map_rw13, lo.s1, d.H, ctx->num_sms, st));
+  CK(launch_gemm_v(V_256_4_4, ctx->map_recv, *m13, ctx->map_rw13, ctx->map_recv, lo.s1, d.H, ctx->num_sms, st));
   ++ctx->launches;
   MARK(6);
   CK(launch_gemm_v(V_256_3_8, ctx->map_act, *m2, ctx->map_rw2, ctx->map_y, lo.s2, d.F, ctx->num_sms, st));
@@ -523,36 +543,77 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
   const uint64_t GL = d.GL, H = d.H, E = d.E, h = d.h;
   const Scratch& s = ctx->sl;
   const CUtensorMap* mx = ctx->maps.get(x, GL * T, H, 128);
-  const CUtensorMap* mw = ctx->maps.get(w_router_next, E, H, 64);
-  const CUtensorMap* m1 = w_res1 ? ctx->maps.get(w_res1, h, H, 64) : mw;
-  if (!mx || !mw || !m1) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
-  SmallGroups sg{};
-  sg.BN = 128;
-  sg.n = w_res1 ? 2 : 1;
-  sg.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_F32, d.E, d.E, ctx->at<float>(s.pprior));
-  if (w_res1) sg.g[1] = mk_group(0, static_cast<int>(GL * T), 0, 1, EPI_SILU_BF16, d.h, d.h, ctx->scratch + s.pact);
-  k_write_sched<<<1, 32, 0, st>>>(ctx->at<GemmSched>(s.s_p1), sg);
-  CKL();
-  CK(launch_gemm<128>(*mx, *mw, *m1, ctx->at<GemmSched>(s.s_p1), d.H, ctx->num_sms, st));
-  ++ctx->launches;
-  if (w_res1) {
-    const CUtensorMap* ma = ctx->maps.get(ctx->scratch + s.pact, GL * T, h, 128);
-    const CUtensorMap* m2 = ctx->maps.get(w_res2, E, h, 64);
-    if (!ma || !m2) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
+  if (!mx) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
+  const int nchunks = (T + kChunk - 1) / kChunk;
+  CK(cudaMemsetAsync(ctx->at<int32_t>(s.pred_local), 0, GL * E * 4, st));
+  const bool fused = !pred_logits && d.k <= kTopkMax && d.E <= 256;
+  if (fused) {
+    // (1) a = bf16(SiLU(Ŵ1 x))  [GL·T, h]   (2) l̂ = [x | a]·[W_{L+1} | Ŵ2]ᵀ (+b) with the
+    // top-k and the per-rank count n̂ fused in the epilogue (one TMEM accumulator for prior
+    // + residual; Eq. (P), R8, R9).
+    const int BN = d.E <= 128 ? 128 : 256;
+    const CUtensorMap* mw = ctx->maps.get(w_router_next, E, H, BN / 2);
+    const CUtensorMap* ma = nullptr;
+    const CUtensorMap* m2 = nullptr;
+    if (w_res1) {
+      const CUtensorMap* m1 = ctx->maps.get(w_res1, h, H, 64);
+      ma = ctx->maps.get(ctx->scratch + s.pact, GL * T, h, 128);
+      m2 = ctx->maps.get(w_res2, E, h, BN / 2);
+      if (!m1 || !ma || !m2) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
+      SmallGroups s1{};
+      s1.BN = 128;
+      s1.n = 1;
+      s1.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_SILU_BF16, d.h, d.h, ctx->scratch + s.pact);
+      k_write_sched<<<1, 32, 0, st>>>(ctx->at<GemmSched>(s.s_p1), s1);
+      CKL();
+      CK(launch_gemm_v(V_128_6_4, *mx, *m1, *m1, *mx, ctx->at<GemmSched>(s.s_p1), d.H, ctx->num_sms, st));
+      ++ctx->launches;
+    }
+    if (!mw) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
     SmallGroups s2{};
-    s2.BN = 128;
+    s2.BN = BN;
     s2.n = 1;
-    s2.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_F32, d.E, d.E, ctx->at<float>(s.pres));
+    s2.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_TOPK_COUNT, d.E, d.E, nullptr);
+    s2.g[0].topk = d.k;
+    s2.g[0].rows_per_rank = T;
+    s2.g[0].aux = ctx->at<int32_t>(s.pred_local);
+    s2.g[0].bias = b_router_next;
     k_write_sched<<<1, 32, 0, st>>>(ctx->at<GemmSched>(s.s_p2), s2);
     CKL();
-    CK(launch_gemm<128>(*ma, *m2, *m2, ctx->at<GemmSched>(s.s_p2), d.h, ctx->num_sms, st));
+    CK(launch_gemm_v(BN == 128 ? V_128_6_4 : V_256_4_4, *mx, *mw, w_res1 ? *m2 : *mw, *mx, ctx->at<GemmSched>(s.s_p2),
+                     d.H, ctx->num_sms, st, w_res1 ? ma : nullptr, w_res1 ? d.h : 0));
     ++ctx->launches;
+  } else {
+    // unfused (debug / k > 8): prior + SiLU activation, residual GEMM, warp top-k; writes logits
+    const CUtensorMap* mw = ctx->maps.get(w_router_next, E, H, 64);
+    const CUtensorMap* m1 = w_res1 ? ctx->maps.get(w_res1, h, H, 64) : mw;
+    if (!mw || !m1) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
+    SmallGroups sg{};
+    sg.BN = 128;
+    sg.n = w_res1 ? 2 : 1;
+    sg.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_F32, d.E, d.E, ctx->at<float>(s.pprior));
+    if (w_res1) sg.g[1] = mk_group(0, static_cast<int>(GL * T), 0, 1, EPI_SILU_BF16, d.h, d.h, ctx->scratch + s.pact);
+    k_write_sched<<<1, 32, 0, st>>>(ctx->at<GemmSched>(s.s_p1), sg);
+    CKL();
+    CK(launch_gemm_v(V_128_6_4, *mx, *mw, *m1, *mx, ctx->at<GemmSched>(s.s_p1), d.H, ctx->num_sms, st));
+    ++ctx->launches;
+    if (w_res1) {
+      const CUtensorMap* ma = ctx->maps.get(ctx->scratch + s.pact, GL * T, h, 128);
+      const CUtensorMap* m2 = ctx->maps.get(w_res2, E, h, 64);
+      if (!ma || !m2) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
+      SmallGroups s2{};
+      s2.BN = 128;
+      s2.n = 1;
+      s2.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_F32, d.E, d.E, ctx->at<float>(s.pres));
+      k_write_sched<<<1, 32, 0, st>>>(ctx->at<GemmSched>(s.s_p2), s2);
+      CKL();
+      CK(launch_gemm_v(V_128_6_4, *ma, *m2, *m2, *ma, ctx->at<GemmSched>(s.s_p2), d.h, ctx->num_sms, st));
+      ++ctx->launches;
+    }
+    launch_topk<true>(d, T, nchunks, st, ctx->at<float>(s.pprior), w_res1 ? ctx->at<float>(s.pres) : nullptr,
+                      b_router_next, nullptr, nullptr, nullptr, nullptr, ctx->at<int32_t>(s.pred_local), pred_logits);
+    CKL();
   }
-  CK(cudaMemsetAsync(ctx->at<int32_t>(s.pred_local), 0, GL * E * 4, st));
-  const int nchunks = (T + kChunk - 1) / kChunk;
-  launch_topk<true>(d, T, nchunks, st, ctx->at<float>(s.pprior), w_res1 ? ctx->at<float>(s.pres) : nullptr,
-                    b_router_next, nullptr, nullptr, nullptr, nullptr, ctx->at<int32_t>(s.pred_local), pred_logits);
-  CKL();
   k_pred_publish<<<d.GL, 256, 0, st>>>(d, ctx->at<int32_t>(s.pred_local), sym_of(ctx), PROBE_BUF_BOARD, pp);
   CKL();
   CK(xbarrier(ctx, BAR_PRED, st));              // n̂ of every rank on every board

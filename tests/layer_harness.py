@@ -87,7 +87,9 @@ def run_gpu(case: CaseCfg):
     res = {}
     rt.forward(0, L0.x, W[0], b[0], w13[0], w2[0], out[0], use_plan=False, topk_ids=ids[0], topk_w=gw[0])
     lay0 = debug(rt, cfg)
-    rt.predict(1, L0.x, W[1], b[1], r1, r2, pred_counts=pc, pred_logits=plog)
+    pc_unfused = torch.empty(G, E, dtype=torch.int32, device=dev)
+    rt.predict(1, L0.x, W[1], b[1], r1, r2, pred_counts=pc_unfused, pred_logits=plog)   # unfused (logits out)
+    rt.predict(1, L0.x, W[1], b[1], r1, r2, pred_counts=pc)                              # fused top-k epilogue
     rt.plan(1, win, replicas=reps, quota=quota, stats=stats)
     rt.prefetch(1, w13[1], w2[1], phase=0)
     rt.forward(1, L1.x, W[1], b[1], w13[1], w2[1], out[1], use_plan=True, topk_ids=ids[1], topk_w=gw[1])
@@ -96,6 +98,7 @@ def run_gpu(case: CaseCfg):
     torch.cuda.synchronize()
     res.update(out=[o.float().cpu().numpy() for o in out], ids=[i.cpu().numpy() for i in ids],
                g=[g.cpu().numpy() for g in gw], pred_counts=pc.cpu().numpy(), pred_logits=plog.cpu().numpy(),
+               pred_counts_unfused=pc_unfused.cpu().numpy(),
                replicas=reps.cpu().numpy(), quota=quota.cpu().numpy(), stats=stats.cpu().numpy(),
                layout=[lay0, lay1])
     # replica slots (bank 1 for layer 1) must hold the home expert's weights bit-exactly
@@ -203,7 +206,8 @@ def compare(case: CaseCfg, gpu, orc, tol: float = 2e-2):
             errs.append(np.abs(got - ref["out"][r]).max())
         report[f"out_err_L{L}"] = float(max(errs) / rms)
         assert max(errs) <= tol * rms, f"output L{L}: max err {max(errs)} > {tol} * RMS {rms}"
-    assert np.array_equal(gpu["pred_counts"], orc["nhat"]), "predicted counts"
+    assert np.array_equal(gpu["pred_counts"], orc["nhat"]), "predicted counts (fused epilogue)"
+    assert np.array_equal(gpu["pred_counts_unfused"], orc["nhat"]), "predicted counts (unfused)"
     pl = orc["pred_logits"]
     report["pred_logit_err"] = float(np.abs(gpu["pred_logits"] - pl).max())
     assert report["pred_logit_err"] <= 1e-5 * max(1.0, np.abs(pl).max()), "predictor logits"
