@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -173,6 +174,7 @@ struct probe_ctx_s {
   int64_t launches = 0;
   uint32_t epoch[kSigKinds] = {0};   // cross-process barrier epochs (identical sequence on every process)
   bool multi_process() const { return cfg.local_ranks != cfg.ep_size; }
+  bool unfused = false;   // PROBE_UNFUSED=1: logits written + separate top-k kernels (debug)
   // phase profiling: prof_max forwards × (PROBE_NPHASE + 1) timing events
   int prof_max = 0, prof_n = 0;
   std::vector<cudaEvent_t> prof_ev;
@@ -333,6 +335,10 @@ probe_status probe_init(const probe_config* cfg, const uint64_t* peer_ptrs, void
   ctx->d = Dims{c.ep_size, c.rank_begin, c.local_ranks, c.num_experts, c.num_experts / c.ep_size, c.top_k,
                 c.hidden, c.ffn, c.res_hidden, c.max_tokens, c.recv_capacity, c.replica_budget};
   ctx->sl = scratch_layout(c);
+  {
+    const char* u = getenv("PROBE_UNFUSED");
+    ctx->unfused = u && u[0] == '1';
+  }
   ctx->scratch = static_cast<uint8_t*>(scratch);
   sym_sizes(c, ctx->sym_bytes);
   const int G = c.ep_size;
@@ -426,7 +432,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   MARK(0);
   // a1 gate: logits = x W_rᵀ on tcgen05 with the top-k + softmax fused in the epilogue
   // (fp32 logits never leave TMEM/registers); then per-chunk dispatch ranks.
-  const bool fused_gate = d.k <= kTopkMax && d.E <= 256;
+  const bool fused_gate = d.k <= kTopkMax && d.E <= 256 && !ctx->unfused;
   SmallGroups sg{};
   sg.n = 1;
   sg.BN = d.E <= 128 ? 128 : 256;
@@ -546,7 +552,7 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
   if (!mx) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
   const int nchunks = (T + kChunk - 1) / kChunk;
   CK(cudaMemsetAsync(ctx->at<int32_t>(s.pred_local), 0, GL * E * 4, st));
-  const bool fused = !pred_logits && d.k <= kTopkMax && d.E <= 256;
+  const bool fused = !pred_logits && d.k <= kTopkMax && d.E <= 256 && !ctx->unfused;
   if (fused) {
     // (1) a = bf16(SiLU(Ŵ1 x))  [GL·T, h]   (2) l̂ = [x | a]·[W_{L+1} | Ŵ2]ᵀ (+b) with the
     // top-k and the per-rank count n̂ fused in the epilogue (one TMEM accumulator for prior
