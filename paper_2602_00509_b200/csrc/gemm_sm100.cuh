@@ -311,8 +311,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
       const int row0 = mb * 128 + q * 32;          // first tile row of this warp
       if (G.mode == EPI_TOPK || G.mode == EPI_TOPK_COUNT) {
-        // row = token (lane); insertion into a register list sorted by (value ↓, id ↑):
-        // columns arrive in ascending expert id, so an equal value never displaces (R3, R4)
+        // row = token (lane); insertion into a register list sorted by (value ↓, id ↑) (R3, R4)
         float tv[kTopkMax];
         int te[kTopkMax];
 #pragma unroll
@@ -330,7 +329,9 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             float x = (e < G.n) ? __uint_as_float(v32[i]) + (G.bias ? __ldg(G.bias + e) : 0.f) : -INFINITY;
 #pragma unroll
             for (int j = 0; j < kTopkMax; ++j) {
-              if (j < kk && x > tv[j]) {
+              // full order (value ↓, id ↑): a displaced (carried) element may tie with a
+              // later-id entry and must then win
+              if (j < kk && (x > tv[j] || (x == tv[j] && e < te[j]))) {
                 const float ov = tv[j];
                 const int oe = te[j];
                 tv[j] = x; te[j] = e;
