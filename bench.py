@@ -226,6 +226,28 @@ def run_probe(args):
         step(L, use_plan=False)
         L += 1
     ms_static, L = timed(args.steps, L, use_plan=False)
+    # ---- single-GPU EP straggler emulation: expert GEMMs partitioned by logical rank
+    #      (~#SMs/G SMs per rank ⇒ GEMM time = the straggler's, Eq. 3); static EP vs PROBE
+    ep_em = None
+    if world == 1 and GL > 1 and not args.no_emulation:
+        from paper_2602_00509_b200._lib import OPT_EP_EMULATION
+        rt.set_option(OPT_EP_EMULATION, 1)
+        for _ in range(2):
+            step(L, use_plan=False)
+            L += 1
+        ms_em_static, L = timed(args.steps, L, use_plan=False)
+        step(L, fwd_plan=False)
+        L += 1
+        step(L)
+        L += 1
+        ms_em_probe, L = timed(args.steps, L)
+        rt.set_option(OPT_EP_EMULATION, 0)
+        ep_em = {"static_ep_ms": ms_em_static, "probe_ms": ms_em_probe,
+                 "speedup_probe_vs_static": ms_em_static / ms_em_probe,
+                 "note": "expert GEMMs split into G CTA sets (one per logical rank, ~148/G SMs each); "
+                         "gate/dispatch/combine unpartitioned"}
+        step(L, fwd_plan=False)
+        L += 1
     # ---- end-to-end through the API with host buffers (pinned), copies inside the timed region
     e2e = None
     if not args.no_e2e:
@@ -286,6 +308,7 @@ def run_probe(args):
             "clocks": clocks,
             "phases_ms": phases,
             "static_ep": {"ms_per_step": ms_static, "speedup_probe_vs_static": ms_static / ms},
+            "ep_emulation": ep_em,
             "balance": {"ir_pre": ir_pre, "ir_post": ir_post, "replicas": nrep},
             "setup_s": gen_s,
         }
@@ -395,6 +418,7 @@ def main():
     ap.add_argument("--zipf", type=float, default=1.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-emulation", action="store_true")
     ap.add_argument("--cpu-tokens", type=int, default=256)
     ap.add_argument("--ref-tokens", type=int, default=16)
     args = ap.parse_args()

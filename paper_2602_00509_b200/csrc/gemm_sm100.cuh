@@ -50,12 +50,36 @@ struct GemmGroup {
 };
 
 constexpr int kMaxGroups = 1024;
+constexpr int kMaxParts = 64;
 
 struct GemmSched {
   int32_t num_groups;
   int32_t total_tiles;
-  int32_t pad[2];
+  int32_t nparts;                    // >1: CTA b serves only partition b % nparts (EP emulation)
+  int32_t pad;
+  int32_t part_tile[kMaxParts + 1];  // tile range [part_tile[p], part_tile[p+1]) of partition p
   GemmGroup g[kMaxGroups];
+};
+
+// Persistent tile iterator.  Default: all CTAs stride over all tiles.  Partitioned
+// (single-GPU EP emulation): the grid is split into `nparts` CTA sets (b % nparts),
+// each set striding only over its logical rank's tiles, so a rank's expert GEMM runs on
+// ~#SMs/nparts SMs and the launch time is the max over ranks (the straggler, Eq. 3).
+struct TileIter {
+  int cur, end, step;
+  __device__ TileIter(const GemmSched* s) {
+    const int np = s->nparts;
+    if (np > 1) {
+      const int p = blockIdx.x % np, j = blockIdx.x / np;
+      step = (static_cast<int>(gridDim.x) - p + np - 1) / np;
+      cur = s->part_tile[p] + j;
+      end = s->part_tile[p + 1];
+    } else {
+      cur = blockIdx.x;
+      end = s->total_tiles;
+      step = gridDim.x;
+    }
+  }
 };
 
 __host__ __device__ inline int gemm_ntiles_n(const GemmGroup& G, int BN) {
@@ -68,6 +92,7 @@ __host__ __device__ inline int gemm_ntiles(const GemmGroup& G, int BN) {
 
 // Serial prefix over the group table (called by one thread).
 __device__ inline void gemm_finalize_sched(GemmSched* s, int BN) {
+  s->nparts = 0;
   int acc = 0;
   for (int i = 0; i < s->num_groups; ++i) {
     s->g[i].tile_start = acc;
@@ -200,7 +225,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int ng = sched->num_groups;
-  const int total = sched->total_tiles;
+  const TileIter it0(sched);
   for (int i = threadIdx.x; i < ng; i += blockDim.x) ts[i] = sched->g[i].tile_start;
 
   if (warp == 0 && lane == 0) {
@@ -232,7 +257,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      for (int tile = it0.cur; tile < it0.end; tile += it0.step) {
         const int gi = gemm_find_group(ts, ng, tile);
         const GemmGroup& G = sched->g[gi];
         const int nt = gemm_ntiles_n(G, BN);
@@ -268,7 +293,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     uint32_t phase = 0;
     int acc = 0;
     uint32_t aphase = 0;
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    for (int tile = it0.cur; tile < it0.end; tile += it0.step) {
       ptx::mbar_wait(&tempty[acc], aphase ^ 1);
       ptx::tc_fence_after();
       const uint32_t d = tmem_base + acc * BN;
@@ -300,7 +325,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     int tsel = 0;
     int acc = 0;
     uint32_t aphase = 0;
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    for (int tile = it0.cur; tile < it0.end; tile += it0.step) {
       const int gi = gemm_find_group(ts, ng, tile);
       const GemmGroup G = sched->g[gi];
       const int nt = gemm_ntiles_n(G, BN);

@@ -439,6 +439,7 @@ struct LayoutOut {
   int32_t* err;
 };
 struct LayoutIn {
+  int nparts;                   // >1: partition the expert GEMMs by local rank (EP emulation)
   const int32_t* board_actual;  // [G][E]
   const int32_t* quota;         // [G][E][G] or null (static EP)
   const int32_t* replicas;      // [G][3] or null
@@ -583,7 +584,15 @@ __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o
       if (i < ng) sc->g[i].tile_start = base + x - v;
       base += __shfl_sync(0xffffffffu, x, 31);
     }
-    if (lane == 0) sc->total_tiles = base;
+    __syncwarp();
+    if (lane == 0) {
+      sc->total_tiles = base;
+      sc->nparts = in.nparts > 1 ? in.nparts : 0;
+      if (in.nparts > 1) {
+        for (int gl = 0; gl < in.nparts; ++gl) sc->part_tile[gl] = sc->g[gl * S].tile_start;
+        sc->part_tile[in.nparts] = base;
+      }
+    }
   }
 }
 

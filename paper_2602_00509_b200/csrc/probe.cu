@@ -175,6 +175,7 @@ struct probe_ctx_s {
   uint32_t epoch[kSigKinds] = {0};   // cross-process barrier epochs (identical sequence on every process)
   bool multi_process() const { return cfg.local_ranks != cfg.ep_size; }
   bool unfused = false;   // PROBE_UNFUSED=1: logits written + separate top-k kernels (debug)
+  bool ep_emulation = false;  // partition expert GEMMs by local rank (probe_set_option)
   // phase profiling: prof_max forwards × (PROBE_NPHASE + 1) timing events
   int prof_max = 0, prof_n = 0;
   std::vector<cudaEvent_t> prof_ev;
@@ -475,6 +476,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   li.quota = use_plan ? ctx->at<int32_t>(s.quota[p]) : nullptr;
   li.replicas = use_plan ? ctx->at<int32_t>(s.reps[p]) : nullptr;
   li.bank = p;
+  li.nparts = (ctx->ep_emulation && d.GL > 1 && d.GL <= kMaxParts) ? d.GL : 0;
   li.act = ctx->scratch + s.act;
   li.y_local = ctx->local_base[PROBE_BUF_Y];
   LayoutOut lo;
@@ -822,6 +824,15 @@ probe_status probe_finalize(probe_ctx ctx) {
 }
 
 int64_t probe_launch_count(probe_ctx ctx) { return ctx ? ctx->launches : 0; }
+
+probe_status probe_set_option(probe_ctx ctx, int32_t option, int64_t value) {
+  if (!ctx) return fail(nullptr, PROBE_EINVAL, "null ctx");
+  switch (option) {
+    case PROBE_OPT_EP_EMULATION: ctx->ep_emulation = value != 0; return PROBE_OK;
+    case PROBE_OPT_UNFUSED_TOPK: ctx->unfused = value != 0; return PROBE_OK;
+  }
+  return fail(ctx, PROBE_EINVAL, "unknown option %d", option);
+}
 
 typedef CUresult (*PFN_getAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
 

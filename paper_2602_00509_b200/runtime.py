@@ -168,6 +168,9 @@ class ProbeRuntime:
               self.ctx)
         return out[:n.value]
 
+    def set_option(self, option: int, value: int):
+        check("probe_set_option", self.lib.probe_set_option(self.ctx, option, int(value)), self.ctx)
+
     def launches(self) -> int:
         return int(self.lib.probe_launch_count(self.ctx))
 

@@ -32,6 +32,7 @@ class CaseCfg:
     capacity_factor: float = 0.0
     bias: bool = False
     sample_tokens: int = 0          # >0: oracle outputs only for this many tokens per rank
+    ep_emulation: bool = False      # partitioned expert GEMMs (single-GPU EP straggler emulation)
 
 
 def f64(t):
@@ -60,6 +61,9 @@ def run_gpu(case: CaseCfg):
                       n_sat=case.n_sat, capacity_factor=case.capacity_factor,
                       bw_bytes_per_us=case.bw_bytes_per_us)
     rt = ProbeRuntime(cfg)
+    if case.ep_emulation:
+        from paper_2602_00509_b200._lib import OPT_EP_EMULATION
+        rt.set_option(OPT_EP_EMULATION, 1)
     dev = "cuda"
     L0 = pi.layer_inputs(sh, case.step, 0, case.zipf_s, device=dev)
     L1 = pi.layer_inputs(sh, case.step, 1, case.zipf_s, device=dev)
