@@ -714,6 +714,9 @@ __global__ void __launch_bounds__(128) k_combine(Dims d, int T, const float* __r
 // =============================================================================
 constexpr int kPrefetchChunk = 64 * 1024;  // bytes
 
+// Register copy (not TMA bulk): the expert-GEMM CTAs leave < 10 KB of shared memory per
+// SM, so a smem-staged copy could not co-reside with them during part 1.  Each thread keeps
+// 8 × 16 B in flight; chunks never straddle the W13 / W2 matrices.
 __global__ void __launch_bounds__(512) k_prefetch(Dims d, const int32_t* __restrict__ replicas, int bank,
                                                   const uint8_t* __restrict__ w13, const uint8_t* __restrict__ w2,
                                                   Sym sym, int buf_rw13, int buf_rw2, int32_t* ctr,
@@ -722,8 +725,9 @@ __global__ void __launch_bounds__(512) k_prefetch(Dims d, const int32_t* __restr
   __shared__ int s_chunk;
   const size_t w13_bytes = static_cast<size_t>(2) * d.F * d.H * 2;
   const size_t w2_bytes = static_cast<size_t>(d.H) * d.F * 2;
-  const size_t per = w13_bytes + w2_bytes;
-  const int cper = static_cast<int>((per + kPrefetchChunk - 1) / kPrefetchChunk);
+  const int c13 = static_cast<int>((w13_bytes + kPrefetchChunk - 1) / kPrefetchChunk);
+  const int c2 = static_cast<int>((w2_bytes + kPrefetchChunk - 1) / kPrefetchChunk);
+  const int cper = c13 + c2;
   // transfers whose sender (home of the expert) is a local rank, in (dst, slot) order
   __shared__ int tr_dst[kMaxG * kMaxRb], tr_slot[kMaxG * kMaxRb], tr_e[kMaxG * kMaxRb];
   __shared__ int s_ntr;
@@ -753,23 +757,28 @@ __global__ void __launch_bounds__(512) k_prefetch(Dims d, const int32_t* __restr
     __syncthreads();
     if (c < 0 || c >= total) break;
     const int ti = c / cper, ci = c % cper;
-    const int e = tr_e[ti];
-    const int le = e - d.R0 * d.EL;      // local expert index within the base weights
-    const size_t off = static_cast<size_t>(ci) * kPrefetchChunk;
-    const size_t len = (off + kPrefetchChunk <= per) ? kPrefetchChunk : per - off;
+    const int le = tr_e[ti] - d.R0 * d.EL;      // local expert index within the base weights
     const int slot = bank * kMaxRb + tr_slot[ti];
-    for (size_t b = threadIdx.x * 16; b < len; b += blockDim.x * 16) {
-      const size_t p = off + b;
-      uint4 v;
-      uint8_t* dstp;
-      if (p < w13_bytes) {
-        v = *reinterpret_cast<const uint4*>(w13 + static_cast<size_t>(le) * w13_bytes + p);
-        dstp = sym.at(buf_rw13, d.G, tr_dst[ti]) + static_cast<size_t>(slot) * w13_bytes + p;
-      } else {
-        v = *reinterpret_cast<const uint4*>(w2 + static_cast<size_t>(le) * w2_bytes + (p - w13_bytes));
-        dstp = sym.at(buf_rw2, d.G, tr_dst[ti]) + static_cast<size_t>(slot) * w2_bytes + (p - w13_bytes);
+    const bool first = ci < c13;
+    const size_t mat = first ? w13_bytes : w2_bytes;
+    const size_t off = static_cast<size_t>(first ? ci : ci - c13) * kPrefetchChunk;
+    const size_t len = (off + kPrefetchChunk <= mat) ? kPrefetchChunk : mat - off;
+    const uint4* src = reinterpret_cast<const uint4*>((first ? w13 : w2) + static_cast<size_t>(le) * mat + off);
+    uint4* dst = reinterpret_cast<uint4*>(sym.at(first ? buf_rw13 : buf_rw2, d.G, tr_dst[ti]) +
+                                          static_cast<size_t>(slot) * mat + off);
+    const int nv = static_cast<int>(len / 16);
+    for (int v0 = 0; v0 < nv; v0 += blockDim.x * 8) {
+      uint4 r[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = v0 + u * blockDim.x + threadIdx.x;
+        if (i < nv) r[u] = __ldg(src + i);
       }
-      *reinterpret_cast<uint4*>(dstp) = v;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = v0 + u * blockDim.x + threadIdx.x;
+        if (i < nv) dst[i] = r[u];
+      }
     }
     if (threadIdx.x == 0 && done_bytes_lo) atomicAdd(done_bytes_lo, static_cast<int32_t>(len >> 10));
   }

@@ -680,7 +680,7 @@ probe_status probe_prefetch(probe_ctx ctx, int32_t next_layer, const void* w13_n
   CK(cudaStreamWaitEvent(st, ctx->ev_plan[pp], 0));
   int32_t* flags = ctx->at<int32_t>(s.flags);
   const bool inflight = ctx->fwd_layer == next_layer - 1;
-  const int grid = 8;   // "controlled SM occupancy"
+  const int grid = 16;  // "controlled SM occupancy": 16 CTAs co-resident with the GEMM
   if (inflight) {
     CK(cudaStreamWaitEvent(st, ctx->ev_gemm[prev], 0));
     k_prefetch<<<grid, 512, 0, st>>>(d, ctx->at<int32_t>(s.reps[pp]), pp, static_cast<const uint8_t*>(w13_next),
