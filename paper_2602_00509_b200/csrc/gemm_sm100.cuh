@@ -352,15 +352,22 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           for (int i = 0; i < 32; ++i) {
             int e = c * 32 + i;
             float x = (e < G.n) ? __uint_as_float(v32[i]) + (G.bias ? __ldg(G.bias + e) : 0.f) : -INFINITY;
+            // early out: ids arrive ascending, so x enters only if it beats the current k-th strictly
+            bool enter = false;
 #pragma unroll
-            for (int j = 0; j < kTopkMax; ++j) {
-              // full order (value ↓, id ↑): a displaced (carried) element may tie with a
-              // later-id entry and must then win
-              if (j < kk && (x > tv[j] || (x == tv[j] && e < te[j]))) {
-                const float ov = tv[j];
-                const int oe = te[j];
-                tv[j] = x; te[j] = e;
-                x = ov; e = oe;
+            for (int j = 0; j < kTopkMax; ++j)
+              if (j == kk - 1) enter = x > tv[j];
+            if (enter) {
+#pragma unroll
+              for (int j = 0; j < kTopkMax; ++j) {
+                // full order (value ↓, id ↑): a displaced (carried) element may tie with a
+                // later-id entry and must then win
+                if (j < kk && (x > tv[j] || (x == tv[j] && e < te[j]))) {
+                  const float ov = tv[j];
+                  const int oe = te[j];
+                  tv[j] = x; te[j] = e;
+                  x = ov; e = oe;
+                }
               }
             }
           }
