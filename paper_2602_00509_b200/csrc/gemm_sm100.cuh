@@ -56,31 +56,34 @@ struct GemmSched {
   int32_t num_groups;
   int32_t total_tiles;
   int32_t nparts;                    // >1: CTA b serves only partition b % nparts (EP emulation)
-  int32_t pad;
+  int32_t counter;                   // dynamic tile counter (reset by the kernel writing the schedule)
   int32_t part_tile[kMaxParts + 1];  // tile range [part_tile[p], part_tile[p+1]) of partition p
+  int32_t part_counter[kMaxParts];   // per-partition tile counters
   GemmGroup g[kMaxGroups];
 };
 
-// Persistent tile iterator.  Default: all CTAs stride over all tiles.  Partitioned
-// (single-GPU EP emulation): the grid is split into `nparts` CTA sets (b % nparts),
-// each set striding only over its logical rank's tiles, so a rank's expert GEMM runs on
-// ~#SMs/nparts SMs and the launch time is the max over ranks (the straggler, Eq. 3).
-struct TileIter {
-  int cur, end, step;
-  __device__ TileIter(const GemmSched* s) {
-    const int np = s->nparts;
-    if (np > 1) {
-      const int p = blockIdx.x % np, j = blockIdx.x / np;
-      step = (static_cast<int>(gridDim.x) - p + np - 1) / np;
-      cur = s->part_tile[p] + j;
-      end = s->part_tile[p + 1];
-    } else {
-      cur = blockIdx.x;
-      end = s->total_tiles;
-      step = gridDim.x;
-    }
+// Dynamic persistent tile scheduling: the producer warp claims the next tile from a
+// global atomic counter and hands it to the MMA and epilogue warps through an
+// mbarrier-guarded shared-memory queue.  CTAs that start late (SMs still busy with a
+// concurrent aux-stream kernel) simply take fewer tiles.  Partitioned mode (single-GPU EP
+// emulation): CTA b serves only partition b % nparts (its logical rank's tiles), so a rank's
+// expert GEMM runs on ~#SMs/nparts SMs and the launch time is the straggler's (Eq. 3).
+constexpr int kTileQ = 8;
+__device__ __forceinline__ int claim_tile(GemmSched* s) {
+  const int np = s->nparts;
+  if (np > 1) {
+    const int p = blockIdx.x % np;
+    const int t = s->part_tile[p] + atomicAdd(&s->part_counter[p], 1);
+    return t < s->part_tile[p + 1] ? t : -1;
   }
-};
+  const int t = atomicAdd(&s->counter, 1);
+  return t < s->total_tiles ? t : -1;
+}
+
+__device__ __forceinline__ void sched_reset_counters(GemmSched* s) {
+  s->counter = 0;
+  for (int p = 0; p < kMaxParts; ++p) s->part_counter[p] = 0;
+}
 
 __host__ __device__ inline int gemm_ntiles_n(const GemmGroup& G, int BN) {
   const int bno = (G.mode == EPI_SWIGLU) ? BN / 2 : BN;
@@ -93,6 +96,7 @@ __host__ __device__ inline int gemm_ntiles(const GemmGroup& G, int BN) {
 // Serial prefix over the group table (called by one thread).
 __device__ inline void gemm_finalize_sched(GemmSched* s, int BN) {
   s->nparts = 0;
+  sched_reset_counters(s);
   int acc = 0;
   for (int i = 0; i < s->num_groups; ++i) {
     s->g[i].tile_start = acc;
@@ -106,7 +110,7 @@ struct GemmSmem {
   static constexpr int A_BYTES = 128 * 128;
   static constexpr int B_BYTES = BN * 128;
   static constexpr int BAR_OFF = STAGES * (A_BYTES + B_BYTES);
-  static constexpr int TS_OFF = BAR_OFF + (2 * STAGES + 4) * 8 + 16;
+  static constexpr int TS_OFF = BAR_OFF + (2 * STAGES + 4 + 2 * kTileQ) * 8 + 16 + kTileQ * 4;
   static constexpr int EPI_OFF = (TS_OFF + (kMaxGroups + 1) * 4 + 1023) / 1024 * 1024;
   // per epilogue warp: NB staging tiles of 32 rows × 128 B, 16-byte chunks XOR-swizzled by
   // (row mod 8) = the TMA SWIZZLE_128B layout (also bank-conflict-free for the manual path)
@@ -209,7 +213,7 @@ template <int BN, int STAGES, int EW = 4>
 __global__ void __launch_bounds__(128 + 32 * EW, 1)
 grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
                     const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmC,
-                    const __grid_constant__ CUtensorMap tmA2, const GemmSched* __restrict__ sched, int K, int K2) {
+                    const __grid_constant__ CUtensorMap tmA2, GemmSched* __restrict__ sched, int K, int K2) {
   using L = GemmSmem<BN, STAGES, EW>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -219,13 +223,15 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* qfull = tempty + 2;                 // tile queue (producer → MMA + epilogue warps)
+  uint64_t* qempty = qfull + kTileQ;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qempty + kTileQ);
+  volatile int* tq = reinterpret_cast<volatile int*>(tmem_slot + 4);
   int* ts = reinterpret_cast<int*>(smem + L::TS_OFF);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int ng = sched->num_groups;
-  const TileIter it0(sched);
   for (int i = threadIdx.x; i < ng; i += blockDim.x) ts[i] = sched->g[i].tile_start;
 
   if (warp == 0 && lane == 0) {
@@ -236,6 +242,10 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
       ptx::mbar_init(&tempty[a], EW);
+    }
+    for (int q = 0; q < kTileQ; ++q) {
+      ptx::mbar_init(&qfull[q], 1);
+      ptx::mbar_init(&qempty[q], 1 + EW);
     }
     ptx::fence_barrier_init();
     ptx::tma_prefetch_desc(&tmA);
@@ -257,7 +267,15 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = it0.cur; tile < it0.end; tile += it0.step) {
+      int qs = 0;
+      uint32_t qph = 0;
+      while (true) {
+        const int tile = claim_tile(sched);
+        ptx::mbar_wait(&qempty[qs], qph ^ 1);
+        tq[qs] = tile;
+        ptx::mbar_arrive(&qfull[qs]);
+        if (++qs == kTileQ) { qs = 0; qph ^= 1; }
+        if (tile < 0) break;
         const int gi = gemm_find_group(ts, ng, tile);
         const GemmGroup& G = sched->g[gi];
         const int nt = gemm_ntiles_n(G, BN);
@@ -293,7 +311,15 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     uint32_t phase = 0;
     int acc = 0;
     uint32_t aphase = 0;
-    for (int tile = it0.cur; tile < it0.end; tile += it0.step) {
+    int qs = 0;
+    uint32_t qph = 0;
+    while (true) {
+      ptx::mbar_wait(&qfull[qs], qph);
+      const int tile = tq[qs];
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&qempty[qs]);
+      if (++qs == kTileQ) { qs = 0; qph ^= 1; }
+      if (tile < 0) break;
       ptx::mbar_wait(&tempty[acc], aphase ^ 1);
       ptx::tc_fence_after();
       const uint32_t d = tmem_base + acc * BN;
@@ -325,7 +351,15 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     int tsel = 0;
     int acc = 0;
     uint32_t aphase = 0;
-    for (int tile = it0.cur; tile < it0.end; tile += it0.step) {
+    int qs = 0;
+    uint32_t qph = 0;
+    while (true) {
+      ptx::mbar_wait(&qfull[qs], qph);
+      const int tile = tq[qs];
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&qempty[qs]);
+      if (++qs == kTileQ) { qs = 0; qph ^= 1; }
+      if (tile < 0) break;
       const int gi = gemm_find_group(ts, ng, tile);
       const GemmGroup G = sched->g[gi];
       const int nt = gemm_ntiles_n(G, BN);

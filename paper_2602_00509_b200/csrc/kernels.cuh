@@ -587,6 +587,7 @@ __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o
     __syncwarp();
     if (lane == 0) {
       sc->total_tiles = base;
+      sched_reset_counters(sc);
       sc->nparts = in.nparts > 1 ? in.nparts : 0;
       if (in.nparts > 1) {
         for (int gl = 0; gl < in.nparts; ++gl) sc->part_tile[gl] = sc->g[gl * S].tile_start;

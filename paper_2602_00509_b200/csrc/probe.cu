@@ -220,7 +220,7 @@ enum GemmVariant { V_128_6_4 = 0, V_256_4_4 = 1, V_256_3_8 = 2, V_128_4_8 = 3 };
 
 template <int BN, int ST, int EW>
 cudaError_t launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, const CUtensorMap& c,
-                          const CUtensorMap& a2, const GemmSched* s, int K, int K2, int grid, cudaStream_t st) {
+                          const CUtensorMap& a2, GemmSched* s, int K, int K2, int grid, cudaStream_t st) {
   using L = GemmSmem<BN, ST, EW>;
   static bool attr = false;
   if (!attr) {
@@ -234,7 +234,7 @@ cudaError_t launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b0, const CUt
 }
 
 cudaError_t launch_gemm_v(int v, const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1,
-                          const CUtensorMap& c, const GemmSched* s, int K, int grid, cudaStream_t st,
+                          const CUtensorMap& c, GemmSched* s, int K, int grid, cudaStream_t st,
                           const CUtensorMap* a2 = nullptr, int K2 = 0) {
   const CUtensorMap& A2 = a2 ? *a2 : a;
   switch (v) {
@@ -248,7 +248,7 @@ cudaError_t launch_gemm_v(int v, const CUtensorMap& a, const CUtensorMap& b0, co
 int variant_bn(int v) { return (v == V_128_6_4 || v == V_128_4_8) ? 128 : 256; }
 
 template <int BN>
-cudaError_t launch_gemm(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, const GemmSched* s, int K,
+cudaError_t launch_gemm(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, GemmSched* s, int K,
                         int grid, cudaStream_t st) {
   return launch_gemm_v(BN == 256 ? V_256_4_4 : V_128_6_4, a, b0, b1, a, s, K, grid, st);
 }
@@ -771,10 +771,16 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
-  cudaError_t e = launch_gemm_v(variant, ma, mb, mb, mc, ds, K, sms, st);   // warm-up / single run
+  // the dynamic tile counter is reset before every launch (the forward path resets it in
+  // the kernel that writes the schedule)
+  cudaError_t e = cudaMemsetAsync(&ds->counter, 0, sizeof(int32_t), st);
+  if (e == cudaSuccess) e = launch_gemm_v(variant, ma, mb, mb, mc, ds, K, sms, st);   // warm-up / single run
   if (e == cudaSuccess && reps > 1) {
     e = cudaEventRecord(e0, st);
-    for (int r = 0; r < reps && e == cudaSuccess; ++r) e = launch_gemm_v(variant, ma, mb, mb, mc, ds, K, sms, st);
+    for (int r = 0; r < reps && e == cudaSuccess; ++r) {
+      e = cudaMemsetAsync(&ds->counter, 0, sizeof(int32_t), st);
+      if (e == cudaSuccess) e = launch_gemm_v(variant, ma, mb, mb, mc, ds, K, sms, st);
+    }
     if (e == cudaSuccess) e = cudaEventRecord(e1, st);
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
