@@ -510,7 +510,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   CK(launch_gemm_v(V_256_4_4, ctx->map_recv, *m13, ctx->map_rw13, ctx->map_recv, lo.s1, d.H, ctx->num_sms, st));
   ++ctx->launches;
   MARK(6);
-  CK(launch_gemm_v(V_256_3_8, ctx->map_act, *m2, ctx->map_rw2, ctx->map_y, lo.s2, d.F, ctx->num_sms, st));
+  CK(launch_gemm_v(V_256_4_4, ctx->map_act, *m2, ctx->map_rw2, ctx->map_y, lo.s2, d.F, ctx->num_sms, st));
   ++ctx->launches;
   CK(xbarrier(ctx, BAR_Y, st));                 // every expert rank's Y rows are complete
   MARK(7);
@@ -730,13 +730,23 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
                               float* ms_out, void* C, void* stream) {
   probe_ctx ctx = nullptr;
   if (!A || !B || !groups || !C || num_groups < 1 || num_groups > kMaxGroups || K < 1 || N < 8 || N % 8 ||
-      reps < 1 || mode < 0 || mode > 4)
+      reps < 1 || mode < 0 || mode > 6)
     return fail(nullptr, PROBE_EINVAL, "probe_test_gemm: bad arguments");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (variant < 0) variant = mode == 1 ? V_256_4_4 : (mode == 2 ? V_256_3_8 : V_128_6_4);
   if (variant > V_128_4_8) return fail(nullptr, PROBE_EINVAL, "bad variant");
   const int BN = variant_bn(variant);
-  const int emode = mode == 1 ? EPI_SWIGLU : (mode == 3 ? EPI_SILU_BF16 : (mode == 4 ? EPI_NONE : EPI_F32));
+  const int emode = mode == 1 ? EPI_SWIGLU
+                    : mode == 3 ? EPI_SILU_BF16
+                    : mode == 4 ? EPI_NONE
+                    : mode == 5 ? EPI_TOPK
+                    : mode == 6 ? EPI_TOPK_COUNT : EPI_F32;
+  void* topk_aux = nullptr;
+  if (emode == EPI_TOPK || emode == EPI_TOPK_COUNT) {
+    if (N > 256) return fail(nullptr, PROBE_EINVAL, "top-k modes need N <= 256");
+    CK(cudaMalloc(&topk_aux, static_cast<size_t>(a_rows) * 8 * 4 + static_cast<size_t>(N) * 4 * 64));
+    CK(cudaMemset(topk_aux, 0, static_cast<size_t>(a_rows) * 8 * 4 + static_cast<size_t>(N) * 4 * 64));
+  }
   const int n_out = mode == 1 ? N / 2 : N;
   std::vector<uint8_t> host(sizeof(GemmSched), 0);
   GemmSched* hs = reinterpret_cast<GemmSched*>(host.data());
@@ -749,6 +759,12 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
     hs->g[i] = mk_group(g[0], g[1], g[2], 0, emode, n_out, n_out, static_cast<uint8_t*>(C) + static_cast<size_t>(g[3]) * n_out * esz);
     hs->g[i].out_row = g[3];
     hs->g[i].tma_out = emode == EPI_F32 && n_out % 32 == 0 ? 1 : 0;
+    if (topk_aux) {   // test hook: k = 8; TOPK writes ids to C, weights to aux; COUNT: counts [64][N]
+      hs->g[i].topk = 8;
+      hs->g[i].rows_per_rank = static_cast<int>((a_rows + 63) / 64);
+      hs->g[i].aux = topk_aux;
+      hs->g[i].out = static_cast<uint8_t*>(C) + static_cast<size_t>(g[3]) * 8 * 4;
+    }
     c_rows = std::max<int64_t>(c_rows, static_cast<int64_t>(g[3]) + g[1]);
     hs->g[i].tile_start = acc;
     acc += gemm_ntiles(hs->g[i], BN);
@@ -792,6 +808,7 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaFree(ds);
+  if (topk_aux) cudaFree(topk_aux);
   if (e != cudaSuccess) return fail(nullptr, PROBE_ECUDA, "probe_test_gemm: %s", cudaGetErrorString(e));
   return PROBE_OK;
 }
