@@ -207,6 +207,60 @@ __device__ __forceinline__ void epi_chunk(float* tiles, int& tsel, int lane, con
   tsel = (tsel + 1) % NB;
 }
 
+// Fused router / predictor top-k (a1, a2): row = token (lane).  The k-element list is
+// sorted by (value ↓, id ↑) (R3, R4) and lives in registers (KK is a compile-time
+// constant so no index is dynamic).  Columns arrive in ascending expert id, so a new value
+// enters only if it beats the current k-th strictly; a displaced (carried) element may tie
+// with a later-id entry and then wins.
+template <int KK, int BN>
+__device__ __forceinline__ void epi_topk(uint32_t tb, int lane, const GemmGroup& G, int row0) {
+  float tv[KK];
+  int te[KK];
+#pragma unroll
+  for (int j = 0; j < KK; ++j) { tv[j] = -INFINITY; te[j] = 0x7fffffff; }
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    if (c * 32 >= G.n) break;
+    uint32_t v32[32];
+    ptx::tmem_ld32(tb + c * 32, v32);
+    ptx::tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      int e = c * 32 + i;
+      float x = (e < G.n) ? __uint_as_float(v32[i]) + (G.bias ? __ldg(G.bias + e) : 0.f) : -INFINITY;
+      if (x > tv[KK - 1]) {
+#pragma unroll
+        for (int j = 0; j < KK; ++j) {
+          if (x > tv[j] || (x == tv[j] && e < te[j])) {
+            const float ov = tv[j];
+            const int oe = te[j];
+            tv[j] = x; te[j] = e;
+            x = ov; e = oe;
+          }
+        }
+      }
+    }
+  }
+  const int row = row0 + lane;
+  if (row >= G.m) return;
+  if (G.mode == EPI_TOPK) {
+    float w[KK], sum = 0.f;
+#pragma unroll
+    for (int j = 0; j < KK; ++j) {
+      w[j] = expf(tv[j] - tv[0]);
+      sum += w[j];
+    }
+    int32_t* ids = reinterpret_cast<int32_t*>(G.out) + static_cast<size_t>(row) * KK;
+    float* gw = reinterpret_cast<float*>(G.aux) + static_cast<size_t>(row) * KK;
+#pragma unroll
+    for (int j = 0; j < KK; ++j) { ids[j] = te[j]; gw[j] = w[j] / sum; }
+  } else {
+    int32_t* cnt = reinterpret_cast<int32_t*>(G.aux) + static_cast<size_t>((G.a_row + row) / G.rows_per_rank) * G.n;
+#pragma unroll
+    for (int j = 0; j < KK; ++j) atomicAdd(cnt + te[j], 1);
+  }
+}
+
 // EW epilogue warps (4 or 8): warp 4+i reads TMEM lane quarter i%4 and handles the
 // column chunks c ≡ i/4 (mod EW/4).  Threads = 128 + 32·EW.
 template <int BN, int STAGES, int EW = 4>
@@ -370,63 +424,15 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
       const int row0 = mb * 128 + q * 32;          // first tile row of this warp
       if (G.mode == EPI_TOPK || G.mode == EPI_TOPK_COUNT) {
-        // row = token (lane); insertion into a register list sorted by (value ↓, id ↑) (R3, R4)
-        float tv[kTopkMax];
-        int te[kTopkMax];
-#pragma unroll
-        for (int j = 0; j < kTopkMax; ++j) { tv[j] = -INFINITY; te[j] = 0x7fffffff; }
-        const int kk = G.topk;
-#pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          if (c * 32 >= G.n) break;
-          uint32_t v32[32];
-          ptx::tmem_ld32(tb + c * 32, v32);
-          ptx::tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            int e = c * 32 + i;
-            float x = (e < G.n) ? __uint_as_float(v32[i]) + (G.bias ? __ldg(G.bias + e) : 0.f) : -INFINITY;
-            // early out: ids arrive ascending, so x enters only if it beats the current k-th strictly
-            bool enter = false;
-#pragma unroll
-            for (int j = 0; j < kTopkMax; ++j)
-              if (j == kk - 1) enter = x > tv[j];
-            if (enter) {
-#pragma unroll
-              for (int j = 0; j < kTopkMax; ++j) {
-                // full order (value ↓, id ↑): a displaced (carried) element may tie with a
-                // later-id entry and must then win
-                if (j < kk && (x > tv[j] || (x == tv[j] && e < te[j]))) {
-                  const float ov = tv[j];
-                  const int oe = te[j];
-                  tv[j] = x; te[j] = e;
-                  x = ov; e = oe;
-                }
-              }
-            }
-          }
-        }
-        const int row = row0 + lane;
-        if (row < G.m) {
-          if (G.mode == EPI_TOPK) {
-            float w[kTopkMax], sum = 0.f;
-#pragma unroll
-            for (int j = 0; j < kTopkMax; ++j) {
-              w[j] = j < kk ? expf(tv[j] - tv[0]) : 0.f;
-              sum += w[j];
-            }
-            int32_t* ids = reinterpret_cast<int32_t*>(G.out) + static_cast<size_t>(row) * kk;
-            float* gw = reinterpret_cast<float*>(G.aux) + static_cast<size_t>(row) * kk;
-#pragma unroll
-            for (int j = 0; j < kTopkMax; ++j)
-              if (j < kk) { ids[j] = te[j]; gw[j] = w[j] / sum; }
-          } else {
-            int32_t* cnt = reinterpret_cast<int32_t*>(G.aux) +
-                           static_cast<size_t>((G.a_row + row) / G.rows_per_rank) * G.n;
-#pragma unroll
-            for (int j = 0; j < kTopkMax; ++j)
-              if (j < kk) atomicAdd(cnt + te[j], 1);
-          }
+        switch (G.topk) {
+          case 1: epi_topk<1, BN>(tb, lane, G, row0); break;
+          case 2: epi_topk<2, BN>(tb, lane, G, row0); break;
+          case 3: epi_topk<3, BN>(tb, lane, G, row0); break;
+          case 4: epi_topk<4, BN>(tb, lane, G, row0); break;
+          case 5: epi_topk<5, BN>(tb, lane, G, row0); break;
+          case 6: epi_topk<6, BN>(tb, lane, G, row0); break;
+          case 7: epi_topk<7, BN>(tb, lane, G, row0); break;
+          default: epi_topk<8, BN>(tb, lane, G, row0); break;
         }
       } else if (G.mode == EPI_SWIGLU) {
 #pragma unroll 1
