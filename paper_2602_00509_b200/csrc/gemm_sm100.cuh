@@ -213,7 +213,7 @@ __device__ __forceinline__ void epi_chunk(float* tiles, int& tsel, int lane, con
 // enters only if it beats the current k-th strictly; a displaced (carried) element may tie
 // with a later-id entry and then wins.
 template <int KK, int BN>
-__device__ __forceinline__ void epi_topk(uint32_t tb, int lane, const GemmGroup& G, int row0) {
+__device__ __forceinline__ void epi_topk(uint32_t tb, int lane, const GemmGroup& G, int row0, float* stage) {
   float tv[KK];
   int te[KK];
 #pragma unroll
@@ -224,10 +224,16 @@ __device__ __forceinline__ void epi_topk(uint32_t tb, int lane, const GemmGroup&
     uint32_t v32[32];
     ptx::tmem_ld32(tb + c * 32, v32);
     ptx::tmem_ld_wait();
+    // stage the row in smem (element i of row r at r·32 + (i ^ r): conflict-free both ways)
+    __syncwarp();
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
+    for (int i = 0; i < 32; ++i) stage[lane * 32 + (i ^ lane)] = __uint_as_float(v32[i]);
+    __syncwarp();
+    const int nv = min(32, G.n - c * 32);
+#pragma unroll 1
+    for (int i = 0; i < nv; ++i) {
       int e = c * 32 + i;
-      float x = (e < G.n) ? __uint_as_float(v32[i]) + (G.bias ? __ldg(G.bias + e) : 0.f) : -INFINITY;
+      float x = stage[lane * 32 + (i ^ lane)] + (G.bias ? __ldg(G.bias + e) : 0.f);
       if (x > tv[KK - 1]) {
 #pragma unroll
         for (int j = 0; j < KK; ++j) {
@@ -425,14 +431,14 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       const int row0 = mb * 128 + q * 32;          // first tile row of this warp
       if (G.mode == EPI_TOPK || G.mode == EPI_TOPK_COUNT) {
         switch (G.topk) {
-          case 1: epi_topk<1, BN>(tb, lane, G, row0); break;
-          case 2: epi_topk<2, BN>(tb, lane, G, row0); break;
-          case 3: epi_topk<3, BN>(tb, lane, G, row0); break;
-          case 4: epi_topk<4, BN>(tb, lane, G, row0); break;
-          case 5: epi_topk<5, BN>(tb, lane, G, row0); break;
-          case 6: epi_topk<6, BN>(tb, lane, G, row0); break;
-          case 7: epi_topk<7, BN>(tb, lane, G, row0); break;
-          default: epi_topk<8, BN>(tb, lane, G, row0); break;
+          case 1: epi_topk<1, BN>(tb, lane, G, row0, tiles); break;
+          case 2: epi_topk<2, BN>(tb, lane, G, row0, tiles); break;
+          case 3: epi_topk<3, BN>(tb, lane, G, row0, tiles); break;
+          case 4: epi_topk<4, BN>(tb, lane, G, row0, tiles); break;
+          case 5: epi_topk<5, BN>(tb, lane, G, row0, tiles); break;
+          case 6: epi_topk<6, BN>(tb, lane, G, row0, tiles); break;
+          case 7: epi_topk<7, BN>(tb, lane, G, row0, tiles); break;
+          default: epi_topk<8, BN>(tb, lane, G, row0, tiles); break;
         }
       } else if (G.mode == EPI_SWIGLU) {
 #pragma unroll 1
