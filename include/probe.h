@@ -216,9 +216,11 @@ probe_status probe_ipc_close(uint64_t dev_ptr_base);
 /* Options.  PROBE_OPT_EP_EMULATION (single-GPU emulation only): the expert GEMMs split the
  * persistent grid into local_ranks CTA sets, each serving only its logical rank's tiles, so
  * a rank's GEMM runs on ~#SMs/local_ranks SMs and the GEMM time is the straggler's (Eq. 3)
- * as on one GPU per rank.  PROBE_OPT_UNFUSED_TOPK: write logits and run the separate
- * top-k kernels instead of the fused GEMM-epilogue top-k (debug). */
-enum { PROBE_OPT_EP_EMULATION = 1, PROBE_OPT_UNFUSED_TOPK = 2 };
+ * as on one GPU per rank.  PROBE_OPT_UNFUSED_TOPK: predictor prior and residual as separate
+ * GEMMs and warp-shuffle top-k kernels (debug reference path).  PROBE_OPT_FUSED_EPILOGUE_TOPK:
+ * do the router/predictor top-k inside the tcgen05 GEMM epilogue instead of the
+ * thread-per-token select kernel (default off: measured slower). */
+enum { PROBE_OPT_EP_EMULATION = 1, PROBE_OPT_UNFUSED_TOPK = 2, PROBE_OPT_FUSED_EPILOGUE_TOPK = 3 };
 probe_status probe_set_option(probe_ctx ctx, int32_t option, int64_t value);
 
 /* Number of library kernel launches enqueued so far by this context (bench accounting). */

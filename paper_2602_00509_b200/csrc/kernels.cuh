@@ -148,6 +148,102 @@ __global__ void __launch_bounds__(128) k_topk(Dims d, int T, const float* __rest
 }
 
 // =============================================================================
+// a1/a2 top-k, thread per token (high occupancy): the block's 128 logit rows are staged
+// in shared memory with coalesced loads (row r, column e at r·E + (e ^ (r & 31)) —
+// conflict-free for the row-wise reads), then each thread keeps a register list sorted
+// by (value ↓, id ↑) (R3, R4; KK compile-time so nothing spills).  Gate mode also writes
+// the softmax over the selected logits (R1) and the per-chunk dispatch ranks (the
+// expert bitmasks of k_rank); predictor mode accumulates n̂[rank][e] (R9).
+// grid (ceil(T/128), GL), block 128; dynamic smem 128·E·4 bytes.
+// =============================================================================
+template <int KK, bool PRED>
+__global__ void __launch_bounds__(128) k_select(Dims d, int T, const float* __restrict__ logits,
+                                                const float* __restrict__ bias, int32_t* __restrict__ ids,
+                                                float* __restrict__ gw, int32_t* __restrict__ pos,
+                                                int32_t* __restrict__ hist, int32_t* __restrict__ counts) {
+  extern __shared__ float lrow[];                  // [128][E] swizzled
+  __shared__ uint32_t mask[kMaxE * 4];
+  __shared__ int32_t scount[kMaxE];
+  const int E = d.E;
+  const int chunk = blockIdx.x, gl = blockIdx.y, nchunks = gridDim.x;
+  const int tl = threadIdx.x, t0 = chunk * kChunk;
+  const int nt = min(kChunk, T - t0);
+  for (int i = tl; i < E * 4; i += blockDim.x) mask[i] = 0u;
+  for (int i = tl; i < E; i += blockDim.x) scount[i] = 0;
+  // coalesced staging: consecutive threads read consecutive columns
+  const float* src = logits + (static_cast<size_t>(gl) * T + t0) * E;
+  for (int i = tl; i < nt * E; i += blockDim.x) {
+    const int r = i / E, e = i % E;
+    float v = src[i];
+    if (bias) v += bias[e];
+    lrow[r * E + (e ^ (r & 31))] = v;
+  }
+  __syncthreads();
+  int te[KK];
+  if (tl < nt) {
+    float tv[KK];
+#pragma unroll
+    for (int j = 0; j < KK; ++j) { tv[j] = -INFINITY; te[j] = 0x7fffffff; }
+    const float* row = lrow + tl * E;
+#pragma unroll 4
+    for (int i = 0; i < E; ++i) {
+      float x = row[i ^ (tl & 31)];
+      int e = i;
+      if (x > tv[KK - 1]) {
+#pragma unroll
+        for (int j = 0; j < KK; ++j) {
+          if (x > tv[j] || (x == tv[j] && e < te[j])) {
+            const float ov = tv[j];
+            const int oe = te[j];
+            tv[j] = x; te[j] = e;
+            x = ov; e = oe;
+          }
+        }
+      }
+    }
+    const size_t o = (static_cast<size_t>(gl) * T + t0 + tl) * KK;
+    if (!PRED) {
+      float w[KK], sum = 0.f;
+#pragma unroll
+      for (int j = 0; j < KK; ++j) {
+        w[j] = expf(tv[j] - tv[0]);
+        sum += w[j];
+      }
+#pragma unroll
+      for (int j = 0; j < KK; ++j) {
+        ids[o + j] = te[j];
+        gw[o + j] = w[j] / sum;
+        atomicOr(&mask[te[j] * 4 + (tl >> 5)], 1u << (tl & 31));
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < KK; ++j) atomicAdd(&scount[te[j]], 1);
+    }
+  }
+  __syncthreads();
+  if (PRED) {
+    for (int e = tl; e < E; e += blockDim.x)
+      if (scount[e]) atomicAdd(&counts[gl * E + e], scount[e]);
+    return;
+  }
+  for (int e = tl; e < E; e += blockDim.x) {
+    const uint32_t* m = &mask[e * 4];
+    hist[(static_cast<size_t>(gl) * nchunks + chunk) * E + e] = __popc(m[0]) + __popc(m[1]) + __popc(m[2]) + __popc(m[3]);
+  }
+  if (tl < nt) {
+    const int w = tl >> 5, b = tl & 31;
+    const size_t o = (static_cast<size_t>(gl) * T + t0 + tl) * KK;
+#pragma unroll
+    for (int j = 0; j < KK; ++j) {
+      const uint32_t* m = &mask[te[j] * 4];
+      int p = __popc(m[w] & ((1u << b) - 1u));
+      for (int ww = 0; ww < w; ++ww) p += __popc(m[ww]);
+      pos[o + j] = p;
+    }
+  }
+}
+
+// =============================================================================
 // a5/a6 helper after the fused gate: per 128-token chunk, expert bitmasks built
 // from the routing ids (order-independent atomicOr) → per-chunk histograms and
 // the rank of every (token, slot) among the chunk's tokens of its expert (token

@@ -176,6 +176,7 @@ struct probe_ctx_s {
   bool multi_process() const { return cfg.local_ranks != cfg.ep_size; }
   bool unfused = false;   // PROBE_UNFUSED=1: logits written + separate top-k kernels (debug)
   bool ep_emulation = false;  // partition expert GEMMs by local rank (probe_set_option)
+  bool fused_epi_topk = false;  // top-k in the GEMM epilogue instead of k_select (probe_set_option)
   // phase profiling: prof_max forwards × (PROBE_NPHASE + 1) timing events
   int prof_max = 0, prof_n = 0;
   std::vector<cudaEvent_t> prof_ev;
@@ -251,6 +252,31 @@ template <int BN>
 cudaError_t launch_gemm(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, GemmSched* s, int K,
                         int grid, cudaStream_t st) {
   return launch_gemm_v(BN == 256 ? V_256_4_4 : V_128_6_4, a, b0, b1, a, s, K, grid, st);
+}
+
+template <bool PRED>
+cudaError_t launch_select(const Dims& d, int T, int nchunks, cudaStream_t st, const float* lg, const float* b,
+                          int32_t* ids, float* gw, int32_t* pos, int32_t* hist, int32_t* cnt) {
+  const size_t smem = static_cast<size_t>(kChunk) * d.E * 4;
+  dim3 grid(nchunks, d.GL);
+#define SEL(KK)                                                                                         \
+  case KK: {                                                                                            \
+    static bool a = false;                                                                              \
+    if (!a) {                                                                                           \
+      cudaError_t e = cudaFuncSetAttribute(k_select<KK, PRED>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                           128 * 256 * 4);                                              \
+      if (e != cudaSuccess) return e;                                                                   \
+      a = true;                                                                                         \
+    }                                                                                                   \
+    k_select<KK, PRED><<<grid, 128, smem, st>>>(d, T, lg, b, ids, gw, pos, hist, cnt);                 \
+    break;                                                                                              \
+  }
+  switch (d.k) {
+    SEL(1) SEL(2) SEL(3) SEL(4) SEL(5) SEL(6) SEL(7) SEL(8)
+    default: return cudaErrorInvalidValue;
+  }
+#undef SEL
+  return cudaGetLastError();
 }
 
 template <bool PRED>
@@ -433,7 +459,12 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   MARK(0);
   // a1 gate: logits = x W_rᵀ on tcgen05 with the top-k + softmax fused in the epilogue
   // (fp32 logits never leave TMEM/registers); then per-chunk dispatch ranks.
-  const bool fused_gate = d.k <= kTopkMax && d.E <= 256 && !ctx->unfused;
+  // a1 gate: logits = x W_rᵀ on tcgen05 (fp32 logits, HBM-bound) → thread-per-token select
+  // (top-k + softmax + dispatch ranks).  The GEMM-epilogue top-k (EPI_TOPK) is available via
+  // PROBE_OPT_FUSED_EPILOGUE_TOPK: it saves the 2×33 MB logits round trip but runs the
+  // serial selection at 1 warp per SM sub-partition, which measured slower.
+  const bool sel = d.k <= kTopkMax && d.E <= kMaxE && !ctx->unfused;
+  const bool fused_gate = sel && ctx->fused_epi_topk;
   SmallGroups sg{};
   sg.n = 1;
   sg.BN = d.E <= 128 ? 128 : 256;
@@ -443,7 +474,6 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
     sg.g[0].aux = ctx->at<float>(s.gw);
     sg.g[0].bias = b_router;
   } else {
-    sg.BN = 128;
     sg.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_F32, d.E, d.E, ctx->at<float>(s.logits));
   }
   const CUtensorMap* mr = ctx->maps.get(w_router, E, H, sg.BN / 2);
@@ -456,6 +486,9 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   if (fused_gate) {
     k_rank<<<dim3(nchunks, d.GL), 128, 0, st>>>(d, T, ctx->at<int32_t>(s.ids), ctx->at<int32_t>(s.pos),
                                                 ctx->at<int32_t>(s.hist));
+  } else if (sel) {
+    CK(launch_select<false>(d, T, nchunks, st, ctx->at<float>(s.logits), b_router, ctx->at<int32_t>(s.ids),
+                            ctx->at<float>(s.gw), ctx->at<int32_t>(s.pos), ctx->at<int32_t>(s.hist), nullptr));
   } else {
     launch_topk<false>(d, T, nchunks, st, ctx->at<float>(s.logits), nullptr, b_router, ctx->at<int32_t>(s.ids),
                        ctx->at<float>(s.gw), ctx->at<int32_t>(s.pos), ctx->at<int32_t>(s.hist), nullptr, nullptr);
@@ -581,16 +614,25 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
     SmallGroups s2{};
     s2.BN = BN;
     s2.n = 1;
-    s2.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_TOPK_COUNT, d.E, d.E, nullptr);
-    s2.g[0].topk = d.k;
-    s2.g[0].rows_per_rank = T;
-    s2.g[0].aux = ctx->at<int32_t>(s.pred_local);
-    s2.g[0].bias = b_router_next;
+    if (ctx->fused_epi_topk) {
+      s2.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_TOPK_COUNT, d.E, d.E, nullptr);
+      s2.g[0].topk = d.k;
+      s2.g[0].rows_per_rank = T;
+      s2.g[0].aux = ctx->at<int32_t>(s.pred_local);
+      s2.g[0].bias = b_router_next;
+    } else {
+      s2.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_F32, d.E, d.E, ctx->at<float>(s.pprior));
+    }
     k_write_sched<<<1, 32, 0, st>>>(ctx->at<GemmSched>(s.s_p2), s2);
     CKL();
     CK(launch_gemm_v(BN == 128 ? V_128_6_4 : V_256_4_4, *mx, *mw, w_res1 ? *m2 : *mw, *mx, ctx->at<GemmSched>(s.s_p2),
                      d.H, ctx->num_sms, st, w_res1 ? ma : nullptr, w_res1 ? d.h : 0));
     ++ctx->launches;
+    if (!ctx->fused_epi_topk) {
+      CK(launch_select<true>(d, T, nchunks, st, ctx->at<float>(s.pprior), b_router_next, nullptr, nullptr, nullptr,
+                             nullptr, ctx->at<int32_t>(s.pred_local)));
+      ++ctx->launches;
+    }
   } else {
     // unfused (debug / k > 8): prior + SiLU activation, residual GEMM, warp top-k; writes logits
     const CUtensorMap* mw = ctx->maps.get(w_router_next, E, H, 64);
@@ -853,6 +895,7 @@ probe_status probe_set_option(probe_ctx ctx, int32_t option, int64_t value) {
   switch (option) {
     case PROBE_OPT_EP_EMULATION: ctx->ep_emulation = value != 0; return PROBE_OK;
     case PROBE_OPT_UNFUSED_TOPK: ctx->unfused = value != 0; return PROBE_OK;
+    case PROBE_OPT_FUSED_EPILOGUE_TOPK: ctx->fused_epi_topk = value != 0; return PROBE_OK;
   }
   return fail(ctx, PROBE_EINVAL, "unknown option %d", option);
 }

@@ -33,6 +33,7 @@ class CaseCfg:
     bias: bool = False
     sample_tokens: int = 0          # >0: oracle outputs only for this many tokens per rank
     ep_emulation: bool = False      # partitioned expert GEMMs (single-GPU EP straggler emulation)
+    fused_epi_topk: bool = False    # router/predictor top-k in the GEMM epilogue
 
 
 def f64(t):
@@ -64,6 +65,9 @@ def run_gpu(case: CaseCfg):
     if case.ep_emulation:
         from paper_2602_00509_b200._lib import OPT_EP_EMULATION
         rt.set_option(OPT_EP_EMULATION, 1)
+    if case.fused_epi_topk:
+        from paper_2602_00509_b200._lib import OPT_FUSED_EPILOGUE_TOPK
+        rt.set_option(OPT_FUSED_EPILOGUE_TOPK, 1)
     dev = "cuda"
     L0 = pi.layer_inputs(sh, case.step, 0, case.zipf_s, device=dev)
     L1 = pi.layer_inputs(sh, case.step, 1, case.zipf_s, device=dev)

@@ -26,6 +26,8 @@ CASES = {
     "bf16-out": CaseCfg(pi.C0.with_(name="bf", E=16, k=4, H=256, F=256, T=96, G=2), out_fp32=False),
     "no-residual": CaseCfg(pi.C0.with_(name="nr", E=16, k=2, H=256, F=128, T=64, G=2), residual=False),
     "budget0": CaseCfg(pi.C0, replica_budget=0),
+    "fused-epilogue-topk": CaseCfg(pi.C0.with_(name="fe", E=64, k=8, H=512, F=256, T=200, G=4), zipf_s=1.3,
+                                  fused_epi_topk=True, bias=True),
     "ep-emulation": CaseCfg(pi.C0.with_(name="epem", E=64, k=8, H=512, F=384, T=300, G=8), zipf_s=1.2,
                             ep_emulation=True),
 }
