@@ -149,19 +149,19 @@ __global__ void __launch_bounds__(128) k_topk(Dims d, int T, const float* __rest
 
 // =============================================================================
 // a1/a2 top-k, thread per token (high occupancy): the block's 128 logit rows are staged
-// in shared memory with coalesced loads (row r, column e at r·E + (e ^ (r & 31)) —
-// conflict-free for the row-wise reads), then each thread keeps a register list sorted
+// in shared memory with coalesced loads (row pitch E+1, odd: conflict-free for both the
+// column-wise staging and the row-wise reads), then each thread keeps a register list sorted
 // by (value ↓, id ↑) (R3, R4; KK compile-time so nothing spills).  Gate mode also writes
 // the softmax over the selected logits (R1) and the per-chunk dispatch ranks (the
 // expert bitmasks of k_rank); predictor mode accumulates n̂[rank][e] (R9).
-// grid (ceil(T/128), GL), block 128; dynamic smem 128·E·4 bytes.
+// grid (ceil(T/128), GL), block 128; dynamic smem 128·(E+1)·4 bytes.
 // =============================================================================
 template <int KK, bool PRED>
 __global__ void __launch_bounds__(128) k_select(Dims d, int T, const float* __restrict__ logits,
                                                 const float* __restrict__ bias, int32_t* __restrict__ ids,
                                                 float* __restrict__ gw, int32_t* __restrict__ pos,
                                                 int32_t* __restrict__ hist, int32_t* __restrict__ counts) {
-  extern __shared__ float lrow[];                  // [128][E] swizzled
+  extern __shared__ float lrow[];                  // [128][E+1]
   __shared__ uint32_t mask[kMaxE * 4];
   __shared__ int32_t scount[kMaxE];
   const int E = d.E;
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(128) k_select(Dims d, int T, const float* __re
     const int r = i / E, e = i % E;
     float v = src[i];
     if (bias) v += bias[e];
-    lrow[r * E + (e ^ (r & 31))] = v;
+    lrow[r * (E + 1) + e] = v;
   }
   __syncthreads();
   int te[KK];
@@ -184,10 +184,10 @@ __global__ void __launch_bounds__(128) k_select(Dims d, int T, const float* __re
     float tv[KK];
 #pragma unroll
     for (int j = 0; j < KK; ++j) { tv[j] = -INFINITY; te[j] = 0x7fffffff; }
-    const float* row = lrow + tl * E;
+    const float* row = lrow + tl * (E + 1);
 #pragma unroll 4
     for (int i = 0; i < E; ++i) {
-      float x = row[i ^ (tl & 31)];
+      float x = row[i];
       int e = i;
       if (x > tv[KK - 1]) {
 #pragma unroll
