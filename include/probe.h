@@ -220,7 +220,8 @@ probe_status probe_ipc_close(uint64_t dev_ptr_base);
  * GEMMs and warp-shuffle top-k kernels (debug reference path).  PROBE_OPT_FUSED_EPILOGUE_TOPK:
  * do the router/predictor top-k inside the tcgen05 GEMM epilogue instead of the
  * thread-per-token select kernel (default off: measured slower). */
-enum { PROBE_OPT_EP_EMULATION = 1, PROBE_OPT_UNFUSED_TOPK = 2, PROBE_OPT_FUSED_EPILOGUE_TOPK = 3 };
+enum { PROBE_OPT_EP_EMULATION = 1, PROBE_OPT_UNFUSED_TOPK = 2, PROBE_OPT_FUSED_EPILOGUE_TOPK = 3,
+       PROBE_OPT_AUX_SMS = 4 /* grid cap (CTAs) of the predictor GEMMs on the aux stream; default #SMs/2 */ };
 probe_status probe_set_option(probe_ctx ctx, int32_t option, int64_t value);
 
 /* Number of library kernel launches enqueued so far by this context (bench accounting). */

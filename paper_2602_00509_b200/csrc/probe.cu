@@ -168,6 +168,7 @@ struct probe_ctx_s {
   int last_fwd_parity = 0;
   int last_T = 0;
   int num_sms = 148;
+  int aux_sms = 74;   // grid cap for aux-stream (predictor) GEMMs: the main track keeps free SMs
   MapCache maps;
   CUtensorMap map_recv, map_act, map_rw13, map_rw2, map_y;
   std::string err;
@@ -403,6 +404,7 @@ probe_status probe_init(const probe_config* cfg, const uint64_t* peer_ptrs, void
   int dev = 0;
   if (e == cudaSuccess) e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  ctx->aux_sms = ctx->num_sms / 2;
   if (e == cudaSuccess) {
     const size_t plan_smem = static_cast<size_t>(G) * c.num_experts * G * 4;
     e = cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(plan_smem));
@@ -607,7 +609,7 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
       s1.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_SILU_BF16, d.h, d.h, ctx->scratch + s.pact);
       k_write_sched<<<1, 32, 0, st>>>(ctx->at<GemmSched>(s.s_p1), s1);
       CKL();
-      CK(launch_gemm_v(V_128_6_4, *mx, *m1, *m1, *mx, ctx->at<GemmSched>(s.s_p1), d.H, ctx->num_sms, st));
+      CK(launch_gemm_v(V_128_6_4, *mx, *m1, *m1, *mx, ctx->at<GemmSched>(s.s_p1), d.H, ctx->aux_sms, st));
       ++ctx->launches;
     }
     if (!mw) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
@@ -626,7 +628,7 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
     k_write_sched<<<1, 32, 0, st>>>(ctx->at<GemmSched>(s.s_p2), s2);
     CKL();
     CK(launch_gemm_v(BN == 128 ? V_128_6_4 : V_256_4_4, *mx, *mw, w_res1 ? *m2 : *mw, *mx, ctx->at<GemmSched>(s.s_p2),
-                     d.H, ctx->num_sms, st, w_res1 ? ma : nullptr, w_res1 ? d.h : 0));
+                     d.H, ctx->aux_sms, st, w_res1 ? ma : nullptr, w_res1 ? d.h : 0));
     ++ctx->launches;
     if (!ctx->fused_epi_topk) {
       CK(launch_select<true>(d, T, nchunks, st, ctx->at<float>(s.pprior), b_router_next, nullptr, nullptr, nullptr,
@@ -645,7 +647,7 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
     if (w_res1) sg.g[1] = mk_group(0, static_cast<int>(GL * T), 0, 1, EPI_SILU_BF16, d.h, d.h, ctx->scratch + s.pact);
     k_write_sched<<<1, 32, 0, st>>>(ctx->at<GemmSched>(s.s_p1), sg);
     CKL();
-    CK(launch_gemm_v(V_128_6_4, *mx, *mw, *m1, *mx, ctx->at<GemmSched>(s.s_p1), d.H, ctx->num_sms, st));
+    CK(launch_gemm_v(V_128_6_4, *mx, *mw, *m1, *mx, ctx->at<GemmSched>(s.s_p1), d.H, ctx->aux_sms, st));
     ++ctx->launches;
     if (w_res1) {
       const CUtensorMap* ma = ctx->maps.get(ctx->scratch + s.pact, GL * T, h, 128);
@@ -657,7 +659,7 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
       s2.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_F32, d.E, d.E, ctx->at<float>(s.pres));
       k_write_sched<<<1, 32, 0, st>>>(ctx->at<GemmSched>(s.s_p2), s2);
       CKL();
-      CK(launch_gemm_v(V_128_6_4, *ma, *m2, *m2, *ma, ctx->at<GemmSched>(s.s_p2), d.h, ctx->num_sms, st));
+      CK(launch_gemm_v(V_128_6_4, *ma, *m2, *m2, *ma, ctx->at<GemmSched>(s.s_p2), d.h, ctx->aux_sms, st));
       ++ctx->launches;
     }
     launch_topk<true>(d, T, nchunks, st, ctx->at<float>(s.pprior), w_res1 ? ctx->at<float>(s.pres) : nullptr,
@@ -896,6 +898,10 @@ probe_status probe_set_option(probe_ctx ctx, int32_t option, int64_t value) {
     case PROBE_OPT_EP_EMULATION: ctx->ep_emulation = value != 0; return PROBE_OK;
     case PROBE_OPT_UNFUSED_TOPK: ctx->unfused = value != 0; return PROBE_OK;
     case PROBE_OPT_FUSED_EPILOGUE_TOPK: ctx->fused_epi_topk = value != 0; return PROBE_OK;
+    case PROBE_OPT_AUX_SMS:
+      if (value < 1 || value > ctx->num_sms) return fail(ctx, PROBE_EINVAL, "aux SM cap %lld out of range", (long long)value);
+      ctx->aux_sms = static_cast<int>(value);
+      return PROBE_OK;
   }
   return fail(ctx, PROBE_EINVAL, "unknown option %d", option);
 }
