@@ -226,6 +226,11 @@ def run_probe(args):
         step(L, use_plan=False)
         L += 1
     ms_static, L = timed(args.steps, L, use_plan=False)
+    rt.profile(args.steps)
+    _, L = timed(args.steps, L, use_plan=False)
+    phs = rt.profile_read()
+    static_phases = {n: float(phs[:, i].mean()) for i, n in enumerate(PHASES)}
+    rt.profile(0)
     # ---- single-GPU EP straggler emulation: expert GEMMs partitioned by logical rank
     #      (~#SMs/G SMs per rank ⇒ GEMM time = the straggler's, Eq. 3); static EP vs PROBE
     ep_em = None
@@ -307,7 +312,8 @@ def run_probe(args):
             "gpu_launches": launches,
             "clocks": clocks,
             "phases_ms": phases,
-            "static_ep": {"ms_per_step": ms_static, "speedup_probe_vs_static": ms_static / ms},
+            "static_ep": {"ms_per_step": ms_static, "speedup_probe_vs_static": ms_static / ms,
+                          "phases_ms": static_phases},
             "ep_emulation": ep_em,
             "balance": {"ir_pre": ir_pre, "ir_post": ir_post, "replicas": nrep},
             "setup_s": gen_s,

@@ -168,7 +168,8 @@ probe_status probe_test_gemm(const void* A, int64_t a_rows, const void* B, int64
                              int32_t mode, void* C, void* stream);
 
 /* Timing hook: as probe_test_gemm with an explicit kernel variant (-1 = default for
- * `mode`; 0: BN=128/6 stages/4 epilogue warps, 1: 256/4/4, 2: 256/3/8, 3: 128/4/8),
+ * `mode`; 0: BN=128/6 stages/4 epilogue warps, 1: 256/4/4, 2: 256/3/8, 3: 128/4/8,
+ * 4: 256/3/4 with 2 staging tiles per epilogue warp, 5: 256/3/4 with 4),
  * run once, then `reps` times between CUDA events on `stream`; *ms_out = mean ms. */
 probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int64_t b_rows,
                               int32_t K, int32_t N, const int32_t* groups, int32_t num_groups,
@@ -187,16 +188,17 @@ probe_status probe_finalize(probe_ctx ctx);
  * recorded forward into ms[n][PROBE_NPHASE] (synchronises) and returns how many
  * forwards were recorded in *n_out.  Phases of the main track: */
 enum {
-  PROBE_PH_GATE = 0,      /* router GEMM + top-k (a1) */
-  PROBE_PH_COUNTS = 1,    /* chunk scan + actual-count all-gather (a3) */
-  PROBE_PH_LAYOUT = 2,    /* materialize plan + layout + GEMM schedules (a5) */
-  PROBE_PH_DISPATCH = 3,  /* token dispatch (a6) */
-  PROBE_PH_WAIT = 4,      /* exposed wait for replica slots (prefetch not hidden, R28) */
-  PROBE_PH_GEMM1 = 5,     /* grouped GEMM1 + SwiGLU epilogue (a7) */
-  PROBE_PH_GEMM2 = 6,     /* grouped GEMM2 (a7) */
-  PROBE_PH_COMBINE = 7,   /* gate-weighted combine (a8) */
-  PROBE_PH_TOTAL = 8,     /* whole forward on the main stream */
-  PROBE_NPHASE = 9
+  PROBE_PH_GATE = 0,      /* router GEMM (a1) */
+  PROBE_PH_SELECT = 1,    /* top-k select + softmax + dispatch ranks (a1) */
+  PROBE_PH_COUNTS = 2,    /* chunk scan + actual-count all-gather (a3) */
+  PROBE_PH_LAYOUT = 3,    /* materialize plan + layout + GEMM schedules (a5) */
+  PROBE_PH_DISPATCH = 4,  /* token dispatch (a6) */
+  PROBE_PH_WAIT = 5,      /* exposed wait for replica slots (prefetch not hidden, R28) */
+  PROBE_PH_GEMM1 = 6,     /* grouped GEMM1 + SwiGLU epilogue (a7) */
+  PROBE_PH_GEMM2 = 7,     /* grouped GEMM2 (a7) */
+  PROBE_PH_COMBINE = 8,   /* gate-weighted combine (a8) */
+  PROBE_PH_TOTAL = 9,     /* whole forward on the main stream */
+  PROBE_NPHASE = 10
 };
 probe_status probe_profile(probe_ctx ctx, int32_t n);
 probe_status probe_profile_read(probe_ctx ctx, float* ms, int32_t* n_out);

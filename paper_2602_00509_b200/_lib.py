@@ -24,8 +24,8 @@ EXPORTS = ["probe_workspace", "probe_init", "probe_moe_forward", "probe_predict"
            "probe_finalize", "probe_launch_count", "probe_profile", "probe_profile_read", "probe_bench_gemm",
            "probe_ipc_export", "probe_ipc_import", "probe_ipc_close", "probe_set_option"]
 OPT_EP_EMULATION, OPT_UNFUSED_TOPK, OPT_FUSED_EPILOGUE_TOPK, OPT_AUX_SMS = 1, 2, 3, 4
-PROBE_NPHASE = 9
-PHASES = ["gate", "counts", "layout", "dispatch", "wait", "gemm1", "gemm2", "combine", "total"]
+PROBE_NPHASE = 10
+PHASES = ["gate", "select", "counts", "layout", "dispatch", "wait", "gemm1", "gemm2", "combine", "total"]
 
 
 class probe_config(C.Structure):

@@ -105,7 +105,7 @@ __device__ inline void gemm_finalize_sched(GemmSched* s, int BN) {
   s->total_tiles = acc;
 }
 
-template <int BN, int STAGES, int EW = 4>
+template <int BN, int STAGES, int EW = 4, int NBUF = (EW == 8 ? 2 : 1)>
 struct GemmSmem {
   static constexpr int A_BYTES = 128 * 128;
   static constexpr int B_BYTES = BN * 128;
@@ -114,7 +114,7 @@ struct GemmSmem {
   static constexpr int EPI_OFF = (TS_OFF + (kMaxGroups + 1) * 4 + 1023) / 1024 * 1024;
   // per epilogue warp: NB staging tiles of 32 rows × 128 B, 16-byte chunks XOR-swizzled by
   // (row mod 8) = the TMA SWIZZLE_128B layout (also bank-conflict-free for the manual path)
-  static constexpr int NB = (EW == 8) ? 2 : 1;
+  static constexpr int NB = NBUF;
   static constexpr int EPI_STRIDE = NB * 4096;
   static constexpr int BYTES = EPI_OFF + EW * EPI_STRIDE + 1024;                // + alignment slack
 };
@@ -269,12 +269,12 @@ __device__ __forceinline__ void epi_topk(uint32_t tb, int lane, const GemmGroup&
 
 // EW epilogue warps (4 or 8): warp 4+i reads TMEM lane quarter i%4 and handles the
 // column chunks c ≡ i/4 (mod EW/4).  Threads = 128 + 32·EW.
-template <int BN, int STAGES, int EW = 4>
+template <int BN, int STAGES, int EW = 4, int NBUF = (EW == 8 ? 2 : 1)>
 __global__ void __launch_bounds__(128 + 32 * EW, 1)
 grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
                     const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmC,
                     const __grid_constant__ CUtensorMap tmA2, GemmSched* __restrict__ sched, int K, int K2) {
-  using L = GemmSmem<BN, STAGES, EW>;
+  using L = GemmSmem<BN, STAGES, EW, NBUF>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;

@@ -218,20 +218,21 @@ probe_status fail(probe_ctx ctx, probe_status st, const char* fmt, ...) {
 
 // GEMM variants: (BN, STAGES, epilogue warps).  V_GATE: logits/predictor (N ≤ 256),
 // V_SWIGLU: expert GEMM1 (bf16 act out), V_F32: expert GEMM2 (fp32 Y out, epilogue-heavy).
-enum GemmVariant { V_128_6_4 = 0, V_256_4_4 = 1, V_256_3_8 = 2, V_128_4_8 = 3 };
+enum GemmVariant { V_128_6_4 = 0, V_256_4_4 = 1, V_256_3_8 = 2, V_128_4_8 = 3, V_256_3_4_NB2 = 4, V_256_3_4_NB4 = 5 };
 
-template <int BN, int ST, int EW>
+template <int BN, int ST, int EW, int NB = (EW == 8 ? 2 : 1)>
 cudaError_t launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, const CUtensorMap& c,
                           const CUtensorMap& a2, GemmSched* s, int K, int K2, int grid, cudaStream_t st) {
-  using L = GemmSmem<BN, ST, EW>;
+  using L = GemmSmem<BN, ST, EW, NB>;
+  static_assert(L::BYTES <= 232448, "shared memory budget");
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(grouped_gemm_kernel<BN, ST, EW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         L::BYTES);
+    cudaError_t e = cudaFuncSetAttribute(grouped_gemm_kernel<BN, ST, EW, NB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  grouped_gemm_kernel<BN, ST, EW><<<grid, 128 + 32 * EW, L::BYTES, st>>>(a, b0, b1, c, a2, s, K, K2);
+  grouped_gemm_kernel<BN, ST, EW, NB><<<grid, 128 + 32 * EW, L::BYTES, st>>>(a, b0, b1, c, a2, s, K, K2);
   return cudaGetLastError();
 }
 
@@ -244,6 +245,8 @@ cudaError_t launch_gemm_v(int v, const CUtensorMap& a, const CUtensorMap& b0, co
     case V_256_4_4: return launch_gemm_t<256, 4, 4>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_256_3_8: return launch_gemm_t<256, 3, 8>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_128_4_8: return launch_gemm_t<128, 4, 8>(a, b0, b1, c, A2, s, K, K2, grid, st);
+    case V_256_3_4_NB2: return launch_gemm_t<256, 3, 4, 2>(a, b0, b1, c, A2, s, K, K2, grid, st);
+    case V_256_3_4_NB4: return launch_gemm_t<256, 3, 4, 4>(a, b0, b1, c, A2, s, K, K2, grid, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -485,6 +488,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   CK(launch_gemm_v(sg.BN == 128 ? V_128_6_4 : V_256_4_4, *mx, *mr, *mr, *mx, ctx->at<GemmSched>(s.s_gate), d.H,
                    ctx->num_sms, st));
   ++ctx->launches;
+  MARK(1);
   if (fused_gate) {
     k_rank<<<dim3(nchunks, d.GL), 128, 0, st>>>(d, T, ctx->at<int32_t>(s.ids), ctx->at<int32_t>(s.pos),
                                                 ctx->at<int32_t>(s.hist));
@@ -497,7 +501,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   }
   CKL();
   CK(cudaEventRecord(ctx->ev_gate[p], st));
-  MARK(1);
+  MARK(2);
   // a3 actual-count all-gather (board kind 0, parity p)
   k_count_scan<<<d.GL, 256, 0, st>>>(d, nchunks, ctx->at<int32_t>(s.hist), ctx->at<int32_t>(s.cbase), sym_of(ctx),
                                      PROBE_BUF_BOARD, p);
@@ -505,7 +509,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   CK(xbarrier(ctx, BAR_COUNTS, st));            // every rank's counts are on every board
   // a5 materialize plan(L) + layout
   if (use_plan) CK(cudaStreamWaitEvent(st, ctx->ev_plan[p], 0));
-  MARK(2);
+  MARK(3);
   LayoutIn li;
   li.board_actual = reinterpret_cast<const int32_t*>(ctx->local_base[PROBE_BUF_BOARD]) + ((p * 2 + 0) * d.G) * d.E;
   li.quota = use_plan ? ctx->at<int32_t>(s.quota[p]) : nullptr;
@@ -525,7 +529,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   lo.err = err;
   k_layout<<<1, 512, static_cast<size_t>(d.G) * d.E * d.G * 4, st>>>(d, li, lo);
   CKL();
-  MARK(3);
+  MARK(4);
   // a6 dispatch
   {
     const int warps = d.GL * T;
@@ -535,20 +539,20 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
                                                 sym_of(ctx), PROBE_BUF_RECV, err);
     CKL();
   }
-  MARK(4);
+  MARK(5);
   CK(xbarrier(ctx, BAR_DISPATCH, st));          // every peer's rows have landed in our receive buffers
   // a9 phase lock: the expert GEMMs need this layer's replica slots
   if (use_plan) CK(cudaStreamWaitEvent(st, ctx->ev_slots[p], 0));
-  MARK(5);
+  MARK(6);
   CK(cudaEventRecord(ctx->ev_gemm[p], st));
   // a7 grouped SwiGLU expert FFN (tcgen05): act = SiLU(X W_gᵀ) ⊙ X W_uᵀ ; Y = act W_dᵀ
   CK(launch_gemm_v(V_256_4_4, ctx->map_recv, *m13, ctx->map_rw13, ctx->map_recv, lo.s1, d.H, ctx->num_sms, st));
   ++ctx->launches;
-  MARK(6);
+  MARK(7);
   CK(launch_gemm_v(V_256_4_4, ctx->map_act, *m2, ctx->map_rw2, ctx->map_y, lo.s2, d.F, ctx->num_sms, st));
   ++ctx->launches;
   CK(xbarrier(ctx, BAR_Y, st));                 // every expert rank's Y rows are complete
-  MARK(7);
+  MARK(8);
   // a8 combine (raises the prefetch suspend flag, R27)
   if (out_fp32)
     k_combine<true><<<d.GL * T, 128, 0, st>>>(d, T, ctx->at<float>(s.gw), ctx->at<int32_t>(s.route), sym_of(ctx),
@@ -558,7 +562,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
                                                PROBE_BUF_Y, out, suspend, layer);
   CKL();
   CK(cudaEventRecord(ctx->ev_comb[p], st));
-  MARK(8);
+  MARK(9);
   if (prof) ++ctx->prof_n;
 #undef MARK
   if (topk_ids) CK(cudaMemcpyAsync(topk_ids, ctx->at<int32_t>(s.ids), GL * T * d.k * 4, cudaMemcpyDeviceToDevice, st));
@@ -778,7 +782,7 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
     return fail(nullptr, PROBE_EINVAL, "probe_test_gemm: bad arguments");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (variant < 0) variant = mode == 1 ? V_256_4_4 : (mode == 2 ? V_256_3_8 : V_128_6_4);
-  if (variant > V_128_4_8) return fail(nullptr, PROBE_EINVAL, "bad variant");
+  if (variant > V_256_3_4_NB4) return fail(nullptr, PROBE_EINVAL, "bad variant");
   const int BN = variant_bn(variant);
   const int emode = mode == 1 ? EPI_SWIGLU
                     : mode == 3 ? EPI_SILU_BF16
@@ -960,7 +964,7 @@ probe_status probe_profile_read(probe_ctx ctx, float* ms, int32_t* n_out) {
   for (int i = 0; i < ctx->prof_n; ++i) {
     cudaEvent_t* ev = &ctx->prof_ev[static_cast<size_t>(i) * (PROBE_NPHASE + 1)];
     // phase j spans marks j..j+1; TOTAL spans 0..8
-    const int order[PROBE_NPHASE][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {4, 5}, {5, 6}, {6, 7}, {7, 8}, {0, 8}};
+    const int order[PROBE_NPHASE][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {4, 5}, {5, 6}, {6, 7}, {7, 8}, {8, 9}, {0, 9}};
     for (int j = 0; j < PROBE_NPHASE; ++j) {
       float t = 0.f;
       CK(cudaEventElapsedTime(&t, ev[order[j][0]], ev[order[j][1]]));
