@@ -148,60 +148,69 @@ __global__ void __launch_bounds__(128) k_topk(Dims d, int T, const float* __rest
 }
 
 // =============================================================================
-// a1/a2 top-k, thread per token (high occupancy): the block's 128 logit rows are staged
-// in shared memory with coalesced loads (row pitch E+1, odd: conflict-free for both the
-// column-wise staging and the row-wise reads), then each thread keeps a register list sorted
-// by (value ↓, id ↑) (R3, R4; KK compile-time so nothing spills).  Gate mode also writes
-// the softmax over the selected logits (R1) and the per-chunk dispatch ranks (the
-// expert bitmasks of k_rank); predictor mode accumulates n̂[rank][e] (R9).
-// grid (ceil(T/128), GL), block 128; dynamic smem 128·(E+1)·4 bytes.
+// a1/a2 top-k, thread per token (high occupancy): each thread streams its logit row
+// with 16-byte loads, 32 values at a time in registers (L1 absorbs the line reuse), and
+// keeps a register list sorted by (value ↓, id ↑) (R3, R4; KK compile-time, no local
+// memory).  Gate mode also writes the softmax over the selected logits (R1) and the
+// per-chunk dispatch ranks (expert bitmasks as in k_rank); predictor mode accumulates
+// n̂[rank][e] (R9).  grid (ceil(T/128), GL), block 128 (thread = token).  E % 32 == 0
+// or E < 32 handled by masking.
 // =============================================================================
 template <int KK, bool PRED>
 __global__ void __launch_bounds__(128) k_select(Dims d, int T, const float* __restrict__ logits,
                                                 const float* __restrict__ bias, int32_t* __restrict__ ids,
                                                 float* __restrict__ gw, int32_t* __restrict__ pos,
                                                 int32_t* __restrict__ hist, int32_t* __restrict__ counts) {
-  extern __shared__ float lrow[];                  // [128][E+1]
   __shared__ uint32_t mask[kMaxE * 4];
   __shared__ int32_t scount[kMaxE];
   const int E = d.E;
   const int chunk = blockIdx.x, gl = blockIdx.y, nchunks = gridDim.x;
-  const int tl = threadIdx.x, t0 = chunk * kChunk;
-  const int nt = min(kChunk, T - t0);
+  const int tl = threadIdx.x, t = chunk * kChunk + tl;
   for (int i = tl; i < E * 4; i += blockDim.x) mask[i] = 0u;
   for (int i = tl; i < E; i += blockDim.x) scount[i] = 0;
-  // coalesced staging: consecutive threads read consecutive columns
-  const float* src = logits + (static_cast<size_t>(gl) * T + t0) * E;
-  for (int i = tl; i < nt * E; i += blockDim.x) {
-    const int r = i / E, e = i % E;
-    float v = src[i];
-    if (bias) v += bias[e];
-    lrow[r * (E + 1) + e] = v;
-  }
   __syncthreads();
   int te[KK];
-  if (tl < nt) {
+  if (t < T) {
     float tv[KK];
 #pragma unroll
     for (int j = 0; j < KK; ++j) { tv[j] = -INFINITY; te[j] = 0x7fffffff; }
-    const float* row = lrow + tl * (E + 1);
-#pragma unroll 4
-    for (int i = 0; i < E; ++i) {
-      float x = row[i];
-      int e = i;
-      if (x > tv[KK - 1]) {
+    const float* row = logits + (static_cast<size_t>(gl) * T + t) * E;
+#pragma unroll 1
+    for (int c = 0; c < E; c += 32) {
+      float v[32];
 #pragma unroll
-        for (int j = 0; j < KK; ++j) {
-          if (x > tv[j] || (x == tv[j] && e < te[j])) {
-            const float ov = tv[j];
-            const int oe = te[j];
-            tv[j] = x; te[j] = e;
-            x = ov; e = oe;
+      for (int q = 0; q < 8; ++q) {
+        if (c + 4 * q + 3 < E) {
+          const float4 f = __ldg(reinterpret_cast<const float4*>(row + c) + q);
+          v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) v[4 * q + u] = (c + 4 * q + u < E) ? row[c + 4 * q + u] : -INFINITY;
+        }
+      }
+      if (bias) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (c + i < E) v[i] += __ldg(bias + c + i);
+      }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        float x = v[i];
+        int e = c + i;
+        if (x > tv[KK - 1]) {
+#pragma unroll
+          for (int j = 0; j < KK; ++j) {
+            if (x > tv[j] || (x == tv[j] && e < te[j])) {
+              const float ov = tv[j];
+              const int oe = te[j];
+              tv[j] = x; te[j] = e;
+              x = ov; e = oe;
+            }
           }
         }
       }
     }
-    const size_t o = (static_cast<size_t>(gl) * T + t0 + tl) * KK;
+    const size_t o = (static_cast<size_t>(gl) * T + t) * KK;
     if (!PRED) {
       float w[KK], sum = 0.f;
 #pragma unroll
@@ -230,9 +239,9 @@ __global__ void __launch_bounds__(128) k_select(Dims d, int T, const float* __re
     const uint32_t* m = &mask[e * 4];
     hist[(static_cast<size_t>(gl) * nchunks + chunk) * E + e] = __popc(m[0]) + __popc(m[1]) + __popc(m[2]) + __popc(m[3]);
   }
-  if (tl < nt) {
+  if (t < T) {
     const int w = tl >> 5, b = tl & 31;
-    const size_t o = (static_cast<size_t>(gl) * T + t0 + tl) * KK;
+    const size_t o = (static_cast<size_t>(gl) * T + t) * KK;
 #pragma unroll
     for (int j = 0; j < KK; ++j) {
       const uint32_t* m = &mask[te[j] * 4];

@@ -261,17 +261,10 @@ cudaError_t launch_gemm(const CUtensorMap& a, const CUtensorMap& b0, const CUten
 template <bool PRED>
 cudaError_t launch_select(const Dims& d, int T, int nchunks, cudaStream_t st, const float* lg, const float* b,
                           int32_t* ids, float* gw, int32_t* pos, int32_t* hist, int32_t* cnt) {
-  const size_t smem = static_cast<size_t>(kChunk) * (d.E + 1) * 4;
+  const size_t smem = 0;
   dim3 grid(nchunks, d.GL);
 #define SEL(KK)                                                                                         \
   case KK: {                                                                                            \
-    static bool a = false;                                                                              \
-    if (!a) {                                                                                           \
-      cudaError_t e = cudaFuncSetAttribute(k_select<KK, PRED>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                           128 * (kMaxE + 1) * 4);                                      \
-      if (e != cudaSuccess) return e;                                                                   \
-      a = true;                                                                                         \
-    }                                                                                                   \
     k_select<KK, PRED><<<grid, 128, smem, st>>>(d, T, lg, b, ids, gw, pos, hist, cnt);                 \
     break;                                                                                              \
   }
