@@ -269,26 +269,40 @@ def run_probe(args):
         e2e = {"value": ms_e2e if shape.name != "C2" else G * T / (ms_e2e / 1e3), "unit": "ms" if shape.name != "C2" else "tokens/s",
                "h2d_bytes_per_step": bi * world, "d2h_bytes_per_step": bo * world}
     rt.check()
-    # ---- roofline: the dominant kernel is grouped GEMM1 (4HF FLOPs per routed pair)
+    # ---- roofline: the dominant kernel is grouped GEMM1 (4HF FLOPs per routed pair).  Its
+    #      algorithmic bytes are the weights of every active (expert, rank) slot + the rows
+    #      read and the activations written; the bound is whichever roof is higher.
     pairs = G * T * shape.k
     fl1 = 4.0 * H * shape.F * pairs / world
     fl2 = 2.0 * H * shape.F * pairs / world
+    active = int((sp.sum(axis=0) > 0).sum())            # (expert, dest) slots with rows
+    by1 = (active * 2 * shape.F * H * 2 + pairs * (H * 2 + shape.F * 2)) / world
+    by2 = (active * H * shape.F * 2 + pairs * (shape.F * 2 + H * 4)) / world
     t1 = phases["gemm1"] / 1e3
     t2 = phases["gemm2"] / 1e3
     peak_tf = pk["bf16_tflops_sustained"]
+    peak_bw = pk["hbm_gbs"]
+    hbm_bound = by1 / (peak_bw * 1e9) > fl1 / (peak_tf * 1e12)
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "gemm1_traffic.json")
     if os.path.exists(tfile):
         tj = json.load(open(tfile))
         if tj.get("config") == shape.name:
             traffic = tj.get("dram_bytes_per_launch")
-    roof = {"kernel": "grouped_gemm_kernel<256,4> (expert GEMM1 + SwiGLU)", "bound": "tensor",
-            "achieved": fl1 / t1 / 1e12, "peak": peak_tf, "unit": "TFLOP/s", "frac": fl1 / t1 / 1e12 / peak_tf,
-            "traffic": traffic, "peak_kind": f"{pk_kind} bf16_tflops_sustained",
-            "algorithmic_flops_per_launch": fl1,
-            "gemm2": {"achieved": fl2 / t2 / 1e12, "frac": fl2 / t2 / 1e12 / peak_tf},
-            "expert_ffn": {"achieved": (fl1 + fl2) / (t1 + t2) / 1e12,
-                           "frac": (fl1 + fl2) / (t1 + t2) / 1e12 / peak_tf}}
+    if hbm_bound:
+        roof = {"kernel": "grouped_gemm_kernel<256,4,4> (expert GEMM1 + SwiGLU)", "bound": "hbm",
+                "achieved": by1 / t1 / 1e9, "peak": peak_bw, "unit": "GB/s", "frac": by1 / t1 / 1e9 / peak_bw,
+                "traffic": traffic, "peak_kind": f"{pk_kind} hbm_gbs", "algorithmic_bytes_per_launch": by1,
+                "gemm2": {"achieved": by2 / t2 / 1e9, "frac": by2 / t2 / 1e9 / peak_bw},
+                "tensor_frac": fl1 / t1 / 1e12 / peak_tf}
+    else:
+        roof = {"kernel": "grouped_gemm_kernel<256,4,4> (expert GEMM1 + SwiGLU)", "bound": "tensor",
+                "achieved": fl1 / t1 / 1e12, "peak": peak_tf, "unit": "TFLOP/s", "frac": fl1 / t1 / 1e12 / peak_tf,
+                "traffic": traffic, "peak_kind": f"{pk_kind} bf16_tflops_sustained",
+                "algorithmic_flops_per_launch": fl1, "algorithmic_bytes_per_launch": by1,
+                "gemm2": {"achieved": fl2 / t2 / 1e12, "frac": fl2 / t2 / 1e12 / peak_tf},
+                "expert_ffn": {"achieved": (fl1 + fl2) / (t1 + t2) / 1e12,
+                               "frac": (fl1 + fl2) / (t1 + t2) / 1e12 / peak_tf}}
     result = None
     if rank == 0:
         cpu = None if args.no_cpu else cpu_baseline(shape, args, sample_tokens=args.cpu_tokens)
