@@ -163,6 +163,8 @@ struct probe_ctx_s {
   uint64_t sym_bytes[PROBE_NBUF];
   cudaStream_t aux = nullptr, pf = nullptr;
   cudaEvent_t ev_gate[2], ev_gemm[2], ev_comb[2], ev_pred[2], ev_plan[2], ev_slots[2];
+  // CUDA-graph awareness: id of the stream capture each event was last recorded in (0 = eager)
+  std::vector<std::pair<cudaEvent_t, unsigned long long>> ev_cap;
   int fwd_layer = -1000, pred_layer[2] = {-1000, -1000}, plan_layer[2] = {-1000, -1000},
       pf_layer[2] = {-1000, -1000};
   int last_fwd_parity = 0;
@@ -295,6 +297,37 @@ GemmGroup mk_group(int a_row, int m, int b_row, int b_sel, int mode, int n, int 
 }
 
 Sym sym_of(probe_ctx ctx) { return Sym{ctx->at<const uint64_t>(ctx->sl.sym)}; }
+
+unsigned long long capture_id(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  unsigned long long id = 0;
+  if (cudaStreamGetCaptureInfo(st, &cs, &id) != cudaSuccess) return 0;
+  return cs == cudaStreamCaptureStatusActive ? id : 0;
+}
+
+cudaError_t ev_record(probe_ctx ctx, cudaEvent_t ev, cudaStream_t st) {
+  cudaError_t e = cudaEventRecord(ev, st);
+  const unsigned long long id = capture_id(st);
+  for (auto& pr : ctx->ev_cap)
+    if (pr.first == ev) { pr.second = id; return e; }
+  ctx->ev_cap.emplace_back(ev, id);
+  return e;
+}
+
+// A capturing stream never waits on an event recorded outside its own capture (illegal in
+// a graph; the contract is that eager work is complete before capture begins).  A
+// non-capturing stream waiting on a captured event is how the aux / prefetch streams fork
+// into the graph.
+cudaError_t ev_wait(probe_ctx ctx, cudaStream_t st, cudaEvent_t ev) {
+  const unsigned long long cur = capture_id(st);
+  if (cur != 0) {
+    unsigned long long evid = 0;
+    for (auto& pr : ctx->ev_cap)
+      if (pr.first == ev) evid = pr.second;
+    if (evid != cur) return cudaSuccess;
+  }
+  return cudaStreamWaitEvent(st, ev, 0);
+}
 
 enum { BAR_COUNTS = 0, BAR_DISPATCH = 1, BAR_Y = 2, BAR_PRED = 3, BAR_PREFETCH = 4 };
 
@@ -493,7 +526,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
                        ctx->at<float>(s.gw), ctx->at<int32_t>(s.pos), ctx->at<int32_t>(s.hist), nullptr, nullptr);
   }
   CKL();
-  CK(cudaEventRecord(ctx->ev_gate[p], st));
+  CK(ev_record(ctx, ctx->ev_gate[p], st));
   MARK(2);
   // a3 actual-count all-gather (board kind 0, parity p)
   k_count_scan<<<d.GL, 256, 0, st>>>(d, nchunks, ctx->at<int32_t>(s.hist), ctx->at<int32_t>(s.cbase), sym_of(ctx),
@@ -501,7 +534,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   CKL();
   CK(xbarrier(ctx, BAR_COUNTS, st));            // every rank's counts are on every board
   // a5 materialize plan(L) + layout
-  if (use_plan) CK(cudaStreamWaitEvent(st, ctx->ev_plan[p], 0));
+  if (use_plan) CK(ev_wait(ctx, st, ctx->ev_plan[p]));
   MARK(3);
   LayoutIn li;
   li.board_actual = reinterpret_cast<const int32_t*>(ctx->local_base[PROBE_BUF_BOARD]) + ((p * 2 + 0) * d.G) * d.E;
@@ -535,9 +568,9 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   MARK(5);
   CK(xbarrier(ctx, BAR_DISPATCH, st));          // every peer's rows have landed in our receive buffers
   // a9 phase lock: the expert GEMMs need this layer's replica slots
-  if (use_plan) CK(cudaStreamWaitEvent(st, ctx->ev_slots[p], 0));
+  if (use_plan) CK(ev_wait(ctx, st, ctx->ev_slots[p]));
   MARK(6);
-  CK(cudaEventRecord(ctx->ev_gemm[p], st));
+  CK(ev_record(ctx, ctx->ev_gemm[p], st));
   // a7 grouped SwiGLU expert FFN (tcgen05): act = SiLU(X W_gᵀ) ⊙ X W_uᵀ ; Y = act W_dᵀ
   CK(launch_gemm_v(V_256_4_4, ctx->map_recv, *m13, ctx->map_rw13, ctx->map_recv, lo.s1, d.H, ctx->num_sms, st));
   ++ctx->launches;
@@ -554,7 +587,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
     k_combine<false><<<d.GL * T, 128, 0, st>>>(d, T, ctx->at<float>(s.gw), ctx->at<int32_t>(s.route), sym_of(ctx),
                                                PROBE_BUF_Y, out, suspend, layer);
   CKL();
-  CK(cudaEventRecord(ctx->ev_comb[p], st));
+  CK(ev_record(ctx, ctx->ev_comb[p], st));
   MARK(9);
   if (prof) ++ctx->prof_n;
 #undef MARK
@@ -579,7 +612,7 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
   d.T = T;
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->aux;
   const int pp = next_layer & 1, prev = (next_layer - 1) & 1;
-  if (ctx->fwd_layer == next_layer - 1) CK(cudaStreamWaitEvent(st, ctx->ev_gate[prev], 0));
+  if (ctx->fwd_layer == next_layer - 1) CK(ev_wait(ctx, st, ctx->ev_gate[prev]));
   const uint64_t GL = d.GL, H = d.H, E = d.E, h = d.h;
   const Scratch& s = ctx->sl;
   const CUtensorMap* mx = ctx->maps.get(x, GL * T, H, 128);
@@ -670,7 +703,7 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
     const int32_t* board = reinterpret_cast<const int32_t*>(ctx->local_base[PROBE_BUF_BOARD]) + ((pp * 2 + 1) * d.G) * d.E;
     CK(cudaMemcpyAsync(pred_counts, board, static_cast<size_t>(d.G) * d.E * 4, cudaMemcpyDeviceToDevice, st));
   }
-  CK(cudaEventRecord(ctx->ev_pred[pp], st));
+  CK(ev_record(ctx, ctx->ev_pred[pp], st));
   ctx->pred_layer[pp] = next_layer;
   return PROBE_OK;
 }
@@ -686,7 +719,7 @@ probe_status probe_plan(probe_ctx ctx, int32_t next_layer, const int32_t* pred_c
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->aux;
   const Dims& d = ctx->d;
   const Scratch& s = ctx->sl;
-  if (!pred_counts) CK(cudaStreamWaitEvent(st, ctx->ev_pred[pp], 0));
+  if (!pred_counts) CK(ev_wait(ctx, st, ctx->ev_pred[pp]));
   const int32_t* nh = pred_counts ? pred_counts
                                   : reinterpret_cast<const int32_t*>(ctx->local_base[PROBE_BUF_BOARD]) + ((pp * 2 + 1) * d.G) * d.E;
   PlanParams pr{ctx->cfg.alpha_ps, ctx->cfg.beta_ps, ctx->cfg.bw_bytes_per_us, ctx->cfg.expert_bytes,
@@ -698,7 +731,7 @@ probe_status probe_plan(probe_ctx ctx, int32_t next_layer, const int32_t* pred_c
   if (replicas) CK(cudaMemcpyAsync(replicas, ctx->at<int32_t>(s.reps[pp]), d.G * kMaxRb * 4, cudaMemcpyDeviceToDevice, st));
   if (quota) CK(cudaMemcpyAsync(quota, ctx->at<int32_t>(s.quota[pp]), smem, cudaMemcpyDeviceToDevice, st));
   if (plan_stats) CK(cudaMemcpyAsync(plan_stats, ctx->at<int64_t>(s.stats[pp]), 64, cudaMemcpyDeviceToDevice, st));
-  CK(cudaEventRecord(ctx->ev_plan[pp], st));
+  CK(ev_record(ctx, ctx->ev_plan[pp], st));
   ctx->plan_layer[pp] = next_layer;
   return PROBE_OK;
 }
@@ -709,7 +742,7 @@ probe_status probe_prefetch(probe_ctx ctx, int32_t next_layer, const void* w13_n
   const int pp = next_layer & 1, prev = (next_layer - 1) & 1;
   if (phase == 1) {
     if (ctx->pf_layer[pp] != next_layer) return fail(ctx, PROBE_ESTATE, "prefetch WAIT(%d) before START", next_layer);
-    CK(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), ctx->ev_slots[pp], 0));
+    CK(ev_wait(ctx, static_cast<cudaStream_t>(stream), ctx->ev_slots[pp]));
     return PROBE_OK;
   }
   if (phase != 0) return fail(ctx, PROBE_EINVAL, "phase must be 0 (START) or 1 (WAIT)");
@@ -718,25 +751,25 @@ probe_status probe_prefetch(probe_ctx ctx, int32_t next_layer, const void* w13_n
   const Dims& d = ctx->d;
   const Scratch& s = ctx->sl;
   cudaStream_t st = ctx->pf;
-  CK(cudaStreamWaitEvent(st, ctx->ev_plan[pp], 0));
+  CK(ev_wait(ctx, st, ctx->ev_plan[pp]));
   int32_t* flags = ctx->at<int32_t>(s.flags);
   const bool inflight = ctx->fwd_layer == next_layer - 1;
   const int grid = 16;  // "controlled SM occupancy": 16 CTAs co-resident with the GEMM
   if (inflight) {
-    CK(cudaStreamWaitEvent(st, ctx->ev_gemm[prev], 0));
+    CK(ev_wait(ctx, st, ctx->ev_gemm[prev]));
     k_prefetch<<<grid, 512, 0, st>>>(d, ctx->at<int32_t>(s.reps[pp]), pp, static_cast<const uint8_t*>(w13_next),
                                      static_cast<const uint8_t*>(w2_next), sym_of(ctx), PROBE_BUF_REP_W13,
                                      PROBE_BUF_REP_W2, ctx->at<int32_t>(s.pfctr[pp]), flags + 1, next_layer,
                                      flags + 2);
     CKL();
-    CK(cudaStreamWaitEvent(st, ctx->ev_comb[prev], 0));
+    CK(ev_wait(ctx, st, ctx->ev_comb[prev]));
   }
   k_prefetch<<<grid, 512, 0, st>>>(d, ctx->at<int32_t>(s.reps[pp]), pp, static_cast<const uint8_t*>(w13_next),
                                    static_cast<const uint8_t*>(w2_next), sym_of(ctx), PROBE_BUF_REP_W13,
                                    PROBE_BUF_REP_W2, ctx->at<int32_t>(s.pfctr[pp]), flags + 1, -1, flags + 3);
   CKL();
   CK(xbarrier(ctx, BAR_PREFETCH, st));          // every sender finished pushing into our slots
-  CK(cudaEventRecord(ctx->ev_slots[pp], st));
+  CK(ev_record(ctx, ctx->ev_slots[pp], st));
   ctx->pf_layer[pp] = next_layer;
   return PROBE_OK;
 }
