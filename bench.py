@@ -109,6 +109,8 @@ def run_probe(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     shape = pi.SHAPES[args.config]
+    if args.ep:
+        shape = shape.with_(G=args.ep)
     G = shape.G
     if G % world:
         raise SystemExit(f"EP={G} ranks cannot be spread over {world} GPUs")
@@ -206,7 +208,18 @@ def run_probe(args):
     ph = rt.profile_read()
     phases = {n: float(ph[:, i].mean()) for i, n in enumerate(PHASES)}
     rt.profile(0)
-    # ---- realized balance of the last layer
+    # ---- diagnostic layer pair (untimed): planner stats, predicted vs actual load, balance
+    pc = torch.empty(G, shape.E, dtype=torch.int32, device=dev)
+    pst = torch.empty(8, dtype=torch.int64, device=dev)
+    li = pool[L % POOL]
+    p, q = L % 2, (L + 1) % 2
+    rt.forward(L, li.x, W[p], None, w13[p], w2[p], out, use_plan=True)
+    rt.predict(L + 1, li.x, W[q], None, res[q][0], res[q][1], pred_counts=pc)
+    rt.plan(L + 1, win, stats=pst)
+    rt.prefetch(L + 1, w13[q], w2[q], phase=0)
+    L += 1
+    step(L)
+    L += 1
     counts = torch.empty(G, shape.E, dtype=torch.int32, device=dev)
     split = torch.empty(G, shape.E, G, dtype=torch.int32, device=dev)
     reps = torch.empty(G, 3, dtype=torch.int32, device=dev)
@@ -214,6 +227,8 @@ def run_probe(args):
     torch.cuda.synchronize(dev)
     EL = shape.E // G
     n = counts.cpu().numpy().astype(np.int64)
+    nh = pc.cpu().numpy().astype(np.int64)
+    stats = pst.cpu().numpy().tolist()
     sc = split.cpu().numpy().astype(np.int64)
     sp = np.diff(np.concatenate([np.zeros((G, shape.E, 1), np.int64), sc], axis=2), axis=2)
     pre = n.sum(axis=0).reshape(G, EL).sum(axis=1)
@@ -221,6 +236,7 @@ def run_probe(args):
     ir_pre = float(pre.max() / pre.mean())
     ir_post = float(post.max() / post.mean())
     nrep = int((reps >= 0).sum().item())
+    load_fidelity = float(np.minimum(nh, n).sum() / max(1, n.sum()))
     # ---- static-EP baseline (same library, replication disabled, no aux track)
     for _ in range(2):
         step(L, use_plan=False)
@@ -303,6 +319,13 @@ def run_probe(args):
                 "gemm2": {"achieved": fl2 / t2 / 1e12, "frac": fl2 / t2 / 1e12 / peak_tf},
                 "expert_ffn": {"achieved": (fl1 + fl2) / (t1 + t2) / 1e12,
                                "frac": (fl1 + fl2) / (t1 + t2) / 1e12 / peak_tf}}
+    # ---- dispatch / combine against the HBM roofline (one GPU: every "peer" store is local HBM)
+    byd = (G * T * H * 2 + pairs * H * 2) / world
+    byc = (pairs * H * 4 + G * T * H * 4) / world
+    bw_report = {"dispatch": {"algorithmic_bytes": byd, "GBps": byd / (phases["dispatch"] / 1e3) / 1e9,
+                              "frac_hbm": byd / (phases["dispatch"] / 1e3) / 1e9 / peak_bw},
+                 "combine": {"algorithmic_bytes": byc, "GBps": byc / (phases["combine"] / 1e3) / 1e9,
+                             "frac_hbm": byc / (phases["combine"] / 1e3) / 1e9 / peak_bw}}
     result = None
     if rank == 0:
         cpu = None if args.no_cpu else cpu_baseline(shape, args, sample_tokens=args.cpu_tokens)
@@ -329,7 +352,11 @@ def run_probe(args):
             "static_ep": {"ms_per_step": ms_static, "speedup_probe_vs_static": ms_static / ms,
                           "phases_ms": static_phases},
             "ep_emulation": ep_em,
-            "balance": {"ir_pre": ir_pre, "ir_post": ir_post, "replicas": nrep},
+            "balance": {"ir_pre": ir_pre, "ir_post": ir_post, "replicas": nrep,
+                        "planner": {"iterations": stats[0], "transfers": stats[1], "maxL_before_ps": stats[2],
+                                    "maxL_after_ps": stats[3]},
+                        "predicted_load_fidelity": load_fidelity},
+            "bandwidth": bw_report,
             "setup_s": gen_s,
         }
         print(json.dumps(result), flush=True)
@@ -439,6 +466,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-emulation", action="store_true")
+    ap.add_argument("--ep", type=int, default=0, help="EP size G (default: the config's, 8)")
     ap.add_argument("--cpu-tokens", type=int, default=256)
     ap.add_argument("--ref-tokens", type=int, default=16)
     args = ap.parse_args()
