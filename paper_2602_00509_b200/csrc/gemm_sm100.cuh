@@ -59,8 +59,11 @@ struct GemmSched {
   int32_t counter;                   // dynamic tile counter (reset by the kernel writing the schedule)
   int32_t part_tile[kMaxParts + 1];  // tile range [part_tile[p], part_tile[p+1]) of partition p
   int32_t part_counter[kMaxParts];   // per-partition tile counters
+  unsigned long long* stats;         // optional per-role wait-cycle counters (timing hook only)
   GemmGroup g[kMaxGroups];
 };
+// stats[0] producer waits on `empty`   stats[1] MMA waits on `full`   stats[2] MMA waits on `tempty`
+// stats[3] epilogue waits on `tfull`   stats[4] epilogue busy          stats[5] tiles    stats[6] CTA cycles
 
 // Dynamic persistent tile scheduling: the producer warp claims the next tile from a
 // global atomic counter and hands it to the MMA and epilogue warps through an
@@ -96,6 +99,7 @@ __host__ __device__ inline int gemm_ntiles(const GemmGroup& G, int BN) {
 // Serial prefix over the group table (called by one thread).
 __device__ inline void gemm_finalize_sched(GemmSched* s, int BN) {
   s->nparts = 0;
+  s->stats = nullptr;
   sched_reset_counters(s);
   int acc = 0;
   for (int i = 0; i < s->num_groups; ++i) {
@@ -269,6 +273,21 @@ __device__ __forceinline__ void epi_topk(uint32_t tb, int lane, const GemmGroup&
 
 // EW epilogue warps (4 or 8): warp 4+i reads TMEM lane quarter i%4 and handles the
 // column chunks c ≡ i/4 (mod EW/4).  Threads = 128 + 32·EW.
+// Per-role wait-cycle counters: compiled only into the analysis build (-DPROBE_GEMM_STATS,
+// tools/gemm_stats.py); the product build has no instrumentation.
+#ifdef PROBE_GEMM_STATS
+#define GEMM_TIMED_WAIT(bar, par, slot)                        \
+  do {                                                         \
+    const long long t0_ = clock64();                           \
+    ptx::mbar_wait(bar, par);                                  \
+    acc_st[slot] += clock64() - t0_;                           \
+  } while (0)
+#define GEMM_STAT(expr) expr
+#else
+#define GEMM_TIMED_WAIT(bar, par, slot) ptx::mbar_wait(bar, par)
+#define GEMM_STAT(expr)
+#endif
+
 template <int BN, int STAGES, int EW = 4, int NBUF = (EW == 8 ? 2 : 1)>
 __global__ void __launch_bounds__(128 + 32 * EW, 1)
 grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
@@ -292,6 +311,8 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int ng = sched->num_groups;
+  GEMM_STAT(long long acc_st[7] = {0, 0, 0, 0, 0, 0, 0});
+  GEMM_STAT(const long long t_kernel0 = clock64());
   for (int i = threadIdx.x; i < ng; i += blockDim.x) ts[i] = sched->g[i].tile_start;
 
   if (warp == 0 && lane == 0) {
@@ -355,7 +376,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           const CUtensorMap* ta = second ? &tmA2 : &tmA;
           const CUtensorMap* tb = (second || G.b_sel) ? &tmB1 : &tmB0;
           const int kc = (second ? kb - kb1 : kb) * 64;
-          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          GEMM_TIMED_WAIT(&empty[stage], phase ^ 1, 0);
           ptx::mbar_arrive_expect_tx(&full[stage], L::A_BYTES + L::B_BYTES);
           ptx::tma_load_2d(ta, &full[stage], sA + stage * L::A_BYTES, kc, arow);
           ptx::tma_load_2d(tb, &full[stage], sB + stage * L::B_BYTES, kc, brow0);
@@ -380,11 +401,11 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       if (lane == 0) ptx::mbar_arrive(&qempty[qs]);
       if (++qs == kTileQ) { qs = 0; qph ^= 1; }
       if (tile < 0) break;
-      ptx::mbar_wait(&tempty[acc], aphase ^ 1);
+      GEMM_TIMED_WAIT(&tempty[acc], aphase ^ 1, 2);
       ptx::tc_fence_after();
       const uint32_t d = tmem_base + acc * BN;
       for (int kb = 0; kb < num_kb; ++kb) {
-        ptx::mbar_wait(&full[stage], phase);
+        GEMM_TIMED_WAIT(&full[stage], phase, 1);
         ptx::tc_fence_after();
         if (lane == 0) {
           const uint64_t a0 = ptx::sdesc_sw128(ptx::smem_u32(sA + stage * L::A_BYTES));
@@ -425,7 +446,9 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       const int nt = gemm_ntiles_n(G, BN);
       const int tin = tile - ts[gi];
       const int mb = tin / nt, nb = tin % nt;
-      ptx::mbar_wait(&tfull[acc], aphase);
+      GEMM_TIMED_WAIT(&tfull[acc], aphase, 3);
+      GEMM_STAT(const long long t_epi0 = clock64());
+      GEMM_STAT(acc_st[5] += 1);
       ptx::tc_fence_after();
       const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
       const int row0 = mb * 128 + q * 32;          // first tile row of this warp
@@ -479,10 +502,18 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+      GEMM_STAT(acc_st[4] += clock64() - t_epi0);
       acc ^= 1;
       if (acc == 0) aphase ^= 1;
     }
   }
+#ifdef PROBE_GEMM_STATS
+  if (sched->stats && lane == 0 && (warp <= 1 || warp == 4)) {
+    acc_st[6] = clock64() - t_kernel0;
+    for (int i = 0; i < 7; ++i)
+      if (acc_st[i]) atomicAdd(&sched->stats[i], static_cast<unsigned long long>(acc_st[i]));
+  }
+#endif
   if (warp >= 4 && lane == 0) ptx::bulk_wait<0>();
   __syncthreads();
   if (warp == 2) {

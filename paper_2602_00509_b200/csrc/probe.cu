@@ -825,6 +825,12 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
   std::vector<uint8_t> host(sizeof(GemmSched), 0);
   GemmSched* hs = reinterpret_cast<GemmSched*>(host.data());
   hs->num_groups = num_groups;
+  unsigned long long* dstats = nullptr;
+  if (getenv("PROBE_GEMM_STATS")) {
+    CK(cudaMalloc(&dstats, 8 * sizeof(unsigned long long)));
+    CK(cudaMemset(dstats, 0, 8 * sizeof(unsigned long long)));
+    hs->stats = dstats;
+  }
   const size_t esz = emode == EPI_SWIGLU || emode == EPI_SILU_BF16 ? 2 : 4;
   int acc = 0;
   int64_t c_rows = 1;
@@ -883,6 +889,14 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
   cudaEventDestroy(e1);
   cudaFree(ds);
   if (topk_aux) cudaFree(topk_aux);
+  if (dstats) {
+    unsigned long long h[8];
+    if (cudaMemcpy(h, dstats, sizeof(h), cudaMemcpyDeviceToHost) == cudaSuccess)
+      fprintf(stderr, "[gemm stats] variant %d reps %d: prod_wait_empty %.3g  mma_wait_full %.3g  mma_wait_tempty %.3g  "
+                      "epi_wait_tfull %.3g  epi_busy %.3g  tiles %llu  cta_cycles %.3g (sums over CTAs)\n",
+              variant, reps + 1, (double)h[0], (double)h[1], (double)h[2], (double)h[3], (double)h[4], h[5], (double)h[6]);
+    cudaFree(dstats);
+  }
   if (e != cudaSuccess) return fail(nullptr, PROBE_ECUDA, "probe_test_gemm: %s", cudaGetErrorString(e));
   return PROBE_OK;
 }
