@@ -282,10 +282,10 @@ __device__ __forceinline__ void epi_topk(uint32_t tb, int lane, const GemmGroup&
     ptx::mbar_wait(bar, par);                                  \
     acc_st[slot] += clock64() - t0_;                           \
   } while (0)
-#define GEMM_STAT(expr) expr
+#define GEMM_STAT(...) __VA_ARGS__
 #else
 #define GEMM_TIMED_WAIT(bar, par, slot) ptx::mbar_wait(bar, par)
-#define GEMM_STAT(expr)
+#define GEMM_STAT(...)
 #endif
 
 template <int BN, int STAGES, int EW = 4, int NBUF = (EW == 8 ? 2 : 1)>

@@ -1,0 +1,43 @@
+"""Per-role wait-cycle breakdown of the expert GEMMs (C1 shapes) using the analysis build
+tools/libprobe_stats.so (nvcc ... -DPROBE_GEMM_STATS).  Prints the library's [gemm stats]
+lines (stderr): producer waits on `empty`, MMA waits on `full` / `tempty`, epilogue waits
+on `tfull` and busy cycles, summed over CTAs."""
+import ctypes as C
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_2602_00509_b200 import _lib  # noqa: E402
+
+os.environ["PROBE_GEMM_STATS"] = "1"
+lib = C.CDLL("tools/libprobe_stats.so")
+lib.probe_bench_gemm.restype = C.c_int32
+lib.probe_bench_gemm.argtypes = _lib.load().probe_bench_gemm.argtypes
+E_loc, rows_per, H, F = 128, 4096, 2048, 768
+M = E_loc * rows_per
+
+
+def run(A, B, groups, N, mode, out, v):
+    flat = (C.c_int32 * (4 * len(groups)))(*[int(x) for g in groups for x in g])
+    ms = C.c_float(0)
+    st = lib.probe_bench_gemm(C.c_void_p(A.data_ptr()), A.shape[0], C.c_void_p(B.data_ptr()), B.shape[0], A.shape[1],
+                              N, flat, len(groups), mode, v, 5, C.byref(ms), C.c_void_p(out.data_ptr()),
+                              C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert st == 0
+    return ms.value
+
+
+A2 = (torch.randn(M, F, device="cuda") * 0.5).to(torch.bfloat16)
+B2 = (torch.randn(E_loc * H, F, device="cuda") / F ** 0.5).to(torch.bfloat16)
+Y = torch.empty(M, H, device="cuda")
+g2 = [[e * rows_per, rows_per, e * H, e * rows_per] for e in range(E_loc)]
+for mode in (2, 4):
+    print("GEMM2 mode", mode, "ms", run(A2, B2, g2, H, mode, Y, 1), flush=True)
+del A2, B2, Y
+A1 = (torch.randn(M, H, device="cuda") * 0.5).to(torch.bfloat16)
+B1 = (torch.randn(E_loc * 2 * F, H, device="cuda") / H ** 0.5).to(torch.bfloat16)
+act = torch.empty(M, F, dtype=torch.bfloat16, device="cuda")
+g1 = [[e * rows_per, rows_per, e * 2 * F, e * rows_per] for e in range(E_loc)]
+print("GEMM1 ms", run(A1, B1, g1, 2 * F, 1, act, 1), flush=True)
