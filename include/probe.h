@@ -169,7 +169,8 @@ probe_status probe_test_gemm(const void* A, int64_t a_rows, const void* B, int64
 
 /* Timing hook: as probe_test_gemm with an explicit kernel variant (-1 = default for
  * `mode`; 0: BN=128/6 stages/4 epilogue warps, 1: 256/4/4, 2: 256/3/8, 3: 128/4/8,
- * 4: 256/3/4 with 2 staging tiles per epilogue warp, 5: 256/3/4 with 4),
+ * 4: 256/3/4 with 2 staging tiles per epilogue warp, 5: 256/3/4 with 4,
+ * 6: CTA pair (cta_group::2), 256-row tiles, 6 stages),
  * run once, then `reps` times between CUDA events on `stream`; *ms_out = mean ms. */
 probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int64_t b_rows,
                               int32_t K, int32_t N, const int32_t* groups, int32_t num_groups,
@@ -223,7 +224,8 @@ probe_status probe_ipc_close(uint64_t dev_ptr_base);
  * do the router/predictor top-k inside the tcgen05 GEMM epilogue instead of the
  * thread-per-token select kernel (default off: measured slower). */
 enum { PROBE_OPT_EP_EMULATION = 1, PROBE_OPT_UNFUSED_TOPK = 2, PROBE_OPT_FUSED_EPILOGUE_TOPK = 3,
-       PROBE_OPT_AUX_SMS = 4 /* grid cap (CTAs) of the predictor GEMMs on the aux stream; default #SMs/2 */ };
+       PROBE_OPT_AUX_SMS = 4 /* grid cap (CTAs) of the predictor GEMMs on the aux stream; default #SMs/2 */,
+       PROBE_OPT_PAIR_GEMM = 5 /* expert GEMMs on CTA pairs (tcgen05 cta_group::2, 256-row tiles) */ };
 probe_status probe_set_option(probe_ctx ctx, int32_t option, int64_t value);
 
 /* Number of library kernel launches enqueued so far by this context (bench accounting). */

@@ -23,7 +23,7 @@ EXPORTS = ["probe_workspace", "probe_init", "probe_moe_forward", "probe_predict"
            "probe_prefetch", "probe_debug_layout", "probe_test_gemm", "probe_check", "probe_last_error",
            "probe_finalize", "probe_launch_count", "probe_profile", "probe_profile_read", "probe_bench_gemm",
            "probe_ipc_export", "probe_ipc_import", "probe_ipc_close", "probe_set_option"]
-OPT_EP_EMULATION, OPT_UNFUSED_TOPK, OPT_FUSED_EPILOGUE_TOPK, OPT_AUX_SMS = 1, 2, 3, 4
+OPT_EP_EMULATION, OPT_UNFUSED_TOPK, OPT_FUSED_EPILOGUE_TOPK, OPT_AUX_SMS, OPT_PAIR_GEMM = 1, 2, 3, 4, 5
 PROBE_NPHASE = 10
 PHASES = ["gate", "select", "counts", "layout", "dispatch", "wait", "gemm1", "gemm2", "combine", "total"]
 

@@ -55,8 +55,10 @@ constexpr int kMaxParts = 64;
 struct GemmSched {
   int32_t num_groups;
   int32_t total_tiles;
-  int32_t nparts;                    // >1: CTA b serves only partition b % nparts (EP emulation)
+  int32_t nparts;                    // >1: CTA (pair) b serves only partition b % nparts (EP emulation)
   int32_t counter;                   // dynamic tile counter (reset by the kernel writing the schedule)
+  int32_t tile_m;                    // rows per tile: 128 (1-CTA MMA) or 256 (CTA pair, cta_group::2)
+  int32_t pad2;
   int32_t part_tile[kMaxParts + 1];  // tile range [part_tile[p], part_tile[p+1]) of partition p
   int32_t part_counter[kMaxParts];   // per-partition tile counters
   unsigned long long* stats;         // optional per-role wait-cycle counters (timing hook only)
@@ -72,10 +74,10 @@ struct GemmSched {
 // emulation): CTA b serves only partition b % nparts (its logical rank's tiles), so a rank's
 // expert GEMM runs on ~#SMs/nparts SMs and the launch time is the straggler's (Eq. 3).
 constexpr int kTileQ = 8;
-__device__ __forceinline__ int claim_tile(GemmSched* s) {
+__device__ __forceinline__ int claim_tile(GemmSched* s, int unit = -1) {
   const int np = s->nparts;
   if (np > 1) {
-    const int p = blockIdx.x % np;
+    const int p = (unit < 0 ? static_cast<int>(blockIdx.x) : unit) % np;
     const int t = s->part_tile[p] + atomicAdd(&s->part_counter[p], 1);
     return t < s->part_tile[p + 1] ? t : -1;
   }
@@ -92,13 +94,14 @@ __host__ __device__ inline int gemm_ntiles_n(const GemmGroup& G, int BN) {
   const int bno = (G.mode == EPI_SWIGLU) ? BN / 2 : BN;
   return (G.n + bno - 1) / bno;
 }
-__host__ __device__ inline int gemm_ntiles(const GemmGroup& G, int BN) {
-  return G.m <= 0 ? 0 : ((G.m + 127) / 128) * gemm_ntiles_n(G, BN);
+__host__ __device__ inline int gemm_ntiles(const GemmGroup& G, int BN, int TM = 128) {
+  return G.m <= 0 ? 0 : ((G.m + TM - 1) / TM) * gemm_ntiles_n(G, BN);
 }
 
 // Serial prefix over the group table (called by one thread).
 __device__ inline void gemm_finalize_sched(GemmSched* s, int BN) {
   s->nparts = 0;
+  s->tile_m = 128;
   s->stats = nullptr;
   sched_reset_counters(s);
   int acc = 0;
@@ -268,6 +271,60 @@ __device__ __forceinline__ void epi_topk(uint32_t tb, int lane, const GemmGroup&
     int32_t* cnt = reinterpret_cast<int32_t*>(G.aux) + static_cast<size_t>((G.a_row + row) / G.rows_per_rank) * G.n;
 #pragma unroll
     for (int j = 0; j < KK; ++j) atomicAdd(cnt + te[j], 1);
+  }
+}
+
+// Epilogue of one output tile for one epilogue warp: TMEM lanes of this warp (row0..row0+31),
+// the column chunks c ≡ part (mod NPART).  Shared by the 1-CTA and the 2-CTA kernels.
+template <int BN, int NB, int NPART>
+__device__ __forceinline__ void epi_tile(uint32_t tb, int lane, int part, const GemmGroup& G, int row0, int nb,
+                                         float* tiles, int& tsel, const CUtensorMap* tmC) {
+  if (G.mode == EPI_TOPK || G.mode == EPI_TOPK_COUNT) {
+    switch (G.topk) {
+      case 1: epi_topk<1, BN>(tb, lane, G, row0, tiles); break;
+      case 2: epi_topk<2, BN>(tb, lane, G, row0, tiles); break;
+      case 3: epi_topk<3, BN>(tb, lane, G, row0, tiles); break;
+      case 4: epi_topk<4, BN>(tb, lane, G, row0, tiles); break;
+      case 5: epi_topk<5, BN>(tb, lane, G, row0, tiles); break;
+      case 6: epi_topk<6, BN>(tb, lane, G, row0, tiles); break;
+      case 7: epi_topk<7, BN>(tb, lane, G, row0, tiles); break;
+      default: epi_topk<8, BN>(tb, lane, G, row0, tiles); break;
+    }
+  } else if (G.mode == EPI_SWIGLU) {
+#pragma unroll 1
+    for (int c = part; c < BN / 64; c += NPART) {
+      uint32_t gv[32], uv[32];
+      ptx::tmem_ld32(tb + c * 32, gv);
+      ptx::tmem_ld32(tb + BN / 2 + c * 32, uv);
+      ptx::tmem_ld_wait();
+      float v[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = silu_f(__uint_as_float(gv[i])) * __uint_as_float(uv[i]);
+      epi_chunk<NB>(tiles, tsel, lane, v, G, tmC, row0, nb * (BN / 2) + c * 32);
+    }
+  } else {
+    // two chunks in flight per TMEM wait
+#pragma unroll 1
+    for (int c = part; c < BN / 32; c += 2 * NPART) {
+      const int c2 = c + NPART;
+      uint32_t va[32], vb[32];
+      ptx::tmem_ld32(tb + c * 32, va);
+      if (c2 < BN / 32) ptx::tmem_ld32(tb + c2 * 32, vb);
+      ptx::tmem_ld_wait();
+      float v[32];
+      const bool silu = G.mode == EPI_SILU_BF16;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int cc = h == 0 ? c : c2;
+        if (cc >= BN / 32) break;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float x = __uint_as_float(h == 0 ? va[i] : vb[i]);
+          v[i] = silu ? silu_f(x) : x;
+        }
+        epi_chunk<NB>(tiles, tsel, lane, v, G, tmC, row0, nb * BN + cc * 32);
+      }
+    }
   }
 }
 
@@ -452,53 +509,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       ptx::tc_fence_after();
       const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
       const int row0 = mb * 128 + q * 32;          // first tile row of this warp
-      if (G.mode == EPI_TOPK || G.mode == EPI_TOPK_COUNT) {
-        switch (G.topk) {
-          case 1: epi_topk<1, BN>(tb, lane, G, row0, tiles); break;
-          case 2: epi_topk<2, BN>(tb, lane, G, row0, tiles); break;
-          case 3: epi_topk<3, BN>(tb, lane, G, row0, tiles); break;
-          case 4: epi_topk<4, BN>(tb, lane, G, row0, tiles); break;
-          case 5: epi_topk<5, BN>(tb, lane, G, row0, tiles); break;
-          case 6: epi_topk<6, BN>(tb, lane, G, row0, tiles); break;
-          case 7: epi_topk<7, BN>(tb, lane, G, row0, tiles); break;
-          default: epi_topk<8, BN>(tb, lane, G, row0, tiles); break;
-        }
-      } else if (G.mode == EPI_SWIGLU) {
-#pragma unroll 1
-        for (int c = part; c < BN / 64; c += NPART) {
-          uint32_t gv[32], uv[32];
-          ptx::tmem_ld32(tb + c * 32, gv);
-          ptx::tmem_ld32(tb + BN / 2 + c * 32, uv);
-          ptx::tmem_ld_wait();
-          float v[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = silu_f(__uint_as_float(gv[i])) * __uint_as_float(uv[i]);
-          epi_chunk<L::NB>(tiles, tsel, lane, v, G, &tmC, row0, nb * (BN / 2) + c * 32);
-        }
-      } else {
-        // two chunks in flight per TMEM wait
-#pragma unroll 1
-        for (int c = part; c < BN / 32; c += 2 * NPART) {
-          const int c2 = c + NPART;
-          uint32_t va[32], vb[32];
-          ptx::tmem_ld32(tb + c * 32, va);
-          if (c2 < BN / 32) ptx::tmem_ld32(tb + c2 * 32, vb);
-          ptx::tmem_ld_wait();
-          float v[32];
-          const bool silu = G.mode == EPI_SILU_BF16;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int cc = h == 0 ? c : c2;
-            if (cc >= BN / 32) break;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const float x = __uint_as_float(h == 0 ? va[i] : vb[i]);
-              v[i] = silu ? silu_f(x) : x;
-            }
-            epi_chunk<L::NB>(tiles, tsel, lane, v, G, &tmC, row0, nb * BN + cc * 32);
-          }
-        }
-      }
+      epi_tile<BN, L::NB, NPART>(tb, lane, part, G, row0, nb, tiles, tsel, &tmC);
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
@@ -519,6 +530,221 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<2 * BN>(tmem_base);
+  }
+}
+
+// =============================================================================
+// CTA-pair variant (tcgen05 cta_group::2): a cluster of 2 CTAs computes a 256 × BN tile.
+// Each CTA loads its own 128 rows of A and ONE HALF of B (rows [0, BN/2) in CTA 0,
+// [BN/2, BN) in CTA 1 — for SwiGLU: gate rows in CTA 0, up rows in CTA 1), so a stage
+// is 32 KB instead of 48 KB and 6 stages fit.  The leader CTA's single thread issues
+// tcgen05.mma.cta_group::2 (M = 256) reading both CTAs' smem; the accumulator rows of
+// each CTA live in its own TMEM and each CTA's epilogue drains its own 128 rows.
+// Barriers: TMA bytes of both CTAs complete on the LEADER's `full` (count 2: leader
+// expect_tx + peer arrive); MMA commits multicast to both CTAs' `empty` / `tfull`;
+// both CTAs' epilogues arrive on the leader's `tempty`.  The leader claims tiles and
+// mirrors them into the peer's queue through DSMEM.
+// =============================================================================
+template <int BN, int STAGES, int EW>
+struct Gemm2Smem {
+  static constexpr int A_BYTES = 128 * 128;
+  static constexpr int B_BYTES = (BN / 2) * 128;
+  static constexpr int BAR_OFF = STAGES * (A_BYTES + B_BYTES);
+  static constexpr int TS_OFF = BAR_OFF + (2 * STAGES + 4 + 2 * kTileQ) * 8 + 16 + kTileQ * 4;
+  static constexpr int EPI_OFF = (TS_OFF + (kMaxGroups + 1) * 4 + 1023) / 1024 * 1024;
+  static constexpr int NB = 1;
+  static constexpr int BYTES = EPI_OFF + EW * NB * 4096 + 1024;
+};
+
+template <int BN, int STAGES, int EW>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EW, 1)
+grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
+                         const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmC,
+                         const __grid_constant__ CUtensorMap tmA2, GemmSched* __restrict__ sched, int K, int K2) {
+  using L = Gemm2Smem<BN, STAGES, EW>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * L::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* qfull = tempty + 2;
+  uint64_t* qempty = qfull + kTileQ;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qempty + kTileQ);
+  volatile int* tq = reinterpret_cast<volatile int*>(tmem_slot + 4);
+  int* ts = reinterpret_cast<int*>(smem + L::TS_OFF);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int ng = sched->num_groups;
+  for (int i = threadIdx.x; i < ng; i += blockDim.x) ts[i] = sched->g[i].tile_start;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 2);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 2 * EW);
+    }
+    for (int q = 0; q < kTileQ; ++q) {
+      ptx::mbar_init(&qfull[q], 1);
+      ptx::mbar_init(&qempty[q], 2 + 2 * EW);   // leader: MMA + EW epilogue; peer: producer + EW epilogue
+    }
+    ptx::fence_barrier_init();
+    ptx::tma_prefetch_desc(&tmA);
+    ptx::tma_prefetch_desc(&tmB0);
+    ptx::tma_prefetch_desc(&tmB1);
+    if (K2 > 0) ptx::tma_prefetch_desc(&tmA2);
+  }
+  if (warp == 2) ptx::tmem_alloc_cg2<2 * BN>(tmem_slot);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();          // barrier inits visible to the peer, TMEM allocated in both CTAs
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int kb1 = (K + 63) / 64;
+  const int num_kb = kb1 + (K2 > 0 ? (K2 + 63) / 64 : 0);
+  const int unit = static_cast<int>(blockIdx.x >> 1);     // cluster index (EP-emulation partition)
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int qs = 0;
+      uint32_t qph = 0;
+      while (true) {
+        int tile;
+        if (leader) {
+          tile = claim_tile(sched, unit);
+          ptx::mbar_wait_cluster(&qempty[qs], qph ^ 1);
+          tq[qs] = tile;
+          ptx::st_cluster_u32(ptx::mapa(ptx::smem_u32(const_cast<int*>(&tq[qs])), 1), static_cast<uint32_t>(tile));
+          ptx::mbar_arrive(&qfull[qs]);
+          ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&qfull[qs]), 1));
+        } else {
+          ptx::mbar_wait_cluster(&qfull[qs], qph);
+          tile = tq[qs];
+          ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&qempty[qs]), 0));
+        }
+        if (++qs == kTileQ) { qs = 0; qph ^= 1; }
+        if (tile < 0) break;
+        const int gi = gemm_find_group(ts, ng, tile);
+        const GemmGroup& G = sched->g[gi];
+        const int nt = gemm_ntiles_n(G, BN);
+        const int tin = tile - ts[gi];
+        const int mb = tin / nt, nb = tin % nt;
+        const int arow = G.a_row + mb * 256 + static_cast<int>(rank) * 128;
+        int brow;
+        if (G.mode == EPI_SWIGLU) brow = G.b_row + (rank ? G.n : 0) + nb * (BN / 2);
+        else brow = G.b_row + nb * BN + static_cast<int>(rank) * (BN / 2);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          const bool second = kb >= kb1;
+          const CUtensorMap* ta = second ? &tmA2 : &tmA;
+          const CUtensorMap* tb = (second || G.b_sel) ? &tmB1 : &tmB0;
+          const int kc = (second ? kb - kb1 : kb) * 64;
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (L::A_BYTES + L::B_BYTES));
+          else ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&full[stage]), 0));
+          ptx::tma_load_2d_cg2(ta, &full[stage], sA + stage * L::A_BYTES, kc, arow);
+          ptx::tma_load_2d_cg2(tb, &full[stage], sB + stage * L::B_BYTES, kc, brow);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader CTA only)
+    if (leader) {
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(256, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t aphase = 0;
+      int qs = 0;
+      uint32_t qph = 0;
+      while (true) {
+        ptx::mbar_wait(&qfull[qs], qph);
+        const int tile = tq[qs];
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&qempty[qs]);
+        if (++qs == kTileQ) { qs = 0; qph ^= 1; }
+        if (tile < 0) break;
+        ptx::mbar_wait_cluster(&tempty[acc], aphase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          ptx::mbar_wait_cluster(&full[stage], phase);
+          ptx::tc_fence_after();
+          if (lane == 0) {
+            const uint64_t a0 = ptx::sdesc_sw128(ptx::smem_u32(sA + stage * L::A_BYTES));
+            const uint64_t b0 = ptx::sdesc_sw128(ptx::smem_u32(sB + stage * L::B_BYTES));
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              ptx::umma_bf16_ss_cg2(d, a0 + 2 * k, b0 + 2 * k, idesc, (kb | k) != 0);
+            ptx::umma_commit_cg2(&empty[stage], 0x3);
+          }
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (lane == 0) ptx::umma_commit_cg2(&tfull[acc], 0x3);
+        __syncwarp();
+        acc ^= 1;
+        if (acc == 0) aphase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue (both CTAs, own 128 rows)
+    const int q = warp & 3;
+    const int part = (warp - 4) >> 2;
+    constexpr int NPART = EW / 4;
+    float* tiles = reinterpret_cast<float*>(smem + L::EPI_OFF + (warp - 4) * L::NB * 4096);
+    int tsel = 0;
+    int acc = 0;
+    uint32_t aphase = 0;
+    int qs = 0;
+    uint32_t qph = 0;
+    const uint32_t tempty_leader0 = ptx::mapa(ptx::smem_u32(&tempty[0]), 0);
+    while (true) {
+      ptx::mbar_wait_cluster(&qfull[qs], qph);
+      const int tile = tq[qs];
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) ptx::mbar_arrive(&qempty[qs]);
+        else ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&qempty[qs]), 0));
+      }
+      if (++qs == kTileQ) { qs = 0; qph ^= 1; }
+      if (tile < 0) break;
+      const int gi = gemm_find_group(ts, ng, tile);
+      const GemmGroup G = sched->g[gi];
+      const int nt = gemm_ntiles_n(G, BN);
+      const int tin = tile - ts[gi];
+      const int mb = tin / nt, nb = tin % nt;
+      ptx::mbar_wait(&tfull[acc], aphase);
+      ptx::tc_fence_after();
+      const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+      const int row0 = mb * 256 + static_cast<int>(rank) * 128 + q * 32;
+      epi_tile<BN, L::NB, NPART>(tb, lane, part, G, row0, nb, tiles, tsel, &tmC);
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) ptx::mbar_arrive(&tempty[acc]);
+        else ptx::mbar_arrive_cluster(tempty_leader0 + acc * 8);
+      }
+      acc ^= 1;
+      if (acc == 0) aphase ^= 1;
+    }
+    if (lane == 0) ptx::bulk_wait<0>();
+  }
+  __syncthreads();
+  ptx::tc_fence_before();
+  ptx::cluster_sync();          // no remote arrive / DSMEM access after this point
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_cg2<2 * BN>(tmem_base);
   }
 }
 

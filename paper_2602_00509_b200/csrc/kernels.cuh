@@ -545,6 +545,7 @@ struct LayoutOut {
 };
 struct LayoutIn {
   int nparts;                   // >1: partition the expert GEMMs by local rank (EP emulation)
+  int tile_m;                   // 128 (1-CTA expert GEMMs) or 256 (CTA-pair expert GEMMs)
   const int32_t* board_actual;  // [G][E]
   const int32_t* quota;         // [G][E][G] or null (static EP)
   const int32_t* replicas;      // [G][3] or null
@@ -667,8 +668,8 @@ __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o
     g2.out = reinterpret_cast<float*>(in.y_local) + static_cast<size_t>(arow) * d.H;
     o.s1->g[i] = g1;
     o.s2->g[i] = g2;
-    t1[i] = gemm_ntiles(g1, 256);
-    t2[i] = gemm_ntiles(g2, 256);
+    t1[i] = gemm_ntiles(g1, 256, in.tile_m);
+    t2[i] = gemm_ntiles(g2, 256, in.tile_m);
   }
   __syncthreads();
   // (7) tile prefix (warp 0: s1, warp 1: s2), warp-parallel exclusive scan in chunks of 32
@@ -692,6 +693,8 @@ __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o
     __syncwarp();
     if (lane == 0) {
       sc->total_tiles = base;
+      sc->tile_m = in.tile_m;
+      sc->stats = nullptr;
       sched_reset_counters(sc);
       sc->nparts = in.nparts > 1 ? in.nparts : 0;
       if (in.nparts > 1) {

@@ -180,6 +180,7 @@ struct probe_ctx_s {
   bool unfused = false;   // PROBE_UNFUSED=1: logits written + separate top-k kernels (debug)
   bool ep_emulation = false;  // partition expert GEMMs by local rank (probe_set_option)
   bool fused_epi_topk = false;  // top-k in the GEMM epilogue instead of k_select (probe_set_option)
+  bool pair_gemm = false;       // expert GEMMs on CTA pairs (cta_group::2) (probe_set_option)
   // phase profiling: prof_max forwards × (PROBE_NPHASE + 1) timing events
   int prof_max = 0, prof_n = 0;
   std::vector<cudaEvent_t> prof_ev;
@@ -220,7 +221,24 @@ probe_status fail(probe_ctx ctx, probe_status st, const char* fmt, ...) {
 
 // GEMM variants: (BN, STAGES, epilogue warps).  V_GATE: logits/predictor (N ≤ 256),
 // V_SWIGLU: expert GEMM1 (bf16 act out), V_F32: expert GEMM2 (fp32 Y out, epilogue-heavy).
-enum GemmVariant { V_128_6_4 = 0, V_256_4_4 = 1, V_256_3_8 = 2, V_128_4_8 = 3, V_256_3_4_NB2 = 4, V_256_3_4_NB4 = 5 };
+enum GemmVariant { V_128_6_4 = 0, V_256_4_4 = 1, V_256_3_8 = 2, V_128_4_8 = 3, V_256_3_4_NB2 = 4, V_256_3_4_NB4 = 5,
+                   V_2CTA_256_6_4 = 6 /* CTA pair, cta_group::2, 256-row tiles */ };
+
+template <int BN, int ST, int EW>
+cudaError_t launch_gemm_2cta(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, const CUtensorMap& c,
+                             const CUtensorMap& a2, GemmSched* s, int K, int K2, int grid, cudaStream_t st) {
+  using L = Gemm2Smem<BN, ST, EW>;
+  static_assert(L::BYTES <= 232448, "shared memory budget");
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(grouped_gemm_2cta_kernel<BN, ST, EW>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  grouped_gemm_2cta_kernel<BN, ST, EW><<<grid & ~1, 128 + 32 * EW, L::BYTES, st>>>(a, b0, b1, c, a2, s, K, K2);
+  return cudaGetLastError();
+}
 
 template <int BN, int ST, int EW, int NB = (EW == 8 ? 2 : 1)>
 cudaError_t launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, const CUtensorMap& c,
@@ -249,10 +267,12 @@ cudaError_t launch_gemm_v(int v, const CUtensorMap& a, const CUtensorMap& b0, co
     case V_128_4_8: return launch_gemm_t<128, 4, 8>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_256_3_4_NB2: return launch_gemm_t<256, 3, 4, 2>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_256_3_4_NB4: return launch_gemm_t<256, 3, 4, 4>(a, b0, b1, c, A2, s, K, K2, grid, st);
+    case V_2CTA_256_6_4: return launch_gemm_2cta<256, 6, 4>(a, b0, b1, c, A2, s, K, K2, grid, st);
   }
   return cudaErrorInvalidValue;
 }
 int variant_bn(int v) { return (v == V_128_6_4 || v == V_128_4_8) ? 128 : 256; }
+int variant_tm(int v) { return v == V_2CTA_256_6_4 ? 256 : 128; }
 
 template <int BN>
 cudaError_t launch_gemm(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, GemmSched* s, int K,
@@ -542,6 +562,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   li.replicas = use_plan ? ctx->at<int32_t>(s.reps[p]) : nullptr;
   li.bank = p;
   li.nparts = (ctx->ep_emulation && d.GL > 1 && d.GL <= kMaxParts) ? d.GL : 0;
+  li.tile_m = ctx->pair_gemm ? 256 : 128;
   li.act = ctx->scratch + s.act;
   li.y_local = ctx->local_base[PROBE_BUF_Y];
   LayoutOut lo;
@@ -572,10 +593,11 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   MARK(6);
   CK(ev_record(ctx, ctx->ev_gemm[p], st));
   // a7 grouped SwiGLU expert FFN (tcgen05): act = SiLU(X W_gᵀ) ⊙ X W_uᵀ ; Y = act W_dᵀ
-  CK(launch_gemm_v(V_256_4_4, ctx->map_recv, *m13, ctx->map_rw13, ctx->map_recv, lo.s1, d.H, ctx->num_sms, st));
+  const int vexp = ctx->pair_gemm ? V_2CTA_256_6_4 : V_256_4_4;
+  CK(launch_gemm_v(vexp, ctx->map_recv, *m13, ctx->map_rw13, ctx->map_recv, lo.s1, d.H, ctx->num_sms, st));
   ++ctx->launches;
   MARK(7);
-  CK(launch_gemm_v(V_256_4_4, ctx->map_act, *m2, ctx->map_rw2, ctx->map_y, lo.s2, d.F, ctx->num_sms, st));
+  CK(launch_gemm_v(vexp, ctx->map_act, *m2, ctx->map_rw2, ctx->map_y, lo.s2, d.F, ctx->num_sms, st));
   ++ctx->launches;
   CK(xbarrier(ctx, BAR_Y, st));                 // every expert rank's Y rows are complete
   MARK(8);
@@ -808,7 +830,8 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
     return fail(nullptr, PROBE_EINVAL, "probe_test_gemm: bad arguments");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (variant < 0) variant = mode == 1 ? V_256_4_4 : (mode == 2 ? V_256_3_8 : V_128_6_4);
-  if (variant > V_256_3_4_NB4) return fail(nullptr, PROBE_EINVAL, "bad variant");
+  if (variant > V_2CTA_256_6_4) return fail(nullptr, PROBE_EINVAL, "bad variant");
+  const int TM = variant_tm(variant);
   const int BN = variant_bn(variant);
   const int emode = mode == 1 ? EPI_SWIGLU
                     : mode == 3 ? EPI_SILU_BF16
@@ -847,9 +870,10 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
     }
     c_rows = std::max<int64_t>(c_rows, static_cast<int64_t>(g[3]) + g[1]);
     hs->g[i].tile_start = acc;
-    acc += gemm_ntiles(hs->g[i], BN);
+    acc += gemm_ntiles(hs->g[i], BN, TM);
   }
   hs->total_tiles = acc;
+  hs->tile_m = TM;
   CUtensorMap ma, mb, mc;
   if (!make_map(&ma, A, a_rows, K, 128) || !make_map(&mb, B, b_rows, K, BN / 2))
     return fail(nullptr, PROBE_ECUDA, "tensor map encode failed");
@@ -942,6 +966,7 @@ probe_status probe_set_option(probe_ctx ctx, int32_t option, int64_t value) {
     case PROBE_OPT_EP_EMULATION: ctx->ep_emulation = value != 0; return PROBE_OK;
     case PROBE_OPT_UNFUSED_TOPK: ctx->unfused = value != 0; return PROBE_OK;
     case PROBE_OPT_FUSED_EPILOGUE_TOPK: ctx->fused_epi_topk = value != 0; return PROBE_OK;
+    case PROBE_OPT_PAIR_GEMM: ctx->pair_gemm = value != 0; return PROBE_OK;
     case PROBE_OPT_AUX_SMS:
       if (value < 1 || value > ctx->num_sms) return fail(ctx, PROBE_EINVAL, "aux SM cap %lld out of range", (long long)value);
       ctx->aux_sms = static_cast<int>(value);

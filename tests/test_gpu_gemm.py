@@ -67,7 +67,9 @@ def test_gemm_swiglu_and_silu():
 
 @pytest.mark.parametrize("mode,N,K,rows,variant", [(0, 256, 256, 40000, 0), (2, 512, 768, 30000, 1),
                                                    (2, 512, 768, 30000, 2), (0, 128, 2048, 65536, 0),
-                                                   (0, 384, 512, 20000, 3), (2, 2048, 768, 9000, 2)])
+                                                   (0, 384, 512, 20000, 3), (2, 2048, 768, 9000, 2),
+                                                   (2, 512, 768, 30000, 6), (2, 2048, 768, 9000, 6),
+                                                   (2, 256, 2048, 700, 6)])
 def test_gemm_multi_tile_per_cta_exact(mode, N, K, rows, variant):
     """Several tiles per persistent CTA (TMEM accumulator double buffer, phase wrap-around),
     every kernel variant (BN, stages, epilogue warps)."""
@@ -86,7 +88,7 @@ def test_gemm_multi_tile_per_cta_exact(mode, N, K, rows, variant):
         assert bad.numel() == 0, (mode, N, K, rows, bad[:10].flatten().tolist())
 
 
-@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("variant", [1, 2, 6])
 def test_gemm_multi_tile_swiglu(variant):
     from paper_2602_00509_b200 import bench_gemm
     F, K, rows = 768, 2048, 20000

@@ -16,7 +16,7 @@ act = torch.empty(M, F, dtype=torch.bfloat16, device="cuda")
 g1 = [[e * rows_per, rows_per, e * 2 * F, e * rows_per] for e in range(E_loc)]
 res = {}
 for rnd in range(4):
-    for v in (1, 2, 4, 5):
+    for v in (1, 6):
         ms = bench_gemm(A2, B2, g2, H, 2, Y, variant=v, reps=5)
         res.setdefault(f"gemm2_v{v}", []).append(round(2.0 * M * H * F / ms / 1e9, 1))
         ms = bench_gemm(A1, B1, g1, 2 * F, 1, act, variant=v, reps=5)
