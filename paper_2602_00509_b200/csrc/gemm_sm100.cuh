@@ -540,8 +540,9 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 // is 32 KB instead of 48 KB and 6 stages fit.  The leader CTA's single thread issues
 // tcgen05.mma.cta_group::2 (M = 256) reading both CTAs' smem; the accumulator rows of
 // each CTA live in its own TMEM and each CTA's epilogue drains its own 128 rows.
-// Barriers: TMA bytes of both CTAs complete on the LEADER's `full` (count 2: leader
-// expect_tx + peer arrive); MMA commits multicast to both CTAs' `empty` / `tfull`;
+// Barriers: TMA bytes of both CTAs complete on the LEADER's `full` (the leader's expect_tx
+// covers both; the peer cannot refill a stage before the MMA has consumed it, so phases
+// never mix); MMA commits multicast to both CTAs' `empty` / `tfull`;
 // both CTAs' epilogues arrive on the leader's `tempty`.  The leader claims tiles and
 // mirrors them into the peer's queue through DSMEM.
 // =============================================================================
@@ -584,7 +585,7 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
   for (int i = threadIdx.x; i < ng; i += blockDim.x) ts[i] = sched->g[i].tile_start;
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      ptx::mbar_init(&full[s], 2);
+      ptx::mbar_init(&full[s], 1);            // leader's expect_tx covers both CTAs' bytes
       ptx::mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -621,9 +622,10 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
         int tile;
         if (leader) {
           tile = claim_tile(sched, unit);
-          ptx::mbar_wait_cluster(&qempty[qs], qph ^ 1);
+          ptx::mbar_wait(&qempty[qs], qph ^ 1);
           tq[qs] = tile;
           ptx::st_cluster_u32(ptx::mapa(ptx::smem_u32(const_cast<int*>(&tq[qs])), 1), static_cast<uint32_t>(tile));
+          ptx::fence_acq_rel_cluster();          // the DSMEM store before the remote arrive (once per tile)
           ptx::mbar_arrive(&qfull[qs]);
           ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&qfull[qs]), 1));
         } else {
@@ -649,7 +651,6 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
           const int kc = (second ? kb - kb1 : kb) * 64;
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (L::A_BYTES + L::B_BYTES));
-          else ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&full[stage]), 0));
           ptx::tma_load_2d_cg2(ta, &full[stage], sA + stage * L::A_BYTES, kc, arow);
           ptx::tma_load_2d_cg2(tb, &full[stage], sB + stage * L::B_BYTES, kc, brow);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -673,11 +674,11 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
         if (lane == 0) ptx::mbar_arrive(&qempty[qs]);
         if (++qs == kTileQ) { qs = 0; qph ^= 1; }
         if (tile < 0) break;
-        ptx::mbar_wait_cluster(&tempty[acc], aphase ^ 1);
+        ptx::mbar_wait(&tempty[acc], aphase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d = tmem_base + acc * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
-          ptx::mbar_wait_cluster(&full[stage], phase);
+          ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
           if (lane == 0) {
             const uint64_t a0 = ptx::sdesc_sw128(ptx::smem_u32(sA + stage * L::A_BYTES));
