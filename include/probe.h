@@ -225,7 +225,8 @@ probe_status probe_ipc_close(uint64_t dev_ptr_base);
  * thread-per-token select kernel (default off: measured slower). */
 enum { PROBE_OPT_EP_EMULATION = 1, PROBE_OPT_UNFUSED_TOPK = 2, PROBE_OPT_FUSED_EPILOGUE_TOPK = 3,
        PROBE_OPT_AUX_SMS = 4 /* grid cap (CTAs) of the predictor GEMMs on the aux stream; default #SMs/2 */,
-       PROBE_OPT_PAIR_GEMM = 5 /* expert GEMMs on CTA pairs (tcgen05 cta_group::2, 256-row tiles) */ };
+       PROBE_OPT_PAIR_GEMM = 5 /* expert GEMMs on CTA pairs (tcgen05 cta_group::2, 256-row tiles);
+                                  default ON, 0 selects the 1-CTA kernel */ };
 probe_status probe_set_option(probe_ctx ctx, int32_t option, int64_t value);
 
 /* Number of library kernel launches enqueued so far by this context (bench accounting). */

@@ -180,7 +180,7 @@ struct probe_ctx_s {
   bool unfused = false;   // PROBE_UNFUSED=1: logits written + separate top-k kernels (debug)
   bool ep_emulation = false;  // partition expert GEMMs by local rank (probe_set_option)
   bool fused_epi_topk = false;  // top-k in the GEMM epilogue instead of k_select (probe_set_option)
-  bool pair_gemm = false;       // expert GEMMs on CTA pairs (cta_group::2) (probe_set_option)
+  bool pair_gemm = true;        // expert GEMMs on CTA pairs (cta_group::2); option turns it off
   // phase profiling: prof_max forwards × (PROBE_NPHASE + 1) timing events
   int prof_max = 0, prof_n = 0;
   std::vector<cudaEvent_t> prof_ev;

@@ -34,7 +34,7 @@ class CaseCfg:
     sample_tokens: int = 0          # >0: oracle outputs only for this many tokens per rank
     ep_emulation: bool = False      # partitioned expert GEMMs (single-GPU EP straggler emulation)
     fused_epi_topk: bool = False    # router/predictor top-k in the GEMM epilogue
-    pair_gemm: bool = False         # expert GEMMs on CTA pairs (cta_group::2)
+    pair_gemm: bool = True          # expert GEMMs on CTA pairs (cta_group::2); False → 1-CTA kernel
 
 
 def f64(t):
@@ -66,9 +66,9 @@ def run_gpu(case: CaseCfg):
     if case.ep_emulation:
         from paper_2602_00509_b200._lib import OPT_EP_EMULATION
         rt.set_option(OPT_EP_EMULATION, 1)
-    if case.pair_gemm:
+    if not case.pair_gemm:
         from paper_2602_00509_b200._lib import OPT_PAIR_GEMM
-        rt.set_option(OPT_PAIR_GEMM, 1)
+        rt.set_option(OPT_PAIR_GEMM, 0)
     if case.fused_epi_topk:
         from paper_2602_00509_b200._lib import OPT_FUSED_EPILOGUE_TOPK
         rt.set_option(OPT_FUSED_EPILOGUE_TOPK, 1)

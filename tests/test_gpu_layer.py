@@ -28,9 +28,10 @@ CASES = {
     "budget0": CaseCfg(pi.C0, replica_budget=0),
     "fused-epilogue-topk": CaseCfg(pi.C0.with_(name="fe", E=64, k=8, H=512, F=256, T=200, G=4), zipf_s=1.3,
                                   fused_epi_topk=True, bias=True),
-    "pair-gemm": CaseCfg(pi.C0.with_(name="pg", E=32, k=4, H=512, F=384, T=333, G=4), zipf_s=1.3, pair_gemm=True),
-    "pair-gemm-ep-emulation": CaseCfg(pi.C0.with_(name="pge", E=64, k=8, H=512, F=256, T=256, G=8), zipf_s=1.2,
-                                      pair_gemm=True, ep_emulation=True),
+    "one-cta-gemm": CaseCfg(pi.C0.with_(name="pg", E=32, k=4, H=512, F=384, T=333, G=4), zipf_s=1.3,
+                            pair_gemm=False),
+    "one-cta-gemm-ep-emulation": CaseCfg(pi.C0.with_(name="pge", E=64, k=8, H=512, F=256, T=256, G=8), zipf_s=1.2,
+                                         pair_gemm=False, ep_emulation=True),
     "ep-emulation": CaseCfg(pi.C0.with_(name="epem", E=64, k=8, H=512, F=384, T=300, G=8), zipf_s=1.2,
                             ep_emulation=True),
 }
