@@ -216,6 +216,13 @@ probe_status probe_ipc_export(const void* dev_ptr, uint8_t handle[64], uint64_t*
 probe_status probe_ipc_import(const uint8_t handle[64], uint64_t offset, uint64_t* dev_ptr);
 probe_status probe_ipc_close(uint64_t dev_ptr_base);
 
+/* Statistics-based baseline (EPLB-like; not PROBE): history[G,E] (device,
+ * caller-owned) += the actual counts n[G,E] of the last forward of `layer` (reset=1 zeroes
+ * first).  Pass history as probe_plan's pred_counts to plan from past statistics instead
+ * of the lookahead predictor. */
+probe_status probe_history_update(probe_ctx ctx, int32_t layer, int32_t reset, int32_t* history,
+                                  void* stream);
+
 /* Options.  PROBE_OPT_EP_EMULATION (single-GPU emulation only): the expert GEMMs split the
  * persistent grid into local_ranks CTA sets, each serving only its logical rank's tiles, so
  * a rank's GEMM runs on ~#SMs/local_ranks SMs and the GEMM time is the straggler's (Eq. 3)

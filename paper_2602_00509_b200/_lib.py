@@ -22,7 +22,8 @@ STATUS = {0: "PROBE_OK", 1: "PROBE_EINVAL", 2: "PROBE_ESHAPE", 3: "PROBE_EBUDGET
 EXPORTS = ["probe_workspace", "probe_init", "probe_moe_forward", "probe_predict", "probe_plan",
            "probe_prefetch", "probe_debug_layout", "probe_test_gemm", "probe_check", "probe_last_error",
            "probe_finalize", "probe_launch_count", "probe_profile", "probe_profile_read", "probe_bench_gemm",
-           "probe_ipc_export", "probe_ipc_import", "probe_ipc_close", "probe_set_option"]
+           "probe_ipc_export", "probe_ipc_import", "probe_ipc_close", "probe_set_option",
+           "probe_history_update"]
 OPT_EP_EMULATION, OPT_UNFUSED_TOPK, OPT_FUSED_EPILOGUE_TOPK, OPT_AUX_SMS, OPT_PAIR_GEMM = 1, 2, 3, 4, 5
 PROBE_NPHASE = 10
 PHASES = ["gate", "select", "counts", "layout", "dispatch", "wait", "gemm1", "gemm2", "combine", "total"]
@@ -78,6 +79,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "probe_ipc_import": (i32, [C.POINTER(C.c_uint8), C.c_uint64, C.POINTER(C.c_uint64)]),
         "probe_ipc_close": (i32, [C.c_uint64]),
         "probe_set_option": (i32, [vp, i32, i64]),
+        "probe_history_update": (i32, [vp, i32, i32, vp, vp]),
         "probe_check": (i32, [vp]),
         "probe_last_error": (C.c_char_p, [vp]),
         "probe_finalize": (i32, [vp]),

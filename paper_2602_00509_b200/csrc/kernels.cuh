@@ -321,6 +321,12 @@ __global__ void k_pred_publish(Dims d, const int32_t* __restrict__ pred_local, S
   }
 }
 
+// history[g][e] = (reset ? 0 : history[g][e]) + n[g][e]  (statistics-based baseline policy)
+__global__ void k_history(int n_elems, const int32_t* __restrict__ counts, int32_t* __restrict__ hist, int reset) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_elems; i += gridDim.x * blockDim.x)
+    hist[i] = (reset ? 0 : hist[i]) + counts[i];
+}
+
 __global__ void k_copy_i32(const int32_t* __restrict__ src, int32_t* __restrict__ dst, int n) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = src[i];
 }

@@ -960,6 +960,17 @@ probe_status probe_finalize(probe_ctx ctx) {
 
 int64_t probe_launch_count(probe_ctx ctx) { return ctx ? ctx->launches : 0; }
 
+probe_status probe_history_update(probe_ctx ctx, int32_t layer, int32_t reset, int32_t* history, void* stream) {
+  if (!ctx || !history) return fail(ctx, PROBE_EINVAL, "probe_history_update: null argument");
+  if (ctx->fwd_layer < layer || ((ctx->fwd_layer - layer) > 1))
+    return fail(ctx, PROBE_ESTATE, "probe_history_update(%d): counts of that layer are no longer on the board", layer);
+  const Dims& d = ctx->d;
+  const int32_t* board = reinterpret_cast<const int32_t*>(ctx->local_base[PROBE_BUF_BOARD]) + (((layer & 1) * 2 + 0) * d.G) * d.E;
+  k_history<<<(d.G * d.E + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(d.G * d.E, board, history, reset);
+  CKL();
+  return PROBE_OK;
+}
+
 probe_status probe_set_option(probe_ctx ctx, int32_t option, int64_t value) {
   if (!ctx) return fail(nullptr, PROBE_EINVAL, "null ctx");
   switch (option) {

@@ -168,6 +168,10 @@ class ProbeRuntime:
               self.ctx)
         return out[:n.value]
 
+    def history_update(self, layer: int, history, reset: bool = False, stream=None):
+        st = self.lib.probe_history_update(self.ctx, layer, int(reset), _ptr(history), _stream(stream))
+        check("probe_history_update", st, self.ctx)
+
     def set_option(self, option: int, value: int):
         check("probe_set_option", self.lib.probe_set_option(self.ctx, option, int(value)), self.ctx)
 

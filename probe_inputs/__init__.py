@@ -136,11 +136,15 @@ class RankDesign:
 
 
 def draw_routing(shape: MoEShape, step: int, layer: int, rank: int, zipf_s: float,
-                 hot_period: int = 1) -> np.ndarray:
+                 hot_period: int = 1, perm_key=None) -> np.ndarray:
     """Gumbel-top-k (without replacement) of log popularity; the popularity
-    permutation is redrawn every `hot_period` steps (hotspot migration)."""
+    permutation is redrawn every `hot_period` steps (hotspot migration).  `perm_key`
+    fixes the permutation independently of (step, layer) (stationary hotspots)."""
     E, k, T = shape.E, shape.k, shape.T
-    perm = rng(shape.name, step // hot_period, layer, "perm", zipf_s).permutation(E)
+    if perm_key is None:
+        perm = rng(shape.name, step // hot_period, layer, "perm", zipf_s).permutation(E)
+    else:
+        perm = rng(shape.name, "perm-key", perm_key, zipf_s).permutation(E)
     pop = zipf_popularity(E, zipf_s, perm)
     g = rng(shape.name, step, layer, rank, "gumbel", zipf_s).gumbel(size=(T, E))
     key = np.log(pop)[None, :] + g
@@ -150,12 +154,12 @@ def draw_routing(shape: MoEShape, step: int, layer: int, rank: int, zipf_s: floa
 
 def design_rank(shape: MoEShape, step: int, layer: int, rank: int, zipf_s: float,
                 accuracy: float, hot_period: int = 1, ties: bool = True,
-                wrap: Optional[int] = None) -> RankDesign:
+                wrap: Optional[int] = None, perm_key=None) -> RankDesign:
     """wrap: layers form a cycle of this length (layer L's "next layer" is (L+1) mod wrap)."""
     E, k, T = shape.E, shape.k, shape.T
-    S = draw_routing(shape, step, layer, rank, zipf_s, hot_period)
+    S = draw_routing(shape, step, layer, rank, zipf_s, hot_period, perm_key)
     nxt = layer + 1 if wrap is None else (layer + 1) % wrap
-    S_next = draw_routing(shape, step, nxt, rank, zipf_s, hot_period)
+    S_next = draw_routing(shape, step, nxt, rank, zipf_s, hot_period, perm_key)
     r = rng(shape.name, step, layer, rank, "design", zipf_s, accuracy)
     numer = np.tile(np.arange(16, 16 - k, -1, dtype=np.int64), (T, 1))
     tie_e = np.full(T, -1, dtype=np.int64)
@@ -277,12 +281,13 @@ class LayerInputs:
 
 def layer_inputs(shape: MoEShape, step: int, layer: int, zipf_s: float = 1.0,
                  accuracy: float = 0.9, ranks: Optional[List[int]] = None, device="cpu",
-                 hot_period: int = 1, ties: bool = True, wrap: Optional[int] = None) -> LayerInputs:
+                 hot_period: int = 1, ties: bool = True, wrap: Optional[int] = None,
+                 perm_key=None) -> LayerInputs:
     ranks = list(range(shape.G)) if ranks is None else ranks
     p = layer % 2
     xs, ds = [], []
     for r in ranks:
-        d = design_rank(shape, step, layer, r, zipf_s, accuracy, hot_period, ties, wrap)
+        d = design_rank(shape, step, layer, r, zipf_s, accuracy, hot_period, ties, wrap, perm_key)
         xs.append(encode_tokens(shape, d, p, step, layer, r, device))
         ds.append(d)
     return LayerInputs(layer, p, torch.stack(xs), ds)
