@@ -1,0 +1,81 @@
+"""GPU: the single-CTA planner kernel (Algorithm 1, R10-R22) bit-exact against the oracle's
+greedy on explicit n̂ matrices (random skewed loads, comm term, n_sat knee, window-derived
+caps, budgets 0..3), and the statistics-based history hook feeding the same planner."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _rt(G, E, **kw):
+    from paper_2602_00509_b200 import ProbeConfig, ProbeRuntime
+    cfg = ProbeConfig(G=G, E=E, k=2, H=256, F=256, T=64, h=64, **kw)
+    return ProbeRuntime(cfg), cfg
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_planner_kernel_matches_oracle(seed):
+    r = np.random.default_rng(seed)
+    G = int(r.choice([2, 4, 8]))
+    E = G * int(r.choice([2, 4, 8, 16, 32]))
+    E = min(E, 256)
+    rb = int(r.integers(0, 4))
+    alpha, beta, nsat = int(r.integers(1, 9000)), int(r.integers(0, 12000)), int(r.integers(0, 300))
+    rt, cfg = _rt(G, E, replica_budget=rb, alpha_ps=alpha, beta_ps=beta, n_sat=nsat, bw_bytes_per_us=770_000)
+    pop = (np.arange(1, E + 1) ** -1.2)[r.permutation(E)]
+    nhat = r.poisson(4000 * pop / pop.sum() * E / G, size=(G, E)).astype(np.int32)
+    wbytes = 6 * 256 * 256
+    windows = r.integers(0, 4 * wbytes * 1000 // 770_000 + 2, size=G).astype(np.int64)
+    reps = torch.empty(G, 3, dtype=torch.int32, device="cuda")
+    quota = torch.empty(G, E, G, dtype=torch.int32, device="cuda")
+    stats = torch.empty(8, dtype=torch.int64, device="cuda")
+    rt.plan(1, torch.from_numpy(windows).cuda(), pred_counts=torch.from_numpy(nhat).cuda(), replicas=reps,
+            quota=quota, stats=stats)
+    torch.cuda.synchronize()
+    pc = O.PlannerConfig(G=G, E=E, replica_budget=rb, kmax=16, alpha_ps=alpha, beta_ps=beta, n_sat=nsat,
+                         bw_bytes_per_us=770_000, expert_bytes=wbytes)
+    plan = O.plan_greedy(nhat, windows.tolist(), pc)
+    exp = np.full((G, 3), -1)
+    for g in range(G):
+        exp[g, :len(plan.replicas[g])] = plan.replicas[g]
+    assert np.array_equal(reps.cpu().numpy(), exp)
+    assert np.array_equal(quota.cpu().numpy(), plan.quota)
+    st = stats.cpu().numpy()
+    assert (st[0], st[1], st[2], st[3]) == (plan.iterations, len(plan.transfers), plan.maxL_before, plan.maxL_after)
+    rt.close()
+
+
+def test_history_hook_feeds_planner():
+    import probe_inputs as pi
+    sh = pi.C0.with_(name="hist", E=16, k=2, H=256, F=256, T=128, G=4)
+    from paper_2602_00509_b200 import ProbeConfig, ProbeRuntime
+    cfg = ProbeConfig(G=sh.G, E=sh.E, k=sh.k, H=sh.H, F=sh.F, T=sh.T, h=sh.h)
+    rt = ProbeRuntime(cfg)
+    W = pi.router_weight(sh, 0, device="cuda")
+    w13, w2 = pi.expert_weights(sh, 0, device="cuda")
+    out = torch.empty(sh.G, sh.T, sh.H, device="cuda")
+    hist = torch.zeros(sh.G, sh.E, dtype=torch.int32, device="cuda")
+    counts = torch.empty(sh.G, sh.E, dtype=torch.int32, device="cuda")
+    total = np.zeros((sh.G, sh.E), dtype=np.int64)
+    for L in range(3):
+        li = pi.layer_inputs(sh, L, 0, 1.3, device="cuda")      # parity-0 router for every layer
+        rt.forward(2 * L, li.x, W, None, w13, w2, out)
+        rt.history_update(2 * L, hist, reset=(L == 0))
+        rt.debug_layout(counts=counts)
+        torch.cuda.synchronize()
+        total += counts.cpu().numpy()
+    assert np.array_equal(hist.cpu().numpy(), total)
+    reps = torch.empty(sh.G, 3, dtype=torch.int32, device="cuda")
+    win = torch.full((sh.G,), 10 ** 9, dtype=torch.int64, device="cuda")
+    rt.plan(7, win, pred_counts=hist, replicas=reps)
+    torch.cuda.synchronize()
+    pc = O.PlannerConfig(G=sh.G, E=sh.E, alpha_ps=1, beta_ps=0, expert_bytes=6 * sh.H * sh.F)
+    plan = O.plan_greedy(total, [10 ** 9] * sh.G, pc)
+    exp = np.full((sh.G, 3), -1)
+    for g in range(sh.G):
+        exp[g, :len(plan.replicas[g])] = plan.replicas[g]
+    assert np.array_equal(reps.cpu().numpy(), exp)
+    rt.close()
