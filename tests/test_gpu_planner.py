@@ -20,8 +20,7 @@ def _rt(G, E, **kw):
 def test_planner_kernel_matches_oracle(seed):
     r = np.random.default_rng(seed)
     G = int(r.choice([2, 4, 8]))
-    E = G * int(r.choice([2, 4, 8, 16, 32]))
-    E = min(E, 256)
+    E = min(max(8, G * int(r.choice([2, 4, 8, 16, 32]))), 256)     # E % G == 0 and E % 8 == 0
     rb = int(r.integers(0, 4))
     alpha, beta, nsat = int(r.integers(1, 9000)), int(r.integers(0, 12000)), int(r.integers(0, 300))
     rt, cfg = _rt(G, E, replica_budget=rb, alpha_ps=alpha, beta_ps=beta, n_sat=nsat, bw_bytes_per_us=770_000)
