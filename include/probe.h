@@ -223,6 +223,36 @@ probe_status probe_ipc_close(uint64_t dev_ptr_base);
 probe_status probe_history_update(probe_ctx ctx, int32_t layer, int32_t reset, int32_t* history,
                                   void* stream);
 
+/* Scale-driven online distillation of the predictor residual (P:387-390
+ * "minimizing the Cross-Entropy loss between the predictor's output and the ground-truth
+ * router's probability distribution"; readings R33-R37 in DESIGN.md §2.5).
+ *
+ * probe_distill_grad: for the GL·T tokens of the local ranks ([GL·T, H] bf16, rank-major as
+ * in probe_predict), x = the hidden state the predictor reads (entering layer L−1), x_next =
+ * the hidden state entering layer L (the teacher's input), w_router/b_router = layer L's
+ * frozen router (bf16 [E,H], fp32 [E] or NULL), w_res1 bf16 [h,H] / w_res2 bf16 [E,h] = the
+ * residual the product path uses.  Computes, all on device:
+ *   student l̂ = W x + b + Ŵ² bf16(SiLU(Ŵ¹ x)),  teacher t = W x_next + b,
+ *   loss = Σ_t CE(softmax(t_t), softmax(l̂_t)),
+ *   grad_res1 fp32 [h,H] = ∂loss/∂Ŵ¹,  grad_res2 fp32 [E,h] = ∂loss/∂Ŵ²  (overwritten; the
+ *   gradient of the SUM over these tokens, R34 — shards add them, then divide by the total),
+ *   stats fp64 [4] (overwritten) = {Σ CE, Σ|S∩P|, Σ|S^⌈k/2⌉∩P|, Σ|S∩P^2k|} with S / P the
+ *   teacher / student top-k sets (R37: top-K accuracy, top-half-K hit, 2×top-K recall);
+ *   student_logits / teacher_logits fp32 [GL·T, E] (optional outputs, WITHOUT the bias).
+ * The first call allocates a workspace (~N·(10h + 12E + 2H) bytes, N = local_ranks ·
+ * max_tokens) and must not be inside a stream capture.  stream NULL = the context's aux
+ * stream; inputs must be complete on `stream`.  Errors: PROBE_EINVAL (null), PROBE_ESHAPE
+ * (res_hidden == 0), PROBE_ECAPACITY (T), PROBE_ESTATE (first call under capture).
+ *
+ * probe_distill_apply (R36): master[i] += scale · grad[i] (fp32, n elements; scale =
+ * −lr / N_total) and w[i] = bf16(master[i]) — the bf16 copy the product path reads. */
+probe_status probe_distill_grad(probe_ctx ctx, const void* x, const void* x_next, int32_t T, const void* w_router,
+                                const float* b_router, const void* w_res1, const void* w_res2, float* grad_res1,
+                                float* grad_res2, double* stats, float* student_logits, float* teacher_logits,
+                                void* stream);
+probe_status probe_distill_apply(probe_ctx ctx, float* master, const float* grad, void* w, int64_t n, float scale,
+                                 void* stream);
+
 /* Options.  PROBE_OPT_EP_EMULATION (single-GPU emulation only): the expert GEMMs split the
  * persistent grid into local_ranks CTA sets, each serving only its logical rank's tiles, so
  * a rank's GEMM runs on ~#SMs/local_ranks SMs and the GEMM time is the straggler's (Eq. 3)

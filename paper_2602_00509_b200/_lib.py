@@ -23,7 +23,7 @@ EXPORTS = ["probe_workspace", "probe_init", "probe_moe_forward", "probe_predict"
            "probe_prefetch", "probe_debug_layout", "probe_test_gemm", "probe_check", "probe_last_error",
            "probe_finalize", "probe_launch_count", "probe_profile", "probe_profile_read", "probe_bench_gemm",
            "probe_ipc_export", "probe_ipc_import", "probe_ipc_close", "probe_set_option",
-           "probe_history_update"]
+           "probe_history_update", "probe_distill_grad", "probe_distill_apply"]
 OPT_EP_EMULATION, OPT_UNFUSED_TOPK, OPT_FUSED_EPILOGUE_TOPK, OPT_AUX_SMS, OPT_PAIR_GEMM = 1, 2, 3, 4, 5
 PROBE_NPHASE = 10
 PHASES = ["gate", "select", "counts", "layout", "dispatch", "wait", "gemm1", "gemm2", "combine", "total"]
@@ -80,6 +80,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "probe_ipc_close": (i32, [C.c_uint64]),
         "probe_set_option": (i32, [vp, i32, i64]),
         "probe_history_update": (i32, [vp, i32, i32, vp, vp]),
+        "probe_distill_grad": (i32, [vp, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+        "probe_distill_apply": (i32, [vp, vp, vp, vp, i64, C.c_float, vp]),
         "probe_check": (i32, [vp]),
         "probe_last_error": (C.c_char_p, [vp]),
         "probe_finalize": (i32, [vp]),

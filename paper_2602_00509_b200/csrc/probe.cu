@@ -14,6 +14,7 @@
 
 #include "../../include/probe.h"
 #include "kernels.cuh"
+#include "distill.cuh"
 
 using namespace probe;
 
@@ -181,6 +182,9 @@ struct probe_ctx_s {
   bool ep_emulation = false;  // partition expert GEMMs by local rank (probe_set_option)
   bool fused_epi_topk = false;  // top-k in the GEMM epilogue instead of k_select (probe_set_option)
   bool pair_gemm = true;        // expert GEMMs on CTA pairs (cta_group::2); option turns it off
+  // distillation workspace (NEXT-1), allocated on the first probe_distill_grad
+  uint8_t* dbuf = nullptr;
+  size_t dbytes = 0;
   // phase profiling: prof_max forwards × (PROBE_NPHASE + 1) timing events
   int prof_max = 0, prof_n = 0;
   std::vector<cudaEvent_t> prof_ev;
@@ -954,6 +958,7 @@ probe_status probe_finalize(probe_ctx ctx) {
   }
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
   if (ctx->pf) cudaStreamDestroy(ctx->pf);
+  if (ctx->dbuf) cudaFree(ctx->dbuf);
   delete ctx;
   return PROBE_OK;
 }
@@ -967,6 +972,139 @@ probe_status probe_history_update(probe_ctx ctx, int32_t layer, int32_t reset, i
   const Dims& d = ctx->d;
   const int32_t* board = reinterpret_cast<const int32_t*>(ctx->local_base[PROBE_BUF_BOARD]) + (((layer & 1) * 2 + 0) * d.G) * d.E;
   k_history<<<(d.G * d.E + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(d.G * d.E, board, history, reset);
+  CKL();
+  return PROBE_OK;
+}
+
+// ---- NEXT-1: online distillation of the predictor residual (R33-R37) ----------
+// Workspace for N = local_ranks · max_tokens tokens, Np = N rounded up to 64:
+//   z fp32 [N,h] | a bf16 [N,h] | aT [h,Np] | lhat, t fp32 [N,E] | gl bf16 [N,E] | glT [E,Np]
+//   | ga fp32 [N,h] | gzT [h,Np] | xT [H,Np] | w2T [h,E] | 6 GEMM schedules
+struct DistillLayout {
+  size_t z, a, aT, lhat, t, gl, glT, ga, gzT, xT, w2T, sched, total;
+  uint64_t Np;
+};
+
+static DistillLayout distill_layout(const probe_config& c) {
+  DistillLayout L{};
+  const uint64_t N = static_cast<uint64_t>(c.local_ranks) * c.max_tokens, Np = al(N, 64);
+  const uint64_t h = c.res_hidden, E = c.num_experts, H = c.hidden;
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o += al(bytes, 1024); return r; };
+  L.Np = Np;
+  L.z = take(N * h * 4);
+  L.a = take(N * h * 2);
+  L.aT = take(h * Np * 2);
+  L.lhat = take(N * E * 4);
+  L.t = take(N * E * 4);
+  L.gl = take(N * E * 2);
+  L.glT = take(E * Np * 2);
+  L.ga = take(N * h * 4);
+  L.gzT = take(h * Np * 2);
+  L.xT = take(H * Np * 2);
+  L.w2T = take(h * E * 2);
+  L.sched = take(6 * sizeof(GemmSched));
+  L.total = o;
+  return L;
+}
+
+probe_status probe_distill_grad(probe_ctx ctx, const void* x, const void* x_next, int32_t T, const void* w_router,
+                                const float* b_router, const void* w_res1, const void* w_res2, float* grad_res1,
+                                float* grad_res2, double* stats, float* student_logits, float* teacher_logits,
+                                void* stream) {
+  if (!ctx) return fail(nullptr, PROBE_EINVAL, "null ctx");
+  if (!x || !x_next || !w_router || !w_res1 || !w_res2 || !grad_res1 || !grad_res2 || !stats)
+    return fail(ctx, PROBE_EINVAL, "probe_distill_grad: null pointer");
+  if (ctx->cfg.res_hidden <= 0) return fail(ctx, PROBE_ESHAPE, "probe_distill_grad: res_hidden == 0");
+  if (T < 1 || T > ctx->cfg.max_tokens) return fail(ctx, PROBE_ECAPACITY, "T=%d outside [1, max_tokens]", T);
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->aux;
+  const DistillLayout DL = distill_layout(ctx->cfg);
+  if (!ctx->dbuf) {
+    if (capture_id(st) != 0)
+      return fail(ctx, PROBE_ESTATE, "probe_distill_grad: first call (workspace allocation) inside stream capture");
+    CK(cudaMalloc(&ctx->dbuf, DL.total));
+    ctx->dbytes = DL.total;
+  }
+  const Dims& d = ctx->d;
+  const int N = d.GL * T, H = d.H, E = d.E, h = d.h;
+  const uint64_t Np = al(static_cast<uint64_t>(N), 64);
+  uint8_t* B = ctx->dbuf;
+  float* z = reinterpret_cast<float*>(B + DL.z);
+  auto* a = reinterpret_cast<__nv_bfloat16*>(B + DL.a);
+  auto* aT = reinterpret_cast<__nv_bfloat16*>(B + DL.aT);
+  float* lhat = student_logits ? student_logits : reinterpret_cast<float*>(B + DL.lhat);
+  float* tl = teacher_logits ? teacher_logits : reinterpret_cast<float*>(B + DL.t);
+  auto* gl = reinterpret_cast<__nv_bfloat16*>(B + DL.gl);
+  auto* glT = reinterpret_cast<__nv_bfloat16*>(B + DL.glT);
+  float* ga = reinterpret_cast<float*>(B + DL.ga);
+  auto* gzT = reinterpret_cast<__nv_bfloat16*>(B + DL.gzT);
+  auto* xT = reinterpret_cast<__nv_bfloat16*>(B + DL.xT);
+  auto* w2T = reinterpret_cast<__nv_bfloat16*>(B + DL.w2T);
+  GemmSched* sch = reinterpret_cast<GemmSched*>(B + DL.sched);
+  const CUtensorMap* mx = ctx->maps.get(x, N, H, 128);
+  const CUtensorMap* mxn = ctx->maps.get(x_next, N, H, 128);
+  const CUtensorMap* mw = ctx->maps.get(w_router, E, H, 64);
+  const CUtensorMap* m1 = ctx->maps.get(w_res1, h, H, 64);
+  const CUtensorMap* m2 = ctx->maps.get(w_res2, E, h, 64);
+  const CUtensorMap* ma = ctx->maps.get(a, N, h, 128);
+  if (!mx || !mxn || !mw || !m1 || !m2 || !ma) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
+  auto gemm = [&](int si, const CUtensorMap& A, const CUtensorMap& B0, const CUtensorMap& B1, int m, int n, int K,
+                  float* out, const CUtensorMap* A2, int K2) -> probe_status {
+    SmallGroups sg{};
+    sg.BN = 128;
+    sg.n = 1;
+    sg.g[0] = mk_group(0, m, 0, 0, EPI_F32, n, n, out);
+    k_write_sched<<<1, 32, 0, st>>>(sch + si, sg);
+    CKL();
+    CK(launch_gemm_v(V_128_6_4, A, B0, B1, A, sch + si, K, ctx->aux_sms, st, A2, K2));
+    ++ctx->launches;
+    return PROBE_OK;
+  };
+  const dim3 tb(32, 8);
+  probe_status r;
+  CK(cudaMemsetAsync(stats, 0, 4 * sizeof(double), st));
+  // operands that the backward contracts over tokens: xᵀ, Ŵ²ᵀ
+  k_transpose_bf16<<<dim3((H + 31) / 32, static_cast<unsigned>((Np + 31) / 32)), tb, 0, st>>>(
+      static_cast<const __nv_bfloat16*>(x), xT, N, H, static_cast<int>(Np));
+  CKL();
+  k_transpose_bf16<<<dim3((h + 31) / 32, (E + 31) / 32), tb, 0, st>>>(static_cast<const __nv_bfloat16*>(w_res2), w2T,
+                                                                      E, h, E);
+  CKL();
+  // forward: z = x Ŵ¹ᵀ;  a = bf16(σ(z));  l̂ = [x | a]·[W | Ŵ²]ᵀ (Eq. (P));  t = x' Wᵀ (R33)
+  if ((r = gemm(0, *mx, *m1, *m1, N, h, H, z, nullptr, 0)) != PROBE_OK) return r;
+  k_act_fwd<<<dim3((h + 31) / 32, static_cast<unsigned>((Np + 31) / 32)), tb, 0, st>>>(z, a, aT, N, h,
+                                                                                      static_cast<int>(Np));
+  CKL();
+  if ((r = gemm(1, *mx, *mw, *m2, N, E, H, lhat, ma, h)) != PROBE_OK) return r;
+  if ((r = gemm(2, *mxn, *mw, *mw, N, E, H, tl, nullptr, 0)) != PROBE_OK) return r;
+  // softmax / CE / g_l = q − p / fidelity (R34, R37)
+  k_distill_ce<<<(N + 31) / 32, 256, 0, st>>>(lhat, tl, b_router, N, E, d.k, static_cast<int>(Np), gl, glT, stats);
+  CKL();
+  // backward (R34, R35): ∇Ŵ² = g_lᵀ a;  g_a = g_l Ŵ²;  g_z = g_a ⊙ σ'(z);  ∇Ŵ¹ = g_zᵀ x
+  const CUtensorMap* mglT = ctx->maps.get(glT, E, Np, 128);
+  const CUtensorMap* maT = ctx->maps.get(aT, h, Np, 64);
+  const CUtensorMap* mgl = ctx->maps.get(gl, N, E, 128);
+  const CUtensorMap* mw2T = ctx->maps.get(w2T, h, E, 64);
+  const CUtensorMap* mgzT = ctx->maps.get(gzT, h, Np, 128);
+  const CUtensorMap* mxT = ctx->maps.get(xT, H, Np, 64);
+  if (!mglT || !maT || !mgl || !mw2T || !mgzT || !mxT) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
+  if ((r = gemm(3, *mglT, *maT, *maT, E, h, static_cast<int>(Np), grad_res2, nullptr, 0)) != PROBE_OK) return r;
+  if ((r = gemm(4, *mgl, *mw2T, *mw2T, N, h, E, ga, nullptr, 0)) != PROBE_OK) return r;
+  k_silu_bwd<<<dim3((h + 31) / 32, static_cast<unsigned>((Np + 31) / 32)), tb, 0, st>>>(ga, z, gzT, N, h,
+                                                                                       static_cast<int>(Np));
+  CKL();
+  if ((r = gemm(5, *mgzT, *mxT, *mxT, h, H, static_cast<int>(Np), grad_res1, nullptr, 0)) != PROBE_OK) return r;
+  return PROBE_OK;
+}
+
+probe_status probe_distill_apply(probe_ctx ctx, float* master, const float* grad, void* w, int64_t n, float scale,
+                                 void* stream) {
+  if (!ctx) return fail(nullptr, PROBE_EINVAL, "null ctx");
+  if (!master || !grad || !w || n < 0) return fail(ctx, PROBE_EINVAL, "probe_distill_apply: bad arguments");
+  if (n == 0) return PROBE_OK;
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->aux;
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, static_cast<int64_t>(ctx->num_sms) * 8);
+  k_sgd<<<static_cast<unsigned>(blocks), 256, 0, st>>>(master, grad, static_cast<__nv_bfloat16*>(w), n, scale);
   CKL();
   return PROBE_OK;
 }

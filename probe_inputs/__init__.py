@@ -308,3 +308,38 @@ def bf16_to_numpy_f64(t: torch.Tensor) -> np.ndarray:
     """Exact decode of a bf16 tensor to float64 numpy (bit manipulation only)."""
     bits = t.detach().cpu().contiguous().view(torch.int16).numpy().astype(np.uint16).astype(np.uint32)
     return (bits << 16).view(np.float32).astype(np.float64)
+
+
+# ----------------------------------------------------------------------------
+# Distillation task (SURVEY NEXT-1; DESIGN.md §3): "feature drift" between adjacent layers
+# ----------------------------------------------------------------------------
+
+@dataclasses.dataclass
+class DistillTask:
+    x: torch.Tensor        # [G, T, H] bf16: the hidden state the predictor reads
+    x_next: torch.Tensor   # [G, T, H] bf16: the hidden state the teacher router reads
+    W: torch.Tensor        # [E, H] bf16: the frozen router of the predicted layer
+    drifted: np.ndarray    # experts whose routing mass the drift relabels
+
+
+def distill_task(shape: MoEShape, step: int, zipf_s: float = 1.2, drift_frac: float = 0.25,
+                 router_scale: float = 4.0, device="cpu") -> DistillTask:
+    """x = layer-0 inputs (whose parity-1 encoding is the prior's prediction P_t); x_next = x
+    plus a fixed linear drift that moves the parity-1 coefficient of every expert e in a
+    seeded set D (|D| = drift_frac·E) onto the next expert of D (cyclic), so the teacher's
+    top-k is P_t relabelled on D: the frozen prior misses those slots (the "untrained"
+    accuracy) and a residual that learns the relabelling recovers them.  The router
+    is the parity-1 router scaled by `router_scale` (a power of two: exact in bf16), which
+    sharpens the teacher distribution without changing any top-k set."""
+    E, n_h = shape.E, shape.n_h
+    li = layer_inputs(shape, step, 0, zipf_s, accuracy=1.0, device=device)
+    D = np.sort(rng(shape.name, "drift-set").choice(E, size=max(2, int(round(drift_frac * E))), replace=False))
+    pi = np.roll(D, -1)
+    Hd = torch.from_numpy(hadamard_rows(n_h, E + D).astype(np.float32)).to(device)
+    Hp = torch.from_numpy(hadamard_rows(n_h, E + pi).astype(np.float32)).to(device)
+    xf = li.x.float()
+    coef = xf[..., :n_h] @ Hd.T                       # ⟨x, h_{E+e}⟩ (exact small integers)
+    xn = li.x.clone()
+    xn[..., :n_h] = (xf[..., :n_h] + coef @ (Hp - Hd) / n_h).to(torch.bfloat16)
+    W = (router_weight(shape, 1).float() * router_scale).to(torch.bfloat16).to(device)
+    return DistillTask(li.x, xn, W, D)
