@@ -237,19 +237,21 @@ probe_status probe_history_update(probe_ctx ctx, int32_t layer, int32_t reset, i
  *   grad_res1 fp32 [h,H] = ∂loss/∂Ŵ¹,  grad_res2 fp32 [E,h] = ∂loss/∂Ŵ²  (overwritten; the
  *   gradient of the SUM over these tokens, R34 — shards add them, then divide by the total),
  *   stats fp64 [4] (overwritten) = {Σ CE, Σ|S∩P|, Σ|S^⌈k/2⌉∩P|, Σ|S∩P^2k|} with S / P the
- *   teacher / student top-k sets (R37: top-K accuracy, top-half-K hit, 2×top-K recall);
+ *   teacher / student top-k sets (R37: top-K accuracy, top-half-K hit, 2×top-K recall); the
+ *   three hit counts are computed only if `fidelity` != 0 (else 0: they cost 24 serial warp
+ *   argmaxes per token);
  *   student_logits / teacher_logits fp32 [GL·T, E] (optional outputs, WITHOUT the bias).
  * The first call allocates a workspace (~N·(10h + 12E + 2H) bytes, N = local_ranks ·
- * max_tokens) and must not be inside a stream capture.  stream NULL = the context's aux
- * stream; inputs must be complete on `stream`.  Errors: PROBE_EINVAL (null), PROBE_ESHAPE
+ * max_tokens) and must not be inside a stream capture.  Everything runs on `stream` (NULL =
+ * the legacy default stream, as in plain CUDA); inputs must be complete on it.  Errors: PROBE_EINVAL (null), PROBE_ESHAPE
  * (res_hidden == 0), PROBE_ECAPACITY (T), PROBE_ESTATE (first call under capture).
  *
  * probe_distill_apply (R36): master[i] += scale · grad[i] (fp32, n elements; scale =
  * −lr / N_total) and w[i] = bf16(master[i]) — the bf16 copy the product path reads. */
 probe_status probe_distill_grad(probe_ctx ctx, const void* x, const void* x_next, int32_t T, const void* w_router,
                                 const float* b_router, const void* w_res1, const void* w_res2, float* grad_res1,
-                                float* grad_res2, double* stats, float* student_logits, float* teacher_logits,
-                                void* stream);
+                                float* grad_res2, double* stats, int32_t fidelity, float* student_logits,
+                                float* teacher_logits, void* stream);
 probe_status probe_distill_apply(probe_ctx ctx, float* master, const float* grad, void* w, int64_t n, float scale,
                                  void* stream);
 

@@ -80,7 +80,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "probe_ipc_close": (i32, [C.c_uint64]),
         "probe_set_option": (i32, [vp, i32, i64]),
         "probe_history_update": (i32, [vp, i32, i32, vp, vp]),
-        "probe_distill_grad": (i32, [vp, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+        "probe_distill_grad": (i32, [vp, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp]),
         "probe_distill_apply": (i32, [vp, vp, vp, vp, i64, C.c_float, vp]),
         "probe_check": (i32, [vp]),
         "probe_last_error": (C.c_char_p, [vp]),

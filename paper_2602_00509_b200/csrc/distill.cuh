@@ -38,19 +38,35 @@ __global__ void k_act_fwd(const float* __restrict__ z, __nv_bfloat16* __restrict
   }
 }
 
-// dst [C, Rp] = src [R, C]ᵀ (bf16), columns ≥ R zero.
-__global__ void k_transpose_bf16(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dst, int R, int C,
-                                 int Rp) {
-  __shared__ __nv_bfloat16 tile[32][33];
-  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
-  for (int i = threadIdx.y; i < 32; i += 8) {
-    const int r = r0 + i, c = c0 + threadIdx.x;
-    tile[i][threadIdx.x] = (r < R && c < C) ? src[static_cast<size_t>(r) * C + c] : __float2bfloat16(0.f);
+// dst [C, Rp] = src [R, C]ᵀ (bf16), columns ≥ R zero.  64×64 tiles, 16-byte global
+// accesses on both sides; shared tile rows are 128 B with the 16-byte chunk index XORed by
+// (row / 8) so the column gathers of the store phase hit 8 different bank groups.
+// Requires C % 8 == 0 and Rp % 8 == 0.
+__global__ void __launch_bounds__(256) k_transpose_bf16(const __nv_bfloat16* __restrict__ src,
+                                                        __nv_bfloat16* __restrict__ dst, int R, int C, int Rp) {
+  __shared__ __align__(16) __nv_bfloat16 tile[64 * 64];
+  const int c0 = blockIdx.x * 64, r0 = blockIdx.y * 64;
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const int v = threadIdx.x + 256 * it, r = v >> 3, cv = v & 7;
+    uint4 val = make_uint4(0, 0, 0, 0);
+    if (r0 + r < R && c0 + cv * 8 < C)
+      val = *reinterpret_cast<const uint4*>(src + static_cast<size_t>(r0 + r) * C + c0 + cv * 8);
+    *reinterpret_cast<uint4*>(tile + r * 64 + ((cv ^ (r >> 3)) & 7) * 8) = val;
   }
   __syncthreads();
-  for (int i = threadIdx.y; i < 32; i += 8) {
-    const int c = c0 + i, r = r0 + threadIdx.x;
-    if (c < C && r < Rp) dst[static_cast<size_t>(c) * Rp + r] = tile[threadIdx.x][i];
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const int v = threadIdx.x + 256 * it, oc = v >> 3, rv = v & 7;
+    if (c0 + oc >= C || r0 + rv * 8 >= Rp) continue;
+    __align__(16) __nv_bfloat16 o[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = rv * 8 + i;
+      o[i] = tile[r * 64 + (((oc >> 3) ^ (r >> 3)) & 7) * 8 + (oc & 7)];
+    }
+    *reinterpret_cast<uint4*>(dst + static_cast<size_t>(c0 + oc) * Rp + r0 + rv * 8) =
+        *reinterpret_cast<const uint4*>(o);
   }
 }
 
@@ -99,22 +115,19 @@ __device__ __forceinline__ int warp_pick(const float (&v)[8], uint32_t taken, in
 // One warp per token row: teacher p = softmax(t + b), student q = softmax(l̂ + b) (R33),
 // CE = logsumexp(l̂+b) − Σ p (l̂+b) (R34), g_l = q − p → bf16 [N,E] and transposed [E,Np];
 // fidelity hit counts (R37).  stats (fp64): [0] Σ CE, [1] Σ|S∩P|, [2] Σ|S^{⌈k/2⌉}∩P|,
-// [3] Σ|S∩P^{2k}|.  Block = 8 warps × 4 rows = 32 tokens.
-__global__ void __launch_bounds__(256) k_distill_ce(const float* __restrict__ lhat, const float* __restrict__ tl,
-                                                    const float* __restrict__ bias, int N, int E, int k, int Np,
-                                                    __nv_bfloat16* __restrict__ gl, __nv_bfloat16* __restrict__ glT,
-                                                    double* __restrict__ stats) {
+// [3] Σ|S∩P^{2k}|.  Block = 32 warps = 32 tokens (one 64-byte segment per expert row of glT).
+__global__ void __launch_bounds__(1024) k_distill_ce(const float* __restrict__ lhat, const float* __restrict__ tl,
+                                                     const float* __restrict__ bias, int N, int E, int k, int Np,
+                                                     __nv_bfloat16* __restrict__ gl, __nv_bfloat16* __restrict__ glT,
+                                                     double* __restrict__ stats) {
   __shared__ __nv_bfloat16 sg[32][kMaxE + 8];
-  __shared__ float sred[8][4];
+  __shared__ float sred[32][4];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * 32;
+  const int n0 = blockIdx.x * 32, n = n0 + warp;
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int rr = 0; rr < 4; ++rr) {
-    const int rl = warp * 4 + rr, n = n0 + rl;
-    if (n >= N) {
-      for (int e = lane; e < E; e += 32) sg[rl][e] = __float2bfloat16(0.f);
-      continue;
-    }
+  if (n >= N) {
+    for (int e = lane; e < E; e += 32) sg[warp][e] = __float2bfloat16(0.f);
+  } else {
     float sv[8], tv[8];
     float sm = -INFINITY, tm = -INFINITY;
 #pragma unroll
@@ -150,15 +163,16 @@ __global__ void __launch_bounds__(256) k_distill_ce(const float* __restrict__ lh
       ts += __shfl_xor_sync(0xffffffffu, ts, o);
       tsl += __shfl_xor_sync(0xffffffffu, tsl, o);
     }
-    if (lane == 0) acc[0] += sm + __logf(ss) - tsl / ts;       // CE_t (R34; every lane holds it)
+    if (lane == 0) acc[0] = sm + __logf(ss) - tsl / ts;       // CE_t (R34; every lane holds it)
     const float is = 1.f / ss, it = 1.f / ts;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int e = lane + 32 * j;
       // g_l = q − p; explicit roundings (no FMA contraction) so q ≡ p gives exactly 0
-      if (e < E) sg[rl][e] = __float2bfloat16(__fsub_rn(__fmul_rn(se[j], is), __fmul_rn(te[j], it)));
+      if (e < E) sg[warp][e] = __float2bfloat16(__fsub_rn(__fmul_rn(se[j], is), __fmul_rn(te[j], it)));
     }
     // fidelity sets (R37): S = teacher top-k (first ⌈k/2⌉ = S^half), P2 = student top-2k
+    // (k == 0: metrics not requested — the serial warp argmaxes dominate this kernel)
     uint32_t mS = 0, mSh = 0, mP = 0, mP2 = 0;
     for (int i = 0; i < k; ++i) {
       const int w = warp_pick(tv, mS, E, lane);
@@ -169,23 +183,18 @@ __global__ void __launch_bounds__(256) k_distill_ce(const float* __restrict__ lh
       const int w = warp_pick(sv, mP2, E, lane);
       if ((w & 31) == lane) { mP2 |= 1u << (w >> 5); if (i < k) mP |= 1u << (w >> 5); }
     }
-    acc[1] += __popc(mS & mP);
-    acc[2] += __popc(mSh & mP);
-    acc[3] += __popc(mS & mP2);
+    acc[1] = __popc(mS & mP);
+    acc[2] = __popc(mSh & mP);
+    acc[3] = __popc(mS & mP2);
   }
-  __syncwarp();
   __syncthreads();
-  // g_l row-major and transposed (pads of the last block are zero rows in sg)
-  for (int i = warp; i < 32; i += 8) {
-    const int n = n0 + i;
-    if (n < N)
-      for (int e = lane; e < E; e += 32) gl[static_cast<size_t>(n) * E + e] = sg[i][e];
+  // g_l row-major (one row per warp) and transposed (32 tokens = 64 B per expert row)
+  if (n < N)
+    for (int e = lane; e < E; e += 32) gl[static_cast<size_t>(n) * E + e] = sg[warp][e];
+  for (int e = warp; e < E; e += 32) {
+    const int nn = n0 + lane;
+    if (nn < Np) glT[static_cast<size_t>(e) * Np + nn] = sg[lane][e];
   }
-  for (int e = warp; e < E; e += 8) {
-    const int n = n0 + lane;
-    if (n < Np) glT[static_cast<size_t>(e) * Np + n] = sg[lane][e];
-  }
-  // stats: CE partial sums in fp32 per warp, integer hit counts exact
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     float v = acc[q];
@@ -195,9 +204,38 @@ __global__ void __launch_bounds__(256) k_distill_ce(const float* __restrict__ lh
   }
   __syncthreads();
   if (threadIdx.x < 4) {
-    double s = 0.0;
-    for (int w = 0; w < 8; ++w) s += sred[w][threadIdx.x];
-    atomicAdd(stats + threadIdx.x, s);
+    double t = 0.0;
+    for (int w = 0; w < 32; ++w) t += sred[w][threadIdx.x];
+    atomicAdd(stats + threadIdx.x, t);
+  }
+}
+
+// out[i] = Σ_{s < S} part[s·n + i] in order s = 0, 1, … (deterministic split-K reduction).
+__global__ void k_sum_partials(const float* __restrict__ part, float* __restrict__ out, int64_t n, int S) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float a = part[i];
+    for (int s = 1; s < S; ++s) a += part[static_cast<size_t>(s) * n + i];
+    out[i] = a;
+  }
+}
+
+// All GEMM schedules of one distillation step written by one launch (thread i → schedule i).
+constexpr int kDistillScheds = 6, kSplitMax = 8;
+struct SchedSpec {
+  int n;
+  GemmGroup g[kSplitMax];
+};
+struct DistillSpecs {
+  SchedSpec s[kDistillScheds];
+};
+__global__ void k_write_scheds(GemmSched* base, DistillSpecs sp) {
+  const int i = threadIdx.x;
+  if (i < kDistillScheds) {
+    GemmSched* s = base + i;
+    s->num_groups = sp.s[i].n;
+    for (int j = 0; j < sp.s[i].n; ++j) s->g[j] = sp.s[i].g[j];
+    gemm_finalize_sched(s, 128);
   }
 }
 

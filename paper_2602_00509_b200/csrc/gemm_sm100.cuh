@@ -44,6 +44,7 @@ struct GemmGroup {
   int32_t tma_out;     // 1: fp32 output through the tmC tensor map (full 32-row slabs)
   int32_t topk;        // EPI_TOPK*: k
   int32_t rows_per_rank;  // EPI_TOPK_COUNT: tokens per rank (rank = (a_row + row) / rows_per_rank)
+  int32_t k_off;       // first K element of the (first) K segment: split-K partial products
   void* out;           // output of row 0 / col 0 of this group (EPI_TOPK: int32 ids [m, k])
   void* aux;           // EPI_TOPK: fp32 weights [m, k]; EPI_TOPK_COUNT: int32 counts [ranks, n]
   const float* bias;   // EPI_TOPK*: optional fp32 bias [n]
@@ -428,11 +429,13 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           brow0 = G.b_row + nb * BN;
           brow1 = brow0 + BN / 2;
         }
+        const int koff = G.k_off;
+        const bool bsel = G.b_sel != 0;
         for (int kb = 0; kb < num_kb; ++kb) {
           const bool second = kb >= kb1;
           const CUtensorMap* ta = second ? &tmA2 : &tmA;
-          const CUtensorMap* tb = (second || G.b_sel) ? &tmB1 : &tmB0;
-          const int kc = (second ? kb - kb1 : kb) * 64;
+          const CUtensorMap* tb = (second || bsel) ? &tmB1 : &tmB0;
+          const int kc = second ? (kb - kb1) * 64 : koff + kb * 64;
           GEMM_TIMED_WAIT(&empty[stage], phase ^ 1, 0);
           ptx::mbar_arrive_expect_tx(&full[stage], L::A_BYTES + L::B_BYTES);
           ptx::tma_load_2d(ta, &full[stage], sA + stage * L::A_BYTES, kc, arow);
@@ -644,11 +647,13 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
         int brow;
         if (G.mode == EPI_SWIGLU) brow = G.b_row + (rank ? G.n : 0) + nb * (BN / 2);
         else brow = G.b_row + nb * BN + static_cast<int>(rank) * (BN / 2);
+        const int koff = G.k_off;
+        const bool bsel = G.b_sel != 0;
         for (int kb = 0; kb < num_kb; ++kb) {
           const bool second = kb >= kb1;
           const CUtensorMap* ta = second ? &tmA2 : &tmA;
-          const CUtensorMap* tb = (second || G.b_sel) ? &tmB1 : &tmB0;
-          const int kc = (second ? kb - kb1 : kb) * 64;
+          const CUtensorMap* tb = (second || bsel) ? &tmB1 : &tmB0;
+          const int kc = second ? (kb - kb1) * 64 : koff + kb * 64;
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (L::A_BYTES + L::B_BYTES));
           ptx::tma_load_2d_cg2(ta, &full[stage], sA + stage * L::A_BYTES, kc, arow);

@@ -665,12 +665,12 @@ __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o
     GemmGroup g1;
     g1.a_row = arow; g1.m = m; g1.b_row = wslot * 2 * d.F; g1.b_sel = is_rep; g1.mode = EPI_SWIGLU;
     g1.n = d.F; g1.ldc = d.F; g1.tile_start = 0; g1.out_row = arow; g1.tma_out = 0;
-    g1.topk = 0; g1.rows_per_rank = 1; g1.aux = nullptr; g1.bias = nullptr;
+    g1.topk = 0; g1.rows_per_rank = 1; g1.k_off = 0; g1.aux = nullptr; g1.bias = nullptr;
     g1.out = reinterpret_cast<__nv_bfloat16*>(in.act) + static_cast<size_t>(arow) * d.F;
     GemmGroup g2;
     g2.a_row = arow; g2.m = m; g2.b_row = wslot * d.H; g2.b_sel = is_rep; g2.mode = EPI_F32;
     g2.n = d.H; g2.ldc = d.H; g2.tile_start = 0; g2.out_row = arow; g2.tma_out = (d.H % 32 == 0);
-    g2.topk = 0; g2.rows_per_rank = 1; g2.aux = nullptr; g2.bias = nullptr;
+    g2.topk = 0; g2.rows_per_rank = 1; g2.k_off = 0; g2.aux = nullptr; g2.bias = nullptr;
     g2.out = reinterpret_cast<float*>(in.y_local) + static_cast<size_t>(arow) * d.H;
     o.s1->g[i] = g1;
     o.s2->g[i] = g2;

@@ -315,7 +315,7 @@ void launch_topk(const Dims& d, int T, int nchunks, cudaStream_t st, const float
 GemmGroup mk_group(int a_row, int m, int b_row, int b_sel, int mode, int n, int ldc, void* out) {
   GemmGroup g;
   g.a_row = a_row; g.m = m; g.b_row = b_row; g.b_sel = b_sel; g.mode = mode; g.n = n; g.ldc = ldc;
-  g.tile_start = 0; g.out_row = 0; g.tma_out = 0; g.topk = 0; g.rows_per_rank = 1; g.out = out;
+  g.tile_start = 0; g.out_row = 0; g.tma_out = 0; g.topk = 0; g.rows_per_rank = 1; g.k_off = 0; g.out = out;
   g.aux = nullptr; g.bias = nullptr;
   return g;
 }
@@ -981,7 +981,7 @@ probe_status probe_history_update(probe_ctx ctx, int32_t layer, int32_t reset, i
 //   z fp32 [N,h] | a bf16 [N,h] | aT [h,Np] | lhat, t fp32 [N,E] | gl bf16 [N,E] | glT [E,Np]
 //   | ga fp32 [N,h] | gzT [h,Np] | xT [H,Np] | w2T [h,E] | 6 GEMM schedules
 struct DistillLayout {
-  size_t z, a, aT, lhat, t, gl, glT, ga, gzT, xT, w2T, sched, total;
+  size_t z, a, aT, lhat, t, gl, glT, ga, gzT, xT, w2T, part, sched, total;
   uint64_t Np;
 };
 
@@ -1003,21 +1003,22 @@ static DistillLayout distill_layout(const probe_config& c) {
   L.gzT = take(h * Np * 2);
   L.xT = take(H * Np * 2);
   L.w2T = take(h * E * 2);
-  L.sched = take(6 * sizeof(GemmSched));
+  L.part = take(static_cast<size_t>(kSplitMax) * std::max(E * h, h * H) * 4);
+  L.sched = take(kDistillScheds * sizeof(GemmSched));
   L.total = o;
   return L;
 }
 
 probe_status probe_distill_grad(probe_ctx ctx, const void* x, const void* x_next, int32_t T, const void* w_router,
                                 const float* b_router, const void* w_res1, const void* w_res2, float* grad_res1,
-                                float* grad_res2, double* stats, float* student_logits, float* teacher_logits,
-                                void* stream) {
+                                float* grad_res2, double* stats, int32_t fidelity, float* student_logits,
+                                float* teacher_logits, void* stream) {
   if (!ctx) return fail(nullptr, PROBE_EINVAL, "null ctx");
   if (!x || !x_next || !w_router || !w_res1 || !w_res2 || !grad_res1 || !grad_res2 || !stats)
     return fail(ctx, PROBE_EINVAL, "probe_distill_grad: null pointer");
   if (ctx->cfg.res_hidden <= 0) return fail(ctx, PROBE_ESHAPE, "probe_distill_grad: res_hidden == 0");
   if (T < 1 || T > ctx->cfg.max_tokens) return fail(ctx, PROBE_ECAPACITY, "T=%d outside [1, max_tokens]", T);
-  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->aux;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);   // NULL = the legacy default stream
   const DistillLayout DL = distill_layout(ctx->cfg);
   if (!ctx->dbuf) {
     if (capture_id(st) != 0)
@@ -1027,7 +1028,8 @@ probe_status probe_distill_grad(probe_ctx ctx, const void* x, const void* x_next
   }
   const Dims& d = ctx->d;
   const int N = d.GL * T, H = d.H, E = d.E, h = d.h;
-  const uint64_t Np = al(static_cast<uint64_t>(N), 64);
+  const int Np = static_cast<int>(al(static_cast<uint64_t>(N), 64));
+  const int grid = ctx->aux_sms;
   uint8_t* B = ctx->dbuf;
   float* z = reinterpret_cast<float*>(B + DL.z);
   auto* a = reinterpret_cast<__nv_bfloat16*>(B + DL.a);
@@ -1040,6 +1042,7 @@ probe_status probe_distill_grad(probe_ctx ctx, const void* x, const void* x_next
   auto* gzT = reinterpret_cast<__nv_bfloat16*>(B + DL.gzT);
   auto* xT = reinterpret_cast<__nv_bfloat16*>(B + DL.xT);
   auto* w2T = reinterpret_cast<__nv_bfloat16*>(B + DL.w2T);
+  float* part = reinterpret_cast<float*>(B + DL.part);
   GemmSched* sch = reinterpret_cast<GemmSched*>(B + DL.sched);
   const CUtensorMap* mx = ctx->maps.get(x, N, H, 128);
   const CUtensorMap* mxn = ctx->maps.get(x_next, N, H, 128);
@@ -1047,53 +1050,83 @@ probe_status probe_distill_grad(probe_ctx ctx, const void* x, const void* x_next
   const CUtensorMap* m1 = ctx->maps.get(w_res1, h, H, 64);
   const CUtensorMap* m2 = ctx->maps.get(w_res2, E, h, 64);
   const CUtensorMap* ma = ctx->maps.get(a, N, h, 128);
-  if (!mx || !mxn || !mw || !m1 || !m2 || !ma) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
-  auto gemm = [&](int si, const CUtensorMap& A, const CUtensorMap& B0, const CUtensorMap& B1, int m, int n, int K,
-                  float* out, const CUtensorMap* A2, int K2) -> probe_status {
-    SmallGroups sg{};
-    sg.BN = 128;
-    sg.n = 1;
-    sg.g[0] = mk_group(0, m, 0, 0, EPI_F32, n, n, out);
-    k_write_sched<<<1, 32, 0, st>>>(sch + si, sg);
-    CKL();
-    CK(launch_gemm_v(V_128_6_4, A, B0, B1, A, sch + si, K, ctx->aux_sms, st, A2, K2));
-    ++ctx->launches;
-    return PROBE_OK;
-  };
-  const dim3 tb(32, 8);
-  probe_status r;
-  CK(cudaMemsetAsync(stats, 0, 4 * sizeof(double), st));
-  // operands that the backward contracts over tokens: xᵀ, Ŵ²ᵀ
-  k_transpose_bf16<<<dim3((H + 31) / 32, static_cast<unsigned>((Np + 31) / 32)), tb, 0, st>>>(
-      static_cast<const __nv_bfloat16*>(x), xT, N, H, static_cast<int>(Np));
-  CKL();
-  k_transpose_bf16<<<dim3((h + 31) / 32, (E + 31) / 32), tb, 0, st>>>(static_cast<const __nv_bfloat16*>(w_res2), w2T,
-                                                                      E, h, E);
-  CKL();
-  // forward: z = x Ŵ¹ᵀ;  a = bf16(σ(z));  l̂ = [x | a]·[W | Ŵ²]ᵀ (Eq. (P));  t = x' Wᵀ (R33)
-  if ((r = gemm(0, *mx, *m1, *m1, N, h, H, z, nullptr, 0)) != PROBE_OK) return r;
-  k_act_fwd<<<dim3((h + 31) / 32, static_cast<unsigned>((Np + 31) / 32)), tb, 0, st>>>(z, a, aT, N, h,
-                                                                                      static_cast<int>(Np));
-  CKL();
-  if ((r = gemm(1, *mx, *mw, *m2, N, E, H, lhat, ma, h)) != PROBE_OK) return r;
-  if ((r = gemm(2, *mxn, *mw, *mw, N, E, H, tl, nullptr, 0)) != PROBE_OK) return r;
-  // softmax / CE / g_l = q − p / fidelity (R34, R37)
-  k_distill_ce<<<(N + 31) / 32, 256, 0, st>>>(lhat, tl, b_router, N, E, d.k, static_cast<int>(Np), gl, glT, stats);
-  CKL();
-  // backward (R34, R35): ∇Ŵ² = g_lᵀ a;  g_a = g_l Ŵ²;  g_z = g_a ⊙ σ'(z);  ∇Ŵ¹ = g_zᵀ x
   const CUtensorMap* mglT = ctx->maps.get(glT, E, Np, 128);
   const CUtensorMap* maT = ctx->maps.get(aT, h, Np, 64);
   const CUtensorMap* mgl = ctx->maps.get(gl, N, E, 128);
   const CUtensorMap* mw2T = ctx->maps.get(w2T, h, E, 64);
   const CUtensorMap* mgzT = ctx->maps.get(gzT, h, Np, 128);
   const CUtensorMap* mxT = ctx->maps.get(xT, H, Np, 64);
-  if (!mglT || !maT || !mgl || !mw2T || !mgzT || !mxT) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
-  if ((r = gemm(3, *mglT, *maT, *maT, E, h, static_cast<int>(Np), grad_res2, nullptr, 0)) != PROBE_OK) return r;
-  if ((r = gemm(4, *mgl, *mw2T, *mw2T, N, h, E, ga, nullptr, 0)) != PROBE_OK) return r;
-  k_silu_bwd<<<dim3((h + 31) / 32, static_cast<unsigned>((Np + 31) / 32)), tb, 0, st>>>(ga, z, gzT, N, h,
-                                                                                       static_cast<int>(Np));
+  if (!mx || !mxn || !mw || !m1 || !m2 || !ma || !mglT || !maT || !mgl || !mw2T || !mgzT || !mxT)
+    return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
+  // Schedules (one launch writes all six).  The two token contractions (K = Np) are split
+  // along K when their output has fewer tiles than the grid: split s covers K elements
+  // [s·Ks, (s+1)·Ks) into part[s], summed in order by k_sum_partials (deterministic).
+  DistillSpecs sp{};
+  int ksplit[kDistillScheds], nsplit[kDistillScheds];
+  auto spec = [&](int si, int m, int n, int K, float* out, bool allow_split) {
+    int S = 1;
+    if (allow_split) {
+      const int tiles = ((m + 127) / 128) * ((n + 127) / 128);
+      S = std::max(1, std::min({kSplitMax, grid / std::max(tiles, 1), K / 512}));
+    }
+    const int Ks = ((K + S - 1) / S + 63) / 64 * 64;
+    S = (K + Ks - 1) / Ks;
+    sp.s[si].n = S;
+    for (int j = 0; j < S; ++j) {
+      sp.s[si].g[j] = mk_group(0, m, 0, 0, EPI_F32, n, n, S > 1 ? part + static_cast<size_t>(j) * m * n : out);
+      sp.s[si].g[j].k_off = j * Ks;
+    }
+    ksplit[si] = S > 1 ? Ks : K;
+    nsplit[si] = S;
+  };
+  spec(0, N, h, H, z, false);            // z = x Ŵ¹ᵀ
+  spec(1, N, E, H, lhat, false);         // l̂ = [x | a]·[W | Ŵ²]ᵀ  (K2 = h)
+  spec(2, N, E, H, tl, false);           // t = x' Wᵀ
+  spec(3, E, h, Np, grad_res2, true);    // ∇Ŵ² = g_lᵀ a
+  spec(4, N, h, E, ga, false);           // g_a = g_l Ŵ²
+  spec(5, h, H, Np, grad_res1, true);    // ∇Ŵ¹ = g_zᵀ x
+  auto gemm = [&](int si, const CUtensorMap& A, const CUtensorMap& B0, const CUtensorMap& B1,
+                  const CUtensorMap* A2, int K2) -> probe_status {
+    CK(launch_gemm_v(V_128_6_4, A, B0, B1, A, sch + si, ksplit[si], grid, st, A2, K2));
+    ++ctx->launches;
+    return PROBE_OK;
+  };
+  auto reduce = [&](int si, float* out, int64_t n) -> probe_status {
+    if (nsplit[si] <= 1) return PROBE_OK;
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, static_cast<int64_t>(ctx->num_sms) * 8);
+    k_sum_partials<<<static_cast<unsigned>(blocks), 256, 0, st>>>(part, out, n, nsplit[si]);
+    CKL();
+    return PROBE_OK;
+  };
+  const dim3 tb(32, 8);
+  probe_status r;
+  CK(cudaMemsetAsync(stats, 0, 4 * sizeof(double), st));
+  k_write_scheds<<<1, 32, 0, st>>>(sch, sp);
   CKL();
-  if ((r = gemm(5, *mgzT, *mxT, *mxT, h, H, static_cast<int>(Np), grad_res1, nullptr, 0)) != PROBE_OK) return r;
+  // operands that the backward contracts over tokens: xᵀ [H, Np], Ŵ²ᵀ [h, E]
+  k_transpose_bf16<<<dim3((H + 63) / 64, (Np + 63) / 64), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), xT,
+                                                                         N, H, Np);
+  CKL();
+  k_transpose_bf16<<<dim3((h + 63) / 64, (E + 63) / 64), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(w_res2),
+                                                                        w2T, E, h, E);
+  CKL();
+  // forward: z = x Ŵ¹ᵀ;  a = bf16(σ(z));  l̂ = [x | a]·[W | Ŵ²]ᵀ (Eq. (P));  t = x' Wᵀ (R33)
+  if ((r = gemm(0, *mx, *m1, *m1, nullptr, 0)) != PROBE_OK) return r;
+  k_act_fwd<<<dim3((h + 31) / 32, (Np + 31) / 32), tb, 0, st>>>(z, a, aT, N, h, Np);
+  CKL();
+  if ((r = gemm(1, *mx, *mw, *m2, ma, h)) != PROBE_OK) return r;
+  if ((r = gemm(2, *mxn, *mw, *mw, nullptr, 0)) != PROBE_OK) return r;
+  // softmax / CE / g_l = q − p / fidelity (R34, R37)
+  k_distill_ce<<<(N + 31) / 32, 1024, 0, st>>>(lhat, tl, b_router, N, E, fidelity ? d.k : 0, Np, gl, glT, stats);
+  CKL();
+  // backward (R34, R35): ∇Ŵ² = g_lᵀ a;  g_a = g_l Ŵ²;  g_z = g_a ⊙ σ'(z);  ∇Ŵ¹ = g_zᵀ x
+  if ((r = gemm(3, *mglT, *maT, *maT, nullptr, 0)) != PROBE_OK) return r;
+  if ((r = reduce(3, grad_res2, static_cast<int64_t>(E) * h)) != PROBE_OK) return r;
+  if ((r = gemm(4, *mgl, *mw2T, *mw2T, nullptr, 0)) != PROBE_OK) return r;
+  k_silu_bwd<<<dim3((h + 31) / 32, (Np + 31) / 32), tb, 0, st>>>(ga, z, gzT, N, h, Np);
+  CKL();
+  if ((r = gemm(5, *mgzT, *mxT, *mxT, nullptr, 0)) != PROBE_OK) return r;
+  if ((r = reduce(5, grad_res1, static_cast<int64_t>(h) * H)) != PROBE_OK) return r;
   return PROBE_OK;
 }
 
@@ -1102,7 +1135,7 @@ probe_status probe_distill_apply(probe_ctx ctx, float* master, const float* grad
   if (!ctx) return fail(nullptr, PROBE_EINVAL, "null ctx");
   if (!master || !grad || !w || n < 0) return fail(ctx, PROBE_EINVAL, "probe_distill_apply: bad arguments");
   if (n == 0) return PROBE_OK;
-  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->aux;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t blocks = std::min<int64_t>((n + 255) / 256, static_cast<int64_t>(ctx->num_sms) * 8);
   k_sgd<<<static_cast<unsigned>(blocks), 256, 0, st>>>(master, grad, static_cast<__nv_bfloat16*>(w), n, scale);
   CKL();

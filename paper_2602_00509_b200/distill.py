@@ -34,24 +34,27 @@ class PredictorDistiller:
         self.g2 = torch.empty_like(self.m2)
         self.stats = torch.empty(4, dtype=torch.float64, device=w_res1.device)
 
-    def grad(self, x, x_next, w_router, b_router=None, student_logits=None, teacher_logits=None, stream=None):
+    def grad(self, x, x_next, w_router, b_router=None, student_logits=None, teacher_logits=None,
+             fidelity: bool = True, stream=None):
         self.rt.distill_grad(x, x_next, w_router, b_router, self.w1, self.w2, self.g1, self.g2, self.stats,
-                             student_logits, teacher_logits, stream)
+                             student_logits, teacher_logits, fidelity, stream)
 
-    def step(self, x, x_next, w_router, b_router=None, lr: float = 1e-2, group=None, stream=None) -> dict:
-        """One distillation step on this process's GL·T tokens; returns the batch metrics
-        (a device→host read of four numbers)."""
-        self.grad(x, x_next, w_router, b_router, stream=stream)
-        n = torch.tensor([float(x.numel() // x.shape[-1])], dtype=torch.float64, device=self.stats.device)
+    def step(self, x, x_next, w_router, b_router=None, lr: float = 1e-2, group=None, stream=None,
+             want_metrics: bool = True) -> Optional[dict]:
+        """One distillation step on this process's GL·T tokens.  Returns the batch metrics
+        (a device→host read of four numbers) unless want_metrics=False."""
+        self.grad(x, x_next, w_router, b_router, fidelity=want_metrics, stream=stream)
+        n_total = float(x.numel() // x.shape[-1])
         if group is not None:
             import torch.distributed as dist
+            n = torch.tensor([n_total], dtype=torch.float64, device=self.stats.device)
             for t in (self.g1, self.g2, self.stats, n):
                 dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-        n_total = float(n.item())
+            n_total = float(n.item())
         scale = -lr / n_total
         self.rt.distill_apply(self.m1, self.g1, self.w1, scale, stream)
         self.rt.distill_apply(self.m2, self.g2, self.w2, scale, stream)
-        return metrics(self.stats, n_total, self.rt.cfg.k)
+        return metrics(self.stats, n_total, self.rt.cfg.k) if want_metrics else None
 
 
 def metrics(stats: torch.Tensor, n_tokens: float, k: int) -> dict:

@@ -173,12 +173,13 @@ class ProbeRuntime:
         check("probe_history_update", st, self.ctx)
 
     def distill_grad(self, x, x_next, w_router, b_router, w_res1, w_res2, grad_res1, grad_res2, stats,
-                     student_logits=None, teacher_logits=None, stream=None):
+                     student_logits=None, teacher_logits=None, fidelity: bool = True, stream=None):
         """probe_distill_grad (NEXT-1): loss / fidelity sums → stats, ∂/∂Ŵ¹, ∂/∂Ŵ²."""
         T = x.shape[-2]
         st = self.lib.probe_distill_grad(self.ctx, _ptr(x), _ptr(x_next), T, _ptr(w_router), _ptr(b_router),
                                          _ptr(w_res1), _ptr(w_res2), _ptr(grad_res1), _ptr(grad_res2), _ptr(stats),
-                                         _ptr(student_logits), _ptr(teacher_logits), _stream(stream))
+                                         int(fidelity), _ptr(student_logits), _ptr(teacher_logits),
+                                         _stream(stream))
         check("probe_distill_grad", st, self.ctx)
 
     def distill_apply(self, master, grad, w, scale: float, stream=None):

@@ -322,7 +322,7 @@ class DistillTask:
     drifted: np.ndarray    # experts whose routing mass the drift relabels
 
 
-def distill_task(shape: MoEShape, step: int, zipf_s: float = 1.2, drift_frac: float = 0.25,
+def distill_task(shape: MoEShape, step: int, zipf_s: float = 1.2, drift_frac: float = 0.35,
                  router_scale: float = 4.0, device="cpu") -> DistillTask:
     """x = layer-0 inputs (whose parity-1 encoding is the prior's prediction P_t); x_next = x
     plus a fixed linear drift that moves the parity-1 coefficient of every expert e in a

@@ -23,6 +23,8 @@ CASES = {
     "mid-ragged": (pi.C0.with_(name="dmid", E=32, k=4, H=512, T=200, G=2, h=128), 200),
     "E256-k8": (pi.C0.with_(name="d256", E=256, k=8, H=1024, T=150, G=1, h=256), 150),
     "h-tail": (pi.C0.with_(name="dht", E=64, k=6, H=256, T=77, G=4, h=40), 77),
+    # N = 3000 tokens: both token contractions run split-K (5 K-splits + ordered reduction)
+    "split-k": (pi.C0.with_(name="dsk", E=32, k=4, H=512, T=1500, G=2, h=128), 1500),
 }
 
 
