@@ -293,7 +293,7 @@ def run_probe(args):
     fl2 = 2.0 * H * shape.F * pairs / world
     active = int((sp.sum(axis=0) > 0).sum())            # (expert, dest) slots with rows
     by1 = (active * 2 * shape.F * H * 2 + pairs * (H * 2 + shape.F * 2)) / world
-    by2 = (active * H * shape.F * 2 + pairs * (shape.F * 2 + H * 4)) / world
+    by2 = (active * H * shape.F * 2 + pairs * (shape.F * 2 + H * 2)) / world     # Y is fp16 (D2)
     t1 = phases["gemm1"] / 1e3
     t2 = phases["gemm2"] / 1e3
     peak_tf = pk["bf16_tflops_sustained"]
@@ -321,7 +321,7 @@ def run_probe(args):
                                "frac": (fl1 + fl2) / (t1 + t2) / 1e12 / peak_tf}}
     # ---- dispatch / combine against the HBM roofline (one GPU: every "peer" store is local HBM)
     byd = (G * T * H * 2 + pairs * H * 2) / world
-    byc = (pairs * H * 4 + G * T * H * 4) / world
+    byc = (pairs * H * 2 + G * T * H * 4) / world                                 # fp16 Y in, fp32 out
     bw_report = {"dispatch": {"algorithmic_bytes": byd, "GBps": byd / (phases["dispatch"] / 1e3) / 1e9,
                               "frac_hbm": byd / (phases["dispatch"] / 1e3) / 1e9 / peak_bw},
                  "combine": {"algorithmic_bytes": byc, "GBps": byc / (phases["combine"] / 1e3) / 1e9,

@@ -79,7 +79,7 @@ typedef struct {
 /* Buffer ids for probe_workspace / probe_init. */
 enum {
   PROBE_BUF_RECV = 0,    /* symmetric [recv_capacity, H] bf16: dispatched token rows (peers write) */
-  PROBE_BUF_Y = 1,       /* symmetric [recv_capacity, H] fp32: expert outputs (peers read in combine) */
+  PROBE_BUF_Y = 1,       /* symmetric [recv_capacity, H] fp16: expert outputs (peers read in combine; D2) */
   PROBE_BUF_REP_W13 = 2, /* symmetric [2*R_b, 2F, H] bf16: replica slots, 2 banks by layer parity */
   PROBE_BUF_REP_W2 = 3,  /* symmetric [2*R_b, H, F] bf16 */
   PROBE_BUF_BOARD = 4,   /* symmetric count boards [2 parity][2 kind][G][E] int32 + flags */
@@ -162,7 +162,9 @@ probe_status probe_debug_layout(probe_ctx ctx, int32_t* counts, int32_t* split, 
 /* Test hook: one grouped bf16 GEMM through the tcgen05 kernel,
  * C[g] (fp32, [m_g, N]) = A[a_row_g : a_row_g + m_g, :K] · B[b_row_g : b_row_g + N, :K]^T
  * (mode 0) or act = SiLU(gate)⊙up (bf16, [m_g, N/2]) with gate rows b_row_g.., up rows
- * b_row_g + N/2.. (mode 1).  groups: host array of num_groups × {a_row, m, b_row, c_row}. */
+ * b_row_g + N/2.. (mode 1); 3: SiLU → bf16, 4: no store, 5/6: fused top-k (k = 8),
+ * 7: fp16 C (the expert-output Y epilogue, TMA stores in SWIZZLE_64B).
+ * groups: host array of num_groups × {a_row, m, b_row, c_row}. */
 probe_status probe_test_gemm(const void* A, int64_t a_rows, const void* B, int64_t b_rows,
                              int32_t K, int32_t N, const int32_t* groups, int32_t num_groups,
                              int32_t mode, void* C, void* stream);
@@ -178,7 +180,8 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
                               void* stream);
 
 /* Synchronise this context's streams; return PROBE_ECAPACITY if the device
- * error word is set (receive overflow: the layer's output is invalid). */
+ * error word is set (receive overflow: the layer's output is invalid), PROBE_ESHAPE if an
+ * expert output exceeded the fp16 range of the Y buffer (|y| > 65504, D2). */
 probe_status probe_check(probe_ctx ctx);
 const char* probe_last_error(probe_ctx ctx);   /* ctx may be NULL (last global error) */
 probe_status probe_finalize(probe_ctx ctx);

@@ -5,18 +5,21 @@
 // the router / predictor GEMMs (a1, a2).
 //
 // Design (sm_100a):
-//  * one CTA per SM (grid = #SMs), static round-robin over output tiles of ALL
-//    groups; group table + tile prefix live in device memory (written by the
-//    layout kernel), so no host sync and CUDA-Graph safe;
+//  * one CTA (or CTA pair) per SM, tiles of ALL groups claimed dynamically from a global
+//    counter; group table + tile prefix live in device memory (written by the layout
+//    kernel), so no host sync and CUDA-Graph safe;
 //  * tile 128 × BN, K-step 64 (one 128-byte SWIZZLE_128B row per operand row);
 //  * warp 0: TMA producer (cp.async.bulk.tensor → STAGES-deep smem ring, mbarriers);
 //    warp 1: single-thread tcgen05.mma issuer (M=128, N=BN, K=16 per instruction,
 //            fp32 accumulator in TMEM, 2 accumulator buffers = 2·BN columns);
 //    warp 2: TMEM allocator;  warps 4-7: epilogue (tcgen05.ld → fused epilogue → st.global);
-//  * epilogues: fp32 store (logits, Y), SwiGLU → bf16 (gate cols | up cols in one
+//  * epilogues: fp32 store (logits), fp16 store (expert output Y), SwiGLU → bf16 (gate cols | up cols in one
 //    accumulator: the B tile is two TMA boxes, gate rows n0.. and up rows F+n0..),
 //    SiLU → bf16 (predictor residual activation, R8 rounding point).
 #pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
 #include "sm100_ptx.cuh"
 
 namespace probe {
@@ -27,8 +30,10 @@ enum : int {
   EPI_SILU_BF16 = 2,   // SiLU → bf16 (predictor residual activation, R8)
   EPI_NONE = 3,        // timing experiments: no stores
   EPI_TOPK = 4,        // router: per-row top-k (logit ↓, id ↑) + softmax over the k → ids, weights (a1)
-  EPI_TOPK_COUNT = 5   // predictor: per-row top-k → atomic per-(rank, expert) counts n̂ (a2, R9)
+  EPI_TOPK_COUNT = 5,  // predictor: per-row top-k → atomic per-(rank, expert) counts n̂ (a2, R9)
+  EPI_F16 = 6          // fp16 C (expert output Y, D2): |y| > 65504 raises kErrYRange in *aux
 };
+constexpr int kErrYRange = 8;   // device error bit (kernels.cuh ERR_Y_RANGE)
 constexpr int kTopkMax = 8;   // fused top-k supports k <= 8 (larger k uses the unfused kernel)
 
 struct GemmGroup {
@@ -151,6 +156,18 @@ __device__ __forceinline__ int swz(int r, int j) { return r * 32 + ((j ^ (r & 7)
 __device__ __forceinline__ void epi_store_manual(const float* tile, int lane, const GemmGroup& G, int row0,
                                                  int col0) {
   if (G.mode == EPI_NONE) return;
+  if (G.mode == EPI_F16) {   // half tile: 32 rows × 64 B, 16-byte chunk j at (j ^ ((r >> 1) & 3))
+    const char* tb = reinterpret_cast<const char*>(tile);
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int rl = it * 8 + (lane >> 2), j = lane & 3;
+      const int grow = row0 + rl;
+      if (grow < G.m && col0 + 8 * j < G.n)
+        *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(G.out) + static_cast<size_t>(grow) * G.ldc + col0 + 8 * j) =
+            *reinterpret_cast<const uint4*>(tb + rl * 64 + ((j ^ ((rl >> 1) & 3)) << 4));
+    }
+    return;
+  }
   if (G.mode == EPI_F32) {
 #pragma unroll
     for (int it = 0; it < 8; ++it) {
@@ -196,9 +213,31 @@ __device__ __forceinline__ void epi_chunk(float* tiles, int& tsel, int lane, con
   float* tile = tiles + tsel * 1024;
   if (lane == 0) ptx::bulk_wait_read<NB - 1>();   // the TMA store that last read this tile is done
   __syncwarp();
+  if (G.mode == EPI_F16) {
+    // row = lane: 32 halves = 64 B in the TMA SWIZZLE_64B layout (chunk j at j ^ ((row >> 1) & 3))
+    bool big = false;
 #pragma unroll
-  for (int j = 0; j < 8; ++j)
-    *reinterpret_cast<float4*>(tile + swz(lane, j)) = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    for (int j = 0; j < 4; ++j) {
+      uint4 p;
+      uint32_t* pw = reinterpret_cast<uint32_t*>(&p);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float a = v[8 * j + 2 * q], b = v[8 * j + 2 * q + 1];
+        big |= fabsf(a) > 65504.f || fabsf(b) > 65504.f;
+        __half2 hh = __floats2half2_rn(a, b);
+        pw[q] = *reinterpret_cast<uint32_t*>(&hh);
+      }
+      *reinterpret_cast<uint4*>(reinterpret_cast<char*>(tile) + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) = p;
+    }
+    // only rows / columns of this group count (tile rows past G.m hold other groups' or
+    // never-written receive rows)
+    big = big && row0 + lane < G.m && col0 < G.n;
+    if (__any_sync(0xffffffffu, big) && lane == 0 && G.aux) atomicOr(reinterpret_cast<int*>(G.aux), kErrYRange);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      *reinterpret_cast<float4*>(tile + swz(lane, j)) = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+  }
   const bool tma = G.tma_out && (row0 + 31 < G.m) && (col0 < G.n);
   if (tma) {
     ptx::fence_proxy_async_smem();

@@ -14,7 +14,7 @@ constexpr int kMaxE = 256;
 constexpr int kMaxK = 16;
 constexpr int kMaxG = 64;
 
-enum : int { ERR_RECV_OVERFLOW = 1, ERR_PLAN = 2, ERR_SHAPE = 4 };
+enum : int { ERR_RECV_OVERFLOW = 1, ERR_PLAN = 2, ERR_SHAPE = 4, ERR_Y_RANGE = kErrYRange };
 
 // Symmetric buffer table: sym[buf * G + r] = address of rank r's buffer `buf`.
 struct Sym {
@@ -546,7 +546,7 @@ struct LayoutOut {
   int32_t* group_rows;  // [G][S]
   int32_t* replicas_used;  // [G][3]
   GemmSched* s1;        // SwiGLU (expert GEMM 1)
-  GemmSched* s2;        // fp32 Y (expert GEMM 2)
+  GemmSched* s2;        // fp16 Y (expert GEMM 2)
   int32_t* err;
 };
 struct LayoutIn {
@@ -557,7 +557,7 @@ struct LayoutIn {
   const int32_t* replicas;      // [G][3] or null
   int bank;                     // replica slot bank = layer parity
   void* act;                    // [GL*cap, F] bf16
-  void* y_local;                // [GL*cap, H] fp32 (this process's Y region)
+  void* y_local;                // [GL*cap, H] fp16 (this process's Y region, D2)
 };
 
 __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o) {
@@ -668,10 +668,10 @@ __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o
     g1.topk = 0; g1.rows_per_rank = 1; g1.k_off = 0; g1.aux = nullptr; g1.bias = nullptr;
     g1.out = reinterpret_cast<__nv_bfloat16*>(in.act) + static_cast<size_t>(arow) * d.F;
     GemmGroup g2;
-    g2.a_row = arow; g2.m = m; g2.b_row = wslot * d.H; g2.b_sel = is_rep; g2.mode = EPI_F32;
+    g2.a_row = arow; g2.m = m; g2.b_row = wslot * d.H; g2.b_sel = is_rep; g2.mode = EPI_F16;
     g2.n = d.H; g2.ldc = d.H; g2.tile_start = 0; g2.out_row = arow; g2.tma_out = (d.H % 32 == 0);
-    g2.topk = 0; g2.rows_per_rank = 1; g2.k_off = 0; g2.aux = nullptr; g2.bias = nullptr;
-    g2.out = reinterpret_cast<float*>(in.y_local) + static_cast<size_t>(arow) * d.H;
+    g2.topk = 0; g2.rows_per_rank = 1; g2.k_off = 0; g2.aux = o.err; g2.bias = nullptr;
+    g2.out = reinterpret_cast<__half*>(in.y_local) + static_cast<size_t>(arow) * d.H;
     o.s1->g[i] = g1;
     o.s2->g[i] = g2;
     t1[i] = gemm_ntiles(g1, 256, in.tile_m);
@@ -785,7 +785,7 @@ __global__ void __launch_bounds__(128) k_combine(Dims d, int T, const float* __r
                                                  const int32_t* __restrict__ route, Sym sym, int buf_y, void* out,
                                                  volatile int32_t* suspend_flag, int layer) {
   if (blockIdx.x == 0 && threadIdx.x == 0 && suspend_flag) *suspend_flag = layer + 1;
-  __shared__ const float4* srcs[kMaxK];
+  __shared__ const uint4* srcs[kMaxK];
   __shared__ float gws[kMaxK];
   const int tok = blockIdx.x;           // gl * T + t
   const int k = d.k;
@@ -794,29 +794,40 @@ __global__ void __launch_bounds__(128) k_combine(Dims d, int T, const float* __r
     const int dd = route[(static_cast<size_t>(tok) * k + j) * 2];
     const int row = route[(static_cast<size_t>(tok) * k + j) * 2 + 1];
     srcs[j] = row < 0 ? nullptr
-                      : reinterpret_cast<const float4*>(sym.at(buf_y, d.G, dd) + static_cast<size_t>(row) * d.H * 4);
+                      : reinterpret_cast<const uint4*>(sym.at(buf_y, d.G, dd) + static_cast<size_t>(row) * d.H * 2);
     gws[j] = gw[static_cast<size_t>(tok) * k + j];
   }
   __syncthreads();
-  const int nv = d.H / 4;
+  // 8 outputs per thread-iteration: one 16-byte fp16 load per slot (Y rows are fp16, D2),
+  // accumulation in fp32 in slot order (R25)
+  const int nv = d.H / 8;
   for (int c = threadIdx.x; c < nv; c += blockDim.x) {
-    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    float a[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = 0.f;
     for (int j = 0; j < k; ++j) {
       if (!srcs[j]) continue;
-      const float4 y = srcs[j][c];
+      const uint4 y = srcs[j][c];
       const float g = gws[j];
-      a.x = fmaf(g, y.x, a.x);
-      a.y = fmaf(g, y.y, a.y);
-      a.z = fmaf(g, y.z, a.z);
-      a.w = fmaf(g, y.w, a.w);
+      const uint32_t yw[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&yw[q]));
+        a[2 * q] = fmaf(g, f.x, a[2 * q]);
+        a[2 * q + 1] = fmaf(g, f.y, a[2 * q + 1]);
+      }
     }
     if (OUT_F32) {
-      reinterpret_cast<float4*>(out)[static_cast<size_t>(tok) * nv + c] = a;
+      float4* o = reinterpret_cast<float4*>(out) + (static_cast<size_t>(tok) * nv + c) * 2;
+      o[0] = make_float4(a[0], a[1], a[2], a[3]);
+      o[1] = make_float4(a[4], a[5], a[6], a[7]);
     } else {
-      uint2 p;
-      p.x = pack_bf16(a.x, a.y);
-      p.y = pack_bf16(a.z, a.w);
-      reinterpret_cast<uint2*>(out)[static_cast<size_t>(tok) * nv + c] = p;
+      uint4 p;
+      p.x = pack_bf16(a[0], a[1]);
+      p.y = pack_bf16(a[2], a[3]);
+      p.z = pack_bf16(a[4], a[5]);
+      p.w = pack_bf16(a[6], a[7]);
+      reinterpret_cast<uint4*>(out)[static_cast<size_t>(tok) * nv + c] = p;
     }
   }
 }

@@ -69,6 +69,18 @@ bool make_map_f32_out(CUtensorMap* m, const void* base, uint64_t rows, uint64_t 
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// fp16 output map for TMA tensor stores: box {32 cols (64 B), 32 rows}, SWIZZLE_64B.
+bool make_map_f16_out(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols) {
+  if (!load_encode()) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t es[2] = {1, 1};
+  return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 struct MapCache {
   struct Ent {
     const void* p = nullptr;
@@ -144,7 +156,7 @@ Scratch scratch_layout(const probe_config& c) {
 void sym_sizes(const probe_config& c, uint64_t b[PROBE_NBUF]) {
   const uint64_t cap = c.recv_capacity, H = c.hidden, F = c.ffn, G = c.ep_size, E = c.num_experts;
   b[PROBE_BUF_RECV] = al(cap * H * 2, 1024);
-  b[PROBE_BUF_Y] = al(cap * H * 4, 1024);
+  b[PROBE_BUF_Y] = al(cap * H * 2, 1024);   // fp16 (D2)
   b[PROBE_BUF_REP_W13] = al(2 * kMaxRb * 2 * F * H * 2, 1024);
   b[PROBE_BUF_REP_W2] = al(2 * kMaxRb * H * F * 2, 1024);
   b[PROBE_BUF_BOARD] = al(4 * G * E * 4 + 1024, 1024);
@@ -473,7 +485,7 @@ probe_status probe_init(const probe_config* cfg, const uint64_t* peer_ptrs, void
             make_map(&ctx->map_act, ctx->scratch + ctx->sl.act, GL * cap, F, 128) &&
             make_map(&ctx->map_rw13, ctx->local_base[PROBE_BUF_REP_W13], GL * 2 * kMaxRb * 2 * F, H, 128) &&
             make_map(&ctx->map_rw2, ctx->local_base[PROBE_BUF_REP_W2], GL * 2 * kMaxRb * H, F, 128) &&
-            make_map_f32_out(&ctx->map_y, ctx->local_base[PROBE_BUF_Y], GL * cap, H);
+            make_map_f16_out(&ctx->map_y, ctx->local_base[PROBE_BUF_Y], GL * cap, H);
   if (!ok) {
     delete ctx;
     return fail(nullptr, PROBE_ECUDA, "probe_init: cuTensorMapEncodeTiled failed");
@@ -830,7 +842,7 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
                               float* ms_out, void* C, void* stream) {
   probe_ctx ctx = nullptr;
   if (!A || !B || !groups || !C || num_groups < 1 || num_groups > kMaxGroups || K < 1 || N < 8 || N % 8 ||
-      reps < 1 || mode < 0 || mode > 6)
+      reps < 1 || mode < 0 || mode > 7)
     return fail(nullptr, PROBE_EINVAL, "probe_test_gemm: bad arguments");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (variant < 0) variant = mode == 1 ? V_256_4_4 : (mode == 2 ? V_256_3_8 : V_128_6_4);
@@ -841,7 +853,8 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
                     : mode == 3 ? EPI_SILU_BF16
                     : mode == 4 ? EPI_NONE
                     : mode == 5 ? EPI_TOPK
-                    : mode == 6 ? EPI_TOPK_COUNT : EPI_F32;
+                    : mode == 6 ? EPI_TOPK_COUNT
+                    : mode == 7 ? EPI_F16 : EPI_F32;
   void* topk_aux = nullptr;
   if (emode == EPI_TOPK || emode == EPI_TOPK_COUNT) {
     if (N > 256) return fail(nullptr, PROBE_EINVAL, "top-k modes need N <= 256");
@@ -858,14 +871,14 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
     CK(cudaMemset(dstats, 0, 8 * sizeof(unsigned long long)));
     hs->stats = dstats;
   }
-  const size_t esz = emode == EPI_SWIGLU || emode == EPI_SILU_BF16 ? 2 : 4;
+  const size_t esz = emode == EPI_SWIGLU || emode == EPI_SILU_BF16 || emode == EPI_F16 ? 2 : 4;
   int acc = 0;
   int64_t c_rows = 1;
   for (int i = 0; i < num_groups; ++i) {
     const int* g = groups + 4 * i;
     hs->g[i] = mk_group(g[0], g[1], g[2], 0, emode, n_out, n_out, static_cast<uint8_t*>(C) + static_cast<size_t>(g[3]) * n_out * esz);
     hs->g[i].out_row = g[3];
-    hs->g[i].tma_out = emode == EPI_F32 && n_out % 32 == 0 ? 1 : 0;
+    hs->g[i].tma_out = (emode == EPI_F32 || emode == EPI_F16) && n_out % 32 == 0 ? 1 : 0;
     if (topk_aux) {   // test hook: k = 8; TOPK writes ids to C, weights to aux; COUNT: counts [64][N]
       hs->g[i].topk = 8;
       hs->g[i].rows_per_rank = static_cast<int>((a_rows + 63) / 64);
@@ -883,6 +896,8 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
     return fail(nullptr, PROBE_ECUDA, "tensor map encode failed");
   if (emode == EPI_F32 && n_out % 32 == 0) {
     if (!make_map_f32_out(&mc, C, c_rows, n_out)) return fail(nullptr, PROBE_ECUDA, "tensor map encode failed");
+  } else if (emode == EPI_F16 && n_out % 32 == 0) {
+    if (!make_map_f16_out(&mc, C, c_rows, n_out)) return fail(nullptr, PROBE_ECUDA, "tensor map encode failed");
   } else {
     mc = ma;
   }
@@ -939,6 +954,8 @@ probe_status probe_check(probe_ctx ctx) {
   if (flags[0] & ERR_RECV_OVERFLOW)
     return fail(ctx, PROBE_ECAPACITY, "receive capacity overflow (ranks [%d,%d), recv_capacity=%d)", ctx->cfg.rank_begin,
                 ctx->cfg.rank_begin + ctx->cfg.local_ranks, ctx->cfg.recv_capacity);
+  if (flags[0] & ERR_Y_RANGE)
+    return fail(ctx, PROBE_ESHAPE, "expert output |y| > 65504 does not fit the fp16 Y buffer (D2)");
   if (flags[0]) return fail(ctx, PROBE_ECUDA, "device error word 0x%x", flags[0]);
   return PROBE_OK;
 }

@@ -102,3 +102,26 @@ def test_gemm_multi_tile_swiglu(variant):
     ref = (torch.nn.functional.silu(g) * u)
     err = ((act.double() - ref).abs() / (ref.abs() + 1e-3)).max().item()
     assert err < 2 ** -7, err
+
+
+@pytest.mark.parametrize("N,K,rows,variant", [(256, 256, 3000, 0), (2048, 768, 9000, 2), (2048, 768, 9000, 6),
+                                              (512, 768, 30000, 6), (2880, 640, 1000, 6)])
+def test_gemm_f16_output_exact(N, K, rows, variant):
+    """The expert-output epilogue (fp16 Y, D2): TMA tensor stores in SWIZZLE_64B for full
+    32-row slabs, masked row stores for group tails.  Dyadic inputs make the fp32
+    accumulator exact, so the fp16 output must equal round-to-nearest-even of the exact
+    product (torch's fp64 → fp16 conversion) bit-for-bit."""
+    from paper_2602_00509_b200 import bench_gemm
+    A = _grid((rows, K), 31 + K)
+    B = _grid((2 * N, K), 32 + K)
+    half = rows // 2 + 77
+    groups = [[0, half, 0, 0], [half, rows - half, N, half]]
+    Cout = torch.full((rows, N), float("nan"), dtype=torch.float16, device="cuda")
+    bench_gemm(A, B, groups, N, 7, Cout, variant=variant, reps=1)
+    torch.cuda.synchronize()
+    ref = _ref(A, B, groups, N)
+    for (a_row, m, b_row, c_row) in groups:
+        exp = ref[c_row].to(torch.float16)
+        got = Cout[c_row:c_row + m]
+        bad = (got.view(torch.int16) != exp.view(torch.int16)).any(dim=1).nonzero()
+        assert bad.numel() == 0, (N, K, rows, variant, bad[:10].flatten().tolist())

@@ -59,3 +59,23 @@ def test_static_ep_identity_and_plan_independence():
     for r in range(sh.G):
         assert np.array_equal(lay0["route"][r, :, :, 0], gpu["ids"][0][r] // (sh.E // sh.G))
     assert gpu["replicas"].max() >= 0, "expected the planner to replicate under s=1.5"
+
+
+def test_fp16_y_range_is_checked():
+    """D2: Y is stored in fp16; an expert output beyond ±65504 must not pass silently —
+    probe_check reports PROBE_ESHAPE (device error bit set by the GEMM2 epilogue)."""
+    import torch
+    from paper_2602_00509_b200 import ProbeConfig, ProbeRuntime
+    from paper_2602_00509_b200._lib import ProbeError
+    sh = pi.C0
+    rt = ProbeRuntime(ProbeConfig(G=sh.G, E=sh.E, k=sh.k, H=sh.H, F=sh.F, T=sh.T, h=sh.h))
+    li = pi.layer_inputs(sh, 0, 0, 1.2, device="cuda")
+    W = pi.router_weight(sh, 0, device="cuda")
+    w13, w2 = pi.expert_weights(sh, 0, device="cuda")
+    out = torch.empty(sh.G, sh.T, sh.H, device="cuda")
+    rt.forward(0, li.x, W, None, w13, w2, out)
+    rt.check()                                        # in range: no error
+    rt.forward(0, li.x, W, None, w13, (w2.float() * 2.0 ** 20).to(torch.bfloat16), out)
+    with pytest.raises(ProbeError, match="65504"):
+        rt.check()
+    rt.close()

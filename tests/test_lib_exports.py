@@ -34,7 +34,7 @@ def test_workspace_and_validation(lib):
     cfg = ProbeConfig(G=8, E=128, k=8, H=2048, F=768, T=8192, h=512, capacity_factor=4.0)
     sz = workspace_sizes(cfg)
     assert sz[_lib.BUF_RECV] == cfg.recv_capacity * 2048 * 2
-    assert sz[_lib.BUF_Y] == cfg.recv_capacity * 2048 * 4
+    assert sz[_lib.BUF_Y] == cfg.recv_capacity * 2048 * 2          # fp16 Y (D2)
     assert sz[_lib.BUF_REP_W13] == 6 * 2 * 768 * 2048 * 2
     assert all(s % 1024 == 0 for s in sz)
     # invalid configs are rejected synchronously with a message (no GPU needed)
