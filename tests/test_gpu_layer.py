@@ -75,7 +75,7 @@ def test_fp16_y_range_is_checked():
     out = torch.empty(sh.G, sh.T, sh.H, device="cuda")
     rt.forward(0, li.x, W, None, w13, w2, out)
     rt.check()                                        # in range: no error
-    rt.forward(0, li.x, W, None, w13, (w2.float() * 2.0 ** 20).to(torch.bfloat16), out)
+    rt.forward(0, li.x, W, None, w13, (w2.float() * 2.0 ** 26).to(torch.bfloat16), out)   # |y| ≈ 1.7e6
     with pytest.raises(ProbeError, match="65504"):
         rt.check()
     rt.close()
