@@ -131,6 +131,9 @@ def run_probe(args):
         rt = make_runtime_distributed(cfg, dev, pg)
     else:
         rt = ProbeRuntime(cfg, dev)
+    if args.aux_sms:
+        from paper_2602_00509_b200._lib import OPT_AUX_SMS
+        rt.set_option(OPT_AUX_SMS, args.aux_sms)
     ranks = list(range(R0, R0 + GL))
     t0 = time.time()
     pool = [pi.layer_inputs(shape, 0, i, args.zipf, ranks=ranks, device=dev, wrap=POOL) for i in range(POOL)]
@@ -523,6 +526,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-emulation", action="store_true")
     ap.add_argument("--ep", type=int, default=0, help="EP size G (default: the config's, 8)")
+    ap.add_argument("--aux-sms", type=int, default=0, help="grid cap of the aux-stream predictor GEMMs (0: #SMs/2)")
     ap.add_argument("--cpu-tokens", type=int, default=256)
     ap.add_argument("--ref-tokens", type=int, default=16)
     args = ap.parse_args()

@@ -172,7 +172,7 @@ probe_status probe_test_gemm(const void* A, int64_t a_rows, const void* B, int64
 /* Timing hook: as probe_test_gemm with an explicit kernel variant (-1 = default for
  * `mode`; 0: BN=128/6 stages/4 epilogue warps, 1: 256/4/4, 2: 256/3/8, 3: 128/4/8,
  * 4: 256/3/4 with 2 staging tiles per epilogue warp, 5: 256/3/4 with 4,
- * 6: CTA pair (cta_group::2), 256-row tiles, 6 stages),
+ * 6: CTA pair (cta_group::2), 256-row tiles, 6 stages, 7: CTA pair with 5 stages and 8 epilogue warps),
  * run once, then `reps` times between CUDA events on `stream`; *ms_out = mean ms. */
 probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int64_t b_rows,
                               int32_t K, int32_t N, const int32_t* groups, int32_t num_groups,

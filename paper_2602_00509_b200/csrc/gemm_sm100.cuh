@@ -210,10 +210,17 @@ __device__ __forceinline__ void epi_chunk(float* tiles, int& tsel, int lane, con
     if (acc == 12345.678f) tiles[lane] = acc;   // keep the TMEM loads alive
     return;
   }
-  float* tile = tiles + tsel * 1024;
-  if (lane == 0) ptx::bulk_wait_read<NB - 1>();   // the TMA store that last read this tile is done
+  // fp16 tiles are 2 KB, so the 4 KB staging slot holds two and the warp can stage the next
+  // chunk while the TMA store of the previous one is still reading (launches never mix
+  // EPI_F16 with other storing modes, so the rotation counts only fp16 stores).
+  const bool f16 = G.mode == EPI_F16;
+  float* tile = f16 ? tiles + tsel * 512 : tiles + tsel * 1024;
+  if (lane == 0) {
+    if (f16) ptx::bulk_wait_read<2 * NB - 1>();
+    else ptx::bulk_wait_read<NB - 1>();          // the TMA store that last read this tile is done
+  }
   __syncwarp();
-  if (G.mode == EPI_F16) {
+  if (f16) {
     // row = lane: 32 halves = 64 B in the TMA SWIZZLE_64B layout (chunk j at j ^ ((row >> 1) & 3))
     bool big = false;
 #pragma unroll
@@ -251,7 +258,7 @@ __device__ __forceinline__ void epi_chunk(float* tiles, int& tsel, int lane, con
     epi_store_manual(tile, lane, G, row0, col0);
   }
   __syncwarp();
-  tsel = (tsel + 1) % NB;
+  tsel = (tsel + 1) % (f16 ? 2 * NB : NB);
 }
 
 // Fused router / predictor top-k (a1, a2): row = token (lane).  The k-element list is

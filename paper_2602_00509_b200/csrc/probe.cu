@@ -238,7 +238,8 @@ probe_status fail(probe_ctx ctx, probe_status st, const char* fmt, ...) {
 // GEMM variants: (BN, STAGES, epilogue warps).  V_GATE: logits/predictor (N ≤ 256),
 // V_SWIGLU: expert GEMM1 (bf16 act out), V_F32: expert GEMM2 (fp32 Y out, epilogue-heavy).
 enum GemmVariant { V_128_6_4 = 0, V_256_4_4 = 1, V_256_3_8 = 2, V_128_4_8 = 3, V_256_3_4_NB2 = 4, V_256_3_4_NB4 = 5,
-                   V_2CTA_256_6_4 = 6 /* CTA pair, cta_group::2, 256-row tiles */ };
+                   V_2CTA_256_6_4 = 6 /* CTA pair, cta_group::2, 256-row tiles */,
+                   V_2CTA_256_5_8 = 7 /* CTA pair with 8 epilogue warps */ };
 
 template <int BN, int ST, int EW>
 cudaError_t launch_gemm_2cta(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, const CUtensorMap& c,
@@ -284,11 +285,12 @@ cudaError_t launch_gemm_v(int v, const CUtensorMap& a, const CUtensorMap& b0, co
     case V_256_3_4_NB2: return launch_gemm_t<256, 3, 4, 2>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_256_3_4_NB4: return launch_gemm_t<256, 3, 4, 4>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_2CTA_256_6_4: return launch_gemm_2cta<256, 6, 4>(a, b0, b1, c, A2, s, K, K2, grid, st);
+    case V_2CTA_256_5_8: return launch_gemm_2cta<256, 5, 8>(a, b0, b1, c, A2, s, K, K2, grid, st);
   }
   return cudaErrorInvalidValue;
 }
 int variant_bn(int v) { return (v == V_128_6_4 || v == V_128_4_8) ? 128 : 256; }
-int variant_tm(int v) { return v == V_2CTA_256_6_4 ? 256 : 128; }
+int variant_tm(int v) { return (v == V_2CTA_256_6_4 || v == V_2CTA_256_5_8) ? 256 : 128; }
 
 template <int BN>
 cudaError_t launch_gemm(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, GemmSched* s, int K,
@@ -846,7 +848,7 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
     return fail(nullptr, PROBE_EINVAL, "probe_test_gemm: bad arguments");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (variant < 0) variant = mode == 1 ? V_256_4_4 : (mode == 2 ? V_256_3_8 : V_128_6_4);
-  if (variant > V_2CTA_256_6_4) return fail(nullptr, PROBE_EINVAL, "bad variant");
+  if (variant > V_2CTA_256_5_8) return fail(nullptr, PROBE_EINVAL, "bad variant");
   const int TM = variant_tm(variant);
   const int BN = variant_bn(variant);
   const int emode = mode == 1 ? EPI_SWIGLU
