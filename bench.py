@@ -48,49 +48,85 @@ def cost_model(shape, pk):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle sampling during the timed region (B200_PROFILING.md)."""
+    """SM clock / clock-event-reason sampling DURING the timed region (B200_PROFILING.md).
 
-    def __init__(self, gpu_index=0):
-        self.gpu = gpu_index
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-        self.p = None
+    NVML from a background thread every 2 ms (the timed region of a C1 run is ~0.1 s, too
+    short for `nvidia-smi -lms`, whose first sample arrives after process start-up); falls
+    back to nvidia-smi when NVML is unavailable."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, gpu_index=0, period_s=0.002):
+        self.gpu, self.period = gpu_index, period_s
+        self.sm, self.mask, self.max_sm = [], 0, None
+        self.h = None
+        self.smi = None
+
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            idx = torch.cuda._get_nvml_device_index(self.gpu)
+        except Exception:
+            idx = self.gpu
+        return pynvml, pynvml.nvmlDeviceGetHandleByIndex(idx)
 
     def __enter__(self):
+        import threading
         try:
-            self.p = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu),
-                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=self.f, stderr=subprocess.DEVNULL)
+            nv, h = self._nvml_handle()
+            self.max_sm = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                nv.nvmlDeviceGetCurrentClocksThrottleReasons
+            self.stop = threading.Event()
+
+            def loop():
+                while not self.stop.is_set():
+                    try:
+                        self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                        self.mask |= int(reasons(h))
+                    except Exception:
+                        pass
+                    time.sleep(self.period)
+
+            self.th = threading.Thread(target=loop, daemon=True)
+            self.th.start()
+            self.h = h
         except Exception:
-            self.p = None
+            self.h = None
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            try:
+                self.smi = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm",
+                     "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+            except Exception:
+                self.smi = None
         return self
 
     def __exit__(self, *a):
-        if self.p is not None:
-            self.p.terminate()
+        if self.h is not None:
+            self.stop.set()
+            self.th.join(timeout=2)
+        if self.smi is not None:
+            self.smi.terminate()
             try:
-                self.p.wait(timeout=5)
+                self.smi.wait(timeout=5)
             except Exception:
-                self.p.kill()
+                self.smi.kill()
+            try:
+                for r in open(self.f.name).read().split("\n"):
+                    c = r.split(",")
+                    if len(c) >= 2 and c[0].strip().replace(".", "").isdigit():
+                        self.sm.append(float(c[0]))
+                        self.max_sm = float(c[1])
+            except Exception:
+                pass
 
     def summary(self):
-        try:
-            rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
-        except Exception:
-            rows = []
-        sm = [float(r[0]) for r in rows if len(r) >= 7 and r[0].strip().replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in rows if len(r) >= 7 and r[1].strip().replace(".", "").isdigit()]
-        reasons = set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in rows:
-            if len(r) >= 7:
-                for i, n in enumerate(names):
-                    if r[3 + i].strip() == "Active":
-                        reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        reasons = sorted(n for bit, n in self.REASONS.items() if self.mask & bit)
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": self.max_sm,
+                "reasons": reasons, "samples": len(self.sm), "source": "nvml" if self.h is not None else "nvidia-smi"}
 
 
 # =============================================================================

@@ -69,7 +69,7 @@ def test_gemm_swiglu_and_silu():
                                                    (2, 512, 768, 30000, 2), (0, 128, 2048, 65536, 0),
                                                    (0, 384, 512, 20000, 3), (2, 2048, 768, 9000, 2),
                                                    (2, 512, 768, 30000, 6), (2, 2048, 768, 9000, 6),
-                                                   (2, 256, 2048, 700, 6)])
+                                                   (2, 256, 2048, 700, 6), (2, 512, 768, 30000, 7)])
 def test_gemm_multi_tile_per_cta_exact(mode, N, K, rows, variant):
     """Several tiles per persistent CTA (TMEM accumulator double buffer, phase wrap-around),
     every kernel variant (BN, stages, epilogue warps)."""
@@ -105,7 +105,7 @@ def test_gemm_multi_tile_swiglu(variant):
 
 
 @pytest.mark.parametrize("N,K,rows,variant", [(256, 256, 3000, 0), (2048, 768, 9000, 2), (2048, 768, 9000, 6),
-                                              (512, 768, 30000, 6), (2880, 640, 1000, 6)])
+                                              (512, 768, 30000, 6), (2880, 640, 1000, 6), (2048, 768, 9000, 7)])
 def test_gemm_f16_output_exact(N, K, rows, variant):
     """The expert-output epilogue (fp16 Y, D2): TMA tensor stores in SWIZZLE_64B for full
     32-row slabs, masked row stores for group tails.  Dyadic inputs make the fp32
