@@ -268,7 +268,13 @@ probe_status probe_distill_apply(probe_ctx ctx, float* master, const float* grad
 enum { PROBE_OPT_EP_EMULATION = 1, PROBE_OPT_UNFUSED_TOPK = 2, PROBE_OPT_FUSED_EPILOGUE_TOPK = 3,
        PROBE_OPT_AUX_SMS = 4 /* grid cap (CTAs) of the predictor GEMMs on the aux stream; default #SMs/2 */,
        PROBE_OPT_PAIR_GEMM = 5 /* expert GEMMs on CTA pairs (tcgen05 cta_group::2, 256-row tiles);
-                                  default ON, 0 selects the 1-CTA kernel */ };
+                                  default ON, 0 selects the 1-CTA kernel */,
+       PROBE_OPT_FUSED_DISPATCH = 6 /* when this process hosts every rank: dispatch writes only the
+                                       receive-row → x-row index and the expert GEMM1 producer gathers
+                                       its A rows from x with TMA gather4 (no receive-buffer copy);
+                                       ignored with local_ranks < ep_size.  Default OFF: measured
+                                       GEMM1 7.5 ms vs 2.5 ms — gather4 delivers ~1 row per ~20
+                                       cycles per SM, 3x below the MMA's A consumption */ };
 probe_status probe_set_option(probe_ctx ctx, int32_t option, int64_t value);
 
 /* Number of library kernel launches enqueued so far by this context (bench accounting). */

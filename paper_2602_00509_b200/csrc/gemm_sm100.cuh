@@ -68,6 +68,9 @@ struct GemmSched {
   int32_t part_tile[kMaxParts + 1];  // tile range [part_tile[p], part_tile[p+1]) of partition p
   int32_t part_counter[kMaxParts];   // per-partition tile counters
   unsigned long long* stats;         // optional per-role wait-cycle counters (timing hook only)
+  // Fused dispatch (a6 → a7): when non-null, A row r of the first K segment is row
+  // gather_idx[r] of the A map (TMA gather4, map box {64, 1}) instead of row r.
+  const int32_t* gather_idx;
   GemmGroup g[kMaxGroups];
 };
 // stats[0] producer waits on `empty`   stats[1] MMA waits on `full`   stats[2] MMA waits on `tempty`
@@ -109,6 +112,7 @@ __device__ inline void gemm_finalize_sched(GemmSched* s, int BN) {
   s->nparts = 0;
   s->tile_m = 128;
   s->stats = nullptr;
+  s->gather_idx = nullptr;
   sched_reset_counters(s);
   int acc = 0;
   for (int i = 0; i < s->num_groups; ++i) {
@@ -448,47 +452,61 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   const int num_kb = kb1 + (K2 > 0 ? (K2 + 63) / 64 : 0);
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      int qs = 0;
-      uint32_t qph = 0;
-      while (true) {
-        const int tile = claim_tile(sched);
+    // ------------------------------------------------------------ TMA producer (warp 0:
+    // lane 0 claims tiles and loads B / A tiles; with a gather index every lane gathers 4 A rows)
+    const int32_t* gidx = sched->gather_idx;
+    int stage = 0;
+    uint32_t phase = 0;
+    int qs = 0;
+    uint32_t qph = 0;
+    while (true) {
+      int tile = 0;
+      if (lane == 0) {
+        tile = claim_tile(sched);
         ptx::mbar_wait(&qempty[qs], qph ^ 1);
         tq[qs] = tile;
         ptx::mbar_arrive(&qfull[qs]);
-        if (++qs == kTileQ) { qs = 0; qph ^= 1; }
-        if (tile < 0) break;
-        const int gi = gemm_find_group(ts, ng, tile);
-        const GemmGroup& G = sched->g[gi];
-        const int nt = gemm_ntiles_n(G, BN);
-        const int tin = tile - ts[gi];
-        const int mb = tin / nt, nb = tin % nt;
-        const int arow = G.a_row + mb * 128;
-        int brow0, brow1;
-        if (G.mode == EPI_SWIGLU) {
-          brow0 = G.b_row + nb * (BN / 2);
-          brow1 = brow0 + G.n;
-        } else {
-          brow0 = G.b_row + nb * BN;
-          brow1 = brow0 + BN / 2;
-        }
-        const int koff = G.k_off;
-        const bool bsel = G.b_sel != 0;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          const bool second = kb >= kb1;
-          const CUtensorMap* ta = second ? &tmA2 : &tmA;
-          const CUtensorMap* tb = (second || bsel) ? &tmB1 : &tmB0;
-          const int kc = second ? (kb - kb1) * 64 : koff + kb * 64;
+      }
+      tile = __shfl_sync(0xffffffffu, tile, 0);
+      if (++qs == kTileQ) { qs = 0; qph ^= 1; }
+      if (tile < 0) break;
+      const int gi = gemm_find_group(ts, ng, tile);
+      const GemmGroup& G = sched->g[gi];
+      const int nt = gemm_ntiles_n(G, BN);
+      const int tin = tile - ts[gi];
+      const int mb = tin / nt, nb = tin % nt;
+      const int arow = G.a_row + mb * 128;
+      int brow0, brow1;
+      if (G.mode == EPI_SWIGLU) {
+        brow0 = G.b_row + nb * (BN / 2);
+        brow1 = brow0 + G.n;
+      } else {
+        brow0 = G.b_row + nb * BN;
+        brow1 = brow0 + BN / 2;
+      }
+      const int koff = G.k_off;
+      const bool bsel = G.b_sel != 0;
+      int g0 = 0, g1 = 0, g2 = 0, g3 = 0;
+      if (gidx) {
+        const int32_t* p = gidx + arow + 4 * lane;
+        g0 = p[0]; g1 = p[1]; g2 = p[2]; g3 = p[3];
+      }
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const bool second = kb >= kb1;
+        const CUtensorMap* ta = second ? &tmA2 : &tmA;
+        const CUtensorMap* tb = (second || bsel) ? &tmB1 : &tmB0;
+        const int kc = second ? (kb - kb1) * 64 : koff + kb * 64;
+        const bool gat = gidx && !second;
+        if (lane == 0) {
           GEMM_TIMED_WAIT(&empty[stage], phase ^ 1, 0);
           ptx::mbar_arrive_expect_tx(&full[stage], L::A_BYTES + L::B_BYTES);
-          ptx::tma_load_2d(ta, &full[stage], sA + stage * L::A_BYTES, kc, arow);
+          if (!gat) ptx::tma_load_2d(ta, &full[stage], sA + stage * L::A_BYTES, kc, arow);
           ptx::tma_load_2d(tb, &full[stage], sB + stage * L::B_BYTES, kc, brow0);
           ptx::tma_load_2d(tb, &full[stage], sB + stage * L::B_BYTES + (BN / 2) * 128, kc, brow1);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
+        __syncwarp();
+        if (gat) ptx::tma_gather4(ta, &full[stage], sA + stage * L::A_BYTES + lane * 512, kc, g0, g1, g2, g3);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
@@ -661,14 +679,17 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
   const int unit = static_cast<int>(blockIdx.x >> 1);     // cluster index (EP-emulation partition)
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer (both CTAs)
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      int qs = 0;
-      uint32_t qph = 0;
-      while (true) {
-        int tile;
+    // ------------------------------------------------------------ TMA producer (both CTAs;
+    // lane 0 handles the tile queue and the TMA tile loads, with a gather index every lane
+    // gathers 4 of this CTA's 128 A rows)
+    const int32_t* gidx = sched->gather_idx;
+    int stage = 0;
+    uint32_t phase = 0;
+    int qs = 0;
+    uint32_t qph = 0;
+    while (true) {
+      int tile = 0;
+      if (lane == 0) {
         if (leader) {
           tile = claim_tile(sched, unit);
           ptx::mbar_wait(&qempty[qs], qph ^ 1);
@@ -682,30 +703,41 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
           tile = tq[qs];
           ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&qempty[qs]), 0));
         }
-        if (++qs == kTileQ) { qs = 0; qph ^= 1; }
-        if (tile < 0) break;
-        const int gi = gemm_find_group(ts, ng, tile);
-        const GemmGroup& G = sched->g[gi];
-        const int nt = gemm_ntiles_n(G, BN);
-        const int tin = tile - ts[gi];
-        const int mb = tin / nt, nb = tin % nt;
-        const int arow = G.a_row + mb * 256 + static_cast<int>(rank) * 128;
-        int brow;
-        if (G.mode == EPI_SWIGLU) brow = G.b_row + (rank ? G.n : 0) + nb * (BN / 2);
-        else brow = G.b_row + nb * BN + static_cast<int>(rank) * (BN / 2);
-        const int koff = G.k_off;
-        const bool bsel = G.b_sel != 0;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          const bool second = kb >= kb1;
-          const CUtensorMap* ta = second ? &tmA2 : &tmA;
-          const CUtensorMap* tb = (second || bsel) ? &tmB1 : &tmB0;
-          const int kc = second ? (kb - kb1) * 64 : koff + kb * 64;
+      }
+      tile = __shfl_sync(0xffffffffu, tile, 0);
+      if (++qs == kTileQ) { qs = 0; qph ^= 1; }
+      if (tile < 0) break;
+      const int gi = gemm_find_group(ts, ng, tile);
+      const GemmGroup& G = sched->g[gi];
+      const int nt = gemm_ntiles_n(G, BN);
+      const int tin = tile - ts[gi];
+      const int mb = tin / nt, nb = tin % nt;
+      const int arow = G.a_row + mb * 256 + static_cast<int>(rank) * 128;
+      int brow;
+      if (G.mode == EPI_SWIGLU) brow = G.b_row + (rank ? G.n : 0) + nb * (BN / 2);
+      else brow = G.b_row + nb * BN + static_cast<int>(rank) * (BN / 2);
+      const int koff = G.k_off;
+      const bool bsel = G.b_sel != 0;
+      int g0 = 0, g1 = 0, g2 = 0, g3 = 0;
+      if (gidx) {
+        const int32_t* p = gidx + arow + 4 * lane;
+        g0 = p[0]; g1 = p[1]; g2 = p[2]; g3 = p[3];
+      }
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const bool second = kb >= kb1;
+        const CUtensorMap* ta = second ? &tmA2 : &tmA;
+        const CUtensorMap* tb = (second || bsel) ? &tmB1 : &tmB0;
+        const int kc = second ? (kb - kb1) * 64 : koff + kb * 64;
+        const bool gat = gidx && !second;
+        if (lane == 0) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (L::A_BYTES + L::B_BYTES));
-          ptx::tma_load_2d_cg2(ta, &full[stage], sA + stage * L::A_BYTES, kc, arow);
+          if (!gat) ptx::tma_load_2d_cg2(ta, &full[stage], sA + stage * L::A_BYTES, kc, arow);
           ptx::tma_load_2d_cg2(tb, &full[stage], sB + stage * L::B_BYTES, kc, brow);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
+        __syncwarp();
+        if (gat) ptx::tma_gather4_cg2(ta, &full[stage], sA + stage * L::A_BYTES + lane * 512, kc, g0, g1, g2, g3);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {

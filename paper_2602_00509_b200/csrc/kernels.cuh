@@ -558,6 +558,7 @@ struct LayoutIn {
   int bank;                     // replica slot bank = layer parity
   void* act;                    // [GL*cap, F] bf16
   void* y_local;                // [GL*cap, H] fp16 (this process's Y region, D2)
+  const int32_t* gather_idx;    // fused dispatch: GEMM1 gathers its A rows through this index (else null)
 };
 
 __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o) {
@@ -701,6 +702,7 @@ __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o
       sc->total_tiles = base;
       sc->tile_m = in.tile_m;
       sc->stats = nullptr;
+      sc->gather_idx = w == 0 ? in.gather_idx : nullptr;
       sched_reset_counters(sc);
       sc->nparts = in.nparts > 1 ? in.nparts : 0;
       if (in.nparts > 1) {
@@ -715,6 +717,8 @@ __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o
 // a6 dispatch: every (token, slot) row of x to its destination's receive buffer
 // (peer store over NVLink for remote ranks).  Warp per token; the x row is read
 // once and written to its k destinations with 16-byte vector stores.
+// Fused mode (gidx != null, every rank in this process): only the route and the
+// receive-row → x-row index are written; the expert GEMM1 producer gathers the rows.
 // =============================================================================
 __global__ void __launch_bounds__(256) k_dispatch(Dims d, int T, const __nv_bfloat16* __restrict__ x,
                                                   const int32_t* __restrict__ ids,
@@ -723,7 +727,7 @@ __global__ void __launch_bounds__(256) k_dispatch(Dims d, int T, const __nv_bflo
                                                   const int32_t* __restrict__ split_cum,
                                                   const int32_t* __restrict__ slot_of,
                                                   const int32_t* __restrict__ src_off, int32_t* __restrict__ route,
-                                                  Sym sym, int buf_recv, int32_t* err) {
+                                                  Sym sym, int buf_recv, int32_t* err, int32_t* __restrict__ gidx) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= d.GL * T) return;
@@ -750,8 +754,15 @@ __global__ void __launch_bounds__(256) k_dispatch(Dims d, int T, const __nv_bflo
     }
     route[(pr * k + lane) * 2] = dd;
     route[(pr * k + lane) * 2 + 1] = row;
-    if (row >= 0) dst_row = sym.at(buf_recv, d.G, dd) + static_cast<size_t>(row) * d.H * 2;
+    if (gidx) {
+      // fused dispatch (all ranks in this process): receive row `row` of dd is x row pr —
+      // GEMM1 gathers it with TMA gather4; nothing is copied
+      if (row >= 0) gidx[static_cast<size_t>(dd - d.R0) * d.cap + row] = static_cast<int32_t>(pr);
+    } else if (row >= 0) {
+      dst_row = sym.at(buf_recv, d.G, dd) + static_cast<size_t>(row) * d.H * 2;
+    }
   }
+  if (gidx) return;
   // copy: the x row is read once (batches of 8 × 16 B per lane in flight) and stored k times
   const uint4* src = reinterpret_cast<const uint4*>(x + pr * d.H);
   const int nv = d.H / 8;

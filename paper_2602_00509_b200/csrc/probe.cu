@@ -109,7 +109,7 @@ struct Scratch {
   size_t sym, logits, pprior, pres, pact, ids, gw, pos, hist, cbase, route, pred_local;
   size_t quota[2], reps[2], stats[2], pfctr[2];
   size_t split_cum, slot_of, src_off, group_rows, reps_used;
-  size_t s_g1, s_g2, s_gate, s_p1, s_p2, flags, act, total;
+  size_t s_g1, s_g2, s_gate, s_p1, s_p2, flags, gidx, act, total;
 };
 
 Scratch scratch_layout(const probe_config& c) {
@@ -148,6 +148,7 @@ Scratch scratch_layout(const probe_config& c) {
   s.s_p1 = take(sizeof(GemmSched));
   s.s_p2 = take(sizeof(GemmSched));
   s.flags = take(256);
+  s.gidx = take((GL * cap + 512) * 4);     // fused dispatch: receive row → x row (+ tile overhang)
   s.act = take(GL * cap * F * 2);
   s.total = al(o, 1024);
   return s;
@@ -194,6 +195,7 @@ struct probe_ctx_s {
   bool ep_emulation = false;  // partition expert GEMMs by local rank (probe_set_option)
   bool fused_epi_topk = false;  // top-k in the GEMM epilogue instead of k_select (probe_set_option)
   bool pair_gemm = true;        // expert GEMMs on CTA pairs (cta_group::2); option turns it off
+  bool fused_dispatch = false;  // single process: GEMM1 gathers x rows (TMA gather4), no receive copy (opt-in: slower)
   // distillation workspace (NEXT-1), allocated on the first probe_distill_grad
   uint8_t* dbuf = nullptr;
   size_t dbytes = 0;
@@ -460,6 +462,8 @@ probe_status probe_init(const probe_config* cfg, const uint64_t* peer_ptrs, void
   }
   cudaError_t e = cudaMemcpy(ctx->scratch + ctx->sl.sym, ctx->peer.data(), PROBE_NSYM * G * 8, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemset(ctx->scratch + ctx->sl.flags, 0, 256);
+  if (e == cudaSuccess)   // gather indices of never-written receive rows stay valid (row 0)
+    e = cudaMemset(ctx->scratch + ctx->sl.gidx, 0, (static_cast<size_t>(cfg->local_ranks) * cfg->recv_capacity + 512) * 4);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->pf, cudaStreamNonBlocking);
   for (int p = 0; p < 2 && e == cudaSuccess; ++p) {
@@ -583,6 +587,11 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   li.tile_m = ctx->pair_gemm ? 256 : 128;
   li.act = ctx->scratch + s.act;
   li.y_local = ctx->local_base[PROBE_BUF_Y];
+  // fused dispatch (a6 → a7): every rank in this process, so GEMM1 can gather the x rows itself
+  const bool fused = ctx->fused_dispatch && !ctx->multi_process();
+  const CUtensorMap* mxg = fused ? ctx->maps.get(x, GL * T, d.H, 1) : nullptr;
+  if (fused && !mxg) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
+  li.gather_idx = fused ? ctx->at<int32_t>(s.gidx) : nullptr;
   LayoutOut lo;
   lo.split_cum = ctx->at<int32_t>(s.split_cum);
   lo.slot_of = ctx->at<int32_t>(s.slot_of);
@@ -601,7 +610,8 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
     k_dispatch<<<(warps + 7) / 8, 256, 0, st>>>(d, T, static_cast<const __nv_bfloat16*>(x), ctx->at<int32_t>(s.ids),
                                                 ctx->at<int32_t>(s.pos), ctx->at<int32_t>(s.cbase),
                                                 lo.split_cum, lo.slot_of, lo.src_off, ctx->at<int32_t>(s.route),
-                                                sym_of(ctx), PROBE_BUF_RECV, err);
+                                                sym_of(ctx), PROBE_BUF_RECV, err,
+                                                fused ? ctx->at<int32_t>(s.gidx) : nullptr);
     CKL();
   }
   MARK(5);
@@ -612,7 +622,8 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   CK(ev_record(ctx, ctx->ev_gemm[p], st));
   // a7 grouped SwiGLU expert FFN (tcgen05): act = SiLU(X W_gᵀ) ⊙ X W_uᵀ ; Y = act W_dᵀ
   const int vexp = ctx->pair_gemm ? V_2CTA_256_6_4 : V_256_4_4;
-  CK(launch_gemm_v(vexp, ctx->map_recv, *m13, ctx->map_rw13, ctx->map_recv, lo.s1, d.H, ctx->num_sms, st));
+  CK(launch_gemm_v(vexp, fused ? *mxg : ctx->map_recv, *m13, ctx->map_rw13, ctx->map_recv, lo.s1, d.H, ctx->num_sms,
+                   st));
   ++ctx->launches;
   MARK(7);
   CK(launch_gemm_v(vexp, ctx->map_act, *m2, ctx->map_rw2, ctx->map_y, lo.s2, d.F, ctx->num_sms, st));
@@ -1168,6 +1179,7 @@ probe_status probe_set_option(probe_ctx ctx, int32_t option, int64_t value) {
     case PROBE_OPT_UNFUSED_TOPK: ctx->unfused = value != 0; return PROBE_OK;
     case PROBE_OPT_FUSED_EPILOGUE_TOPK: ctx->fused_epi_topk = value != 0; return PROBE_OK;
     case PROBE_OPT_PAIR_GEMM: ctx->pair_gemm = value != 0; return PROBE_OK;
+    case PROBE_OPT_FUSED_DISPATCH: ctx->fused_dispatch = value != 0; return PROBE_OK;
     case PROBE_OPT_AUX_SMS:
       if (value < 1 || value > ctx->num_sms) return fail(ctx, PROBE_EINVAL, "aux SM cap %lld out of range", (long long)value);
       ctx->aux_sms = static_cast<int>(value);

@@ -198,6 +198,26 @@ __device__ __forceinline__ void st_cluster_u32(uint32_t cluster_addr, uint32_t v
 }
 // 2-CTA TMA load: data lands in THIS CTA's smem, the transaction bytes are counted on the
 // LEADER CTA's mbarrier (peer bit 24 of the shared::cluster address cleared).
+// TMA gather4 (sm_100a): 4 rows r0..r3 × box[0] columns from a 2-D map whose box is {cols, 1},
+// written as 4 consecutive smem rows (the swizzle follows the smem address, like a tile load).
+__device__ __forceinline__ void tma_gather4(const CUtensorMap* m, uint64_t* bar, void* dst, int c0, int r0, int r1,
+                                            int r2, int r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+      : "memory");
+}
+// CTA-pair form: completes on the LEADER CTA's barrier (peer bit of the address cleared).
+__device__ __forceinline__ void tma_gather4_cg2(const CUtensorMap* m, uint64_t* bar_local, void* dst, int c0, int r0,
+                                                int r1, int r2, int r3) {
+  const uint32_t bar = smem_u32(bar_local) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_2d_cg2(const CUtensorMap* m, uint64_t* bar_local, void* dst, int c0, int c1) {
   const uint32_t bar = smem_u32(bar_local) & 0xFEFFFFFFu;
   asm volatile(
