@@ -161,7 +161,7 @@ def run_probe(args):
     alpha_ps, beta_ps, n_sat, bw_Bpus = cost_model(shape, pk)
     cfg = ProbeConfig(G=G, E=shape.E, k=shape.k, H=shape.H, F=shape.F, T=shape.T, h=shape.h, rank_begin=R0,
                       local_ranks=GL, replica_budget=3, kmax=16, n_sat=n_sat, alpha_ps=alpha_ps, beta_ps=beta_ps,
-                      bw_bytes_per_us=bw_Bpus, capacity_factor=4.0 if G > 1 else 1.0)
+                      bw_bytes_per_us=bw_Bpus, capacity_factor=args.cap if G > 1 else 1.0)
     if world > 1:
         from paper_2602_00509_b200.dist import make_runtime_distributed
         rt = make_runtime_distributed(cfg, dev, pg)
@@ -562,6 +562,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-emulation", action="store_true")
     ap.add_argument("--ep", type=int, default=0, help="EP size G (default: the config's, 8)")
+    ap.add_argument("--cap", type=float, default=4.0, help="receive capacity per rank in units of T·k")
     ap.add_argument("--aux-sms", type=int, default=0, help="grid cap of the aux-stream predictor GEMMs (0: #SMs/2)")
     ap.add_argument("--cpu-tokens", type=int, default=256)
     ap.add_argument("--ref-tokens", type=int, default=16)
