@@ -267,7 +267,8 @@ probe_status probe_distill_apply(probe_ctx ctx, float* master, const float* grad
  * thread-per-token select kernel (default off: measured slower). */
 enum { PROBE_OPT_EP_EMULATION = 1, PROBE_OPT_UNFUSED_TOPK = 2, PROBE_OPT_FUSED_EPILOGUE_TOPK = 3,
        PROBE_OPT_AUX_SMS = 4 /* grid cap (CTAs) of the predictor GEMMs on the aux stream; default #SMs/2 */,
-       PROBE_OPT_PAIR_GEMM = 5 /* expert GEMMs on CTA pairs (tcgen05 cta_group::2, 256-row tiles);
+       PROBE_OPT_PAIR_GEMM = 5 /* expert GEMMs on CTA pairs (tcgen05 cta_group::2, 256-row tiles) when the
+                                  mean rows per local expert T·k·G/E is at least 256 (else 1-CTA);
                                   default ON, 0 selects the 1-CTA kernel */,
        PROBE_OPT_FUSED_DISPATCH = 6 /* when this process hosts every rank: dispatch writes only the
                                        receive-row → x-row index and the expert GEMM1 producer gathers

@@ -584,7 +584,11 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   li.replicas = use_plan ? ctx->at<int32_t>(s.reps[p]) : nullptr;
   li.bank = p;
   li.nparts = (ctx->ep_emulation && d.GL > 1 && d.GL <= kMaxParts) ? d.GL : 0;
-  li.tile_m = ctx->pair_gemm ? 256 : 128;
+  // CTA pairs pay off when expert groups fill 256-row tiles; decode-sized groups (mean rows per
+  // local expert T·k·G/E below 256, e.g. C2: 64) run faster on the 1-CTA kernel (measured:
+  // C2 expert GEMMs 1.45 ms on pairs vs 1.15 ms on single CTAs)
+  const bool pair = ctx->pair_gemm && static_cast<int64_t>(T) * d.k * d.G >= 256LL * d.E;
+  li.tile_m = pair ? 256 : 128;
   li.act = ctx->scratch + s.act;
   li.y_local = ctx->local_base[PROBE_BUF_Y];
   // fused dispatch (a6 → a7): every rank in this process, so GEMM1 can gather the x rows itself
@@ -621,7 +625,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   MARK(6);
   CK(ev_record(ctx, ctx->ev_gemm[p], st));
   // a7 grouped SwiGLU expert FFN (tcgen05): act = SiLU(X W_gᵀ) ⊙ X W_uᵀ ; Y = act W_dᵀ
-  const int vexp = ctx->pair_gemm ? V_2CTA_256_6_4 : V_256_4_4;
+  const int vexp = pair ? V_2CTA_256_6_4 : V_256_4_4;
   CK(launch_gemm_v(vexp, fused ? *mxg : ctx->map_recv, *m13, ctx->map_rw13, ctx->map_recv, lo.s1, d.H, ctx->num_sms,
                    st));
   ++ctx->launches;

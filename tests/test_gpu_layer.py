@@ -34,8 +34,12 @@ CASES = {
                                          pair_gemm=False, ep_emulation=True),
     "ep-emulation": CaseCfg(pi.C0.with_(name="epem", E=64, k=8, H=512, F=384, T=300, G=8), zipf_s=1.2,
                             ep_emulation=True),
+    # CTA-pair expert GEMMs (chosen when T·k·G/E ≥ 256 rows per local expert)
+    "pair-gemm": CaseCfg(pi.C0.with_(name="pgl", E=16, k=4, H=256, F=256, T=700, G=4), zipf_s=1.3),
+    "pair-gemm-ep-emulation": CaseCfg(pi.C0.with_(name="pgle", E=16, k=4, H=256, F=384, T=600, G=4), zipf_s=1.2,
+                                      ep_emulation=True),
     # opt-in fused dispatch: expert GEMM1 gathers its rows from x with TMA gather4
-    "fused-dispatch-gather": CaseCfg(pi.C0.with_(name="fdg", E=32, k=4, H=512, F=384, T=333, G=4), zipf_s=1.3,
+    "fused-dispatch-gather": CaseCfg(pi.C0.with_(name="fdg", E=16, k=4, H=512, F=384, T=1100, G=4), zipf_s=1.3,
                                      fused_dispatch=True),
     "fused-dispatch-gather-one-cta": CaseCfg(pi.C0.with_(name="fdg1", E=32, k=4, H=512, F=256, T=200, G=4),
                                              zipf_s=1.3, fused_dispatch=True, pair_gemm=False),
