@@ -170,6 +170,9 @@ def run_probe(args):
     if args.aux_sms:
         from paper_2602_00509_b200._lib import OPT_AUX_SMS
         rt.set_option(OPT_AUX_SMS, args.aux_sms)
+    if args.fused_dispatch:
+        from paper_2602_00509_b200._lib import OPT_FUSED_DISPATCH
+        rt.set_option(OPT_FUSED_DISPATCH, args.fused_dispatch)
     ranks = list(range(R0, R0 + GL))
     t0 = time.time()
     pool = [pi.layer_inputs(shape, 0, i, args.zipf, ranks=ranks, device=dev, wrap=POOL) for i in range(POOL)]
@@ -562,6 +565,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-emulation", action="store_true")
     ap.add_argument("--ep", type=int, default=0, help="EP size G (default: the config's, 8)")
+    ap.add_argument("--fused-dispatch", type=int, default=0, choices=[0, 1, 2],
+                    help="GEMM1 gathers x rows: 1 TMA gather4, 2 cp.async warps (default 0: receive copy)")
     ap.add_argument("--cap", type=float, default=4.0, help="receive capacity per rank in units of T·k")
     ap.add_argument("--aux-sms", type=int, default=0, help="grid cap of the aux-stream predictor GEMMs (0: #SMs/2)")
     ap.add_argument("--cpu-tokens", type=int, default=256)

@@ -271,11 +271,11 @@ enum { PROBE_OPT_EP_EMULATION = 1, PROBE_OPT_UNFUSED_TOPK = 2, PROBE_OPT_FUSED_E
                                   mean rows per local expert T·k·G/E is at least 256 (else 1-CTA);
                                   default ON, 0 selects the 1-CTA kernel */,
        PROBE_OPT_FUSED_DISPATCH = 6 /* when this process hosts every rank: dispatch writes only the
-                                       receive-row → x-row index and the expert GEMM1 producer gathers
-                                       its A rows from x with TMA gather4 (no receive-buffer copy);
-                                       ignored with local_ranks < ep_size.  Default OFF: measured
-                                       GEMM1 7.5 ms vs 2.5 ms — gather4 delivers ~1 row per ~20
-                                       cycles per SM, 3x below the MMA's A consumption */ };
+                                       receive-row → x-row index and expert GEMM1 gathers its A rows
+                                       from x (no receive-buffer copy).  1: TMA gather4 in the
+                                       producer warp; 2: 16-byte cp.async by two gather warps (1-CTA
+                                       kernel).  Ignored with local_ranks < ep_size.  Default 0: see
+                                       DESIGN.md §6 for the measurements */ };
 probe_status probe_set_option(probe_ctx ctx, int32_t option, int64_t value);
 
 /* Number of library kernel launches enqueued so far by this context (bench accounting). */

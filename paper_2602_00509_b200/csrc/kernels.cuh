@@ -559,6 +559,7 @@ struct LayoutIn {
   void* act;                    // [GL*cap, F] bf16
   void* y_local;                // [GL*cap, H] fp16 (this process's Y region, D2)
   const int32_t* gather_idx;    // fused dispatch: GEMM1 gathers its A rows through this index (else null)
+  const void* gather_src;       // software gather: x rows (bf16, H per row); null = TMA gather4
 };
 
 __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o) {
@@ -703,6 +704,8 @@ __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o
       sc->tile_m = in.tile_m;
       sc->stats = nullptr;
       sc->gather_idx = w == 0 ? in.gather_idx : nullptr;
+      sc->gather_src = w == 0 ? in.gather_src : nullptr;
+      sc->gather_ld = d.H;
       sched_reset_counters(sc);
       sc->nparts = in.nparts > 1 ? in.nparts : 0;
       if (in.nparts > 1) {

@@ -195,7 +195,7 @@ struct probe_ctx_s {
   bool ep_emulation = false;  // partition expert GEMMs by local rank (probe_set_option)
   bool fused_epi_topk = false;  // top-k in the GEMM epilogue instead of k_select (probe_set_option)
   bool pair_gemm = true;        // expert GEMMs on CTA pairs (cta_group::2); option turns it off
-  bool fused_dispatch = false;  // single process: GEMM1 gathers x rows (TMA gather4), no receive copy (opt-in: slower)
+  int fused_dispatch = 0;       // single process, GEMM1 gathers x rows: 1 TMA gather4, 2 cp.async warps (opt-in)
   // distillation workspace (NEXT-1), allocated on the first probe_distill_grad
   uint8_t* dbuf = nullptr;
   size_t dbytes = 0;
@@ -587,15 +587,17 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   // CTA pairs pay off when expert groups fill 256-row tiles; decode-sized groups (mean rows per
   // local expert T·k·G/E below 256, e.g. C2: 64) run faster on the 1-CTA kernel (measured:
   // C2 expert GEMMs 1.45 ms on pairs vs 1.15 ms on single CTAs)
-  const bool pair = ctx->pair_gemm && static_cast<int64_t>(T) * d.k * d.G >= 256LL * d.E;
+  // fused dispatch (a6 → a7): every rank in this process, so GEMM1 can gather the x rows itself
+  const bool fused = ctx->fused_dispatch != 0 && !ctx->multi_process();
+  const bool sw_gather = fused && ctx->fused_dispatch == 2;        // cp.async gather: 1-CTA kernel
+  const bool pair = ctx->pair_gemm && !sw_gather && static_cast<int64_t>(T) * d.k * d.G >= 256LL * d.E;
   li.tile_m = pair ? 256 : 128;
   li.act = ctx->scratch + s.act;
   li.y_local = ctx->local_base[PROBE_BUF_Y];
-  // fused dispatch (a6 → a7): every rank in this process, so GEMM1 can gather the x rows itself
-  const bool fused = ctx->fused_dispatch && !ctx->multi_process();
-  const CUtensorMap* mxg = fused ? ctx->maps.get(x, GL * T, d.H, 1) : nullptr;
-  if (fused && !mxg) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
+  const CUtensorMap* mxg = fused && ctx->fused_dispatch == 1 ? ctx->maps.get(x, GL * T, d.H, 1) : nullptr;
+  if (fused && ctx->fused_dispatch == 1 && !mxg) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
   li.gather_idx = fused ? ctx->at<int32_t>(s.gidx) : nullptr;
+  li.gather_src = sw_gather ? x : nullptr;
   LayoutOut lo;
   lo.split_cum = ctx->at<int32_t>(s.split_cum);
   lo.slot_of = ctx->at<int32_t>(s.slot_of);
@@ -626,7 +628,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   CK(ev_record(ctx, ctx->ev_gemm[p], st));
   // a7 grouped SwiGLU expert FFN (tcgen05): act = SiLU(X W_gᵀ) ⊙ X W_uᵀ ; Y = act W_dᵀ
   const int vexp = pair ? V_2CTA_256_6_4 : V_256_4_4;
-  CK(launch_gemm_v(vexp, fused ? *mxg : ctx->map_recv, *m13, ctx->map_rw13, ctx->map_recv, lo.s1, d.H, ctx->num_sms,
+  CK(launch_gemm_v(vexp, mxg ? *mxg : ctx->map_recv, *m13, ctx->map_rw13, ctx->map_recv, lo.s1, d.H, ctx->num_sms,
                    st));
   ++ctx->launches;
   MARK(7);
@@ -1183,7 +1185,10 @@ probe_status probe_set_option(probe_ctx ctx, int32_t option, int64_t value) {
     case PROBE_OPT_UNFUSED_TOPK: ctx->unfused = value != 0; return PROBE_OK;
     case PROBE_OPT_FUSED_EPILOGUE_TOPK: ctx->fused_epi_topk = value != 0; return PROBE_OK;
     case PROBE_OPT_PAIR_GEMM: ctx->pair_gemm = value != 0; return PROBE_OK;
-    case PROBE_OPT_FUSED_DISPATCH: ctx->fused_dispatch = value != 0; return PROBE_OK;
+    case PROBE_OPT_FUSED_DISPATCH:
+      if (value < 0 || value > 2) return fail(ctx, PROBE_EINVAL, "fused dispatch mode %lld not in {0,1,2}", (long long)value);
+      ctx->fused_dispatch = static_cast<int>(value);
+      return PROBE_OK;
     case PROBE_OPT_AUX_SMS:
       if (value < 1 || value > ctx->num_sms) return fail(ctx, PROBE_EINVAL, "aux SM cap %lld out of range", (long long)value);
       ctx->aux_sms = static_cast<int>(value);

@@ -35,7 +35,7 @@ class CaseCfg:
     ep_emulation: bool = False      # partitioned expert GEMMs (single-GPU EP straggler emulation)
     fused_epi_topk: bool = False    # router/predictor top-k in the GEMM epilogue
     pair_gemm: bool = True          # expert GEMMs on CTA pairs (cta_group::2); False → 1-CTA kernel
-    fused_dispatch: bool = False    # True → GEMM1 gathers x rows (TMA gather4) instead of the receive copy
+    fused_dispatch: int = 0         # 1/2: GEMM1 gathers x rows (TMA gather4 / cp.async) instead of the receive copy
 
 
 def f64(t):
@@ -72,7 +72,7 @@ def run_gpu(case: CaseCfg):
         rt.set_option(OPT_PAIR_GEMM, 0)
     if case.fused_dispatch:
         from paper_2602_00509_b200._lib import OPT_FUSED_DISPATCH
-        rt.set_option(OPT_FUSED_DISPATCH, 1)
+        rt.set_option(OPT_FUSED_DISPATCH, int(case.fused_dispatch))
     if case.fused_epi_topk:
         from paper_2602_00509_b200._lib import OPT_FUSED_EPILOGUE_TOPK
         rt.set_option(OPT_FUSED_EPILOGUE_TOPK, 1)

@@ -45,6 +45,10 @@ CASES = {
                                              zipf_s=1.3, fused_dispatch=True, pair_gemm=False),
     "fused-dispatch-gather-ep-emulation": CaseCfg(pi.C0.with_(name="fdge", E=64, k=8, H=512, F=256, T=256, G=8),
                                                   zipf_s=1.2, fused_dispatch=True, ep_emulation=True),
+    "fused-dispatch-cp-async": CaseCfg(pi.C0.with_(name="fdc", E=32, k=4, H=512, F=384, T=333, G=4), zipf_s=1.3,
+                                       fused_dispatch=2),
+    "fused-dispatch-cp-async-ep-emulation": CaseCfg(pi.C0.with_(name="fdce", E=64, k=8, H=512, F=256, T=256, G=8),
+                                                    zipf_s=1.2, fused_dispatch=2, ep_emulation=True),
 }
 
 
