@@ -10,7 +10,9 @@
  *
  * Conventions for every entry point:
  *  - Pointers are DEVICE pointers unless stated; row-major; bf16 = IEEE bfloat16
- *    (uint16 storage), fp32 = IEEE binary32.
+ *    (uint16 storage), fp32 = IEEE binary32.  "act" below = the activation/weight element
+ *    type selected by probe_config.dtype: bf16 (default) or fp32 (parity path); every
+ *    activation / weight pointer documented as bf16 is fp32 when dtype = PROBE_FP32.
  *  - `stream` is a cudaStream_t passed as void* (no CUDA headers needed).
  *  - Every call only ENQUEUES work on its stream(s) and never synchronises the
  *    host (CUDA-Graph safe), except probe_check/probe_finalize.
@@ -69,19 +71,25 @@ typedef struct {
   int32_t replica_budget; /* R_b <= 3 redundant experts per rank; 0 => static EP */
   int32_t kmax;           /* planner iteration cap k_max (16) */
   int32_t n_sat;          /* η_g knee in pairs: c(m) = max(m, n_sat) for m > 0 (Eq. 2, R11) */
-  int32_t reserved;       /* must be 0 */
+  int32_t dtype;          /* PROBE_BF16 (product path: bf16 operands on tcgen05, fp32 accumulate)
+                             or PROBE_FP32 (parity path: x, router, predictor and expert weights fp32,
+                             SIMT fp32 GEMMs; north_star's 1e-5·RMS bound).  Selects the element type of
+                             every activation/weight pointer below and of the RECV/Y/replica buffers. */
   int64_t alpha_ps;       /* compute cost per routed pair, picoseconds (F̄/F_peak, R11) */
   int64_t beta_ps;        /* comm cost per remote pair, picoseconds (2·2H/BW_net, Eq. 5, λ=1) */
   int64_t bw_bytes_per_us;/* BW_net for Eq. 6 replica caps */
-  int64_t expert_bytes;   /* 𝒲 = 6·H·F bytes (bf16); checked */
+  int64_t expert_bytes;   /* 𝒲 = 3·H·F·sizeof(dtype) bytes (6HF for bf16, 12HF for fp32); checked */
 } probe_config;
+
+/* probe_config.dtype */
+enum { PROBE_BF16 = 0, PROBE_FP32 = 1 };
 
 /* Buffer ids for probe_workspace / probe_init. */
 enum {
-  PROBE_BUF_RECV = 0,    /* symmetric [recv_capacity, H] bf16: dispatched token rows (peers write) */
-  PROBE_BUF_Y = 1,       /* symmetric [recv_capacity, H] fp16: expert outputs (peers read in combine; D2) */
-  PROBE_BUF_REP_W13 = 2, /* symmetric [2*R_b, 2F, H] bf16: replica slots, 2 banks by layer parity */
-  PROBE_BUF_REP_W2 = 3,  /* symmetric [2*R_b, H, F] bf16 */
+  PROBE_BUF_RECV = 0,    /* symmetric [recv_capacity, H] act (bf16/fp32): dispatched token rows (peers write) */
+  PROBE_BUF_Y = 1,       /* symmetric [recv_capacity, H] fp16 (fp32 when dtype = PROBE_FP32): expert outputs (peers read in combine; D2) */
+  PROBE_BUF_REP_W13 = 2, /* symmetric [2*R_b, 2F, H] act: replica slots, 2 banks by layer parity */
+  PROBE_BUF_REP_W2 = 3,  /* symmetric [2*R_b, H, F] act */
   PROBE_BUF_BOARD = 4,   /* symmetric count boards [2 parity][2 kind][G][E] int32 + flags */
   PROBE_BUF_SIGNAL = 5,  /* symmetric signal pad (cross-process barriers) */
   PROBE_NSYM = 6,
@@ -105,10 +113,12 @@ probe_status probe_init(const probe_config* cfg, const uint64_t* peer_ptrs, void
 /* Main track for layer L: gate (ground-truth router + top-k, R1-R5) →
  * actual-count all-gather → materialize plan(L) on the actual counts (R23) →
  * dispatch (R24 layout) → grouped SwiGLU GEMMs → gate-weighted combine (R25).
- *   x         [local_ranks, T, H] bf16 (this process's ranks, rank_begin first)
- *   w_router  [E, H] bf16;  b_router [E] fp32 or NULL
- *   w13       [local_ranks*E/G, 2F, H] bf16 base experts of the local ranks (gate rows 0..F-1, up F..2F-1)
- *   w2        [local_ranks*E/G, H, F] bf16
+ *   x         [local_ranks, T, H] act (this process's ranks, rank_begin first)
+ *   w_router  [E, H] act;  b_router [E] fp32 or NULL
+ *   w13       [local_ranks*E/G, 2F, H] act base experts of the local ranks (gate rows 0..F-1, up F..2F-1)
+ *   w2        [local_ranks*E/G, H, F] act
+ * dtype = PROBE_FP32: every GEMM is fp32 (SIMT, ascending-K FMA), the SwiGLU activation and Y
+ * stay fp32; routing/plan/layout are the same integer kernels as the bf16 path.
  *   use_plan  0 ⇒ static EP (P′); 1 ⇒ the plan computed by probe_plan(layer)
  *   out       [local_ranks, T, H], fp32 if out_fp32 else bf16
  *   topk_ids  [local_ranks, T, k] int32 or NULL;  topk_w [local_ranks, T, k] fp32 or NULL
@@ -122,7 +132,8 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
 /* Lookahead predictor for layer `next_layer` (Eq. (P)): l̂ = W x + b + Ŵ2·bf16(SiLU(Ŵ1 x))
  * on the CURRENT layer's input x (R6), top-k (lowest-id ties), per-rank predicted
  * counts n̂[r][e] (R9) all-gathered into every rank's count board.
- *   w_res1 [h, H] bf16 or NULL, w_res2 [E, h] bf16 or NULL (NULL ⇒ frozen prior only)
+ *   x, w_router_next act;  w_res1 [h, H] act or NULL, w_res2 [E, h] act or NULL (NULL ⇒ frozen prior only);
+ *   the activation is rounded to bf16 in both dtypes (R8: part of the predictor's definition)
  *   pred_counts [G, E] int32 out or NULL;  pred_logits [local_ranks, T, E] fp32 out or NULL
  * If probe_moe_forward(next_layer-1) was enqueued, waits for its gate (x ready). */
 probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int32_t T,
@@ -247,7 +258,8 @@ probe_status probe_history_update(probe_ctx ctx, int32_t layer, int32_t reset, i
  * The first call allocates a workspace (~N·(10h + 12E + 2H) bytes, N = local_ranks ·
  * max_tokens) and must not be inside a stream capture.  Everything runs on `stream` (NULL =
  * the legacy default stream, as in plain CUDA); inputs must be complete on it.  Errors: PROBE_EINVAL (null), PROBE_ESHAPE
- * (res_hidden == 0), PROBE_ECAPACITY (T), PROBE_ESTATE (first call under capture).
+ * (res_hidden == 0, or dtype = PROBE_FP32: distillation is bf16-only), PROBE_ECAPACITY (T),
+ * PROBE_ESTATE (first call under capture).
  *
  * probe_distill_apply (R36): master[i] += scale · grad[i] (fp32, n elements; scale =
  * −lr / N_total) and w[i] = bf16(master[i]) — the bf16 copy the product path reads. */

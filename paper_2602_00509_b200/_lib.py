@@ -25,6 +25,7 @@ EXPORTS = ["probe_workspace", "probe_init", "probe_moe_forward", "probe_predict"
            "probe_ipc_export", "probe_ipc_import", "probe_ipc_close", "probe_set_option",
            "probe_history_update", "probe_distill_grad", "probe_distill_apply"]
 OPT_EP_EMULATION, OPT_UNFUSED_TOPK, OPT_FUSED_EPILOGUE_TOPK, OPT_AUX_SMS, OPT_PAIR_GEMM, OPT_FUSED_DISPATCH = 1, 2, 3, 4, 5, 6
+DTYPES = {"bf16": 0, "fp32": 1}      # probe_config.dtype (PROBE_BF16, PROBE_FP32)
 PROBE_NPHASE = 10
 PHASES = ["gate", "select", "counts", "layout", "dispatch", "wait", "gemm1", "gemm2", "combine", "total"]
 
@@ -33,7 +34,7 @@ class probe_config(C.Structure):
     _fields_ = [("ep_size", C.c_int32), ("rank_begin", C.c_int32), ("local_ranks", C.c_int32),
                 ("num_experts", C.c_int32), ("top_k", C.c_int32), ("hidden", C.c_int32), ("ffn", C.c_int32),
                 ("res_hidden", C.c_int32), ("max_tokens", C.c_int32), ("recv_capacity", C.c_int32),
-                ("replica_budget", C.c_int32), ("kmax", C.c_int32), ("n_sat", C.c_int32), ("reserved", C.c_int32),
+                ("replica_budget", C.c_int32), ("kmax", C.c_int32), ("n_sat", C.c_int32), ("dtype", C.c_int32),
                 ("alpha_ps", C.c_int64), ("beta_ps", C.c_int64), ("bw_bytes_per_us", C.c_int64),
                 ("expert_bytes", C.c_int64)]
 

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libprobe.so")
 SOURCES = ["csrc/probe.cu"]
-DEPS = ["csrc/probe.cu", "csrc/kernels.cuh", "csrc/gemm_sm100.cuh", "csrc/sm100_ptx.cuh", "csrc/distill.cuh",
+DEPS = ["csrc/probe.cu", "csrc/kernels.cuh", "csrc/gemm_sm100.cuh", "csrc/sm100_ptx.cuh", "csrc/distill.cuh", "csrc/sgemm_f32.cuh",
         os.path.join("..", "include", "probe.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -560,6 +560,7 @@ struct LayoutIn {
   void* y_local;                // [GL*cap, H] fp16 (this process's Y region, D2)
   const int32_t* gather_idx;    // fused dispatch: GEMM1 gathers its A rows through this index (else null)
   const void* gather_src;       // software gather: x rows (bf16, H per row); null = TMA gather4
+  int f32;                      // fp32 parity path: act and Y are fp32, GEMM2 stores EPI_F32
 };
 
 __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o) {
@@ -668,12 +669,12 @@ __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o
     g1.a_row = arow; g1.m = m; g1.b_row = wslot * 2 * d.F; g1.b_sel = is_rep; g1.mode = EPI_SWIGLU;
     g1.n = d.F; g1.ldc = d.F; g1.tile_start = 0; g1.out_row = arow; g1.tma_out = 0;
     g1.topk = 0; g1.rows_per_rank = 1; g1.k_off = 0; g1.aux = nullptr; g1.bias = nullptr;
-    g1.out = reinterpret_cast<__nv_bfloat16*>(in.act) + static_cast<size_t>(arow) * d.F;
+    g1.out = static_cast<uint8_t*>(in.act) + static_cast<size_t>(arow) * d.F * (in.f32 ? 4 : 2);
     GemmGroup g2;
-    g2.a_row = arow; g2.m = m; g2.b_row = wslot * d.H; g2.b_sel = is_rep; g2.mode = EPI_F16;
-    g2.n = d.H; g2.ldc = d.H; g2.tile_start = 0; g2.out_row = arow; g2.tma_out = (d.H % 32 == 0);
+    g2.a_row = arow; g2.m = m; g2.b_row = wslot * d.H; g2.b_sel = is_rep; g2.mode = in.f32 ? EPI_F32 : EPI_F16;
+    g2.n = d.H; g2.ldc = d.H; g2.tile_start = 0; g2.out_row = arow; g2.tma_out = !in.f32 && (d.H % 32 == 0);
     g2.topk = 0; g2.rows_per_rank = 1; g2.k_off = 0; g2.aux = o.err; g2.bias = nullptr;
-    g2.out = reinterpret_cast<__half*>(in.y_local) + static_cast<size_t>(arow) * d.H;
+    g2.out = static_cast<uint8_t*>(in.y_local) + static_cast<size_t>(arow) * d.H * (in.f32 ? 4 : 2);
     o.s1->g[i] = g1;
     o.s2->g[i] = g2;
     t1[i] = gemm_ntiles(g1, 256, in.tile_m);
@@ -723,7 +724,7 @@ __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o
 // Fused mode (gidx != null, every rank in this process): only the route and the
 // receive-row → x-row index are written; the expert GEMM1 producer gathers the rows.
 // =============================================================================
-__global__ void __launch_bounds__(256) k_dispatch(Dims d, int T, const __nv_bfloat16* __restrict__ x,
+__global__ void __launch_bounds__(256) k_dispatch(Dims d, int T, const uint8_t* __restrict__ x, int row_bytes,
                                                   const int32_t* __restrict__ ids,
                                                   const int32_t* __restrict__ pos,
                                                   const int32_t* __restrict__ cbase,
@@ -762,13 +763,13 @@ __global__ void __launch_bounds__(256) k_dispatch(Dims d, int T, const __nv_bflo
       // GEMM1 gathers it with TMA gather4; nothing is copied
       if (row >= 0) gidx[static_cast<size_t>(dd - d.R0) * d.cap + row] = static_cast<int32_t>(pr);
     } else if (row >= 0) {
-      dst_row = sym.at(buf_recv, d.G, dd) + static_cast<size_t>(row) * d.H * 2;
+      dst_row = sym.at(buf_recv, d.G, dd) + static_cast<size_t>(row) * row_bytes;
     }
   }
   if (gidx) return;
   // copy: the x row is read once (batches of 8 × 16 B per lane in flight) and stored k times
-  const uint4* src = reinterpret_cast<const uint4*>(x + pr * d.H);
-  const int nv = d.H / 8;
+  const uint4* src = reinterpret_cast<const uint4*>(x + pr * row_bytes);
+  const int nv = row_bytes / 16;
   for (int c0 = 0; c0 < nv; c0 += 32 * 8) {
     uint4 v[8];
 #pragma unroll
@@ -794,7 +795,7 @@ __global__ void __launch_bounds__(256) k_dispatch(Dims d, int T, const __nv_bflo
 // The first CTA raises the prefetch suspend flag (split-phase, R27).
 // block per token, 128 threads.
 // =============================================================================
-template <bool OUT_F32>
+template <bool OUT_F32, bool Y_F32 = false>
 __global__ void __launch_bounds__(128) k_combine(Dims d, int T, const float* __restrict__ gw,
                                                  const int32_t* __restrict__ route, Sym sym, int buf_y, void* out,
                                                  volatile int32_t* suspend_flag, int layer) {
@@ -808,7 +809,8 @@ __global__ void __launch_bounds__(128) k_combine(Dims d, int T, const float* __r
     const int dd = route[(static_cast<size_t>(tok) * k + j) * 2];
     const int row = route[(static_cast<size_t>(tok) * k + j) * 2 + 1];
     srcs[j] = row < 0 ? nullptr
-                      : reinterpret_cast<const uint4*>(sym.at(buf_y, d.G, dd) + static_cast<size_t>(row) * d.H * 2);
+                      : reinterpret_cast<const uint4*>(sym.at(buf_y, d.G, dd) +
+                                                       static_cast<size_t>(row) * d.H * (Y_F32 ? 4 : 2));
     gws[j] = gw[static_cast<size_t>(tok) * k + j];
   }
   __syncthreads();
@@ -821,8 +823,16 @@ __global__ void __launch_bounds__(128) k_combine(Dims d, int T, const float* __r
     for (int i = 0; i < 8; ++i) a[i] = 0.f;
     for (int j = 0; j < k; ++j) {
       if (!srcs[j]) continue;
-      const uint4 y = srcs[j][c];
       const float g = gws[j];
+      if (Y_F32) {   // fp32 parity path: two 16-byte loads of fp32 Y per 8 outputs
+        const float4 y0 = reinterpret_cast<const float4*>(srcs[j])[2 * c];
+        const float4 y1 = reinterpret_cast<const float4*>(srcs[j])[2 * c + 1];
+        const float f[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
+#pragma unroll
+        for (int q = 0; q < 8; ++q) a[q] = fmaf(g, f[q], a[q]);
+        continue;
+      }
+      const uint4 y = srcs[j][c];
       const uint32_t yw[4] = {y.x, y.y, y.z, y.w};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -861,10 +871,10 @@ __global__ void __launch_bounds__(512) k_prefetch(Dims d, const int32_t* __restr
                                                   const uint8_t* __restrict__ w13, const uint8_t* __restrict__ w2,
                                                   Sym sym, int buf_rw13, int buf_rw2, int32_t* ctr,
                                                   const volatile int32_t* suspend_flag, int suspend_at,
-                                                  int32_t* done_bytes_lo) {
+                                                  int32_t* done_bytes_lo, int elem_bytes) {
   __shared__ int s_chunk;
-  const size_t w13_bytes = static_cast<size_t>(2) * d.F * d.H * 2;
-  const size_t w2_bytes = static_cast<size_t>(d.H) * d.F * 2;
+  const size_t w13_bytes = static_cast<size_t>(2) * d.F * d.H * elem_bytes;
+  const size_t w2_bytes = static_cast<size_t>(d.H) * d.F * elem_bytes;
   const int c13 = static_cast<int>((w13_bytes + kPrefetchChunk - 1) / kPrefetchChunk);
   const int c2 = static_cast<int>((w2_bytes + kPrefetchChunk - 1) / kPrefetchChunk);
   const int cper = c13 + c2;

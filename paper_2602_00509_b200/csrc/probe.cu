@@ -15,6 +15,7 @@
 #include "../../include/probe.h"
 #include "kernels.cuh"
 #include "distill.cuh"
+#include "sgemm_f32.cuh"
 
 using namespace probe;
 
@@ -104,6 +105,8 @@ struct MapCache {
 };
 
 size_t al(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+// bytes per element of activations / weights / Y: 2 (bf16 path; Y fp16, D2) or 4 (PROBE_FP32)
+size_t esz(const probe_config& c) { return c.dtype == PROBE_FP32 ? 4 : 2; }
 
 struct Scratch {
   size_t sym, logits, pprior, pres, pact, ids, gw, pos, hist, cbase, route, pred_local;
@@ -123,7 +126,7 @@ Scratch scratch_layout(const probe_config& c) {
   s.logits = take(GL * T * E * 4);
   s.pprior = take(GL * T * E * 4);
   s.pres = take(GL * T * E * 4);
-  s.pact = take(GL * T * h * 2);
+  s.pact = take(GL * T * h * esz(c));
   s.ids = take(GL * T * k * 4);
   s.gw = take(GL * T * k * 4);
   s.pos = take(GL * T * k * 4);
@@ -149,17 +152,18 @@ Scratch scratch_layout(const probe_config& c) {
   s.s_p2 = take(sizeof(GemmSched));
   s.flags = take(256);
   s.gidx = take((GL * cap + 512) * 4);     // fused dispatch: receive row → x row (+ tile overhang)
-  s.act = take(GL * cap * F * 2);
+  s.act = take(GL * cap * F * esz(c));
   s.total = al(o, 1024);
   return s;
 }
 
 void sym_sizes(const probe_config& c, uint64_t b[PROBE_NBUF]) {
   const uint64_t cap = c.recv_capacity, H = c.hidden, F = c.ffn, G = c.ep_size, E = c.num_experts;
-  b[PROBE_BUF_RECV] = al(cap * H * 2, 1024);
-  b[PROBE_BUF_Y] = al(cap * H * 2, 1024);   // fp16 (D2)
-  b[PROBE_BUF_REP_W13] = al(2 * kMaxRb * 2 * F * H * 2, 1024);
-  b[PROBE_BUF_REP_W2] = al(2 * kMaxRb * H * F * 2, 1024);
+  const uint64_t es = esz(c);
+  b[PROBE_BUF_RECV] = al(cap * H * es, 1024);
+  b[PROBE_BUF_Y] = al(cap * H * es, 1024);   // fp16 (D2) / fp32
+  b[PROBE_BUF_REP_W13] = al(2 * kMaxRb * 2 * F * H * es, 1024);
+  b[PROBE_BUF_REP_W2] = al(2 * kMaxRb * H * F * es, 1024);
   b[PROBE_BUF_BOARD] = al(4 * G * E * 4 + 1024, 1024);
   b[PROBE_BUF_SIGNAL] = 4096;
   b[PROBE_BUF_SCRATCH] = scratch_layout(c).total;
@@ -191,6 +195,7 @@ struct probe_ctx_s {
   int64_t launches = 0;
   uint32_t epoch[kSigKinds] = {0};   // cross-process barrier epochs (identical sequence on every process)
   bool multi_process() const { return cfg.local_ranks != cfg.ep_size; }
+  bool f32() const { return cfg.dtype == PROBE_FP32; }   // fp32 parity path (SIMT GEMMs)
   bool unfused = false;   // PROBE_UNFUSED=1: logits written + separate top-k kernels (debug)
   bool ep_emulation = false;  // partition expert GEMMs by local rank (probe_set_option)
   bool fused_epi_topk = false;  // top-k in the GEMM epilogue instead of k_select (probe_set_option)
@@ -371,6 +376,14 @@ cudaError_t ev_wait(probe_ctx ctx, cudaStream_t st, cudaEvent_t ev) {
 
 enum { BAR_COUNTS = 0, BAR_DISPATCH = 1, BAR_Y = 2, BAR_PRED = 3, BAR_PREFETCH = 4 };
 
+// fp32 parity path: grouped SIMT GEMM over a device-resident schedule (sgemm_f32.cuh)
+cudaError_t launch_sgemm(probe_ctx ctx, const GemmSched* sc, const void* A, const void* B0, const void* B1, int K,
+                         cudaStream_t st) {
+  k_sgemm_grouped<<<ctx->num_sms * 4, 256, 0, st>>>(sc, static_cast<const float*>(A), static_cast<const float*>(B0),
+                                                    static_cast<const float*>(B1), K);
+  return cudaGetLastError();
+}
+
 // Cross-process barrier (no-op when this process hosts every rank: stream order suffices).
 cudaError_t xbarrier(probe_ctx ctx, int kind, cudaStream_t st) {
   if (!ctx->multi_process()) return cudaSuccess;
@@ -414,10 +427,10 @@ static probe_status validate(const probe_config& c) {
   if (c.kmax < 0) return fail(nullptr, PROBE_EINVAL, "kmax < 0");
   if (c.n_sat < 0 || c.alpha_ps < 0 || c.beta_ps < 0 || c.bw_bytes_per_us < 0)
     return fail(nullptr, PROBE_EINVAL, "negative cost constant");
-  if (c.expert_bytes != 6ll * c.hidden * c.ffn)
-    return fail(nullptr, PROBE_EINVAL, "expert_bytes %lld != 6*H*F = %lld", (long long)c.expert_bytes,
-                6ll * c.hidden * c.ffn);
-  if (c.reserved != 0) return fail(nullptr, PROBE_EINVAL, "reserved must be 0");
+  if (c.dtype != PROBE_BF16 && c.dtype != PROBE_FP32) return fail(nullptr, PROBE_EINVAL, "dtype %d not in {0, 1}", c.dtype);
+  if (c.expert_bytes != 3ll * c.hidden * c.ffn * static_cast<int64_t>(esz(c)))
+    return fail(nullptr, PROBE_EINVAL, "expert_bytes %lld != 3*H*F*sizeof(dtype) = %lld", (long long)c.expert_bytes,
+                3ll * c.hidden * c.ffn * static_cast<int64_t>(esz(c)));
   return PROBE_OK;
 }
 
@@ -519,10 +532,11 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const uint64_t GL = d.GL, H = d.H, F = d.F, E = d.E;
   const int nchunks = (T + kChunk - 1) / kChunk;
-  const CUtensorMap* mx = ctx->maps.get(x, GL * T, H, 128);
-  const CUtensorMap* m13 = ctx->maps.get(w13, GL * d.EL * 2 * F, H, 128);
-  const CUtensorMap* m2 = ctx->maps.get(w2, GL * d.EL * H, F, 128);
-  if (!mx || !m13 || !m2) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
+  const bool f32 = ctx->f32();
+  const CUtensorMap* mx = f32 ? nullptr : ctx->maps.get(x, GL * T, H, 128);
+  const CUtensorMap* m13 = f32 ? nullptr : ctx->maps.get(w13, GL * d.EL * 2 * F, H, 128);
+  const CUtensorMap* m2 = f32 ? nullptr : ctx->maps.get(w2, GL * d.EL * H, F, 128);
+  if (!f32 && (!mx || !m13 || !m2)) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
   const Scratch& s = ctx->sl;
   int32_t* err = ctx->at<int32_t>(s.flags);
   int32_t* suspend = err + 1;
@@ -537,7 +551,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   // PROBE_OPT_FUSED_EPILOGUE_TOPK: it saves the 2×33 MB logits round trip but runs the
   // serial selection at 1 warp per SM sub-partition, which measured slower.
   const bool sel = d.k <= kTopkMax && d.E <= kMaxE && !ctx->unfused;
-  const bool fused_gate = sel && ctx->fused_epi_topk;
+  const bool fused_gate = sel && ctx->fused_epi_topk && !f32;
   SmallGroups sg{};
   sg.n = 1;
   sg.BN = d.E <= 128 ? 128 : 256;
@@ -549,12 +563,16 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   } else {
     sg.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_F32, d.E, d.E, ctx->at<float>(s.logits));
   }
-  const CUtensorMap* mr = ctx->maps.get(w_router, E, H, sg.BN / 2);
-  if (!mr) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
   k_write_sched<<<1, 32, 0, st>>>(ctx->at<GemmSched>(s.s_gate), sg);
   CKL();
-  CK(launch_gemm_v(sg.BN == 128 ? V_128_6_4 : V_256_4_4, *mx, *mr, *mr, *mx, ctx->at<GemmSched>(s.s_gate), d.H,
-                   ctx->num_sms, st));
+  if (f32) {
+    CK(launch_sgemm(ctx, ctx->at<GemmSched>(s.s_gate), x, w_router, w_router, d.H, st));
+  } else {
+    const CUtensorMap* mr = ctx->maps.get(w_router, E, H, sg.BN / 2);
+    if (!mr) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
+    CK(launch_gemm_v(sg.BN == 128 ? V_128_6_4 : V_256_4_4, *mx, *mr, *mr, *mx, ctx->at<GemmSched>(s.s_gate), d.H,
+                     ctx->num_sms, st));
+  }
   ++ctx->launches;
   MARK(1);
   if (fused_gate) {
@@ -588,7 +606,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   // local expert T·k·G/E below 256, e.g. C2: 64) run faster on the 1-CTA kernel (measured:
   // C2 expert GEMMs 1.45 ms on pairs vs 1.15 ms on single CTAs)
   // fused dispatch (a6 → a7): every rank in this process, so GEMM1 can gather the x rows itself
-  const bool fused = ctx->fused_dispatch != 0 && !ctx->multi_process();
+  const bool fused = ctx->fused_dispatch != 0 && !ctx->multi_process() && !f32;
   const bool sw_gather = fused && ctx->fused_dispatch == 2;        // cp.async gather: 1-CTA kernel
   const bool pair = ctx->pair_gemm && !sw_gather && static_cast<int64_t>(T) * d.k * d.G >= 256LL * d.E;
   li.tile_m = pair ? 256 : 128;
@@ -598,6 +616,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   if (fused && ctx->fused_dispatch == 1 && !mxg) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
   li.gather_idx = fused ? ctx->at<int32_t>(s.gidx) : nullptr;
   li.gather_src = sw_gather ? x : nullptr;
+  li.f32 = f32;
   LayoutOut lo;
   lo.split_cum = ctx->at<int32_t>(s.split_cum);
   lo.slot_of = ctx->at<int32_t>(s.slot_of);
@@ -613,7 +632,8 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   // a6 dispatch
   {
     const int warps = d.GL * T;
-    k_dispatch<<<(warps + 7) / 8, 256, 0, st>>>(d, T, static_cast<const __nv_bfloat16*>(x), ctx->at<int32_t>(s.ids),
+    k_dispatch<<<(warps + 7) / 8, 256, 0, st>>>(d, T, static_cast<const uint8_t*>(x), static_cast<int>(H * esz(ctx->cfg)),
+                                                ctx->at<int32_t>(s.ids),
                                                 ctx->at<int32_t>(s.pos), ctx->at<int32_t>(s.cbase),
                                                 lo.split_cum, lo.slot_of, lo.src_off, ctx->at<int32_t>(s.route),
                                                 sym_of(ctx), PROBE_BUF_RECV, err,
@@ -628,16 +648,30 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   CK(ev_record(ctx, ctx->ev_gemm[p], st));
   // a7 grouped SwiGLU expert FFN (tcgen05): act = SiLU(X W_gᵀ) ⊙ X W_uᵀ ; Y = act W_dᵀ
   const int vexp = pair ? V_2CTA_256_6_4 : V_256_4_4;
-  CK(launch_gemm_v(vexp, mxg ? *mxg : ctx->map_recv, *m13, ctx->map_rw13, ctx->map_recv, lo.s1, d.H, ctx->num_sms,
-                   st));
+  if (f32) {
+    CK(launch_sgemm(ctx, lo.s1, ctx->local_base[PROBE_BUF_RECV], w13, ctx->local_base[PROBE_BUF_REP_W13], d.H, st));
+  } else {
+    CK(launch_gemm_v(vexp, mxg ? *mxg : ctx->map_recv, *m13, ctx->map_rw13, ctx->map_recv, lo.s1, d.H, ctx->num_sms,
+                     st));
+  }
   ++ctx->launches;
   MARK(7);
-  CK(launch_gemm_v(vexp, ctx->map_act, *m2, ctx->map_rw2, ctx->map_y, lo.s2, d.F, ctx->num_sms, st));
+  if (f32) {
+    CK(launch_sgemm(ctx, lo.s2, ctx->scratch + s.act, w2, ctx->local_base[PROBE_BUF_REP_W2], d.F, st));
+  } else {
+    CK(launch_gemm_v(vexp, ctx->map_act, *m2, ctx->map_rw2, ctx->map_y, lo.s2, d.F, ctx->num_sms, st));
+  }
   ++ctx->launches;
   CK(xbarrier(ctx, BAR_Y, st));                 // every expert rank's Y rows are complete
   MARK(8);
   // a8 combine (raises the prefetch suspend flag, R27)
-  if (out_fp32)
+  if (f32 && out_fp32)
+    k_combine<true, true><<<d.GL * T, 128, 0, st>>>(d, T, ctx->at<float>(s.gw), ctx->at<int32_t>(s.route),
+                                                    sym_of(ctx), PROBE_BUF_Y, out, suspend, layer);
+  else if (f32)
+    k_combine<false, true><<<d.GL * T, 128, 0, st>>>(d, T, ctx->at<float>(s.gw), ctx->at<int32_t>(s.route),
+                                                     sym_of(ctx), PROBE_BUF_Y, out, suspend, layer);
+  else if (out_fp32)
     k_combine<true><<<d.GL * T, 128, 0, st>>>(d, T, ctx->at<float>(s.gw), ctx->at<int32_t>(s.route), sym_of(ctx),
                                               PROBE_BUF_Y, out, suspend, layer);
   else
@@ -672,12 +706,38 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
   if (ctx->fwd_layer == next_layer - 1) CK(ev_wait(ctx, st, ctx->ev_gate[prev]));
   const uint64_t GL = d.GL, H = d.H, E = d.E, h = d.h;
   const Scratch& s = ctx->sl;
-  const CUtensorMap* mx = ctx->maps.get(x, GL * T, H, 128);
-  if (!mx) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
+  const bool f32 = ctx->f32();
+  const CUtensorMap* mx = f32 ? nullptr : ctx->maps.get(x, GL * T, H, 128);
+  if (!f32 && !mx) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
   const int nchunks = (T + kChunk - 1) / kChunk;
   CK(cudaMemsetAsync(ctx->at<int32_t>(s.pred_local), 0, GL * E * 4, st));
   const bool fused = !pred_logits && d.k <= kTopkMax && d.E <= 256 && !ctx->unfused;
-  if (fused) {
+  if (f32) {
+    // fp32 parity path: prior x·W_{L+1}ᵀ and z = x·Ŵ1ᵀ → a = bf16(SiLU(z)) (R8) in one grouped
+    // SIMT launch, residual a·Ŵ2ᵀ, then the warp top-k sums prior + b + residual (Eq. (P))
+    SmallGroups sg{};
+    sg.BN = 128;
+    sg.n = w_res1 ? 2 : 1;
+    sg.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_F32, d.E, d.E, ctx->at<float>(s.pprior));
+    if (w_res1) sg.g[1] = mk_group(0, static_cast<int>(GL * T), 0, 1, EPI_SILU_BF16, d.h, d.h, ctx->scratch + s.pact);
+    k_write_sched<<<1, 32, 0, st>>>(ctx->at<GemmSched>(s.s_p1), sg);
+    CKL();
+    CK(launch_sgemm(ctx, ctx->at<GemmSched>(s.s_p1), x, w_router_next, w_res1 ? w_res1 : w_router_next, d.H, st));
+    ++ctx->launches;
+    if (w_res1) {
+      SmallGroups s2{};
+      s2.BN = 128;
+      s2.n = 1;
+      s2.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_F32, d.E, d.E, ctx->at<float>(s.pres));
+      k_write_sched<<<1, 32, 0, st>>>(ctx->at<GemmSched>(s.s_p2), s2);
+      CKL();
+      CK(launch_sgemm(ctx, ctx->at<GemmSched>(s.s_p2), ctx->scratch + s.pact, w_res2, w_res2, d.h, st));
+      ++ctx->launches;
+    }
+    launch_topk<true>(d, T, nchunks, st, ctx->at<float>(s.pprior), w_res1 ? ctx->at<float>(s.pres) : nullptr,
+                      b_router_next, nullptr, nullptr, nullptr, nullptr, ctx->at<int32_t>(s.pred_local), pred_logits);
+    CKL();
+  } else if (fused) {
     // (1) a = bf16(SiLU(Ŵ1 x))  [GL·T, h]   (2) l̂ = [x | a]·[W_{L+1} | Ŵ2]ᵀ (+b) with the
     // top-k and the per-rank count n̂ fused in the epilogue (one TMEM accumulator for prior
     // + residual; Eq. (P), R8, R9).
@@ -817,13 +877,14 @@ probe_status probe_prefetch(probe_ctx ctx, int32_t next_layer, const void* w13_n
     k_prefetch<<<grid, 512, 0, st>>>(d, ctx->at<int32_t>(s.reps[pp]), pp, static_cast<const uint8_t*>(w13_next),
                                      static_cast<const uint8_t*>(w2_next), sym_of(ctx), PROBE_BUF_REP_W13,
                                      PROBE_BUF_REP_W2, ctx->at<int32_t>(s.pfctr[pp]), flags + 1, next_layer,
-                                     flags + 2);
+                                     flags + 2, static_cast<int>(esz(ctx->cfg)));
     CKL();
     CK(ev_wait(ctx, st, ctx->ev_comb[prev]));
   }
   k_prefetch<<<grid, 512, 0, st>>>(d, ctx->at<int32_t>(s.reps[pp]), pp, static_cast<const uint8_t*>(w13_next),
                                    static_cast<const uint8_t*>(w2_next), sym_of(ctx), PROBE_BUF_REP_W13,
-                                   PROBE_BUF_REP_W2, ctx->at<int32_t>(s.pfctr[pp]), flags + 1, -1, flags + 3);
+                                   PROBE_BUF_REP_W2, ctx->at<int32_t>(s.pfctr[pp]), flags + 1, -1, flags + 3,
+                                   static_cast<int>(esz(ctx->cfg)));
   CKL();
   CK(xbarrier(ctx, BAR_PREFETCH, st));          // every sender finished pushing into our slots
   CK(ev_record(ctx, ctx->ev_slots[pp], st));
@@ -1053,6 +1114,7 @@ probe_status probe_distill_grad(probe_ctx ctx, const void* x, const void* x_next
   if (!x || !x_next || !w_router || !w_res1 || !w_res2 || !grad_res1 || !grad_res2 || !stats)
     return fail(ctx, PROBE_EINVAL, "probe_distill_grad: null pointer");
   if (ctx->cfg.res_hidden <= 0) return fail(ctx, PROBE_ESHAPE, "probe_distill_grad: res_hidden == 0");
+  if (ctx->f32()) return fail(ctx, PROBE_ESHAPE, "probe_distill_grad: bf16 only (dtype = PROBE_FP32)");
   if (T < 1 || T > ctx->cfg.max_tokens) return fail(ctx, PROBE_ECAPACITY, "T=%d outside [1, max_tokens]", T);
   cudaStream_t st = static_cast<cudaStream_t>(stream);   // NULL = the legacy default stream
   const DistillLayout DL = distill_layout(ctx->cfg);

@@ -35,6 +35,7 @@ class ProbeConfig:
     beta_ps: int = 0
     bw_bytes_per_us: int = 770_000
     capacity_factor: float = 0.0   # >0 ⇒ recv_capacity = factor · T·k (rounded up to 128)
+    dtype: str = "bf16"            # "bf16" (product path, tcgen05) or "fp32" (parity path, SIMT fp32 GEMMs)
 
     def __post_init__(self):
         if self.local_ranks == 0:
@@ -48,8 +49,18 @@ class ProbeConfig:
 
     def to_c(self) -> probe_config:
         return probe_config(self.G, self.rank_begin, self.local_ranks, self.E, self.k, self.H, self.F, self.h,
-                            self.T, self.recv_capacity, self.replica_budget, self.kmax, self.n_sat, 0,
-                            self.alpha_ps, self.beta_ps, self.bw_bytes_per_us, 6 * self.H * self.F)
+                            self.T, self.recv_capacity, self.replica_budget, self.kmax, self.n_sat,
+                            _lib.DTYPES[self.dtype], self.alpha_ps, self.beta_ps, self.bw_bytes_per_us,
+                            self.expert_bytes)
+
+    @property
+    def torch_dtype(self):
+        return torch.float32 if self.dtype == "fp32" else torch.bfloat16
+
+    @property
+    def expert_bytes(self) -> int:
+        """𝒲 = 3·H·F·sizeof(dtype): W13 [2F,H] + W2 [H,F]."""
+        return 3 * self.H * self.F * (4 if self.dtype == "fp32" else 2)
 
 
 def _ptr(t: Optional[torch.Tensor]):
@@ -114,8 +125,8 @@ class ProbeRuntime:
 
     def replica_slots(self, local_rank: int):
         c = self.cfg
-        w13 = self.sym_view(_lib.BUF_REP_W13, local_rank, torch.bfloat16, (6, 2 * c.F, c.H))
-        w2 = self.sym_view(_lib.BUF_REP_W2, local_rank, torch.bfloat16, (6, c.H, c.F))
+        w13 = self.sym_view(_lib.BUF_REP_W13, local_rank, c.torch_dtype, (6, 2 * c.F, c.H))
+        w2 = self.sym_view(_lib.BUF_REP_W2, local_rank, c.torch_dtype, (6, c.H, c.F))
         return w13, w2
 
     # ------------------------------------------------------------------ API

@@ -233,16 +233,17 @@ def router_weight(shape: MoEShape, parity: int, device="cpu") -> torch.Tensor:
     return w.to(torch.bfloat16).to(device)
 
 
-def expert_weights(shape: MoEShape, parity: int, experts=None, device="cpu"):
-    """W13 [E,2F,H] (gate rows 0..F-1, up rows F..2F-1) and W2 [E,H,F], bf16(N(0,1)/sqrt(fan_in))."""
+def expert_weights(shape: MoEShape, parity: int, experts=None, device="cpu", dtype=torch.bfloat16):
+    """W13 [E,2F,H] (gate rows 0..F-1, up rows F..2F-1) and W2 [E,H,F], N(0,1)/sqrt(fan_in) stored
+    in `dtype` (bf16: rounded; fp32: the full fp32 draw, for the fp32 parity path)."""
     E, H, F = shape.E, shape.H, shape.F
     experts = range(E) if experts is None else experts
-    w13 = torch.empty(len(experts), 2 * F, H, dtype=torch.bfloat16)
-    w2 = torch.empty(len(experts), H, F, dtype=torch.bfloat16)
+    w13 = torch.empty(len(experts), 2 * F, H, dtype=dtype)
+    w2 = torch.empty(len(experts), H, F, dtype=dtype)
     for i, e in enumerate(experts):
         g = torch_gen(shape.name, parity, int(e), "experts")
-        w13[i] = (torch.randn(2 * F, H, generator=g) / math.sqrt(H)).to(torch.bfloat16)
-        w2[i] = (torch.randn(H, F, generator=g) / math.sqrt(F)).to(torch.bfloat16)
+        w13[i] = (torch.randn(2 * F, H, generator=g) / math.sqrt(H)).to(dtype)
+        w2[i] = (torch.randn(H, F, generator=g) / math.sqrt(F)).to(dtype)
     return w13.to(device), w2.to(device)
 
 

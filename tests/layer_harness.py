@@ -36,9 +36,16 @@ class CaseCfg:
     fused_epi_topk: bool = False    # router/predictor top-k in the GEMM epilogue
     pair_gemm: bool = True          # expert GEMMs on CTA pairs (cta_group::2); False → 1-CTA kernel
     fused_dispatch: int = 0         # 1/2: GEMM1 gathers x rows (TMA gather4 / cp.async) instead of the receive copy
+    dtype: str = "bf16"             # "fp32": parity path (fp32 operands, SIMT fp32 GEMMs, fp32 expert weights)
+
+    @property
+    def es(self) -> int:
+        return 4 if self.dtype == "fp32" else 2
 
 
 def f64(t):
+    if t.dtype == torch.float32:
+        return t.detach().cpu().double().numpy()
     return pi.bf16_to_numpy_f64(t)
 
 
@@ -62,7 +69,7 @@ def run_gpu(case: CaseCfg):
     cfg = ProbeConfig(G=G, E=E, k=k, H=H, F=F, T=T, h=h if case.residual else 0,
                       replica_budget=case.replica_budget, alpha_ps=case.alpha_ps, beta_ps=case.beta_ps,
                       n_sat=case.n_sat, capacity_factor=case.capacity_factor,
-                      bw_bytes_per_us=case.bw_bytes_per_us)
+                      bw_bytes_per_us=case.bw_bytes_per_us, dtype=case.dtype)
     rt = ProbeRuntime(cfg)
     if case.ep_emulation:
         from paper_2602_00509_b200._lib import OPT_EP_EMULATION
@@ -86,10 +93,15 @@ def run_gpu(case: CaseCfg):
     w13 = [None, None]
     w2 = [None, None]
     for p in (0, 1):
-        w13[p], w2[p] = pi.expert_weights(sh, p, device=dev)
+        w13[p], w2[p] = pi.expert_weights(sh, p, device=dev, dtype=cfg.torch_dtype)
     r1, r2 = pi.predictor_residual(sh, 1, zero=not case.residual, device=dev)
     if not case.residual:
         r1 = r2 = None
+    if case.dtype == "fp32":   # routing inputs keep their (exact) generator values, stored as fp32
+        L0.x, L1.x = L0.x.float(), L1.x.float()
+        W = [w.float() for w in W]
+        if r1 is not None:
+            r1, r2 = r1.float(), r2.float()
     odt = torch.float32 if case.out_fp32 else torch.bfloat16
     out = [torch.empty(G, T, H, dtype=odt, device=dev) for _ in (0, 1)]
     ids = [torch.empty(G, T, k, dtype=torch.int32, device=dev) for _ in (0, 1)]
@@ -124,8 +136,8 @@ def run_gpu(case: CaseCfg):
         for q in range(3):
             e = int(res["replicas"][r, q])
             if e >= 0:
-                slots.append(bool(torch.equal(sw13[3 + q].view(torch.int16), w13[1][e].view(torch.int16)) and
-                                  torch.equal(sw2[3 + q].view(torch.int16), w2[1][e].view(torch.int16))))
+                slots.append(bool(torch.equal(sw13[3 + q].view(torch.uint8), w13[1][e].view(torch.uint8)) and
+                                  torch.equal(sw2[3 + q].view(torch.uint8), w2[1][e].view(torch.uint8))))
     res["slots_ok"] = slots
     inputs = dict(L0=L0, L1=L1, W=W, b=b, w13=w13, w2=w2, r1=r1, r2=r2)
     rt.close()
@@ -181,7 +193,7 @@ def run_oracle(case: CaseCfg, inputs, tokens=None):
     nhat = np.stack(nhat)
     pcfg = O.PlannerConfig(G=G, E=E, replica_budget=case.replica_budget, kmax=16, alpha_ps=case.alpha_ps,
                            beta_ps=case.beta_ps, n_sat=case.n_sat, bw_bytes_per_us=case.bw_bytes_per_us,
-                           expert_bytes=6 * sh.H * sh.F)
+                           expert_bytes=3 * sh.H * sh.F * case.es)
     plan = O.plan_greedy(nhat, [case.window_ns] * G, pcfg)
     ref1 = O.layer_reference(xs1, W[1], b[1], k, plan, G, E, W13[1], W2[1], tokens)
     return dict(ref=[ref0, ref1], nhat=nhat, plan=plan, pred_logits=np.stack(plog), tokens=tokens)

@@ -94,3 +94,27 @@ def test_fp16_y_range_is_checked():
     with pytest.raises(ProbeError, match="65504"):
         rt.check()
     rt.close()
+
+
+# fp32 parity path (probe_config.dtype = PROBE_FP32): north_star's fp32 bound, 1e-5·RMS.  fp32
+# expert weights (full fp32 draws, not bf16 values), SIMT fp32 GEMMs, fp32 Y and combine; routing,
+# plan and layout must still be bit-exact.  Cases span several 64×64 SIMT tiles with ragged tails.
+FP32_CASES = {
+    "fp32-C0": CaseCfg(pi.C0, zipf_s=1.5, dtype="fp32"),
+    "fp32-mid-ragged": CaseCfg(pi.C0.with_(name="mid32", E=32, k=4, H=512, F=256, T=200, G=4), zipf_s=1.2,
+                               bias=True, dtype="fp32"),
+    "fp32-G8-E64": CaseCfg(pi.C0.with_(name="g832", E=64, k=8, H=512, F=384, T=160, G=8), zipf_s=1.0,
+                           alpha_ps=5, beta_ps=1, n_sat=16, dtype="fp32"),
+    "fp32-G1": CaseCfg(pi.C0.with_(name="g132", E=16, k=4, H=256, F=320, T=300, G=1), zipf_s=1.0, dtype="fp32"),
+    "fp32-no-residual-budget0": CaseCfg(pi.C0.with_(name="nr32", E=16, k=2, H=256, F=128, T=64, G=2),
+                                        residual=False, replica_budget=0, dtype="fp32"),
+}
+
+
+@pytest.mark.parametrize("name", list(FP32_CASES))
+def test_layer_parity_fp32(name):
+    case = FP32_CASES[name]
+    gpu, inputs = run_gpu(case)
+    orc = run_oracle(case, inputs)
+    rep = compare(case, gpu, orc, tol=1e-5)
+    print(name, rep)

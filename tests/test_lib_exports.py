@@ -50,6 +50,27 @@ def test_workspace_and_validation(lib):
     bad = cfg.to_c()
     bad.expert_bytes = 1
     assert lib.probe_init(C.byref(bad), arr, C.c_void_p(1024), C.byref(C.c_void_p())) == 1
+    bad = cfg.to_c()
+    bad.dtype = 2              # only PROBE_BF16 / PROBE_FP32
+    assert lib.probe_init(C.byref(bad), arr, C.c_void_p(1024), C.byref(C.c_void_p())) == 1
+
+
+def test_fp32_workspace(lib):
+    """dtype = PROBE_FP32 (parity path): receive rows, Y and replica slots are fp32, and
+    𝒲 = 3·H·F·4 is the checked expert size."""
+    from paper_2602_00509_b200 import ProbeConfig, workspace_sizes
+    c16 = ProbeConfig(G=2, E=8, k=2, H=256, F=512, T=64, h=64)
+    c32 = ProbeConfig(G=2, E=8, k=2, H=256, F=512, T=64, h=64, dtype="fp32")
+    s16, s32 = workspace_sizes(c16), workspace_sizes(c32)
+    assert c32.to_c().dtype == 1 and c32.expert_bytes == 12 * 256 * 512
+    for b in (_lib.BUF_RECV, _lib.BUF_Y, _lib.BUF_REP_W13, _lib.BUF_REP_W2):
+        assert s32[b] == 2 * s16[b], b
+    assert s32[_lib.BUF_SCRATCH] > s16[_lib.BUF_SCRATCH]
+    bad = c32.to_c()
+    bad.expert_bytes = 6 * 256 * 512          # the bf16 size is wrong for fp32
+    arr = (C.c_uint64 * 7)()
+    assert lib.probe_init(C.byref(bad), arr, C.c_void_p(1024), C.byref(C.c_void_p())) == 1
+    assert b"sizeof(dtype)" in lib.probe_last_error(None)
 
 
 @pytest.mark.skipif(shutil.which("cuobjdump") is None, reason="cuobjdump missing")
