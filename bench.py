@@ -142,6 +142,11 @@ def run_probe(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.gpus != world:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world} (launch N>1 with torchrun)")
+    # PROBE_BENCH_SHARED_GPU=1: functional check of the N>1 path on a one-GPU box — every rank
+    # on cuda:0 over gloo (NCCL refuses two ranks on one device); never a performance number
+    shared = os.environ.get("PROBE_BENCH_SHARED_GPU") == "1" and world > 1
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     shape = pi.SHAPES[args.config]
@@ -155,7 +160,10 @@ def run_probe(args):
     pg = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         pg = dist.group.WORLD
     pk, pk_kind = peaks()
     alpha_ps, beta_ps, n_sat, bw_Bpus = cost_model(shape, pk)
@@ -173,6 +181,9 @@ def run_probe(args):
     if args.fused_dispatch:
         from paper_2602_00509_b200._lib import OPT_FUSED_DISPATCH
         rt.set_option(OPT_FUSED_DISPATCH, args.fused_dispatch)
+    if args.overlap is not None:
+        from paper_2602_00509_b200._lib import OPT_OVERLAP_DISPATCH
+        rt.set_option(OPT_OVERLAP_DISPATCH, args.overlap)
     ranks = list(range(R0, R0 + GL))
     t0 = time.time()
     pool = [pi.layer_inputs(shape, 0, i, args.zipf, ranks=ranks, device=dev, wrap=POOL) for i in range(POOL)]
@@ -186,7 +197,9 @@ def run_probe(args):
     res = [pi.predictor_residual(shape, p, device=dev) for p in (0, 1)]
     gen_s = time.time() - t0
     T, H = shape.T, shape.H
-    out = torch.empty(GL, T, H, dtype=torch.float32, device=dev)
+    # layer output in the model's activation dtype (bf16, R25's product mode); --out-fp32 keeps the
+    # fp32 parity-mode output (twice the combine writes and the e2e D2H bytes)
+    out = torch.empty(GL, T, H, dtype=torch.float32 if args.out_fp32 else torch.bfloat16, device=dev)
     # hiding window (R26): modeled per-rank expert-GEMM time at the balanced load
     gemm_ns = window_ns(H, shape.F, T, shape.k, pk)
     win = torch.full((G,), gemm_ns, dtype=torch.int64, device=dev)
@@ -226,7 +239,7 @@ def run_probe(args):
         barrier()
         ms = ev0.elapsed_time(ev1) / nsteps
         if pg is not None:
-            t = torch.tensor([ms], device=dev)
+            t = torch.tensor([ms], device="cpu" if shared else dev)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             ms = float(t.item())
         return ms, L
@@ -370,7 +383,7 @@ def run_probe(args):
             barrier()
             ms = ev0.elapsed_time(ev1) / nsteps
             if pg is not None:
-                t = torch.tensor([ms], device=dev)
+                t = torch.tensor([ms], device="cpu" if shared else dev)
                 torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
                 ms = float(t.item())
             return ms, L
@@ -419,7 +432,7 @@ def run_probe(args):
                                "frac": (fl1 + fl2) / (t1 + t2) / 1e12 / peak_tf}}
     # ---- dispatch / combine against the HBM roofline (one GPU: every "peer" store is local HBM)
     byd = (G * T * H * 2 + pairs * H * 2) / world
-    byc = (pairs * H * 2 + G * T * H * 4) / world                                 # fp16 Y in, fp32 out
+    byc = (pairs * H * 2 + G * T * H * out.element_size()) / world                # fp16 Y in, bf16/fp32 out
     bw_report = {"dispatch": {"algorithmic_bytes": byd, "GBps": byd / (phases["dispatch"] / 1e3) / 1e9,
                               "frac_hbm": byd / (phases["dispatch"] / 1e3) / 1e9 / peak_bw},
                  "combine": {"algorithmic_bytes": byc, "GBps": byc / (phases["combine"] / 1e3) / 1e9,
@@ -438,6 +451,7 @@ def run_probe(args):
                                      "migrating layer to layer, encoded predictor accuracy 0.9; random-init experts",
             "config": {"workload": f"{shape.name}: E={shape.E} top-{shape.k} H={H} F={shape.F} "
                                    f"T={T}/rank EP={G} ({GL} logical ranks per GPU)",
+                       "out_dtype": "fp32" if args.out_fp32 else "bf16",
                        "zipf_s": args.zipf, "replica_budget": 3, "kmax": 16, "alpha_ps": alpha_ps,
                        "beta_ps": beta_ps, "n_sat": n_sat, "window_ns": gemm_ns,
                        "l2": "inputs larger than L2 (x 268 MB/layer at C1, weights 1.2 GB/parity); no flush"},
@@ -567,6 +581,9 @@ def main():
     ap.add_argument("--ep", type=int, default=0, help="EP size G (default: the config's, 8)")
     ap.add_argument("--fused-dispatch", type=int, default=0, choices=[0, 1, 2],
                     help="GEMM1 gathers x rows: 1 TMA gather4, 2 cp.async warps (default 0: receive copy)")
+    ap.add_argument("--overlap", type=int, default=None, choices=[0, 1, 2],
+                    help="pull-copy dispatch overlapped with expert GEMM1 (default: the library's)")
+    ap.add_argument("--out-fp32", action="store_true", help="fp32 layer output (parity mode) instead of bf16")
     ap.add_argument("--cap", type=float, default=4.0, help="receive capacity per rank in units of T·k")
     ap.add_argument("--aux-sms", type=int, default=0, help="grid cap of the aux-stream predictor GEMMs (0: #SMs/2)")
     ap.add_argument("--cpu-tokens", type=int, default=256)

@@ -287,7 +287,14 @@ enum { PROBE_OPT_EP_EMULATION = 1, PROBE_OPT_UNFUSED_TOPK = 2, PROBE_OPT_FUSED_E
                                        from x (no receive-buffer copy).  1: TMA gather4 in the
                                        producer warp; 2: 16-byte cp.async by two gather warps (1-CTA
                                        kernel).  Ignored with local_ranks < ep_size.  Default 0: see
-                                       DESIGN.md §6 for the measurements */ };
+                                       DESIGN.md §6 for the measurements */,
+       PROBE_OPT_OVERLAP_DISPATCH = 7 /* when this process hosts every rank and the expert GEMMs run
+                                         on CTA pairs: dispatch writes the receive-row → x-row index,
+                                         then a persistent pull-copy kernel fills the receive buffers
+                                         in GEMM tile order while expert GEMM1 (programmatic dependent
+                                         launch) runs beside it, acquiring per-128-row flags before
+                                         each tile's A loads (a6 overlapped with a7 tile by tile).
+                                         Ignored otherwise (recv_capacity % 128 != 0, fp32 path). */ };
 probe_status probe_set_option(probe_ctx ctx, int32_t option, int64_t value);
 
 /* Number of library kernel launches enqueued so far by this context (bench accounting). */

@@ -75,6 +75,12 @@ struct GemmSched {
   const int32_t* gather_idx;
   const void* gather_src;
   int32_t gather_ld;
+  // Overlapped dispatch (a6 ∥ a7): when non-null, A rows [128b, 128b+128) of the A map may be
+  // read only once a_ready[b] == ready_epoch (written with release by the pull-dispatch copy
+  // kernel running concurrently); the producer acquires it before the tile's first A load.
+  int32_t ready_epoch;
+  int32_t copy_counter;              // pull-dispatch block counter (reset with the schedule)
+  const int32_t* a_ready;
   GemmGroup g[kMaxGroups];
 };
 // stats[0] producer waits on `empty`   stats[1] MMA waits on `full`   stats[2] MMA waits on `tempty`
@@ -118,6 +124,7 @@ __device__ inline void gemm_finalize_sched(GemmSched* s, int BN) {
   s->stats = nullptr;
   s->gather_idx = nullptr;
   s->gather_src = nullptr;
+  s->a_ready = nullptr;
   sched_reset_counters(s);
   int acc = 0;
   for (int i = 0; i < s->num_groups; ++i) {
@@ -683,23 +690,23 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 // both CTAs' epilogues arrive on the leader's `tempty`.  The leader claims tiles and
 // mirrors them into the peer's queue through DSMEM.
 // =============================================================================
-template <int BN, int STAGES, int EW>
+template <int BN, int STAGES, int EW, int NBUF = 1>
 struct Gemm2Smem {
   static constexpr int A_BYTES = 128 * 128;
   static constexpr int B_BYTES = (BN / 2) * 128;
   static constexpr int BAR_OFF = STAGES * (A_BYTES + B_BYTES);
   static constexpr int TS_OFF = BAR_OFF + (2 * STAGES + 4 + 2 * kTileQ) * 8 + 16 + kTileQ * 4;
   static constexpr int EPI_OFF = (TS_OFF + (kMaxGroups + 1) * 4 + 1023) / 1024 * 1024;
-  static constexpr int NB = 1;
+  static constexpr int NB = NBUF;
   static constexpr int BYTES = EPI_OFF + EW * NB * 4096 + 1024;
 };
 
-template <int BN, int STAGES, int EW>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EW, 1)
+template <int BN, int STAGES, int EW, int MAXR = 255, int NBUF = 1>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EW, 1) __maxnreg__(MAXR)
 grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
                          const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmC,
                          const __grid_constant__ CUtensorMap tmA2, GemmSched* __restrict__ sched, int K, int K2) {
-  using L = Gemm2Smem<BN, STAGES, EW>;
+  using L = Gemm2Smem<BN, STAGES, EW, NBUF>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -753,6 +760,8 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
     // lane 0 handles the tile queue and the TMA tile loads, with a gather index every lane
     // gathers 4 of this CTA's 128 A rows)
     const int32_t* gidx = sched->gather_idx;
+    const int32_t* rdy = sched->a_ready;
+    const int rdy_epoch = rdy ? sched->ready_epoch : 0;
     int stage = 0;
     uint32_t phase = 0;
     int qs = 0;
@@ -792,6 +801,17 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
       if (gidx) {
         const int32_t* p = gidx + arow + 4 * lane;
         g0 = p[0]; g1 = p[1]; g2 = p[2]; g3 = p[3];
+      }
+      if (rdy && lane == 0) {
+        // overlapped dispatch: this CTA's valid A rows must have landed (acquire the block
+        // flags of the pull-dispatch copy, then order the async-proxy TMA reads after them)
+        const int need = min(128, G.m - (mb * 256 + static_cast<int>(rank) * 128));
+        if (need > 0) {
+          const int b0 = arow >> 7, b1 = (arow + need - 1) >> 7;
+          for (int b = b0; b <= b1; ++b)
+            while (ptx::ld_acquire_gpu(rdy + b) != rdy_epoch) __nanosleep(64);
+          ptx::fence_proxy_async_global();
+        }
       }
       for (int kb = 0; kb < num_kb; ++kb) {
         const bool second = kb >= kb1;

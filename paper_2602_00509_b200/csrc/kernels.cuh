@@ -561,6 +561,7 @@ struct LayoutIn {
   const int32_t* gather_idx;    // fused dispatch: GEMM1 gathers its A rows through this index (else null)
   const void* gather_src;       // software gather: x rows (bf16, H per row); null = TMA gather4
   int f32;                      // fp32 parity path: act and Y are fp32, GEMM2 stores EPI_F32
+  const int32_t* a_ready;       // overlapped dispatch: GEMM1 acquires these block flags (else null)
 };
 
 __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o) {
@@ -706,6 +707,9 @@ __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o
       sc->stats = nullptr;
       sc->gather_idx = w == 0 ? in.gather_idx : nullptr;
       sc->gather_src = w == 0 ? in.gather_src : nullptr;
+      sc->a_ready = w == 0 ? in.a_ready : nullptr;
+      sc->ready_epoch = sc->ready_epoch + 1;        // this layer's flag value (flags of older layers differ)
+      sc->copy_counter = 0;
       sc->gather_ld = d.H;
       sched_reset_counters(sc);
       sc->nparts = in.nparts > 1 ? in.nparts : 0;
@@ -785,6 +789,92 @@ __global__ void __launch_bounds__(256) k_dispatch(Dims d, int T, const uint8_t* 
         const int c = c0 + u * 32 + lane;
         if (c < nv) dst[c] = v[u];
       }
+    }
+  }
+}
+
+// =============================================================================
+// a6 ∥ a7 overlapped (pull) dispatch, single process: k_dispatch has written only the
+// receive-row → x-row index (gidx); this persistent copy kernel fills the receive buffers
+// in 128-row blocks, in the order the expert GEMM1 claims its tiles, and publishes each
+// block with a release flag (= the schedule's epoch).  It triggers programmatic dependent
+// launch at entry, so GEMM1 starts beside it on the same SMs and its producer acquires
+// the flags of a tile's rows before the TMA loads: the copy (HBM) overlaps the tensor-core
+// work tile by tile instead of preceding it.  Block order: local destination major
+// (GEMM claims groups in order), or round-robin over destinations under EP emulation
+// (each destination's GEMM partition starts at once).  Never waits on anything, so it
+// always completes (no deadlock whatever the residency of the dependent GEMM).
+// =============================================================================
+__global__ void __launch_bounds__(256, 4) k_dispatch_pull(Dims d, const uint8_t* __restrict__ x, int row_bytes,
+                                                       const int32_t* __restrict__ gidx,
+                                                       const int32_t* __restrict__ group_rows, GemmSched* s1,
+                                                       int32_t* __restrict__ ready, uint8_t* __restrict__ recv,
+                                                       int interleave) {
+  ptx::griddep_launch_dependents();
+  __shared__ int nblk[kMaxG + 1], used[kMaxG];
+  __shared__ int unit_s;
+  const int S = d.EL + kMaxRb;
+  const int GL = d.GL;
+  if (threadIdx.x < GL) {
+    const int r = d.R0 + threadIdx.x;
+    int u = 0;
+    for (int j = 0; j < S; ++j) u += group_rows[r * S + j];
+    used[threadIdx.x] = min(u, d.cap);
+    nblk[threadIdx.x] = (min(u, d.cap) + 127) >> 7;
+  }
+  __syncthreads();
+  int maxb = 0, totb = 0;
+  for (int g = 0; g < GL; ++g) {
+    maxb = max(maxb, nblk[g]);
+    totb += nblk[g];
+  }
+  const int nunits = interleave ? maxb * GL : totb;
+  const int epoch = s1->ready_epoch;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nv = row_bytes / 16;
+  const int bpd = d.cap >> 7;                      // flag blocks per destination (cap % 128 == 0)
+  while (true) {
+    if (threadIdx.x == 0) unit_s = atomicAdd(&s1->copy_counter, 1);
+    __syncthreads();
+    const int u = unit_s;
+    __syncthreads();
+    if (u >= nunits) break;
+    int gl, blk;
+    if (interleave) {
+      gl = u % GL;
+      blk = u / GL;
+      if (blk >= nblk[gl]) continue;
+    } else {
+      gl = 0;
+      blk = u;
+      while (blk >= nblk[gl]) blk -= nblk[gl++];
+    }
+    const int r_end = min(blk * 128 + 128, used[gl]);
+    const size_t base = static_cast<size_t>(gl) * d.cap;
+    // warp w: rows blk·128 + w, +8, ...; 8 × 16 B per lane in flight (≤ 64 registers, so a
+    // copy CTA stays co-resident with the register-capped GEMM1 CTA of the same SM)
+    for (int r0 = blk * 128 + warp; r0 < r_end; r0 += 8) {
+      const uint4* s0 = reinterpret_cast<const uint4*>(x + static_cast<size_t>(gidx[base + r0]) * row_bytes);
+      uint4* d0 = reinterpret_cast<uint4*>(recv + (base + r0) * row_bytes);
+      for (int c0 = 0; c0 < nv; c0 += 32 * 8) {
+        uint4 v0[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int c = c0 + q * 32 + lane;
+          if (c < nv) v0[q] = __ldg(s0 + c);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int c = c0 + q * 32 + lane;
+          if (c < nv) d0[c] = v0[q];
+        }
+      }
+    }
+    ptx::fence_proxy_async_global();               // the rows are read by TMA (async proxy)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      ptx::st_release_gpu(ready + static_cast<size_t>(gl) * bpd + blk, epoch);
     }
   }
 }

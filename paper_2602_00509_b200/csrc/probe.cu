@@ -112,7 +112,7 @@ struct Scratch {
   size_t sym, logits, pprior, pres, pact, ids, gw, pos, hist, cbase, route, pred_local;
   size_t quota[2], reps[2], stats[2], pfctr[2];
   size_t split_cum, slot_of, src_off, group_rows, reps_used;
-  size_t s_g1, s_g2, s_gate, s_p1, s_p2, flags, gidx, act, total;
+  size_t s_g1, s_g2, s_gate, s_p1, s_p2, flags, gidx, ready, act, total;
 };
 
 Scratch scratch_layout(const probe_config& c) {
@@ -152,6 +152,7 @@ Scratch scratch_layout(const probe_config& c) {
   s.s_p2 = take(sizeof(GemmSched));
   s.flags = take(256);
   s.gidx = take((GL * cap + 512) * 4);     // fused dispatch: receive row → x row (+ tile overhang)
+  s.ready = take((GL * cap / 128 + 4) * 4); // overlapped dispatch: per-128-row-block landed flags
   s.act = take(GL * cap * F * esz(c));
   s.total = al(o, 1024);
   return s;
@@ -201,6 +202,7 @@ struct probe_ctx_s {
   bool fused_epi_topk = false;  // top-k in the GEMM epilogue instead of k_select (probe_set_option)
   bool pair_gemm = true;        // expert GEMMs on CTA pairs (cta_group::2); option turns it off
   int fused_dispatch = 0;       // single process, GEMM1 gathers x rows: 1 TMA gather4, 2 cp.async warps (opt-in)
+  int overlap_dispatch = 0;     // single process: pull-copy dispatch overlapped with GEMM1 (flags + PDL)
   // distillation workspace (NEXT-1), allocated on the first probe_distill_grad
   uint8_t* dbuf = nullptr;
   size_t dbytes = 0;
@@ -246,22 +248,52 @@ probe_status fail(probe_ctx ctx, probe_status st, const char* fmt, ...) {
 // V_SWIGLU: expert GEMM1 (bf16 act out), V_F32: expert GEMM2 (fp32 Y out, epilogue-heavy).
 enum GemmVariant { V_128_6_4 = 0, V_256_4_4 = 1, V_256_3_8 = 2, V_128_4_8 = 3, V_256_3_4_NB2 = 4, V_256_3_4_NB4 = 5,
                    V_2CTA_256_6_4 = 6 /* CTA pair, cta_group::2, 256-row tiles */,
-                   V_2CTA_256_5_8 = 7 /* CTA pair with 8 epilogue warps */ };
+                   V_2CTA_256_5_8 = 7 /* CTA pair with 8 epilogue warps */,
+                   V_2CTA_256_5_4_NB2 = 8 /* CTA pair, 5 stages, 2 staging slots per epilogue warp */,
+                   V_2CTA_256_4_4_NB4 = 9 /* CTA pair, 4 stages, 4 staging slots per epilogue warp */ };
 
-template <int BN, int ST, int EW>
+template <int BN, int ST, int EW, int NB = 1>
 cudaError_t launch_gemm_2cta(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, const CUtensorMap& c,
                              const CUtensorMap& a2, GemmSched* s, int K, int K2, int grid, cudaStream_t st) {
-  using L = Gemm2Smem<BN, ST, EW>;
+  using L = Gemm2Smem<BN, ST, EW, NB>;
   static_assert(L::BYTES <= 232448, "shared memory budget");
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(grouped_gemm_2cta_kernel<BN, ST, EW>,
+    cudaError_t e = cudaFuncSetAttribute(grouped_gemm_2cta_kernel<BN, ST, EW, 255, NB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  grouped_gemm_2cta_kernel<BN, ST, EW><<<grid & ~1, 128 + 32 * EW, L::BYTES, st>>>(a, b0, b1, c, a2, s, K, K2);
+  grouped_gemm_2cta_kernel<BN, ST, EW, 255, NB><<<grid & ~1, 128 + 32 * EW, L::BYTES, st>>>(a, b0, b1, c, a2, s, K,
+                                                                                            K2);
   return cudaGetLastError();
+}
+
+// Expert GEMM1 of the overlapped dispatch: programmatic dependent launch after the pull-copy
+// kernel (which triggers at entry), register-capped so a copy CTA stays co-resident per SM.
+constexpr int kOverlapMaxReg = 192;
+cudaError_t launch_gemm1_overlap(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1,
+                                 const CUtensorMap& c, GemmSched* s, int K, int grid, cudaStream_t st,
+                                 bool pdl = true) {
+  using L = Gemm2Smem<256, 6, 4>;
+  auto* kern = grouped_gemm_2cta_kernel<256, 6, 4, kOverlapMaxReg>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid & ~1);
+  cfg.blockDim = dim3(128 + 32 * 4);
+  cfg.dynamicSmemBytes = L::BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, a, b0, b1, c, a, s, K, 0);
 }
 
 template <int BN, int ST, int EW, int NB = (EW == 8 ? 2 : 1)>
@@ -293,11 +325,13 @@ cudaError_t launch_gemm_v(int v, const CUtensorMap& a, const CUtensorMap& b0, co
     case V_256_3_4_NB4: return launch_gemm_t<256, 3, 4, 4>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_2CTA_256_6_4: return launch_gemm_2cta<256, 6, 4>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_2CTA_256_5_8: return launch_gemm_2cta<256, 5, 8>(a, b0, b1, c, A2, s, K, K2, grid, st);
+    case V_2CTA_256_5_4_NB2: return launch_gemm_2cta<256, 5, 4, 2>(a, b0, b1, c, A2, s, K, K2, grid, st);
+    case V_2CTA_256_4_4_NB4: return launch_gemm_2cta<256, 4, 4, 4>(a, b0, b1, c, A2, s, K, K2, grid, st);
   }
   return cudaErrorInvalidValue;
 }
 int variant_bn(int v) { return (v == V_128_6_4 || v == V_128_4_8) ? 128 : 256; }
-int variant_tm(int v) { return (v == V_2CTA_256_6_4 || v == V_2CTA_256_5_8) ? 256 : 128; }
+int variant_tm(int v) { return v >= V_2CTA_256_6_4 ? 256 : 128; }
 
 template <int BN>
 cudaError_t launch_gemm(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, GemmSched* s, int K,
@@ -477,6 +511,10 @@ probe_status probe_init(const probe_config* cfg, const uint64_t* peer_ptrs, void
   if (e == cudaSuccess) e = cudaMemset(ctx->scratch + ctx->sl.flags, 0, 256);
   if (e == cudaSuccess)   // gather indices of never-written receive rows stay valid (row 0)
     e = cudaMemset(ctx->scratch + ctx->sl.gidx, 0, (static_cast<size_t>(cfg->local_ranks) * cfg->recv_capacity + 512) * 4);
+  if (e == cudaSuccess)   // overlapped dispatch: flags and the schedule epochs start at 0
+    e = cudaMemset(ctx->scratch + ctx->sl.ready, 0, (static_cast<size_t>(cfg->local_ranks) * cfg->recv_capacity / 128 + 4) * 4);
+  if (e == cudaSuccess) e = cudaMemset(ctx->scratch + ctx->sl.s_g1, 0, sizeof(GemmSched));
+  if (e == cudaSuccess) e = cudaMemset(ctx->scratch + ctx->sl.s_g2, 0, sizeof(GemmSched));
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->pf, cudaStreamNonBlocking);
   for (int p = 0; p < 2 && e == cudaSuccess; ++p) {
@@ -617,6 +655,10 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   li.gather_idx = fused ? ctx->at<int32_t>(s.gidx) : nullptr;
   li.gather_src = sw_gather ? x : nullptr;
   li.f32 = f32;
+  // overlapped dispatch (a6 ∥ a7): single process, CTA-pair GEMM1, 128-aligned capacity
+  const bool overlap = ctx->overlap_dispatch && !fused && !ctx->multi_process() && !f32 && pair &&
+                       d.cap % 128 == 0 && ctx->pair_gemm;
+  li.a_ready = overlap ? ctx->at<int32_t>(s.ready) : nullptr;
   LayoutOut lo;
   lo.split_cum = ctx->at<int32_t>(s.split_cum);
   lo.slot_of = ctx->at<int32_t>(s.slot_of);
@@ -637,24 +679,45 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
                                                 ctx->at<int32_t>(s.pos), ctx->at<int32_t>(s.cbase),
                                                 lo.split_cum, lo.slot_of, lo.src_off, ctx->at<int32_t>(s.route),
                                                 sym_of(ctx), PROBE_BUF_RECV, err,
-                                                fused ? ctx->at<int32_t>(s.gidx) : nullptr);
+                                                (fused || overlap) ? ctx->at<int32_t>(s.gidx) : nullptr);
     CKL();
   }
   MARK(5);
-  CK(xbarrier(ctx, BAR_DISPATCH, st));          // every peer's rows have landed in our receive buffers
-  // a9 phase lock: the expert GEMMs need this layer's replica slots
-  if (use_plan) CK(ev_wait(ctx, st, ctx->ev_slots[p]));
-  MARK(6);
-  CK(ev_record(ctx, ctx->ev_gemm[p], st));
+  if (overlap) {
+    // slots ready before the copy (nothing may sit between the copy and the dependent GEMM1)
+    if (use_plan) CK(ev_wait(ctx, st, ctx->ev_slots[p]));
+    const bool serial = ctx->overlap_dispatch == 2;   // analysis: copy, then the capped GEMM1 (no PDL)
+    if (!serial) MARK(6);
+    CK(ev_record(ctx, ctx->ev_gemm[p], st));
+    k_dispatch_pull<<<ctx->num_sms, 256, 0, st>>>(d, static_cast<const uint8_t*>(x), static_cast<int>(H * 2),
+                                                  ctx->at<int32_t>(s.gidx), lo.group_rows, lo.s1,
+                                                  ctx->at<int32_t>(s.ready),
+                                                  static_cast<uint8_t*>(ctx->local_base[PROBE_BUF_RECV]),
+                                                  li.nparts > 1 ? 1 : 0);
+    CKL();
+    if (serial) MARK(6);
+    CK(launch_gemm1_overlap(ctx->map_recv, *m13, ctx->map_rw13, ctx->map_recv, lo.s1, d.H, ctx->num_sms, st,
+                            !serial));
+    ++ctx->launches;
+  } else {
+    CK(xbarrier(ctx, BAR_DISPATCH, st));          // every peer's rows have landed in our receive buffers
+    // a9 phase lock: the expert GEMMs need this layer's replica slots
+    if (use_plan) CK(ev_wait(ctx, st, ctx->ev_slots[p]));
+    MARK(6);
+    CK(ev_record(ctx, ctx->ev_gemm[p], st));
+  }
   // a7 grouped SwiGLU expert FFN (tcgen05): act = SiLU(X W_gᵀ) ⊙ X W_uᵀ ; Y = act W_dᵀ
   const int vexp = pair ? V_2CTA_256_6_4 : V_256_4_4;
-  if (f32) {
+  if (overlap) {
+    // GEMM1 already enqueued beside the pull copy
+  } else if (f32) {
     CK(launch_sgemm(ctx, lo.s1, ctx->local_base[PROBE_BUF_RECV], w13, ctx->local_base[PROBE_BUF_REP_W13], d.H, st));
+    ++ctx->launches;
   } else {
     CK(launch_gemm_v(vexp, mxg ? *mxg : ctx->map_recv, *m13, ctx->map_rw13, ctx->map_recv, lo.s1, d.H, ctx->num_sms,
                      st));
+    ++ctx->launches;
   }
-  ++ctx->launches;
   MARK(7);
   if (f32) {
     CK(launch_sgemm(ctx, lo.s2, ctx->scratch + s.act, w2, ctx->local_base[PROBE_BUF_REP_W2], d.F, st));
@@ -926,7 +989,7 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
     return fail(nullptr, PROBE_EINVAL, "probe_test_gemm: bad arguments");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (variant < 0) variant = mode == 1 ? V_256_4_4 : (mode == 2 ? V_256_3_8 : V_128_6_4);
-  if (variant > V_2CTA_256_5_8) return fail(nullptr, PROBE_EINVAL, "bad variant");
+  if (variant > V_2CTA_256_4_4_NB4) return fail(nullptr, PROBE_EINVAL, "bad variant");
   const int TM = variant_tm(variant);
   const int BN = variant_bn(variant);
   const int emode = mode == 1 ? EPI_SWIGLU
@@ -1250,6 +1313,10 @@ probe_status probe_set_option(probe_ctx ctx, int32_t option, int64_t value) {
     case PROBE_OPT_FUSED_DISPATCH:
       if (value < 0 || value > 2) return fail(ctx, PROBE_EINVAL, "fused dispatch mode %lld not in {0,1,2}", (long long)value);
       ctx->fused_dispatch = static_cast<int>(value);
+      return PROBE_OK;
+    case PROBE_OPT_OVERLAP_DISPATCH:
+      if (value < 0 || value > 2) return fail(ctx, PROBE_EINVAL, "overlap mode %lld not in {0,1,2}", (long long)value);
+      ctx->overlap_dispatch = static_cast<int>(value);
       return PROBE_OK;
     case PROBE_OPT_AUX_SMS:
       if (value < 1 || value > ctx->num_sms) return fail(ctx, PROBE_EINVAL, "aux SM cap %lld out of range", (long long)value);

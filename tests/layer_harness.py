@@ -36,6 +36,7 @@ class CaseCfg:
     fused_epi_topk: bool = False    # router/predictor top-k in the GEMM epilogue
     pair_gemm: bool = True          # expert GEMMs on CTA pairs (cta_group::2); False → 1-CTA kernel
     fused_dispatch: int = 0         # 1/2: GEMM1 gathers x rows (TMA gather4 / cp.async) instead of the receive copy
+    overlap_dispatch: Optional[bool] = None   # pull-copy dispatch overlapped with GEMM1 (None: library default)
     dtype: str = "bf16"             # "fp32": parity path (fp32 operands, SIMT fp32 GEMMs, fp32 expert weights)
 
     @property
@@ -80,6 +81,9 @@ def run_gpu(case: CaseCfg):
     if case.fused_dispatch:
         from paper_2602_00509_b200._lib import OPT_FUSED_DISPATCH
         rt.set_option(OPT_FUSED_DISPATCH, int(case.fused_dispatch))
+    if case.overlap_dispatch is not None:
+        from paper_2602_00509_b200._lib import OPT_OVERLAP_DISPATCH
+        rt.set_option(OPT_OVERLAP_DISPATCH, int(case.overlap_dispatch))
     if case.fused_epi_topk:
         from paper_2602_00509_b200._lib import OPT_FUSED_EPILOGUE_TOPK
         rt.set_option(OPT_FUSED_EPILOGUE_TOPK, 1)

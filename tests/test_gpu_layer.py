@@ -49,6 +49,15 @@ CASES = {
                                        fused_dispatch=2),
     "fused-dispatch-cp-async-ep-emulation": CaseCfg(pi.C0.with_(name="fdce", E=64, k=8, H=512, F=256, T=256, G=8),
                                                     zipf_s=1.2, fused_dispatch=2, ep_emulation=True),
+    # overlapped dispatch: pull copy in GEMM tile order, GEMM1 beside it (PDL) acquiring per-block flags
+    "overlap-dispatch": CaseCfg(pi.C0.with_(name="ovd", E=16, k=4, H=512, F=384, T=1100, G=4), zipf_s=1.3,
+                                overlap_dispatch=True),
+    "overlap-dispatch-ragged": CaseCfg(pi.C0.with_(name="ovr", E=16, k=4, H=256, F=256, T=701, G=4), zipf_s=1.2,
+                                       overlap_dispatch=True, bias=True),
+    "overlap-dispatch-ep-emulation": CaseCfg(pi.C0.with_(name="ove", E=16, k=4, H=256, F=384, T=600, G=4),
+                                             zipf_s=1.2, overlap_dispatch=True, ep_emulation=True),
+    "overlap-dispatch-off": CaseCfg(pi.C0.with_(name="ovo", E=16, k=4, H=256, F=256, T=700, G=4), zipf_s=1.3,
+                                    overlap_dispatch=False),
 }
 
 
