@@ -726,6 +726,8 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
   const uint32_t rank = ptx::cluster_ctarank();
   const bool leader = rank == 0;
   const int ng = sched->num_groups;
+  GEMM_STAT(long long acc_st[7] = {0, 0, 0, 0, 0, 0, 0});
+  GEMM_STAT(const long long t_kernel0 = clock64());
   for (int i = threadIdx.x; i < ng; i += blockDim.x) ts[i] = sched->g[i].tile_start;
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -820,7 +822,7 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
         const int kc = second ? (kb - kb1) * 64 : koff + kb * 64;
         const bool gat = gidx && !second;
         if (lane == 0) {
-          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          GEMM_TIMED_WAIT(&empty[stage], phase ^ 1, 0);
           if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (L::A_BYTES + L::B_BYTES));
           if (!gat) ptx::tma_load_2d_cg2(ta, &full[stage], sA + stage * L::A_BYTES, kc, arow);
           ptx::tma_load_2d_cg2(tb, &full[stage], sB + stage * L::B_BYTES, kc, brow);
@@ -847,11 +849,11 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
         if (lane == 0) ptx::mbar_arrive(&qempty[qs]);
         if (++qs == kTileQ) { qs = 0; qph ^= 1; }
         if (tile < 0) break;
-        ptx::mbar_wait(&tempty[acc], aphase ^ 1);
+        GEMM_TIMED_WAIT(&tempty[acc], aphase ^ 1, 2);
         ptx::tc_fence_after();
         const uint32_t d = tmem_base + acc * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
-          ptx::mbar_wait(&full[stage], phase);
+          GEMM_TIMED_WAIT(&full[stage], phase, 1);
           ptx::tc_fence_after();
           if (lane == 0) {
             const uint64_t a0 = ptx::sdesc_sw128(ptx::smem_u32(sA + stage * L::A_BYTES));
@@ -897,11 +899,14 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
       const int nt = gemm_ntiles_n(G, BN);
       const int tin = tile - ts[gi];
       const int mb = tin / nt, nb = tin % nt;
-      ptx::mbar_wait(&tfull[acc], aphase);
+      GEMM_TIMED_WAIT(&tfull[acc], aphase, 3);
+      GEMM_STAT(const long long t_epi0 = clock64());
+      GEMM_STAT(acc_st[5] += 1);
       ptx::tc_fence_after();
       const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
       const int row0 = mb * 256 + static_cast<int>(rank) * 128 + q * 32;
       epi_tile<BN, L::NB, NPART>(tb, lane, part, G, row0, nb, tiles, tsel, &tmC);
+      GEMM_STAT(acc_st[4] += clock64() - t_epi0);
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -913,6 +918,13 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
     }
     if (lane == 0) ptx::bulk_wait<0>();
   }
+#ifdef PROBE_GEMM_STATS
+  if (sched->stats && lane == 0 && rank == 0 && (warp <= 1 || warp == 4)) {
+    acc_st[6] = clock64() - t_kernel0;
+    for (int i = 0; i < 7; ++i)
+      if (acc_st[i]) atomicAdd(&sched->stats[i], static_cast<unsigned long long>(acc_st[i]));
+  }
+#endif
   __syncthreads();
   ptx::tc_fence_before();
   ptx::cluster_sync();          // no remote arrive / DSMEM access after this point

@@ -31,13 +31,16 @@ def run(A, B, groups, N, mode, out, v):
 
 A2 = (torch.randn(M, F, device="cuda") * 0.5).to(torch.bfloat16)
 B2 = (torch.randn(E_loc * H, F, device="cuda") / F ** 0.5).to(torch.bfloat16)
+V = int(sys.argv[1]) if len(sys.argv) > 1 else 6     # 6: CTA-pair <256,6,4> (product default)
 Y = torch.empty(M, H, device="cuda")
 g2 = [[e * rows_per, rows_per, e * H, e * rows_per] for e in range(E_loc)]
-for mode in (2, 4):
-    print("GEMM2 mode", mode, "ms", run(A2, B2, g2, H, mode, Y, 1), flush=True)
+for mode in (7, 4):      # fp16 Y (product), no stores
+    ms = run(A2, B2, g2, H, mode, Y, V)
+    print("GEMM2 mode", mode, "ms", ms, "TF/s", round(2.0 * M * H * F / ms / 1e9, 1), flush=True)
 del A2, B2, Y
 A1 = (torch.randn(M, H, device="cuda") * 0.5).to(torch.bfloat16)
 B1 = (torch.randn(E_loc * 2 * F, H, device="cuda") / H ** 0.5).to(torch.bfloat16)
 act = torch.empty(M, F, dtype=torch.bfloat16, device="cuda")
 g1 = [[e * rows_per, rows_per, e * 2 * F, e * rows_per] for e in range(E_loc)]
-print("GEMM1 ms", run(A1, B1, g1, 2 * F, 1, act, 1), flush=True)
+ms = run(A1, B1, g1, 2 * F, 1, act, V)
+print("GEMM1 ms", ms, "TF/s", round(4.0 * M * H * F / ms / 1e9, 1), flush=True)
