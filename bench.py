@@ -201,7 +201,7 @@ def run_probe(args):
     # fp32 parity-mode output (twice the combine writes and the e2e D2H bytes)
     out = torch.empty(GL, T, H, dtype=torch.float32 if args.out_fp32 else torch.bfloat16, device=dev)
     # hiding window (R26): modeled per-rank expert-GEMM time at the balanced load
-    gemm_ns = window_ns(H, shape.F, T, shape.k, pk)
+    gemm_ns = window_ns(H, shape.F, T, shape.k, pk, E=shape.E, G=G)
     win = torch.full((G,), gemm_ns, dtype=torch.int64, device=dev)
     main = torch.cuda.current_stream(dev)
 
@@ -253,9 +253,15 @@ def run_probe(args):
     rt.check()
     # ---- timed region (PROBE)
     launches0 = rt.launches()
+    pf0 = rt.prefetch_kib()
     with ClockSampler(local) as clk:
         ms, L = timed(args.steps, L)
     launches = rt.launches() - launches0
+    pf1 = rt.prefetch_kib()
+    prefetch = {"part1_MB_per_layer": (pf1[0] - pf0[0]) / 1024 / args.steps,
+                "part2_MB_per_layer": (pf1[1] - pf0[1]) / 1024 / args.steps,
+                "note": "replica weights pushed by this process: part 1 beside the expert GEMMs, part 2 after "
+                        "the combine (split phase, P:469)"}
     clocks = clk.summary()
     # ---- per-phase profile (separate pass; CUDA events on the launching stream)
     rt.profile(args.steps)
@@ -389,7 +395,7 @@ def run_probe(args):
             return ms, L
 
         _, L = timed_e2e(2, L)             # warm the copy streams
-        ms_e2e, L = timed_e2e(max(3, min(args.steps, 10)), L)
+        ms_e2e, L = timed_e2e(max(3, args.steps), L)      # steady state: fill and drain amortised
         bi = x_dev[0].numel() * x_dev[0].element_size()
         bo = out.numel() * out.element_size()
         e2e = {"value": ms_e2e if shape.name != "C2" else G * T / (ms_e2e / 1e3), "unit": "ms" if shape.name != "C2" else "tokens/s",
@@ -469,6 +475,7 @@ def run_probe(args):
                                     "maxL_after_ps": stats[3]},
                         "predicted_load_fidelity": load_fidelity},
             "bandwidth": bw_report,
+            "prefetch": prefetch,
             "setup_s": gen_s,
         }
         print(json.dumps(result), flush=True)

@@ -170,6 +170,12 @@ probe_status probe_prefetch(probe_ctx ctx, int32_t next_layer, const void* w13_n
 probe_status probe_debug_layout(probe_ctx ctx, int32_t* counts, int32_t* split, int32_t* route,
                                 int32_t* group_rows, int32_t* replicas_used, void* stream);
 
+/* Split-phase prefetch accounting (R27): out[0] / out[1] (device int32) = KiB of replica
+ * weights this process has pushed so far in part 1 (during the expert GEMMs, before the
+ * combine's suspend flag) / in part 2 (after the combine).  Cumulative since probe_init;
+ * enqueued on `stream` after the context's prefetch stream work issued so far. */
+probe_status probe_debug_prefetch(probe_ctx ctx, int32_t* out, void* stream);
+
 /* Test hook: one grouped bf16 GEMM through the tcgen05 kernel,
  * C[g] (fp32, [m_g, N]) = A[a_row_g : a_row_g + m_g, :K] · B[b_row_g : b_row_g + N, :K]^T
  * (mode 0) or act = SiLU(gate)⊙up (bf16, [m_g, N/2]) with gate rows b_row_g.., up rows

@@ -30,7 +30,16 @@ def cost_model(H: int, F: int, pk=None):
     return alpha_ps, beta_ps, n_sat, int(BW_NET / 1e6)
 
 
-def window_ns(H: int, F: int, T: int, k: int, pk=None) -> int:
-    """Hiding window (R26): modeled expert-GEMM time of a balanced rank, in ns."""
+def window_ns(H: int, F: int, T: int, k: int, pk=None, E: int = 0, G: int = 0) -> int:
+    """Hiding window (R26): modeled expert-GEMM time of a balanced rank, in ns.
+
+    With E and G given, the model is the planner's own cost (R11) of the balanced rank:
+    α·Σ_e c(m_e) over its E/G experts, m = T·k·G/E rows each, c(m) = max(m, n_sat) — so a
+    decode-sized GEMM (m < n_sat, weight-bandwidth bound) gets its weight-streaming time,
+    not its FLOP time (C2: 123 µs instead of 37 µs).  Without them: FLOP time T·k·6HF/F_peak."""
     pk = pk or peaks()[0]
-    return int(6.0 * H * F * T * k / (pk["bf16_tflops_sustained"] * 1e12) * 1e9)
+    pairs = T * k
+    if E and G:
+        _, _, n_sat, _ = cost_model(H, F, pk)
+        pairs = (E // G) * max(T * k * G / E, n_sat)
+    return int(6.0 * H * F * pairs / (pk["bf16_tflops_sustained"] * 1e12) * 1e9)

@@ -408,8 +408,8 @@ __device__ __forceinline__ void epi_tile(uint32_t tb, int lane, int part, const 
 #define GEMM_STAT(...)
 #endif
 
-template <int BN, int STAGES, int EW = 4, int NBUF = (EW == 8 ? 2 : 1)>
-__global__ void __launch_bounds__(128 + 32 * EW, 1)
+template <int BN, int STAGES, int EW = 4, int NBUF = (EW == 8 ? 2 : 1), int MAXR = 255>
+__global__ void __launch_bounds__(128 + 32 * EW, 1) __maxnreg__(MAXR)
 grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
                     const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmC,
                     const __grid_constant__ CUtensorMap tmA2, GemmSched* __restrict__ sched, int K, int K2) {

@@ -334,7 +334,10 @@ __global__ void k_copy_i32(const int32_t* __restrict__ src, int32_t* __restrict_
 // =============================================================================
 // a4: Greedy Balance-Optimal Planning (Algorithm 1) on ONE CTA,
 // integer costs (R11), readings R13-R22.  Every rank runs it on the same n̂ (R10).
-// State in shared memory; incremental cost updates (only r_src and r_dst change).
+// Incremental cost updates (only r_src and r_dst change).  The split [G][E][G] lives in the
+// quota output itself (global memory, L1/L2-resident): with ≤ 6 KB of shared memory and 64
+// threads the planner CTA fits beside a persistent expert-GEMM CTA (≈ 214 KB smem), so the
+// plan for L+1 completes during layer L's GEMM instead of waiting for a free SM.
 // =============================================================================
 struct PlanParams {
   int64_t alpha, beta, bw, wbytes;
@@ -343,11 +346,11 @@ struct PlanParams {
 
 __device__ __forceinline__ int64_t cost_c(int64_t m, int n_sat) { return m == 0 ? 0 : (m > n_sat ? m : n_sat); }
 
-__global__ void __launch_bounds__(256) k_plan(Dims d, PlanParams pp, const int32_t* __restrict__ nhat,
-                                              const int64_t* __restrict__ window_ns, int32_t* __restrict__ quota,
-                                              int32_t* __restrict__ replicas, int64_t* __restrict__ stats,
-                                              int32_t* __restrict__ prefetch_ctr) {
-  extern __shared__ int32_t sp[];                 // split [G][E][G]
+__global__ void __launch_bounds__(64) k_plan(Dims d, PlanParams pp, const int32_t* __restrict__ nhat,
+                                             const int64_t* __restrict__ window_ns, int32_t* quota,
+                                             int32_t* __restrict__ replicas, int64_t* __restrict__ stats,
+                                             int32_t* __restrict__ prefetch_ctr) {
+  int32_t* sp = quota;                            // split [G][E][G], updated in place
   __shared__ int64_t comp[kMaxG], L[kMaxG], Lb[kMaxG];
   __shared__ int64_t inn[kMaxG], outv[kMaxG], load[kMaxG];
   __shared__ int32_t cap[kMaxG], nin[kMaxG], nout[kMaxG], rep[kMaxG * kMaxRb];
@@ -505,8 +508,7 @@ __global__ void __launch_bounds__(256) k_plan(Dims d, PlanParams pp, const int32
     }
   }
   __syncthreads();
-  // outputs: quota = split; replicas sorted (slot order); stats
-  for (int i = tid; i < G * E * G; i += blockDim.x) quota[i] = sp[i];
+  // outputs: quota = split (already in place); replicas sorted (slot order); stats
   if (tid < G) {
     int rr[kMaxRb];
     for (int i = 0; i < kMaxRb; ++i) rr[i] = rep[tid * kMaxRb + i];

@@ -250,22 +250,26 @@ enum GemmVariant { V_128_6_4 = 0, V_256_4_4 = 1, V_256_3_8 = 2, V_128_4_8 = 3, V
                    V_2CTA_256_6_4 = 6 /* CTA pair, cta_group::2, 256-row tiles */,
                    V_2CTA_256_5_8 = 7 /* CTA pair with 8 epilogue warps */,
                    V_2CTA_256_5_4_NB2 = 8 /* CTA pair, 5 stages, 2 staging slots per epilogue warp */,
-                   V_2CTA_256_4_4_NB4 = 9 /* CTA pair, 4 stages, 4 staging slots per epilogue warp */ };
+                   V_2CTA_256_4_4_NB4 = 9 /* CTA pair, 4 stages, 4 staging slots per epilogue warp */,
+                   V_256_4_4_EXP = 10 /* 1-CTA <256,4,4> register-capped for the expert GEMMs */ };
 
-template <int BN, int ST, int EW, int NB = 1>
+// Expert GEMMs leave registers for one 128-thread prefetch CTA per SM (a9 part 1 runs beside them)
+constexpr int kExpertMaxReg = 216;
+
+template <int BN, int ST, int EW, int NB = 1, int MAXR = 255>
 cudaError_t launch_gemm_2cta(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, const CUtensorMap& c,
                              const CUtensorMap& a2, GemmSched* s, int K, int K2, int grid, cudaStream_t st) {
   using L = Gemm2Smem<BN, ST, EW, NB>;
   static_assert(L::BYTES <= 232448, "shared memory budget");
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(grouped_gemm_2cta_kernel<BN, ST, EW, 255, NB>,
+    cudaError_t e = cudaFuncSetAttribute(grouped_gemm_2cta_kernel<BN, ST, EW, MAXR, NB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  grouped_gemm_2cta_kernel<BN, ST, EW, 255, NB><<<grid & ~1, 128 + 32 * EW, L::BYTES, st>>>(a, b0, b1, c, a2, s, K,
-                                                                                            K2);
+  grouped_gemm_2cta_kernel<BN, ST, EW, MAXR, NB><<<grid & ~1, 128 + 32 * EW, L::BYTES, st>>>(a, b0, b1, c, a2, s, K,
+                                                                                             K2);
   return cudaGetLastError();
 }
 
@@ -296,19 +300,19 @@ cudaError_t launch_gemm1_overlap(const CUtensorMap& a, const CUtensorMap& b0, co
   return cudaLaunchKernelEx(&cfg, kern, a, b0, b1, c, a, s, K, 0);
 }
 
-template <int BN, int ST, int EW, int NB = (EW == 8 ? 2 : 1)>
+template <int BN, int ST, int EW, int NB = (EW == 8 ? 2 : 1), int MAXR = 255>
 cudaError_t launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, const CUtensorMap& c,
                           const CUtensorMap& a2, GemmSched* s, int K, int K2, int grid, cudaStream_t st) {
   using L = GemmSmem<BN, ST, EW, NB>;
   static_assert(L::BYTES <= 232448, "shared memory budget");
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(grouped_gemm_kernel<BN, ST, EW, NB>,
+    cudaError_t e = cudaFuncSetAttribute(grouped_gemm_kernel<BN, ST, EW, NB, MAXR>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  grouped_gemm_kernel<BN, ST, EW, NB><<<grid, 128 + 32 * EW, L::BYTES, st>>>(a, b0, b1, c, a2, s, K, K2);
+  grouped_gemm_kernel<BN, ST, EW, NB, MAXR><<<grid, 128 + 32 * EW, L::BYTES, st>>>(a, b0, b1, c, a2, s, K, K2);
   return cudaGetLastError();
 }
 
@@ -323,7 +327,8 @@ cudaError_t launch_gemm_v(int v, const CUtensorMap& a, const CUtensorMap& b0, co
     case V_128_4_8: return launch_gemm_t<128, 4, 8>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_256_3_4_NB2: return launch_gemm_t<256, 3, 4, 2>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_256_3_4_NB4: return launch_gemm_t<256, 3, 4, 4>(a, b0, b1, c, A2, s, K, K2, grid, st);
-    case V_2CTA_256_6_4: return launch_gemm_2cta<256, 6, 4>(a, b0, b1, c, A2, s, K, K2, grid, st);
+    case V_2CTA_256_6_4: return launch_gemm_2cta<256, 6, 4, 1, kExpertMaxReg>(a, b0, b1, c, A2, s, K, K2, grid, st);
+    case V_256_4_4_EXP: return launch_gemm_t<256, 4, 4, 1, kExpertMaxReg>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_2CTA_256_5_8: return launch_gemm_2cta<256, 5, 8>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_2CTA_256_5_4_NB2: return launch_gemm_2cta<256, 5, 4, 2>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_2CTA_256_4_4_NB4: return launch_gemm_2cta<256, 4, 4, 4>(a, b0, b1, c, A2, s, K, K2, grid, st);
@@ -331,7 +336,7 @@ cudaError_t launch_gemm_v(int v, const CUtensorMap& a, const CUtensorMap& b0, co
   return cudaErrorInvalidValue;
 }
 int variant_bn(int v) { return (v == V_128_6_4 || v == V_128_4_8) ? 128 : 256; }
-int variant_tm(int v) { return v >= V_2CTA_256_6_4 ? 256 : 128; }
+int variant_tm(int v) { return (v >= V_2CTA_256_6_4 && v <= V_2CTA_256_4_4_NB4) ? 256 : 128; }
 
 template <int BN>
 cudaError_t launch_gemm(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, GemmSched* s, int K,
@@ -515,8 +520,16 @@ probe_status probe_init(const probe_config* cfg, const uint64_t* peer_ptrs, void
     e = cudaMemset(ctx->scratch + ctx->sl.ready, 0, (static_cast<size_t>(cfg->local_ranks) * cfg->recv_capacity / 128 + 4) * 4);
   if (e == cudaSuccess) e = cudaMemset(ctx->scratch + ctx->sl.s_g1, 0, sizeof(GemmSched));
   if (e == cudaSuccess) e = cudaMemset(ctx->scratch + ctx->sl.s_g2, 0, sizeof(GemmSched));
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->pf, cudaStreamNonBlocking);
+  // The aux track (predictor, planner) and the prefetch run on the highest-priority streams:
+  // the block scheduler then hands them SMs as soon as main-track CTAs retire, so the plan
+  // for L+1 is ready during dispatch(L) and prefetch part 1 can run beside the expert GEMMs
+  // (with default priority the 8192 dispatch CTAs and then the persistent GEMM CTAs went
+  // first, the planner — 32 KB of shared memory, no room beside a GEMM CTA — ran after
+  // GEMM2, and part 1 found the combine's suspend flag already raised).
+  int prio_lo = 0, prio_hi = 0;
+  if (e == cudaSuccess) e = cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&ctx->aux, cudaStreamNonBlocking, prio_hi);
+  if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&ctx->pf, cudaStreamNonBlocking, prio_hi);
   for (int p = 0; p < 2 && e == cudaSuccess; ++p) {
     cudaEvent_t* evs[6] = {&ctx->ev_gate[p], &ctx->ev_gemm[p], &ctx->ev_comb[p], &ctx->ev_pred[p], &ctx->ev_plan[p],
                            &ctx->ev_slots[p]};
@@ -528,10 +541,8 @@ probe_status probe_init(const probe_config* cfg, const uint64_t* peer_ptrs, void
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, dev);
   ctx->aux_sms = ctx->num_sms / 2;
   if (e == cudaSuccess) {
-    const size_t plan_smem = static_cast<size_t>(G) * c.num_experts * G * 4;
-    e = cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(plan_smem));
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_layout, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(plan_smem));
+    const size_t split_smem = static_cast<size_t>(G) * c.num_experts * G * 4;   // k_layout's split [G][E][G]
+    e = cudaFuncSetAttribute(k_layout, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(split_smem));
   }
   if (e != cudaSuccess) {
     delete ctx;
@@ -707,7 +718,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
     CK(ev_record(ctx, ctx->ev_gemm[p], st));
   }
   // a7 grouped SwiGLU expert FFN (tcgen05): act = SiLU(X W_gᵀ) ⊙ X W_uᵀ ; Y = act W_dᵀ
-  const int vexp = pair ? V_2CTA_256_6_4 : V_256_4_4;
+  const int vexp = pair ? V_2CTA_256_6_4 : V_256_4_4_EXP;
   if (overlap) {
     // GEMM1 already enqueued beside the pull copy
   } else if (f32) {
@@ -904,9 +915,9 @@ probe_status probe_plan(probe_ctx ctx, int32_t next_layer, const int32_t* pred_c
                                   : reinterpret_cast<const int32_t*>(ctx->local_base[PROBE_BUF_BOARD]) + ((pp * 2 + 1) * d.G) * d.E;
   PlanParams pr{ctx->cfg.alpha_ps, ctx->cfg.beta_ps, ctx->cfg.bw_bytes_per_us, ctx->cfg.expert_bytes,
                 ctx->cfg.n_sat, ctx->cfg.kmax, ctx->cfg.replica_budget};
-  const size_t smem = static_cast<size_t>(d.G) * d.E * d.G * 4;
-  k_plan<<<1, 256, smem, st>>>(d, pr, nh, window_ns, ctx->at<int32_t>(s.quota[pp]), ctx->at<int32_t>(s.reps[pp]),
-                                ctx->at<int64_t>(s.stats[pp]), ctx->at<int32_t>(s.pfctr[pp]));
+  const size_t smem = static_cast<size_t>(d.G) * d.E * d.G * 4;    // quota bytes
+  k_plan<<<1, 64, 0, st>>>(d, pr, nh, window_ns, ctx->at<int32_t>(s.quota[pp]), ctx->at<int32_t>(s.reps[pp]),
+                            ctx->at<int64_t>(s.stats[pp]), ctx->at<int32_t>(s.pfctr[pp]));
   CKL();
   if (replicas) CK(cudaMemcpyAsync(replicas, ctx->at<int32_t>(s.reps[pp]), d.G * kMaxRb * 4, cudaMemcpyDeviceToDevice, st));
   if (quota) CK(cudaMemcpyAsync(quota, ctx->at<int32_t>(s.quota[pp]), smem, cudaMemcpyDeviceToDevice, st));
@@ -934,10 +945,12 @@ probe_status probe_prefetch(probe_ctx ctx, int32_t next_layer, const void* w13_n
   CK(ev_wait(ctx, st, ctx->ev_plan[pp]));
   int32_t* flags = ctx->at<int32_t>(s.flags);
   const bool inflight = ctx->fwd_layer == next_layer - 1;
-  const int grid = 16;  // "controlled SM occupancy": 16 CTAs co-resident with the GEMM
+  const int grid = 16;  // part 2 (after the combine): "controlled SM occupancy"
   if (inflight) {
+    // part 1 beside the expert GEMMs: one 128-thread CTA per SM fits in the registers the
+    // register-capped expert GEMM CTAs leave free (216 × 256 + 64 × 128 < 64 K)
     CK(ev_wait(ctx, st, ctx->ev_gemm[prev]));
-    k_prefetch<<<grid, 512, 0, st>>>(d, ctx->at<int32_t>(s.reps[pp]), pp, static_cast<const uint8_t*>(w13_next),
+    k_prefetch<<<ctx->num_sms, 128, 0, st>>>(d, ctx->at<int32_t>(s.reps[pp]), pp, static_cast<const uint8_t*>(w13_next),
                                      static_cast<const uint8_t*>(w2_next), sym_of(ctx), PROBE_BUF_REP_W13,
                                      PROBE_BUF_REP_W2, ctx->at<int32_t>(s.pfctr[pp]), flags + 1, next_layer,
                                      flags + 2, static_cast<int>(esz(ctx->cfg)));
@@ -952,6 +965,18 @@ probe_status probe_prefetch(probe_ctx ctx, int32_t next_layer, const void* w13_n
   CK(xbarrier(ctx, BAR_PREFETCH, st));          // every sender finished pushing into our slots
   CK(ev_record(ctx, ctx->ev_slots[pp], st));
   ctx->pf_layer[pp] = next_layer;
+  return PROBE_OK;
+}
+
+probe_status probe_debug_prefetch(probe_ctx ctx, int32_t* out, void* stream) {
+  if (!ctx || !out) return fail(ctx, PROBE_EINVAL, "probe_debug_prefetch: null argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaEvent_t ev;
+  CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CK(cudaEventRecord(ev, ctx->pf));
+  CK(cudaStreamWaitEvent(st, ev, 0));
+  CK(cudaEventDestroy(ev));
+  CK(cudaMemcpyAsync(out, ctx->at<int32_t>(ctx->sl.flags) + 2, 8, cudaMemcpyDeviceToDevice, st));
   return PROBE_OK;
 }
 
@@ -989,7 +1014,7 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
     return fail(nullptr, PROBE_EINVAL, "probe_test_gemm: bad arguments");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (variant < 0) variant = mode == 1 ? V_256_4_4 : (mode == 2 ? V_256_3_8 : V_128_6_4);
-  if (variant > V_2CTA_256_4_4_NB4) return fail(nullptr, PROBE_EINVAL, "bad variant");
+  if (variant > V_256_4_4_EXP) return fail(nullptr, PROBE_EINVAL, "bad variant");
   const int TM = variant_tm(variant);
   const int BN = variant_bn(variant);
   const int emode = mode == 1 ? EPI_SWIGLU

@@ -164,6 +164,13 @@ class ProbeRuntime:
                                          _ptr(replicas), _stream(stream))
         check("probe_debug_layout", st, self.ctx)
 
+    def prefetch_kib(self, stream=None):
+        """(part 1, part 2) KiB of replica weights pushed so far (split-phase accounting)."""
+        out = torch.zeros(2, dtype=torch.int32, device=self.device)
+        check("probe_debug_prefetch", self.lib.probe_debug_prefetch(self.ctx, _ptr(out), _stream(stream)), self.ctx)
+        v = out.cpu()
+        return int(v[0]), int(v[1])
+
     def check(self):
         check("probe_check", self.lib.probe_check(self.ctx), self.ctx)
 

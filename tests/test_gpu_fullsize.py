@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 def bench_case(shape, zipf_s=1.0, sample=24, cap=4.0):
     a, b, n, bw = cost_model(shape.H, shape.F)
     return CaseCfg(shape, zipf_s=zipf_s, alpha_ps=a, beta_ps=b, n_sat=n, bw_bytes_per_us=bw,
-                   window_ns=window_ns(shape.H, shape.F, shape.T, shape.k), capacity_factor=cap,
+                   window_ns=window_ns(shape.H, shape.F, shape.T, shape.k, E=shape.E, G=shape.G), capacity_factor=cap,
                    sample_tokens=sample)
 
 

@@ -47,7 +47,7 @@ def main():
     W = [pi.router_weight(sh, p, device=dev) for p in (0, 1)]
     ex = [pi.expert_weights(sh, p, device=dev) for p in (0, 1)]
     res = [pi.predictor_residual(sh, p, device=dev) for p in (0, 1)]
-    win = torch.full((G,), window_ns(H, F_, T, sh.k), dtype=torch.int64, device=dev)
+    win = torch.full((G,), window_ns(H, F_, T, sh.k, E=sh.E, G=G), dtype=torch.int64, device=dev)
     out = torch.empty(G, T, H, device=dev)
     # attention stand-in weights (Qwen3-30B-A3B attention shapes)
     nq, nkv, hd = 32, 4, 128

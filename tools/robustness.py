@@ -43,7 +43,7 @@ pools = {ph: [pi.layer_inputs(shape, 0, i, args.zipf, device=dev, wrap=POOL, per
 W = [pi.router_weight(shape, p, device=dev) for p in (0, 1)]
 ex = [pi.expert_weights(shape, p, device=dev) for p in (0, 1)]
 res = [pi.predictor_residual(shape, p, device=dev) for p in (0, 1)]
-win = torch.full((G,), window_ns(H, F, T, k), dtype=torch.int64, device=dev)
+win = torch.full((G,), window_ns(H, F, T, k, E=E, G=G), dtype=torch.int64, device=dev)
 out = torch.empty(G, T, H, device=dev)
 hist = [torch.zeros(G, E, dtype=torch.int32, device=dev) for _ in (0, 1)]
 
