@@ -170,7 +170,7 @@ def design_rank(shape: MoEShape, step: int, layer: int, rank: int, zipf_s: float
         for t in np.nonzero(in_set)[0]:
             j = int(r.integers(0, k - 1))
             numer[t, j + 1] = numer[t, j]
-        for t in np.nonzero(boundary)[0]:
+        for t in np.nonzero(boundary)[0] if k < E else ():   # k = E: no expert outside the set
             cand = np.setdiff1d(np.arange(E), S[t])
             tie_e[t] = int(cand[r.integers(0, len(cand))])
     # prediction: each slot of S_next kept with prob `accuracy`, else a uniform
@@ -180,6 +180,9 @@ def design_rank(shape: MoEShape, step: int, layer: int, rank: int, zipf_s: float
     for j in range(k):
         rep = r.random(T) >= accuracy
         idx = np.nonzero(rep)[0]
+        # degenerate 2k >= E: a token whose S_next ∪ P already covers every expert keeps its slot
+        full = np.array([len(np.union1d(S_next[t], P[t])) >= E for t in idx], dtype=bool)
+        idx = idx[~full]
         while len(idx):
             cand = r.integers(0, E, size=len(idx))
             bad = (cand[:, None] == S_next[idx]).any(axis=1) | (cand[:, None] == P[idx]).any(axis=1)

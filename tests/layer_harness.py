@@ -38,6 +38,7 @@ class CaseCfg:
     fused_dispatch: int = 0         # 1/2: GEMM1 gathers x rows (TMA gather4 / cp.async) instead of the receive copy
     overlap_dispatch: Optional[bool] = None   # pull-copy dispatch overlapped with GEMM1 (None: library default)
     dtype: str = "bf16"             # "fp32": parity path (fp32 operands, SIMT fp32 GEMMs, fp32 expert weights)
+    max_tokens: int = 0             # >T: context capacity above the T this layer call runs with
 
     @property
     def es(self) -> int:
@@ -67,7 +68,7 @@ def run_gpu(case: CaseCfg):
     from paper_2602_00509_b200 import ProbeConfig, ProbeRuntime
     sh = case.shape
     G, E, k, H, F, T, h = sh.G, sh.E, sh.k, sh.H, sh.F, sh.T, sh.h
-    cfg = ProbeConfig(G=G, E=E, k=k, H=H, F=F, T=T, h=h if case.residual else 0,
+    cfg = ProbeConfig(G=G, E=E, k=k, H=H, F=F, T=max(T, case.max_tokens), h=h if case.residual else 0,
                       replica_budget=case.replica_budget, alpha_ps=case.alpha_ps, beta_ps=case.beta_ps,
                       n_sat=case.n_sat, capacity_factor=case.capacity_factor,
                       bw_bytes_per_us=case.bw_bytes_per_us, dtype=case.dtype)
@@ -118,14 +119,14 @@ def run_gpu(case: CaseCfg):
     win = torch.full((G,), case.window_ns, dtype=torch.int64, device=dev)
     res = {}
     rt.forward(0, L0.x, W[0], b[0], w13[0], w2[0], out[0], use_plan=False, topk_ids=ids[0], topk_w=gw[0])
-    lay0 = debug(rt, cfg)
+    lay0 = debug(rt, cfg, T)
     pc_unfused = torch.empty(G, E, dtype=torch.int32, device=dev)
     rt.predict(1, L0.x, W[1], b[1], r1, r2, pred_counts=pc_unfused, pred_logits=plog)   # unfused (logits out)
     rt.predict(1, L0.x, W[1], b[1], r1, r2, pred_counts=pc)                              # fused top-k epilogue
     rt.plan(1, win, replicas=reps, quota=quota, stats=stats)
     rt.prefetch(1, w13[1], w2[1], phase=0)
     rt.forward(1, L1.x, W[1], b[1], w13[1], w2[1], out[1], use_plan=True, topk_ids=ids[1], topk_w=gw[1])
-    lay1 = debug(rt, cfg)
+    lay1 = debug(rt, cfg, T)
     rt.check()
     torch.cuda.synchronize()
     res.update(out=[o.float().cpu().numpy() for o in out], ids=[i.cpu().numpy() for i in ids],
@@ -148,8 +149,9 @@ def run_gpu(case: CaseCfg):
     return res, inputs
 
 
-def debug(rt, cfg):
-    G, E, k, T = cfg.G, cfg.E, cfg.k, cfg.T
+def debug(rt, cfg, T=None):
+    G, E, k = cfg.G, cfg.E, cfg.k
+    T = cfg.T if T is None else T
     S = E // G + 3
     counts = torch.empty(G, E, dtype=torch.int32, device="cuda")
     split = torch.empty(G, E, G, dtype=torch.int32, device="cuda")

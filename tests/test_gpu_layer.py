@@ -58,6 +58,13 @@ CASES = {
                                              zipf_s=1.2, overlap_dispatch=True, ep_emulation=True),
     "overlap-dispatch-off": CaseCfg(pi.C0.with_(name="ovo", E=16, k=4, H=256, F=256, T=700, G=4), zipf_s=1.3,
                                     overlap_dispatch=False),
+    # degenerate top-k: k = 1, k = E (every expert chosen by every token), k = 9 > 8 (unfused select kernel; the exact-bf16 encoding caps k near 9)
+    "k1": CaseCfg(pi.C0.with_(name="k1", E=8, k=1, H=256, F=256, T=130, G=2), zipf_s=1.5),
+    "k-eq-E": CaseCfg(pi.C0.with_(name="kE", E=8, k=8, H=256, F=128, T=70, G=2), zipf_s=1.0),
+    "k9-unfused-select": CaseCfg(pi.C0.with_(name="k9b", E=32, k=9, H=256, F=128, T=100, G=2), zipf_s=1.2),
+    # the layer call runs with T below the context's max_tokens (workspaces sized for 4x more)
+    "T-below-capacity": CaseCfg(pi.C0.with_(name="tbc", E=16, k=4, H=256, F=256, T=77, G=4), zipf_s=1.3,
+                                max_tokens=300),
 }
 
 
@@ -127,3 +134,31 @@ def test_layer_parity_fp32(name):
     orc = run_oracle(case, inputs)
     rep = compare(case, gpu, orc, tol=1e-5)
     print(name, rep)
+
+
+def test_boundary_errors():
+    """Host-checkable errors (include/probe.h): T outside [1, max_tokens] → PROBE_ECAPACITY,
+    use_plan without probe_plan/probe_prefetch for that layer → PROBE_ESTATE, null pointers →
+    PROBE_EINVAL; the context stays usable after each refused call."""
+    import torch
+    from paper_2602_00509_b200 import ProbeConfig, ProbeRuntime
+    from paper_2602_00509_b200._lib import ProbeError
+    sh = pi.C0
+    rt = ProbeRuntime(ProbeConfig(G=sh.G, E=sh.E, k=sh.k, H=sh.H, F=sh.F, T=sh.T, h=sh.h))
+    li = pi.layer_inputs(sh, 0, 0, 1.2, device="cuda")
+    W = pi.router_weight(sh, 0, device="cuda")
+    w13, w2 = pi.expert_weights(sh, 0, device="cuda")
+    out = torch.empty(sh.G, sh.T, sh.H, device="cuda")
+    big = torch.zeros(sh.G, sh.T + 1, sh.H, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ProbeError, match="CAPACITY"):
+        rt.forward(0, big, W, None, w13, w2, out)
+    with pytest.raises(ProbeError, match="CAPACITY"):
+        rt.forward(0, li.x[:, :0], W, None, w13, w2, out)
+    with pytest.raises(ProbeError, match="STATE"):
+        rt.forward(3, li.x, W, None, w13, w2, out, use_plan=True)
+    with pytest.raises(ProbeError, match="INVAL"):
+        rt.forward(0, li.x, W, None, w13, None, out)
+    rt.forward(0, li.x, W, None, w13, w2, out)      # still usable
+    rt.check()
+    assert torch.isfinite(out).all()
+    rt.close()
