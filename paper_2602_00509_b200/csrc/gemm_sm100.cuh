@@ -292,8 +292,7 @@ __device__ __forceinline__ void epi_topk(uint32_t tb, int lane, const GemmGroup&
   for (int c = 0; c < BN / 32; ++c) {
     if (c * 32 >= G.n) break;
     uint32_t v32[32];
-    ptx::tmem_ld32(tb + c * 32, v32);
-    ptx::tmem_ld_wait();
+    ptx::tmem_ld32_wait(tb + c * 32, v32);
     // stage the row in smem (element i of row r at r·32 + (i ^ r): conflict-free both ways)
     __syncwarp();
 #pragma unroll
@@ -357,9 +356,7 @@ __device__ __forceinline__ void epi_tile(uint32_t tb, int lane, int part, const 
 #pragma unroll 1
     for (int c = part; c < BN / 64; c += NPART) {
       uint32_t gv[32], uv[32];
-      ptx::tmem_ld32(tb + c * 32, gv);
-      ptx::tmem_ld32(tb + BN / 2 + c * 32, uv);
-      ptx::tmem_ld_wait();
+      ptx::tmem_ld32x2_wait(tb + c * 32, gv, tb + BN / 2 + c * 32, uv);
       float v[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = silu_f(__uint_as_float(gv[i])) * __uint_as_float(uv[i]);
@@ -371,9 +368,8 @@ __device__ __forceinline__ void epi_tile(uint32_t tb, int lane, int part, const 
     for (int c = part; c < BN / 32; c += 2 * NPART) {
       const int c2 = c + NPART;
       uint32_t va[32], vb[32];
-      ptx::tmem_ld32(tb + c * 32, va);
-      if (c2 < BN / 32) ptx::tmem_ld32(tb + c2 * 32, vb);
-      ptx::tmem_ld_wait();
+      if (c2 < BN / 32) ptx::tmem_ld32x2_wait(tb + c * 32, va, tb + c2 * 32, vb);
+      else ptx::tmem_ld32_wait(tb + c * 32, va);
       float v[32];
       const bool silu = G.mode == EPI_SILU_BF16;
 #pragma unroll

@@ -958,8 +958,12 @@ constexpr int kPrefetchChunk = 64 * 1024;  // bytes
 
 // Register copy (not TMA bulk): the expert-GEMM CTAs leave < 10 KB of shared memory per
 // SM, so a smem-staged copy could not co-reside with them during part 1.  Each thread keeps
-// 8 × 16 B in flight; chunks never straddle the W13 / W2 matrices.
-__global__ void __launch_bounds__(512) k_prefetch(Dims d, const int32_t* __restrict__ replicas, int bank,
+// U × 16 B in flight; chunks never straddle the W13 / W2 matrices.  Part 1 uses the
+// register-capped instance (MAXR = kPrefetchPart1Reg, U = 4) so that one 128-thread CTA fits
+// beside an expert-GEMM CTA capped at (64 K − 128·MAXR) / 256 registers.
+constexpr int kPrefetchPart1Reg = 32;
+template <int MAXR = 255, int U = 8>
+__global__ void __launch_bounds__(512) __maxnreg__(MAXR) k_prefetch(Dims d, const int32_t* __restrict__ replicas, int bank,
                                                   const uint8_t* __restrict__ w13, const uint8_t* __restrict__ w2,
                                                   Sym sym, int buf_rw13, int buf_rw2, int32_t* ctr,
                                                   const volatile int32_t* suspend_flag, int suspend_at,
@@ -1009,15 +1013,15 @@ __global__ void __launch_bounds__(512) k_prefetch(Dims d, const int32_t* __restr
     uint4* dst = reinterpret_cast<uint4*>(sym.at(first ? buf_rw13 : buf_rw2, d.G, tr_dst[ti]) +
                                           static_cast<size_t>(slot) * mat + off);
     const int nv = static_cast<int>(len / 16);
-    for (int v0 = 0; v0 < nv; v0 += blockDim.x * 8) {
-      uint4 r[8];
+    for (int v0 = 0; v0 < nv; v0 += blockDim.x * U) {
+      uint4 r[U];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int i = v0 + u * blockDim.x + threadIdx.x;
         if (i < nv) r[u] = __ldg(src + i);
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int i = v0 + u * blockDim.x + threadIdx.x;
         if (i < nv) dst[i] = r[u];
       }

@@ -253,8 +253,9 @@ enum GemmVariant { V_128_6_4 = 0, V_256_4_4 = 1, V_256_3_8 = 2, V_128_4_8 = 3, V
                    V_2CTA_256_4_4_NB4 = 9 /* CTA pair, 4 stages, 4 staging slots per epilogue warp */,
                    V_256_4_4_EXP = 10 /* 1-CTA <256,4,4> register-capped for the expert GEMMs */ };
 
-// Expert GEMMs leave registers for one 128-thread prefetch CTA per SM (a9 part 1 runs beside them)
-constexpr int kExpertMaxReg = 216;
+// Expert GEMMs leave registers for one 128-thread prefetch CTA per SM (a9 part 1 runs beside them):
+// 256 × 240 + 128 × 32 = 64 K.  (216 spilled 36 B per thread and cost ~5% GEMM time.)
+constexpr int kExpertMaxReg = (65536 - 128 * kPrefetchPart1Reg) / 256;
 
 template <int BN, int ST, int EW, int NB = 1, int MAXR = 255>
 cudaError_t launch_gemm_2cta(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, const CUtensorMap& c,
@@ -948,16 +949,16 @@ probe_status probe_prefetch(probe_ctx ctx, int32_t next_layer, const void* w13_n
   const int grid = 16;  // part 2 (after the combine): "controlled SM occupancy"
   if (inflight) {
     // part 1 beside the expert GEMMs: one 128-thread CTA per SM fits in the registers the
-    // register-capped expert GEMM CTAs leave free (216 × 256 + 64 × 128 < 64 K)
+    // register-capped expert GEMM CTAs leave free (kExpertMaxReg × 256 + kPrefetchPart1Reg × 128 = 64 K)
     CK(ev_wait(ctx, st, ctx->ev_gemm[prev]));
-    k_prefetch<<<ctx->num_sms, 128, 0, st>>>(d, ctx->at<int32_t>(s.reps[pp]), pp, static_cast<const uint8_t*>(w13_next),
+    k_prefetch<kPrefetchPart1Reg, 4><<<ctx->num_sms, 128, 0, st>>>(d, ctx->at<int32_t>(s.reps[pp]), pp, static_cast<const uint8_t*>(w13_next),
                                      static_cast<const uint8_t*>(w2_next), sym_of(ctx), PROBE_BUF_REP_W13,
                                      PROBE_BUF_REP_W2, ctx->at<int32_t>(s.pfctr[pp]), flags + 1, next_layer,
                                      flags + 2, static_cast<int>(esz(ctx->cfg)));
     CKL();
     CK(ev_wait(ctx, st, ctx->ev_comb[prev]));
   }
-  k_prefetch<<<grid, 512, 0, st>>>(d, ctx->at<int32_t>(s.reps[pp]), pp, static_cast<const uint8_t*>(w13_next),
+  k_prefetch<><<<grid, 512, 0, st>>>(d, ctx->at<int32_t>(s.reps[pp]), pp, static_cast<const uint8_t*>(w13_next),
                                    static_cast<const uint8_t*>(w2_next), sym_of(ctx), PROBE_BUF_REP_W13,
                                    PROBE_BUF_REP_W2, ctx->at<int32_t>(s.pfctr[pp]), flags + 1, -1, flags + 3,
                                    static_cast<int>(esz(ctx->cfg)));

@@ -7,6 +7,7 @@ is not predicted, R29) → predict(L1) → plan(L1) → prefetch(L1) → forward
 from __future__ import annotations
 
 import dataclasses
+import os
 from typing import Optional
 
 import numpy as np
@@ -119,6 +120,8 @@ def run_gpu(case: CaseCfg):
     win = torch.full((G,), case.window_ns, dtype=torch.int64, device=dev)
     res = {}
     rt.forward(0, L0.x, W[0], b[0], w13[0], w2[0], out[0], use_plan=False, topk_ids=ids[0], topk_w=gw[0])
+    if os.environ.get("PROBE_TEST_SYNC_L0"):      # debugging aid: serialise layer 0 before the aux track
+        torch.cuda.synchronize()
     lay0 = debug(rt, cfg, T)
     pc_unfused = torch.empty(G, E, dtype=torch.int32, device=dev)
     rt.predict(1, L0.x, W[1], b[1], r1, r2, pred_counts=pc_unfused, pred_logits=plog)   # unfused (logits out)

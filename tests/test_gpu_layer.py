@@ -62,6 +62,11 @@ CASES = {
     "k1": CaseCfg(pi.C0.with_(name="k1", E=8, k=1, H=256, F=256, T=130, G=2), zipf_s=1.5),
     "k-eq-E": CaseCfg(pi.C0.with_(name="kE", E=8, k=8, H=256, F=128, T=70, G=2), zipf_s=1.0),
     "k9-unfused-select": CaseCfg(pi.C0.with_(name="k9b", E=32, k=9, H=256, F=128, T=100, G=2), zipf_s=1.2),
+    # H, F not multiples of the 256-column tile: ragged N in GEMM1 (2F) and GEMM2 (H), ragged K
+    "ragged-HF": CaseCfg(pi.C0.with_(name="rhf", E=16, k=4, H=320, F=320, T=64, G=2), zipf_s=1.3),
+    "C2-dims-static": CaseCfg(pi.C0.with_(name="c2s", E=16, k=4, H=2880, F=2880, T=64, G=2), zipf_s=1.3,
+                              replica_budget=0),
+    "C2-dims": CaseCfg(pi.C0.with_(name="c2d", E=16, k=4, H=2880, F=2880, T=64, G=2), zipf_s=1.3),
     # the layer call runs with T below the context's max_tokens (workspaces sized for 4x more)
     "T-below-capacity": CaseCfg(pi.C0.with_(name="tbc", E=16, k=4, H=256, F=256, T=77, G=4), zipf_s=1.3,
                                 max_tokens=300),
@@ -152,8 +157,11 @@ def test_boundary_errors():
     big = torch.zeros(sh.G, sh.T + 1, sh.H, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(ProbeError, match="CAPACITY"):
         rt.forward(0, big, W, None, w13, w2, out)
-    with pytest.raises(ProbeError, match="CAPACITY"):
-        rt.forward(0, li.x[:, :0], W, None, w13, w2, out)
+    from paper_2602_00509_b200._lib import STATUS
+    from paper_2602_00509_b200.runtime import _ptr
+    st = rt.lib.probe_moe_forward(rt.ctx, 0, _ptr(li.x), 0, _ptr(W), None, _ptr(w13), _ptr(w2), 0, _ptr(out), 1,
+                                  None, None, None)                       # T = 0, valid pointers
+    assert STATUS[st] == "PROBE_ECAPACITY"
     with pytest.raises(ProbeError, match="STATE"):
         rt.forward(3, li.x, W, None, w13, w2, out, use_plan=True)
     with pytest.raises(ProbeError, match="INVAL"):
