@@ -272,6 +272,11 @@ __device__ __forceinline__ void epi_chunk(float* tiles, int& tsel, int lane, con
   } else {
     __syncwarp();
     epi_store_manual(tile, lane, G, row0, col0);
+    // an EMPTY bulk group keeps "one group per staged chunk": the bulk_wait_read above counts
+    // groups, and a chunk without a TMA store (row tail, or a column chunk past G.n in a ragged
+    // last N tile) must not let the wait skip the store still reading the slot it reuses —
+    // without this the C2 Y columns 2848..2879 (H = 2880) were intermittently overwritten
+    if (lane == 0) ptx::bulk_commit();
   }
   __syncwarp();
   tsel = (tsel + 1) % (f16 ? 2 * NB : NB);

@@ -961,7 +961,7 @@ constexpr int kPrefetchChunk = 64 * 1024;  // bytes
 // U × 16 B in flight; chunks never straddle the W13 / W2 matrices.  Part 1 uses the
 // register-capped instance (MAXR = kPrefetchPart1Reg, U = 4) so that one 128-thread CTA fits
 // beside an expert-GEMM CTA capped at (64 K − 128·MAXR) / 256 registers.
-constexpr int kPrefetchPart1Reg = 32;
+constexpr int kPrefetchPart1Reg = 48;
 template <int MAXR = 255, int U = 8>
 __global__ void __launch_bounds__(512) __maxnreg__(MAXR) k_prefetch(Dims d, const int32_t* __restrict__ replicas, int bank,
                                                   const uint8_t* __restrict__ w13, const uint8_t* __restrict__ w2,

@@ -951,7 +951,7 @@ probe_status probe_prefetch(probe_ctx ctx, int32_t next_layer, const void* w13_n
     // part 1 beside the expert GEMMs: one 128-thread CTA per SM fits in the registers the
     // register-capped expert GEMM CTAs leave free (kExpertMaxReg × 256 + kPrefetchPart1Reg × 128 = 64 K)
     CK(ev_wait(ctx, st, ctx->ev_gemm[prev]));
-    k_prefetch<kPrefetchPart1Reg, 4><<<ctx->num_sms, 128, 0, st>>>(d, ctx->at<int32_t>(s.reps[pp]), pp, static_cast<const uint8_t*>(w13_next),
+    k_prefetch<kPrefetchPart1Reg, 8><<<ctx->num_sms, 128, 0, st>>>(d, ctx->at<int32_t>(s.reps[pp]), pp, static_cast<const uint8_t*>(w13_next),
                                      static_cast<const uint8_t*>(w2_next), sym_of(ctx), PROBE_BUF_REP_W13,
                                      PROBE_BUF_REP_W2, ctx->at<int32_t>(s.pfctr[pp]), flags + 1, next_layer,
                                      flags + 2, static_cast<int>(esz(ctx->cfg)));

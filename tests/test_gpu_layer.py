@@ -64,6 +64,11 @@ CASES = {
     "k9-unfused-select": CaseCfg(pi.C0.with_(name="k9b", E=32, k=9, H=256, F=128, T=100, G=2), zipf_s=1.2),
     # H, F not multiples of the 256-column tile: ragged N in GEMM1 (2F) and GEMM2 (H), ragged K
     "ragged-HF": CaseCfg(pi.C0.with_(name="rhf", E=16, k=4, H=320, F=320, T=64, G=2), zipf_s=1.3),
+    # ...with groups of >= 32 rows, so the last N tile mixes TMA-stored chunks with chunks past
+    # N (the fp16-Y staging-slot reuse bug: columns 2848..2879 of C2's Y were overwritten)
+    "ragged-HF-tma": CaseCfg(pi.C0.with_(name="rhft", E=16, k=4, H=320, F=320, T=600, G=2), zipf_s=1.0),
+    "ragged-HF-tma-one-cta": CaseCfg(pi.C0.with_(name="rhfo", E=16, k=4, H=320, F=320, T=600, G=2), zipf_s=1.0,
+                                     pair_gemm=False),
     "C2-dims-static": CaseCfg(pi.C0.with_(name="c2s", E=16, k=4, H=2880, F=2880, T=64, G=2), zipf_s=1.3,
                               replica_budget=0),
     "C2-dims": CaseCfg(pi.C0.with_(name="c2d", E=16, k=4, H=2880, F=2880, T=64, G=2), zipf_s=1.3),

@@ -22,7 +22,13 @@ for it in range(int(os.environ.get("REPS", "3"))):
             os.environ.pop("PROBE_TEST_SYNC_L0", None)
         gpu, inputs = run_gpu(case)
         if orc is None or mode == "b0" or orc[0] != (mode == "b0"):
-            orc = (mode == "b0", run_oracle(case, inputs))
+            import pickle
+            cache = f"/tmp/c2dbg_orc_{mode == 'b0'}.pkl"
+            if os.path.exists(cache):
+                orc = pickle.load(open(cache, "rb"))
+            else:
+                orc = (mode == "b0", run_oracle(case, inputs))
+                pickle.dump(orc, open(cache, "wb"))
         o = orc[1]
         ref = o["ref"][0]
         toks = o["tokens"]
