@@ -254,8 +254,10 @@ enum GemmVariant { V_128_6_4 = 0, V_256_4_4 = 1, V_256_3_8 = 2, V_128_4_8 = 3, V
                    V_256_4_4_EXP = 10 /* 1-CTA <256,4,4> register-capped for the expert GEMMs */ };
 
 // Expert GEMMs leave registers for one 128-thread prefetch CTA per SM (a9 part 1 runs beside them):
-// 256 × 240 + 128 × 32 = 64 K.  (216 spilled 36 B per thread and cost ~5% GEMM time.)
-constexpr int kExpertMaxReg = (65536 - 128 * kPrefetchPart1Reg) / 256;
+// 256 × 224 + 128 × 48 = 62 K.  Splits that fill exactly 64 K (240 + 32, 232 + 48) did not
+// co-reside (C2 part 1 stalled, 100 µs exposed wait), so 2 K registers stay free.
+constexpr int kExpertMaxReg = 224;
+static_assert(256 * kExpertMaxReg + 128 * kPrefetchPart1Reg <= 65536 - 2048, "part-1 prefetch CTA must fit");
 
 template <int BN, int ST, int EW, int NB = 1, int MAXR = 255>
 cudaError_t launch_gemm_2cta(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, const CUtensorMap& c,
