@@ -258,6 +258,12 @@ enum GemmVariant { V_128_6_4 = 0, V_256_4_4 = 1, V_256_3_8 = 2, V_128_4_8 = 3, V
 // co-reside (C2 part 1 stalled, 100 µs exposed wait), so 2 K registers stay free.
 constexpr int kExpertMaxReg = 224;
 static_assert(256 * kExpertMaxReg + 128 * kPrefetchPart1Reg <= 65536 - 2048, "part-1 prefetch CTA must fit");
+// The 1-CTA expert GEMM (decode-sized groups, C2) keeps the lower cap 216: A/B at C2 on one
+// box, 2 runs each: 216 → 1.53–1.54 M tok/s, part 1 pushes 95 of 119 MB, exposed wait 24 µs;
+// 224 → 1.43 M tok/s, 71 MB, 110–118 µs.
+#ifndef PROBE_EXP1_MAXREG
+#define PROBE_EXP1_MAXREG 216
+#endif
 
 template <int BN, int ST, int EW, int NB = 1, int MAXR = 255>
 cudaError_t launch_gemm_2cta(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, const CUtensorMap& c,
@@ -331,7 +337,7 @@ cudaError_t launch_gemm_v(int v, const CUtensorMap& a, const CUtensorMap& b0, co
     case V_256_3_4_NB2: return launch_gemm_t<256, 3, 4, 2>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_256_3_4_NB4: return launch_gemm_t<256, 3, 4, 4>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_2CTA_256_6_4: return launch_gemm_2cta<256, 6, 4, 1, kExpertMaxReg>(a, b0, b1, c, A2, s, K, K2, grid, st);
-    case V_256_4_4_EXP: return launch_gemm_t<256, 4, 4, 1, kExpertMaxReg>(a, b0, b1, c, A2, s, K, K2, grid, st);
+    case V_256_4_4_EXP: return launch_gemm_t<256, 4, 4, 1, PROBE_EXP1_MAXREG>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_2CTA_256_5_8: return launch_gemm_2cta<256, 5, 8>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_2CTA_256_5_4_NB2: return launch_gemm_2cta<256, 5, 4, 2>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_2CTA_256_4_4_NB4: return launch_gemm_2cta<256, 4, 4, 4>(a, b0, b1, c, A2, s, K, K2, grid, st);
