@@ -422,14 +422,18 @@ def run_probe(args):
         tj = json.load(open(tfile))
         if tj.get("config") == shape.name:
             traffic = tj.get("dram_bytes_per_launch")
+    # the library runs the expert GEMMs on CTA pairs when T·k·G ≥ 256·E (256-row tiles fill)
+    kname = ("grouped_gemm_2cta_kernel<256,6,4,224> (expert GEMM1 + SwiGLU, tcgen05 cta_group::2)"
+             if T * shape.k * G >= 256 * shape.E else
+             "grouped_gemm_kernel<256,4,4,1,216> (expert GEMM1 + SwiGLU, tcgen05, 1-CTA 128-row tiles)")
     if hbm_bound:
-        roof = {"kernel": "grouped_gemm_2cta_kernel<256,6,4> (expert GEMM1 + SwiGLU, tcgen05 cta_group::2)", "bound": "hbm",
+        roof = {"kernel": kname, "bound": "hbm",
                 "achieved": by1 / t1 / 1e9, "peak": peak_bw, "unit": "GB/s", "frac": by1 / t1 / 1e9 / peak_bw,
                 "traffic": traffic, "peak_kind": f"{pk_kind} hbm_gbs", "algorithmic_bytes_per_launch": by1,
                 "gemm2": {"achieved": by2 / t2 / 1e9, "frac": by2 / t2 / 1e9 / peak_bw},
                 "tensor_frac": fl1 / t1 / 1e12 / peak_tf}
     else:
-        roof = {"kernel": "grouped_gemm_2cta_kernel<256,6,4> (expert GEMM1 + SwiGLU, tcgen05 cta_group::2)", "bound": "tensor",
+        roof = {"kernel": kname, "bound": "tensor",
                 "achieved": fl1 / t1 / 1e12, "peak": peak_tf, "unit": "TFLOP/s", "frac": fl1 / t1 / 1e12 / peak_tf,
                 "traffic": traffic, "peak_kind": f"{pk_kind} bf16_tflops_sustained",
                 "algorithmic_flops_per_launch": fl1, "algorithmic_bytes_per_launch": by1,
