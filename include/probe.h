@@ -16,6 +16,11 @@
  *  - `stream` is a cudaStream_t passed as void* (no CUDA headers needed).
  *  - Every call only ENQUEUES work on its stream(s) and never synchronises the
  *    host (CUDA-Graph safe), except probe_check/probe_finalize.
+ *    Graph capture rule: a capturing stream cannot wait on an event recorded outside its
+ *    capture, so the library omits those cross-capture waits (e.g. a captured forward of
+ *    layer L on the plan of L enqueued eagerly).  The caller must therefore complete all
+ *    eager work of the context (cudaDeviceSynchronize) before beginning a capture.
+ *    Cross-process barriers keep their epochs in device memory, so replays stay ordered.
  *  - Host-checkable problems (null/out-of-range scalar, shape, call order)
  *    return a status synchronously and set probe_last_error(); nothing is
  *    enqueued in that case.  Device-detected problems (receive-capacity
@@ -135,6 +140,8 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
  *   x, w_router_next act;  w_res1 [h, H] act or NULL, w_res2 [E, h] act or NULL (NULL ⇒ frozen prior only);
  *   the activation is rounded to bf16 in both dtypes (R8: part of the predictor's definition)
  *   pred_counts [G, E] int32 out or NULL;  pred_logits [local_ranks, T, E] fp32 out or NULL
+ *   (pred_logits are written by the same product-path kernels that produce n̂: the top-k
+ *   select kernel stores exactly the l̂ values it ranks)
  * If probe_moe_forward(next_layer-1) was enqueued, waits for its gate (x ready). */
 probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int32_t T,
                            const void* w_router_next, const float* b_router_next,
@@ -175,6 +182,16 @@ probe_status probe_debug_layout(probe_ctx ctx, int32_t* counts, int32_t* split, 
  * combine's suspend flag) / in part 2 (after the combine).  Cumulative since probe_init;
  * enqueued on `stream` after the context's prefetch stream work issued so far. */
 probe_status probe_debug_prefetch(probe_ctx ctx, int32_t* out, void* stream);
+
+/* Device status words (device int32 out[8], enqueued on `stream` after the work issued so far
+ * on the context's aux and prefetch streams): out[0] error word (bit 0 receive overflow,
+ * bit 2 plan, bit 3 fp16 Y range), out[1] prefetch suspend flag, out[2] / out[3] prefetch
+ * part-1 / part-2 KiB, out[4] number of layers that FELL BACK TO STATIC EP because the
+ * plan's layout would have overflowed some rank's recv_capacity (SURVEY §8(b) Errors: the
+ * layout kernel decides this on device, identically on every rank, and runs static EP for
+ * that layer; semantic equivalence P:364 keeps the output the same function).  If static
+ * EP itself overflows, the error word is set and probe_check returns PROBE_ECAPACITY. */
+probe_status probe_debug_flags(probe_ctx ctx, int32_t* out, void* stream);
 
 /* Test hook: one grouped bf16 GEMM through the tcgen05 kernel,
  * C[g] (fp32, [m_g, N]) = A[a_row_g : a_row_g + m_g, :K] · B[b_row_g : b_row_g + N, :K]^T

@@ -29,7 +29,7 @@ __all__ = [
     "round_bf16", "router_logits", "topk_ids", "gate", "silu", "predictor_logits",
     "predict_counts", "PlannerConfig", "Plan", "replica_caps", "rank_costs",
     "token_loads", "plan_greedy", "static_plan", "materialize", "slot_experts",
-    "dispatch_layout", "Layout", "swiglu_expert", "combine", "moe_layer_outputs",
+    "dispatch_layout", "Layout", "swiglu_expert", "combine", "moe_layer_outputs", "moe_outputs_ranks",
     "imbalance_ratio", "expert_compute_time", "traffic_volumes", "transfer_latency",
     "exposed_overhead", "replica_slot_schedule", "layer_reference",
 ]
@@ -391,6 +391,28 @@ def moe_layer_outputs(x: np.ndarray, ids: np.ndarray, g: np.ndarray,
     return combine(g[tokens], y)
 
 
+def moe_outputs_ranks(xs: List[np.ndarray], ids: List[np.ndarray], gs: List[np.ndarray], W13, W2,
+                      tokens: Optional[List[Sequence[int]]] = None) -> List[np.ndarray]:
+    """moe_layer_outputs for every source rank at once, loop over experts outermost, so
+    each expert's weights are read once for all ranks (W13/W2 may decode on access).
+    Same arithmetic: y_{t,j} = swiglu_expert(x_t) with expert ids[t,j], then combine in
+    slot order (R4, R25)."""
+    G = len(xs)
+    toks = [list(range(xs[s].shape[0])) if tokens is None else list(tokens[s]) for s in range(G)]
+    k = ids[0].shape[1]
+    H = xs[0].shape[1]
+    ys = [np.zeros((len(toks[s]), k, H)) for s in range(G)]
+    sub = [ids[s][np.asarray(toks[s], dtype=np.int64)] for s in range(G)]
+    experts = sorted(set(int(v) for s in range(G) for v in sub[s].reshape(-1)))
+    for e in experts:
+        w13, w2 = W13[e], W2[e]
+        for s in range(G):
+            ti, jj = np.nonzero(sub[s] == e)
+            if len(ti):
+                ys[s][ti, jj] = swiglu_expert(xs[s][np.asarray(toks[s])[ti]], w13, w2)
+    return [combine(gs[s][np.asarray(toks[s], dtype=np.int64)], ys[s]) for s in range(G)]
+
+
 # =============================================================================
 # analytical model (§3, Eq. 1–6) — used by tests as pins and by reporting
 # =============================================================================
@@ -474,8 +496,5 @@ def layer_reference(xs: List[np.ndarray], W: np.ndarray, b: Optional[np.ndarray]
     lay = dispatch_layout(ids, split, replicas, G, E) if with_layout else None
     outs = None
     if W13 is not None:
-        outs = []
-        for s in range(G):
-            tk = None if tokens is None else tokens[s]
-            outs.append(moe_layer_outputs(xs[s], ids[s], gs[s], W13, W2, tk))
+        outs = moe_outputs_ranks(xs, ids, gs, W13, W2, tokens)
     return dict(ids=ids, g=gs, n=n, split=split, layout=lay, out=outs, replicas=replicas)

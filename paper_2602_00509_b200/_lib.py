@@ -20,7 +20,7 @@ STATUS = {0: "PROBE_OK", 1: "PROBE_EINVAL", 2: "PROBE_ESHAPE", 3: "PROBE_EBUDGET
 
 # every exported symbol declared in include/probe.h
 EXPORTS = ["probe_workspace", "probe_init", "probe_moe_forward", "probe_predict", "probe_plan",
-           "probe_prefetch", "probe_debug_layout", "probe_debug_prefetch", "probe_test_gemm", "probe_check", "probe_last_error",
+           "probe_prefetch", "probe_debug_layout", "probe_debug_prefetch", "probe_debug_flags", "probe_test_gemm", "probe_check", "probe_last_error",
            "probe_finalize", "probe_launch_count", "probe_profile", "probe_profile_read", "probe_bench_gemm",
            "probe_ipc_export", "probe_ipc_import", "probe_ipc_close", "probe_set_option",
            "probe_history_update", "probe_distill_grad", "probe_distill_apply"]
@@ -75,6 +75,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "probe_prefetch": (i32, [vp, i32, vp, vp, i32, vp]),
         "probe_debug_layout": (i32, [vp, vp, vp, vp, vp, vp, vp]),
         "probe_debug_prefetch": (i32, [vp, vp, vp]),
+        "probe_debug_flags": (i32, [vp, vp, vp]),
         "probe_test_gemm": (i32, [vp, i64, vp, i64, i32, i32, C.POINTER(C.c_int32), i32, i32, vp, vp]),
         "probe_bench_gemm": (i32, [vp, i64, vp, i64, i32, i32, C.POINTER(C.c_int32), i32, i32, i32, i32,
                                    C.POINTER(C.c_float), vp, vp]),

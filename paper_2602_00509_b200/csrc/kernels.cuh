@@ -160,7 +160,8 @@ template <int KK, bool PRED>
 __global__ void __launch_bounds__(128) k_select(Dims d, int T, const float* __restrict__ logits,
                                                 const float* __restrict__ bias, int32_t* __restrict__ ids,
                                                 float* __restrict__ gw, int32_t* __restrict__ pos,
-                                                int32_t* __restrict__ hist, int32_t* __restrict__ counts) {
+                                                int32_t* __restrict__ hist, int32_t* __restrict__ counts,
+                                                float* __restrict__ logits_out = nullptr) {
   __shared__ uint32_t mask[kMaxE * 4];
   __shared__ int32_t scount[kMaxE];
   const int E = d.E;
@@ -192,6 +193,12 @@ __global__ void __launch_bounds__(128) k_select(Dims d, int T, const float* __re
 #pragma unroll
         for (int i = 0; i < 32; ++i)
           if (c + i < E) v[i] += __ldg(bias + c + i);
+      }
+      if (PRED && logits_out) {   // l̂ = prior + residual + b, exactly the values the selection ranks
+        float* lo = logits_out + (static_cast<size_t>(gl) * T + t) * E + c;
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (c + i < E) lo[i] = v[i];
       }
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
@@ -550,6 +557,7 @@ struct LayoutOut {
   GemmSched* s1;        // SwiGLU (expert GEMM 1)
   GemmSched* s2;        // fp16 Y (expert GEMM 2)
   int32_t* err;
+  int32_t* fallbacks;   // count of layers that fell back to static EP (plan would overflow) or null
 };
 struct LayoutIn {
   int nparts;                   // >1: partition the expert GEMMs by local rank (EP emulation)
@@ -566,25 +574,17 @@ struct LayoutIn {
   const int32_t* a_ready;       // overlapped dispatch: GEMM1 acquires these block flags (else null)
 };
 
-__global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o) {
-  extern __shared__ int32_t sm_split[];            // [G][E][G] materialized split
-  __shared__ int32_t reps[kMaxG * kMaxRb];
-  constexpr int kMaxGS = kMaxE + kMaxRb * kMaxG;   // G·S = E + 3G
-  __shared__ int32_t gt[kMaxGS];                   // rows per (dest, slot)
-  __shared__ int32_t gpre[kMaxGS];                 // first row of (dest, slot)
-  __shared__ int32_t t1[kMaxGroups], t2[kMaxGroups];
-  const int G = d.G, E = d.E, EL = d.EL, S = EL + kMaxRb;
-  const int tid = threadIdx.x;
-  for (int i = tid; i < G * kMaxRb; i += blockDim.x) reps[i] = in.replicas ? in.replicas[i] : -1;
-  __syncthreads();
-  // (1) materialize (R23), one thread per (s, e)
-  for (int i = tid; i < G * E; i += blockDim.x) {
+// R23 for every (s, e): split[s][e][t] from the quota (or static EP when quota == null)
+__device__ void layout_materialize(const Dims& d, const LayoutIn& in, const int32_t* reps, int32_t* sm_split,
+                                   const int32_t* quota) {
+  const int G = d.G, E = d.E, EL = d.EL;
+  for (int i = threadIdx.x; i < G * E; i += blockDim.x) {
     const int s = i / E, e = i % E;
     const int n = in.board_actual[s * E + e];
     int a[kMaxG];
     int P = 0;
     for (int t = 0; t < G; ++t) {
-      a[t] = in.quota ? in.quota[(s * E + e) * G + t] : 0;
+      a[t] = quota ? quota[(s * E + e) * G + t] : 0;
       P += a[t];
     }
     if (P == 0) {
@@ -602,11 +602,57 @@ __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o
       }
       a[tstar] += n - sum;
     }
+    for (int t = 0; t < G; ++t) sm_split[(s * E + e) * G + t] = a[t];
+  }
+}
+
+__global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o) {
+  extern __shared__ int32_t sm_split[];            // [G][E][G] materialized split
+  __shared__ int32_t reps[kMaxG * kMaxRb];
+  constexpr int kMaxGS = kMaxE + kMaxRb * kMaxG;   // G·S = E + 3G
+  __shared__ int32_t gt[kMaxGS];                   // rows per (dest, slot)
+  __shared__ int32_t gpre[kMaxGS];                 // first row of (dest, slot)
+  __shared__ int32_t t1[kMaxGroups], t2[kMaxGroups];
+  __shared__ int32_t dtot[kMaxG];
+  __shared__ int s_fallback;
+  const int G = d.G, E = d.E, EL = d.EL, S = EL + kMaxRb;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < G * kMaxRb; i += blockDim.x) reps[i] = in.replicas ? in.replicas[i] : -1;
+  for (int i = tid; i < G; i += blockDim.x) dtot[i] = 0;
+  __syncthreads();
+  // (1) materialize (R23), one thread per (s, e)
+  layout_materialize(d, in, reps, sm_split, in.quota);
+  __syncthreads();
+  // (1b) device-side static-EP fallback (probe.h, SURVEY §8(b) Errors): if the plan would
+  // overflow some destination's receive capacity (a misprediction sending replicas more rows
+  // than the plan expected), this layer runs static EP instead — decided identically on
+  // every rank from the same all-gathered counts, no host synchronization.
+  if (in.quota) {
+    for (int i = tid; i < G * E; i += blockDim.x)
+      for (int t = 0; t < G; ++t) {
+        const int v = sm_split[i * G + t];
+        if (v) atomicAdd(&dtot[t], v);
+      }
+    __syncthreads();
+    if (tid == 0) {
+      int over = 0;
+      for (int t = 0; t < G; ++t) over |= dtot[t] > d.cap;
+      s_fallback = over;
+      if (over && o.fallbacks) atomicAdd(o.fallbacks, 1);
+    }
+    __syncthreads();
+    if (s_fallback) {
+      for (int i = tid; i < G * kMaxRb; i += blockDim.x) reps[i] = -1;
+      __syncthreads();
+      layout_materialize(d, in, reps, sm_split, nullptr);
+      __syncthreads();
+    }
+  }
+  for (int i = tid; i < G * E; i += blockDim.x) {
     int run = 0;
     for (int t = 0; t < G; ++t) {
-      run += a[t];
-      sm_split[(s * E + e) * G + t] = a[t];
-      o.split_cum[(s * E + e) * G + t] = run;
+      run += sm_split[i * G + t];
+      o.split_cum[i * G + t] = run;
     }
   }
   // (2) local slot of every expert on every rank
@@ -959,8 +1005,11 @@ constexpr int kPrefetchChunk = 64 * 1024;  // bytes
 // Register copy (not TMA bulk): the expert-GEMM CTAs leave < 10 KB of shared memory per
 // SM, so a smem-staged copy could not co-reside with them during part 1.  Each thread keeps
 // U × 16 B in flight; chunks never straddle the W13 / W2 matrices.  Part 1 uses the
-// register-capped instance (MAXR = kPrefetchPart1Reg, U = 4) so that one 128-thread CTA fits
-// beside an expert-GEMM CTA capped at (64 K − 128·MAXR) / 256 registers.
+// register-capped instance (MAXR = kPrefetchPart1Reg, U = 8) so that one 128-thread CTA fits
+// beside an expert-GEMM CTA capped at (64 K − 2 K − 128·MAXR) / 256 registers.
+// Suspension compares the flag for EQUALITY with the layer whose combine suspends this part
+// (the combine of layer L stores L + 1): layer ids restart every serving step, so a flag left
+// at N by the previous step's last combine must not stop part 1 of an early layer.
 constexpr int kPrefetchPart1Reg = 48;
 template <int MAXR = 255, int U = 8>
 __global__ void __launch_bounds__(512) __maxnreg__(MAXR) k_prefetch(Dims d, const int32_t* __restrict__ replicas, int bank,
@@ -995,7 +1044,7 @@ __global__ void __launch_bounds__(512) __maxnreg__(MAXR) k_prefetch(Dims d, cons
   while (true) {
     if (threadIdx.x == 0) {
       int c = -1;
-      if (!(suspend_at >= 0 && *suspend_flag >= suspend_at)) c = atomicAdd(ctr, 1);
+      if (!(suspend_at >= 0 && *suspend_flag == suspend_at)) c = atomicAdd(ctr, 1);
       s_chunk = c;
     }
     __syncthreads();
@@ -1032,28 +1081,41 @@ __global__ void __launch_bounds__(512) __maxnreg__(MAXR) k_prefetch(Dims d, cons
 
 // =============================================================================
 // Cross-process barrier over the symmetric signal pads (one-sided NVLink stores).
-// Every local rank l stores `epoch` into slot [kind][R0+l] of EVERY rank's pad
+// The epoch of each barrier kind is a DEVICE counter (this process's scratch): the
+// kernel reads it, uses counter + 1 and writes that back when done, so a barrier
+// captured in a CUDA graph advances on every replay (a host-side epoch frozen into the
+// captured launch would let replayed barriers pass at once).  Each kind runs on one
+// stream (stream-ordered), and every process issues the same sequence of kinds, so the
+// counters advance in lockstep across processes.
+// Every local rank l stores the epoch into slot [kind][R0+l] of EVERY rank's pad
 // (release, system scope), then waits until its own pad holds >= epoch from all
 // G ranks (acquire, system scope).  Orders all prior writes of this stream
 // (dispatch rows, count boards, Y rows, replica pushes) before peers proceed.
 // One block of GL·G threads; 30 s watchdog (trap) instead of a silent hang.
 // =============================================================================
 constexpr int kSigKinds = 8;
-__global__ void k_xbarrier(Dims d, Sym sym, int buf_sig, int kind, uint32_t epoch) {
+__global__ void k_xbarrier(Dims d, Sym sym, int buf_sig, int kind, uint32_t* epoch_ctr) {
+  __shared__ uint32_t s_ep;
   const int i = threadIdx.x;
-  if (i >= d.GL * d.G) return;
-  const int l = i / d.G, r = i % d.G;
-  uint32_t* peer = reinterpret_cast<uint32_t*>(sym.at(buf_sig, d.G, r)) + kind * kMaxG + (d.R0 + l);
-  asm volatile("fence.acq_rel.sys;" ::: "memory");
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(peer), "r"(epoch) : "memory");
-  const uint32_t* mine = reinterpret_cast<const uint32_t*>(sym.at(buf_sig, d.G, d.R0 + l)) + kind * kMaxG + r;
-  uint32_t v;
-  const uint64_t t0 = ptx::globaltimer_ns();
-  while (true) {
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
-    if (static_cast<int32_t>(v - epoch) >= 0) break;
-    if (ptx::globaltimer_ns() - t0 > 30000000000ull) __trap();
+  if (i == 0) s_ep = epoch_ctr[kind] + 1u;
+  __syncthreads();
+  const uint32_t epoch = s_ep;
+  if (i < d.GL * d.G) {
+    const int l = i / d.G, r = i % d.G;
+    uint32_t* peer = reinterpret_cast<uint32_t*>(sym.at(buf_sig, d.G, r)) + kind * kMaxG + (d.R0 + l);
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(peer), "r"(epoch) : "memory");
+    const uint32_t* mine = reinterpret_cast<const uint32_t*>(sym.at(buf_sig, d.G, d.R0 + l)) + kind * kMaxG + r;
+    uint32_t v;
+    const uint64_t t0 = ptx::globaltimer_ns();
+    while (true) {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
+      if (static_cast<int32_t>(v - epoch) >= 0) break;
+      if (ptx::globaltimer_ns() - t0 > 30000000000ull) __trap();
+    }
   }
+  __syncthreads();
+  if (i == 0) epoch_ctr[kind] = epoch;
 }
 
 // small helper: write a host-described group list into a device schedule

@@ -194,7 +194,6 @@ struct probe_ctx_s {
   CUtensorMap map_recv, map_act, map_rw13, map_rw2, map_y;
   std::string err;
   int64_t launches = 0;
-  uint32_t epoch[kSigKinds] = {0};   // cross-process barrier epochs (identical sequence on every process)
   bool multi_process() const { return cfg.local_ranks != cfg.ep_size; }
   bool f32() const { return cfg.dtype == PROBE_FP32; }   // fp32 parity path (SIMT GEMMs)
   bool unfused = false;   // PROBE_UNFUSED=1: logits written + separate top-k kernels (debug)
@@ -264,19 +263,31 @@ static_assert(256 * kExpertMaxReg + 128 * kPrefetchPart1Reg <= 65536 - 2048, "pa
 #ifndef PROBE_EXP1_MAXREG
 #define PROBE_EXP1_MAXREG 216
 #endif
+// ptxas at 216: the 1-CTA expert GEMM keeps a 48-byte stack (59 LDL/STL, C2 A/B above);
+// at 255: 16 bytes.  Any override must still leave room for the part-1 prefetch CTA.
+static_assert(256 * PROBE_EXP1_MAXREG + 128 * kPrefetchPart1Reg <= 65536 - 2048, "part-1 prefetch CTA must fit");
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel instance PER DEVICE (a
+// process driving several devices must set it on each).
+template <class K>
+cudaError_t smem_attr_once(K kern, int bytes, uint64_t& done_mask) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if ((done_mask >> (dev & 63)) & 1ull) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done_mask |= 1ull << (dev & 63);
+  return e;
+}
 
 template <int BN, int ST, int EW, int NB = 1, int MAXR = 255>
 cudaError_t launch_gemm_2cta(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, const CUtensorMap& c,
                              const CUtensorMap& a2, GemmSched* s, int K, int K2, int grid, cudaStream_t st) {
   using L = Gemm2Smem<BN, ST, EW, NB>;
   static_assert(L::BYTES <= 232448, "shared memory budget");
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(grouped_gemm_2cta_kernel<BN, ST, EW, MAXR, NB>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static uint64_t attr = 0;
+  cudaError_t e = smem_attr_once(grouped_gemm_2cta_kernel<BN, ST, EW, MAXR, NB>, L::BYTES, attr);
+  if (e != cudaSuccess) return e;
   grouped_gemm_2cta_kernel<BN, ST, EW, MAXR, NB><<<grid & ~1, 128 + 32 * EW, L::BYTES, st>>>(a, b0, b1, c, a2, s, K,
                                                                                              K2);
   return cudaGetLastError();
@@ -290,12 +301,9 @@ cudaError_t launch_gemm1_overlap(const CUtensorMap& a, const CUtensorMap& b0, co
                                  bool pdl = true) {
   using L = Gemm2Smem<256, 6, 4>;
   auto* kern = grouped_gemm_2cta_kernel<256, 6, 4, kOverlapMaxReg>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static uint64_t attr = 0;
+  cudaError_t e = smem_attr_once(kern, L::BYTES, attr);
+  if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid & ~1);
   cfg.blockDim = dim3(128 + 32 * 4);
@@ -314,13 +322,9 @@ cudaError_t launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b0, const CUt
                           const CUtensorMap& a2, GemmSched* s, int K, int K2, int grid, cudaStream_t st) {
   using L = GemmSmem<BN, ST, EW, NB>;
   static_assert(L::BYTES <= 232448, "shared memory budget");
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(grouped_gemm_kernel<BN, ST, EW, NB, MAXR>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static uint64_t attr = 0;
+  cudaError_t e = smem_attr_once(grouped_gemm_kernel<BN, ST, EW, NB, MAXR>, L::BYTES, attr);
+  if (e != cudaSuccess) return e;
   grouped_gemm_kernel<BN, ST, EW, NB, MAXR><<<grid, 128 + 32 * EW, L::BYTES, st>>>(a, b0, b1, c, a2, s, K, K2);
   return cudaGetLastError();
 }
@@ -355,12 +359,13 @@ cudaError_t launch_gemm(const CUtensorMap& a, const CUtensorMap& b0, const CUten
 
 template <bool PRED>
 cudaError_t launch_select(const Dims& d, int T, int nchunks, cudaStream_t st, const float* lg, const float* b,
-                          int32_t* ids, float* gw, int32_t* pos, int32_t* hist, int32_t* cnt) {
+                          int32_t* ids, float* gw, int32_t* pos, int32_t* hist, int32_t* cnt,
+                          float* lo = nullptr) {
   const size_t smem = 0;
   dim3 grid(nchunks, d.GL);
 #define SEL(KK)                                                                                         \
   case KK: {                                                                                            \
-    k_select<KK, PRED><<<grid, 128, smem, st>>>(d, T, lg, b, ids, gw, pos, hist, cnt);                 \
+    k_select<KK, PRED><<<grid, 128, smem, st>>>(d, T, lg, b, ids, gw, pos, hist, cnt, lo);             \
     break;                                                                                              \
   }
   switch (d.k) {
@@ -423,6 +428,11 @@ cudaError_t ev_wait(probe_ctx ctx, cudaStream_t st, cudaEvent_t ev) {
 }
 
 enum { BAR_COUNTS = 0, BAR_DISPATCH = 1, BAR_Y = 2, BAR_PRED = 3, BAR_PREFETCH = 4 };
+// scratch flags (int32 words): 0 device error word, 1 prefetch suspend flag, 2/3 prefetch
+// part-1/part-2 KiB pushed, 4 static-EP fallbacks, kEpochSlot.. cross-process barrier epochs (one per kind)
+constexpr int kEpochSlot = 16;
+constexpr int kFallbackSlot = 4;   // layers whose plan would have overflowed → ran static EP
+static_assert(kEpochSlot + kSigKinds <= 64, "flags area is 256 bytes");
 
 // fp32 parity path: grouped SIMT GEMM over a device-resident schedule (sgemm_f32.cuh)
 cudaError_t launch_sgemm(probe_ctx ctx, const GemmSched* sc, const void* A, const void* B0, const void* B1, int K,
@@ -435,9 +445,10 @@ cudaError_t launch_sgemm(probe_ctx ctx, const GemmSched* sc, const void* A, cons
 // Cross-process barrier (no-op when this process hosts every rank: stream order suffices).
 cudaError_t xbarrier(probe_ctx ctx, int kind, cudaStream_t st) {
   if (!ctx->multi_process()) return cudaSuccess;
-  const uint32_t ep = ++ctx->epoch[kind];
   const Dims& d = ctx->d;
-  k_xbarrier<<<1, ((d.GL * d.G + 31) / 32) * 32, 0, st>>>(d, sym_of(ctx), PROBE_BUF_SIGNAL, kind, ep);
+  // epochs live in device memory (flags[kEpochSlot + kind]) so graph replays advance them
+  k_xbarrier<<<1, ((d.GL * d.G + 31) / 32) * 32, 0, st>>>(d, sym_of(ctx), PROBE_BUF_SIGNAL, kind,
+                                                          reinterpret_cast<uint32_t*>(ctx->at<int32_t>(ctx->sl.flags) + kEpochSlot));
   ++ctx->launches;
   return cudaGetLastError();
 }
@@ -688,6 +699,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   lo.s1 = ctx->at<GemmSched>(s.s_g1);
   lo.s2 = ctx->at<GemmSched>(s.s_g2);
   lo.err = err;
+  lo.fallbacks = err + kFallbackSlot;
   k_layout<<<1, 512, static_cast<size_t>(d.G) * d.E * d.G * 4, st>>>(d, li, lo);
   CKL();
   MARK(4);
@@ -794,7 +806,11 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
   if (!f32 && !mx) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
   const int nchunks = (T + kChunk - 1) / kChunk;
   CK(cudaMemsetAsync(ctx->at<int32_t>(s.pred_local), 0, GL * E * 4, st));
-  const bool fused = !pred_logits && d.k <= kTopkMax && d.E <= 256 && !ctx->unfused;
+  // The product path (K-concatenated GEMM + k_select) also serves pred_logits requests: the
+  // select kernel writes l̂ = prior + residual + b as it ranks it, so the logits a caller
+  // inspects are the ones that produced n̂ (only the debug/unfused path and k > 8 differ).
+  const bool fused = d.k <= kTopkMax && d.E <= 256 && !ctx->unfused;
+  const bool epi_topk = ctx->fused_epi_topk && !pred_logits;   // epilogue top-k keeps no logits
   if (f32) {
     // fp32 parity path: prior x·W_{L+1}ᵀ and z = x·Ŵ1ᵀ → a = bf16(SiLU(z)) (R8) in one grouped
     // SIMT launch, residual a·Ŵ2ᵀ, then the warp top-k sums prior + b + residual (Eq. (P))
@@ -846,7 +862,7 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
     SmallGroups s2{};
     s2.BN = BN;
     s2.n = 1;
-    if (ctx->fused_epi_topk) {
+    if (epi_topk) {
       s2.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_TOPK_COUNT, d.E, d.E, nullptr);
       s2.g[0].topk = d.k;
       s2.g[0].rows_per_rank = T;
@@ -860,9 +876,9 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
     CK(launch_gemm_v(BN == 128 ? V_128_6_4 : V_256_4_4, *mx, *mw, w_res1 ? *m2 : *mw, *mx, ctx->at<GemmSched>(s.s_p2),
                      d.H, ctx->aux_sms, st, w_res1 ? ma : nullptr, w_res1 ? d.h : 0));
     ++ctx->launches;
-    if (!ctx->fused_epi_topk) {
+    if (!epi_topk) {
       CK(launch_select<true>(d, T, nchunks, st, ctx->at<float>(s.pprior), b_router_next, nullptr, nullptr, nullptr,
-                             nullptr, ctx->at<int32_t>(s.pred_local)));
+                             nullptr, ctx->at<int32_t>(s.pred_local), pred_logits));
       ++ctx->launches;
     }
   } else {
@@ -957,7 +973,7 @@ probe_status probe_prefetch(probe_ctx ctx, int32_t next_layer, const void* w13_n
   const int grid = 16;  // part 2 (after the combine): "controlled SM occupancy"
   if (inflight) {
     // part 1 beside the expert GEMMs: one 128-thread CTA per SM fits in the registers the
-    // register-capped expert GEMM CTAs leave free (kExpertMaxReg × 256 + kPrefetchPart1Reg × 128 = 64 K)
+    // register-capped expert GEMM CTAs leave free (kExpertMaxReg × 256 + kPrefetchPart1Reg × 128 ≤ 62 K)
     CK(ev_wait(ctx, st, ctx->ev_gemm[prev]));
     k_prefetch<kPrefetchPart1Reg, 8><<<ctx->num_sms, 128, 0, st>>>(d, ctx->at<int32_t>(s.reps[pp]), pp, static_cast<const uint8_t*>(w13_next),
                                      static_cast<const uint8_t*>(w2_next), sym_of(ctx), PROBE_BUF_REP_W13,
@@ -986,6 +1002,20 @@ probe_status probe_debug_prefetch(probe_ctx ctx, int32_t* out, void* stream) {
   CK(cudaStreamWaitEvent(st, ev, 0));
   CK(cudaEventDestroy(ev));
   CK(cudaMemcpyAsync(out, ctx->at<int32_t>(ctx->sl.flags) + 2, 8, cudaMemcpyDeviceToDevice, st));
+  return PROBE_OK;
+}
+
+probe_status probe_debug_flags(probe_ctx ctx, int32_t* out, void* stream) {
+  if (!ctx || !out) return fail(ctx, PROBE_EINVAL, "probe_debug_flags: null argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaEvent_t ev;
+  CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CK(cudaEventRecord(ev, ctx->pf));
+  CK(cudaStreamWaitEvent(st, ev, 0));
+  CK(cudaEventRecord(ev, ctx->aux));
+  CK(cudaStreamWaitEvent(st, ev, 0));
+  CK(cudaEventDestroy(ev));
+  CK(cudaMemcpyAsync(out, ctx->at<int32_t>(ctx->sl.flags), 8 * 4, cudaMemcpyDeviceToDevice, st));
   return PROBE_OK;
 }
 

@@ -43,7 +43,9 @@ def export_handles(tensors: Sequence[torch.Tensor]):
     return out
 
 
-def import_handles(handles, own: Sequence[torch.Tensor] = None):
+def import_handles(handles, opened: List[int] = None):
+    """Map peer allocations; the mapped bases (address − offset) are appended to `opened` so
+    the caller can unmap them (close_handles) when the runtime is closed."""
     lib = _lib.load()
     ptrs = []
     for (h, off) in handles:
@@ -51,7 +53,15 @@ def import_handles(handles, own: Sequence[torch.Tensor] = None):
         p = C.c_uint64(0)
         check("probe_ipc_import", lib.probe_ipc_import(arr, off, C.byref(p)))
         ptrs.append(int(p.value))
+        if opened is not None:
+            opened.append(int(p.value) - int(off))
     return ptrs
+
+
+def close_handles(bases: Sequence[int]):
+    lib = _lib.load()
+    for b in bases:
+        check("probe_ipc_close", lib.probe_ipc_close(C.c_uint64(b)))
 
 
 def exchange(obj, group=None):
@@ -75,12 +85,14 @@ def make_runtime_distributed(cfg: ProbeConfig, device, group=None) -> ProbeRunti
     torch.cuda.synchronize(device)
     mine = export_handles(sym)
     allh = exchange(mine, group)
-    bases = []
+    bases, opened = [], []
     for p in range(world):
         if p == proc:
             bases.append([t.data_ptr() for t in sym])
         else:
-            bases.append(import_handles(allh[p]))
+            bases.append(import_handles(allh[p], opened))
     table = build_peer_table(bases, sizes, cfg.G)
     dist.barrier(group)
-    return ProbeRuntime(cfg, device, peer_tables=table, sym_buffers=sym)
+    rt = ProbeRuntime(cfg, device, peer_tables=table, sym_buffers=sym)
+    rt.on_close(lambda: close_handles(opened))   # unmap the peers' allocations with the context
+    return rt

@@ -171,6 +171,13 @@ class ProbeRuntime:
         v = out.cpu()
         return int(v[0]), int(v[1])
 
+    def flags(self, stream=None):
+        """Device status words (probe_debug_flags): error, suspend, part-1 KiB, part-2 KiB,
+        static-EP fallbacks, ... (8 int32)."""
+        out = torch.zeros(8, dtype=torch.int32, device=self.device)
+        check("probe_debug_flags", self.lib.probe_debug_flags(self.ctx, _ptr(out), _stream(stream)), self.ctx)
+        return [int(v) for v in out.cpu()]
+
     def check(self):
         check("probe_check", self.lib.probe_check(self.ctx), self.ctx)
 
@@ -212,10 +219,17 @@ class ProbeRuntime:
     def launches(self) -> int:
         return int(self.lib.probe_launch_count(self.ctx))
 
+    def on_close(self, fn):
+        """Register a callback run once after the context is finalized (e.g. IPC unmapping)."""
+        self._closers = getattr(self, "_closers", []) + [fn]
+
     def close(self):
         if self.ctx:
             self.lib.probe_finalize(self.ctx)
             self.ctx = C.c_void_p()
+            for fn in getattr(self, "_closers", []):
+                fn()
+            self._closers = []
 
     def __del__(self):
         try:

@@ -275,6 +275,30 @@ def predictor_residual(shape: MoEShape, parity: int, zero: bool = False, device=
     return w1.to(device), w2.to(torch.bfloat16).to(device)
 
 
+def predictor_residual_relabel(shape: MoEShape, parity: int, frac: float = 0.25, device="cpu"):
+    """A residual large enough to CHANGE the predicted top-k sets, with every value exact.
+
+    For a seeded expert set D (|D| = max(2, round(frac·E)), at most h) and the cyclic shift
+    σ on D:  Ŵ1[j, :n_h] = 2·Had[parity·E + D_j] (zeros elsewhere, rows j >= |D| zero) and
+    Ŵ2[σ(D_j), j] = +2^-5, Ŵ2[D_j, j] = -2^-5.  On an encoded token the product Ŵ1 x reads
+    the designed integer coefficient of each D_j exactly (0 or a numerator 17-k..16), so the
+    activation is 0 or a value far from any bf16 rounding boundary, and Ŵ2 a moves the prior
+    coefficient of D_j onto σ(D_j): the predicted set becomes P_t relabelled on D, in
+    multiples of 1/16 (exact in fp32 in any order).  Only random draws and fixed tensor
+    construction here; the expected counts come from the oracle."""
+    E, H, h, n_h = shape.E, shape.H, shape.h, shape.n_h
+    m = min(h, max(2, int(round(frac * E))))
+    D = np.sort(rng(shape.name, parity, "relabel-set", frac).choice(E, size=m, replace=False))
+    sig = np.roll(D, -1)
+    w1 = torch.zeros(h, H, dtype=torch.float32)
+    w1[:m, :n_h] = 2.0 * torch.from_numpy(hadamard_rows(n_h, parity * E + D).astype(np.float32))
+    w2 = torch.zeros(E, h, dtype=torch.float32)
+    j = torch.arange(m)
+    w2[torch.from_numpy(sig), j] = 2.0 ** -5
+    w2[torch.from_numpy(D), j] = -(2.0 ** -5)
+    return w1.to(torch.bfloat16).to(device), w2.to(torch.bfloat16).to(device)
+
+
 @dataclasses.dataclass
 class LayerInputs:
     layer: int
@@ -306,6 +330,45 @@ def dyadic(shape_, *seed_parts, lim=32, scale=2.0 ** -4, device="cpu"):
     r = rng(*seed_parts)
     v = r.integers(-lim, lim + 1, size=shape_).astype(np.float32) * scale
     return torch.from_numpy(v).to(torch.bfloat16).to(device)
+
+
+NATURAL_SCALE = 2.0 ** -6     # x and router entries: integers in [-32, 32] times 2^-6
+
+
+def natural_router(shape: MoEShape, layer: int, step: int = 0, zipf_s: float = 1.2, beta: float = 1.0,
+                   dup_frac: float = 0.125, device="cpu"):
+    """Router W [E,H] bf16 and bias b [E] fp32 of the "natural" generator.
+
+    W on the 5-bit dyadic grid (|i| <= 32, scale 2^-6); a seeded dup_frac of the experts
+    copy the row (and bias) of a lower-id expert, so exact logit ties occur whenever both
+    are in contention (pins the lowest-id rule, R3).  Skew: dyadic bias
+    b_e = round_{2^-4}(beta · log p_{π(e)}) with the Zipf popularity permuted per
+    (step, layer) (hotspot migration).  Logits x·Wᵀ + b are exact in fp32 in any order:
+    products are multiples of 2^-12 and |ℓ| < 2^(log2(H)-2) + 8, inside 24 bits."""
+    E, H = shape.E, shape.H
+    W = dyadic((E, H), shape.name, layer % 2, "natural-router", scale=NATURAL_SCALE).float()
+    perm = rng(shape.name, step, layer, "natural-perm", zipf_s).permutation(E)
+    pop = zipf_popularity(E, zipf_s, perm)
+    b = np.round(beta * np.log(pop) * 16.0) / 16.0
+    r = rng(shape.name, layer % 2, "natural-dups")
+    ndup = int(round(dup_frac * E))
+    dups = r.choice(np.arange(1, E), size=ndup, replace=False)
+    for e in np.sort(dups):
+        src = int(r.integers(0, e))
+        W[e] = W[src]
+        b[e] = b[src]
+    return W.to(torch.bfloat16).to(device), torch.from_numpy(b.astype(np.float32)).to(device)
+
+
+def natural_layer_inputs(shape: MoEShape, step: int, layer: int, ranks: Optional[List[int]] = None,
+                         device="cpu") -> "LayerInputs":
+    """Tokens of the natural generator: x [G,T,H] on the 5-bit dyadic grid (scale 2^-6),
+    i.i.d. per (step, layer, rank); routing is whatever the router and bias make of it
+    (negative and dense logits, exact ties from duplicated router rows)."""
+    ranks = list(range(shape.G)) if ranks is None else ranks
+    xs = [dyadic((shape.T, shape.H), shape.name, step, layer, r, "natural-x", scale=NATURAL_SCALE, device=device)
+          for r in ranks]
+    return LayerInputs(layer, layer % 2, torch.stack(xs), [])
 
 
 def bf16_to_numpy_f64(t: torch.Tensor) -> np.ndarray:

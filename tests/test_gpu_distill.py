@@ -4,7 +4,12 @@ the C-ABI (probe_distill_grad / probe_distill_apply) against the fp64 oracle.
 Tolerances (DESIGN.md §4): teacher logits 1e-5·RMS (bf16 operands, fp32 accumulation);
 student logits 2e-3·RMS (the bf16 activation can round the other way where the GPU's fp32
 SiLU and the oracle's fp64 SiLU straddle a bf16 midpoint); summed CE 1e-3 relative; the
-gradients 2e-2 in norm (q − p and g_z are bf16 GEMM operands, R35); fidelity hit counts
+gradients ELEMENT-WISE: max_ij |∇_gpu − ∇_oracle| <= 2e-2 · RMS(∇_oracle), the layer-output
+criterion.  Derivation: each gradient element is a token sum Σ_t u_t v_t whose operands
+(q − p, g_z) are rounded to bf16 (R35, relative 2^-9 each); the rounding errors are
+independent across t, so the error is ≈ 2^-9·sqrt(Σ_t (u_t v_t)^2), while the element
+itself is a sum of mixed-sign terms of the same size (RMS ≈ sqrt(Σ (u v)^2)): error/RMS ≈
+2^-9 per element, ≈ 1e-2 at the maximum over 10^5 elements; fidelity hit counts
 bit-exact, decided on the GPU's own fp32 logits on both sides (③).
 """
 import math
@@ -80,9 +85,12 @@ def test_distill_grad_parity(name):
     # fidelity counts: same decision precision on both sides (fp32 logits + fp32 bias)
     hits = O.fidelity_counts((sl.cpu() + b.cpu()).numpy(), (tl.cpu() + b.cpu()).numpy(), sh.k)
     assert tuple(int(v) for v in s[1:]) == hits, (s[1:], hits)
-    e1, e2 = _rel(g1.double().cpu().numpy(), o1), _rel(g2.double().cpu().numpy(), o2)
-    print(name, "loss", s[0], loss, "grad rel err", e1, e2, "hits", hits, "N", N)
-    assert e1 <= 2e-2 and e2 <= 2e-2, (e1, e2)
+    G1, G2 = g1.double().cpu().numpy(), g2.double().cpu().numpy()
+    e1, e2 = _rel(G1, o1), _rel(G2, o2)
+    m1 = float(np.abs(G1 - o1).max() / np.sqrt((o1 ** 2).mean()))
+    m2 = float(np.abs(G2 - o2).max() / np.sqrt((o2 ** 2).mean()))
+    print(name, "loss", s[0], loss, "grad rel err", e1, e2, "max elem err / RMS", m1, m2, "hits", hits, "N", N)
+    assert m1 <= 2e-2 and m2 <= 2e-2, (m1, m2)
     rt.close()
 
 

@@ -72,6 +72,19 @@ CASES = {
     "C2-dims-static": CaseCfg(pi.C0.with_(name="c2s", E=16, k=4, H=2880, F=2880, T=64, G=2), zipf_s=1.3,
                               replica_budget=0),
     "C2-dims": CaseCfg(pi.C0.with_(name="c2d", E=16, k=4, H=2880, F=2880, T=64, G=2), zipf_s=1.3),
+    # natural generator: dyadic x / router, negative and dense logits, exact ties
+    # from duplicated router rows, Zipf skew through a dyadic bias
+    "natural-C0": CaseCfg(pi.C0, zipf_s=1.2, gen="natural", residual=False),
+    "natural-mid": CaseCfg(pi.C0.with_(name="natm", E=64, k=8, H=512, F=256, T=300, G=4), zipf_s=1.2,
+                           gen="natural", residual=False),
+    "natural-mid-bf16-out": CaseCfg(pi.C0.with_(name="natb", E=32, k=4, H=768, F=256, T=257, G=4), zipf_s=1.0,
+                                    gen="natural", residual=False, out_fp32=False),
+    # a predictor residual that changes n̂ (exact relabelling), through the product path
+    "relabel-residual-C0": CaseCfg(pi.C0, zipf_s=1.2, residual_kind="relabel"),
+    "relabel-residual-mid": CaseCfg(pi.C0.with_(name="rl", E=32, k=4, H=512, F=256, T=300, G=4), zipf_s=1.2,
+                                    residual_kind="relabel", bias=True),
+    "relabel-residual-epilogue-topk": CaseCfg(pi.C0.with_(name="rle", E=64, k=8, H=512, F=256, T=200, G=4),
+                                              zipf_s=1.3, residual_kind="relabel", fused_epi_topk=True),
     # the layer call runs with T below the context's max_tokens (workspaces sized for 4x more)
     "T-below-capacity": CaseCfg(pi.C0.with_(name="tbc", E=16, k=4, H=256, F=256, T=77, G=4), zipf_s=1.3,
                                 max_tokens=300),
@@ -87,6 +100,8 @@ def test_layer_parity(name):
     print(name, rep)
     if name == "budget0":
         assert rep["replicas"] == 0
+    if case.residual_kind == "relabel":
+        assert rep["residual_changes_nhat"]
 
 
 def test_static_ep_identity_and_plan_independence():

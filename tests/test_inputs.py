@@ -34,3 +34,21 @@ def test_static_ir_calibration_c1_shape():
             loads += np.bincount(S.reshape(-1) // (shape.E // shape.G), minlength=shape.G)
         irs.append(imbalance_ratio(loads))
     assert 1.2 < np.mean(irs) < 2.6
+
+
+def test_natural_generator_logits_exact_with_ties():
+    """Natural generator: logits x·Wᵀ + b exact in fp32 in any summation order
+    (fp32 torch matmul == fp64), negative and dense, with exact ties from duplicated router rows."""
+    import numpy as np
+    import torch
+    import probe_inputs as pi
+    sh = pi.C0.with_(name="nat", E=64, k=8, H=2048, F=64, T=256, G=1)
+    W, b = pi.natural_router(sh, 0, 0, 1.2)
+    x = pi.natural_layer_inputs(sh, 0, 0).x[0]
+    l64 = pi.bf16_to_numpy_f64(x) @ pi.bf16_to_numpy_f64(W).T + b.double().numpy()[None, :]
+    l32 = (x.float() @ W.float().T + b[None, :]).double().numpy()
+    l32r = (x.float().flip(1) @ W.float().flip(1).T + b[None, :]).double().numpy()   # another order
+    assert np.array_equal(l64, l32) and np.array_equal(l64, l32r)
+    assert (l64 < 0).mean() > 0.3
+    srt = np.sort(l64, axis=1)[:, ::-1]
+    assert (srt[:, 0] == srt[:, 1]).any() or (l64[:, :, None] == l64[:, None, :]).sum() > l64.size

@@ -164,3 +164,31 @@ def test_designed_prediction_accuracy_near_paper():
 def test_silu_values():
     assert silu(np.array([0.0]))[0] == 0.0
     assert abs(silu(np.array([1.0]))[0] - 1.0 / (1.0 + math.exp(-1.0))) < 1e-16
+
+
+def test_relabel_residual_moves_predicted_sets_exactly():
+    """probe_inputs.predictor_residual_relabel: Eq. (P) with this residual must predict the
+    designed set P_t relabelled by the cyclic shift σ on the seeded set D, with every logit a
+    multiple of 1/16 (so the GPU's fp32 logits equal the oracle's), and n̂ must differ from the
+    prior-only counts (the residual matters for the plan)."""
+    import probe_inputs as pi
+    from oracle import predictor_logits, topk_ids
+    sh = pi.C0.with_(name="rl", E=32, k=4, H=512, F=64, T=300, G=2)
+    li = pi.layer_inputs(sh, 0, 0, 1.2)
+    W = pi.bf16_to_numpy_f64(pi.router_weight(sh, 1))
+    w1, w2 = pi.predictor_residual_relabel(sh, 1)
+    W1, W2 = pi.bf16_to_numpy_f64(w1), pi.bf16_to_numpy_f64(w2)
+    D = np.nonzero(W2.min(axis=1) < 0)[0]
+    sig = {int(D[i]): int(np.roll(D, -1)[i]) for i in range(len(D))}
+    changed = False
+    for r in range(sh.G):
+        x = pi.bf16_to_numpy_f64(li.x[r])
+        l, a = predictor_logits(x, W, None, W1, W2)
+        assert np.array_equal(l * 16, np.round(l * 16)), "logits off the 1/16 grid"
+        P = li.designs[r].P
+        want = np.sort(np.vectorize(lambda e: sig.get(int(e), int(e)))(P), axis=1)
+        got = np.sort(topk_ids(l, sh.k), axis=1)
+        assert np.array_equal(got, want)
+        prior, _ = predictor_logits(x, W, None, None, None)
+        changed |= not np.array_equal(np.sort(topk_ids(prior, sh.k), axis=1), got)
+    assert changed

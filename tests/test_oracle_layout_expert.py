@@ -143,3 +143,28 @@ def test_integer_cost_is_eq2():
     from oracle.probe_oracle import _c
     for m in [0, 1, 63, 64, 256, 1000]:
         assert _c(m, 256) * 1e9 / 1e15 == pytest.approx(expert_compute_time(m, 1e9, 1e15, 256))
+
+
+def test_moe_outputs_ranks_matches_per_token_brute_force():
+    """The expert-outer loop (moe_outputs_ranks) against a per-(token, slot) brute force
+    written from the definition out_t = Σ_j g_tj · SwiGLU_{ids_tj}(x_t), on sampled tokens."""
+    from oracle import moe_outputs_ranks
+    r = np.random.default_rng(5)
+    G, T, H, F, E, k = 3, 13, 8, 12, 5, 2
+    W13 = {e: r.standard_normal((2 * F, H)) for e in range(E)}
+    W2 = {e: r.standard_normal((H, F)) for e in range(E)}
+    xs = [r.standard_normal((T, H)) for _ in range(G)]
+    ids = [np.stack([r.choice(E, size=k, replace=False) for _ in range(T)]) for _ in range(G)]
+    gs = [r.random((T, k)) for _ in range(G)]
+    toks = [[0, 4, 12], list(range(T)), [7]]
+    outs = moe_outputs_ranks(xs, ids, gs, W13, W2, toks)
+    for s in range(G):
+        for i, t in enumerate(toks[s]):
+            want = np.zeros(H)
+            for j in range(k):
+                e = ids[s][t, j]
+                gg = W13[e][:F] @ xs[s][t]
+                uu = W13[e][F:] @ xs[s][t]
+                want += gs[s][t, j] * (W2[e] @ (gg / (1 + np.exp(-gg)) * uu))
+            assert np.allclose(outs[s][i], want, rtol=1e-12, atol=1e-12)
+        assert np.allclose(outs[s], moe_layer_outputs(xs[s], ids[s], gs[s], W13, W2, toks[s]), rtol=1e-13, atol=1e-13)
