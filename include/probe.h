@@ -80,6 +80,13 @@ typedef struct {
                              or PROBE_FP32 (parity path: x, router, predictor and expert weights fp32,
                              SIMT fp32 GEMMs; north_star's 1e-5·RMS bound).  Selects the element type of
                              every activation/weight pointer below and of the RECV/Y/replica buffers. */
+  int32_t dedup_wire;     /* 0: dispatch ships one row per routed (token, slot) and the combine pulls per-slot Y
+                             rows (D1, D2).  1: the wire format of §8(a) a6/a8 — ONE row per unique
+                             (token, destination rank) plus per-slot metadata; the receiver expands it into the
+                             grouped-GEMM rows locally; the expert rank sums g·y over the token's co-located
+                             slots in fp32 (slot order) and pushes ONE fp16 partial per (token, destination)
+                             back to the source, which sums partials in ascending destination order (R25). */
+  int32_t reserved0;      /* must be 0 */
   int64_t alpha_ps;       /* compute cost per routed pair, picoseconds (F̄/F_peak, R11) */
   int64_t beta_ps;        /* comm cost per remote pair, picoseconds (2·2H/BW_net, Eq. 5, λ=1) */
   int64_t bw_bytes_per_us;/* BW_net for Eq. 6 replica caps */
@@ -97,9 +104,13 @@ enum {
   PROBE_BUF_REP_W2 = 3,  /* symmetric [2*R_b, H, F] act */
   PROBE_BUF_BOARD = 4,   /* symmetric count boards [2 parity][2 kind][G][E] int32 + flags */
   PROBE_BUF_SIGNAL = 5,  /* symmetric signal pad (cross-process barriers) */
-  PROBE_NSYM = 6,
-  PROBE_BUF_SCRATCH = 6, /* private scratch for ALL local ranks of this process */
-  PROBE_NBUF = 7
+  PROBE_BUF_META = 6,    /* symmetric [recv_capacity] int4 per received row (dedup_wire): first row of its
+                            (token, dest) pair, next row of the pair, gate weight, return index */
+  PROBE_BUF_COMB = 7,    /* symmetric [max_tokens, min(k, G), H] fp16 (fp32 when dtype = PROBE_FP32): per
+                            (token, destination) partial sums pushed back by the expert ranks (dedup_wire) */
+  PROBE_NSYM = 8,
+  PROBE_BUF_SCRATCH = 8, /* private scratch for ALL local ranks of this process */
+  PROBE_NBUF = 9
 };
 
 /* Sizes to allocate.  bytes[i] for i < PROBE_NSYM is PER LOGICAL RANK; the
@@ -230,13 +241,15 @@ enum {
   PROBE_PH_SELECT = 1,    /* top-k select + softmax + dispatch ranks (a1) */
   PROBE_PH_COUNTS = 2,    /* chunk scan + actual-count all-gather (a3) */
   PROBE_PH_LAYOUT = 3,    /* materialize plan + layout + GEMM schedules (a5) */
-  PROBE_PH_DISPATCH = 4,  /* token dispatch (a6) */
-  PROBE_PH_WAIT = 5,      /* exposed wait for replica slots (prefetch not hidden, R28) */
-  PROBE_PH_GEMM1 = 6,     /* grouped GEMM1 + SwiGLU epilogue (a7) */
-  PROBE_PH_GEMM2 = 7,     /* grouped GEMM2 (a7) */
-  PROBE_PH_COMBINE = 8,   /* gate-weighted combine (a8) */
-  PROBE_PH_TOTAL = 9,     /* whole forward on the main stream */
-  PROBE_NPHASE = 10
+  PROBE_PH_DISPATCH = 4,  /* token dispatch (a6) incl. the cross-process barrier */
+  PROBE_PH_EXPAND = 5,    /* dedup wire: receiver-side expansion into slot rows (empty otherwise) */
+  PROBE_PH_WAIT = 6,      /* exposed wait for replica slots (prefetch not hidden, R28) */
+  PROBE_PH_GEMM1 = 7,     /* grouped GEMM1 + SwiGLU epilogue (a7) */
+  PROBE_PH_GEMM2 = 8,     /* grouped GEMM2 (a7) */
+  PROBE_PH_COMBINE = 9,   /* gate-weighted combine (a8): per-slot pull, or the expert-side partials (dedup) */
+  PROBE_PH_REDUCE = 10,   /* dedup wire: source-side sum of the partials (empty otherwise) */
+  PROBE_PH_TOTAL = 11,    /* whole forward on the main stream */
+  PROBE_NPHASE = 12
 };
 probe_status probe_profile(probe_ctx ctx, int32_t n);
 probe_status probe_profile_read(probe_ctx ctx, float* ms, int32_t* n_out);

@@ -393,24 +393,29 @@ def moe_layer_outputs(x: np.ndarray, ids: np.ndarray, g: np.ndarray,
 
 def moe_outputs_ranks(xs: List[np.ndarray], ids: List[np.ndarray], gs: List[np.ndarray], W13, W2,
                       tokens: Optional[List[Sequence[int]]] = None) -> List[np.ndarray]:
-    """moe_layer_outputs for every source rank at once, loop over experts outermost, so
-    each expert's weights are read once for all ranks (W13/W2 may decode on access).
-    Same arithmetic: y_{t,j} = swiglu_expert(x_t) with expert ids[t,j], then combine in
-    slot order (R4, R25)."""
+    """moe_layer_outputs for every source rank at once: loop over experts outermost and
+    evaluate each expert once on the rows (token, slot) of ALL ranks routed to it, so its
+    weights are read once (W13/W2 may decode on access).  Same arithmetic: every row of
+    y_{t,j} = swiglu_expert(x_t) with expert ids[t,j] (rows are independent), then combine
+    in slot order (R4, R25)."""
     G = len(xs)
-    toks = [list(range(xs[s].shape[0])) if tokens is None else list(tokens[s]) for s in range(G)]
+    toks = [np.asarray(list(range(xs[s].shape[0])) if tokens is None else list(tokens[s]), dtype=np.int64)
+            for s in range(G)]
     k = ids[0].shape[1]
     H = xs[0].shape[1]
     ys = [np.zeros((len(toks[s]), k, H)) for s in range(G)]
-    sub = [ids[s][np.asarray(toks[s], dtype=np.int64)] for s in range(G)]
+    sub = [ids[s][toks[s]] for s in range(G)]
     experts = sorted(set(int(v) for s in range(G) for v in sub[s].reshape(-1)))
     for e in experts:
-        w13, w2 = W13[e], W2[e]
+        hits = [np.nonzero(sub[s] == e) for s in range(G)]
+        rows = np.concatenate([xs[s][toks[s][hits[s][0]]] for s in range(G)], axis=0)
+        y = swiglu_expert(rows, W13[e], W2[e])
+        o = 0
         for s in range(G):
-            ti, jj = np.nonzero(sub[s] == e)
-            if len(ti):
-                ys[s][ti, jj] = swiglu_expert(xs[s][np.asarray(toks[s])[ti]], w13, w2)
-    return [combine(gs[s][np.asarray(toks[s], dtype=np.int64)], ys[s]) for s in range(G)]
+            ti, jj = hits[s]
+            ys[s][ti, jj] = y[o:o + len(ti)]
+            o += len(ti)
+    return [combine(gs[s][toks[s]], ys[s]) for s in range(G)]
 
 
 # =============================================================================

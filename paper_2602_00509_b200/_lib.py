@@ -11,9 +11,9 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libprobe.so")
 
-PROBE_NSYM = 6
-PROBE_NBUF = 7
-BUF_RECV, BUF_Y, BUF_REP_W13, BUF_REP_W2, BUF_BOARD, BUF_SIGNAL, BUF_SCRATCH = range(7)
+PROBE_NSYM = 8
+PROBE_NBUF = 9
+BUF_RECV, BUF_Y, BUF_REP_W13, BUF_REP_W2, BUF_BOARD, BUF_SIGNAL, BUF_META, BUF_COMB, BUF_SCRATCH = range(9)
 
 STATUS = {0: "PROBE_OK", 1: "PROBE_EINVAL", 2: "PROBE_ESHAPE", 3: "PROBE_EBUDGET", 4: "PROBE_ECAPACITY",
           5: "PROBE_ECUDA", 6: "PROBE_ECOMM", 7: "PROBE_ESTATE"}
@@ -27,8 +27,9 @@ EXPORTS = ["probe_workspace", "probe_init", "probe_moe_forward", "probe_predict"
 OPT_EP_EMULATION, OPT_UNFUSED_TOPK, OPT_FUSED_EPILOGUE_TOPK, OPT_AUX_SMS, OPT_PAIR_GEMM, OPT_FUSED_DISPATCH = 1, 2, 3, 4, 5, 6
 OPT_OVERLAP_DISPATCH = 7
 DTYPES = {"bf16": 0, "fp32": 1}      # probe_config.dtype (PROBE_BF16, PROBE_FP32)
-PROBE_NPHASE = 10
-PHASES = ["gate", "select", "counts", "layout", "dispatch", "wait", "gemm1", "gemm2", "combine", "total"]
+PROBE_NPHASE = 12
+PHASES = ["gate", "select", "counts", "layout", "dispatch", "expand", "wait", "gemm1", "gemm2", "combine", "reduce",
+          "total"]
 
 
 class probe_config(C.Structure):
@@ -36,6 +37,7 @@ class probe_config(C.Structure):
                 ("num_experts", C.c_int32), ("top_k", C.c_int32), ("hidden", C.c_int32), ("ffn", C.c_int32),
                 ("res_hidden", C.c_int32), ("max_tokens", C.c_int32), ("recv_capacity", C.c_int32),
                 ("replica_budget", C.c_int32), ("kmax", C.c_int32), ("n_sat", C.c_int32), ("dtype", C.c_int32),
+                ("dedup_wire", C.c_int32), ("reserved0", C.c_int32),
                 ("alpha_ps", C.c_int64), ("beta_ps", C.c_int64), ("bw_bytes_per_us", C.c_int64),
                 ("expert_bytes", C.c_int64)]
 

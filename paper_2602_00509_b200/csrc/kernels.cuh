@@ -842,6 +842,306 @@ __global__ void __launch_bounds__(256) k_dispatch(Dims d, int T, const uint8_t* 
 }
 
 // =============================================================================
+// a6 dedup wire format (probe_config.dedup_wire, §8(a) a6: "one row per unique (token,
+// dest), plus per-slot metadata"; Eq. 4's λ dedup).  Warp per token as in
+// k_dispatch; within the token, slot j is the HEAD of its (token, dest) pair if no earlier
+// slot has the same destination.  Only heads ship the x row (to the head's receive row);
+// every slot ships a 16-byte meta record to its receive row on the destination:
+//   {first row of the pair, next row of the pair in slot order (or -1), g_{t,j} (fp32 bits),
+//    return index = src · T·KQ + t·KQ + q}
+// q = rank of the destination among the token's distinct destinations (ascending): the
+// expert rank's partial sum for (t, dest) is pushed to COMB[t·KQ + q] of the source, and
+// the source sums q ascending (R25).  The receiver's k_expand copies the head row locally to
+// the pair's other receive rows, so the grouped GEMM sees the usual per-slot layout (R24).
+// =============================================================================
+struct MetaRow {
+  int32_t first, next, gbits, ret;
+};
+
+__device__ __forceinline__ void route_slot(const Dims& d, int T, int gl, int t, int lane, const int32_t* ids,
+                                           const int32_t* pos, const int32_t* cbase, const int32_t* split_cum,
+                                           const int32_t* slot_of, const int32_t* src_off, int32_t* route,
+                                           int32_t* err, int& dd_out, int& row_out) {
+  const int s = d.R0 + gl;
+  const int nchunks = (T + kChunk - 1) / kChunk;
+  const int S = d.EL + kMaxRb;
+  const int k = d.k;
+  const size_t pr = static_cast<size_t>(gl) * T + t;
+  const int e = ids[pr * k + lane];
+  const int p = cbase[(static_cast<size_t>(gl) * nchunks + t / kChunk) * d.E + e] + pos[pr * k + lane];
+  const int* c = &split_cum[(s * d.E + e) * d.G];
+  int dd = 0;
+  while (dd < d.G - 1 && c[dd] <= p) ++dd;
+  const int excl = dd > 0 ? c[dd - 1] : 0;
+  const int sl = slot_of[dd * d.E + e];
+  int row = (sl < 0) ? -1 : src_off[(dd * S + sl) * d.G + s] + (p - excl);
+  if (sl < 0 || row >= d.cap || c[dd] <= p) {
+    atomicOr(err, ERR_RECV_OVERFLOW);
+    row = -1;
+  }
+  route[(pr * k + lane) * 2] = dd;
+  route[(pr * k + lane) * 2 + 1] = row;
+  dd_out = dd;
+  row_out = row;
+}
+
+__global__ void __launch_bounds__(256) k_dispatch_dedup(Dims d, int T, const uint8_t* __restrict__ x, int row_bytes,
+                                                        const int32_t* __restrict__ ids,
+                                                        const int32_t* __restrict__ pos,
+                                                        const int32_t* __restrict__ cbase,
+                                                        const int32_t* __restrict__ split_cum,
+                                                        const int32_t* __restrict__ slot_of,
+                                                        const int32_t* __restrict__ src_off,
+                                                        int32_t* __restrict__ route, const float* __restrict__ gw,
+                                                        Sym sym, int buf_recv, int buf_meta, int KQ, int32_t* err) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= d.GL * T) return;
+  const int gl = warp / T, t = warp % T;
+  const int k = d.k;
+  const size_t pr = static_cast<size_t>(gl) * T + t;
+  int dd = -1, row = -1;
+  if (lane < k) route_slot(d, T, gl, t, lane, ids, pos, cbase, split_cum, slot_of, src_off, route, err, dd, row);
+  const bool valid = lane < k && row >= 0;
+  int first = row, next = -1, head = valid ? 1 : 0;
+  for (int i = 0; i < k; ++i) {
+    const int di = __shfl_sync(0xffffffffu, dd, i);
+    const int ri = __shfl_sync(0xffffffffu, row, i);
+    if (valid && ri >= 0 && di == dd) {
+      if (i < lane && head) { first = ri; head = 0; }
+      if (i > lane && next < 0) next = ri;
+    }
+  }
+  const uint32_t heads = __ballot_sync(0xffffffffu, head != 0);
+  int q = 0;
+  for (uint32_t m = heads; m; m &= m - 1) {
+    const int i = __ffs(m) - 1;
+    const int di = __shfl_sync(0xffffffffu, dd, i);   // heads is warp-uniform: every lane runs this loop
+    if (di < dd) ++q;
+  }
+  uint8_t* dst_row = nullptr;
+  if (valid) {
+    MetaRow mr;
+    mr.first = first;
+    mr.next = next;
+    mr.gbits = __float_as_int(gw[pr * k + lane]);
+    mr.ret = (d.R0 + gl) * (T * KQ) + t * KQ + q;
+    *reinterpret_cast<int4*>(sym.at(buf_meta, d.G, dd) + static_cast<size_t>(row) * sizeof(MetaRow)) =
+        make_int4(mr.first, mr.next, mr.gbits, mr.ret);
+    if (head) dst_row = sym.at(buf_recv, d.G, dd) + static_cast<size_t>(row) * row_bytes;
+  }
+  const uint4* src = reinterpret_cast<const uint4*>(x + pr * row_bytes);
+  const int nv = row_bytes / 16;
+  for (int c0 = 0; c0 < nv; c0 += 32 * 8) {
+    uint4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int c = c0 + u * 32 + lane;
+      if (c < nv) v[u] = __ldg(src + c);
+    }
+    for (uint32_t m = heads; m; m &= m - 1) {
+      const int j = __ffs(m) - 1;
+      uint4* dst = reinterpret_cast<uint4*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(dst_row), j));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = c0 + u * 32 + lane;
+        if (c < nv) dst[c] = v[u];
+      }
+    }
+  }
+}
+
+// rows used on every local destination (Σ of its slot group sizes, clamped to cap) → smem
+__device__ __forceinline__ int used_rows_smem(const Dims& d, const int32_t* group_rows, int* used) {
+  const int S = d.EL + kMaxRb;
+  if (threadIdx.x < d.GL) {
+    int u = 0;
+    for (int j = 0; j < S; ++j) u += group_rows[(d.R0 + threadIdx.x) * S + j];
+    used[threadIdx.x] = min(u, d.cap);
+  }
+  __syncthreads();
+  int tot = 0;
+  for (int g = 0; g < d.GL; ++g) tot += used[g];
+  return tot;
+}
+
+// receiver side of the dedup wire: copy each pair's head row to the pair's other rows (local)
+__global__ void __launch_bounds__(256) k_expand(Dims d, const int32_t* __restrict__ group_rows, Sym sym,
+                                                int buf_meta, int buf_recv, int row_bytes) {
+  __shared__ int used[kMaxG];
+  const int tot = used_rows_smem(d, group_rows, used);
+  const int lane = threadIdx.x & 31;
+  const int nv = row_bytes / 16;
+  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < tot; w += (gridDim.x * blockDim.x) >> 5) {
+    int gl = 0, r = w;
+    while (r >= used[gl]) r -= used[gl++];
+    const int4* meta = reinterpret_cast<const int4*>(sym.at(buf_meta, d.G, d.R0 + gl));
+    uint8_t* recv = sym.at(buf_recv, d.G, d.R0 + gl);
+    const int first = meta[r].x;
+    if (first == r) continue;
+    const uint4* s0 = reinterpret_cast<const uint4*>(recv + static_cast<size_t>(first) * row_bytes);
+    uint4* d0 = reinterpret_cast<uint4*>(recv + static_cast<size_t>(r) * row_bytes);
+    for (int c0 = 0; c0 < nv; c0 += 32 * 8) {
+      uint4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = c0 + u * 32 + lane;
+        if (c < nv) v[u] = s0[c];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = c0 + u * 32 + lane;
+        if (c < nv) d0[c] = v[u];
+      }
+    }
+  }
+}
+
+// =============================================================================
+// a8 combine, dedup wire (R25): on the EXPERT rank, for every (token, dest) pair (its head
+// row), acc = Σ_{slots of the pair, slot order} g · y in fp32, pushed as ONE fp16 (fp32 in
+// the fp32 parity path) row to the source's COMB[t·KQ + q]; the source then sums its
+// partials in ascending destination order (k_combine_reduce).  The first CTA raises the
+// prefetch suspend flag (R27): the combine phase begins here.
+// =============================================================================
+template <bool Y_F32>
+__global__ void __launch_bounds__(256) k_combine_partial(Dims d, int T, const int32_t* __restrict__ group_rows,
+                                                         Sym sym, int buf_meta, int buf_y, int buf_comb, int KQ,
+                                                         volatile int32_t* suspend_flag, int layer) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && suspend_flag) *suspend_flag = layer + 1;
+  __shared__ int used[kMaxG];
+  const int tot = used_rows_smem(d, group_rows, used);
+  const int lane = threadIdx.x & 31;
+  constexpr int ES = Y_F32 ? 4 : 2;
+  const size_t rb = static_cast<size_t>(d.H) * ES;
+  const int nv = d.H / 8;                       // 8 outputs per lane-iteration
+  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < tot; w += (gridDim.x * blockDim.x) >> 5) {
+    int gl = 0, r = w;
+    while (r >= used[gl]) r -= used[gl++];
+    const int4* meta = reinterpret_cast<const int4*>(sym.at(buf_meta, d.G, d.R0 + gl));
+    const uint8_t* y = sym.at(buf_y, d.G, d.R0 + gl);
+    const int4 m0 = meta[r];
+    if (m0.x != r) continue;                     // not the head of its pair
+    int rows[kMaxK];
+    float gs[kMaxK];
+    int n = 0;
+    for (int q = r; q >= 0 && n < kMaxK;) {
+      const int4 m = q == r ? m0 : meta[q];
+      rows[n] = q;
+      gs[n] = __int_as_float(m.z);
+      ++n;
+      q = m.y;
+    }
+    const int per = T * KQ;
+    const int src = m0.w / per, idx = m0.w % per;
+    uint8_t* dst = sym.at(buf_comb, d.G, src) + static_cast<size_t>(idx) * rb;
+    for (int c = lane; c < nv; c += 32) {
+      float a[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = 0.f;
+      for (int j = 0; j < n; ++j) {
+        const uint8_t* yr = y + static_cast<size_t>(rows[j]) * rb;
+        if (Y_F32) {
+          const float4 y0 = reinterpret_cast<const float4*>(yr)[2 * c];
+          const float4 y1 = reinterpret_cast<const float4*>(yr)[2 * c + 1];
+          const float f[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
+#pragma unroll
+          for (int i = 0; i < 8; ++i) a[i] = fmaf(gs[j], f[i], a[i]);
+        } else {
+          const uint4 v = reinterpret_cast<const uint4*>(yr)[c];
+          const uint32_t yw[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&yw[i]));
+            a[2 * i] = fmaf(gs[j], f.x, a[2 * i]);
+            a[2 * i + 1] = fmaf(gs[j], f.y, a[2 * i + 1]);
+          }
+        }
+      }
+      if (Y_F32) {
+        float4* o = reinterpret_cast<float4*>(dst) + 2 * c;
+        o[0] = make_float4(a[0], a[1], a[2], a[3]);
+        o[1] = make_float4(a[4], a[5], a[6], a[7]);
+      } else {
+        uint4 o;
+        __half2 h0 = __floats2half2_rn(a[0], a[1]), h1 = __floats2half2_rn(a[2], a[3]);
+        __half2 h2 = __floats2half2_rn(a[4], a[5]), h3 = __floats2half2_rn(a[6], a[7]);
+        o.x = *reinterpret_cast<uint32_t*>(&h0);
+        o.y = *reinterpret_cast<uint32_t*>(&h1);
+        o.z = *reinterpret_cast<uint32_t*>(&h2);
+        o.w = *reinterpret_cast<uint32_t*>(&h3);
+        reinterpret_cast<uint4*>(dst)[c] = o;
+      }
+    }
+  }
+}
+
+// source side (R25): out[t] = Σ_{q = 0..u_t-1} COMB[t·KQ + q] in fp32 (ascending destination),
+// u_t = the token's number of distinct destinations with a valid receive row.  Block per token.
+template <bool OUT_F32, bool Y_F32>
+__global__ void __launch_bounds__(128) k_combine_reduce(Dims d, int T, const int32_t* __restrict__ route, Sym sym,
+                                                        int buf_comb, int KQ, void* out) {
+  __shared__ int s_u;
+  const int tok = blockIdx.x;                    // gl * T + t
+  const int gl = tok / T, t = tok % T;
+  const int k = d.k;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int dd = -1;
+    if (lane < k && route[(static_cast<size_t>(tok) * k + lane) * 2 + 1] >= 0)
+      dd = route[(static_cast<size_t>(tok) * k + lane) * 2];
+    int head = dd >= 0;
+    for (int i = 0; i < k; ++i) {
+      const int di = __shfl_sync(0xffffffffu, dd, i);
+      if (i < lane && di == dd) head = 0;
+    }
+    const uint32_t hm = __ballot_sync(0xffffffffu, head != 0);
+    if (lane == 0) s_u = __popc(hm);
+  }
+  __syncthreads();
+  const int u = s_u;
+  constexpr int ES = Y_F32 ? 4 : 2;
+  const size_t rb = static_cast<size_t>(d.H) * ES;
+  const uint8_t* base = sym.at(buf_comb, d.G, d.R0 + gl) + (static_cast<size_t>(t) * KQ) * rb;
+  const int nv = d.H / 8;
+  for (int c = threadIdx.x; c < nv; c += blockDim.x) {
+    float a[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = 0.f;
+    for (int q = 0; q < u; ++q) {
+      const uint8_t* pr = base + q * rb;
+      if (Y_F32) {
+        const float4 y0 = reinterpret_cast<const float4*>(pr)[2 * c];
+        const float4 y1 = reinterpret_cast<const float4*>(pr)[2 * c + 1];
+        a[0] += y0.x; a[1] += y0.y; a[2] += y0.z; a[3] += y0.w;
+        a[4] += y1.x; a[5] += y1.y; a[6] += y1.z; a[7] += y1.w;
+      } else {
+        const uint4 v = reinterpret_cast<const uint4*>(pr)[c];
+        const uint32_t yw[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&yw[i]));
+          a[2 * i] += f.x;
+          a[2 * i + 1] += f.y;
+        }
+      }
+    }
+    if (OUT_F32) {
+      float4* o = reinterpret_cast<float4*>(out) + (static_cast<size_t>(tok) * nv + c) * 2;
+      o[0] = make_float4(a[0], a[1], a[2], a[3]);
+      o[1] = make_float4(a[4], a[5], a[6], a[7]);
+    } else {
+      uint4 p;
+      p.x = pack_bf16(a[0], a[1]);
+      p.y = pack_bf16(a[2], a[3]);
+      p.z = pack_bf16(a[4], a[5]);
+      p.w = pack_bf16(a[6], a[7]);
+      reinterpret_cast<uint4*>(out)[static_cast<size_t>(tok) * nv + c] = p;
+    }
+  }
+}
+
+// =============================================================================
 // a6 ∥ a7 overlapped (pull) dispatch, single process: k_dispatch has written only the
 // receive-row → x-row index (gidx); this persistent copy kernel fills the receive buffers
 // in 128-row blocks, in the order the expert GEMM1 claims its tiles, and publishes each

@@ -167,6 +167,10 @@ void sym_sizes(const probe_config& c, uint64_t b[PROBE_NBUF]) {
   b[PROBE_BUF_REP_W2] = al(2 * kMaxRb * H * F * es, 1024);
   b[PROBE_BUF_BOARD] = al(4 * G * E * 4 + 1024, 1024);
   b[PROBE_BUF_SIGNAL] = 4096;
+  // dedup wire (§8(a) a6/a8): per-receive-row meta records and the source-side partial rows
+  const uint64_t KQ = static_cast<uint64_t>(c.top_k < c.ep_size ? c.top_k : c.ep_size);
+  b[PROBE_BUF_META] = c.dedup_wire ? al(cap * 16, 1024) : 1024;
+  b[PROBE_BUF_COMB] = c.dedup_wire ? al(static_cast<uint64_t>(c.max_tokens) * KQ * H * es, 1024) : 1024;
   b[PROBE_BUF_SCRATCH] = scratch_layout(c).total;
 }
 
@@ -478,6 +482,11 @@ static probe_status validate(const probe_config& c) {
   if (c.res_hidden < 0 || c.res_hidden % 8) return fail(nullptr, PROBE_ESHAPE, "res_hidden %d must be a multiple of 8", c.res_hidden);
   if (c.num_experts % 8) return fail(nullptr, PROBE_ESHAPE, "num_experts %d must be a multiple of 8", c.num_experts);
   if (c.max_tokens < 1 || c.recv_capacity < 1) return fail(nullptr, PROBE_EINVAL, "max_tokens/recv_capacity must be >= 1");
+  // the local ranks' RECV / Y copies are one contiguous [local_ranks·cap, H] tensor for the GEMMs'
+  // TMA maps: cap·H·sizeof(act) must be a multiple of the 1024-byte buffer stride (H % 64 == 0)
+  if (c.recv_capacity % 8) return fail(nullptr, PROBE_EINVAL, "recv_capacity %d must be a multiple of 8", c.recv_capacity);
+  if (c.dedup_wire != 0 && c.dedup_wire != 1) return fail(nullptr, PROBE_EINVAL, "dedup_wire %d not in {0, 1}", c.dedup_wire);
+  if (c.reserved0 != 0) return fail(nullptr, PROBE_EINVAL, "reserved0 must be 0");
   if (static_cast<int64_t>(c.local_ranks) * c.recv_capacity > (1ll << 30) ||
       static_cast<int64_t>(c.local_ranks) * c.max_tokens > (1ll << 28))
     return fail(nullptr, PROBE_ECAPACITY, "capacity too large");
@@ -704,22 +713,41 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   CKL();
   MARK(4);
   // a6 dispatch
+  const bool dedup = ctx->cfg.dedup_wire != 0 && !fused && !overlap;
+  const int KQ = d.k < d.G ? d.k : d.G;      // distinct destinations per token, at most
+  const int row_bytes = static_cast<int>(H * esz(ctx->cfg));
   {
     const int warps = d.GL * T;
-    k_dispatch<<<(warps + 7) / 8, 256, 0, st>>>(d, T, static_cast<const uint8_t*>(x), static_cast<int>(H * esz(ctx->cfg)),
-                                                ctx->at<int32_t>(s.ids),
-                                                ctx->at<int32_t>(s.pos), ctx->at<int32_t>(s.cbase),
-                                                lo.split_cum, lo.slot_of, lo.src_off, ctx->at<int32_t>(s.route),
-                                                sym_of(ctx), PROBE_BUF_RECV, err,
-                                                (fused || overlap) ? ctx->at<int32_t>(s.gidx) : nullptr);
+    if (dedup) {
+      k_dispatch_dedup<<<(warps + 7) / 8, 256, 0, st>>>(d, T, static_cast<const uint8_t*>(x), row_bytes,
+                                                       ctx->at<int32_t>(s.ids), ctx->at<int32_t>(s.pos),
+                                                       ctx->at<int32_t>(s.cbase), lo.split_cum, lo.slot_of,
+                                                       lo.src_off, ctx->at<int32_t>(s.route), ctx->at<float>(s.gw),
+                                                       sym_of(ctx), PROBE_BUF_RECV, PROBE_BUF_META, KQ, err);
+    } else {
+      k_dispatch<<<(warps + 7) / 8, 256, 0, st>>>(d, T, static_cast<const uint8_t*>(x), row_bytes,
+                                                  ctx->at<int32_t>(s.ids),
+                                                  ctx->at<int32_t>(s.pos), ctx->at<int32_t>(s.cbase),
+                                                  lo.split_cum, lo.slot_of, lo.src_off, ctx->at<int32_t>(s.route),
+                                                  sym_of(ctx), PROBE_BUF_RECV, err,
+                                                  (fused || overlap) ? ctx->at<int32_t>(s.gidx) : nullptr);
+    }
     CKL();
   }
+  if (!overlap) CK(xbarrier(ctx, BAR_DISPATCH, st));   // every peer's rows have landed in our receive buffers
   MARK(5);
+  if (dedup) {
+    // receiver: expand each (token, dest) wire row into the pair's other slot rows (local HBM)
+    k_expand<<<ctx->num_sms * 4, 256, 0, st>>>(d, lo.group_rows, sym_of(ctx), PROBE_BUF_META, PROBE_BUF_RECV,
+                                               row_bytes);
+    CKL();
+  }
+  MARK(6);
   if (overlap) {
     // slots ready before the copy (nothing may sit between the copy and the dependent GEMM1)
     if (use_plan) CK(ev_wait(ctx, st, ctx->ev_slots[p]));
     const bool serial = ctx->overlap_dispatch == 2;   // analysis: copy, then the capped GEMM1 (no PDL)
-    if (!serial) MARK(6);
+    if (!serial) MARK(7);
     CK(ev_record(ctx, ctx->ev_gemm[p], st));
     k_dispatch_pull<<<ctx->num_sms, 256, 0, st>>>(d, static_cast<const uint8_t*>(x), static_cast<int>(H * 2),
                                                   ctx->at<int32_t>(s.gidx), lo.group_rows, lo.s1,
@@ -727,15 +755,14 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
                                                   static_cast<uint8_t*>(ctx->local_base[PROBE_BUF_RECV]),
                                                   li.nparts > 1 ? 1 : 0);
     CKL();
-    if (serial) MARK(6);
+    if (serial) MARK(7);
     CK(launch_gemm1_overlap(ctx->map_recv, *m13, ctx->map_rw13, ctx->map_recv, lo.s1, d.H, ctx->num_sms, st,
                             !serial));
     ++ctx->launches;
   } else {
-    CK(xbarrier(ctx, BAR_DISPATCH, st));          // every peer's rows have landed in our receive buffers
     // a9 phase lock: the expert GEMMs need this layer's replica slots
     if (use_plan) CK(ev_wait(ctx, st, ctx->ev_slots[p]));
-    MARK(6);
+    MARK(7);
     CK(ev_record(ctx, ctx->ev_gemm[p], st));
   }
   // a7 grouped SwiGLU expert FFN (tcgen05): act = SiLU(X W_gᵀ) ⊙ X W_uᵀ ; Y = act W_dᵀ
@@ -750,17 +777,27 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
                      st));
     ++ctx->launches;
   }
-  MARK(7);
+  MARK(8);
   if (f32) {
     CK(launch_sgemm(ctx, lo.s2, ctx->scratch + s.act, w2, ctx->local_base[PROBE_BUF_REP_W2], d.F, st));
   } else {
     CK(launch_gemm_v(vexp, ctx->map_act, *m2, ctx->map_rw2, ctx->map_y, lo.s2, d.F, ctx->num_sms, st));
   }
   ++ctx->launches;
-  CK(xbarrier(ctx, BAR_Y, st));                 // every expert rank's Y rows are complete
-  MARK(8);
+  if (!dedup) CK(xbarrier(ctx, BAR_Y, st));     // every expert rank's Y rows are complete (the combine pulls)
+  MARK(9);
   // a8 combine (raises the prefetch suspend flag, R27)
-  if (f32 && out_fp32)
+  if (dedup) {
+    // expert side: one fp32 partial per (token, dest) over its co-located slots → the source's COMB (R25)
+    if (f32)
+      k_combine_partial<true><<<ctx->num_sms * 4, 256, 0, st>>>(d, T, lo.group_rows, sym_of(ctx), PROBE_BUF_META,
+                                                                PROBE_BUF_Y, PROBE_BUF_COMB, KQ, suspend, layer);
+    else
+      k_combine_partial<false><<<ctx->num_sms * 4, 256, 0, st>>>(d, T, lo.group_rows, sym_of(ctx), PROBE_BUF_META,
+                                                                 PROBE_BUF_Y, PROBE_BUF_COMB, KQ, suspend, layer);
+    CKL();
+    CK(xbarrier(ctx, BAR_Y, st));               // every expert rank's partials have landed on their sources
+  } else if (f32 && out_fp32)
     k_combine<true, true><<<d.GL * T, 128, 0, st>>>(d, T, ctx->at<float>(s.gw), ctx->at<int32_t>(s.route),
                                                     sym_of(ctx), PROBE_BUF_Y, out, suspend, layer);
   else if (f32)
@@ -773,8 +810,18 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
     k_combine<false><<<d.GL * T, 128, 0, st>>>(d, T, ctx->at<float>(s.gw), ctx->at<int32_t>(s.route), sym_of(ctx),
                                                PROBE_BUF_Y, out, suspend, layer);
   CKL();
+  MARK(10);
+  if (dedup) {
+    // source side: Σ of the token's partials in ascending destination order (R25)
+    const int* rt_ = ctx->at<int32_t>(s.route);
+    if (f32 && out_fp32) k_combine_reduce<true, true><<<d.GL * T, 128, 0, st>>>(d, T, rt_, sym_of(ctx), PROBE_BUF_COMB, KQ, out);
+    else if (f32) k_combine_reduce<false, true><<<d.GL * T, 128, 0, st>>>(d, T, rt_, sym_of(ctx), PROBE_BUF_COMB, KQ, out);
+    else if (out_fp32) k_combine_reduce<true, false><<<d.GL * T, 128, 0, st>>>(d, T, rt_, sym_of(ctx), PROBE_BUF_COMB, KQ, out);
+    else k_combine_reduce<false, false><<<d.GL * T, 128, 0, st>>>(d, T, rt_, sym_of(ctx), PROBE_BUF_COMB, KQ, out);
+    CKL();
+  }
   CK(ev_record(ctx, ctx->ev_comb[p], st));
-  MARK(9);
+  MARK(11);
   if (prof) ++ctx->prof_n;
 #undef MARK
   if (topk_ids) CK(cudaMemcpyAsync(topk_ids, ctx->at<int32_t>(s.ids), GL * T * d.k * 4, cudaMemcpyDeviceToDevice, st));
@@ -1443,8 +1490,11 @@ probe_status probe_profile_read(probe_ctx ctx, float* ms, int32_t* n_out) {
   CK(cudaDeviceSynchronize());
   for (int i = 0; i < ctx->prof_n; ++i) {
     cudaEvent_t* ev = &ctx->prof_ev[static_cast<size_t>(i) * (PROBE_NPHASE + 1)];
-    // phase j spans marks j..j+1; TOTAL spans 0..8
-    const int order[PROBE_NPHASE][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {4, 5}, {5, 6}, {6, 7}, {7, 8}, {8, 9}, {0, 9}};
+    // phase j spans marks j..j+1; TOTAL spans the first to the last mark
+    int order[PROBE_NPHASE][2];
+    for (int j = 0; j + 1 < PROBE_NPHASE; ++j) { order[j][0] = j; order[j][1] = j + 1; }
+    order[PROBE_NPHASE - 1][0] = 0;
+    order[PROBE_NPHASE - 1][1] = PROBE_NPHASE - 1;
     for (int j = 0; j < PROBE_NPHASE; ++j) {
       float t = 0.f;
       CK(cudaEventElapsedTime(&t, ev[order[j][0]], ev[order[j][1]]));

@@ -36,6 +36,7 @@ class ProbeConfig:
     bw_bytes_per_us: int = 770_000
     capacity_factor: float = 0.0   # >0 ⇒ recv_capacity = factor · T·k (rounded up to 128)
     dtype: str = "bf16"            # "bf16" (product path, tcgen05) or "fp32" (parity path, SIMT fp32 GEMMs)
+    dedup_wire: bool = False       # one wire row per unique (token, dest) + R25 partial-sum combine
 
     def __post_init__(self):
         if self.local_ranks == 0:
@@ -50,8 +51,8 @@ class ProbeConfig:
     def to_c(self) -> probe_config:
         return probe_config(self.G, self.rank_begin, self.local_ranks, self.E, self.k, self.H, self.F, self.h,
                             self.T, self.recv_capacity, self.replica_budget, self.kmax, self.n_sat,
-                            _lib.DTYPES[self.dtype], self.alpha_ps, self.beta_ps, self.bw_bytes_per_us,
-                            self.expert_bytes)
+                            _lib.DTYPES[self.dtype], int(self.dedup_wire), 0, self.alpha_ps, self.beta_ps,
+                            self.bw_bytes_per_us, self.expert_bytes)
 
     @property
     def torch_dtype(self):

@@ -42,6 +42,7 @@ class CaseCfg:
     max_tokens: int = 0             # >T: context capacity above the T this layer call runs with
     gen: str = "hadamard"           # "natural": 5-bit dyadic x / router, dyadic Zipf bias, duplicated router rows
     residual_kind: str = "bounded"  # "relabel": exact residual that changes the predicted sets (n̂)
+    dedup_wire: bool = False        # one wire row per unique (token, dest) + R25 partial-sum combine
 
     @property
     def es(self) -> int:
@@ -72,7 +73,7 @@ def run_gpu(case: CaseCfg):
     cfg = ProbeConfig(G=G, E=E, k=k, H=H, F=F, T=max(T, case.max_tokens), h=h if case.residual else 0,
                       replica_budget=case.replica_budget, alpha_ps=case.alpha_ps, beta_ps=case.beta_ps,
                       n_sat=case.n_sat, capacity_factor=case.capacity_factor,
-                      bw_bytes_per_us=case.bw_bytes_per_us, dtype=case.dtype)
+                      bw_bytes_per_us=case.bw_bytes_per_us, dtype=case.dtype, dedup_wire=case.dedup_wire)
     rt = ProbeRuntime(cfg)
     if case.ep_emulation:
         from paper_2602_00509_b200._lib import OPT_EP_EMULATION
@@ -130,7 +131,7 @@ def run_gpu(case: CaseCfg):
     rt.forward(0, L0.x, W[0], b[0], w13[0], w2[0], out[0], use_plan=False, topk_ids=ids[0], topk_w=gw[0])
     if os.environ.get("PROBE_TEST_SYNC_L0"):      # debugging aid: serialise layer 0 before the aux track
         torch.cuda.synchronize()
-    lay0 = debug(rt, cfg, T)
+    lay0 = debug(rt, cfg, T, L0.x)
     # the product path both times: once also returning the logits k_select ranks, once as the bench runs it
     pc_logits = torch.empty(G, E, dtype=torch.int32, device=dev)
     rt.predict(1, L0.x, W[1], b[1], r1, r2, pred_counts=pc_logits, pred_logits=plog)
@@ -138,7 +139,7 @@ def run_gpu(case: CaseCfg):
     rt.plan(1, win, replicas=reps, quota=quota, stats=stats)
     rt.prefetch(1, w13[1], w2[1], phase=0)
     rt.forward(1, L1.x, W[1], b[1], w13[1], w2[1], out[1], use_plan=True, topk_ids=ids[1], topk_w=gw[1])
-    lay1 = debug(rt, cfg, T)
+    lay1 = debug(rt, cfg, T, L1.x)
     rt.check()
     torch.cuda.synchronize()
     res.update(out=[o.float().cpu().numpy() for o in out], ids=[i.cpu().numpy() for i in ids],
@@ -161,7 +162,7 @@ def run_gpu(case: CaseCfg):
     return res, inputs
 
 
-def debug(rt, cfg, T=None):
+def debug(rt, cfg, T=None, x=None):
     G, E, k = cfg.G, cfg.E, cfg.k
     T = cfg.T if T is None else T
     S = E // G + 3
@@ -172,8 +173,27 @@ def debug(rt, cfg, T=None):
     reps = torch.empty(G, 3, dtype=torch.int32, device="cuda")
     rt.debug_layout(counts, split, route, rows, reps)
     torch.cuda.synchronize()
-    return dict(counts=counts.cpu().numpy(), split_cum=split.cpu().numpy(), route=route.cpu().numpy(),
-                group_rows=rows.cpu().numpy(), replicas=reps.cpu().numpy())
+    out = dict(counts=counts.cpu().numpy(), split_cum=split.cpu().numpy(), route=route.cpu().numpy(),
+               group_rows=rows.cpu().numpy(), replicas=reps.cpu().numpy())
+    if x is not None:
+        out["recv_ok"] = recv_rows_match(rt, cfg, x, route)
+    return out
+
+
+def recv_rows_match(rt, cfg, x, route):
+    """Dispatch payload pin (a6): every routed (token, slot) row of every destination's receive
+    buffer equals the source's x row bit for bit (after the dedup expansion when enabled)."""
+    from paper_2602_00509_b200 import _lib
+    G, H, cap = cfg.G, cfg.H, cfg.recv_capacity
+    recv = torch.stack([rt.sym_view(_lib.BUF_RECV, r, x.dtype, (cap, H)) for r in range(G)])
+    dd, rr = route[..., 0].long(), route[..., 1].long()
+    valid = rr >= 0
+    ok = True
+    for s in range(x.shape[0]):                      # per source rank (bounded memory at full size)
+        got = recv[dd[s].clamp(min=0), rr[s].clamp(min=0)]            # [T, k, H]
+        same = (got == x[s][:, None, :]) | (got.isnan() & x[s][:, None, :].isnan())
+        ok &= bool((same | ~valid[s][..., None]).all())
+    return ok
 
 
 def sampled_tokens(case: CaseCfg):
@@ -228,6 +248,13 @@ def group_rows_oracle(lay: O.Layout, G, E):
     return out
 
 
+def half_ulp_bf16(v):
+    """Half a bf16 ulp at |v| (8 significant bits): 2^(floor(log2|v|) - 8); 0 at v = 0."""
+    v = np.asarray(v, dtype=np.float64)
+    m, e = np.frexp(v)                      # v = m·2^e, m in [0.5, 1)  ⇒ floor(log2 v) = e - 1
+    return np.where(v > 0, np.ldexp(1.0, e - 1 - 8), 0.0)
+
+
 def compare(case: CaseCfg, gpu, orc, tol: float = 2e-2):
     """Bit-exact: ids, counts, predicted counts, plan, split, route, group sizes, replica bytes.
     Tolerance: gate weights (1e-6 abs), predictor logits (1e-5 rel), outputs (tol · RMS)."""
@@ -246,14 +273,23 @@ def compare(case: CaseCfg, gpu, orc, tol: float = 2e-2):
             assert np.array_equal(lay["route"][r, :, :, 0], ref["layout"].dest[r]), f"route dest L{L} r{r}"
             assert np.array_equal(lay["route"][r, :, :, 1], ref["layout"].row[r]), f"route row L{L} r{r}"
         assert np.array_equal(lay["group_rows"], group_rows_oracle(ref["layout"], G, E)), f"group rows L{L}"
-        errs = []
+        if "recv_ok" in lay:
+            assert lay["recv_ok"], f"receive rows differ from the dispatched x rows L{L}"
+        errs, excess = [], []
         rms = np.sqrt(np.mean(np.concatenate([o.reshape(-1) for o in ref["out"]]) ** 2))
         toks = orc.get("tokens")
         for r in range(G):
             got = gpu["out"][L][r] if toks is None else gpu["out"][L][r][toks[r]]
-            errs.append(np.abs(got - ref["out"][r]).max())
+            err = np.abs(got - ref["out"][r])
+            errs.append(err.max())
+            # bf16 output = the fp32 result rounded to bf16: each element may additionally be off by
+            # half a bf16 ulp of its value (2^(floor(log2|v|) - 8)); the 2e-2·RMS bound applies to the rest
+            rnd = 0.0 if case.out_fp32 else half_ulp_bf16(np.maximum(np.abs(got), np.abs(ref["out"][r])))
+            excess.append((err - rnd).max())
         report[f"out_err_L{L}"] = float(max(errs) / rms)
-        assert max(errs) <= tol * rms, f"output L{L}: max err {max(errs)} > {tol} * RMS {rms}"
+        if not case.out_fp32:
+            report[f"out_err_beyond_bf16_rounding_L{L}"] = float(max(excess) / rms)
+        assert max(excess) <= tol * rms, f"output L{L}: max err {max(excess)} > {tol} * RMS {rms}"
     assert np.array_equal(gpu["pred_counts"], orc["nhat"]), "predicted counts"
     assert np.array_equal(gpu["pred_counts_logits"], orc["nhat"]), "predicted counts (call returning logits)"
     pl = orc["pred_logits"]

@@ -55,8 +55,8 @@ def test_plan_overflow_falls_back_to_static_ep():
     n = ref1["n"]
     split = O.materialize(n, plan.quota, plan.replicas, G, E)
     planned = [int(split[:, :, r].sum()) for r in range(G)]
-    cap = max(rows)
-    assert planned[hot] > cap, (planned, rows)          # the plan would overflow, static fits exactly
+    cap = (max(rows) + 7) // 8 * 8                       # recv_capacity is a multiple of 8
+    assert planned[hot] > cap, (planned, rows)          # the plan would overflow, static fits
     cfg = ProbeConfig(G=G, E=E, k=SH.k, H=SH.H, F=SH.F, T=SH.T, h=0, recv_capacity=cap)
     rt = ProbeRuntime(cfg)
     out = [torch.empty(G, SH.T, SH.H, device="cuda") for _ in (0, 1)]
@@ -97,7 +97,7 @@ def test_static_overflow_raises_ecapacity():
     G = SH.G
     li0, _, W, w = _inputs(1.5)
     _, rows = _static_rows(li0.x, W[0])
-    cfg = ProbeConfig(G=G, E=SH.E, k=SH.k, H=SH.H, F=SH.F, T=SH.T, h=0, recv_capacity=max(rows) - 1)
+    cfg = ProbeConfig(G=G, E=SH.E, k=SH.k, H=SH.H, F=SH.F, T=SH.T, h=0, recv_capacity=(max(rows) - 1) // 8 * 8)
     rt = ProbeRuntime(cfg)
     out = torch.empty(G, SH.T, SH.H, device="cuda")
     rt.forward(0, li0.x, W[0], None, w[0][0], w[0][1], out)

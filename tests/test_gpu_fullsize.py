@@ -1,11 +1,14 @@
 """GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times
 (8 logical EP ranks on one B200, capacity 4·T·k, planner constants from measured peaks,
-bf16 layer output as the bench writes it).
+fp32 layer output as the bench writes it — R25 "output fp32 for parity").
 
 Routing, counts, predicted counts, plan, split, dispatch route and group sizes are
 compared bit-exactly over ALL tokens; layer outputs within 2e-2·RMS (north_star's bf16
 bound) over >= 4096 tokens per rank at C1 (always including the ragged-tail token) and
-over every token at C2 and C3 (T = 2048).
+over every token at C2 and C3 (T = 2048).  The bf16-output cases bound the error beyond
+the output's own bf16 rounding (half an ulp of each value, up to 2^-8 relative) by the same
+2e-2·RMS: rounding alone reaches ≈1.6e-2·RMS at 10^8 outputs, so a bf16
+output cannot meet 2e-2·RMS against fp64 on its own, whatever computes it.
 """
 import pytest
 
@@ -16,7 +19,7 @@ from paper_2602_00509_b200.costs import cost_model, window_ns
 pytestmark = pytest.mark.gpu
 
 
-def bench_case(shape, zipf_s=1.0, sample=4096, cap=4.0, out_fp32=False, **kw):
+def bench_case(shape, zipf_s=1.0, sample=4096, cap=4.0, out_fp32=True, **kw):
     a, b, n, bw = cost_model(shape.H, shape.F)
     return CaseCfg(shape, zipf_s=zipf_s, alpha_ps=a, beta_ps=b, n_sat=n, bw_bytes_per_us=bw,
                    window_ns=window_ns(shape.H, shape.F, shape.T, shape.k, E=shape.E, G=shape.G), capacity_factor=cap,
@@ -26,11 +29,12 @@ def bench_case(shape, zipf_s=1.0, sample=4096, cap=4.0, out_fp32=False, **kw):
 CASES = {
     "C1-bench": bench_case(pi.C1),
     "C1-s1.5": bench_case(pi.C1, zipf_s=1.5),
-    "C1-fp32-out": bench_case(pi.C1, sample=1024, out_fp32=True),
+    "C1-bf16-out": bench_case(pi.C1, sample=1024, out_fp32=False),
     # a residual that changes n̂ (exact relabelling of the designed prediction)
     "C1-relabel-residual": bench_case(pi.C1, zipf_s=1.2, sample=512, residual_kind="relabel"),
     # natural generator: negative / dense logits and exact ties through the product gate
     "C1-natural-T1024": bench_case(pi.C1.with_(T=1024), zipf_s=1.2, sample=0, gen="natural", residual=False),
+    "C1-dedup-wire": bench_case(pi.C1, sample=1024, dedup_wire=True),
     "C2-decode": bench_case(pi.C2, sample=0),
     "C3-T2048": bench_case(pi.C3.with_(T=2048), sample=0, cap=3.0),
 }

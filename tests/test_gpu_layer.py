@@ -85,6 +85,21 @@ CASES = {
                                     residual_kind="relabel", bias=True),
     "relabel-residual-epilogue-topk": CaseCfg(pi.C0.with_(name="rle", E=64, k=8, H=512, F=256, T=200, G=4),
                                               zipf_s=1.3, residual_kind="relabel", fused_epi_topk=True),
+    # dedup wire (§8(a) a6/a8): one row per unique (token, dest) + receiver expansion; expert-side
+    # fp32 partials per (token, dest) pushed to the source, summed in ascending dest order (R25)
+    "dedup-C0": CaseCfg(pi.C0, zipf_s=1.5, dedup_wire=True),
+    "dedup-G8-E64": CaseCfg(pi.C0.with_(name="dg8", E=64, k=8, H=512, F=384, T=160, G=8), zipf_s=1.0, alpha_ps=5,
+                            beta_ps=1, n_sat=16, dedup_wire=True),
+    "dedup-pair-gemm-bias": CaseCfg(pi.C0.with_(name="dpg", E=16, k=4, H=256, F=256, T=700, G=4), zipf_s=1.3,
+                                    bias=True, dedup_wire=True),
+    "dedup-bf16-out": CaseCfg(pi.C0.with_(name="dbf", E=16, k=4, H=256, F=256, T=96, G=2), out_fp32=False,
+                              dedup_wire=True),
+    "dedup-ragged-HF-ep-emulation": CaseCfg(pi.C0.with_(name="drh", E=32, k=8, H=320, F=320, T=300, G=4),
+                                            zipf_s=1.2, ep_emulation=True, dedup_wire=True),
+    "dedup-k-eq-E": CaseCfg(pi.C0.with_(name="dkE", E=8, k=8, H=256, F=128, T=70, G=2), zipf_s=1.0,
+                            dedup_wire=True),
+    "dedup-natural": CaseCfg(pi.C0.with_(name="dnat", E=64, k=8, H=512, F=256, T=300, G=4), zipf_s=1.2,
+                             gen="natural", residual=False, dedup_wire=True),
     # the layer call runs with T below the context's max_tokens (workspaces sized for 4x more)
     "T-below-capacity": CaseCfg(pi.C0.with_(name="tbc", E=16, k=4, H=256, F=256, T=77, G=4), zipf_s=1.3,
                                 max_tokens=300),
@@ -149,6 +164,8 @@ FP32_CASES = {
     "fp32-G1": CaseCfg(pi.C0.with_(name="g132", E=16, k=4, H=256, F=320, T=300, G=1), zipf_s=1.0, dtype="fp32"),
     "fp32-no-residual-budget0": CaseCfg(pi.C0.with_(name="nr32", E=16, k=2, H=256, F=128, T=64, G=2),
                                         residual=False, replica_budget=0, dtype="fp32"),
+    "fp32-dedup-G8": CaseCfg(pi.C0.with_(name="d832", E=64, k=8, H=512, F=256, T=160, G=8), zipf_s=1.0,
+                             dtype="fp32", dedup_wire=True),
 }
 
 
