@@ -163,6 +163,8 @@ def run_probe(args):
         # the dedup wire format (one row per unique (token, dest), R25 partial combine) on the same
         # inputs: the NVLink-product format, measured here with every "remote" row in local HBM
         result["dedup_wire"] = measure(shape, args, env, light=True, dedup=True)
+        # NEXT-4 predictive pre-dispatch on top of the dedup wire (overlaps the wire with the gate)
+        result["predispatch"] = measure(shape, args, env, light=True, dedup=True, predispatch=True)
     if args.config == "C1" and not args.no_decode:
         # BASELINE.json's metric has two halves: prefill latency (C1, this line's value) and
         # decode tokens/s (C2, GPT-OSS-120B-shaped, batch 256 per rank) — measured in the same run
@@ -176,7 +178,7 @@ def run_probe(args):
     return result
 
 
-def measure(shape, args, env, light=False, dedup=None):
+def measure(shape, args, env, light=False, dedup=None, predispatch=False):
     """Bench one configuration: PROBE (timed, profiled), static EP, and unless `light` the
     EP emulation, e2e, roofline and CPU baseline.  Rank 0 returns the JSON dict (else None)."""
     from paper_2602_00509_b200 import ProbeConfig, ProbeRuntime
@@ -192,7 +194,7 @@ def measure(shape, args, env, light=False, dedup=None):
     cfg = ProbeConfig(G=G, E=shape.E, k=shape.k, H=shape.H, F=shape.F, T=shape.T, h=shape.h, rank_begin=R0,
                       local_ranks=GL, replica_budget=3, kmax=16, n_sat=n_sat, alpha_ps=alpha_ps, beta_ps=beta_ps,
                       bw_bytes_per_us=bw_Bpus, capacity_factor=args.cap if G > 1 else 1.0,
-                      dedup_wire=args.dedup if dedup is None else dedup)
+                      dedup_wire=(args.dedup if dedup is None else dedup) or predispatch, predispatch=predispatch)
     if world > 1:
         from paper_2602_00509_b200.dist import make_runtime_distributed
         rt = make_runtime_distributed(cfg, dev, pg)
@@ -243,6 +245,8 @@ def measure(shape, args, env, light=False, dedup=None):
         rt.forward(L, xx, W[p], None, w13[p], w2[p], out, use_plan=fp)
         if use_plan:
             rt.predict(L + 1, xx, W[q], None, res[q][0], res[q][1])
+            if not args.modeled_window:     # R26: last measured GEMM window of every rank (+ attention)
+                rt.window(win, attention_ns=args.attn_ns, fallback_ns=gemm_ns)
             rt.plan(L + 1, win)
             rt.prefetch(L + 1, w13[q], w2[q], phase=0)
 
@@ -283,15 +287,29 @@ def measure(shape, args, env, light=False, dedup=None):
     # ---- timed region (PROBE)
     launches0 = rt.launches()
     pf0 = rt.prefetch_kib()
+    fl0 = rt.flags()
     with ClockSampler(local) as clk:
         ms, L = timed(args.steps, L)
     launches = rt.launches() - launches0
     pf1 = rt.prefetch_kib()
+    fl1 = rt.flags()
+    pred_disp = None
+    if predispatch:
+        hits, miss = fl1[5] - fl0[5], fl1[6] - fl0[6]
+        pred_disp = {"pairs_predispatched_hit": hits, "pairs_shipped_after_gate": miss,
+                     "hit_rate": hits / max(1, hits + miss),
+                     "note": "(token, dest) pairs whose x row was pushed to the home rank of a predicted expert "
+                             "during the gate (NEXT-4, P:586) vs shipped by the dispatch after the gate"}
     prefetch = {"part1_MB_per_layer": (pf1[0] - pf0[0]) / 1024 / args.steps,
                 "part2_MB_per_layer": (pf1[1] - pf0[1]) / 1024 / args.steps,
                 "note": "replica weights pushed by this process: part 1 beside the expert GEMMs, part 2 after "
                         "the combine (split phase, P:469)"}
     clocks = clk.summary()
+    torch.cuda.synchronize(dev)
+    win_used = [int(v) for v in win.cpu()]
+    caps = [int(min(3, (w * bw_Bpus) // (cfg.expert_bytes * 1000))) for w in win_used]
+    window_rep = {"source": "modeled" if args.modeled_window else "measured (probe_window, R26)",
+                  "window_ns": win_used, "caps": caps, "modeled_ns": gemm_ns, "attention_ns": args.attn_ns}
     # ---- per-phase profile (separate pass; CUDA events on the launching stream)
     rt.profile(args.steps)
     ms_prof, L = timed(args.steps, L)
@@ -408,6 +426,8 @@ def measure(shape, args, env, light=False, dedup=None):
                     main.wait_event(e)
                 rt.forward(L, x_dev[bsel], W[p], None, w13[p], w2[p], o_dev[bsel], use_plan=True)
                 rt.predict(L + 1, x_dev[bsel], W[q], None, res[q][0], res[q][1], stream=auxs)
+                if not args.modeled_window:
+                    rt.window(win, attention_ns=args.attn_ns, fallback_ns=gemm_ns, stream=auxs)
                 rt.plan(L + 1, win, stream=auxs)
                 rt.prefetch(L + 1, w13[q], w2[q], phase=0)
                 e_main, e_aux = torch.cuda.Event(), torch.cuda.Event()
@@ -502,6 +522,7 @@ def measure(shape, args, env, light=False, dedup=None):
                               "ms_per_step": ms_static, "speedup_probe_vs_static": ms_static / ms,
                               "phases_ms": static_phases},
                 "phases_ms": phases, "gpu_launches": launches, "clocks": clocks, "prefetch": prefetch, "wire": wire,
+                "predispatch": pred_disp, "window": window_rep,
                 "balance": {"ir_pre": ir_pre, "ir_post": ir_post, "replicas": nrep,
                             "planner_iterations": stats[0]}}
     if rank == 0:
@@ -539,6 +560,7 @@ def measure(shape, args, env, light=False, dedup=None):
                         "predicted_load_fidelity": load_fidelity},
             "bandwidth": bw_report,
             "wire": wire,
+            "window": window_rep,
             "prefetch": prefetch,
             "setup_s": gen_s,
         }
@@ -725,6 +747,9 @@ def main():
     ap.add_argument("--no-emulation", action="store_true")
     ap.add_argument("--no-decode", action="store_true", help="skip the C2 decode sub-measurement of the C1 line")
     ap.add_argument("--dedup", action="store_true", help="dedup wire format for the headline measurement")
+    ap.add_argument("--modeled-window", action="store_true",
+                    help="plan with the modeled hiding window instead of the measured one (R26)")
+    ap.add_argument("--attn-ns", type=int, default=0, help="attention window added to the measured GEMM window")
     ap.add_argument("--no-dedup-sub", action="store_true", help="skip the dedup-wire sub-measurement")
     ap.add_argument("--ep", type=int, default=0, help="EP size G (default: the config's, 8)")
     ap.add_argument("--fused-dispatch", type=int, default=0, choices=[0, 1, 2],

@@ -86,7 +86,12 @@ typedef struct {
                              grouped-GEMM rows locally; the expert rank sums g·y over the token's co-located
                              slots in fp32 (slot order) and pushes ONE fp16 partial per (token, destination)
                              back to the source, which sums partials in ascending destination order (R25). */
-  int32_t reserved0;      /* must be 0 */
+  int32_t predispatch;    /* NEXT-4 ("pre-dispatch hidden states to high-confidence experts"), needs
+                             dedup_wire = 1: when layer L was predicted (probe_predict(L) + probe_plan(L)),
+                             probe_moe_forward(L) pushes every token's x row to the HOME ranks of its predicted
+                             experts on a side stream WHILE the gate computes the actual routing; the dispatch
+                             then ships payload only for (token, dest) pairs the prediction missed, and the
+                             receiver expands hits from the pre-dispatch buffer.  0 = off. */
   int64_t alpha_ps;       /* compute cost per routed pair, picoseconds (F̄/F_peak, R11) */
   int64_t beta_ps;        /* comm cost per remote pair, picoseconds (2·2H/BW_net, Eq. 5, λ=1) */
   int64_t bw_bytes_per_us;/* BW_net for Eq. 6 replica caps */
@@ -108,9 +113,10 @@ enum {
                             (token, dest) pair, next row of the pair, gate weight, return index */
   PROBE_BUF_COMB = 7,    /* symmetric [max_tokens, min(k, G), H] fp16 (fp32 when dtype = PROBE_FP32): per
                             (token, destination) partial sums pushed back by the expert ranks (dedup_wire) */
-  PROBE_NSYM = 8,
-  PROBE_BUF_SCRATCH = 8, /* private scratch for ALL local ranks of this process */
-  PROBE_NBUF = 9
+  PROBE_BUF_PRE = 8,     /* symmetric [G sources, max_tokens, H] act: pre-dispatched rows (predispatch) */
+  PROBE_NSYM = 9,
+  PROBE_BUF_SCRATCH = 9, /* private scratch for ALL local ranks of this process */
+  PROBE_NBUF = 10
 };
 
 /* Sizes to allocate.  bytes[i] for i < PROBE_NSYM is PER LOGICAL RANK; the
@@ -194,6 +200,16 @@ probe_status probe_debug_layout(probe_ctx ctx, int32_t* counts, int32_t* split, 
  * enqueued on `stream` after the context's prefetch stream work issued so far. */
 probe_status probe_debug_prefetch(probe_ctx ctx, int32_t* out, void* stream);
 
+/* Measured hiding window (R26, "confined within the computation window"):
+ * window_ns[r] (device int64 [G] out) = the most recently measured expert-GEMM phase of rank r
+ * (%globaltimer stamps around GEMM1..GEMM2 of every probe_moe_forward, all-gathered into every
+ * rank's count board, so all ranks plan from identical windows), or fallback_ns where no layer
+ * has been measured yet, plus attention_ns (the attention window that follows, caller-given).
+ * Device to device, no host synchronisation; enqueued on `stream` (NULL = the aux stream, i.e.
+ * before a probe_plan issued without a stream).  One step stale by construction (R26). */
+probe_status probe_window(probe_ctx ctx, int64_t attention_ns, int64_t fallback_ns, int64_t* window_ns,
+                          void* stream);
+
 /* Device status words (device int32 out[8], enqueued on `stream` after the work issued so far
  * on the context's aux and prefetch streams): out[0] error word (bit 0 receive overflow,
  * bit 2 plan, bit 3 fp16 Y range), out[1] prefetch suspend flag, out[2] / out[3] prefetch
@@ -249,7 +265,9 @@ enum {
   PROBE_PH_COMBINE = 9,   /* gate-weighted combine (a8): per-slot pull, or the expert-side partials (dedup) */
   PROBE_PH_REDUCE = 10,   /* dedup wire: source-side sum of the partials (empty otherwise) */
   PROBE_PH_TOTAL = 11,    /* whole forward on the main stream */
-  PROBE_NPHASE = 12
+  PROBE_PH_PREDISPATCH = 12, /* NEXT-4: forward start → pre-dispatch done (side stream; 0 when not used).
+                                Compare with gate + select + counts + layout: the overlap */
+  PROBE_NPHASE = 13
 };
 probe_status probe_profile(probe_ctx ctx, int32_t n);
 probe_status probe_profile_read(probe_ctx ctx, float* ms, int32_t* n_out);

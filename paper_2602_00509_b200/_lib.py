@@ -11,25 +11,25 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libprobe.so")
 
-PROBE_NSYM = 8
-PROBE_NBUF = 9
-BUF_RECV, BUF_Y, BUF_REP_W13, BUF_REP_W2, BUF_BOARD, BUF_SIGNAL, BUF_META, BUF_COMB, BUF_SCRATCH = range(9)
+PROBE_NSYM = 9
+PROBE_NBUF = 10
+BUF_RECV, BUF_Y, BUF_REP_W13, BUF_REP_W2, BUF_BOARD, BUF_SIGNAL, BUF_META, BUF_COMB, BUF_PRE, BUF_SCRATCH = range(10)
 
 STATUS = {0: "PROBE_OK", 1: "PROBE_EINVAL", 2: "PROBE_ESHAPE", 3: "PROBE_EBUDGET", 4: "PROBE_ECAPACITY",
           5: "PROBE_ECUDA", 6: "PROBE_ECOMM", 7: "PROBE_ESTATE"}
 
 # every exported symbol declared in include/probe.h
 EXPORTS = ["probe_workspace", "probe_init", "probe_moe_forward", "probe_predict", "probe_plan",
-           "probe_prefetch", "probe_debug_layout", "probe_debug_prefetch", "probe_debug_flags", "probe_test_gemm", "probe_check", "probe_last_error",
+           "probe_prefetch", "probe_debug_layout", "probe_debug_prefetch", "probe_debug_flags", "probe_window", "probe_test_gemm", "probe_check", "probe_last_error",
            "probe_finalize", "probe_launch_count", "probe_profile", "probe_profile_read", "probe_bench_gemm",
            "probe_ipc_export", "probe_ipc_import", "probe_ipc_close", "probe_set_option",
            "probe_history_update", "probe_distill_grad", "probe_distill_apply"]
 OPT_EP_EMULATION, OPT_UNFUSED_TOPK, OPT_FUSED_EPILOGUE_TOPK, OPT_AUX_SMS, OPT_PAIR_GEMM, OPT_FUSED_DISPATCH = 1, 2, 3, 4, 5, 6
 OPT_OVERLAP_DISPATCH = 7
 DTYPES = {"bf16": 0, "fp32": 1}      # probe_config.dtype (PROBE_BF16, PROBE_FP32)
-PROBE_NPHASE = 12
+PROBE_NPHASE = 13
 PHASES = ["gate", "select", "counts", "layout", "dispatch", "expand", "wait", "gemm1", "gemm2", "combine", "reduce",
-          "total"]
+          "total", "predispatch"]
 
 
 class probe_config(C.Structure):
@@ -37,7 +37,7 @@ class probe_config(C.Structure):
                 ("num_experts", C.c_int32), ("top_k", C.c_int32), ("hidden", C.c_int32), ("ffn", C.c_int32),
                 ("res_hidden", C.c_int32), ("max_tokens", C.c_int32), ("recv_capacity", C.c_int32),
                 ("replica_budget", C.c_int32), ("kmax", C.c_int32), ("n_sat", C.c_int32), ("dtype", C.c_int32),
-                ("dedup_wire", C.c_int32), ("reserved0", C.c_int32),
+                ("dedup_wire", C.c_int32), ("predispatch", C.c_int32),
                 ("alpha_ps", C.c_int64), ("beta_ps", C.c_int64), ("bw_bytes_per_us", C.c_int64),
                 ("expert_bytes", C.c_int64)]
 
@@ -78,6 +78,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "probe_debug_layout": (i32, [vp, vp, vp, vp, vp, vp, vp]),
         "probe_debug_prefetch": (i32, [vp, vp, vp]),
         "probe_debug_flags": (i32, [vp, vp, vp]),
+        "probe_window": (i32, [vp, i64, i64, vp, vp]),
         "probe_test_gemm": (i32, [vp, i64, vp, i64, i32, i32, C.POINTER(C.c_int32), i32, i32, vp, vp]),
         "probe_bench_gemm": (i32, [vp, i64, vp, i64, i32, i32, C.POINTER(C.c_int32), i32, i32, i32, i32,
                                    C.POINTER(C.c_float), vp, vp]),

@@ -161,7 +161,8 @@ __global__ void __launch_bounds__(128) k_select(Dims d, int T, const float* __re
                                                 const float* __restrict__ bias, int32_t* __restrict__ ids,
                                                 float* __restrict__ gw, int32_t* __restrict__ pos,
                                                 int32_t* __restrict__ hist, int32_t* __restrict__ counts,
-                                                float* __restrict__ logits_out = nullptr) {
+                                                float* __restrict__ logits_out = nullptr,
+                                                int32_t* __restrict__ pred_ids = nullptr) {
   __shared__ uint32_t mask[kMaxE * 4];
   __shared__ int32_t scount[kMaxE];
   const int E = d.E;
@@ -234,6 +235,10 @@ __global__ void __launch_bounds__(128) k_select(Dims d, int T, const float* __re
     } else {
 #pragma unroll
       for (int j = 0; j < KK; ++j) atomicAdd(&scount[te[j]], 1);
+      if (pred_ids) {            // predicted sets per token (NEXT-4 pre-dispatch reads them)
+#pragma unroll
+        for (int j = 0; j < KK; ++j) pred_ids[o + j] = te[j];
+      }
     }
   }
   __syncthreads();
@@ -325,6 +330,35 @@ __global__ void k_pred_publish(Dims d, const int32_t* __restrict__ pred_local, S
     const int off = board_off(d, parity, 1) + (d.R0 + gl) * d.E + e;
     const int v = pred_local[gl * d.E + e];
     for (int r = 0; r < d.G; ++r) reinterpret_cast<int32_t*>(sym.at(buf_board, d.G, r))[off] = v;
+  }
+}
+
+// R26 measured hiding window: the expert-GEMM phase of this process's ranks is stamped with
+// %globaltimer (phase 0: start, before GEMM1; phase 1: end, after GEMM2) and its duration is
+// stored for every local rank into EVERY rank's count board (int64 slot after the [2][2][G][E]
+// counts), so every rank plans from the same all-gathered windows (R10).  One thread.
+__device__ __forceinline__ int64_t* window_board(const Dims& d, uint8_t* board) {
+  return reinterpret_cast<int64_t*>(board + static_cast<size_t>(4) * d.G * d.E * 4);
+}
+__global__ void k_window_stamp(Dims d, int64_t* t0, int phase, Sym sym, int buf_board) {
+  const uint64_t now = ptx::globaltimer_ns();
+  if (phase == 0) {
+    *t0 = static_cast<int64_t>(now);
+    return;
+  }
+  const int64_t w = static_cast<int64_t>(now) - *t0;
+  for (int r = 0; r < d.G; ++r) {
+    int64_t* wb = window_board(d, sym.at(buf_board, d.G, r));
+    for (int gl = 0; gl < d.GL; ++gl) wb[d.R0 + gl] = w;
+  }
+}
+// window_ns[r] = measured[r] (or fallback_ns where nothing was measured yet) + attention_ns
+__global__ void k_window_read(Dims d, const uint8_t* board, int64_t attention_ns, int64_t fallback_ns,
+                              int64_t* window_ns) {
+  const int64_t* wb = window_board(d, const_cast<uint8_t*>(board));
+  for (int r = threadIdx.x; r < d.G; r += blockDim.x) {
+    const int64_t m = wb[r];
+    window_ns[r] = (m > 0 ? m : fallback_ns) + attention_ns;
   }
 }
 
@@ -854,6 +888,54 @@ __global__ void __launch_bounds__(256) k_dispatch(Dims d, int T, const uint8_t* 
 // the source sums q ascending (R25).  The receiver's k_expand copies the head row locally to
 // the pair's other receive rows, so the grouped GEMM sees the usual per-slot layout (R24).
 // =============================================================================
+// NEXT-4 pre-dispatch: warp per token; the HOME ranks of the token's predicted experts
+// (bitmask over ranks, identical to the one the dispatch recomputes) receive the x row in their
+// PRE buffer at [source rank][token] while the gate is still computing the actual routing.
+__device__ __forceinline__ uint64_t predicted_home_mask(const Dims& d, const int32_t* pids, size_t pr, int lane) {
+  uint64_t m = 0;
+  if (lane < d.k) m = 1ull << (pids[pr * d.k + lane] / d.EL);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const uint32_t lo = __shfl_xor_sync(0xffffffffu, static_cast<uint32_t>(m), off);
+    const uint32_t hi = __shfl_xor_sync(0xffffffffu, static_cast<uint32_t>(m >> 32), off);
+    m |= (static_cast<uint64_t>(hi) << 32) | lo;
+  }
+  return m;
+}
+
+__global__ void __launch_bounds__(256) k_predispatch(Dims d, int T, int max_T, const uint8_t* __restrict__ x,
+                                                     int row_bytes, const int32_t* __restrict__ pids, Sym sym,
+                                                     int buf_pre) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= d.GL * T) return;
+  const int gl = warp / T, t = warp % T;
+  const size_t pr = static_cast<size_t>(gl) * T + t;
+  const uint64_t mask = predicted_home_mask(d, pids, pr, lane);
+  const size_t off = (static_cast<size_t>(d.R0 + gl) * max_T + t) * row_bytes;
+  const uint4* src = reinterpret_cast<const uint4*>(x + pr * row_bytes);
+  const int nv = row_bytes / 16;
+  for (int c0 = 0; c0 < nv; c0 += 32 * 8) {
+    uint4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int c = c0 + u * 32 + lane;
+      if (c < nv) v[u] = __ldg(src + c);
+    }
+    for (uint64_t m = mask; m; m &= m - 1) {
+      const int r = __ffsll(static_cast<long long>(m)) - 1;
+      uint4* dst = reinterpret_cast<uint4*>(sym.at(buf_pre, d.G, r) + off);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = c0 + u * 32 + lane;
+        if (c < nv) dst[c] = v[u];
+      }
+    }
+  }
+}
+
+constexpr int kMetaPre = 1 << 30;   // MetaRow.first flag: the pair's payload sits in PRE[src][t]
+
 struct MetaRow {
   int32_t first, next, gbits, ret;
 };
@@ -893,7 +975,8 @@ __global__ void __launch_bounds__(256) k_dispatch_dedup(Dims d, int T, const uin
                                                         const int32_t* __restrict__ slot_of,
                                                         const int32_t* __restrict__ src_off,
                                                         int32_t* __restrict__ route, const float* __restrict__ gw,
-                                                        Sym sym, int buf_recv, int buf_meta, int KQ, int32_t* err) {
+                                                        Sym sym, int buf_recv, int buf_meta, int KQ, int32_t* err,
+                                                        const int32_t* __restrict__ pids, int32_t* hit_ctr) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= d.GL * T) return;
@@ -913,6 +996,17 @@ __global__ void __launch_bounds__(256) k_dispatch_dedup(Dims d, int T, const uin
     }
   }
   const uint32_t heads = __ballot_sync(0xffffffffu, head != 0);
+  // NEXT-4: pairs whose destination is the home of a predicted expert were pre-dispatched
+  bool hit = false;
+  if (pids) {
+    const uint64_t pm = predicted_home_mask(d, pids, pr, lane);
+    hit = valid && ((pm >> dd) & 1ull);
+    const uint32_t hh = __ballot_sync(0xffffffffu, hit && head);
+    if (lane == 0 && hit_ctr) {
+      atomicAdd(hit_ctr, __popc(hh));
+      atomicAdd(hit_ctr + 1, __popc(heads & ~hh));
+    }
+  }
   int q = 0;
   for (uint32_t m = heads; m; m &= m - 1) {
     const int i = __ffs(m) - 1;
@@ -922,13 +1016,13 @@ __global__ void __launch_bounds__(256) k_dispatch_dedup(Dims d, int T, const uin
   uint8_t* dst_row = nullptr;
   if (valid) {
     MetaRow mr;
-    mr.first = first;
+    mr.first = first | (hit ? kMetaPre : 0);
     mr.next = next;
     mr.gbits = __float_as_int(gw[pr * k + lane]);
     mr.ret = (d.R0 + gl) * (T * KQ) + t * KQ + q;
     *reinterpret_cast<int4*>(sym.at(buf_meta, d.G, dd) + static_cast<size_t>(row) * sizeof(MetaRow)) =
         make_int4(mr.first, mr.next, mr.gbits, mr.ret);
-    if (head) dst_row = sym.at(buf_recv, d.G, dd) + static_cast<size_t>(row) * row_bytes;
+    if (head && !hit) dst_row = sym.at(buf_recv, d.G, dd) + static_cast<size_t>(row) * row_bytes;
   }
   const uint4* src = reinterpret_cast<const uint4*>(x + pr * row_bytes);
   const int nv = row_bytes / 16;
@@ -942,6 +1036,7 @@ __global__ void __launch_bounds__(256) k_dispatch_dedup(Dims d, int T, const uin
     for (uint32_t m = heads; m; m &= m - 1) {
       const int j = __ffs(m) - 1;
       uint4* dst = reinterpret_cast<uint4*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(dst_row), j));
+      if (!dst) continue;                      // pre-dispatched (hit): the receiver has the row
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int c = c0 + u * 32 + lane;
@@ -967,7 +1062,8 @@ __device__ __forceinline__ int used_rows_smem(const Dims& d, const int32_t* grou
 
 // receiver side of the dedup wire: copy each pair's head row to the pair's other rows (local)
 __global__ void __launch_bounds__(256) k_expand(Dims d, const int32_t* __restrict__ group_rows, Sym sym,
-                                                int buf_meta, int buf_recv, int row_bytes) {
+                                                int buf_meta, int buf_recv, int row_bytes, int T, int KQ,
+                                                int buf_pre, int max_T) {
   __shared__ int used[kMaxG];
   const int tot = used_rows_smem(d, group_rows, used);
   const int lane = threadIdx.x & 31;
@@ -977,9 +1073,19 @@ __global__ void __launch_bounds__(256) k_expand(Dims d, const int32_t* __restric
     while (r >= used[gl]) r -= used[gl++];
     const int4* meta = reinterpret_cast<const int4*>(sym.at(buf_meta, d.G, d.R0 + gl));
     uint8_t* recv = sym.at(buf_recv, d.G, d.R0 + gl);
-    const int first = meta[r].x;
-    if (first == r) continue;
-    const uint4* s0 = reinterpret_cast<const uint4*>(recv + static_cast<size_t>(first) * row_bytes);
+    const int4 m = meta[r];
+    const int first = m.x & ~kMetaPre;
+    const bool pre = (m.x & kMetaPre) != 0;
+    if (first == r && !pre) continue;
+    const uint8_t* srow;
+    if (pre) {   // NEXT-4 hit: the row was pre-dispatched into PRE[src][t] of this rank
+      const int per = T * KQ;
+      const int src = m.w / per, t = (m.w % per) / KQ;
+      srow = sym.at(buf_pre, d.G, d.R0 + gl) + (static_cast<size_t>(src) * max_T + t) * row_bytes;
+    } else {
+      srow = recv + static_cast<size_t>(first) * row_bytes;
+    }
+    const uint4* s0 = reinterpret_cast<const uint4*>(srow);
     uint4* d0 = reinterpret_cast<uint4*>(recv + static_cast<size_t>(r) * row_bytes);
     for (int c0 = 0; c0 < nv; c0 += 32 * 8) {
       uint4 v[8];
@@ -1021,7 +1127,7 @@ __global__ void __launch_bounds__(256) k_combine_partial(Dims d, int T, const in
     const int4* meta = reinterpret_cast<const int4*>(sym.at(buf_meta, d.G, d.R0 + gl));
     const uint8_t* y = sym.at(buf_y, d.G, d.R0 + gl);
     const int4 m0 = meta[r];
-    if (m0.x != r) continue;                     // not the head of its pair
+    if ((m0.x & ~kMetaPre) != r) continue;       // not the head of its pair
     int rows[kMaxK];
     float gs[kMaxK];
     int n = 0;

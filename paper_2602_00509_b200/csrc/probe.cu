@@ -110,9 +110,9 @@ size_t esz(const probe_config& c) { return c.dtype == PROBE_FP32 ? 4 : 2; }
 
 struct Scratch {
   size_t sym, logits, pprior, pres, pact, ids, gw, pos, hist, cbase, route, pred_local;
-  size_t quota[2], reps[2], stats[2], pfctr[2];
+  size_t quota[2], reps[2], stats[2], pfctr[2], pids[2];
   size_t split_cum, slot_of, src_off, group_rows, reps_used;
-  size_t s_g1, s_g2, s_gate, s_p1, s_p2, flags, gidx, ready, act, total;
+  size_t s_g1, s_g2, s_gate, s_p1, s_p2, flags, win_t0, gidx, ready, act, total;
 };
 
 Scratch scratch_layout(const probe_config& c) {
@@ -139,6 +139,7 @@ Scratch scratch_layout(const probe_config& c) {
     s.reps[p] = take(G * kMaxRb * 4);
     s.stats[p] = take(8 * 8);
     s.pfctr[p] = take(16);
+    s.pids[p] = take(c.predispatch ? GL * T * k * 4 : 16);   // predicted top-k sets (NEXT-4)
   }
   s.split_cum = take(G * E * G * 4);
   s.slot_of = take(G * E * 4);
@@ -151,6 +152,7 @@ Scratch scratch_layout(const probe_config& c) {
   s.s_p1 = take(sizeof(GemmSched));
   s.s_p2 = take(sizeof(GemmSched));
   s.flags = take(256);
+  s.win_t0 = take(64);
   s.gidx = take((GL * cap + 512) * 4);     // fused dispatch: receive row → x row (+ tile overhang)
   s.ready = take((GL * cap / 128 + 4) * 4); // overlapped dispatch: per-128-row-block landed flags
   s.act = take(GL * cap * F * esz(c));
@@ -165,12 +167,13 @@ void sym_sizes(const probe_config& c, uint64_t b[PROBE_NBUF]) {
   b[PROBE_BUF_Y] = al(cap * H * es, 1024);   // fp16 (D2) / fp32
   b[PROBE_BUF_REP_W13] = al(2 * kMaxRb * 2 * F * H * es, 1024);
   b[PROBE_BUF_REP_W2] = al(2 * kMaxRb * H * F * es, 1024);
-  b[PROBE_BUF_BOARD] = al(4 * G * E * 4 + 1024, 1024);
+  b[PROBE_BUF_BOARD] = al(4 * G * E * 4 + 1024, 1024);   // + int64 [G] measured windows (R26)
   b[PROBE_BUF_SIGNAL] = 4096;
   // dedup wire (§8(a) a6/a8): per-receive-row meta records and the source-side partial rows
   const uint64_t KQ = static_cast<uint64_t>(c.top_k < c.ep_size ? c.top_k : c.ep_size);
   b[PROBE_BUF_META] = c.dedup_wire ? al(cap * 16, 1024) : 1024;
   b[PROBE_BUF_COMB] = c.dedup_wire ? al(static_cast<uint64_t>(c.max_tokens) * KQ * H * es, 1024) : 1024;
+  b[PROBE_BUF_PRE] = c.predispatch ? al(static_cast<uint64_t>(G) * c.max_tokens * H * es, 1024) : 1024;
   b[PROBE_BUF_SCRATCH] = scratch_layout(c).total;
 }
 
@@ -184,7 +187,9 @@ struct probe_ctx_s {
   std::vector<uint64_t> peer;   // host copy [NSYM][G]
   uint8_t* local_base[PROBE_NSYM];
   uint64_t sym_bytes[PROBE_NBUF];
-  cudaStream_t aux = nullptr, pf = nullptr;
+  cudaStream_t aux = nullptr, pf = nullptr, pd = nullptr;   // pd: NEXT-4 pre-dispatch side stream
+  cudaEvent_t ev_fwd_start = nullptr, ev_pd_done = nullptr;
+  int pred_T[2] = {0, 0};
   cudaEvent_t ev_gate[2], ev_gemm[2], ev_comb[2], ev_pred[2], ev_plan[2], ev_slots[2];
   // CUDA-graph awareness: id of the stream capture each event was last recorded in (0 = eager)
   std::vector<std::pair<cudaEvent_t, unsigned long long>> ev_cap;
@@ -364,12 +369,12 @@ cudaError_t launch_gemm(const CUtensorMap& a, const CUtensorMap& b0, const CUten
 template <bool PRED>
 cudaError_t launch_select(const Dims& d, int T, int nchunks, cudaStream_t st, const float* lg, const float* b,
                           int32_t* ids, float* gw, int32_t* pos, int32_t* hist, int32_t* cnt,
-                          float* lo = nullptr) {
+                          float* lo = nullptr, int32_t* pids = nullptr) {
   const size_t smem = 0;
   dim3 grid(nchunks, d.GL);
 #define SEL(KK)                                                                                         \
   case KK: {                                                                                            \
-    k_select<KK, PRED><<<grid, 128, smem, st>>>(d, T, lg, b, ids, gw, pos, hist, cnt, lo);             \
+    k_select<KK, PRED><<<grid, 128, smem, st>>>(d, T, lg, b, ids, gw, pos, hist, cnt, lo, pids);       \
     break;                                                                                              \
   }
   switch (d.k) {
@@ -436,6 +441,7 @@ enum { BAR_COUNTS = 0, BAR_DISPATCH = 1, BAR_Y = 2, BAR_PRED = 3, BAR_PREFETCH =
 // part-1/part-2 KiB pushed, 4 static-EP fallbacks, kEpochSlot.. cross-process barrier epochs (one per kind)
 constexpr int kEpochSlot = 16;
 constexpr int kFallbackSlot = 4;   // layers whose plan would have overflowed → ran static EP
+constexpr int kHitSlot = 5;        // NEXT-4: (token, dest) pairs pre-dispatched (hit) / shipped after the gate (miss)
 static_assert(kEpochSlot + kSigKinds <= 64, "flags area is 256 bytes");
 
 // fp32 parity path: grouped SIMT GEMM over a device-resident schedule (sgemm_f32.cuh)
@@ -486,7 +492,8 @@ static probe_status validate(const probe_config& c) {
   // TMA maps: cap·H·sizeof(act) must be a multiple of the 1024-byte buffer stride (H % 64 == 0)
   if (c.recv_capacity % 8) return fail(nullptr, PROBE_EINVAL, "recv_capacity %d must be a multiple of 8", c.recv_capacity);
   if (c.dedup_wire != 0 && c.dedup_wire != 1) return fail(nullptr, PROBE_EINVAL, "dedup_wire %d not in {0, 1}", c.dedup_wire);
-  if (c.reserved0 != 0) return fail(nullptr, PROBE_EINVAL, "reserved0 must be 0");
+  if (c.predispatch != 0 && c.predispatch != 1) return fail(nullptr, PROBE_EINVAL, "predispatch %d not in {0, 1}", c.predispatch);
+  if (c.predispatch && !c.dedup_wire) return fail(nullptr, PROBE_EINVAL, "predispatch requires dedup_wire = 1");
   if (static_cast<int64_t>(c.local_ranks) * c.recv_capacity > (1ll << 30) ||
       static_cast<int64_t>(c.local_ranks) * c.max_tokens > (1ll << 28))
     return fail(nullptr, PROBE_ECAPACITY, "capacity too large");
@@ -559,6 +566,9 @@ probe_status probe_init(const probe_config* cfg, const uint64_t* peer_ptrs, void
   if (e == cudaSuccess) e = cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&ctx->aux, cudaStreamNonBlocking, prio_hi);
   if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&ctx->pf, cudaStreamNonBlocking, prio_hi);
+  if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&ctx->pd, cudaStreamNonBlocking, prio_hi);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_fwd_start, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_pd_done, cudaEventDisableTiming);
   for (int p = 0; p < 2 && e == cudaSuccess; ++p) {
     cudaEvent_t* evs[6] = {&ctx->ev_gate[p], &ctx->ev_gemm[p], &ctx->ev_comb[p], &ctx->ev_pred[p], &ctx->ev_plan[p],
                            &ctx->ev_slots[p]};
@@ -622,6 +632,24 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
 #define MARK(ph) \
   if (prof) CK(cudaEventRecord(ctx->pev(ph), st))
   MARK(0);
+  // NEXT-4 pre-dispatch: this layer was predicted, so push every token's x row to the home
+  // ranks of its predicted experts on a side stream while the gate below computes the routing
+  const int row_bytes = static_cast<int>(H * esz(ctx->cfg));
+  const bool predisp = ctx->cfg.predispatch && use_plan && ctx->pred_layer[p] == layer && ctx->pred_T[p] == T &&
+                       ctx->fused_dispatch == 0 && ctx->overlap_dispatch == 0 && !f32;
+  if (predisp) {
+    CK(ev_record(ctx, ctx->ev_fwd_start, st));
+    CK(ev_wait(ctx, ctx->pd, ctx->ev_fwd_start));
+    CK(ev_wait(ctx, ctx->pd, ctx->ev_plan[p]));     // predicted sets of this layer (predict → plan, aux)
+    k_predispatch<<<(static_cast<int>(GL) * T + 7) / 8, 256, 0, ctx->pd>>>(
+        d, T, ctx->cfg.max_tokens, static_cast<const uint8_t*>(x), row_bytes, ctx->at<int32_t>(s.pids[p]),
+        sym_of(ctx), PROBE_BUF_PRE);
+    CKL();
+    if (prof) CK(cudaEventRecord(ctx->pev(PROBE_NPHASE - 1), ctx->pd));
+    CK(ev_record(ctx, ctx->ev_pd_done, ctx->pd));
+  } else if (prof) {
+    CK(cudaEventRecord(ctx->pev(PROBE_NPHASE - 1), st));
+  }
   // a1 gate: logits = x W_rᵀ on tcgen05 with the top-k + softmax fused in the epilogue
   // (fp32 logits never leave TMEM/registers); then per-chunk dispatch ranks.
   // a1 gate: logits = x W_rᵀ on tcgen05 (fp32 logits, HBM-bound) → thread-per-token select
@@ -715,7 +743,6 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   // a6 dispatch
   const bool dedup = ctx->cfg.dedup_wire != 0 && !fused && !overlap;
   const int KQ = d.k < d.G ? d.k : d.G;      // distinct destinations per token, at most
-  const int row_bytes = static_cast<int>(H * esz(ctx->cfg));
   {
     const int warps = d.GL * T;
     if (dedup) {
@@ -723,7 +750,9 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
                                                        ctx->at<int32_t>(s.ids), ctx->at<int32_t>(s.pos),
                                                        ctx->at<int32_t>(s.cbase), lo.split_cum, lo.slot_of,
                                                        lo.src_off, ctx->at<int32_t>(s.route), ctx->at<float>(s.gw),
-                                                       sym_of(ctx), PROBE_BUF_RECV, PROBE_BUF_META, KQ, err);
+                                                       sym_of(ctx), PROBE_BUF_RECV, PROBE_BUF_META, KQ, err,
+                                                       predisp ? ctx->at<int32_t>(s.pids[p]) : nullptr,
+                                                       err + kHitSlot);
     } else {
       k_dispatch<<<(warps + 7) / 8, 256, 0, st>>>(d, T, static_cast<const uint8_t*>(x), row_bytes,
                                                   ctx->at<int32_t>(s.ids),
@@ -734,12 +763,13 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
     }
     CKL();
   }
+  if (predisp) CK(ev_wait(ctx, st, ctx->ev_pd_done));  // pre-dispatched rows complete before the barrier
   if (!overlap) CK(xbarrier(ctx, BAR_DISPATCH, st));   // every peer's rows have landed in our receive buffers
   MARK(5);
   if (dedup) {
     // receiver: expand each (token, dest) wire row into the pair's other slot rows (local HBM)
     k_expand<<<ctx->num_sms * 4, 256, 0, st>>>(d, lo.group_rows, sym_of(ctx), PROBE_BUF_META, PROBE_BUF_RECV,
-                                               row_bytes);
+                                               row_bytes, T, KQ, PROBE_BUF_PRE, ctx->cfg.max_tokens);
     CKL();
   }
   MARK(6);
@@ -767,6 +797,10 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   }
   // a7 grouped SwiGLU expert FFN (tcgen05): act = SiLU(X W_gᵀ) ⊙ X W_uᵀ ; Y = act W_dᵀ
   const int vexp = pair ? V_2CTA_256_6_4 : V_256_4_4_EXP;
+  if (!overlap) {   // R26: the measured hiding window starts with the expert GEMMs
+    k_window_stamp<<<1, 1, 0, st>>>(d, ctx->at<int64_t>(s.win_t0), 0, sym_of(ctx), PROBE_BUF_BOARD);
+    CKL();
+  }
   if (overlap) {
     // GEMM1 already enqueued beside the pull copy
   } else if (f32) {
@@ -784,6 +818,10 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
     CK(launch_gemm_v(vexp, ctx->map_act, *m2, ctx->map_rw2, ctx->map_y, lo.s2, d.F, ctx->num_sms, st));
   }
   ++ctx->launches;
+  if (!overlap) {
+    k_window_stamp<<<1, 1, 0, st>>>(d, ctx->at<int64_t>(s.win_t0), 1, sym_of(ctx), PROBE_BUF_BOARD);
+    CKL();
+  }
   if (!dedup) CK(xbarrier(ctx, BAR_Y, st));     // every expert rank's Y rows are complete (the combine pulls)
   MARK(9);
   // a8 combine (raises the prefetch suspend flag, R27)
@@ -857,7 +895,9 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
   // select kernel writes l̂ = prior + residual + b as it ranks it, so the logits a caller
   // inspects are the ones that produced n̂ (only the debug/unfused path and k > 8 differ).
   const bool fused = d.k <= kTopkMax && d.E <= 256 && !ctx->unfused;
-  const bool epi_topk = ctx->fused_epi_topk && !pred_logits;   // epilogue top-k keeps no logits
+  // epilogue top-k keeps neither logits nor per-token sets (NEXT-4 pre-dispatch needs the sets)
+  const bool epi_topk = ctx->fused_epi_topk && !pred_logits && !ctx->cfg.predispatch;
+  int32_t* pids = ctx->cfg.predispatch ? ctx->at<int32_t>(s.pids[pp]) : nullptr;
   if (f32) {
     // fp32 parity path: prior x·W_{L+1}ᵀ and z = x·Ŵ1ᵀ → a = bf16(SiLU(z)) (R8) in one grouped
     // SIMT launch, residual a·Ŵ2ᵀ, then the warp top-k sums prior + b + residual (Eq. (P))
@@ -925,7 +965,7 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
     ++ctx->launches;
     if (!epi_topk) {
       CK(launch_select<true>(d, T, nchunks, st, ctx->at<float>(s.pprior), b_router_next, nullptr, nullptr, nullptr,
-                             nullptr, ctx->at<int32_t>(s.pred_local), pred_logits));
+                             nullptr, ctx->at<int32_t>(s.pred_local), pred_logits, pids));
       ++ctx->launches;
     }
   } else {
@@ -968,6 +1008,7 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
   }
   CK(ev_record(ctx, ctx->ev_pred[pp], st));
   ctx->pred_layer[pp] = next_layer;
+  ctx->pred_T[pp] = (pids && fused && !f32) ? T : 0;   // per-token sets exist only on the select path
   return PROBE_OK;
 }
 
@@ -1049,6 +1090,16 @@ probe_status probe_debug_prefetch(probe_ctx ctx, int32_t* out, void* stream) {
   CK(cudaStreamWaitEvent(st, ev, 0));
   CK(cudaEventDestroy(ev));
   CK(cudaMemcpyAsync(out, ctx->at<int32_t>(ctx->sl.flags) + 2, 8, cudaMemcpyDeviceToDevice, st));
+  return PROBE_OK;
+}
+
+probe_status probe_window(probe_ctx ctx, int64_t attention_ns, int64_t fallback_ns, int64_t* window_ns,
+                          void* stream) {
+  if (!ctx || !window_ns) return fail(ctx, PROBE_EINVAL, "probe_window: null argument");
+  if (attention_ns < 0 || fallback_ns < 0) return fail(ctx, PROBE_EINVAL, "probe_window: negative time");
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->aux;
+  k_window_read<<<1, 64, 0, st>>>(ctx->d, ctx->local_base[PROBE_BUF_BOARD], attention_ns, fallback_ns, window_ns);
+  CKL();
   return PROBE_OK;
 }
 
@@ -1229,6 +1280,10 @@ probe_status probe_finalize(probe_ctx ctx) {
   }
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
   if (ctx->pf) cudaStreamDestroy(ctx->pf);
+  if (ctx->pd) cudaStreamDestroy(ctx->pd);
+  if (ctx->ev_fwd_start) cudaEventDestroy(ctx->ev_fwd_start);
+  if (ctx->ev_pd_done) cudaEventDestroy(ctx->ev_pd_done);
+  for (auto e : ctx->prof_ev) cudaEventDestroy(e);
   if (ctx->dbuf) cudaFree(ctx->dbuf);
   delete ctx;
   return PROBE_OK;
@@ -1491,10 +1546,13 @@ probe_status probe_profile_read(probe_ctx ctx, float* ms, int32_t* n_out) {
   for (int i = 0; i < ctx->prof_n; ++i) {
     cudaEvent_t* ev = &ctx->prof_ev[static_cast<size_t>(i) * (PROBE_NPHASE + 1)];
     // phase j spans marks j..j+1; TOTAL spans the first to the last mark
+    // marks 0..PROBE_PH_TOTAL on the main stream; the last event = pre-dispatch done (side stream)
     int order[PROBE_NPHASE][2];
-    for (int j = 0; j + 1 < PROBE_NPHASE; ++j) { order[j][0] = j; order[j][1] = j + 1; }
-    order[PROBE_NPHASE - 1][0] = 0;
-    order[PROBE_NPHASE - 1][1] = PROBE_NPHASE - 1;
+    for (int j = 0; j < PROBE_PH_TOTAL; ++j) { order[j][0] = j; order[j][1] = j + 1; }
+    order[PROBE_PH_TOTAL][0] = 0;
+    order[PROBE_PH_TOTAL][1] = PROBE_PH_TOTAL;
+    order[PROBE_PH_PREDISPATCH][0] = 0;
+    order[PROBE_PH_PREDISPATCH][1] = PROBE_PH_PREDISPATCH;
     for (int j = 0; j < PROBE_NPHASE; ++j) {
       float t = 0.f;
       CK(cudaEventElapsedTime(&t, ev[order[j][0]], ev[order[j][1]]));

@@ -37,6 +37,7 @@ class ProbeConfig:
     capacity_factor: float = 0.0   # >0 ⇒ recv_capacity = factor · T·k (rounded up to 128)
     dtype: str = "bf16"            # "bf16" (product path, tcgen05) or "fp32" (parity path, SIMT fp32 GEMMs)
     dedup_wire: bool = False       # one wire row per unique (token, dest) + R25 partial-sum combine
+    predispatch: bool = False      # NEXT-4: pre-dispatch to predicted experts' home ranks during the gate
 
     def __post_init__(self):
         if self.local_ranks == 0:
@@ -51,7 +52,7 @@ class ProbeConfig:
     def to_c(self) -> probe_config:
         return probe_config(self.G, self.rank_begin, self.local_ranks, self.E, self.k, self.H, self.F, self.h,
                             self.T, self.recv_capacity, self.replica_budget, self.kmax, self.n_sat,
-                            _lib.DTYPES[self.dtype], int(self.dedup_wire), 0, self.alpha_ps, self.beta_ps,
+                            _lib.DTYPES[self.dtype], int(self.dedup_wire), int(self.predispatch), self.alpha_ps, self.beta_ps,
                             self.bw_bytes_per_us, self.expert_bytes)
 
     @property
@@ -171,6 +172,12 @@ class ProbeRuntime:
         check("probe_debug_prefetch", self.lib.probe_debug_prefetch(self.ctx, _ptr(out), _stream(stream)), self.ctx)
         v = out.cpu()
         return int(v[0]), int(v[1])
+
+    def window(self, window_ns, attention_ns: int = 0, fallback_ns: int = 0, stream=None):
+        """probe_window (R26): window_ns[G] (device int64) ← measured per-rank GEMM window + attention."""
+        s = None if stream is None else _stream(stream)
+        st = self.lib.probe_window(self.ctx, int(attention_ns), int(fallback_ns), _ptr(window_ns), s)
+        check("probe_window", st, self.ctx)
 
     def flags(self, stream=None):
         """Device status words (probe_debug_flags): error, suspend, part-1 KiB, part-2 KiB,

@@ -43,6 +43,7 @@ class CaseCfg:
     gen: str = "hadamard"           # "natural": 5-bit dyadic x / router, dyadic Zipf bias, duplicated router rows
     residual_kind: str = "bounded"  # "relabel": exact residual that changes the predicted sets (n̂)
     dedup_wire: bool = False        # one wire row per unique (token, dest) + R25 partial-sum combine
+    predispatch: bool = False       # NEXT-4: pre-dispatch to predicted experts' home ranks during the gate
 
     @property
     def es(self) -> int:
@@ -73,7 +74,8 @@ def run_gpu(case: CaseCfg):
     cfg = ProbeConfig(G=G, E=E, k=k, H=H, F=F, T=max(T, case.max_tokens), h=h if case.residual else 0,
                       replica_budget=case.replica_budget, alpha_ps=case.alpha_ps, beta_ps=case.beta_ps,
                       n_sat=case.n_sat, capacity_factor=case.capacity_factor,
-                      bw_bytes_per_us=case.bw_bytes_per_us, dtype=case.dtype, dedup_wire=case.dedup_wire)
+                      bw_bytes_per_us=case.bw_bytes_per_us, dtype=case.dtype,
+                      dedup_wire=case.dedup_wire or case.predispatch, predispatch=case.predispatch)
     rt = ProbeRuntime(cfg)
     if case.ep_emulation:
         from paper_2602_00509_b200._lib import OPT_EP_EMULATION
@@ -140,6 +142,7 @@ def run_gpu(case: CaseCfg):
     rt.prefetch(1, w13[1], w2[1], phase=0)
     rt.forward(1, L1.x, W[1], b[1], w13[1], w2[1], out[1], use_plan=True, topk_ids=ids[1], topk_w=gw[1])
     lay1 = debug(rt, cfg, T, L1.x)
+    res["flags"] = rt.flags()
     rt.check()
     torch.cuda.synchronize()
     res.update(out=[o.float().cpu().numpy() for o in out], ids=[i.cpu().numpy() for i in ids],
@@ -306,5 +309,7 @@ def compare(case: CaseCfg, gpu, orc, tol: float = 2e-2):
     assert all(gpu["slots_ok"]), "replica slot bytes differ from home expert weights"
     report["replicas"] = int((exp_reps >= 0).sum())
     report["residual_changes_nhat"] = bool(orc["residual_changes_nhat"])
+    if case.predispatch:
+        report["predispatch_hits"], report["predispatch_misses"] = gpu["flags"][5], gpu["flags"][6]
     report["iterations"] = plan.iterations
     return report

@@ -35,6 +35,7 @@ CASES = {
     # natural generator: negative / dense logits and exact ties through the product gate
     "C1-natural-T1024": bench_case(pi.C1.with_(T=1024), zipf_s=1.2, sample=0, gen="natural", residual=False),
     "C1-dedup-wire": bench_case(pi.C1, sample=1024, dedup_wire=True),
+    "C1-predispatch": bench_case(pi.C1, sample=1024, predispatch=True),
     "C2-decode": bench_case(pi.C2, sample=0),
     "C3-T2048": bench_case(pi.C3.with_(T=2048), sample=0, cap=3.0),
 }

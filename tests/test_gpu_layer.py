@@ -100,6 +100,15 @@ CASES = {
                             dedup_wire=True),
     "dedup-natural": CaseCfg(pi.C0.with_(name="dnat", E=64, k=8, H=512, F=256, T=300, G=4), zipf_s=1.2,
                              gen="natural", residual=False, dedup_wire=True),
+    # NEXT-4 predictive pre-dispatch: layer 1 rows pushed to the predicted experts' home ranks
+    # during its gate; only missed (token, dest) pairs ship after the gate; hits expand from PRE
+    "predispatch-C0": CaseCfg(pi.C0, zipf_s=1.5, predispatch=True),
+    "predispatch-G8-E64": CaseCfg(pi.C0.with_(name="pd8", E=64, k=8, H=512, F=384, T=160, G=8), zipf_s=1.0,
+                                  alpha_ps=5, beta_ps=1, n_sat=16, predispatch=True),
+    "predispatch-relabel-ragged": CaseCfg(pi.C0.with_(name="pdr", E=32, k=4, H=320, F=320, T=301, G=4), zipf_s=1.2,
+                                          residual_kind="relabel", bias=True, predispatch=True),
+    "predispatch-T-below-capacity": CaseCfg(pi.C0.with_(name="pdt", E=16, k=4, H=256, F=256, T=77, G=4),
+                                            zipf_s=1.3, max_tokens=300, predispatch=True),
     # the layer call runs with T below the context's max_tokens (workspaces sized for 4x more)
     "T-below-capacity": CaseCfg(pi.C0.with_(name="tbc", E=16, k=4, H=256, F=256, T=77, G=4), zipf_s=1.3,
                                 max_tokens=300),
@@ -117,6 +126,8 @@ def test_layer_parity(name):
         assert rep["replicas"] == 0
     if case.residual_kind == "relabel":
         assert rep["residual_changes_nhat"]
+    if case.predispatch:
+        assert rep["predispatch_hits"] > 0 and rep["predispatch_hits"] + rep["predispatch_misses"] > 0
 
 
 def test_static_ep_identity_and_plan_independence():

@@ -1,7 +1,13 @@
-"""GPU: the multi-process EP path for real — two processes on ONE B200, each hosting one
-logical rank (G=2), symmetric buffers shared through CUDA IPC handles exchanged over
-torch.distributed (gloo), cross-process device barriers on the signal pads.  Results are
-compared with the fp64 oracle exactly as in the single-process tests."""
+"""GPU: the multi-process EP path for real — two processes on ONE B200, each hosting a block
+of logical ranks, symmetric buffers shared through CUDA IPC handles exchanged over
+torch.distributed (gloo), cross-process device barriers on the signal pads (epochs in device
+memory).  Results are compared with the fp64 oracle exactly as in the single-process tests.
+
+Cases: G=2 with one rank per process (C0); G=8 with four ranks per process (replicas and
+dispatch rows cross the process boundary) in bf16, in the fp32 parity path, and with the
+dedup wire + NEXT-4 pre-dispatch; and a CUDA-graph case where each process captures one full
+dual-track layer step and replays it three times (cross-process barriers inside the graph).
+"""
 import os
 import socket
 import sys
@@ -14,6 +20,17 @@ import torch.multiprocessing as mp
 pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
+C0 = dict(name="C0", E=8, k=2, H=256, F=512, T=64, G=2)
+G8 = dict(name="mp8", E=64, k=8, H=512, F=256, T=200, G=8)
+CASES = {
+    "C0-1-rank-per-process": dict(shape=C0, zipf=1.5),
+    "G8-4-ranks-per-process": dict(shape=G8, zipf=1.2),
+    "G8-fp32": dict(shape=G8, zipf=1.2, dtype="fp32"),
+    "G8-dedup-predispatch": dict(shape=G8, zipf=1.2, dedup=True),
+    "G8-graph-replay": dict(shape=G8, zipf=1.2, graph=True),
+    "G8-graph-replay-dedup": dict(shape=G8, zipf=1.2, graph=True, dedup=True),
+}
+
 
 def _free_port():
     s = socket.socket()
@@ -23,7 +40,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q, zipf):
+def _worker(rank, world, port, q, spec):
     sys.path.insert(0, os.path.dirname(HERE))
     sys.path.insert(0, HERE)
     import torch.distributed as dist
@@ -35,76 +52,114 @@ def _worker(rank, world, port, q, zipf):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
-    sh = pi.C0
+    sh = pi.MoEShape(**spec["shape"])
+    zipf, dtype, dedup, graph = spec["zipf"], spec.get("dtype", "bf16"), spec.get("dedup", False), spec.get("graph", False)
     G, E, k, H, F, T = sh.G, sh.E, sh.k, sh.H, sh.F, sh.T
-    EL = E // G
-    cfg = ProbeConfig(G=G, E=E, k=k, H=H, F=F, T=T, h=sh.h, rank_begin=rank, local_ranks=1,
-                      replica_budget=3, alpha_ps=1, beta_ps=0, n_sat=0)
+    EL, gl = E // G, G // world
+    R0 = rank * gl
+    ranks = list(range(R0, R0 + gl))
+    cfg = ProbeConfig(G=G, E=E, k=k, H=H, F=F, T=T, h=sh.h, rank_begin=R0, local_ranks=gl, replica_budget=3,
+                      alpha_ps=1, beta_ps=0, n_sat=0, dtype=dtype, dedup_wire=dedup, predispatch=dedup)
     rt = make_runtime_distributed(cfg, dev)
-    L0 = pi.layer_inputs(sh, 0, 0, zipf, ranks=[rank], device=dev)
-    L1 = pi.layer_inputs(sh, 0, 1, zipf, ranks=[rank], device=dev)
+    L = [pi.layer_inputs(sh, 0, i, zipf, ranks=ranks, device=dev) for i in (0, 1)]
     W = [pi.router_weight(sh, p, device=dev) for p in (0, 1)]
     w13, w2 = [], []
     for p in (0, 1):
-        a, b = pi.expert_weights(sh, p, experts=range(rank * EL, (rank + 1) * EL), device=dev)
+        a, b = pi.expert_weights(sh, p, experts=range(R0 * EL, (R0 + gl) * EL), device=dev, dtype=cfg.torch_dtype)
         w13.append(a)
         w2.append(b)
     r1, r2 = pi.predictor_residual(sh, 1, device=dev)
-    out = [torch.empty(1, T, H, device=dev) for _ in (0, 1)]
-    ids = [torch.empty(1, T, k, dtype=torch.int32, device=dev) for _ in (0, 1)]
+    xs = [li.x for li in L]
+    if dtype == "fp32":
+        xs = [x.float() for x in xs]
+        W = [w.float() for w in W]
+        r1, r2 = r1.float(), r2.float()
+    out = [torch.empty(gl, T, H, device=dev) for _ in (0, 1)]
+    ids = [torch.empty(gl, T, k, dtype=torch.int32, device=dev) for _ in (0, 1)]
     reps = torch.empty(G, 3, dtype=torch.int32, device=dev)
     quota = torch.empty(G, E, G, dtype=torch.int32, device=dev)
     pc = torch.empty(G, E, dtype=torch.int32, device=dev)
     win = torch.full((G,), 10 ** 9, dtype=torch.int64, device=dev)
-    rt.forward(0, L0.x, W[0], None, w13[0], w2[0], out[0], topk_ids=ids[0])
-    rt.predict(1, L0.x, W[1], None, r1, r2, pred_counts=pc)
+    rt.forward(0, xs[0], W[0], None, w13[0], w2[0], out[0], topk_ids=ids[0])
+    rt.predict(1, xs[0], W[1], None, r1, r2, pred_counts=pc)
     rt.plan(1, win, replicas=reps, quota=quota)
     rt.prefetch(1, w13[1], w2[1], phase=0)
-    rt.forward(1, L1.x, W[1], None, w13[1], w2[1], out[1], use_plan=True, topk_ids=ids[1])
+    outs1 = []
+    if not graph:
+        rt.forward(1, xs[1], W[1], None, w13[1], w2[1], out[1], use_plan=True, topk_ids=ids[1])
+        outs1.append(out[1].cpu().numpy())
+    else:
+        torch.cuda.synchronize()
+        dist.barrier()
+        s = torch.cuda.Stream()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            rt.forward(1, xs[1], W[1], None, w13[1], w2[1], out[1], use_plan=True, topk_ids=ids[1], stream=s)
+            rt.predict(2, xs[1], W[0], None, r1, r2)
+            rt.plan(2, win)
+            rt.prefetch(2, w13[0], w2[0], phase=0)
+            rt.prefetch(2, phase=1, stream=s)
+        for _ in range(3):
+            out[1].zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            outs1.append(out[1].cpu().numpy())
     rt.check()
     torch.cuda.synchronize()
-    q.put((rank, [o.cpu().numpy() for o in out], [i.cpu().numpy() for i in ids], pc.cpu().numpy(),
-           reps.cpu().numpy(), quota.cpu().numpy()))
+    q.put((rank, out[0].cpu().numpy(), outs1, [i.cpu().numpy() for i in ids], pc.cpu().numpy(), reps.cpu().numpy(),
+           quota.cpu().numpy(), rt.flags()))
     dist.barrier()
     rt.close()
     dist.destroy_process_group()
 
 
-def test_two_processes_one_gpu_ipc():
+@pytest.mark.parametrize("name", list(CASES))
+def test_two_processes_one_gpu_ipc(name):
     sys.path.insert(0, HERE)
-    import oracle as O
     import probe_inputs as pi
     from layer_harness import CaseCfg, run_oracle
-    zipf = 1.5
+    spec = CASES[name]
+    zipf, dtype = spec["zipf"], spec.get("dtype", "bf16")
     world = 2
     port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, q, zipf)) for r in range(world)]
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q, spec)) for r in range(world)]
     for p in ps:
         p.start()
     try:
-        res = sorted([q.get(timeout=240) for _ in range(world)], key=lambda t: t[0])
+        res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda t: t[0])
     finally:
         for p in ps:
             p.join(timeout=60)
             if p.is_alive():
                 p.kill()
     assert all(p.exitcode == 0 for p in ps)
-    sh = pi.C0
-    case = CaseCfg(sh, zipf_s=zipf)
+    sh = pi.MoEShape(**spec["shape"])
+    gl = sh.G // world
+    case = CaseCfg(sh, zipf_s=zipf, dtype=dtype)
+    tdt = torch.float32 if dtype == "fp32" else torch.bfloat16
     inputs = dict(L0=pi.layer_inputs(sh, 0, 0, zipf), L1=pi.layer_inputs(sh, 0, 1, zipf),
                   W=[pi.router_weight(sh, p) for p in (0, 1)], b=[None, None],
-                  w13=[pi.expert_weights(sh, p)[0] for p in (0, 1)], w2=[pi.expert_weights(sh, p)[1] for p in (0, 1)])
+                  w13=[pi.expert_weights(sh, p, dtype=tdt)[0] for p in (0, 1)],
+                  w2=[pi.expert_weights(sh, p, dtype=tdt)[1] for p in (0, 1)])
     inputs["r1"], inputs["r2"] = pi.predictor_residual(sh, 1)
     orc = run_oracle(case, inputs)
     plan = orc["plan"]
     assert any(plan.replicas)
-    for rank, outs, ids, pc, reps, quota in res:
+    # some replica must live on a rank of the OTHER process than its home (cross-process prefetch)
+    assert any(e // (sh.E // sh.G) // gl != r // gl for r in range(sh.G) for e in plan.replicas[r])
+    tol = 1e-5 if dtype == "fp32" else 2e-2
+    for rank, out0, outs1, ids, pc, reps, quota, flags in res:
         assert np.array_equal(pc, orc["nhat"])
         assert np.array_equal(quota, plan.quota)
-        for L in (0, 1):
+        if spec.get("dedup"):
+            assert flags[5] > 0                                 # pre-dispatch hits
+        for L, outs in ((0, [out0]), (1, outs1)):
             ref = orc["ref"][L]
-            assert np.array_equal(ids[L][0], ref["ids"][rank])
             rms = np.sqrt(np.mean(np.concatenate([o.reshape(-1) for o in ref["out"]]) ** 2))
-            assert np.abs(outs[L][0] - ref["out"][rank]).max() <= 2e-2 * rms
+            for li in range(gl):
+                r = rank * gl + li
+                assert np.array_equal(ids[L][li], ref["ids"][r])
+                for o in outs:
+                    assert np.abs(o[li] - ref["out"][r]).max() <= tol * rms, (name, L, r)

@@ -78,3 +78,44 @@ def test_history_hook_feeds_planner():
         exp[g, :len(plan.replicas[g])] = plan.replicas[g]
     assert np.array_equal(reps.cpu().numpy(), exp)
     rt.close()
+
+
+def test_measured_window_feeds_planner():
+    """R26: probe_window returns the last measured expert-GEMM window of every rank (+ attention),
+    device to device; before any forward it returns the fallback; the planner's caps then follow
+    the MEASURED windows (plan bit-exact vs the oracle on the same windows)."""
+    import probe_inputs as pi
+    sh = pi.C0.with_(name="win", E=16, k=2, H=512, F=512, T=512, G=4)
+    from paper_2602_00509_b200 import ProbeConfig, ProbeRuntime
+    wbytes = 6 * sh.H * sh.F
+    bw = 770_000
+    cfg = ProbeConfig(G=sh.G, E=sh.E, k=sh.k, H=sh.H, F=sh.F, T=sh.T, h=sh.h, bw_bytes_per_us=bw)
+    rt = ProbeRuntime(cfg)
+    win = torch.empty(sh.G, dtype=torch.int64, device="cuda")
+    rt.window(win, attention_ns=5, fallback_ns=1234, stream=torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    assert win.cpu().tolist() == [1239] * sh.G                  # nothing measured yet → fallback
+    li = pi.layer_inputs(sh, 0, 0, 1.5, device="cuda")
+    W = pi.router_weight(sh, 0, device="cuda")
+    w13, w2 = pi.expert_weights(sh, 0, device="cuda")
+    out = torch.empty(sh.G, sh.T, sh.H, device="cuda")
+    rt.forward(0, li.x, W, None, w13, w2, out)
+    attn = 3 * wbytes * 1000 // bw // 2                          # ≈ 1.5 replicas' worth of transfer time
+    rt.window(win, attention_ns=attn, fallback_ns=10 ** 12, stream=torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    w = win.cpu().numpy()
+    assert (w > attn).all() and (w < attn + 10 ** 9).all() and len(set(w.tolist())) == 1   # one process: one GEMM
+    nhat = np.zeros((sh.G, sh.E), dtype=np.int32)
+    nhat[:, :4] = 400                                            # rank 0's experts hot everywhere
+    nhat[:, 4:] = 10
+    reps = torch.empty(sh.G, 3, dtype=torch.int32, device="cuda")
+    rt.plan(1, win, pred_counts=torch.from_numpy(nhat).cuda(), replicas=reps)
+    torch.cuda.synchronize()
+    pc = O.PlannerConfig(G=sh.G, E=sh.E, alpha_ps=1, beta_ps=0, bw_bytes_per_us=bw, expert_bytes=wbytes)
+    plan = O.plan_greedy(nhat, w.tolist(), pc)
+    assert plan.caps == O.replica_caps(w.tolist(), pc)
+    exp = np.full((sh.G, 3), -1)
+    for g in range(sh.G):
+        exp[g, :len(plan.replicas[g])] = plan.replicas[g]
+    assert np.array_equal(reps.cpu().numpy(), exp)
+    rt.close()
