@@ -206,6 +206,12 @@ def measure(shape, args, env, light=False, dedup=None, predispatch=False):
     if args.fused_dispatch:
         from paper_2602_00509_b200._lib import OPT_FUSED_DISPATCH
         rt.set_option(OPT_FUSED_DISPATCH, args.fused_dispatch)
+    if args.aux_start:
+        from paper_2602_00509_b200._lib import OPT_AUX_START
+        rt.set_option(OPT_AUX_START, args.aux_start)
+    if args.pred_maxreg:
+        from paper_2602_00509_b200._lib import OPT_PRED_MAXREG
+        rt.set_option(OPT_PRED_MAXREG, args.pred_maxreg)
     if args.overlap is not None:
         from paper_2602_00509_b200._lib import OPT_OVERLAP_DISPATCH
         rt.set_option(OPT_OVERLAP_DISPATCH, args.overlap)
@@ -759,6 +765,8 @@ def main():
     ap.add_argument("--out-bf16", action="store_true", help="bf16 layer output instead of fp32 (the parity-tested default)")
     ap.add_argument("--cap", type=float, default=4.0, help="receive capacity per rank in units of T·k")
     ap.add_argument("--aux-sms", type=int, default=0, help="grid cap of the aux-stream predictor GEMMs (0: #SMs/2)")
+    ap.add_argument("--aux-start", type=int, default=0, help="1: predictor starts after dispatch (not beside it)")
+    ap.add_argument("--pred-maxreg", type=int, default=0, help="192: register-capped predictor GEMMs")
     ap.add_argument("--cpu-tokens", type=int, default=1024, help="oracle expert-FFN sample, tokens per rank")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -342,6 +342,10 @@ enum { PROBE_OPT_EP_EMULATION = 1, PROBE_OPT_UNFUSED_TOPK = 2, PROBE_OPT_FUSED_E
                                        producer warp; 2: 16-byte cp.async by two gather warps (1-CTA
                                        kernel).  Ignored with local_ranks < ep_size.  Default 0: see
                                        DESIGN.md §6 for the measurements */,
+       PROBE_OPT_AUX_START = 8 /* 0 (default): predict(L+1) starts when gate(L) is done, i.e. beside
+                                  dispatch(L); 1: after dispatch(L) (beside the expert GEMMs) */,
+       PROBE_OPT_PRED_MAXREG = 9 /* 0 (default) or 192: register-capped predictor GEMMs so a dispatch CTA
+                                    co-resides on the SMs the aux track holds */,
        PROBE_OPT_OVERLAP_DISPATCH = 7 /* when this process hosts every rank and the expert GEMMs run
                                          on CTA pairs: dispatch writes the receive-row → x-row index,
                                          then a persistent pull-copy kernel fills the receive buffers

@@ -1110,7 +1110,7 @@ __global__ void __launch_bounds__(256) k_expand(Dims d, const int32_t* __restric
 // partials in ascending destination order (k_combine_reduce).  The first CTA raises the
 // prefetch suspend flag (R27): the combine phase begins here.
 // =============================================================================
-template <bool Y_F32>
+template <bool Y_F32, int KC>
 __global__ void __launch_bounds__(256) k_combine_partial(Dims d, int T, const int32_t* __restrict__ group_rows,
                                                          Sym sym, int buf_meta, int buf_y, int buf_comb, int KQ,
                                                          volatile int32_t* suspend_flag, int layer) {
@@ -1119,8 +1119,9 @@ __global__ void __launch_bounds__(256) k_combine_partial(Dims d, int T, const in
   const int tot = used_rows_smem(d, group_rows, used);
   const int lane = threadIdx.x & 31;
   constexpr int ES = Y_F32 ? 4 : 2;
+  constexpr int U = 2;                          // 16-byte chunks per lane in flight per chain row
   const size_t rb = static_cast<size_t>(d.H) * ES;
-  const int nv = d.H / 8;                       // 8 outputs per lane-iteration
+  const int nv = static_cast<int>(rb / 16);     // 16-byte chunks per row
   for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < tot; w += (gridDim.x * blockDim.x) >> 5) {
     int gl = 0, r = w;
     while (r >= used[gl]) r -= used[gl++];
@@ -1128,55 +1129,72 @@ __global__ void __launch_bounds__(256) k_combine_partial(Dims d, int T, const in
     const uint8_t* y = sym.at(buf_y, d.G, d.R0 + gl);
     const int4 m0 = meta[r];
     if ((m0.x & ~kMetaPre) != r) continue;       // not the head of its pair
-    int rows[kMaxK];
-    float gs[kMaxK];
-    int n = 0;
-    for (int q = r; q >= 0 && n < kMaxK;) {
-      const int4 m = q == r ? m0 : meta[q];
-      rows[n] = q;
-      gs[n] = __int_as_float(m.z);
-      ++n;
-      q = m.y;
+    // the pair's rows in slot order (compile-time bound KC: registers, no local memory)
+    const uint4* src[KC];
+    float gs[KC];
+    int q = r;
+    int4 m = m0;
+#pragma unroll
+    for (int j = 0; j < KC; ++j) {
+      src[j] = nullptr;
+      gs[j] = 0.f;
+      if (q >= 0) {
+        if (j > 0) m = meta[q];
+        src[j] = reinterpret_cast<const uint4*>(y + static_cast<size_t>(q) * rb);
+        gs[j] = __int_as_float(m.z);
+        q = m.y;
+      }
     }
     const int per = T * KQ;
-    const int src = m0.w / per, idx = m0.w % per;
-    uint8_t* dst = sym.at(buf_comb, d.G, src) + static_cast<size_t>(idx) * rb;
-    for (int c = lane; c < nv; c += 32) {
-      float a[8];
+    const int srank = m0.w / per, idx = m0.w % per;
+    uint4* dst = reinterpret_cast<uint4*>(sym.at(buf_comb, d.G, srank) + static_cast<size_t>(idx) * rb);
+    for (int c0 = lane; c0 < nv; c0 += 32 * U) {
+      float a[U][8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) a[i] = 0.f;
-      for (int j = 0; j < n; ++j) {
-        const uint8_t* yr = y + static_cast<size_t>(rows[j]) * rb;
-        if (Y_F32) {
-          const float4 y0 = reinterpret_cast<const float4*>(yr)[2 * c];
-          const float4 y1 = reinterpret_cast<const float4*>(yr)[2 * c + 1];
-          const float f[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
+      for (int u = 0; u < U; ++u)
 #pragma unroll
-          for (int i = 0; i < 8; ++i) a[i] = fmaf(gs[j], f[i], a[i]);
-        } else {
-          const uint4 v = reinterpret_cast<const uint4*>(yr)[c];
-          const uint32_t yw[4] = {v.x, v.y, v.z, v.w};
+        for (int i = 0; i < 8; ++i) a[u][i] = 0.f;
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&yw[i]));
-            a[2 * i] = fmaf(gs[j], f.x, a[2 * i]);
-            a[2 * i + 1] = fmaf(gs[j], f.y, a[2 * i + 1]);
+      for (int j = 0; j < KC; ++j) {
+        if (!src[j]) break;
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (c0 + 32 * u < nv) v[u] = src[j][c0 + 32 * u];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (Y_F32) {   // 16 bytes = 4 fp32: columns (c0 + 32u)·4 .. +3
+            a[u][0] = fmaf(gs[j], __uint_as_float(v[u].x), a[u][0]);
+            a[u][1] = fmaf(gs[j], __uint_as_float(v[u].y), a[u][1]);
+            a[u][2] = fmaf(gs[j], __uint_as_float(v[u].z), a[u][2]);
+            a[u][3] = fmaf(gs[j], __uint_as_float(v[u].w), a[u][3]);
+          } else {
+            const uint32_t yw[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&yw[i]));
+              a[u][2 * i] = fmaf(gs[j], f.x, a[u][2 * i]);
+              a[u][2 * i + 1] = fmaf(gs[j], f.y, a[u][2 * i + 1]);
+            }
           }
         }
       }
-      if (Y_F32) {
-        float4* o = reinterpret_cast<float4*>(dst) + 2 * c;
-        o[0] = make_float4(a[0], a[1], a[2], a[3]);
-        o[1] = make_float4(a[4], a[5], a[6], a[7]);
-      } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (c0 + 32 * u >= nv) continue;
         uint4 o;
-        __half2 h0 = __floats2half2_rn(a[0], a[1]), h1 = __floats2half2_rn(a[2], a[3]);
-        __half2 h2 = __floats2half2_rn(a[4], a[5]), h3 = __floats2half2_rn(a[6], a[7]);
-        o.x = *reinterpret_cast<uint32_t*>(&h0);
-        o.y = *reinterpret_cast<uint32_t*>(&h1);
-        o.z = *reinterpret_cast<uint32_t*>(&h2);
-        o.w = *reinterpret_cast<uint32_t*>(&h3);
-        reinterpret_cast<uint4*>(dst)[c] = o;
+        if (Y_F32) {
+          o = make_uint4(__float_as_uint(a[u][0]), __float_as_uint(a[u][1]), __float_as_uint(a[u][2]),
+                         __float_as_uint(a[u][3]));
+        } else {
+          __half2 h0 = __floats2half2_rn(a[u][0], a[u][1]), h1 = __floats2half2_rn(a[u][2], a[u][3]);
+          __half2 h2 = __floats2half2_rn(a[u][4], a[u][5]), h3 = __floats2half2_rn(a[u][6], a[u][7]);
+          o.x = *reinterpret_cast<uint32_t*>(&h0);
+          o.y = *reinterpret_cast<uint32_t*>(&h1);
+          o.z = *reinterpret_cast<uint32_t*>(&h2);
+          o.w = *reinterpret_cast<uint32_t*>(&h3);
+        }
+        dst[c0 + 32 * u] = o;
       }
     }
   }

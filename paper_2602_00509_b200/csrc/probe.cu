@@ -190,7 +190,9 @@ struct probe_ctx_s {
   cudaStream_t aux = nullptr, pf = nullptr, pd = nullptr;   // pd: NEXT-4 pre-dispatch side stream
   cudaEvent_t ev_fwd_start = nullptr, ev_pd_done = nullptr;
   int pred_T[2] = {0, 0};
-  cudaEvent_t ev_gate[2], ev_gemm[2], ev_comb[2], ev_pred[2], ev_plan[2], ev_slots[2];
+  cudaEvent_t ev_gate[2], ev_gemm[2], ev_comb[2], ev_pred[2], ev_plan[2], ev_slots[2], ev_disp[2];
+  int aux_start = 0;     // PROBE_OPT_AUX_START: predictor(L+1) starts after gate(L) (0) or dispatch(L) (1)
+  int pred_maxreg = 0;   // PROBE_OPT_PRED_MAXREG: 192 ⇒ register-capped predictor GEMMs (a dispatch CTA fits beside)
   // CUDA-graph awareness: id of the stream capture each event was last recorded in (0 = eager)
   std::vector<std::pair<cudaEvent_t, unsigned long long>> ev_cap;
   int fwd_layer = -1000, pred_layer[2] = {-1000, -1000}, plan_layer[2] = {-1000, -1000},
@@ -259,7 +261,8 @@ enum GemmVariant { V_128_6_4 = 0, V_256_4_4 = 1, V_256_3_8 = 2, V_128_4_8 = 3, V
                    V_2CTA_256_5_8 = 7 /* CTA pair with 8 epilogue warps */,
                    V_2CTA_256_5_4_NB2 = 8 /* CTA pair, 5 stages, 2 staging slots per epilogue warp */,
                    V_2CTA_256_4_4_NB4 = 9 /* CTA pair, 4 stages, 4 staging slots per epilogue warp */,
-                   V_256_4_4_EXP = 10 /* 1-CTA <256,4,4> register-capped for the expert GEMMs */ };
+                   V_256_4_4_EXP = 10 /* 1-CTA <256,4,4> register-capped for the expert GEMMs */,
+                   V_128_6_4_R192 = 11 /* predictor GEMMs capped at 192 registers: a dispatch CTA fits beside */ };
 
 // Expert GEMMs leave registers for one 128-thread prefetch CTA per SM (a9 part 1 runs beside them):
 // 256 × 224 + 128 × 48 = 62 K.  Splits that fill exactly 64 K (240 + 32, 232 + 48) did not
@@ -351,13 +354,14 @@ cudaError_t launch_gemm_v(int v, const CUtensorMap& a, const CUtensorMap& b0, co
     case V_256_3_4_NB4: return launch_gemm_t<256, 3, 4, 4>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_2CTA_256_6_4: return launch_gemm_2cta<256, 6, 4, 1, kExpertMaxReg>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_256_4_4_EXP: return launch_gemm_t<256, 4, 4, 1, PROBE_EXP1_MAXREG>(a, b0, b1, c, A2, s, K, K2, grid, st);
+    case V_128_6_4_R192: return launch_gemm_t<128, 6, 4, 1, 192>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_2CTA_256_5_8: return launch_gemm_2cta<256, 5, 8>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_2CTA_256_5_4_NB2: return launch_gemm_2cta<256, 5, 4, 2>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_2CTA_256_4_4_NB4: return launch_gemm_2cta<256, 4, 4, 4>(a, b0, b1, c, A2, s, K, K2, grid, st);
   }
   return cudaErrorInvalidValue;
 }
-int variant_bn(int v) { return (v == V_128_6_4 || v == V_128_4_8) ? 128 : 256; }
+int variant_bn(int v) { return (v == V_128_6_4 || v == V_128_4_8 || v == V_128_6_4_R192) ? 128 : 256; }
 int variant_tm(int v) { return (v >= V_2CTA_256_6_4 && v <= V_2CTA_256_4_4_NB4) ? 256 : 128; }
 
 template <int BN>
@@ -570,8 +574,8 @@ probe_status probe_init(const probe_config* cfg, const uint64_t* peer_ptrs, void
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_fwd_start, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_pd_done, cudaEventDisableTiming);
   for (int p = 0; p < 2 && e == cudaSuccess; ++p) {
-    cudaEvent_t* evs[6] = {&ctx->ev_gate[p], &ctx->ev_gemm[p], &ctx->ev_comb[p], &ctx->ev_pred[p], &ctx->ev_plan[p],
-                           &ctx->ev_slots[p]};
+    cudaEvent_t* evs[7] = {&ctx->ev_gate[p], &ctx->ev_gemm[p], &ctx->ev_comb[p], &ctx->ev_pred[p], &ctx->ev_plan[p],
+                           &ctx->ev_slots[p], &ctx->ev_disp[p]};
     for (auto* ev : evs)
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
   }
@@ -763,6 +767,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
     }
     CKL();
   }
+  CK(ev_record(ctx, ctx->ev_disp[p], st));
   if (predisp) CK(ev_wait(ctx, st, ctx->ev_pd_done));  // pre-dispatched rows complete before the barrier
   if (!overlap) CK(xbarrier(ctx, BAR_DISPATCH, st));   // every peer's rows have landed in our receive buffers
   MARK(5);
@@ -827,12 +832,14 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   // a8 combine (raises the prefetch suspend flag, R27)
   if (dedup) {
     // expert side: one fp32 partial per (token, dest) over its co-located slots → the source's COMB (R25)
-    if (f32)
-      k_combine_partial<true><<<ctx->num_sms * 4, 256, 0, st>>>(d, T, lo.group_rows, sym_of(ctx), PROBE_BUF_META,
-                                                                PROBE_BUF_Y, PROBE_BUF_COMB, KQ, suspend, layer);
-    else
-      k_combine_partial<false><<<ctx->num_sms * 4, 256, 0, st>>>(d, T, lo.group_rows, sym_of(ctx), PROBE_BUF_META,
-                                                                 PROBE_BUF_Y, PROBE_BUF_COMB, KQ, suspend, layer);
+#define PARTIAL(YF, KC)                                                                                      \
+  k_combine_partial<YF, KC><<<ctx->num_sms * 4, 256, 0, st>>>(d, T, lo.group_rows, sym_of(ctx), PROBE_BUF_META, \
+                                                              PROBE_BUF_Y, PROBE_BUF_COMB, KQ, suspend, layer)
+    if (f32 && d.k <= 8) PARTIAL(true, 8);
+    else if (f32) PARTIAL(true, kMaxK);
+    else if (d.k <= 8) PARTIAL(false, 8);
+    else PARTIAL(false, kMaxK);
+#undef PARTIAL
     CKL();
     CK(xbarrier(ctx, BAR_Y, st));               // every expert rank's partials have landed on their sources
   } else if (f32 && out_fp32)
@@ -883,7 +890,8 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
   d.T = T;
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->aux;
   const int pp = next_layer & 1, prev = (next_layer - 1) & 1;
-  if (ctx->fwd_layer == next_layer - 1) CK(ev_wait(ctx, st, ctx->ev_gate[prev]));
+  if (ctx->fwd_layer == next_layer - 1)
+    CK(ev_wait(ctx, st, ctx->aux_start ? ctx->ev_disp[prev] : ctx->ev_gate[prev]));
   const uint64_t GL = d.GL, H = d.H, E = d.E, h = d.h;
   const Scratch& s = ctx->sl;
   const bool f32 = ctx->f32();
@@ -942,7 +950,8 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
       s1.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_SILU_BF16, d.h, d.h, ctx->scratch + s.pact);
       k_write_sched<<<1, 32, 0, st>>>(ctx->at<GemmSched>(s.s_p1), s1);
       CKL();
-      CK(launch_gemm_v(V_128_6_4, *mx, *m1, *m1, *mx, ctx->at<GemmSched>(s.s_p1), d.H, ctx->aux_sms, st));
+      CK(launch_gemm_v(ctx->pred_maxreg ? V_128_6_4_R192 : V_128_6_4, *mx, *m1, *m1, *mx, ctx->at<GemmSched>(s.s_p1),
+                       d.H, ctx->aux_sms, st));
       ++ctx->launches;
     }
     if (!mw) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
@@ -960,8 +969,9 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
     }
     k_write_sched<<<1, 32, 0, st>>>(ctx->at<GemmSched>(s.s_p2), s2);
     CKL();
-    CK(launch_gemm_v(BN == 128 ? V_128_6_4 : V_256_4_4, *mx, *mw, w_res1 ? *m2 : *mw, *mx, ctx->at<GemmSched>(s.s_p2),
-                     d.H, ctx->aux_sms, st, w_res1 ? ma : nullptr, w_res1 ? d.h : 0));
+    CK(launch_gemm_v(BN == 128 ? (ctx->pred_maxreg ? V_128_6_4_R192 : V_128_6_4) : V_256_4_4, *mx, *mw,
+                     w_res1 ? *m2 : *mw, *mx, ctx->at<GemmSched>(s.s_p2), d.H, ctx->aux_sms, st, w_res1 ? ma : nullptr,
+                     w_res1 ? d.h : 0));
     ++ctx->launches;
     if (!epi_topk) {
       CK(launch_select<true>(d, T, nchunks, st, ctx->at<float>(s.pprior), b_router_next, nullptr, nullptr, nullptr,
@@ -1277,6 +1287,7 @@ probe_status probe_finalize(probe_ctx ctx) {
   for (int p = 0; p < 2; ++p) {
     cudaEventDestroy(ctx->ev_gate[p]); cudaEventDestroy(ctx->ev_gemm[p]); cudaEventDestroy(ctx->ev_comb[p]);
     cudaEventDestroy(ctx->ev_pred[p]); cudaEventDestroy(ctx->ev_plan[p]); cudaEventDestroy(ctx->ev_slots[p]);
+    cudaEventDestroy(ctx->ev_disp[p]);
   }
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
   if (ctx->pf) cudaStreamDestroy(ctx->pf);
@@ -1476,6 +1487,14 @@ probe_status probe_set_option(probe_ctx ctx, int32_t option, int64_t value) {
     case PROBE_OPT_UNFUSED_TOPK: ctx->unfused = value != 0; return PROBE_OK;
     case PROBE_OPT_FUSED_EPILOGUE_TOPK: ctx->fused_epi_topk = value != 0; return PROBE_OK;
     case PROBE_OPT_PAIR_GEMM: ctx->pair_gemm = value != 0; return PROBE_OK;
+    case PROBE_OPT_AUX_START:
+      if (value < 0 || value > 1) return fail(ctx, PROBE_EINVAL, "aux start %lld not in {0, 1}", (long long)value);
+      ctx->aux_start = static_cast<int>(value);
+      return PROBE_OK;
+    case PROBE_OPT_PRED_MAXREG:
+      if (value != 0 && value != 192) return fail(ctx, PROBE_EINVAL, "predictor register cap %lld not in {0, 192}", (long long)value);
+      ctx->pred_maxreg = static_cast<int>(value);
+      return PROBE_OK;
     case PROBE_OPT_FUSED_DISPATCH:
       if (value < 0 || value > 2) return fail(ctx, PROBE_EINVAL, "fused dispatch mode %lld not in {0,1,2}", (long long)value);
       ctx->fused_dispatch = static_cast<int>(value);

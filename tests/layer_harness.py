@@ -86,6 +86,7 @@ def run_gpu(case: CaseCfg):
     if case.fused_dispatch:
         from paper_2602_00509_b200._lib import OPT_FUSED_DISPATCH
         rt.set_option(OPT_FUSED_DISPATCH, int(case.fused_dispatch))
+        rt._fused_dispatch = int(case.fused_dispatch)
     if case.overlap_dispatch is not None:
         from paper_2602_00509_b200._lib import OPT_OVERLAP_DISPATCH
         rt.set_option(OPT_OVERLAP_DISPATCH, int(case.overlap_dispatch))
@@ -178,7 +179,7 @@ def debug(rt, cfg, T=None, x=None):
     torch.cuda.synchronize()
     out = dict(counts=counts.cpu().numpy(), split_cum=split.cpu().numpy(), route=route.cpu().numpy(),
                group_rows=rows.cpu().numpy(), replicas=reps.cpu().numpy())
-    if x is not None:
+    if x is not None and not getattr(rt, "_fused_dispatch", 0):   # fused modes gather from x, no receive copy
         out["recv_ok"] = recv_rows_match(rt, cfg, x, route)
     return out
 

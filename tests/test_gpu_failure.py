@@ -61,7 +61,6 @@ def test_plan_overflow_falls_back_to_static_ep():
     rt = ProbeRuntime(cfg)
     out = [torch.empty(G, SH.T, SH.H, device="cuda") for _ in (0, 1)]
     ids = torch.empty(G, SH.T, SH.k, dtype=torch.int32, device="cuda")
-    rt.forward(0, li0.x, W[0], None, w[0][0], w[0][1], out[0])
     pc = torch.from_numpy(nhat.astype(np.int32)).cuda()
     win = torch.full((G,), 10 ** 9, dtype=torch.int64, device="cuda")
     reps = torch.empty(G, 3, dtype=torch.int32, device="cuda")
