@@ -203,7 +203,9 @@ probe_status probe_debug_prefetch(probe_ctx ctx, int32_t* out, void* stream);
 /* Measured hiding window (R26, "confined within the computation window"):
  * window_ns[r] (device int64 [G] out) = the most recently measured expert-GEMM phase of rank r
  * (%globaltimer stamps around GEMM1..GEMM2 of every probe_moe_forward, all-gathered into every
- * rank's count board, so all ranks plan from identical windows), or fallback_ns where no layer
+ * rank's count board, so all ranks plan from identical windows; when a process hosts several
+ * logical ranks their tiles share one grouped GEMM and rank r gets the row share
+ * T_GEMM · rows_r / Σ rows, its GEMM time on a GPU of its own), or fallback_ns where no layer
  * has been measured yet, plus attention_ns (the attention window that follows, caller-given).
  * Device to device, no host synchronisation; enqueued on `stream` (NULL = the aux stream, i.e.
  * before a probe_plan issued without a stream).  One step stale by construction (R26). */
@@ -346,6 +348,9 @@ enum { PROBE_OPT_EP_EMULATION = 1, PROBE_OPT_UNFUSED_TOPK = 2, PROBE_OPT_FUSED_E
                                   dispatch(L); 1: after dispatch(L) (beside the expert GEMMs) */,
        PROBE_OPT_PRED_MAXREG = 9 /* 0 (default) or 192: register-capped predictor GEMMs so a dispatch CTA
                                     co-resides on the SMs the aux track holds */,
+       PROBE_OPT_L2_HINTS = 10 /* TMA L2 eviction hints of the CTA-pair expert GEMMs: bits 0-2 GEMM1,
+                                  bits 4-6 GEMM2; per GEMM bit 0 output stores evict_first, bit 1 weight
+                                  (B) loads evict_last, bit 2 activation (A) loads evict_first */,
        PROBE_OPT_OVERLAP_DISPATCH = 7 /* when this process hosts every rank and the expert GEMMs run
                                          on CTA pairs: dispatch writes the receive-row → x-row index,
                                          then a persistent pull-copy kernel fills the receive buffers

@@ -64,7 +64,8 @@ struct GemmSched {
   int32_t nparts;                    // >1: CTA (pair) b serves only partition b % nparts (EP emulation)
   int32_t counter;                   // dynamic tile counter (reset by the kernel writing the schedule)
   int32_t tile_m;                    // rows per tile: 128 (1-CTA MMA) or 256 (CTA pair, cta_group::2)
-  int32_t pad2;
+  int32_t l2hint;                    // CTA-pair kernel TMA L2 hints: bit 0 C stores evict_first, bit 1 B loads
+                                     // evict_last, bit 2 A loads evict_first (0 = none)
   int32_t part_tile[kMaxParts + 1];  // tile range [part_tile[p], part_tile[p+1]) of partition p
   int32_t part_counter[kMaxParts];   // per-partition tile counters
   unsigned long long* stats;         // optional per-role wait-cycle counters (timing hook only)
@@ -218,7 +219,8 @@ __device__ __forceinline__ void epi_store_manual(const float* tile, int lane, co
 // rotates over NB tiles; lane 0 owns the bulk-async group of this warp.
 template <int NB>
 __device__ __forceinline__ void epi_chunk(float* tiles, int& tsel, int lane, const float (&v)[32],
-                                          const GemmGroup& G, const CUtensorMap* tmC, int row0, int col0) {
+                                          const GemmGroup& G, const CUtensorMap* tmC, int row0, int col0,
+                                          uint64_t store_pol = 0) {
   if (G.mode == EPI_NONE) {
     float acc = 0.f;
 #pragma unroll
@@ -266,7 +268,8 @@ __device__ __forceinline__ void epi_chunk(float* tiles, int& tsel, int lane, con
     ptx::fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
-      ptx::tma_store_2d(tmC, tile, col0, G.out_row + row0);
+      if (store_pol) ptx::tma_store_2d_hint(tmC, tile, col0, G.out_row + row0, store_pol);
+      else ptx::tma_store_2d(tmC, tile, col0, G.out_row + row0);
       ptx::bulk_commit();
     }
   } else {
@@ -345,7 +348,7 @@ __device__ __forceinline__ void epi_topk(uint32_t tb, int lane, const GemmGroup&
 // the column chunks c ≡ part (mod NPART).  Shared by the 1-CTA and the 2-CTA kernels.
 template <int BN, int NB, int NPART>
 __device__ __forceinline__ void epi_tile(uint32_t tb, int lane, int part, const GemmGroup& G, int row0, int nb,
-                                         float* tiles, int& tsel, const CUtensorMap* tmC) {
+                                         float* tiles, int& tsel, const CUtensorMap* tmC, uint64_t store_pol = 0) {
   if (G.mode == EPI_TOPK || G.mode == EPI_TOPK_COUNT) {
     switch (G.topk) {
       case 1: epi_topk<1, BN>(tb, lane, G, row0, tiles); break;
@@ -365,7 +368,7 @@ __device__ __forceinline__ void epi_tile(uint32_t tb, int lane, int part, const 
       float v[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = silu_f(__uint_as_float(gv[i])) * __uint_as_float(uv[i]);
-      epi_chunk<NB>(tiles, tsel, lane, v, G, tmC, row0, nb * (BN / 2) + c * 32);
+      epi_chunk<NB>(tiles, tsel, lane, v, G, tmC, row0, nb * (BN / 2) + c * 32, store_pol);
     }
   } else {
     // two chunks in flight per TMEM wait
@@ -386,7 +389,7 @@ __device__ __forceinline__ void epi_tile(uint32_t tb, int lane, int part, const 
           const float x = __uint_as_float(h == 0 ? va[i] : vb[i]);
           v[i] = silu ? silu_f(x) : x;
         }
-        epi_chunk<NB>(tiles, tsel, lane, v, G, tmC, row0, nb * BN + cc * 32);
+        epi_chunk<NB>(tiles, tsel, lane, v, G, tmC, row0, nb * BN + cc * 32, store_pol);
       }
     }
   }
@@ -765,6 +768,9 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
     const int32_t* gidx = sched->gather_idx;
     const int32_t* rdy = sched->a_ready;
     const int rdy_epoch = rdy ? sched->ready_epoch : 0;
+    const int l2h = sched->l2hint;
+    const uint64_t pol_a = (l2h & 4) ? ptx::policy_evict_first() : 0;
+    const uint64_t pol_b = (l2h & 2) ? ptx::policy_evict_last() : 0;
     int stage = 0;
     uint32_t phase = 0;
     int qs = 0;
@@ -825,8 +831,12 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
         if (lane == 0) {
           GEMM_TIMED_WAIT(&empty[stage], phase ^ 1, 0);
           if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (L::A_BYTES + L::B_BYTES));
-          if (!gat) ptx::tma_load_2d_cg2(ta, &full[stage], sA + stage * L::A_BYTES, kc, arow);
-          ptx::tma_load_2d_cg2(tb, &full[stage], sB + stage * L::B_BYTES, kc, brow);
+          if (!gat) {
+            if (pol_a) ptx::tma_load_2d_cg2_hint(ta, &full[stage], sA + stage * L::A_BYTES, kc, arow, pol_a);
+            else ptx::tma_load_2d_cg2(ta, &full[stage], sA + stage * L::A_BYTES, kc, arow);
+          }
+          if (pol_b) ptx::tma_load_2d_cg2_hint(tb, &full[stage], sB + stage * L::B_BYTES, kc, brow, pol_b);
+          else ptx::tma_load_2d_cg2(tb, &full[stage], sB + stage * L::B_BYTES, kc, brow);
         }
         __syncwarp();
         if (gat) ptx::tma_gather4_cg2(ta, &full[stage], sA + stage * L::A_BYTES + lane * 512, kc, g0, g1, g2, g3);
@@ -885,6 +895,7 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
     int qs = 0;
     uint32_t qph = 0;
     const uint32_t tempty_leader0 = ptx::mapa(ptx::smem_u32(&tempty[0]), 0);
+    const uint64_t store_pol = (sched->l2hint & 1) ? ptx::policy_evict_first() : 0;
     while (true) {
       ptx::mbar_wait_cluster(&qfull[qs], qph);
       const int tile = tq[qs];
@@ -906,7 +917,7 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
       ptx::tc_fence_after();
       const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
       const int row0 = mb * 256 + static_cast<int>(rank) * 128 + q * 32;
-      epi_tile<BN, L::NB, NPART>(tb, lane, part, G, row0, nb, tiles, tsel, &tmC);
+      epi_tile<BN, L::NB, NPART>(tb, lane, part, G, row0, nb, tiles, tsel, &tmC, store_pol);
       GEMM_STAT(acc_st[4] += clock64() - t_epi0);
       ptx::tc_fence_before();
       __syncwarp();

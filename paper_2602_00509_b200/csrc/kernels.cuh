@@ -156,8 +156,13 @@ __global__ void __launch_bounds__(128) k_topk(Dims d, int T, const float* __rest
 // n̂[rank][e] (R9).  grid (ceil(T/128), GL), block 128 (thread = token).  E % 32 == 0
 // or E < 32 handled by masking.
 // =============================================================================
+// The predictor instance (PRED) is capped at 64 registers (8 CTAs of 128 threads per SM) and
+// streams 16 logits per step: it must fit beside a persistent expert-GEMM CTA (224 × 256
+// registers) when the aux track still runs after the expert GEMMs started (C3 on one GPU:
+// the 4-TFLOP predictor outlasts the dispatch; a 95-register select then waited for the
+// GEMMs to end, the plan came after the combine and split-phase part 1 pushed nothing).
 template <int KK, bool PRED>
-__global__ void __launch_bounds__(128) k_select(Dims d, int T, const float* __restrict__ logits,
+__global__ void __launch_bounds__(128, PRED ? 8 : 1) k_select(Dims d, int T, const float* __restrict__ logits,
                                                 const float* __restrict__ bias, int32_t* __restrict__ ids,
                                                 float* __restrict__ gw, int32_t* __restrict__ pos,
                                                 int32_t* __restrict__ hist, int32_t* __restrict__ counts,
@@ -177,11 +182,12 @@ __global__ void __launch_bounds__(128) k_select(Dims d, int T, const float* __re
 #pragma unroll
     for (int j = 0; j < KK; ++j) { tv[j] = -INFINITY; te[j] = 0x7fffffff; }
     const float* row = logits + (static_cast<size_t>(gl) * T + t) * E;
+    constexpr int CW = PRED ? 16 : 32;     // logits per step
 #pragma unroll 1
-    for (int c = 0; c < E; c += 32) {
-      float v[32];
+    for (int c = 0; c < E; c += CW) {
+      float v[CW];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < CW / 4; ++q) {
         if (c + 4 * q + 3 < E) {
           const float4 f = __ldg(reinterpret_cast<const float4*>(row + c) + q);
           v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
@@ -192,17 +198,17 @@ __global__ void __launch_bounds__(128) k_select(Dims d, int T, const float* __re
       }
       if (bias) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
+        for (int i = 0; i < CW; ++i)
           if (c + i < E) v[i] += __ldg(bias + c + i);
       }
       if (PRED && logits_out) {   // l̂ = prior + residual + b, exactly the values the selection ranks
         float* lo = logits_out + (static_cast<size_t>(gl) * T + t) * E + c;
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
+        for (int i = 0; i < CW; ++i)
           if (c + i < E) lo[i] = v[i];
       }
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
+      for (int i = 0; i < CW; ++i) {
         float x = v[i];
         int e = c + i;
         if (x > tv[KK - 1]) {
@@ -334,22 +340,33 @@ __global__ void k_pred_publish(Dims d, const int32_t* __restrict__ pred_local, S
 }
 
 // R26 measured hiding window: the expert-GEMM phase of this process's ranks is stamped with
-// %globaltimer (phase 0: start, before GEMM1; phase 1: end, after GEMM2) and its duration is
-// stored for every local rank into EVERY rank's count board (int64 slot after the [2][2][G][E]
-// counts), so every rank plans from the same all-gathered windows (R10).  One thread.
+// %globaltimer (phase 0: start, before GEMM1; phase 1: end, after GEMM2) and stored for every
+// local rank into EVERY rank's count board (int64 slot after the [2][2][G][E] counts), so every
+// rank plans from the same all-gathered windows (R10).  One process per GPU (one local rank):
+// the window is the measured GEMM time.  Several logical ranks sharing one GPU run their
+// tiles in one grouped GEMM, so the measured time covers all of them; rank r's window is then
+// its share by rows, T_GEMM · rows_r / Σ rows — the time its GEMMs take when the GPU is its
+// own, i.e. the window it has on the system being emulated.  One thread.
 __device__ __forceinline__ int64_t* window_board(const Dims& d, uint8_t* board) {
   return reinterpret_cast<int64_t*>(board + static_cast<size_t>(4) * d.G * d.E * 4);
 }
-__global__ void k_window_stamp(Dims d, int64_t* t0, int phase, Sym sym, int buf_board) {
+__global__ void k_window_stamp(Dims d, int64_t* t0, int phase, Sym sym, int buf_board,
+                               const int32_t* __restrict__ group_rows) {
   const uint64_t now = ptx::globaltimer_ns();
   if (phase == 0) {
     *t0 = static_cast<int64_t>(now);
     return;
   }
   const int64_t w = static_cast<int64_t>(now) - *t0;
-  for (int r = 0; r < d.G; ++r) {
-    int64_t* wb = window_board(d, sym.at(buf_board, d.G, r));
-    for (int gl = 0; gl < d.GL; ++gl) wb[d.R0 + gl] = w;
+  const int S = d.EL + kMaxRb;
+  int64_t tot = 0;
+  for (int gl = 0; gl < d.GL; ++gl)
+    for (int j = 0; j < S; ++j) tot += group_rows[(d.R0 + gl) * S + j];
+  for (int gl = 0; gl < d.GL; ++gl) {
+    int64_t rows = 0;
+    for (int j = 0; j < S; ++j) rows += group_rows[(d.R0 + gl) * S + j];
+    const int64_t wr = (d.GL == 1 || tot == 0) ? w : w * rows / tot;
+    for (int r = 0; r < d.G; ++r) window_board(d, sym.at(buf_board, d.G, r))[d.R0 + gl] = wr > 0 ? wr : 1;
   }
 }
 // window_ns[r] = measured[r] (or fallback_ns where nothing was measured yet) + attention_ns
@@ -606,6 +623,7 @@ struct LayoutIn {
   const void* gather_src;       // software gather: x rows (bf16, H per row); null = TMA gather4
   int f32;                      // fp32 parity path: act and Y are fp32, GEMM2 stores EPI_F32
   const int32_t* a_ready;       // overlapped dispatch: GEMM1 acquires these block flags (else null)
+  int l2hint;                   // TMA L2 hints: bits 0-2 expert GEMM1, bits 4-6 expert GEMM2 (GemmSched::l2hint)
 };
 
 // R23 for every (s, e): split[s][e][t] from the quota (or static EP when quota == null)
@@ -790,6 +808,7 @@ __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o
       sc->gather_idx = w == 0 ? in.gather_idx : nullptr;
       sc->gather_src = w == 0 ? in.gather_src : nullptr;
       sc->a_ready = w == 0 ? in.a_ready : nullptr;
+      sc->l2hint = w == 0 ? (in.l2hint & 7) : ((in.l2hint >> 4) & 7);
       sc->ready_epoch = sc->ready_epoch + 1;        // this layer's flag value (flags of older layers differ)
       sc->copy_counter = 0;
       sc->gather_ld = d.H;

@@ -192,6 +192,7 @@ struct probe_ctx_s {
   int pred_T[2] = {0, 0};
   cudaEvent_t ev_gate[2], ev_gemm[2], ev_comb[2], ev_pred[2], ev_plan[2], ev_slots[2], ev_disp[2];
   int aux_start = 0;     // PROBE_OPT_AUX_START: predictor(L+1) starts after gate(L) (0) or dispatch(L) (1)
+  int l2hint = 0;        // PROBE_OPT_L2_HINTS: TMA L2 eviction hints of the expert GEMMs (LayoutIn::l2hint)
   int pred_maxreg = 0;   // PROBE_OPT_PRED_MAXREG: 192 ⇒ register-capped predictor GEMMs (a dispatch CTA fits beside)
   // CUDA-graph awareness: id of the stream capture each event was last recorded in (0 = eager)
   std::vector<std::pair<cudaEvent_t, unsigned long long>> ev_cap;
@@ -731,6 +732,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   const bool overlap = ctx->overlap_dispatch && !fused && !ctx->multi_process() && !f32 && pair &&
                        d.cap % 128 == 0 && ctx->pair_gemm;
   li.a_ready = overlap ? ctx->at<int32_t>(s.ready) : nullptr;
+  li.l2hint = ctx->l2hint;
   LayoutOut lo;
   lo.split_cum = ctx->at<int32_t>(s.split_cum);
   lo.slot_of = ctx->at<int32_t>(s.slot_of);
@@ -803,7 +805,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   // a7 grouped SwiGLU expert FFN (tcgen05): act = SiLU(X W_gᵀ) ⊙ X W_uᵀ ; Y = act W_dᵀ
   const int vexp = pair ? V_2CTA_256_6_4 : V_256_4_4_EXP;
   if (!overlap) {   // R26: the measured hiding window starts with the expert GEMMs
-    k_window_stamp<<<1, 1, 0, st>>>(d, ctx->at<int64_t>(s.win_t0), 0, sym_of(ctx), PROBE_BUF_BOARD);
+    k_window_stamp<<<1, 1, 0, st>>>(d, ctx->at<int64_t>(s.win_t0), 0, sym_of(ctx), PROBE_BUF_BOARD, lo.group_rows);
     CKL();
   }
   if (overlap) {
@@ -824,7 +826,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   }
   ++ctx->launches;
   if (!overlap) {
-    k_window_stamp<<<1, 1, 0, st>>>(d, ctx->at<int64_t>(s.win_t0), 1, sym_of(ctx), PROBE_BUF_BOARD);
+    k_window_stamp<<<1, 1, 0, st>>>(d, ctx->at<int64_t>(s.win_t0), 1, sym_of(ctx), PROBE_BUF_BOARD, lo.group_rows);
     CKL();
   }
   if (!dedup) CK(xbarrier(ctx, BAR_Y, st));     // every expert rank's Y rows are complete (the combine pulls)
@@ -1490,6 +1492,10 @@ probe_status probe_set_option(probe_ctx ctx, int32_t option, int64_t value) {
     case PROBE_OPT_AUX_START:
       if (value < 0 || value > 1) return fail(ctx, PROBE_EINVAL, "aux start %lld not in {0, 1}", (long long)value);
       ctx->aux_start = static_cast<int>(value);
+      return PROBE_OK;
+    case PROBE_OPT_L2_HINTS:
+      if (value < 0 || value > 0x77) return fail(ctx, PROBE_EINVAL, "L2 hint mask 0x%llx", (long long)value);
+      ctx->l2hint = static_cast<int>(value);
       return PROBE_OK;
     case PROBE_OPT_PRED_MAXREG:
       if (value != 0 && value != 192) return fail(ctx, PROBE_EINVAL, "predictor register cap %lld not in {0, 192}", (long long)value);

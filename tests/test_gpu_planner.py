@@ -92,7 +92,7 @@ def test_measured_window_feeds_planner():
     cfg = ProbeConfig(G=sh.G, E=sh.E, k=sh.k, H=sh.H, F=sh.F, T=sh.T, h=sh.h, bw_bytes_per_us=bw)
     rt = ProbeRuntime(cfg)
     win = torch.empty(sh.G, dtype=torch.int64, device="cuda")
-    rt.window(win, attention_ns=5, fallback_ns=1234, stream=torch.cuda.current_stream())
+    rt.window(win, attention_ns=5, fallback_ns=1234)          # aux stream (NULL stream argument)
     torch.cuda.synchronize()
     assert win.cpu().tolist() == [1239] * sh.G                  # nothing measured yet → fallback
     li = pi.layer_inputs(sh, 0, 0, 1.5, device="cuda")
@@ -100,11 +100,19 @@ def test_measured_window_feeds_planner():
     w13, w2 = pi.expert_weights(sh, 0, device="cuda")
     out = torch.empty(sh.G, sh.T, sh.H, device="cuda")
     rt.forward(0, li.x, W, None, w13, w2, out)
+    torch.cuda.synchronize()                                     # the aux stream does not order after stream 0
     attn = 3 * wbytes * 1000 // bw // 2                          # ≈ 1.5 replicas' worth of transfer time
-    rt.window(win, attention_ns=attn, fallback_ns=10 ** 12, stream=torch.cuda.current_stream())
+    rt.window(win, attention_ns=attn, fallback_ns=10 ** 12)
     torch.cuda.synchronize()
     w = win.cpu().numpy()
-    assert (w > attn).all() and (w < attn + 10 ** 9).all() and len(set(w.tolist())) == 1   # one process: one GEMM
+    assert (w > attn).all() and (w < attn + 10 ** 9).all()      # measured (not the fallback)
+    # one process hosts all ranks: one grouped GEMM, rank r's window = its row share of it
+    rows = torch.empty(sh.G, sh.E // sh.G + 3, dtype=torch.int32, device="cuda")
+    rt.debug_layout(group_rows=rows)
+    torch.cuda.synchronize()
+    share = rows.sum(dim=1).double().cpu().numpy()
+    m = (w - attn).astype(np.float64)
+    assert np.allclose(m / m.sum(), share / share.sum(), atol=1e-6)
     nhat = np.zeros((sh.G, sh.E), dtype=np.int32)
     nhat[:, :4] = 400                                            # rank 0's experts hot everywhere
     nhat[:, 4:] = 10
