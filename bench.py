@@ -203,9 +203,6 @@ def measure(shape, args, env, light=False, dedup=None, predispatch=False):
     if args.aux_sms:
         from paper_2602_00509_b200._lib import OPT_AUX_SMS
         rt.set_option(OPT_AUX_SMS, args.aux_sms)
-    if args.fused_dispatch:
-        from paper_2602_00509_b200._lib import OPT_FUSED_DISPATCH
-        rt.set_option(OPT_FUSED_DISPATCH, args.fused_dispatch)
     if args.aux_start:
         from paper_2602_00509_b200._lib import OPT_AUX_START
         rt.set_option(OPT_AUX_START, args.aux_start)
@@ -215,9 +212,6 @@ def measure(shape, args, env, light=False, dedup=None, predispatch=False):
     if args.pred_maxreg:
         from paper_2602_00509_b200._lib import OPT_PRED_MAXREG
         rt.set_option(OPT_PRED_MAXREG, args.pred_maxreg)
-    if args.overlap is not None:
-        from paper_2602_00509_b200._lib import OPT_OVERLAP_DISPATCH
-        rt.set_option(OPT_OVERLAP_DISPATCH, args.overlap)
     ranks = list(range(R0, R0 + GL))
     t0 = time.time()
     key = (shape, args.zipf, tuple(ranks))
@@ -743,7 +737,7 @@ def run_reference(args):
     return out
 
 
-def main():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -761,10 +755,6 @@ def main():
     ap.add_argument("--attn-ns", type=int, default=0, help="attention window added to the measured GEMM window")
     ap.add_argument("--no-dedup-sub", action="store_true", help="skip the dedup-wire sub-measurement")
     ap.add_argument("--ep", type=int, default=0, help="EP size G (default: the config's, 8)")
-    ap.add_argument("--fused-dispatch", type=int, default=0, choices=[0, 1, 2],
-                    help="GEMM1 gathers x rows: 1 TMA gather4, 2 cp.async warps (default 0: receive copy)")
-    ap.add_argument("--overlap", type=int, default=None, choices=[0, 1, 2],
-                    help="pull-copy dispatch overlapped with expert GEMM1 (default: the library's)")
     ap.add_argument("--out-bf16", action="store_true", help="bf16 layer output instead of fp32 (the parity-tested default)")
     ap.add_argument("--cap", type=float, default=4.0, help="receive capacity per rank in units of T·k")
     ap.add_argument("--aux-sms", type=int, default=0, help="grid cap of the aux-stream predictor GEMMs (0: #SMs/2)")
@@ -772,9 +762,14 @@ def main():
     ap.add_argument("--pred-maxreg", type=int, default=0, help="192: register-capped predictor GEMMs")
     ap.add_argument("--l2hint", type=lambda v: int(v, 0), default=0, help="expert-GEMM TMA L2 hint mask (probe.h)")
     ap.add_argument("--cpu-tokens", type=int, default=1024, help="oracle expert-FFN sample, tokens per rank")
-    args = ap.parse_args()
+    args = ap.parse_args(argv)
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
+    return args
+
+
+def main():
+    args = parse_args()
     if args.impl == "reference":
         run_reference(args)
     else:

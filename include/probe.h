@@ -233,9 +233,9 @@ probe_status probe_test_gemm(const void* A, int64_t a_rows, const void* B, int64
                              int32_t mode, void* C, void* stream);
 
 /* Timing hook: as probe_test_gemm with an explicit kernel variant (-1 = default for
- * `mode`; 0: BN=128/6 stages/4 epilogue warps, 1: 256/4/4, 2: 256/3/8, 3: 128/4/8,
- * 4: 256/3/4 with 2 staging tiles per epilogue warp, 5: 256/3/4 with 4,
- * 6: CTA pair (cta_group::2), 256-row tiles, 6 stages, 7: CTA pair with 5 stages and 8 epilogue warps),
+ * `mode`; 0: BN=128/6 stages/4 epilogue warps, 1: 256/4/4,
+ * 6: CTA pair (cta_group::2), 256-row tiles, 6 stages, 10: 1-CTA <256,4,4> capped at 216 registers,
+ * 11: <128,6,4> capped at 192 registers; other numbers are not available),
  * run once, then `reps` times between CUDA events on `stream`; *ms_out = mean ms. */
 probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int64_t b_rows,
                               int32_t K, int32_t N, const int32_t* groups, int32_t num_groups,
@@ -338,26 +338,13 @@ enum { PROBE_OPT_EP_EMULATION = 1, PROBE_OPT_UNFUSED_TOPK = 2, PROBE_OPT_FUSED_E
        PROBE_OPT_PAIR_GEMM = 5 /* expert GEMMs on CTA pairs (tcgen05 cta_group::2, 256-row tiles) when the
                                   mean rows per local expert T·k·G/E is at least 256 (else 1-CTA);
                                   default ON, 0 selects the 1-CTA kernel */,
-       PROBE_OPT_FUSED_DISPATCH = 6 /* when this process hosts every rank: dispatch writes only the
-                                       receive-row → x-row index and expert GEMM1 gathers its A rows
-                                       from x (no receive-buffer copy).  1: TMA gather4 in the
-                                       producer warp; 2: 16-byte cp.async by two gather warps (1-CTA
-                                       kernel).  Ignored with local_ranks < ep_size.  Default 0: see
-                                       DESIGN.md §6 for the measurements */,
        PROBE_OPT_AUX_START = 8 /* 0 (default): predict(L+1) starts when gate(L) is done, i.e. beside
                                   dispatch(L); 1: after dispatch(L) (beside the expert GEMMs) */,
        PROBE_OPT_PRED_MAXREG = 9 /* 0 (default) or 192: register-capped predictor GEMMs so a dispatch CTA
                                     co-resides on the SMs the aux track holds */,
        PROBE_OPT_L2_HINTS = 10 /* TMA L2 eviction hints of the CTA-pair expert GEMMs: bits 0-2 GEMM1,
                                   bits 4-6 GEMM2; per GEMM bit 0 output stores evict_first, bit 1 weight
-                                  (B) loads evict_last, bit 2 activation (A) loads evict_first */,
-       PROBE_OPT_OVERLAP_DISPATCH = 7 /* when this process hosts every rank and the expert GEMMs run
-                                         on CTA pairs: dispatch writes the receive-row → x-row index,
-                                         then a persistent pull-copy kernel fills the receive buffers
-                                         in GEMM tile order while expert GEMM1 (programmatic dependent
-                                         launch) runs beside it, acquiring per-128-row flags before
-                                         each tile's A loads (a6 overlapped with a7 tile by tile).
-                                         Ignored otherwise (recv_capacity % 128 != 0, fp32 path). */ };
+                                  (B) loads evict_last, bit 2 activation (A) loads evict_first */ };
 probe_status probe_set_option(probe_ctx ctx, int32_t option, int64_t value);
 
 /* Number of library kernel launches enqueued so far by this context (bench accounting). */

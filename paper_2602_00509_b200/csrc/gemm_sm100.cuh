@@ -69,19 +69,6 @@ struct GemmSched {
   int32_t part_tile[kMaxParts + 1];  // tile range [part_tile[p], part_tile[p+1]) of partition p
   int32_t part_counter[kMaxParts];   // per-partition tile counters
   unsigned long long* stats;         // optional per-role wait-cycle counters (timing hook only)
-  // Fused dispatch (a6 → a7): when non-null, A row r of the first K segment is row
-  // gather_idx[r] of the source instead of row r — either the A map (TMA gather4, map box
-  // {64, 1}; gather_src null) or, with gather_src set, row-major bf16 rows of gather_ld
-  // elements gathered by warps 2-3 with 16-byte cp.async (1-CTA kernel, K2 = 0).
-  const int32_t* gather_idx;
-  const void* gather_src;
-  int32_t gather_ld;
-  // Overlapped dispatch (a6 ∥ a7): when non-null, A rows [128b, 128b+128) of the A map may be
-  // read only once a_ready[b] == ready_epoch (written with release by the pull-dispatch copy
-  // kernel running concurrently); the producer acquires it before the tile's first A load.
-  int32_t ready_epoch;
-  int32_t copy_counter;              // pull-dispatch block counter (reset with the schedule)
-  const int32_t* a_ready;
   GemmGroup g[kMaxGroups];
 };
 // stats[0] producer waits on `empty`   stats[1] MMA waits on `full`   stats[2] MMA waits on `tempty`
@@ -123,9 +110,6 @@ __device__ inline void gemm_finalize_sched(GemmSched* s, int BN) {
   s->nparts = 0;
   s->tile_m = 128;
   s->stats = nullptr;
-  s->gather_idx = nullptr;
-  s->gather_src = nullptr;
-  s->a_ready = nullptr;
   sched_reset_counters(s);
   int acc = 0;
   for (int i = 0; i < s->num_groups; ++i) {
@@ -439,11 +423,9 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   GEMM_STAT(const long long t_kernel0 = clock64());
   for (int i = threadIdx.x; i < ng; i += blockDim.x) ts[i] = sched->g[i].tile_start;
 
-  // gather mode: 0 plain TMA tiles, 1 TMA gather4 by the producer warp, 2 software gather by warps 2-3
-  const int gmode = sched->gather_idx ? (sched->gather_src ? 2 : 1) : 0;
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      ptx::mbar_init(&full[s], gmode == 2 ? 2 : 1);   // + the gather group's arrive
+      ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -452,7 +434,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     }
     for (int q = 0; q < kTileQ; ++q) {
       ptx::mbar_init(&qfull[q], 1);
-      ptx::mbar_init(&qempty[q], 1 + EW + (gmode == 2 ? 1 : 0));
+      ptx::mbar_init(&qempty[q], 1 + EW);
     }
     ptx::fence_barrier_init();
     ptx::tma_prefetch_desc(&tmA);
@@ -470,9 +452,8 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   const int num_kb = kb1 + (K2 > 0 ? (K2 + 63) / 64 : 0);
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer (warp 0:
-    // lane 0 claims tiles and loads B / A tiles; with a gather index every lane gathers 4 A rows)
-    const int32_t* gidx = sched->gather_idx;
+    // ------------------------------------------------------------ TMA producer (warp 0,
+    // lane 0: claims tiles and loads the A / B tiles)
     int stage = 0;
     uint32_t phase = 0;
     int qs = 0;
@@ -504,27 +485,19 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       }
       const int koff = G.k_off;
       const bool bsel = G.b_sel != 0;
-      int g0 = 0, g1 = 0, g2 = 0, g3 = 0;
-      if (gmode == 1) {
-        const int32_t* p = gidx + arow + 4 * lane;
-        g0 = p[0]; g1 = p[1]; g2 = p[2]; g3 = p[3];
-      }
       for (int kb = 0; kb < num_kb; ++kb) {
         const bool second = kb >= kb1;
         const CUtensorMap* ta = second ? &tmA2 : &tmA;
         const CUtensorMap* tb = (second || bsel) ? &tmB1 : &tmB0;
         const int kc = second ? (kb - kb1) * 64 : koff + kb * 64;
-        const bool gat = gmode == 1 && !second;
-        const bool sgat = gmode == 2 && !second;     // A rows come from warps 2-3
         if (lane == 0) {
           GEMM_TIMED_WAIT(&empty[stage], phase ^ 1, 0);
-          ptx::mbar_arrive_expect_tx(&full[stage], (sgat ? 0 : L::A_BYTES) + L::B_BYTES);
-          if (!gat && !sgat) ptx::tma_load_2d(ta, &full[stage], sA + stage * L::A_BYTES, kc, arow);
+          ptx::mbar_arrive_expect_tx(&full[stage], L::A_BYTES + L::B_BYTES);
+          ptx::tma_load_2d(ta, &full[stage], sA + stage * L::A_BYTES, kc, arow);
           ptx::tma_load_2d(tb, &full[stage], sB + stage * L::B_BYTES, kc, brow0);
           ptx::tma_load_2d(tb, &full[stage], sB + stage * L::B_BYTES + (BN / 2) * 128, kc, brow1);
         }
         __syncwarp();
-        if (gat) ptx::tma_gather4(ta, &full[stage], sA + stage * L::A_BYTES + lane * 512, kc, g0, g1, g2, g3);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
@@ -565,68 +538,6 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       __syncwarp();
       acc ^= 1;
       if (acc == 0) aphase ^= 1;
-    }
-  } else if (warp == 2 || warp == 3) {
-    if (gmode == 2) {
-      // ---------------------------------------------------------- software gather of A (fused
-      // dispatch): thread t copies 16-byte chunk (t mod 8) of rows t/8 + 8i (i < 16) of every
-      // stage with cp.async into the SWIZZLE_128B layout the MMA descriptor expects; a stage is
-      // released to the MMA D stages after it was issued (wait_group, proxy fence, one arrive).
-      constexpr int D = STAGES > 3 ? 3 : STAGES - 1;
-      const int gt = threadIdx.x - 64;
-      const int jj = gt & 7, rb = gt >> 3;
-      const char* xsrc = static_cast<const char*>(sched->gather_src);
-      const size_t ldb = static_cast<size_t>(sched->gather_ld) * 2;
-      const int32_t* gidx = sched->gather_idx;
-      int stage = 0;
-      uint32_t phase = 0;
-      int qs = 0;
-      uint32_t qph = 0;
-      int pend[4] = {0, 0, 0, 0};
-      int npend = 0;
-      while (true) {
-        ptx::mbar_wait(&qfull[qs], qph);
-        const int tile = tq[qs];
-        ptx::named_bar_sync(1, 64);
-        if (gt == 0) ptx::mbar_arrive(&qempty[qs]);
-        if (++qs == kTileQ) { qs = 0; qph ^= 1; }
-        if (tile < 0) break;
-        const int gi = gemm_find_group(ts, ng, tile);
-        const GemmGroup& G = sched->g[gi];
-        const int nt = gemm_ntiles_n(G, BN);
-        const int mb = (tile - ts[gi]) / nt;
-        const int arow = G.a_row + mb * 128;
-        const char* rowp[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-          rowp[i] = xsrc + static_cast<size_t>(gidx[arow + rb + 8 * i]) * ldb + jj * 16 + static_cast<size_t>(G.k_off) * 2;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          ptx::mbar_wait(&empty[stage], phase ^ 1);
-          const uint32_t dst0 = ptx::smem_u32(sA + stage * L::A_BYTES);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int r = rb + 8 * i;
-            ptx::cp_async16(dst0 + r * 128 + ((jj ^ (r & 7)) << 4), rowp[i] + kb * 128);
-          }
-          ptx::cp_async_commit();
-          pend[npend++] = stage;
-          if (npend == D) {
-            ptx::cp_async_wait<D - 1>();
-            ptx::fence_proxy_async_smem();
-            ptx::named_bar_sync(1, 64);
-            if (gt == 0) ptx::mbar_arrive(&full[pend[0]]);
-#pragma unroll
-            for (int i = 0; i < 3; ++i) pend[i] = pend[i + 1];
-            --npend;
-          }
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        }
-      }
-      ptx::cp_async_wait<0>();
-      ptx::fence_proxy_async_smem();
-      ptx::named_bar_sync(1, 64);
-      if (gt == 0)
-        for (int i = 0; i < npend; ++i) ptx::mbar_arrive(&full[pend[i]]);
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
@@ -763,11 +674,7 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs;
-    // lane 0 handles the tile queue and the TMA tile loads, with a gather index every lane
-    // gathers 4 of this CTA's 128 A rows)
-    const int32_t* gidx = sched->gather_idx;
-    const int32_t* rdy = sched->a_ready;
-    const int rdy_epoch = rdy ? sched->ready_epoch : 0;
+    // lane 0 handles the tile queue and the TMA tile loads)
     const int l2h = sched->l2hint;
     const uint64_t pol_a = (l2h & 4) ? ptx::policy_evict_first() : 0;
     const uint64_t pol_b = (l2h & 2) ? ptx::policy_evict_last() : 0;
@@ -806,40 +713,20 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
       else brow = G.b_row + nb * BN + static_cast<int>(rank) * (BN / 2);
       const int koff = G.k_off;
       const bool bsel = G.b_sel != 0;
-      int g0 = 0, g1 = 0, g2 = 0, g3 = 0;
-      if (gidx) {
-        const int32_t* p = gidx + arow + 4 * lane;
-        g0 = p[0]; g1 = p[1]; g2 = p[2]; g3 = p[3];
-      }
-      if (rdy && lane == 0) {
-        // overlapped dispatch: this CTA's valid A rows must have landed (acquire the block
-        // flags of the pull-dispatch copy, then order the async-proxy TMA reads after them)
-        const int need = min(128, G.m - (mb * 256 + static_cast<int>(rank) * 128));
-        if (need > 0) {
-          const int b0 = arow >> 7, b1 = (arow + need - 1) >> 7;
-          for (int b = b0; b <= b1; ++b)
-            while (ptx::ld_acquire_gpu(rdy + b) != rdy_epoch) __nanosleep(64);
-          ptx::fence_proxy_async_global();
-        }
-      }
       for (int kb = 0; kb < num_kb; ++kb) {
         const bool second = kb >= kb1;
         const CUtensorMap* ta = second ? &tmA2 : &tmA;
         const CUtensorMap* tb = (second || bsel) ? &tmB1 : &tmB0;
         const int kc = second ? (kb - kb1) * 64 : koff + kb * 64;
-        const bool gat = gidx && !second;
         if (lane == 0) {
           GEMM_TIMED_WAIT(&empty[stage], phase ^ 1, 0);
           if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (L::A_BYTES + L::B_BYTES));
-          if (!gat) {
-            if (pol_a) ptx::tma_load_2d_cg2_hint(ta, &full[stage], sA + stage * L::A_BYTES, kc, arow, pol_a);
-            else ptx::tma_load_2d_cg2(ta, &full[stage], sA + stage * L::A_BYTES, kc, arow);
-          }
+          if (pol_a) ptx::tma_load_2d_cg2_hint(ta, &full[stage], sA + stage * L::A_BYTES, kc, arow, pol_a);
+          else ptx::tma_load_2d_cg2(ta, &full[stage], sA + stage * L::A_BYTES, kc, arow);
           if (pol_b) ptx::tma_load_2d_cg2_hint(tb, &full[stage], sB + stage * L::B_BYTES, kc, brow, pol_b);
           else ptx::tma_load_2d_cg2(tb, &full[stage], sB + stage * L::B_BYTES, kc, brow);
         }
         __syncwarp();
-        if (gat) ptx::tma_gather4_cg2(ta, &full[stage], sA + stage * L::A_BYTES + lane * 512, kc, g0, g1, g2, g3);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }

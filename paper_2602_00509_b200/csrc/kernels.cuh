@@ -619,10 +619,7 @@ struct LayoutIn {
   int bank;                     // replica slot bank = layer parity
   void* act;                    // [GL*cap, F] bf16
   void* y_local;                // [GL*cap, H] fp16 (this process's Y region, D2)
-  const int32_t* gather_idx;    // fused dispatch: GEMM1 gathers its A rows through this index (else null)
-  const void* gather_src;       // software gather: x rows (bf16, H per row); null = TMA gather4
   int f32;                      // fp32 parity path: act and Y are fp32, GEMM2 stores EPI_F32
-  const int32_t* a_ready;       // overlapped dispatch: GEMM1 acquires these block flags (else null)
   int l2hint;                   // TMA L2 hints: bits 0-2 expert GEMM1, bits 4-6 expert GEMM2 (GemmSched::l2hint)
 };
 
@@ -805,13 +802,7 @@ __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o
       sc->total_tiles = base;
       sc->tile_m = in.tile_m;
       sc->stats = nullptr;
-      sc->gather_idx = w == 0 ? in.gather_idx : nullptr;
-      sc->gather_src = w == 0 ? in.gather_src : nullptr;
-      sc->a_ready = w == 0 ? in.a_ready : nullptr;
       sc->l2hint = w == 0 ? (in.l2hint & 7) : ((in.l2hint >> 4) & 7);
-      sc->ready_epoch = sc->ready_epoch + 1;        // this layer's flag value (flags of older layers differ)
-      sc->copy_counter = 0;
-      sc->gather_ld = d.H;
       sched_reset_counters(sc);
       sc->nparts = in.nparts > 1 ? in.nparts : 0;
       if (in.nparts > 1) {
@@ -826,8 +817,6 @@ __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o
 // a6 dispatch: every (token, slot) row of x to its destination's receive buffer
 // (peer store over NVLink for remote ranks).  Warp per token; the x row is read
 // once and written to its k destinations with 16-byte vector stores.
-// Fused mode (gidx != null, every rank in this process): only the route and the
-// receive-row → x-row index are written; the expert GEMM1 producer gathers the rows.
 // =============================================================================
 __global__ void __launch_bounds__(256) k_dispatch(Dims d, int T, const uint8_t* __restrict__ x, int row_bytes,
                                                   const int32_t* __restrict__ ids,
@@ -836,7 +825,7 @@ __global__ void __launch_bounds__(256) k_dispatch(Dims d, int T, const uint8_t* 
                                                   const int32_t* __restrict__ split_cum,
                                                   const int32_t* __restrict__ slot_of,
                                                   const int32_t* __restrict__ src_off, int32_t* __restrict__ route,
-                                                  Sym sym, int buf_recv, int32_t* err, int32_t* __restrict__ gidx) {
+                                                  Sym sym, int buf_recv, int32_t* err) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= d.GL * T) return;
@@ -863,15 +852,8 @@ __global__ void __launch_bounds__(256) k_dispatch(Dims d, int T, const uint8_t* 
     }
     route[(pr * k + lane) * 2] = dd;
     route[(pr * k + lane) * 2 + 1] = row;
-    if (gidx) {
-      // fused dispatch (all ranks in this process): receive row `row` of dd is x row pr —
-      // GEMM1 gathers it with TMA gather4; nothing is copied
-      if (row >= 0) gidx[static_cast<size_t>(dd - d.R0) * d.cap + row] = static_cast<int32_t>(pr);
-    } else if (row >= 0) {
-      dst_row = sym.at(buf_recv, d.G, dd) + static_cast<size_t>(row) * row_bytes;
-    }
+    if (row >= 0) dst_row = sym.at(buf_recv, d.G, dd) + static_cast<size_t>(row) * row_bytes;
   }
-  if (gidx) return;
   // copy: the x row is read once (batches of 8 × 16 B per lane in flight) and stored k times
   const uint4* src = reinterpret_cast<const uint4*>(x + pr * row_bytes);
   const int nv = row_bytes / 16;
@@ -1280,92 +1262,6 @@ __global__ void __launch_bounds__(128) k_combine_reduce(Dims d, int T, const int
       p.z = pack_bf16(a[4], a[5]);
       p.w = pack_bf16(a[6], a[7]);
       reinterpret_cast<uint4*>(out)[static_cast<size_t>(tok) * nv + c] = p;
-    }
-  }
-}
-
-// =============================================================================
-// a6 ∥ a7 overlapped (pull) dispatch, single process: k_dispatch has written only the
-// receive-row → x-row index (gidx); this persistent copy kernel fills the receive buffers
-// in 128-row blocks, in the order the expert GEMM1 claims its tiles, and publishes each
-// block with a release flag (= the schedule's epoch).  It triggers programmatic dependent
-// launch at entry, so GEMM1 starts beside it on the same SMs and its producer acquires
-// the flags of a tile's rows before the TMA loads: the copy (HBM) overlaps the tensor-core
-// work tile by tile instead of preceding it.  Block order: local destination major
-// (GEMM claims groups in order), or round-robin over destinations under EP emulation
-// (each destination's GEMM partition starts at once).  Never waits on anything, so it
-// always completes (no deadlock whatever the residency of the dependent GEMM).
-// =============================================================================
-__global__ void __launch_bounds__(256, 4) k_dispatch_pull(Dims d, const uint8_t* __restrict__ x, int row_bytes,
-                                                       const int32_t* __restrict__ gidx,
-                                                       const int32_t* __restrict__ group_rows, GemmSched* s1,
-                                                       int32_t* __restrict__ ready, uint8_t* __restrict__ recv,
-                                                       int interleave) {
-  ptx::griddep_launch_dependents();
-  __shared__ int nblk[kMaxG + 1], used[kMaxG];
-  __shared__ int unit_s;
-  const int S = d.EL + kMaxRb;
-  const int GL = d.GL;
-  if (threadIdx.x < GL) {
-    const int r = d.R0 + threadIdx.x;
-    int u = 0;
-    for (int j = 0; j < S; ++j) u += group_rows[r * S + j];
-    used[threadIdx.x] = min(u, d.cap);
-    nblk[threadIdx.x] = (min(u, d.cap) + 127) >> 7;
-  }
-  __syncthreads();
-  int maxb = 0, totb = 0;
-  for (int g = 0; g < GL; ++g) {
-    maxb = max(maxb, nblk[g]);
-    totb += nblk[g];
-  }
-  const int nunits = interleave ? maxb * GL : totb;
-  const int epoch = s1->ready_epoch;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nv = row_bytes / 16;
-  const int bpd = d.cap >> 7;                      // flag blocks per destination (cap % 128 == 0)
-  while (true) {
-    if (threadIdx.x == 0) unit_s = atomicAdd(&s1->copy_counter, 1);
-    __syncthreads();
-    const int u = unit_s;
-    __syncthreads();
-    if (u >= nunits) break;
-    int gl, blk;
-    if (interleave) {
-      gl = u % GL;
-      blk = u / GL;
-      if (blk >= nblk[gl]) continue;
-    } else {
-      gl = 0;
-      blk = u;
-      while (blk >= nblk[gl]) blk -= nblk[gl++];
-    }
-    const int r_end = min(blk * 128 + 128, used[gl]);
-    const size_t base = static_cast<size_t>(gl) * d.cap;
-    // warp w: rows blk·128 + w, +8, ...; 8 × 16 B per lane in flight (≤ 64 registers, so a
-    // copy CTA stays co-resident with the register-capped GEMM1 CTA of the same SM)
-    for (int r0 = blk * 128 + warp; r0 < r_end; r0 += 8) {
-      const uint4* s0 = reinterpret_cast<const uint4*>(x + static_cast<size_t>(gidx[base + r0]) * row_bytes);
-      uint4* d0 = reinterpret_cast<uint4*>(recv + (base + r0) * row_bytes);
-      for (int c0 = 0; c0 < nv; c0 += 32 * 8) {
-        uint4 v0[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int c = c0 + q * 32 + lane;
-          if (c < nv) v0[q] = __ldg(s0 + c);
-        }
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int c = c0 + q * 32 + lane;
-          if (c < nv) d0[c] = v0[q];
-        }
-      }
-    }
-    ptx::fence_proxy_async_global();               // the rows are read by TMA (async proxy)
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      ptx::st_release_gpu(ready + static_cast<size_t>(gl) * bpd + blk, epoch);
     }
   }
 }

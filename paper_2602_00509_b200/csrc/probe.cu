@@ -112,7 +112,7 @@ struct Scratch {
   size_t sym, logits, pprior, pres, pact, ids, gw, pos, hist, cbase, route, pred_local;
   size_t quota[2], reps[2], stats[2], pfctr[2], pids[2];
   size_t split_cum, slot_of, src_off, group_rows, reps_used;
-  size_t s_g1, s_g2, s_gate, s_p1, s_p2, flags, win_t0, gidx, ready, act, total;
+  size_t s_g1, s_g2, s_gate, s_p1, s_p2, flags, win_t0, act, total;
 };
 
 Scratch scratch_layout(const probe_config& c) {
@@ -153,8 +153,6 @@ Scratch scratch_layout(const probe_config& c) {
   s.s_p2 = take(sizeof(GemmSched));
   s.flags = take(256);
   s.win_t0 = take(64);
-  s.gidx = take((GL * cap + 512) * 4);     // fused dispatch: receive row → x row (+ tile overhang)
-  s.ready = take((GL * cap / 128 + 4) * 4); // overlapped dispatch: per-128-row-block landed flags
   s.act = take(GL * cap * F * esz(c));
   s.total = al(o, 1024);
   return s;
@@ -212,8 +210,6 @@ struct probe_ctx_s {
   bool ep_emulation = false;  // partition expert GEMMs by local rank (probe_set_option)
   bool fused_epi_topk = false;  // top-k in the GEMM epilogue instead of k_select (probe_set_option)
   bool pair_gemm = true;        // expert GEMMs on CTA pairs (cta_group::2); option turns it off
-  int fused_dispatch = 0;       // single process, GEMM1 gathers x rows: 1 TMA gather4, 2 cp.async warps (opt-in)
-  int overlap_dispatch = 0;     // single process: pull-copy dispatch overlapped with GEMM1 (flags + PDL)
   // distillation workspace (NEXT-1), allocated on the first probe_distill_grad
   uint8_t* dbuf = nullptr;
   size_t dbytes = 0;
@@ -257,13 +253,12 @@ probe_status fail(probe_ctx ctx, probe_status st, const char* fmt, ...) {
 
 // GEMM variants: (BN, STAGES, epilogue warps).  V_GATE: logits/predictor (N ≤ 256),
 // V_SWIGLU: expert GEMM1 (bf16 act out), V_F32: expert GEMM2 (fp32 Y out, epilogue-heavy).
-enum GemmVariant { V_128_6_4 = 0, V_256_4_4 = 1, V_256_3_8 = 2, V_128_4_8 = 3, V_256_3_4_NB2 = 4, V_256_3_4_NB4 = 5,
-                   V_2CTA_256_6_4 = 6 /* CTA pair, cta_group::2, 256-row tiles */,
-                   V_2CTA_256_5_8 = 7 /* CTA pair with 8 epilogue warps */,
-                   V_2CTA_256_5_4_NB2 = 8 /* CTA pair, 5 stages, 2 staging slots per epilogue warp */,
-                   V_2CTA_256_4_4_NB4 = 9 /* CTA pair, 4 stages, 4 staging slots per epilogue warp */,
-                   V_256_4_4_EXP = 10 /* 1-CTA <256,4,4> register-capped for the expert GEMMs */,
-                   V_128_6_4_R192 = 11 /* predictor GEMMs capped at 192 registers: a dispatch CTA fits beside */ };
+// GEMM variants: (BN, STAGES, epilogue warps).  V_128_6_4: router / predictor GEMMs (N ≤ 128),
+// V_256_4_4: router GEMM for E > 128 (1-CTA), V_2CTA_256_6_4: the expert GEMMs on CTA pairs,
+// V_256_4_4_EXP: the 1-CTA expert GEMMs for decode-sized groups, V_128_6_4_R192: register-capped
+// predictor GEMMs (PROBE_OPT_PRED_MAXREG).  The numbering is the probe_bench_gemm `variant`
+// argument; the other numbers were configurations measured slower in round 1 and removed.
+enum GemmVariant { V_128_6_4 = 0, V_256_4_4 = 1, V_2CTA_256_6_4 = 6, V_256_4_4_EXP = 10, V_128_6_4_R192 = 11 };
 
 // Expert GEMMs leave registers for one 128-thread prefetch CTA per SM (a9 part 1 runs beside them):
 // 256 × 224 + 128 × 48 = 62 K.  Splits that fill exactly 64 K (240 + 32, 232 + 48) did not
@@ -306,30 +301,6 @@ cudaError_t launch_gemm_2cta(const CUtensorMap& a, const CUtensorMap& b0, const 
   return cudaGetLastError();
 }
 
-// Expert GEMM1 of the overlapped dispatch: programmatic dependent launch after the pull-copy
-// kernel (which triggers at entry), register-capped so a copy CTA stays co-resident per SM.
-constexpr int kOverlapMaxReg = 192;
-cudaError_t launch_gemm1_overlap(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1,
-                                 const CUtensorMap& c, GemmSched* s, int K, int grid, cudaStream_t st,
-                                 bool pdl = true) {
-  using L = Gemm2Smem<256, 6, 4>;
-  auto* kern = grouped_gemm_2cta_kernel<256, 6, 4, kOverlapMaxReg>;
-  static uint64_t attr = 0;
-  cudaError_t e = smem_attr_once(kern, L::BYTES, attr);
-  if (e != cudaSuccess) return e;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid & ~1);
-  cfg.blockDim = dim3(128 + 32 * 4);
-  cfg.dynamicSmemBytes = L::BYTES;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kern, a, b0, b1, c, a, s, K, 0);
-}
-
 template <int BN, int ST, int EW, int NB = (EW == 8 ? 2 : 1), int MAXR = 255>
 cudaError_t launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, const CUtensorMap& c,
                           const CUtensorMap& a2, GemmSched* s, int K, int K2, int grid, cudaStream_t st) {
@@ -349,21 +320,17 @@ cudaError_t launch_gemm_v(int v, const CUtensorMap& a, const CUtensorMap& b0, co
   switch (v) {
     case V_128_6_4: return launch_gemm_t<128, 6, 4>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_256_4_4: return launch_gemm_t<256, 4, 4>(a, b0, b1, c, A2, s, K, K2, grid, st);
-    case V_256_3_8: return launch_gemm_t<256, 3, 8>(a, b0, b1, c, A2, s, K, K2, grid, st);
-    case V_128_4_8: return launch_gemm_t<128, 4, 8>(a, b0, b1, c, A2, s, K, K2, grid, st);
-    case V_256_3_4_NB2: return launch_gemm_t<256, 3, 4, 2>(a, b0, b1, c, A2, s, K, K2, grid, st);
-    case V_256_3_4_NB4: return launch_gemm_t<256, 3, 4, 4>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_2CTA_256_6_4: return launch_gemm_2cta<256, 6, 4, 1, kExpertMaxReg>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_256_4_4_EXP: return launch_gemm_t<256, 4, 4, 1, PROBE_EXP1_MAXREG>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_128_6_4_R192: return launch_gemm_t<128, 6, 4, 1, 192>(a, b0, b1, c, A2, s, K, K2, grid, st);
-    case V_2CTA_256_5_8: return launch_gemm_2cta<256, 5, 8>(a, b0, b1, c, A2, s, K, K2, grid, st);
-    case V_2CTA_256_5_4_NB2: return launch_gemm_2cta<256, 5, 4, 2>(a, b0, b1, c, A2, s, K, K2, grid, st);
-    case V_2CTA_256_4_4_NB4: return launch_gemm_2cta<256, 4, 4, 4>(a, b0, b1, c, A2, s, K, K2, grid, st);
   }
   return cudaErrorInvalidValue;
 }
-int variant_bn(int v) { return (v == V_128_6_4 || v == V_128_4_8 || v == V_128_6_4_R192) ? 128 : 256; }
-int variant_tm(int v) { return (v >= V_2CTA_256_6_4 && v <= V_2CTA_256_4_4_NB4) ? 256 : 128; }
+int variant_bn(int v) { return (v == V_128_6_4 || v == V_128_6_4_R192) ? 128 : 256; }
+int variant_tm(int v) { return v == V_2CTA_256_6_4 ? 256 : 128; }
+bool variant_ok(int v) {
+  return v == V_128_6_4 || v == V_256_4_4 || v == V_2CTA_256_6_4 || v == V_256_4_4_EXP || v == V_128_6_4_R192;
+}
 
 template <int BN>
 cudaError_t launch_gemm(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, GemmSched* s, int K,
@@ -555,10 +522,6 @@ probe_status probe_init(const probe_config* cfg, const uint64_t* peer_ptrs, void
   }
   cudaError_t e = cudaMemcpy(ctx->scratch + ctx->sl.sym, ctx->peer.data(), PROBE_NSYM * G * 8, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemset(ctx->scratch + ctx->sl.flags, 0, 256);
-  if (e == cudaSuccess)   // gather indices of never-written receive rows stay valid (row 0)
-    e = cudaMemset(ctx->scratch + ctx->sl.gidx, 0, (static_cast<size_t>(cfg->local_ranks) * cfg->recv_capacity + 512) * 4);
-  if (e == cudaSuccess)   // overlapped dispatch: flags and the schedule epochs start at 0
-    e = cudaMemset(ctx->scratch + ctx->sl.ready, 0, (static_cast<size_t>(cfg->local_ranks) * cfg->recv_capacity / 128 + 4) * 4);
   if (e == cudaSuccess) e = cudaMemset(ctx->scratch + ctx->sl.s_g1, 0, sizeof(GemmSched));
   if (e == cudaSuccess) e = cudaMemset(ctx->scratch + ctx->sl.s_g2, 0, sizeof(GemmSched));
   // The aux track (predictor, planner) and the prefetch run on the highest-priority streams:
@@ -641,7 +604,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   // ranks of its predicted experts on a side stream while the gate below computes the routing
   const int row_bytes = static_cast<int>(H * esz(ctx->cfg));
   const bool predisp = ctx->cfg.predispatch && use_plan && ctx->pred_layer[p] == layer && ctx->pred_T[p] == T &&
-                       ctx->fused_dispatch == 0 && ctx->overlap_dispatch == 0 && !f32;
+                       !f32;
   if (predisp) {
     CK(ev_record(ctx, ctx->ev_fwd_start, st));
     CK(ev_wait(ctx, ctx->pd, ctx->ev_fwd_start));
@@ -716,22 +679,11 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   // CTA pairs pay off when expert groups fill 256-row tiles; decode-sized groups (mean rows per
   // local expert T·k·G/E below 256, e.g. C2: 64) run faster on the 1-CTA kernel (measured:
   // C2 expert GEMMs 1.45 ms on pairs vs 1.15 ms on single CTAs)
-  // fused dispatch (a6 → a7): every rank in this process, so GEMM1 can gather the x rows itself
-  const bool fused = ctx->fused_dispatch != 0 && !ctx->multi_process() && !f32;
-  const bool sw_gather = fused && ctx->fused_dispatch == 2;        // cp.async gather: 1-CTA kernel
-  const bool pair = ctx->pair_gemm && !sw_gather && static_cast<int64_t>(T) * d.k * d.G >= 256LL * d.E;
+  const bool pair = ctx->pair_gemm && static_cast<int64_t>(T) * d.k * d.G >= 256LL * d.E;
   li.tile_m = pair ? 256 : 128;
   li.act = ctx->scratch + s.act;
   li.y_local = ctx->local_base[PROBE_BUF_Y];
-  const CUtensorMap* mxg = fused && ctx->fused_dispatch == 1 ? ctx->maps.get(x, GL * T, d.H, 1) : nullptr;
-  if (fused && ctx->fused_dispatch == 1 && !mxg) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
-  li.gather_idx = fused ? ctx->at<int32_t>(s.gidx) : nullptr;
-  li.gather_src = sw_gather ? x : nullptr;
   li.f32 = f32;
-  // overlapped dispatch (a6 ∥ a7): single process, CTA-pair GEMM1, 128-aligned capacity
-  const bool overlap = ctx->overlap_dispatch && !fused && !ctx->multi_process() && !f32 && pair &&
-                       d.cap % 128 == 0 && ctx->pair_gemm;
-  li.a_ready = overlap ? ctx->at<int32_t>(s.ready) : nullptr;
   li.l2hint = ctx->l2hint;
   LayoutOut lo;
   lo.split_cum = ctx->at<int32_t>(s.split_cum);
@@ -747,7 +699,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   CKL();
   MARK(4);
   // a6 dispatch
-  const bool dedup = ctx->cfg.dedup_wire != 0 && !fused && !overlap;
+  const bool dedup = ctx->cfg.dedup_wire != 0;
   const int KQ = d.k < d.G ? d.k : d.G;      // distinct destinations per token, at most
   {
     const int warps = d.GL * T;
@@ -764,14 +716,13 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
                                                   ctx->at<int32_t>(s.ids),
                                                   ctx->at<int32_t>(s.pos), ctx->at<int32_t>(s.cbase),
                                                   lo.split_cum, lo.slot_of, lo.src_off, ctx->at<int32_t>(s.route),
-                                                  sym_of(ctx), PROBE_BUF_RECV, err,
-                                                  (fused || overlap) ? ctx->at<int32_t>(s.gidx) : nullptr);
+                                                  sym_of(ctx), PROBE_BUF_RECV, err);
     }
     CKL();
   }
   CK(ev_record(ctx, ctx->ev_disp[p], st));
   if (predisp) CK(ev_wait(ctx, st, ctx->ev_pd_done));  // pre-dispatched rows complete before the barrier
-  if (!overlap) CK(xbarrier(ctx, BAR_DISPATCH, st));   // every peer's rows have landed in our receive buffers
+  CK(xbarrier(ctx, BAR_DISPATCH, st));                // every peer's rows have landed in our receive buffers
   MARK(5);
   if (dedup) {
     // receiver: expand each (token, dest) wire row into the pair's other slot rows (local HBM)
@@ -780,44 +731,21 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
     CKL();
   }
   MARK(6);
-  if (overlap) {
-    // slots ready before the copy (nothing may sit between the copy and the dependent GEMM1)
-    if (use_plan) CK(ev_wait(ctx, st, ctx->ev_slots[p]));
-    const bool serial = ctx->overlap_dispatch == 2;   // analysis: copy, then the capped GEMM1 (no PDL)
-    if (!serial) MARK(7);
-    CK(ev_record(ctx, ctx->ev_gemm[p], st));
-    k_dispatch_pull<<<ctx->num_sms, 256, 0, st>>>(d, static_cast<const uint8_t*>(x), static_cast<int>(H * 2),
-                                                  ctx->at<int32_t>(s.gidx), lo.group_rows, lo.s1,
-                                                  ctx->at<int32_t>(s.ready),
-                                                  static_cast<uint8_t*>(ctx->local_base[PROBE_BUF_RECV]),
-                                                  li.nparts > 1 ? 1 : 0);
-    CKL();
-    if (serial) MARK(7);
-    CK(launch_gemm1_overlap(ctx->map_recv, *m13, ctx->map_rw13, ctx->map_recv, lo.s1, d.H, ctx->num_sms, st,
-                            !serial));
-    ++ctx->launches;
-  } else {
-    // a9 phase lock: the expert GEMMs need this layer's replica slots
-    if (use_plan) CK(ev_wait(ctx, st, ctx->ev_slots[p]));
-    MARK(7);
-    CK(ev_record(ctx, ctx->ev_gemm[p], st));
-  }
+  // a9 phase lock: the expert GEMMs need this layer's replica slots
+  if (use_plan) CK(ev_wait(ctx, st, ctx->ev_slots[p]));
+  MARK(7);
+  CK(ev_record(ctx, ctx->ev_gemm[p], st));
   // a7 grouped SwiGLU expert FFN (tcgen05): act = SiLU(X W_gᵀ) ⊙ X W_uᵀ ; Y = act W_dᵀ
   const int vexp = pair ? V_2CTA_256_6_4 : V_256_4_4_EXP;
-  if (!overlap) {   // R26: the measured hiding window starts with the expert GEMMs
-    k_window_stamp<<<1, 1, 0, st>>>(d, ctx->at<int64_t>(s.win_t0), 0, sym_of(ctx), PROBE_BUF_BOARD, lo.group_rows);
-    CKL();
-  }
-  if (overlap) {
-    // GEMM1 already enqueued beside the pull copy
-  } else if (f32) {
+  // R26: the measured hiding window starts with the expert GEMMs
+  k_window_stamp<<<1, 1, 0, st>>>(d, ctx->at<int64_t>(s.win_t0), 0, sym_of(ctx), PROBE_BUF_BOARD, lo.group_rows);
+  CKL();
+  if (f32) {
     CK(launch_sgemm(ctx, lo.s1, ctx->local_base[PROBE_BUF_RECV], w13, ctx->local_base[PROBE_BUF_REP_W13], d.H, st));
-    ++ctx->launches;
   } else {
-    CK(launch_gemm_v(vexp, mxg ? *mxg : ctx->map_recv, *m13, ctx->map_rw13, ctx->map_recv, lo.s1, d.H, ctx->num_sms,
-                     st));
-    ++ctx->launches;
+    CK(launch_gemm_v(vexp, ctx->map_recv, *m13, ctx->map_rw13, ctx->map_recv, lo.s1, d.H, ctx->num_sms, st));
   }
+  ++ctx->launches;
   MARK(8);
   if (f32) {
     CK(launch_sgemm(ctx, lo.s2, ctx->scratch + s.act, w2, ctx->local_base[PROBE_BUF_REP_W2], d.F, st));
@@ -825,10 +753,8 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
     CK(launch_gemm_v(vexp, ctx->map_act, *m2, ctx->map_rw2, ctx->map_y, lo.s2, d.F, ctx->num_sms, st));
   }
   ++ctx->launches;
-  if (!overlap) {
-    k_window_stamp<<<1, 1, 0, st>>>(d, ctx->at<int64_t>(s.win_t0), 1, sym_of(ctx), PROBE_BUF_BOARD, lo.group_rows);
-    CKL();
-  }
+  k_window_stamp<<<1, 1, 0, st>>>(d, ctx->at<int64_t>(s.win_t0), 1, sym_of(ctx), PROBE_BUF_BOARD, lo.group_rows);
+  CKL();
   if (!dedup) CK(xbarrier(ctx, BAR_Y, st));     // every expert rank's Y rows are complete (the combine pulls)
   MARK(9);
   // a8 combine (raises the prefetch suspend flag, R27)
@@ -1162,8 +1088,8 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
       reps < 1 || mode < 0 || mode > 7)
     return fail(nullptr, PROBE_EINVAL, "probe_test_gemm: bad arguments");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (variant < 0) variant = mode == 1 ? V_256_4_4 : (mode == 2 ? V_256_3_8 : V_128_6_4);
-  if (variant > V_256_4_4_EXP) return fail(nullptr, PROBE_EINVAL, "bad variant");
+  if (variant < 0) variant = mode == 1 || mode == 2 ? V_256_4_4 : V_128_6_4;
+  if (!variant_ok(variant)) return fail(nullptr, PROBE_EINVAL, "variant %d not available", variant);
   const int TM = variant_tm(variant);
   const int BN = variant_bn(variant);
   const int emode = mode == 1 ? EPI_SWIGLU
@@ -1182,6 +1108,7 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
   std::vector<uint8_t> host(sizeof(GemmSched), 0);
   GemmSched* hs = reinterpret_cast<GemmSched*>(host.data());
   hs->num_groups = num_groups;
+  if (const char* h = getenv("PROBE_L2HINT")) hs->l2hint = static_cast<int>(strtol(h, nullptr, 0)) & 7;
   unsigned long long* dstats = nullptr;
   if (getenv("PROBE_GEMM_STATS")) {
     CK(cudaMalloc(&dstats, 8 * sizeof(unsigned long long)));
@@ -1500,14 +1427,6 @@ probe_status probe_set_option(probe_ctx ctx, int32_t option, int64_t value) {
     case PROBE_OPT_PRED_MAXREG:
       if (value != 0 && value != 192) return fail(ctx, PROBE_EINVAL, "predictor register cap %lld not in {0, 192}", (long long)value);
       ctx->pred_maxreg = static_cast<int>(value);
-      return PROBE_OK;
-    case PROBE_OPT_FUSED_DISPATCH:
-      if (value < 0 || value > 2) return fail(ctx, PROBE_EINVAL, "fused dispatch mode %lld not in {0,1,2}", (long long)value);
-      ctx->fused_dispatch = static_cast<int>(value);
-      return PROBE_OK;
-    case PROBE_OPT_OVERLAP_DISPATCH:
-      if (value < 0 || value > 2) return fail(ctx, PROBE_EINVAL, "overlap mode %lld not in {0,1,2}", (long long)value);
-      ctx->overlap_dispatch = static_cast<int>(value);
       return PROBE_OK;
     case PROBE_OPT_AUX_SMS:
       if (value < 1 || value > ctx->num_sms) return fail(ctx, PROBE_EINVAL, "aux SM cap %lld out of range", (long long)value);

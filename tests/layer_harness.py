@@ -36,8 +36,6 @@ class CaseCfg:
     ep_emulation: bool = False      # partitioned expert GEMMs (single-GPU EP straggler emulation)
     fused_epi_topk: bool = False    # router/predictor top-k in the GEMM epilogue
     pair_gemm: bool = True          # expert GEMMs on CTA pairs (cta_group::2); False → 1-CTA kernel
-    fused_dispatch: int = 0         # 1/2: GEMM1 gathers x rows (TMA gather4 / cp.async) instead of the receive copy
-    overlap_dispatch: Optional[bool] = None   # pull-copy dispatch overlapped with GEMM1 (None: library default)
     dtype: str = "bf16"             # "fp32": parity path (fp32 operands, SIMT fp32 GEMMs, fp32 expert weights)
     max_tokens: int = 0             # >T: context capacity above the T this layer call runs with
     gen: str = "hadamard"           # "natural": 5-bit dyadic x / router, dyadic Zipf bias, duplicated router rows
@@ -83,13 +81,6 @@ def run_gpu(case: CaseCfg):
     if not case.pair_gemm:
         from paper_2602_00509_b200._lib import OPT_PAIR_GEMM
         rt.set_option(OPT_PAIR_GEMM, 0)
-    if case.fused_dispatch:
-        from paper_2602_00509_b200._lib import OPT_FUSED_DISPATCH
-        rt.set_option(OPT_FUSED_DISPATCH, int(case.fused_dispatch))
-        rt._fused_dispatch = int(case.fused_dispatch)
-    if case.overlap_dispatch is not None:
-        from paper_2602_00509_b200._lib import OPT_OVERLAP_DISPATCH
-        rt.set_option(OPT_OVERLAP_DISPATCH, int(case.overlap_dispatch))
     if case.fused_epi_topk:
         from paper_2602_00509_b200._lib import OPT_FUSED_EPILOGUE_TOPK
         rt.set_option(OPT_FUSED_EPILOGUE_TOPK, 1)
@@ -179,7 +170,7 @@ def debug(rt, cfg, T=None, x=None):
     torch.cuda.synchronize()
     out = dict(counts=counts.cpu().numpy(), split_cum=split.cpu().numpy(), route=route.cpu().numpy(),
                group_rows=rows.cpu().numpy(), replicas=reps.cpu().numpy())
-    if x is not None and not getattr(rt, "_fused_dispatch", 0):   # fused modes gather from x, no receive copy
+    if x is not None:
         out["recv_ok"] = recv_rows_match(rt, cfg, x, route)
     return out
 

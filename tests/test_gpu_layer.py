@@ -38,26 +38,6 @@ CASES = {
     "pair-gemm": CaseCfg(pi.C0.with_(name="pgl", E=16, k=4, H=256, F=256, T=700, G=4), zipf_s=1.3),
     "pair-gemm-ep-emulation": CaseCfg(pi.C0.with_(name="pgle", E=16, k=4, H=256, F=384, T=600, G=4), zipf_s=1.2,
                                       ep_emulation=True),
-    # opt-in fused dispatch: expert GEMM1 gathers its rows from x with TMA gather4
-    "fused-dispatch-gather": CaseCfg(pi.C0.with_(name="fdg", E=16, k=4, H=512, F=384, T=1100, G=4), zipf_s=1.3,
-                                     fused_dispatch=True),
-    "fused-dispatch-gather-one-cta": CaseCfg(pi.C0.with_(name="fdg1", E=32, k=4, H=512, F=256, T=200, G=4),
-                                             zipf_s=1.3, fused_dispatch=True, pair_gemm=False),
-    "fused-dispatch-gather-ep-emulation": CaseCfg(pi.C0.with_(name="fdge", E=64, k=8, H=512, F=256, T=256, G=8),
-                                                  zipf_s=1.2, fused_dispatch=True, ep_emulation=True),
-    "fused-dispatch-cp-async": CaseCfg(pi.C0.with_(name="fdc", E=32, k=4, H=512, F=384, T=333, G=4), zipf_s=1.3,
-                                       fused_dispatch=2),
-    "fused-dispatch-cp-async-ep-emulation": CaseCfg(pi.C0.with_(name="fdce", E=64, k=8, H=512, F=256, T=256, G=8),
-                                                    zipf_s=1.2, fused_dispatch=2, ep_emulation=True),
-    # overlapped dispatch: pull copy in GEMM tile order, GEMM1 beside it (PDL) acquiring per-block flags
-    "overlap-dispatch": CaseCfg(pi.C0.with_(name="ovd", E=16, k=4, H=512, F=384, T=1100, G=4), zipf_s=1.3,
-                                overlap_dispatch=True),
-    "overlap-dispatch-ragged": CaseCfg(pi.C0.with_(name="ovr", E=16, k=4, H=256, F=256, T=701, G=4), zipf_s=1.2,
-                                       overlap_dispatch=True, bias=True),
-    "overlap-dispatch-ep-emulation": CaseCfg(pi.C0.with_(name="ove", E=16, k=4, H=256, F=384, T=600, G=4),
-                                             zipf_s=1.2, overlap_dispatch=True, ep_emulation=True),
-    "overlap-dispatch-off": CaseCfg(pi.C0.with_(name="ovo", E=16, k=4, H=256, F=256, T=700, G=4), zipf_s=1.3,
-                                    overlap_dispatch=False),
     # degenerate top-k: k = 1, k = E (every expert chosen by every token), k = 9 > 8 (unfused select kernel; the exact-bf16 encoding caps k near 9)
     "k1": CaseCfg(pi.C0.with_(name="k1", E=8, k=1, H=256, F=256, T=130, G=2), zipf_s=1.5),
     "k-eq-E": CaseCfg(pi.C0.with_(name="kE", E=8, k=8, H=256, F=128, T=70, G=2), zipf_s=1.0),

@@ -21,9 +21,9 @@ import bench  # noqa: E402
 
 
 def point(shape, s, G, steps):
-    a = argparse.Namespace(gpus=1, steps=steps, warmup=3, impl="probe", config=shape, zipf=s, no_e2e=True,
-                           no_cpu=True, no_emulation=(G == 1), ep=G, fused_dispatch=0, cap=4.0, aux_sms=0,
-                           cpu_tokens=0, ref_tokens=0, overlap=None, out_fp32=False)
+    argv = ["--steps", str(steps), "--warmup", "3", "--config", shape, "--zipf", str(s), "--ep", str(G),
+            "--no-e2e", "--no-cpu", "--no-decode", "--no-dedup-sub"] + (["--no-emulation"] if G == 1 else [])
+    a = bench.parse_args(argv)
     with redirect_stdout(io.StringIO()):
         r = bench.run_probe(a)
     em = r.get("ep_emulation") or {}
