@@ -204,8 +204,9 @@ probe_status probe_debug_prefetch(probe_ctx ctx, int32_t* out, void* stream);
  * window_ns[r] (device int64 [G] out) = the most recently measured expert-GEMM phase of rank r
  * (%globaltimer stamps around GEMM1..GEMM2 of every probe_moe_forward, all-gathered into every
  * rank's count board, so all ranks plan from identical windows; when a process hosts several
- * logical ranks their tiles share one grouped GEMM and rank r gets the row share
- * T_GEMM · rows_r / Σ rows, its GEMM time on a GPU of its own), or fallback_ns where no layer
+ * logical ranks their tiles share one grouped GEMM and rank r gets its share by the planner's
+ * compute cost, T_GEMM · C_r / Σ C with C_r = Σ_{active slots} max(rows, n_sat) (R11) — its GEMM
+ * time on a GPU of its own), or fallback_ns where no layer
  * has been measured yet, plus attention_ns (the attention window that follows, caller-given).
  * Device to device, no host synchronisation; enqueued on `stream` (NULL = the aux stream, i.e.
  * before a probe_plan issued without a stream).  One step stale by construction (R26). */

@@ -345,27 +345,34 @@ __global__ void k_pred_publish(Dims d, const int32_t* __restrict__ pred_local, S
 // rank plans from the same all-gathered windows (R10).  One process per GPU (one local rank):
 // the window is the measured GEMM time.  Several logical ranks sharing one GPU run their
 // tiles in one grouped GEMM, so the measured time covers all of them; rank r's window is then
-// its share by rows, T_GEMM · rows_r / Σ rows — the time its GEMMs take when the GPU is its
-// own, i.e. the window it has on the system being emulated.  One thread.
+// its share of it by the planner's own compute cost (R11), T_GEMM · C_r / Σ C with
+// C_r = Σ_{slots j of r with rows} max(rows_j, n_sat) — the time its GEMMs take on a GPU of its
+// own: rows for prefill-sized groups, weight streaming (n_sat per active expert) for decode.
 __device__ __forceinline__ int64_t* window_board(const Dims& d, uint8_t* board) {
   return reinterpret_cast<int64_t*>(board + static_cast<size_t>(4) * d.G * d.E * 4);
 }
+__device__ __forceinline__ int64_t rank_gemm_cost(const Dims& d, const int32_t* group_rows, int r, int n_sat) {
+  const int S = d.EL + kMaxRb;
+  int64_t c = 0;
+  for (int j = 0; j < S; ++j) {
+    const int m = group_rows[r * S + j];
+    if (m > 0) c += m > n_sat ? m : n_sat;
+  }
+  return c;
+}
 __global__ void k_window_stamp(Dims d, int64_t* t0, int phase, Sym sym, int buf_board,
-                               const int32_t* __restrict__ group_rows) {
+                               const int32_t* __restrict__ group_rows, int n_sat) {
   const uint64_t now = ptx::globaltimer_ns();
   if (phase == 0) {
     *t0 = static_cast<int64_t>(now);
     return;
   }
   const int64_t w = static_cast<int64_t>(now) - *t0;
-  const int S = d.EL + kMaxRb;
   int64_t tot = 0;
-  for (int gl = 0; gl < d.GL; ++gl)
-    for (int j = 0; j < S; ++j) tot += group_rows[(d.R0 + gl) * S + j];
+  for (int gl = 0; gl < d.GL; ++gl) tot += rank_gemm_cost(d, group_rows, d.R0 + gl, n_sat);
   for (int gl = 0; gl < d.GL; ++gl) {
-    int64_t rows = 0;
-    for (int j = 0; j < S; ++j) rows += group_rows[(d.R0 + gl) * S + j];
-    const int64_t wr = (d.GL == 1 || tot == 0) ? w : w * rows / tot;
+    const int64_t c = rank_gemm_cost(d, group_rows, d.R0 + gl, n_sat);
+    const int64_t wr = (d.GL == 1 || tot == 0) ? w : w * c / tot;
     for (int r = 0; r < d.G; ++r) window_board(d, sym.at(buf_board, d.G, r))[d.R0 + gl] = wr > 0 ? wr : 1;
   }
 }

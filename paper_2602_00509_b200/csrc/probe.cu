@@ -738,7 +738,8 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   // a7 grouped SwiGLU expert FFN (tcgen05): act = SiLU(X W_gᵀ) ⊙ X W_uᵀ ; Y = act W_dᵀ
   const int vexp = pair ? V_2CTA_256_6_4 : V_256_4_4_EXP;
   // R26: the measured hiding window starts with the expert GEMMs
-  k_window_stamp<<<1, 1, 0, st>>>(d, ctx->at<int64_t>(s.win_t0), 0, sym_of(ctx), PROBE_BUF_BOARD, lo.group_rows);
+  k_window_stamp<<<1, 1, 0, st>>>(d, ctx->at<int64_t>(s.win_t0), 0, sym_of(ctx), PROBE_BUF_BOARD, lo.group_rows,
+                                  ctx->cfg.n_sat);
   CKL();
   if (f32) {
     CK(launch_sgemm(ctx, lo.s1, ctx->local_base[PROBE_BUF_RECV], w13, ctx->local_base[PROBE_BUF_REP_W13], d.H, st));
@@ -753,7 +754,8 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
     CK(launch_gemm_v(vexp, ctx->map_act, *m2, ctx->map_rw2, ctx->map_y, lo.s2, d.F, ctx->num_sms, st));
   }
   ++ctx->launches;
-  k_window_stamp<<<1, 1, 0, st>>>(d, ctx->at<int64_t>(s.win_t0), 1, sym_of(ctx), PROBE_BUF_BOARD, lo.group_rows);
+  k_window_stamp<<<1, 1, 0, st>>>(d, ctx->at<int64_t>(s.win_t0), 1, sym_of(ctx), PROBE_BUF_BOARD, lo.group_rows,
+                                  ctx->cfg.n_sat);
   CKL();
   if (!dedup) CK(xbarrier(ctx, BAR_Y, st));     // every expert rank's Y rows are complete (the combine pulls)
   MARK(9);

@@ -106,13 +106,14 @@ def test_measured_window_feeds_planner():
     torch.cuda.synchronize()
     w = win.cpu().numpy()
     assert (w > attn).all() and (w < attn + 10 ** 9).all()      # measured (not the fallback)
-    # one process hosts all ranks: one grouped GEMM, rank r's window = its row share of it
+    # one process hosts all ranks: one grouped GEMM; rank r's window = its share by the planner's
+    # compute cost Σ_active slots max(rows, n_sat) (n_sat = 0 here: the row share)
     rows = torch.empty(sh.G, sh.E // sh.G + 3, dtype=torch.int32, device="cuda")
     rt.debug_layout(group_rows=rows)
     torch.cuda.synchronize()
     share = rows.sum(dim=1).double().cpu().numpy()
     m = (w - attn).astype(np.float64)
-    assert np.allclose(m / m.sum(), share / share.sum(), atol=1e-6)
+    assert np.allclose(m / m.sum(), share / share.sum(), rtol=1e-3, atol=1e-4)   # integer ns division
     nhat = np.zeros((sh.G, sh.E), dtype=np.int32)
     nhat[:, :4] = 400                                            # rank 0's experts hot everywhere
     nhat[:, 4:] = 10
