@@ -125,38 +125,13 @@ __device__ __forceinline__ void bulk_wait() {
   asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
 // Ampere-style async copy global → shared (16 bytes, L2 only) and its group bookkeeping.
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
 // Named barrier over `n` threads (id 1..15; id 0 is __syncthreads).
-__device__ __forceinline__ void named_bar_sync(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 // Generic-proxy global writes ↔ async-proxy (TMA) global reads of the same data.
-__device__ __forceinline__ void fence_proxy_async_global() {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-__device__ __forceinline__ int ld_acquire_gpu(const int32_t* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_gpu(int32_t* p, int v) {
-  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 // Programmatic dependent launch: let the next kernel in the stream (launched with
 // cudaLaunchAttributeProgrammaticStreamSerialization) start while this grid runs.
-__device__ __forceinline__ void griddep_launch_dependents() {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
 
 // ---------------------------------------------------------------- tcgen05
 // Shared-memory matrix descriptor (tcgen05 "matrix descriptor"): K-major operand
@@ -268,26 +243,6 @@ __device__ __forceinline__ void st_cluster_u32(uint32_t cluster_addr, uint32_t v
 }
 // 2-CTA TMA load: data lands in THIS CTA's smem, the transaction bytes are counted on the
 // LEADER CTA's mbarrier (peer bit 24 of the shared::cluster address cleared).
-// TMA gather4 (sm_100a): 4 rows r0..r3 × box[0] columns from a 2-D map whose box is {cols, 1},
-// written as 4 consecutive smem rows (the swizzle follows the smem address, like a tile load).
-__device__ __forceinline__ void tma_gather4(const CUtensorMap* m, uint64_t* bar, void* dst, int c0, int r0, int r1,
-                                            int r2, int r3) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
-      : "memory");
-}
-// CTA-pair form: completes on the LEADER CTA's barrier (peer bit of the address cleared).
-__device__ __forceinline__ void tma_gather4_cg2(const CUtensorMap* m, uint64_t* bar_local, void* dst, int c0, int r0,
-                                                int r1, int r2, int r3) {
-  const uint32_t bar = smem_u32(bar_local) & 0xFEFFFFFFu;
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
-      : "memory");
-}
 __device__ __forceinline__ void tma_load_2d_cg2(const CUtensorMap* m, uint64_t* bar_local, void* dst, int c0, int c1) {
   const uint32_t bar = smem_u32(bar_local) & 0xFEFFFFFFu;
   asm volatile(
