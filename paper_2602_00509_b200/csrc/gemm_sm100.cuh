@@ -81,15 +81,23 @@ struct GemmSched {
 // emulation): CTA b serves only partition b % nparts (its logical rank's tiles), so a rank's
 // expert GEMM runs on ~#SMs/nparts SMs and the launch time is the straggler's (Eq. 3).
 constexpr int kTileQ = 8;
-__device__ __forceinline__ int claim_tile(GemmSched* s, int unit = -1) {
+// Claim split in two so the atomic's latency hides behind a whole tile of TMA issue: the raw
+// counter value is requested when a tile starts and turned into a tile id (or -1) when the
+// next tile is published (K = 768 tiles are only 12 k-blocks long, so a claim at the tile
+// boundary can show up as operand waits of the MMA).
+__device__ __forceinline__ int claim_raw(GemmSched* s, int unit) {
+  const int np = s->nparts;
+  if (np > 1) return atomicAdd(&s->part_counter[(unit < 0 ? static_cast<int>(blockIdx.x) : unit) % np], 1);
+  return atomicAdd(&s->counter, 1);
+}
+__device__ __forceinline__ int claim_finish(const GemmSched* s, int unit, int raw) {
   const int np = s->nparts;
   if (np > 1) {
     const int p = (unit < 0 ? static_cast<int>(blockIdx.x) : unit) % np;
-    const int t = s->part_tile[p] + atomicAdd(&s->part_counter[p], 1);
+    const int t = s->part_tile[p] + raw;
     return t < s->part_tile[p + 1] ? t : -1;
   }
-  const int t = atomicAdd(&s->counter, 1);
-  return t < s->total_tiles ? t : -1;
+  return raw < s->total_tiles ? raw : -1;
 }
 
 __device__ __forceinline__ void sched_reset_counters(GemmSched* s) {
@@ -458,10 +466,12 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     uint32_t phase = 0;
     int qs = 0;
     uint32_t qph = 0;
+    int raw_next = lane == 0 ? claim_raw(sched, -1) : 0;
     while (true) {
       int tile = 0;
       if (lane == 0) {
-        tile = claim_tile(sched);
+        tile = claim_finish(sched, -1, raw_next);
+        if (tile >= 0) raw_next = claim_raw(sched, -1);   // next tile's claim in flight during this tile
         ptx::mbar_wait(&qempty[qs], qph ^ 1);
         tq[qs] = tile;
         ptx::mbar_arrive(&qfull[qs]);
@@ -682,11 +692,13 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
     uint32_t phase = 0;
     int qs = 0;
     uint32_t qph = 0;
+    int raw_next = (lane == 0 && leader) ? claim_raw(sched, unit) : 0;
     while (true) {
       int tile = 0;
       if (lane == 0) {
         if (leader) {
-          tile = claim_tile(sched, unit);
+          tile = claim_finish(sched, unit, raw_next);
+          if (tile >= 0) raw_next = claim_raw(sched, unit);   // next claim in flight during this tile
           ptx::mbar_wait(&qempty[qs], qph ^ 1);
           tq[qs] = tile;
           ptx::st_cluster_u32(ptx::mapa(ptx::smem_u32(const_cast<int*>(&tq[qs])), 1), static_cast<uint32_t>(tile));
