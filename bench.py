@@ -503,12 +503,28 @@ def measure(shape, args, env, light=False, dedup=None, predispatch=False):
                 "expert_ffn": {"achieved": (fl1 + fl2) / (t1 + t2) / 1e12,
                                "frac": (fl1 + fl2) / (t1 + t2) / 1e12 / peak_tf}}
     # ---- dispatch / combine against the HBM roofline (one GPU: every "peer" store is local HBM)
-    byd = (G * T * H * 2 + pairs * H * 2) / world
-    byc = (pairs * H * 2 + G * T * H * out.element_size()) / world                # fp16 Y in, bf16/fp32 out
-    bw_report = {"dispatch": {"algorithmic_bytes": byd, "GBps": byd / (phases["dispatch"] / 1e3) / 1e9,
-                              "frac_hbm": byd / (phases["dispatch"] / 1e3) / 1e9 / peak_bw},
-                 "combine": {"algorithmic_bytes": byc, "GBps": byc / (phases["combine"] / 1e3) / 1e9,
-                             "frac_hbm": byc / (phases["combine"] / 1e3) / 1e9 / peak_bw}}
+    if cfg.dedup_wire:   # x read + one row per unique (token, dest) + 16-B meta per slot; Y read + partials out/in + out
+        # (wire rows are this process's own ranks' rows; G·T and pairs cover the EP group)
+        byd = (G * T * H * 2 + pairs * 16) / world + wire["rows_unique_token_dest"] * H * 2
+        byc = (pairs * H * 2 + G * T * H * out.element_size()) / world + 2 * wire["rows_unique_token_dest"] * H * 2
+    else:                # x read + one row per routed pair; fp16 Y rows in, bf16/fp32 out
+        byd = (G * T * H * 2 + pairs * H * 2) / world
+        byc = (pairs * H * 2 + G * T * H * out.element_size()) / world
+    # §8(d)'s unit for the All-to-All: 2H bytes per unique (token, REMOTE destination) — the
+    # bytes that would cross NVLink on 8 GPUs; here every "remote" row lands in local HBM
+    s8d = 2.0 * H * wire["rows_unique_remote"]          # this process's ranks' rows
+    disp_ms = phases["dispatch"]
+    comb_ms = phases["combine"] + phases["reduce"]
+    bw_report = {"dispatch": {"algorithmic_bytes": byd, "GBps": byd / (disp_ms / 1e3) / 1e9,
+                              "frac_hbm": byd / (disp_ms / 1e3) / 1e9 / peak_bw,
+                              "s8d_bytes": s8d, "s8d_GBps": s8d / (disp_ms / 1e3) / 1e9,
+                              "s8d_frac_hbm": s8d / (disp_ms / 1e3) / 1e9 / peak_bw},
+                 "combine": {"algorithmic_bytes": byc, "GBps": byc / (comb_ms / 1e3) / 1e9,
+                             "frac_hbm": byc / (comb_ms / 1e3) / 1e9 / peak_bw,
+                             "s8d_bytes": s8d, "s8d_GBps": s8d / (comb_ms / 1e3) / 1e9},
+                 "note": "algorithmic_bytes = this kernel's own HBM traffic model (per-slot rows: x read + 2H per "
+                         "routed pair written); s8d = SURVEY §8(d)'s 2H B per unique (token, remote destination). "
+                         "One GPU: the 'NVLink' bytes are local HBM, so fractions are of HBM"}
     result = None
     decode = shape.name == "C2"
     if rank == 0 and light:
@@ -525,7 +541,7 @@ def measure(shape, args, env, light=False, dedup=None, predispatch=False):
                               "ms_per_step": ms_static, "speedup_probe_vs_static": ms_static / ms,
                               "phases_ms": static_phases},
                 "phases_ms": phases, "gpu_launches": launches, "clocks": clocks, "prefetch": prefetch, "wire": wire,
-                "predispatch": pred_disp, "window": window_rep,
+                "predispatch": pred_disp, "window": window_rep, "bandwidth": bw_report,
                 "balance": {"ir_pre": ir_pre, "ir_post": ir_post, "replicas": nrep,
                             "planner_iterations": stats[0]}}
     if rank == 0:
