@@ -47,11 +47,14 @@ def test_planner_kernel_matches_oracle(seed):
     rt.close()
 
 
-def test_history_hook_feeds_planner():
+@pytest.mark.parametrize("budget", [3, 2])
+def test_history_hook_feeds_planner(budget):
+    """NEXT-3: the statistics-based one-shot policy (history of actual counts → the same
+    planner); budget 2 = the paper's EPLB configuration, 2 redundant slots per rank."""
     import probe_inputs as pi
     sh = pi.C0.with_(name="hist", E=16, k=2, H=256, F=256, T=128, G=4)
     from paper_2602_00509_b200 import ProbeConfig, ProbeRuntime
-    cfg = ProbeConfig(G=sh.G, E=sh.E, k=sh.k, H=sh.H, F=sh.F, T=sh.T, h=sh.h)
+    cfg = ProbeConfig(G=sh.G, E=sh.E, k=sh.k, H=sh.H, F=sh.F, T=sh.T, h=sh.h, replica_budget=budget)
     rt = ProbeRuntime(cfg)
     W = pi.router_weight(sh, 0, device="cuda")
     w13, w2 = pi.expert_weights(sh, 0, device="cuda")
@@ -71,8 +74,9 @@ def test_history_hook_feeds_planner():
     win = torch.full((sh.G,), 10 ** 9, dtype=torch.int64, device="cuda")
     rt.plan(7, win, pred_counts=hist, replicas=reps)
     torch.cuda.synchronize()
-    pc = O.PlannerConfig(G=sh.G, E=sh.E, alpha_ps=1, beta_ps=0, expert_bytes=6 * sh.H * sh.F)
+    pc = O.PlannerConfig(G=sh.G, E=sh.E, replica_budget=budget, alpha_ps=1, beta_ps=0, expert_bytes=6 * sh.H * sh.F)
     plan = O.plan_greedy(total, [10 ** 9] * sh.G, pc)
+    assert max(len(r) for r in plan.replicas) <= budget
     exp = np.full((sh.G, 3), -1)
     for g in range(sh.G):
         exp[g, :len(plan.replicas[g])] = plan.replicas[g]

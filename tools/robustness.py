@@ -18,6 +18,7 @@ import torch
 sys.path.insert(0, ".")
 import probe_inputs as pi  # noqa: E402
 from paper_2602_00509_b200 import ProbeConfig, ProbeRuntime  # noqa: E402
+from paper_2602_00509_b200._lib import PHASES  # noqa: E402
 from paper_2602_00509_b200._lib import OPT_EP_EMULATION  # noqa: E402
 from paper_2602_00509_b200.costs import cost_model, window_ns  # noqa: E402
 
@@ -32,10 +33,14 @@ args = ap.parse_args()
 shape = pi.C1.with_(T=args.T)
 G, E, k, H, F, T = shape.G, shape.E, shape.k, shape.H, shape.F, shape.T
 a, b, n, bw = cost_model(H, F)
-cfg = ProbeConfig(G=G, E=E, k=k, H=H, F=F, T=T, h=shape.h, n_sat=n, alpha_ps=a, beta_ps=b, bw_bytes_per_us=bw,
-                  capacity_factor=4.0)
-rt = ProbeRuntime(cfg)
-rt.set_option(OPT_EP_EMULATION, 1)
+# PROBE: 3 redundant experts per rank; the statistics-based one-shot policy is configured
+# as the paper's EPLB baseline, 2 redundant expert slots per layer per rank
+rts = {}
+for name, budget in (("probe", 3), ("eplb", 2)):
+    cfg = ProbeConfig(G=G, E=E, k=k, H=H, F=F, T=T, h=shape.h, n_sat=n, alpha_ps=a, beta_ps=b,
+                      bw_bytes_per_us=bw, capacity_factor=4.0, replica_budget=budget)
+    rts[name] = ProbeRuntime(cfg)
+    rts[name].set_option(OPT_EP_EMULATION, 1)
 dev = "cuda"
 POOL = 4
 pools = {ph: [pi.layer_inputs(shape, 0, i, args.zipf, device=dev, wrap=POOL, perm_key=key) for i in range(POOL)]
@@ -49,6 +54,7 @@ hist = [torch.zeros(G, E, dtype=torch.int32, device=dev) for _ in (0, 1)]
 
 
 def run(policy):
+    rt = rts["eplb" if policy == "eplb" else "probe"]
     seq = ["A"] * args.layers_a + ["B"] * args.layers_b
     rt.profile(len(seq))
     planned = False
@@ -69,7 +75,7 @@ def run(policy):
                 rt.plan(L + 1, win, pred_counts=hist[q])
                 rt.prefetch(L + 1, ex[q][0], ex[q][1], phase=0)
                 planned = True
-    ms = rt.profile_read()[:, -1].numpy()
+    ms = rt.profile_read()[:, PHASES.index("total")].numpy()
     na = args.layers_a
     skip = max(args.history + 2, 4)
     return {"phase_A_ms": float(np.mean(ms[skip:na])), "phase_B_ms": float(np.mean(ms[na + 2:])),
@@ -82,5 +88,6 @@ for policy in ("static", "probe", "eplb"):
     result[policy] = run(policy)
 result["config"] = {"shape": "C1", "T": T, "G": G, "zipf": args.zipf, "layers_a": args.layers_a,
                     "layers_b": args.layers_b, "history_layers": args.history,
+                    "replica_budget": {"probe": 3, "eplb": 2},
                     "note": "EP straggler emulation on one B200; hotspot permutation A then B"}
 print(json.dumps(result))
