@@ -1279,7 +1279,7 @@ __global__ void __launch_bounds__(128) k_combine_reduce(Dims d, int T, const int
 // The first CTA raises the prefetch suspend flag (split-phase, R27).
 // block per token, 128 threads.
 // =============================================================================
-template <bool OUT_F32, bool Y_F32 = false>
+template <bool OUT_F32, bool Y_F32 = false, int KC = kMaxK>
 __global__ void __launch_bounds__(128) k_combine(Dims d, int T, const float* __restrict__ gw,
                                                  const int32_t* __restrict__ route, Sym sym, int buf_y, void* out,
                                                  volatile int32_t* suspend_flag, int layer) {
@@ -1305,24 +1305,34 @@ __global__ void __launch_bounds__(128) k_combine(Dims d, int T, const float* __r
     float a[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) a[i] = 0.f;
-    for (int j = 0; j < k; ++j) {
-      if (!srcs[j]) continue;
-      const float g = gws[j];
-      if (Y_F32) {   // fp32 parity path: two 16-byte loads of fp32 Y per 8 outputs
+    if (Y_F32) {     // fp32 parity path: two 16-byte loads of fp32 Y per 8 outputs
+      for (int j = 0; j < k; ++j) {
+        if (!srcs[j]) continue;
+        const float g = gws[j];
         const float4 y0 = reinterpret_cast<const float4*>(srcs[j])[2 * c];
         const float4 y1 = reinterpret_cast<const float4*>(srcs[j])[2 * c + 1];
         const float f[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
 #pragma unroll
         for (int q = 0; q < 8; ++q) a[q] = fmaf(g, f[q], a[q]);
-        continue;
       }
-      const uint4 y = srcs[j][c];
-      const uint32_t yw[4] = {y.x, y.y, y.z, y.w};
+    } else {
+      // issue the token's k loads (≤ KC, peer rows over NVLink) before any use, so a pull keeps
+      // k requests in flight per thread; then accumulate in slot order (R25)
+      uint4 y[KC];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&yw[q]));
-        a[2 * q] = fmaf(g, f.x, a[2 * q]);
-        a[2 * q + 1] = fmaf(g, f.y, a[2 * q + 1]);
+      for (int j = 0; j < KC; ++j)
+        if (j < k && srcs[j]) y[j] = srcs[j][c];
+#pragma unroll
+      for (int j = 0; j < KC; ++j) {
+        if (j >= k || !srcs[j]) continue;
+        const float g = gws[j];
+        const uint32_t yw[4] = {y[j].x, y[j].y, y[j].z, y[j].w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&yw[q]));
+          a[2 * q] = fmaf(g, f.x, a[2 * q]);
+          a[2 * q + 1] = fmaf(g, f.y, a[2 * q + 1]);
+        }
       }
     }
     if (OUT_F32) {

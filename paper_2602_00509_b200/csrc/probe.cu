@@ -778,12 +778,16 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   else if (f32)
     k_combine<false, true><<<d.GL * T, 128, 0, st>>>(d, T, ctx->at<float>(s.gw), ctx->at<int32_t>(s.route),
                                                      sym_of(ctx), PROBE_BUF_Y, out, suspend, layer);
-  else if (out_fp32)
-    k_combine<true><<<d.GL * T, 128, 0, st>>>(d, T, ctx->at<float>(s.gw), ctx->at<int32_t>(s.route), sym_of(ctx),
-                                              PROBE_BUF_Y, out, suspend, layer);
-  else
-    k_combine<false><<<d.GL * T, 128, 0, st>>>(d, T, ctx->at<float>(s.gw), ctx->at<int32_t>(s.route), sym_of(ctx),
-                                               PROBE_BUF_Y, out, suspend, layer);
+  else {
+#define COMBINE(OF, KC)                                                                                   \
+  k_combine<OF, false, KC><<<d.GL * T, 128, 0, st>>>(d, T, ctx->at<float>(s.gw), ctx->at<int32_t>(s.route), \
+                                                     sym_of(ctx), PROBE_BUF_Y, out, suspend, layer)
+    if (out_fp32 && d.k <= 8) COMBINE(true, 8);
+    else if (out_fp32) COMBINE(true, kMaxK);
+    else if (d.k <= 8) COMBINE(false, 8);
+    else COMBINE(false, kMaxK);
+#undef COMBINE
+  }
   CKL();
   MARK(10);
   if (dedup) {
