@@ -159,7 +159,7 @@ def run_probe(args):
     if args.ep:
         shape = shape.with_(G=args.ep)
     result = measure(shape, args, env, light=False)
-    if world == 1 and not args.no_dedup_sub and result is not None and not args.dedup:
+    if world == 1 and not args.no_dedup_sub and result is not None and args.wire != "dedup":
         # the dedup wire format (one row per unique (token, dest), R25 partial combine) on the same
         # inputs: the NVLink-product format, measured here with every "remote" row in local HBM
         result["dedup_wire"] = measure(shape, args, env, light=True, dedup=True)
@@ -178,6 +178,13 @@ def run_probe(args):
     return result
 
 
+def _wire_dedup(args, world):
+    """Wire format of the headline measurement: `--wire auto` uses the dedup format (one row per
+    unique (token, destination), D6) when the ranks span processes — i.e. GPUs joined by NVLink —
+    and the per-slot rows (D1) when one process hosts every rank (all "remote" rows are local HBM)."""
+    return args.wire == "dedup" or (args.wire == "auto" and world > 1)
+
+
 def measure(shape, args, env, light=False, dedup=None, predispatch=False):
     """Bench one configuration: PROBE (timed, profiled), static EP, and unless `light` the
     EP emulation, e2e, roofline and CPU baseline.  Rank 0 returns the JSON dict (else None)."""
@@ -194,7 +201,8 @@ def measure(shape, args, env, light=False, dedup=None, predispatch=False):
     cfg = ProbeConfig(G=G, E=shape.E, k=shape.k, H=shape.H, F=shape.F, T=shape.T, h=shape.h, rank_begin=R0,
                       local_ranks=GL, replica_budget=3, kmax=16, n_sat=n_sat, alpha_ps=alpha_ps, beta_ps=beta_ps,
                       bw_bytes_per_us=bw_Bpus, capacity_factor=args.cap if G > 1 else 1.0,
-                      dedup_wire=(args.dedup if dedup is None else dedup) or predispatch, predispatch=predispatch)
+                      dedup_wire=(_wire_dedup(args, world) if dedup is None else dedup) or predispatch,
+                      predispatch=predispatch)
     if world > 1:
         from paper_2602_00509_b200.dist import make_runtime_distributed
         rt = make_runtime_distributed(cfg, dev, pg)
@@ -561,6 +569,7 @@ def measure(shape, args, env, light=False, dedup=None, predispatch=False):
             "config": {"workload": f"{shape.name}: E={shape.E} top-{shape.k} H={H} F={shape.F} "
                                    f"T={T}/rank EP={G} ({GL} logical ranks per GPU)",
                        "out_dtype": "bf16" if args.out_bf16 else "fp32",
+                       "wire": "dedup (one row per unique (token, dest))" if cfg.dedup_wire else "per-slot rows",
                        "zipf_s": args.zipf, "replica_budget": 3, "kmax": 16, "alpha_ps": alpha_ps,
                        "beta_ps": beta_ps, "n_sat": n_sat, "window_ns": gemm_ns,
                        "l2": "inputs larger than L2 (x 268 MB/layer at C1, weights 1.2 GB/parity); no flush"},
@@ -765,7 +774,8 @@ def parse_args(argv=None):
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-emulation", action="store_true")
     ap.add_argument("--no-decode", action="store_true", help="skip the C2 decode sub-measurement of the C1 line")
-    ap.add_argument("--dedup", action="store_true", help="dedup wire format for the headline measurement")
+    ap.add_argument("--wire", default="auto", choices=["auto", "slot", "dedup"],
+                    help="dispatch/combine wire format (auto: dedup across processes, per-slot in one process)")
     ap.add_argument("--modeled-window", action="store_true",
                     help="plan with the modeled hiding window instead of the measured one (R26)")
     ap.add_argument("--attn-ns", type=int, default=0, help="attention window added to the measured GEMM window")
