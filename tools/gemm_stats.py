@@ -29,14 +29,21 @@ def run(A, B, groups, N, mode, out, v):
     return ms.value
 
 
-A2 = (torch.randn(M, F, device="cuda") * 0.5).to(torch.bfloat16)
-B2 = (torch.randn(E_loc * H, F, device="cuda") / F ** 0.5).to(torch.bfloat16)
 V = int(sys.argv[1]) if len(sys.argv) > 1 else 6     # 6: CTA-pair <256,6,4> (product default)
 Y = torch.empty(M, H, device="cuda")
 g2 = [[e * rows_per, rows_per, e * H, e * rows_per] for e in range(E_loc)]
-for mode in (7, 4):      # fp16 Y (product), no stores
-    ms = run(A2, B2, g2, H, mode, Y, V)
-    print("GEMM2 mode", mode, "ms", ms, "TF/s", round(2.0 * M * H * F / ms / 1e9, 1), flush=True)
+for K in (768, 1536, 2048):   # GEMM2 is K = F = 768; longer K isolates the per-tile cost
+    A2 = (torch.randn(M, K, device="cuda") * 0.5).to(torch.bfloat16)
+    B2 = (torch.randn(E_loc * H, K, device="cuda") / K ** 0.5).to(torch.bfloat16)
+    for mode in (7, 4):      # fp16 Y (product), no stores
+        ms = run(A2, B2, g2, H, mode, Y, V)
+        print("GEMM2-shape K", K, "mode", mode, "ms", ms, "TF/s", round(2.0 * M * H * K / ms / 1e9, 1), flush=True)
+    del A2, B2
+# one group of all rows (no group boundaries / ragged tiles)
+A2 = (torch.randn(M, F, device="cuda") * 0.5).to(torch.bfloat16)
+B2 = (torch.randn(H, F, device="cuda") / F ** 0.5).to(torch.bfloat16)
+ms = run(A2, B2, [[0, M, 0, 0]], H, 7, Y, V)
+print("GEMM2 one group ms", ms, "TF/s", round(2.0 * M * H * F / ms / 1e9, 1), flush=True)
 del A2, B2, Y
 A1 = (torch.randn(M, H, device="cuda") * 0.5).to(torch.bfloat16)
 B1 = (torch.randn(E_loc * 2 * F, H, device="cuda") / H ** 0.5).to(torch.bfloat16)

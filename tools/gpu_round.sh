@@ -1,12 +1,10 @@
-# one gpurun session: all GPU tests, the default bench line, sub-configs, ncu launch list
+# one gpurun session: GEMM study (wait counters), GPU tests, bench, 2-process functional bench
 mkdir -p gpurun_out
-python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 1200 -rf --tb=short -s > gpurun_out/t_all.log 2>&1
-tail -3 gpurun_out/t_all.log
-timeout 900 python bench.py > gpurun_out/bench_r02.json 2> gpurun_out/bench_r02.err
-timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/ref_r02.json 2>&1
-Q="--no-cpu --no-e2e --no-decode --no-dedup-sub"
-timeout 900 python bench.py $Q --config C3 --steps 5 --warmup 3 --cap 3 > gpurun_out/bench_r02_c3.json 2>&1
-timeout 300 python bench.py $Q --config C2 > gpurun_out/bench_r02_c2.json 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"grouped_gemm|k_|sgemm" -c 200 --csv \
-    --log-file gpurun_out/launches_r02.csv python bench.py --steps 2 --warmup 3 $Q --no-emulation > /dev/null 2>&1
-timeout 600 python tools/layer_loop.py --layers 8 --reps 3 > gpurun_out/layer_loop_r02.json 2>&1
+python tools/gemm_stats.py 6 > gpurun_out/gemm_stats.log 2>&1
+python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 1200 -rf --tb=short -k "not fullsize" > gpurun_out/t1.log 2>&1
+tail -3 gpurun_out/t1.log
+timeout 900 python bench.py > gpurun_out/bench_r02b.json 2> gpurun_out/bench_r02b.err
+PROBE_BENCH_SHARED_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+    --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 3 --warmup 3 --no-cpu --no-e2e \
+    > gpurun_out/bench_shared2.json 2> gpurun_out/bench_shared2.err
+tail -c 300 gpurun_out/bench_shared2.err
