@@ -214,6 +214,9 @@ def measure(shape, args, env, light=False, dedup=None, predispatch=False):
     if args.aux_start:
         from paper_2602_00509_b200._lib import OPT_AUX_START
         rt.set_option(OPT_AUX_START, args.aux_start)
+    if args.pred_pair is not None:
+        from paper_2602_00509_b200._lib import OPT_PRED_PAIR
+        rt.set_option(OPT_PRED_PAIR, args.pred_pair)
     if args.l2hint:
         from paper_2602_00509_b200._lib import OPT_L2_HINTS
         rt.set_option(OPT_L2_HINTS, args.l2hint)
@@ -786,6 +789,8 @@ def parse_args(argv=None):
     ap.add_argument("--aux-sms", type=int, default=0, help="grid cap of the aux-stream predictor GEMMs (0: #SMs/2)")
     ap.add_argument("--aux-start", type=int, default=0, help="1: predictor starts after dispatch (not beside it)")
     ap.add_argument("--pred-maxreg", type=int, default=0, help="192: register-capped predictor GEMMs")
+    ap.add_argument("--pred-pair", type=int, default=None, choices=[0, 1],
+                    help="predictor Ŵ1·x GEMM on CTA pairs (library default 1)")
     ap.add_argument("--l2hint", type=lambda v: int(v, 0), default=0, help="expert-GEMM TMA L2 hint mask (probe.h)")
     ap.add_argument("--cpu-tokens", type=int, default=1024, help="oracle expert-FFN sample, tokens per rank")
     args = ap.parse_args(argv)

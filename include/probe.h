@@ -343,6 +343,8 @@ enum { PROBE_OPT_EP_EMULATION = 1, PROBE_OPT_UNFUSED_TOPK = 2, PROBE_OPT_FUSED_E
                                   dispatch(L); 1: after dispatch(L) (beside the expert GEMMs) */,
        PROBE_OPT_PRED_MAXREG = 9 /* 0 (default) or 192: register-capped predictor GEMMs so a dispatch CTA
                                     co-resides on the SMs the aux track holds */,
+       PROBE_OPT_PRED_PAIR = 11 /* 1 (default): the predictor's Ŵ1·x GEMM (h ≥ 256 columns) runs on CTA
+                                   pairs (256×256 tiles); 0: the 1-CTA 128×128 kernel */,
        PROBE_OPT_L2_HINTS = 10 /* TMA L2 eviction hints of the CTA-pair expert GEMMs: bits 0-2 GEMM1,
                                   bits 4-6 GEMM2; per GEMM bit 0 output stores evict_first, bit 1 weight
                                   (B) loads evict_last, bit 2 activation (A) loads evict_first */ };

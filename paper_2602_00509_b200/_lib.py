@@ -25,7 +25,7 @@ EXPORTS = ["probe_workspace", "probe_init", "probe_moe_forward", "probe_predict"
            "probe_ipc_export", "probe_ipc_import", "probe_ipc_close", "probe_set_option",
            "probe_history_update", "probe_distill_grad", "probe_distill_apply"]
 OPT_EP_EMULATION, OPT_UNFUSED_TOPK, OPT_FUSED_EPILOGUE_TOPK, OPT_AUX_SMS, OPT_PAIR_GEMM = 1, 2, 3, 4, 5
-OPT_AUX_START, OPT_PRED_MAXREG, OPT_L2_HINTS = 8, 9, 10
+OPT_AUX_START, OPT_PRED_MAXREG, OPT_L2_HINTS, OPT_PRED_PAIR = 8, 9, 10, 11
 DTYPES = {"bf16": 0, "fp32": 1}      # probe_config.dtype (PROBE_BF16, PROBE_FP32)
 PROBE_NPHASE = 13
 PHASES = ["gate", "select", "counts", "layout", "dispatch", "expand", "wait", "gemm1", "gemm2", "combine", "reduce",

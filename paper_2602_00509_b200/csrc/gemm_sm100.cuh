@@ -114,15 +114,15 @@ __host__ __device__ inline int gemm_ntiles(const GemmGroup& G, int BN, int TM = 
 }
 
 // Serial prefix over the group table (called by one thread).
-__device__ inline void gemm_finalize_sched(GemmSched* s, int BN) {
+__device__ inline void gemm_finalize_sched(GemmSched* s, int BN, int TM = 128) {
   s->nparts = 0;
-  s->tile_m = 128;
+  s->tile_m = TM;
   s->stats = nullptr;
   sched_reset_counters(s);
   int acc = 0;
   for (int i = 0; i < s->num_groups; ++i) {
     s->g[i].tile_start = acc;
-    acc += gemm_ntiles(s->g[i], BN);
+    acc += gemm_ntiles(s->g[i], BN, TM);
   }
   s->total_tiles = acc;
 }

@@ -362,17 +362,26 @@ __device__ __forceinline__ int64_t rank_gemm_cost(const Dims& d, const int32_t* 
 }
 __global__ void k_window_stamp(Dims d, int64_t* t0, int phase, Sym sym, int buf_board,
                                const int32_t* __restrict__ group_rows, int n_sat) {
-  const uint64_t now = ptx::globaltimer_ns();
+  // phase 0: one thread stamps; phase 1: thread gl (< GL ≤ 64) handles local rank gl
+  __shared__ int64_t cost[kMaxG];
+  __shared__ int64_t s_w, s_tot;
+  const int gl = threadIdx.x;
   if (phase == 0) {
-    *t0 = static_cast<int64_t>(now);
+    if (gl == 0) *t0 = static_cast<int64_t>(ptx::globaltimer_ns());
     return;
   }
-  const int64_t w = static_cast<int64_t>(now) - *t0;
-  int64_t tot = 0;
-  for (int gl = 0; gl < d.GL; ++gl) tot += rank_gemm_cost(d, group_rows, d.R0 + gl, n_sat);
-  for (int gl = 0; gl < d.GL; ++gl) {
-    const int64_t c = rank_gemm_cost(d, group_rows, d.R0 + gl, n_sat);
-    const int64_t wr = (d.GL == 1 || tot == 0) ? w : w * c / tot;
+  if (gl == 0) s_w = static_cast<int64_t>(ptx::globaltimer_ns()) - *t0;
+  if (gl < d.GL) cost[gl] = rank_gemm_cost(d, group_rows, d.R0 + gl, n_sat);
+  __syncthreads();
+  if (gl == 0) {
+    int64_t tot = 0;
+    for (int i = 0; i < d.GL; ++i) tot += cost[i];
+    s_tot = tot;
+  }
+  __syncthreads();
+  if (gl < d.GL) {
+    const int64_t w = s_w, tot = s_tot;
+    const int64_t wr = (d.GL == 1 || tot == 0) ? w : w * cost[gl] / tot;
     for (int r = 0; r < d.G; ++r) window_board(d, sym.at(buf_board, d.G, r))[d.R0 + gl] = wr > 0 ? wr : 1;
   }
 }
@@ -1479,12 +1488,13 @@ struct SmallGroups {
   int n;
   int BN;
   GemmGroup g[2];
+  int TM;   // rows per tile: 128 (1-CTA kernel, the default when 0) or 256 (CTA pair)
 };
 __global__ void k_write_sched(GemmSched* s, SmallGroups sg) {
   if (threadIdx.x == 0) {
     s->num_groups = sg.n;
     for (int i = 0; i < sg.n; ++i) s->g[i] = sg.g[i];
-    gemm_finalize_sched(s, sg.BN);
+    gemm_finalize_sched(s, sg.BN, sg.TM ? sg.TM : 128);
   }
 }
 

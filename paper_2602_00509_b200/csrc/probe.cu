@@ -191,6 +191,7 @@ struct probe_ctx_s {
   cudaEvent_t ev_gate[2], ev_gemm[2], ev_comb[2], ev_pred[2], ev_plan[2], ev_slots[2], ev_disp[2];
   int aux_start = 0;     // PROBE_OPT_AUX_START: predictor(L+1) starts after gate(L) (0) or dispatch(L) (1)
   int l2hint = 0;        // PROBE_OPT_L2_HINTS: TMA L2 eviction hints of the expert GEMMs (LayoutIn::l2hint)
+  bool pred_pair = true;  // PROBE_OPT_PRED_PAIR: the predictor's Ŵ1·x GEMM on CTA pairs
   int pred_maxreg = 0;   // PROBE_OPT_PRED_MAXREG: 192 ⇒ register-capped predictor GEMMs (a dispatch CTA fits beside)
   // CUDA-graph awareness: id of the stream capture each event was last recorded in (0 = eager)
   std::vector<std::pair<cudaEvent_t, unsigned long long>> ev_cap;
@@ -754,7 +755,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
     CK(launch_gemm_v(vexp, ctx->map_act, *m2, ctx->map_rw2, ctx->map_y, lo.s2, d.F, ctx->num_sms, st));
   }
   ++ctx->launches;
-  k_window_stamp<<<1, 1, 0, st>>>(d, ctx->at<int64_t>(s.win_t0), 1, sym_of(ctx), PROBE_BUF_BOARD, lo.group_rows,
+  k_window_stamp<<<1, 64, 0, st>>>(d, ctx->at<int64_t>(s.win_t0), 1, sym_of(ctx), PROBE_BUF_BOARD, lo.group_rows,
                                   ctx->cfg.n_sat);
   CKL();
   if (!dedup) CK(xbarrier(ctx, BAR_Y, st));     // every expert rank's Y rows are complete (the combine pulls)
@@ -874,18 +875,23 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
     const CUtensorMap* ma = nullptr;
     const CUtensorMap* m2 = nullptr;
     if (w_res1) {
-      const CUtensorMap* m1 = ctx->maps.get(w_res1, h, H, 64);
+      // z = x Ŵ1ᵀ (N = h): on CTA pairs (256×256 tiles, tcgen05 cta_group::2) when h fills a
+      // 256-column tile — it is 75% of the predictor's FLOPs (C1: 137 of 180 GFLOP), and the
+      // 1-CTA <128,6,4> kernel ran it at 56% of its SMs' peak beside the dispatch
+      const bool pair1 = ctx->pred_pair && d.h >= 256 && static_cast<int64_t>(GL) * T >= 256;
+      const CUtensorMap* m1 = ctx->maps.get(w_res1, h, H, pair1 ? 128 : 64);
       ma = ctx->maps.get(ctx->scratch + s.pact, GL * T, h, 128);
       m2 = ctx->maps.get(w_res2, E, h, BN / 2);
       if (!m1 || !ma || !m2) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
       SmallGroups s1{};
-      s1.BN = 128;
+      s1.BN = pair1 ? 256 : 128;
+      s1.TM = pair1 ? 256 : 128;
       s1.n = 1;
       s1.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_SILU_BF16, d.h, d.h, ctx->scratch + s.pact);
       k_write_sched<<<1, 32, 0, st>>>(ctx->at<GemmSched>(s.s_p1), s1);
       CKL();
-      CK(launch_gemm_v(ctx->pred_maxreg ? V_128_6_4_R192 : V_128_6_4, *mx, *m1, *m1, *mx, ctx->at<GemmSched>(s.s_p1),
-                       d.H, ctx->aux_sms, st));
+      const int v1 = pair1 ? V_2CTA_256_6_4 : (ctx->pred_maxreg ? V_128_6_4_R192 : V_128_6_4);
+      CK(launch_gemm_v(v1, *mx, *m1, *m1, *mx, ctx->at<GemmSched>(s.s_p1), d.H, ctx->aux_sms, st));
       ++ctx->launches;
     }
     if (!mw) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
@@ -1426,6 +1432,7 @@ probe_status probe_set_option(probe_ctx ctx, int32_t option, int64_t value) {
       if (value < 0 || value > 1) return fail(ctx, PROBE_EINVAL, "aux start %lld not in {0, 1}", (long long)value);
       ctx->aux_start = static_cast<int>(value);
       return PROBE_OK;
+    case PROBE_OPT_PRED_PAIR: ctx->pred_pair = value != 0; return PROBE_OK;
     case PROBE_OPT_L2_HINTS:
       if (value < 0 || value > 0x77) return fail(ctx, PROBE_EINVAL, "L2 hint mask 0x%llx", (long long)value);
       ctx->l2hint = static_cast<int>(value);

@@ -89,6 +89,11 @@ CASES = {
                                           residual_kind="relabel", bias=True, predispatch=True),
     "predispatch-T-below-capacity": CaseCfg(pi.C0.with_(name="pdt", E=16, k=4, H=256, F=256, T=77, G=4),
                                             zipf_s=1.3, max_tokens=300, predispatch=True),
+    # predictor residual width h = H/4 >= 256: Ŵ1·x on CTA pairs (PROBE_OPT_PRED_PAIR), ragged T
+    "predictor-pair-gemm": CaseCfg(pi.C0.with_(name="ppg", E=32, k=4, H=1024, F=256, T=301, G=4), zipf_s=1.2,
+                                   bias=True),
+    "predictor-pair-gemm-relabel": CaseCfg(pi.C0.with_(name="ppr", E=64, k=8, H=1536, F=256, T=200, G=4),
+                                           zipf_s=1.2, residual_kind="relabel"),
     # the layer call runs with T below the context's max_tokens (workspaces sized for 4x more)
     "T-below-capacity": CaseCfg(pi.C0.with_(name="tbc", E=16, k=4, H=256, F=256, T=77, G=4), zipf_s=1.3,
                                 max_tokens=300),

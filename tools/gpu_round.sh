@@ -1,10 +1,11 @@
-# one gpurun session: GEMM study (wait counters), GPU tests, bench, 2-process functional bench
+# one gpurun session: GPU tests (layer + predictor + full-size C1), A/B of the predictor on CTA pairs
 mkdir -p gpurun_out
-python tools/gemm_stats.py 6 > gpurun_out/gemm_stats.log 2>&1
-python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 1200 -rf --tb=short -k "not fullsize" > gpurun_out/t1.log 2>&1
+python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 1200 -rf --tb=short -s -k "layer_parity or planner or fullsize_parity[C1-bench] or fullsize_parity[C1-relabel" > gpurun_out/t1.log 2>&1
 tail -3 gpurun_out/t1.log
-timeout 900 python bench.py > gpurun_out/bench_r02b.json 2> gpurun_out/bench_r02b.err
-PROBE_BENCH_SHARED_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
-    --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 3 --warmup 3 --no-cpu --no-e2e \
-    > gpurun_out/bench_shared2.json 2> gpurun_out/bench_shared2.err
-tail -c 300 gpurun_out/bench_shared2.err
+Q="--no-cpu --no-e2e --no-emulation --no-decode --no-dedup-sub"
+for i in 1 2; do
+  timeout 300 python bench.py $Q > gpurun_out/ab_pair1_$i.json 2>&1
+  timeout 300 python bench.py $Q --pred-pair 0 > gpurun_out/ab_pair0_$i.json 2>&1
+done
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"grouped_gemm|k_|sgemm" -c 60 --csv \
+    --log-file gpurun_out/launches_pair.csv python bench.py --steps 2 --warmup 3 $Q > /dev/null 2>&1
