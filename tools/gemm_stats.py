@@ -51,3 +51,15 @@ act = torch.empty(M, F, dtype=torch.bfloat16, device="cuda")
 g1 = [[e * rows_per, rows_per, e * 2 * F, e * rows_per] for e in range(E_loc)]
 ms = run(A1, B1, g1, 2 * F, 1, act, V)
 print("GEMM1 ms", ms, "TF/s", round(4.0 * M * H * F / ms / 1e9, 1), flush=True)
+del A1, B1, act
+# predictor Ŵ1·x shape (C1: M = 65536 tokens, N = h = 512, K = H = 2048): SiLU→bf16 (mode 3,
+# manual stores), no store (4), fp32 TMA stores (0); 1-CTA <128,6,4> (0) and CTA pairs (6)
+Mp, Np, Kp = 65536, 512, 2048
+Ap = (torch.randn(Mp, Kp, device="cuda") * 0.5).to(torch.bfloat16)
+Bp = (torch.randn(Np, Kp, device="cuda") / Kp ** 0.5).to(torch.bfloat16)
+Cp = torch.empty(Mp, Np, device="cuda")
+for v in (0, 6):
+    for mode in (3, 4, 0):
+        ms = run(Ap, Bp, [[0, Mp, 0, 0]], Np, mode, Cp, v)
+        print("predictor W1x variant", v, "mode", mode, "ms", ms, "TF/s", round(2.0 * Mp * Np * Kp / ms / 1e9, 1),
+              flush=True)
