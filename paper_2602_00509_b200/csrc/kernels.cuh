@@ -781,7 +781,7 @@ __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o
     const int arow = gl * d.cap + (off < d.cap ? off : d.cap);
     GemmGroup g1;
     g1.a_row = arow; g1.m = m; g1.b_row = wslot * 2 * d.F; g1.b_sel = is_rep; g1.mode = EPI_SWIGLU;
-    g1.n = d.F; g1.ldc = d.F; g1.tile_start = 0; g1.out_row = arow; g1.tma_out = 0;
+    g1.n = d.F; g1.ldc = d.F; g1.tile_start = 0; g1.out_row = arow; g1.tma_out = !in.f32;   // bf16 act by TMA
     g1.topk = 0; g1.rows_per_rank = 1; g1.k_off = 0; g1.aux = nullptr; g1.bias = nullptr;
     g1.out = static_cast<uint8_t*>(in.act) + static_cast<size_t>(arow) * d.F * (in.f32 ? 4 : 2);
     GemmGroup g2;

@@ -82,6 +82,19 @@ bool make_map_f16_out(CUtensorMap* m, const void* base, uint64_t rows, uint64_t 
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// bf16 output map for TMA tensor stores (the SwiGLU / SiLU activations): box {32 cols (64 B),
+// 32 rows}, SWIZZLE_64B — the same staging layout as the fp16 Y map.
+bool make_map_bf16_out(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols) {
+  if (!load_encode()) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t es[2] = {1, 1};
+  return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 struct MapCache {
   struct Ent {
     const void* p = nullptr;
@@ -202,7 +215,7 @@ struct probe_ctx_s {
   int num_sms = 148;
   int aux_sms = 74;   // grid cap for aux-stream (predictor) GEMMs: the main track keeps free SMs
   MapCache maps;
-  CUtensorMap map_recv, map_act, map_rw13, map_rw2, map_y;
+  CUtensorMap map_recv, map_act, map_rw13, map_rw2, map_y, map_act_out;
   std::string err;
   int64_t launches = 0;
   bool multi_process() const { return cfg.local_ranks != cfg.ep_size; }
@@ -561,7 +574,8 @@ probe_status probe_init(const probe_config* cfg, const uint64_t* peer_ptrs, void
             make_map(&ctx->map_act, ctx->scratch + ctx->sl.act, GL * cap, F, 128) &&
             make_map(&ctx->map_rw13, ctx->local_base[PROBE_BUF_REP_W13], GL * 2 * kMaxRb * 2 * F, H, 128) &&
             make_map(&ctx->map_rw2, ctx->local_base[PROBE_BUF_REP_W2], GL * 2 * kMaxRb * H, F, 128) &&
-            make_map_f16_out(&ctx->map_y, ctx->local_base[PROBE_BUF_Y], GL * cap, H);
+            make_map_f16_out(&ctx->map_y, ctx->local_base[PROBE_BUF_Y], GL * cap, H) &&
+            (c.dtype == PROBE_FP32 || make_map_bf16_out(&ctx->map_act_out, ctx->scratch + ctx->sl.act, GL * cap, F));
   if (!ok) {
     delete ctx;
     return fail(nullptr, PROBE_ECUDA, "probe_init: cuTensorMapEncodeTiled failed");
@@ -745,7 +759,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   if (f32) {
     CK(launch_sgemm(ctx, lo.s1, ctx->local_base[PROBE_BUF_RECV], w13, ctx->local_base[PROBE_BUF_REP_W13], d.H, st));
   } else {
-    CK(launch_gemm_v(vexp, ctx->map_recv, *m13, ctx->map_rw13, ctx->map_recv, lo.s1, d.H, ctx->num_sms, st));
+    CK(launch_gemm_v(vexp, ctx->map_recv, *m13, ctx->map_rw13, ctx->map_act_out, lo.s1, d.H, ctx->num_sms, st));
   }
   ++ctx->launches;
   MARK(8);
@@ -888,10 +902,14 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
       s1.TM = pair1 ? 256 : 128;
       s1.n = 1;
       s1.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_SILU_BF16, d.h, d.h, ctx->scratch + s.pact);
+      // a = bf16(SiLU(z)) written by TMA tensor stores (per-lane stores halved this GEMM's rate)
+      CUtensorMap mact;
+      const bool tma_act = d.h % 32 == 0 && make_map_bf16_out(&mact, ctx->scratch + s.pact, GL * T, h);
+      s1.g[0].tma_out = tma_act ? 1 : 0;
       k_write_sched<<<1, 32, 0, st>>>(ctx->at<GemmSched>(s.s_p1), s1);
       CKL();
       const int v1 = pair1 ? V_2CTA_256_6_4 : (ctx->pred_maxreg ? V_128_6_4_R192 : V_128_6_4);
-      CK(launch_gemm_v(v1, *mx, *m1, *m1, *mx, ctx->at<GemmSched>(s.s_p1), d.H, ctx->aux_sms, st));
+      CK(launch_gemm_v(v1, *mx, *m1, *m1, tma_act ? mact : *mx, ctx->at<GemmSched>(s.s_p1), d.H, ctx->aux_sms, st));
       ++ctx->launches;
     }
     if (!mw) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
@@ -1134,7 +1152,8 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
     const int* g = groups + 4 * i;
     hs->g[i] = mk_group(g[0], g[1], g[2], 0, emode, n_out, n_out, static_cast<uint8_t*>(C) + static_cast<size_t>(g[3]) * n_out * esz);
     hs->g[i].out_row = g[3];
-    hs->g[i].tma_out = (emode == EPI_F32 || emode == EPI_F16) && n_out % 32 == 0 ? 1 : 0;
+    hs->g[i].tma_out =
+        (emode == EPI_F32 || emode == EPI_F16 || emode == EPI_SWIGLU || emode == EPI_SILU_BF16) && n_out % 32 == 0 ? 1 : 0;
     if (topk_aux) {   // test hook: k = 8; TOPK writes ids to C, weights to aux; COUNT: counts [64][N]
       hs->g[i].topk = 8;
       hs->g[i].rows_per_rank = static_cast<int>((a_rows + 63) / 64);
@@ -1154,6 +1173,8 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
     if (!make_map_f32_out(&mc, C, c_rows, n_out)) return fail(nullptr, PROBE_ECUDA, "tensor map encode failed");
   } else if (emode == EPI_F16 && n_out % 32 == 0) {
     if (!make_map_f16_out(&mc, C, c_rows, n_out)) return fail(nullptr, PROBE_ECUDA, "tensor map encode failed");
+  } else if ((emode == EPI_SWIGLU || emode == EPI_SILU_BF16) && n_out % 32 == 0) {
+    if (!make_map_bf16_out(&mc, C, c_rows, n_out)) return fail(nullptr, PROBE_ECUDA, "tensor map encode failed");
   } else {
     mc = ma;
   }
