@@ -150,7 +150,11 @@ __device__ __forceinline__ int gemm_find_group(const int* ts, int ng, int tile) 
   return lo;
 }
 
-__device__ __forceinline__ float silu_f(float v) { return v / (1.0f + __expf(-v)); }
+// SiLU in the tensor-core epilogues: MUFU exp + MUFU reciprocal (__fdividef, 2 ulp; → 0 for
+// v < -88 where the denominator overflows).  An IEEE division here made the SiLU epilogues
+// 3.5× costlier than a plain store (per-role counters: the predictor's Ŵ1·x GEMM was
+// epilogue-bound, 685 vs 1107 TF/s), far above the bf16 rounding that follows (2^-9).
+__device__ __forceinline__ float silu_f(float v) { return __fdividef(v, 1.0f + __expf(-v)); }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
