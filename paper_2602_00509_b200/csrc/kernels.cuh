@@ -156,6 +156,48 @@ __global__ void __launch_bounds__(128) k_topk(Dims d, int T, const float* __rest
 // n̂[rank][e] (R9).  grid (ceil(T/128), GL), block 128 (thread = token).  E % 32 == 0
 // or E < 32 handled by masking.
 // =============================================================================
+// Top-k by sorting networks (R3, R4): keys ordered by (value ↓, id ↑), a total order, so any
+// correct network gives the lowest-id tie rule.  Each group of 8 logits is sorted with the
+// 19-comparator odd-even merge network, merged into the running top 8 (the element-wise
+// better of top[i] and group[7-i] is bitonic and holds the top 8 of both), and re-sorted
+// with a 12-comparator bitonic cleaner.  Branch-free with independent comparators per
+// stage: the former insertion chain was predicated over every logit (11 K instructions per
+// warp at C1) and latency-bound at 13 warps per SM.
+__device__ __forceinline__ void topk_ce(float& av, int& ae, float& bv, int& be) {
+  const bool s = (bv > av) || (bv == av && be < ae);
+  const float tv = s ? bv : av;
+  const int te = s ? be : ae;
+  bv = s ? av : bv;
+  be = s ? ae : be;
+  av = tv;
+  ae = te;
+}
+__device__ __forceinline__ void topk_sort8(float (&v)[8], int (&e)[8]) {
+#define CE(i, j) topk_ce(v[i], e[i], v[j], e[j])
+  CE(0, 1); CE(2, 3); CE(4, 5); CE(6, 7);
+  CE(0, 2); CE(1, 3); CE(4, 6); CE(5, 7);
+  CE(1, 2); CE(5, 6);
+  CE(0, 4); CE(1, 5); CE(2, 6); CE(3, 7);
+  CE(2, 4); CE(3, 5);
+  CE(1, 2); CE(3, 4); CE(5, 6);
+#undef CE
+}
+__device__ __forceinline__ void topk_merge8(float (&tv)[8], int (&te)[8], const float (&gv)[8], const int (&ge)[8]) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float bv = gv[7 - i];
+    const int be = ge[7 - i];
+    const bool s = (bv > tv[i]) || (bv == tv[i] && be < te[i]);
+    tv[i] = s ? bv : tv[i];
+    te[i] = s ? be : te[i];
+  }
+#define CE(i, j) topk_ce(tv[i], te[i], tv[j], te[j])
+  CE(0, 4); CE(1, 5); CE(2, 6); CE(3, 7);
+  CE(0, 2); CE(1, 3); CE(4, 6); CE(5, 7);
+  CE(0, 1); CE(2, 3); CE(4, 5); CE(6, 7);
+#undef CE
+}
+
 // The predictor instance (PRED) is capped at 64 registers (8 CTAs of 128 threads per SM) and
 // streams 16 logits per step: it must fit beside a persistent expert-GEMM CTA (224 × 256
 // registers) when the aux track still runs after the expert GEMMs started (C3 on one GPU:
@@ -176,13 +218,13 @@ __global__ void __launch_bounds__(128, PRED ? 8 : 1) k_select(Dims d, int T, con
   for (int i = tl; i < E * 4; i += blockDim.x) mask[i] = 0u;
   for (int i = tl; i < E; i += blockDim.x) scount[i] = 0;
   __syncthreads();
-  int te[KK];
+  int te[8];
   if (t < T) {
-    float tv[KK];
+    float tv[8];   // running top 8, sorted by (value ↓, id ↑); the first KK are the selection
 #pragma unroll
-    for (int j = 0; j < KK; ++j) { tv[j] = -INFINITY; te[j] = 0x7fffffff; }
+    for (int j = 0; j < 8; ++j) { tv[j] = -INFINITY; te[j] = 0x7fffffff; }
     const float* row = logits + (static_cast<size_t>(gl) * T + t) * E;
-    constexpr int CW = PRED ? 16 : 32;     // logits per step
+    constexpr int CW = PRED ? 8 : 32;      // logits per step (8-wide groups)
 #pragma unroll 1
     for (int c = 0; c < E; c += CW) {
       float v[CW];
@@ -208,20 +250,13 @@ __global__ void __launch_bounds__(128, PRED ? 8 : 1) k_select(Dims d, int T, con
           if (c + i < E) lo[i] = v[i];
       }
 #pragma unroll
-      for (int i = 0; i < CW; ++i) {
-        float x = v[i];
-        int e = c + i;
-        if (x > tv[KK - 1]) {
+      for (int g = 0; g < CW / 8; ++g) {
+        float gv[8];
+        int ge[8];
 #pragma unroll
-          for (int j = 0; j < KK; ++j) {
-            if (x > tv[j] || (x == tv[j] && e < te[j])) {
-              const float ov = tv[j];
-              const int oe = te[j];
-              tv[j] = x; te[j] = e;
-              x = ov; e = oe;
-            }
-          }
-        }
+        for (int i = 0; i < 8; ++i) { gv[i] = v[8 * g + i]; ge[i] = c + 8 * g + i; }
+        topk_sort8(gv, ge);
+        topk_merge8(tv, te, gv, ge);
       }
     }
     const size_t o = (static_cast<size_t>(gl) * T + t) * KK;
