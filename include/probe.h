@@ -236,7 +236,8 @@ probe_status probe_test_gemm(const void* A, int64_t a_rows, const void* B, int64
 /* Timing hook: as probe_test_gemm with an explicit kernel variant (-1 = default for
  * `mode`; 0: BN=128/6 stages/4 epilogue warps, 1: 256/4/4,
  * 6: CTA pair (cta_group::2), 256-row tiles, 6 stages, 10: 1-CTA <256,4,4> capped at 216 registers,
- * 11: <128,6,4> capped at 192 registers; other numbers are not available),
+ * 11: <128,6,4> capped at 192 registers, 12: CTA pair with 256×128 tiles and 8 stages; other numbers
+ * are not available),
  * run once, then `reps` times between CUDA events on `stream`; *ms_out = mean ms. */
 probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int64_t b_rows,
                               int32_t K, int32_t N, const int32_t* groups, int32_t num_groups,
@@ -343,8 +344,8 @@ enum { PROBE_OPT_EP_EMULATION = 1, PROBE_OPT_UNFUSED_TOPK = 2, PROBE_OPT_FUSED_E
                                   dispatch(L); 1: after dispatch(L) (beside the expert GEMMs) */,
        PROBE_OPT_PRED_MAXREG = 9 /* 0 (default) or 192: register-capped predictor GEMMs so a dispatch CTA
                                     co-resides on the SMs the aux track holds */,
-       PROBE_OPT_PRED_PAIR = 11 /* 1 (default): the predictor's Ŵ1·x GEMM (h ≥ 256 columns) runs on CTA
-                                   pairs (256×256 tiles); 0: the 1-CTA 128×128 kernel */,
+       PROBE_OPT_PRED_PAIR = 11 /* 1 (default): the predictor's GEMMs run on CTA pairs (Ŵ1·x: 256×256 tiles
+                                   when h ≥ 256; [x | a]·[W | Ŵ2]ᵀ: 256×E tiles); 0: the 1-CTA 128-row kernel */,
        PROBE_OPT_L2_HINTS = 10 /* TMA L2 eviction hints of the CTA-pair expert GEMMs: bits 0-2 GEMM1,
                                   bits 4-6 GEMM2; per GEMM bit 0 output stores evict_first, bit 1 weight
                                   (B) loads evict_last, bit 2 activation (A) loads evict_first */ };

@@ -272,7 +272,8 @@ probe_status fail(probe_ctx ctx, probe_status st, const char* fmt, ...) {
 // V_256_4_4_EXP: the 1-CTA expert GEMMs for decode-sized groups, V_128_6_4_R192: register-capped
 // predictor GEMMs (PROBE_OPT_PRED_MAXREG).  The numbering is the probe_bench_gemm `variant`
 // argument; the other numbers were configurations measured slower in round 1 and removed.
-enum GemmVariant { V_128_6_4 = 0, V_256_4_4 = 1, V_2CTA_256_6_4 = 6, V_256_4_4_EXP = 10, V_128_6_4_R192 = 11 };
+enum GemmVariant { V_128_6_4 = 0, V_256_4_4 = 1, V_2CTA_256_6_4 = 6, V_256_4_4_EXP = 10, V_128_6_4_R192 = 11,
+                   V_2CTA_128_8_4 = 12 /* CTA pair, 256×128 tiles, 8 stages: the predictor's N = E = 128 GEMM */ };
 
 // Expert GEMMs leave registers for one 128-thread prefetch CTA per SM (a9 part 1 runs beside them):
 // 256 × 224 + 128 × 48 = 62 K.  Splits that fill exactly 64 K (240 + 32, 232 + 48) did not
@@ -337,13 +338,15 @@ cudaError_t launch_gemm_v(int v, const CUtensorMap& a, const CUtensorMap& b0, co
     case V_2CTA_256_6_4: return launch_gemm_2cta<256, 6, 4, 1, kExpertMaxReg>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_256_4_4_EXP: return launch_gemm_t<256, 4, 4, 1, PROBE_EXP1_MAXREG>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_128_6_4_R192: return launch_gemm_t<128, 6, 4, 1, 192>(a, b0, b1, c, A2, s, K, K2, grid, st);
+    case V_2CTA_128_8_4: return launch_gemm_2cta<128, 8, 4, 1, kExpertMaxReg>(a, b0, b1, c, A2, s, K, K2, grid, st);
   }
   return cudaErrorInvalidValue;
 }
-int variant_bn(int v) { return (v == V_128_6_4 || v == V_128_6_4_R192) ? 128 : 256; }
-int variant_tm(int v) { return v == V_2CTA_256_6_4 ? 256 : 128; }
+int variant_bn(int v) { return (v == V_128_6_4 || v == V_128_6_4_R192 || v == V_2CTA_128_8_4) ? 128 : 256; }
+int variant_tm(int v) { return (v == V_2CTA_256_6_4 || v == V_2CTA_128_8_4) ? 256 : 128; }
 bool variant_ok(int v) {
-  return v == V_128_6_4 || v == V_256_4_4 || v == V_2CTA_256_6_4 || v == V_256_4_4_EXP || v == V_128_6_4_R192;
+  return v == V_128_6_4 || v == V_256_4_4 || v == V_2CTA_256_6_4 || v == V_256_4_4_EXP || v == V_128_6_4_R192 ||
+         v == V_2CTA_128_8_4;
 }
 
 template <int BN>
@@ -913,8 +916,11 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
       ++ctx->launches;
     }
     if (!mw) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
+    // the K-concatenated prior + residual GEMM on CTA pairs as well (not with the epilogue top-k)
+    const bool pair2 = ctx->pred_pair && !epi_topk && static_cast<int64_t>(GL) * T >= 256;
     SmallGroups s2{};
     s2.BN = BN;
+    s2.TM = pair2 ? 256 : 128;
     s2.n = 1;
     if (epi_topk) {
       s2.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_TOPK_COUNT, d.E, d.E, nullptr);
@@ -927,9 +933,10 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
     }
     k_write_sched<<<1, 32, 0, st>>>(ctx->at<GemmSched>(s.s_p2), s2);
     CKL();
-    CK(launch_gemm_v(BN == 128 ? (ctx->pred_maxreg ? V_128_6_4_R192 : V_128_6_4) : V_256_4_4, *mx, *mw,
-                     w_res1 ? *m2 : *mw, *mx, ctx->at<GemmSched>(s.s_p2), d.H, ctx->aux_sms, st, w_res1 ? ma : nullptr,
-                     w_res1 ? d.h : 0));
+    const int v2 = pair2 ? (BN == 128 ? V_2CTA_128_8_4 : V_2CTA_256_6_4)
+                         : (BN == 128 ? (ctx->pred_maxreg ? V_128_6_4_R192 : V_128_6_4) : V_256_4_4);
+    CK(launch_gemm_v(v2, *mx, *mw, w_res1 ? *m2 : *mw, *mx, ctx->at<GemmSched>(s.s_p2), d.H, ctx->aux_sms, st,
+                     w_res1 ? ma : nullptr, w_res1 ? d.h : 0));
     ++ctx->launches;
     if (!epi_topk) {
       CK(launch_select<true>(d, T, nchunks, st, ctx->at<float>(s.pprior), b_router_next, nullptr, nullptr, nullptr,

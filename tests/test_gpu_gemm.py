@@ -69,7 +69,8 @@ def test_gemm_swiglu_and_silu():
                                                    (2, 512, 768, 30000, 10), (0, 128, 2048, 65536, 0),
                                                    (0, 384, 512, 20000, 11), (2, 2048, 768, 9000, 10),
                                                    (2, 512, 768, 30000, 6), (2, 2048, 768, 9000, 6),
-                                                   (2, 256, 2048, 700, 6), (0, 128, 2560, 30000, 11)])
+                                                   (2, 256, 2048, 700, 6), (0, 128, 2560, 30000, 11),
+                                                   (0, 128, 2560, 30000, 12), (2, 136, 640, 9001, 12)])
 def test_gemm_multi_tile_per_cta_exact(mode, N, K, rows, variant):
     """Several tiles per persistent CTA (TMEM accumulator double buffer, phase wrap-around),
     every kernel variant (BN, stages, epilogue warps)."""
