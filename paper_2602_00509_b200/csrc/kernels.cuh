@@ -1518,6 +1518,13 @@ __global__ void k_xbarrier(Dims d, Sym sym, int buf_sig, int kind, uint32_t* epo
   if (i == 0) epoch_ctr[kind] = epoch;
 }
 
+// analysis helper: one thread spins for ns nanoseconds (%globaltimer)
+__global__ void k_spin(long long ns) {
+  const uint64_t t0 = ptx::globaltimer_ns();
+  while (static_cast<long long>(ptx::globaltimer_ns() - t0) < ns) {
+  }
+}
+
 // small helper: write a host-described group list into a device schedule
 struct SmallGroups {
   int n;

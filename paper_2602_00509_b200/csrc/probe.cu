@@ -220,6 +220,8 @@ struct probe_ctx_s {
   int64_t launches = 0;
   bool multi_process() const { return cfg.local_ranks != cfg.ep_size; }
   bool f32() const { return cfg.dtype == PROBE_FP32; }   // fp32 parity path (SIMT GEMMs)
+  bool dbg_gemm2_repeat = false;   // PROBE_DEBUG_GEMM2_REPEAT=1 (analysis)
+  int dbg_gap_us = 0;              // PROBE_DEBUG_GAP_US (analysis)
   bool unfused = false;   // PROBE_UNFUSED=1: logits written + separate top-k kernels (debug)
   bool ep_emulation = false;  // partition expert GEMMs by local rank (probe_set_option)
   bool fused_epi_topk = false;  // top-k in the GEMM epilogue instead of k_select (probe_set_option)
@@ -512,6 +514,11 @@ probe_status probe_init(const probe_config* cfg, const uint64_t* peer_ptrs, void
   {
     const char* u = getenv("PROBE_UNFUSED");
     ctx->unfused = u && u[0] == '1';
+    // analysis only (GEMM2's in-layer rate): repeat GEMM2 inside its phase / idle gap before it
+    const char* r2 = getenv("PROBE_DEBUG_GEMM2_REPEAT");
+    ctx->dbg_gemm2_repeat = r2 && r2[0] == '1';
+    const char* gap = getenv("PROBE_DEBUG_GAP_US");
+    ctx->dbg_gap_us = gap ? atoi(gap) : 0;
   }
   ctx->scratch = static_cast<uint8_t*>(scratch);
   sym_sizes(c, ctx->sym_bytes);
@@ -765,11 +772,16 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
     CK(launch_gemm_v(vexp, ctx->map_recv, *m13, ctx->map_rw13, ctx->map_act_out, lo.s1, d.H, ctx->num_sms, st));
   }
   ++ctx->launches;
+  if (ctx->dbg_gap_us > 0) k_spin<<<1, 1, 0, st>>>(ctx->dbg_gap_us * 1000ll);
   MARK(8);
   if (f32) {
     CK(launch_sgemm(ctx, lo.s2, ctx->scratch + s.act, w2, ctx->local_base[PROBE_BUF_REP_W2], d.F, st));
   } else {
     CK(launch_gemm_v(vexp, ctx->map_act, *m2, ctx->map_rw2, ctx->map_y, lo.s2, d.F, ctx->num_sms, st));
+    if (ctx->dbg_gemm2_repeat && li.nparts == 0) {   // same result again, after a GEMM2 instead of a GEMM1
+      CK(cudaMemsetAsync(&lo.s2->counter, 0, sizeof(int32_t), st));
+      CK(launch_gemm_v(vexp, ctx->map_act, *m2, ctx->map_rw2, ctx->map_y, lo.s2, d.F, ctx->num_sms, st));
+    }
   }
   ++ctx->launches;
   k_window_stamp<<<1, 64, 0, st>>>(d, ctx->at<int64_t>(s.win_t0), 1, sym_of(ctx), PROBE_BUF_BOARD, lo.group_rows,
