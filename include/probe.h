@@ -282,8 +282,10 @@ probe_status probe_profile_read(probe_ctx ctx, float* ms, int32_t* n_out);
  * the address to place in probe_init's peer table; probe_ipc_close unmaps an imported base
  * (address returned by import minus offset).  When local_ranks < ep_size, forward /
  * predict / prefetch insert device-side barriers on the symmetric signal pad
- * (st.release.sys / ld.acquire.sys): after the count all-gather, after dispatch, after the
- * expert GEMMs, after the predicted-count all-gather, and after the replica pushes. */
+ * (st.release.sys / ld.acquire.sys, epochs kept in device memory so captured graphs replay
+ * correctly): after the count all-gather, after dispatch (and the pre-dispatch), after the
+ * expert GEMMs (per-slot wire) or after the partial-sum push (dedup wire), after the
+ * predicted-count all-gather, and after the replica pushes. */
 probe_status probe_ipc_export(const void* dev_ptr, uint8_t handle[64], uint64_t* offset);
 probe_status probe_ipc_import(const uint8_t handle[64], uint64_t offset, uint64_t* dev_ptr);
 probe_status probe_ipc_close(uint64_t dev_ptr_base);
