@@ -353,10 +353,17 @@ __global__ void k_count_scan(Dims d, int nchunks, const int32_t* __restrict__ hi
   const int gl = blockIdx.x;
   for (int e = threadIdx.x; e < d.E; e += blockDim.x) {
     int run = 0;
-    for (int c = 0; c < nchunks; ++c) {
-      const size_t o = (static_cast<size_t>(gl) * nchunks + c) * d.E + e;
-      cbase[o] = run;
-      run += hist[o];
+    // 8 chunk histograms in flight per step (the scan is a serial chain of L2 round trips otherwise)
+    for (int c0 = 0; c0 < nchunks; c0 += 8) {
+      int h[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        h[u] = c0 + u < nchunks ? hist[(static_cast<size_t>(gl) * nchunks + c0 + u) * d.E + e] : 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (c0 + u < nchunks) cbase[(static_cast<size_t>(gl) * nchunks + c0 + u) * d.E + e] = run;
+        run += h[u];
+      }
     }
     const int off = board_off(d, parity, 0) + (d.R0 + gl) * d.E + e;
     for (int r = 0; r < d.G; ++r) reinterpret_cast<int32_t*>(sym.at(buf_board, d.G, r))[off] = run;
