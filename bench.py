@@ -185,6 +185,18 @@ def _wire_dedup(args, world):
     return args.wire == "dedup" or (args.wire == "auto" and world > 1)
 
 
+def _gate_fuse(args, GL, shape):
+    """`--gate-fuse auto`: the gate GEMM of layer L also computes layer L+1's prior logits and
+    predictor activation (x read once, probe_config.fuse_gate_predictor) when several logical ranks
+    share this GPU — their dispatch is HBM-bound and an aux-stream predictor re-reading x slows it.
+    With one rank per GPU the NVLink dispatch leaves the SMs idle and hides the aux-stream predictor
+    (P:467), so the paper's placement stays."""
+    ok = shape.E % 32 == 0 and shape.k <= 8
+    if args.gate_fuse == "auto":
+        return ok and GL > 1
+    return ok and args.gate_fuse == "1"
+
+
 def measure(shape, args, env, light=False, dedup=None, predispatch=False):
     """Bench one configuration: PROBE (timed, profiled), static EP, and unless `light` the
     EP emulation, e2e, roofline and CPU baseline.  Rank 0 returns the JSON dict (else None)."""
@@ -202,7 +214,7 @@ def measure(shape, args, env, light=False, dedup=None, predispatch=False):
                       local_ranks=GL, replica_budget=3, kmax=16, n_sat=n_sat, alpha_ps=alpha_ps, beta_ps=beta_ps,
                       bw_bytes_per_us=bw_Bpus, capacity_factor=args.cap if G > 1 else 1.0,
                       dedup_wire=(_wire_dedup(args, world) if dedup is None else dedup) or predispatch,
-                      predispatch=predispatch)
+                      predispatch=predispatch, fuse_gate_predictor=_gate_fuse(args, GL, shape))
     if world > 1:
         from paper_2602_00509_b200.dist import make_runtime_distributed
         rt = make_runtime_distributed(cfg, dev, pg)
@@ -256,6 +268,8 @@ def measure(shape, args, env, light=False, dedup=None, predispatch=False):
         q = (L + 1) % 2
         xx = li.x if x is None else x
         fp = (use_plan and L > 0) if fwd_plan is None else fwd_plan
+        if use_plan and cfg.fuse_gate_predictor:
+            rt.predict_prepare(L + 1, W[q], res[q][0])
         rt.forward(L, xx, W[p], None, w13[p], w2[p], out, use_plan=fp)
         if use_plan:
             rt.predict(L + 1, xx, W[q], None, res[q][0], res[q][1])
@@ -335,6 +349,8 @@ def measure(shape, args, env, light=False, dedup=None, predispatch=False):
     pst = torch.empty(8, dtype=torch.int64, device=dev)
     li = pool[L % POOL]
     p, q = L % 2, (L + 1) % 2
+    if cfg.fuse_gate_predictor:
+        rt.predict_prepare(L + 1, W[q], res[q][0])
     rt.forward(L, li.x, W[p], None, w13[p], w2[p], out, use_plan=True)
     rt.predict(L + 1, li.x, W[q], None, res[q][0], res[q][1], pred_counts=pc)
     rt.plan(L + 1, win, stats=pst)
@@ -438,6 +454,8 @@ def measure(shape, args, env, light=False, dedup=None, predispatch=False):
                 main.wait_event(ev_in)
                 for e in o_free[bsel]:
                     main.wait_event(e)
+                if cfg.fuse_gate_predictor:
+                    rt.predict_prepare(L + 1, W[q], res[q][0])
                 rt.forward(L, x_dev[bsel], W[p], None, w13[p], w2[p], o_dev[bsel], use_plan=True)
                 rt.predict(L + 1, x_dev[bsel], W[q], None, res[q][0], res[q][1], stream=auxs)
                 if not args.modeled_window:
@@ -547,7 +565,8 @@ def measure(shape, args, env, light=False, dedup=None, predispatch=False):
                                        f"T={T}/rank{' (decode batch)' if decode else ''} EP={G} "
                                        f"({GL} logical ranks per GPU)",
                            "zipf_s": args.zipf, "window_ns": gemm_ns, "n_sat": n_sat,
-                           "dedup_wire": bool(cfg.dedup_wire), "out_dtype": "bf16" if args.out_bf16 else "fp32"},
+                           "dedup_wire": bool(cfg.dedup_wire), "out_dtype": "bf16" if args.out_bf16 else "fp32",
+                           "gate_fused_predictor": bool(cfg.fuse_gate_predictor)},
                 "static_ep": {"value": val(ms_static), "unit": "tokens/s" if decode else "ms",
                               "ms_per_step": ms_static, "speedup_probe_vs_static": ms_static / ms,
                               "phases_ms": static_phases},
@@ -573,6 +592,7 @@ def measure(shape, args, env, light=False, dedup=None, predispatch=False):
                                    f"T={T}/rank EP={G} ({GL} logical ranks per GPU)",
                        "out_dtype": "bf16" if args.out_bf16 else "fp32",
                        "wire": "dedup (one row per unique (token, dest))" if cfg.dedup_wire else "per-slot rows",
+                       "gate_fused_predictor": bool(cfg.fuse_gate_predictor),
                        "zipf_s": args.zipf, "replica_budget": 3, "kmax": 16, "alpha_ps": alpha_ps,
                        "beta_ps": beta_ps, "n_sat": n_sat, "window_ns": gemm_ns,
                        "l2": "inputs larger than L2 (x 268 MB/layer at C1, weights 1.2 GB/parity); no flush"},
@@ -793,6 +813,9 @@ def parse_args(argv=None):
                     help="predictor Ŵ1·x GEMM on CTA pairs (library default 1)")
     ap.add_argument("--l2hint", type=lambda v: int(v, 0), default=0, help="expert-GEMM TMA L2 hint mask (probe.h)")
     ap.add_argument("--cpu-tokens", type=int, default=1024, help="oracle expert-FFN sample, tokens per rank")
+    ap.add_argument("--gate-fuse", default="auto", choices=["auto", "0", "1"],
+                    help="gate GEMM also computes the next layer's prior + predictor activation "
+                         "(auto: when several logical ranks share the GPU)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

@@ -92,6 +92,15 @@ typedef struct {
                              experts on a side stream WHILE the gate computes the actual routing; the dispatch
                              then ships payload only for (token, dest) pairs the prediction missed, and the
                              receiver expands hits from the pre-dispatch buffer.  0 = off. */
+  int32_t fuse_gate_predictor; /* 1: after probe_predict_prepare(L+1), probe_moe_forward(L) computes the gate
+                             logits W_L·x, the NEXT layer's prior W_{L+1}·x and the predictor activation
+                             a = bf16(SiLU(Ŵ¹_{L+1}·x)) (Eq. (P), R8) in ONE tensor-core GEMM over x, and
+                             probe_predict(L+1) runs only the residual Ŵ²·a, the top-k and n̂.  Eq. (P) is
+                             unchanged; x is read once instead of three times, but the predictor's x-side
+                             FLOPs move from the aux stream onto the gate.  Pays when the dispatch is HBM-bound
+                             (several logical ranks per GPU); with one rank per GPU the NVLink dispatch hides
+                             the aux-stream predictor and 0 is right.  Requires bf16, E % 32 == 0 and
+                             top_k <= 8.  0 = off. */
   int64_t alpha_ps;       /* compute cost per routed pair, picoseconds (F̄/F_peak, R11) */
   int64_t beta_ps;        /* comm cost per remote pair, picoseconds (2·2H/BW_net, Eq. 5, λ=1) */
   int64_t bw_bytes_per_us;/* BW_net for Eq. 6 replica caps */
@@ -164,6 +173,20 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
                            const void* w_router_next, const float* b_router_next,
                            const void* w_res1, const void* w_res2, int32_t* pred_counts,
                            float* pred_logits, void* stream);
+
+/* Fused gate + predictor stage 1 (probe_config.fuse_gate_predictor = 1).  Arms the NEXT
+ * probe_moe_forward(next_layer - 1) of this context: its gate GEMM then multiplies x by
+ * [W_{next_layer-1} ; w_router_next ; w_res1] in one tcgen05 pass (x read once, tiles of the
+ * three weight blocks interleaved per row chunk so they share x in L2) and keeps the prior
+ * logits W_{next_layer}·x (fp32) and a = bf16(SiLU(Ŵ¹·x)) (R8) for probe_predict(next_layer),
+ * which must then be called with the same x, T, w_router_next and w_res1 (otherwise it
+ * recomputes both, so the result never depends on the arming).  Eq. (P) is unchanged: only the
+ * place where its two x-side products are computed moves.
+ *   w_router_next [E, H] bf16;  w_res1 [h, H] bf16 or NULL (prior only)
+ * Host-side only (records pointers; enqueues nothing).  PROBE_ESTATE if the config did not
+ * enable the fusion. */
+probe_status probe_predict_prepare(probe_ctx ctx, int32_t next_layer, const void* w_router_next,
+                                   const void* w_res1);
 
 /* Balance planning for `next_layer` (Algorithm 1 under R10-R22; integer costs).
  *   pred_counts [G, E] int32 device, or NULL ⇒ the board written by probe_predict

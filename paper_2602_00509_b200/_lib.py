@@ -23,7 +23,7 @@ EXPORTS = ["probe_workspace", "probe_init", "probe_moe_forward", "probe_predict"
            "probe_prefetch", "probe_debug_layout", "probe_debug_prefetch", "probe_debug_flags", "probe_window", "probe_test_gemm", "probe_check", "probe_last_error",
            "probe_finalize", "probe_launch_count", "probe_profile", "probe_profile_read", "probe_bench_gemm",
            "probe_ipc_export", "probe_ipc_import", "probe_ipc_close", "probe_set_option",
-           "probe_history_update", "probe_distill_grad", "probe_distill_apply"]
+           "probe_history_update", "probe_distill_grad", "probe_distill_apply", "probe_predict_prepare"]
 OPT_EP_EMULATION, OPT_UNFUSED_TOPK, OPT_FUSED_EPILOGUE_TOPK, OPT_AUX_SMS, OPT_PAIR_GEMM = 1, 2, 3, 4, 5
 OPT_AUX_START, OPT_PRED_MAXREG, OPT_L2_HINTS, OPT_PRED_PAIR = 8, 9, 10, 11
 DTYPES = {"bf16": 0, "fp32": 1}      # probe_config.dtype (PROBE_BF16, PROBE_FP32)
@@ -37,7 +37,7 @@ class probe_config(C.Structure):
                 ("num_experts", C.c_int32), ("top_k", C.c_int32), ("hidden", C.c_int32), ("ffn", C.c_int32),
                 ("res_hidden", C.c_int32), ("max_tokens", C.c_int32), ("recv_capacity", C.c_int32),
                 ("replica_budget", C.c_int32), ("kmax", C.c_int32), ("n_sat", C.c_int32), ("dtype", C.c_int32),
-                ("dedup_wire", C.c_int32), ("predispatch", C.c_int32),
+                ("dedup_wire", C.c_int32), ("predispatch", C.c_int32), ("fuse_gate_predictor", C.c_int32),
                 ("alpha_ps", C.c_int64), ("beta_ps", C.c_int64), ("bw_bytes_per_us", C.c_int64),
                 ("expert_bytes", C.c_int64)]
 
@@ -55,7 +55,9 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    if path == LIB_PATH:
+    if path == LIB_PATH and os.environ.get("PROBE_LIB_PATH"):   # A/B of two builds (tools only)
+        path = os.environ["PROBE_LIB_PATH"]
+    elif path == LIB_PATH:
         from . import build as _build
         try:
             if _build.stale():
@@ -73,6 +75,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "probe_init": (i32, [C.POINTER(probe_config), C.POINTER(C.c_uint64), vp, C.POINTER(vp)]),
         "probe_moe_forward": (i32, [vp, i32, vp, i32, vp, vp, vp, vp, i32, vp, i32, vp, vp, vp]),
         "probe_predict": (i32, [vp, i32, vp, i32, vp, vp, vp, vp, vp, vp, vp]),
+        "probe_predict_prepare": (i32, [vp, i32, vp, vp]),
         "probe_plan": (i32, [vp, i32, vp, vp, vp, vp, vp, vp]),
         "probe_prefetch": (i32, [vp, i32, vp, vp, i32, vp]),
         "probe_debug_layout": (i32, [vp, vp, vp, vp, vp, vp, vp]),

@@ -31,7 +31,9 @@ enum : int {
   EPI_NONE = 3,        // timing experiments: no stores
   EPI_TOPK = 4,        // router: per-row top-k (logit ↓, id ↑) + softmax over the k → ids, weights (a1)
   EPI_TOPK_COUNT = 5,  // predictor: per-row top-k → atomic per-(rank, expert) counts n̂ (a2, R9)
-  EPI_F16 = 6          // fp16 C (expert output Y, D2): |y| > 65504 raises kErrYRange in *aux
+  EPI_F16 = 6,         // fp16 C (expert output Y, D2): |y| > 65504 raises kErrYRange in *aux
+  EPI_F32_ACC = 7      // fp32 C = accumulator + aux (same layout): the predictor residual added onto
+                       // the prior logits (Eq. (P)); out-of-place, so a repeated call gives the same C
 };
 constexpr int kErrYRange = 8;   // device error bit (kernels.cuh ERR_Y_RANGE)
 constexpr int kTopkMax = 8;   // fused top-k supports k <= 8 (larger k uses the unfused kernel)
@@ -50,6 +52,8 @@ struct GemmGroup {
   int32_t topk;        // EPI_TOPK*: k
   int32_t rows_per_rank;  // EPI_TOPK_COUNT: tokens per rank (rank = (a_row + row) / rows_per_rank)
   int32_t k_off;       // first K element of the (first) K segment: split-K partial products
+  int32_t n_split;     // EPI_F32, > 0: columns >= n_split go to `aux` at column - n_split (same ldc);
+                       // a multiple of 32, so no 32-column chunk straddles it
   void* out;           // output of row 0 / col 0 of this group (EPI_TOPK: int32 ids [m, k])
   void* aux;           // EPI_TOPK: fp32 weights [m, k]; EPI_TOPK_COUNT: int32 counts [ranks, n]
   const float* bias;   // EPI_TOPK*: optional fp32 bias [n]
@@ -181,14 +185,27 @@ __device__ __forceinline__ void epi_store_manual(const float* tile, int lane, co
     }
     return;
   }
-  if (G.mode == EPI_F32) {
+  if (G.mode == EPI_F32 || G.mode == EPI_F32_ACC) {
+    // fused gate + predictor GEMM (EPI_F32 with n_split): the chunk lands in the second output
+    const bool hi = G.n_split > 0 && col0 >= G.n_split;
+    float* base = reinterpret_cast<float*>(hi ? G.aux : G.out);
+    const int c0 = hi ? col0 - G.n_split : col0;
+    const int nlim = hi ? G.n - G.n_split : (G.n_split > 0 ? G.n_split : G.n);
+    const bool accum = G.mode == EPI_F32_ACC;
 #pragma unroll
     for (int it = 0; it < 8; ++it) {
       const int rl = it * 4 + (lane >> 3), j = lane & 7;
       const int grow = row0 + rl;
-      if (grow < G.m && col0 + 4 * j < G.n)
-        *reinterpret_cast<float4*>(reinterpret_cast<float*>(G.out) + static_cast<size_t>(grow) * G.ldc + col0 + 4 * j) =
-            *reinterpret_cast<const float4*>(tile + swz(rl, j));
+      if (grow < G.m && c0 + 4 * j < nlim) {
+        float4* dst = reinterpret_cast<float4*>(base + static_cast<size_t>(grow) * G.ldc + c0 + 4 * j);
+        float4 v = *reinterpret_cast<const float4*>(tile + swz(rl, j));
+        if (accum) {
+          const float4 o = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(G.aux) +
+                                                            static_cast<size_t>(grow) * G.ldc + c0 + 4 * j);
+          v.x = o.x + v.x; v.y = o.y + v.y; v.z = o.z + v.z; v.w = o.w + v.w;
+        }
+        *dst = v;
+      }
     }
   } else {
 #pragma unroll
@@ -231,7 +248,8 @@ __device__ __forceinline__ void epi_chunk(float* tiles, int& tsel, int lane, con
   // halves the predictor's SiLU GEMM time against per-lane stores (C1 shape: 216 → ~120 µs).
   const bool bf16t = G.tma_out && (G.mode == EPI_SWIGLU || G.mode == EPI_SILU_BF16);
   const bool f16 = G.mode == EPI_F16 || bf16t;
-  float* tile = f16 ? tiles + tsel * 512 : tiles + tsel * 1024;
+  const int slot = tsel & 0xff;
+  float* tile = f16 ? tiles + slot * 512 : tiles + slot * 1024;
   if (lane == 0) {
     if (f16) ptx::bulk_wait_read<2 * NB - 1>();
     else ptx::bulk_wait_read<NB - 1>();          // the TMA store that last read this tile is done
@@ -285,7 +303,7 @@ __device__ __forceinline__ void epi_chunk(float* tiles, int& tsel, int lane, con
     if (lane == 0) ptx::bulk_commit();
   }
   __syncwarp();
-  tsel = (tsel + 1) % (f16 ? 2 * NB : NB);
+  tsel = (tsel & ~0xff) | ((slot + 1) % (f16 ? 2 * NB : NB));
 }
 
 // Fused router / predictor top-k (a1, a2): row = token (lane).  The k-element list is
@@ -375,6 +393,15 @@ __device__ __forceinline__ void epi_tile(uint32_t tb, int lane, int part, const 
     }
   } else {
     // two chunks in flight per TMEM wait
+    // A launch may mix 32-bit and 16-bit staging only across groups (the fused gate +
+    // predictor GEMM: fp32 logits tiles, then TMA-stored bf16 activation tiles).  The slot
+    // rotation assumes one geometry, so a change of kind drains this warp's stores first.
+    const int kind = (G.mode == EPI_F16 || (G.tma_out && G.mode == EPI_SILU_BF16)) ? 0x100 : 0;
+    if ((tsel & 0x100) != kind) {
+      if (lane == 0) ptx::bulk_wait_read<0>();
+      __syncwarp();
+      tsel = kind;
+    }
 #pragma unroll 1
     for (int c = part; c < BN / 32; c += 2 * NPART) {
       const int c2 = c + NPART;
@@ -704,43 +731,62 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
     int qs = 0;
     uint32_t qph = 0;
     int raw_next = (lane == 0 && leader) ? claim_raw(sched, unit) : 0;
-    while (true) {
-      int tile = 0;
+    // Tile ids go through the queue ONE TILE AHEAD: the next tile is claimed / published (leader)
+    // or received (peer) right after the current tile's first k-block is issued, and its group
+    // descriptor is loaded then, so the queue fence, the group search and the descriptor's
+    // global-memory latency overlap the current tile's loads instead of stalling the ring at the
+    // tile boundary (K = 768 tiles are only 12 k-blocks: this boundary cost was ~15% of GEMM2).
+    auto next_tile = [&]() -> int {
+      int t = 0;
       if (lane == 0) {
         if (leader) {
-          tile = claim_finish(sched, unit, raw_next);
-          if (tile >= 0) raw_next = claim_raw(sched, unit);   // next claim in flight during this tile
+          t = claim_finish(sched, unit, raw_next);
+          if (t >= 0) raw_next = claim_raw(sched, unit);   // next claim in flight during this tile
           ptx::mbar_wait(&qempty[qs], qph ^ 1);
-          tq[qs] = tile;
-          ptx::st_cluster_u32(ptx::mapa(ptx::smem_u32(const_cast<int*>(&tq[qs])), 1), static_cast<uint32_t>(tile));
+          tq[qs] = t;
+          ptx::st_cluster_u32(ptx::mapa(ptx::smem_u32(const_cast<int*>(&tq[qs])), 1), static_cast<uint32_t>(t));
           ptx::fence_acq_rel_cluster();          // the DSMEM store before the remote arrive (once per tile)
           ptx::mbar_arrive(&qfull[qs]);
           ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&qfull[qs]), 1));
         } else {
           ptx::mbar_wait_cluster(&qfull[qs], qph);
-          tile = tq[qs];
+          t = tq[qs];
           ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&qempty[qs]), 0));
         }
       }
-      tile = __shfl_sync(0xffffffffu, tile, 0);
+      t = __shfl_sync(0xffffffffu, t, 0);
       if (++qs == kTileQ) { qs = 0; qph ^= 1; }
-      if (tile < 0) break;
-      const int gi = gemm_find_group(ts, ng, tile);
-      const GemmGroup& G = sched->g[gi];
-      const int nt = gemm_ntiles_n(G, BN);
-      const int tin = tile - ts[gi];
-      const int mb = tin / nt, nb = tin % nt;
-      const int arow = G.a_row + mb * 256 + static_cast<int>(rank) * 128;
+      return t;
+    };
+    // raw descriptor fields of a tile (loaded early, used one tile later)
+    struct Desc { int tin, nt, a_row, b_row, mode, n, k_off, b_sel; };
+    auto load_desc = [&](int t) -> Desc {
+      Desc d;
+      const int gi = gemm_find_group(ts, ng, t);
+      const GemmGroup* G = &sched->g[gi];
+      d.tin = t - ts[gi];
+      d.a_row = G->a_row; d.b_row = G->b_row; d.mode = G->mode; d.n = G->n; d.k_off = G->k_off; d.b_sel = G->b_sel;
+      return d;
+    };
+    int tile = next_tile();
+    Desc nd{};
+    if (tile >= 0) nd = load_desc(tile);
+    while (tile >= 0) {
+      const Desc cd = nd;
+      const int bno = cd.mode == EPI_SWIGLU ? BN / 2 : BN;
+      const int nt = (cd.n + bno - 1) / bno;
+      const int mb = cd.tin / nt, nb = cd.tin % nt;
+      const int arow = cd.a_row + mb * 256 + static_cast<int>(rank) * 128;
       int brow;
-      if (G.mode == EPI_SWIGLU) brow = G.b_row + (rank ? G.n : 0) + nb * (BN / 2);
-      else brow = G.b_row + nb * BN + static_cast<int>(rank) * (BN / 2);
-      const int koff = G.k_off;
-      const bool bsel = G.b_sel != 0;
+      if (cd.mode == EPI_SWIGLU) brow = cd.b_row + (rank ? cd.n : 0) + nb * (BN / 2);
+      else brow = cd.b_row + nb * BN + static_cast<int>(rank) * (BN / 2);
+      const bool bsel = cd.b_sel != 0;
+      int nxt = -1;
       for (int kb = 0; kb < num_kb; ++kb) {
         const bool second = kb >= kb1;
         const CUtensorMap* ta = second ? &tmA2 : &tmA;
         const CUtensorMap* tb = (second || bsel) ? &tmB1 : &tmB0;
-        const int kc = second ? (kb - kb1) * 64 : koff + kb * 64;
+        const int kc = second ? (kb - kb1) * 64 : cd.k_off + kb * 64;
         if (lane == 0) {
           GEMM_TIMED_WAIT(&empty[stage], phase ^ 1, 0);
           if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (L::A_BYTES + L::B_BYTES));
@@ -751,7 +797,16 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        if (kb == 0) {
+          nxt = next_tile();
+          if (nxt >= 0) nd = load_desc(nxt);
+        }
       }
+      if (num_kb == 0) {
+        nxt = next_tile();
+        if (nxt >= 0) nd = load_desc(nxt);
+      }
+      tile = nxt;
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader CTA only)

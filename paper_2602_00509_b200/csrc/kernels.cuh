@@ -1547,4 +1547,39 @@ __global__ void k_write_sched(GemmSched* s, SmallGroups sg) {
   }
 }
 
+// Fused gate + predictor stage 1 (probe_config.fuse_gate_predictor): the proto groups (row 0,
+// M rows) are repeated for every chunk of CM rows, chunk-major, so the tiles that run at the
+// same time share their A rows — x streams from HBM once and the other weight blocks' tiles of
+// the chunk hit L2.  One block; thread i writes group i, thread 0 then forms the tile prefix.
+__global__ void k_write_sched_chunked(GemmSched* s, SmallGroups sg, int M, int CM) {
+  const int nc = (M + CM - 1) / CM;
+  const int ng = nc * sg.n;
+  for (int i = threadIdx.x; i < ng; i += blockDim.x) {
+    const int c = i / sg.n;
+    GemmGroup g = sg.g[i % sg.n];
+    const int r0 = c * CM;
+    const size_t es = (g.mode == EPI_F32 || g.mode == EPI_F32_ACC) ? 4 : 2;
+    g.a_row += r0;
+    g.m = min(CM, M - r0);
+    g.out_row += r0;
+    g.out = static_cast<uint8_t*>(g.out) + static_cast<size_t>(r0) * g.ldc * es;
+    if (g.n_split > 0) g.aux = static_cast<uint8_t*>(g.aux) + static_cast<size_t>(r0) * g.ldc * es;
+    s->g[i] = g;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s->num_groups = ng;
+    gemm_finalize_sched(s, sg.BN, sg.TM ? sg.TM : 128);
+  }
+}
+
+// [W_L ; W_{L+1} ; Ŵ1] row blocks into one B operand (16-byte copies; byte counts % 16 == 0)
+__global__ void k_concat3(uint4* __restrict__ dst, const uint4* __restrict__ a, int64_t na,
+                          const uint4* __restrict__ b, int64_t nb, const uint4* __restrict__ c, int64_t nc) {
+  const int64_t n = na + nb + nc;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[i] = i < na ? a[i] : (i < na + nb ? b[i - na] : c[i - na - nb]);
+}
+
 }  // namespace probe

@@ -126,6 +126,7 @@ struct Scratch {
   size_t quota[2], reps[2], stats[2], pfctr[2], pids[2];
   size_t split_cum, slot_of, src_off, group_rows, reps_used;
   size_t s_g1, s_g2, s_gate, s_p1, s_p2, flags, win_t0, act, total;
+  size_t gprior[2], gact[2], wcat, s_gp;   // fused gate + predictor stage 1 (by predicted-layer parity)
 };
 
 Scratch scratch_layout(const probe_config& c) {
@@ -167,6 +168,15 @@ Scratch scratch_layout(const probe_config& c) {
   s.flags = take(256);
   s.win_t0 = take(64);
   s.act = take(GL * cap * F * esz(c));
+  // fused gate + predictor stage 1: prior logits and activation double-buffered by the parity of
+  // the predicted layer (gate(L+1) on the main stream may run while predict(L+1) still reads them)
+  const bool gp = c.fuse_gate_predictor != 0;
+  for (int p = 0; p < 2; ++p) {
+    s.gprior[p] = take(gp ? GL * T * E * 4 : 16);
+    s.gact[p] = take(gp ? GL * T * h * 2 : 16);
+  }
+  s.wcat = take(gp ? (2 * E + h) * c.hidden * 2 : 16);
+  s.s_gp = take(gp ? sizeof(GemmSched) : 16);
   s.total = al(o, 1024);
   return s;
 }
@@ -210,6 +220,12 @@ struct probe_ctx_s {
   std::vector<std::pair<cudaEvent_t, unsigned long long>> ev_cap;
   int fwd_layer = -1000, pred_layer[2] = {-1000, -1000}, plan_layer[2] = {-1000, -1000},
       pf_layer[2] = {-1000, -1000};
+  // fused gate + predictor stage 1: armed by probe_predict_prepare, done by the forward
+  int gp_next = -1000;
+  const void* gp_wn = nullptr;
+  const void* gp_w1 = nullptr;
+  struct GpDone { int layer = -1000; const void* x = nullptr; int T = 0; const void* wn = nullptr; const void* w1 = nullptr; };
+  GpDone gp_done[2];
   int last_fwd_parity = 0;
   int last_T = 0;
   int num_sms = 148;
@@ -389,7 +405,7 @@ void launch_topk(const Dims& d, int T, int nchunks, cudaStream_t st, const float
 GemmGroup mk_group(int a_row, int m, int b_row, int b_sel, int mode, int n, int ldc, void* out) {
   GemmGroup g;
   g.a_row = a_row; g.m = m; g.b_row = b_row; g.b_sel = b_sel; g.mode = mode; g.n = n; g.ldc = ldc;
-  g.tile_start = 0; g.out_row = 0; g.tma_out = 0; g.topk = 0; g.rows_per_rank = 1; g.k_off = 0; g.out = out;
+  g.tile_start = 0; g.out_row = 0; g.tma_out = 0; g.topk = 0; g.rows_per_rank = 1; g.k_off = 0; g.n_split = 0; g.out = out;
   g.aux = nullptr; g.bias = nullptr;
   return g;
 }
@@ -485,6 +501,10 @@ static probe_status validate(const probe_config& c) {
   if (c.dedup_wire != 0 && c.dedup_wire != 1) return fail(nullptr, PROBE_EINVAL, "dedup_wire %d not in {0, 1}", c.dedup_wire);
   if (c.predispatch != 0 && c.predispatch != 1) return fail(nullptr, PROBE_EINVAL, "predispatch %d not in {0, 1}", c.predispatch);
   if (c.predispatch && !c.dedup_wire) return fail(nullptr, PROBE_EINVAL, "predispatch requires dedup_wire = 1");
+  if (c.fuse_gate_predictor != 0 && c.fuse_gate_predictor != 1)
+    return fail(nullptr, PROBE_EINVAL, "fuse_gate_predictor %d not in {0, 1}", c.fuse_gate_predictor);
+  if (c.fuse_gate_predictor && (c.dtype != PROBE_BF16 || c.num_experts % 32 || c.top_k > kTopkMax))
+    return fail(nullptr, PROBE_ESHAPE, "fuse_gate_predictor needs bf16, E %% 32 == 0 and top_k <= %d", kTopkMax);
   if (static_cast<int64_t>(c.local_ranks) * c.recv_capacity > (1ll << 30) ||
       static_cast<int64_t>(c.local_ranks) * c.max_tokens > (1ll << 28))
     return fail(nullptr, PROBE_ECAPACITY, "capacity too large");
@@ -651,10 +671,56 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   // serial selection at 1 warp per SM sub-partition, which measured slower.
   const bool sel = d.k <= kTopkMax && d.E <= kMaxE && !ctx->unfused;
   const bool fused_gate = sel && ctx->fused_epi_topk && !f32;
+  // fused gate + predictor stage 1 (probe_predict_prepare(layer+1) armed it): one GEMM over x for
+  // [W_L ; W_{L+1} ; Ŵ1] → gate logits, prior logits of L+1, a = bf16(SiLU(Ŵ1 x)) (Eq. (P), R8)
+  const bool gp = ctx->cfg.fuse_gate_predictor && ctx->gp_next == layer + 1 && sel && !fused_gate && !f32;
+  const int gpp = (layer + 1) & 1;
+  if (gp) {
+    const uint64_t M = GL * T, h = d.h;
+    const bool res = ctx->gp_w1 != nullptr;
+    const uint64_t wrows = 2 * E + (res ? h : 0);
+    const int64_t blk = static_cast<int64_t>(E * H * 2 / 16);
+    k_concat3<<<ctx->num_sms, 256, 0, st>>>(ctx->at<uint4>(s.wcat), static_cast<const uint4*>(w_router), blk,
+                                            static_cast<const uint4*>(ctx->gp_wn), blk,
+                                            static_cast<const uint4*>(ctx->gp_w1),
+                                            res ? static_cast<int64_t>(h * H * 2 / 16) : 0);
+    CKL();
+    const bool pairg = M >= 256;
+    const CUtensorMap* mw = ctx->maps.get(ctx->scratch + s.wcat, wrows, H, 128);
+    if (!mw) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
+    CUtensorMap mact;
+    const bool tma_act = res && h % 32 == 0 && make_map_bf16_out(&mact, ctx->scratch + s.gact[gpp], M, h);
+    SmallGroups sg{};
+    sg.BN = 256;
+    sg.TM = pairg ? 256 : 128;
+    sg.n = res ? 2 : 1;
+    sg.g[0] = mk_group(0, static_cast<int>(M), 0, 0, EPI_F32, 2 * d.E, d.E, ctx->at<float>(s.logits));
+    sg.g[0].n_split = d.E;
+    sg.g[0].aux = ctx->at<float>(s.gprior[gpp]);
+    if (res) {
+      sg.g[1] = mk_group(0, static_cast<int>(M), 2 * d.E, 0, EPI_SILU_BF16, d.h, d.h, ctx->scratch + s.gact[gpp]);
+      sg.g[1].tma_out = tma_act ? 1 : 0;
+    }
+    // ≤ 256 row chunks (≤ 512 groups), each a whole number of tiles
+    const int TM = sg.TM;
+    const int CM = static_cast<int>(((M + 255) / 256 + TM - 1) / TM * TM);
+    k_write_sched_chunked<<<1, 256, 0, st>>>(ctx->at<GemmSched>(s.s_gp), sg, static_cast<int>(M), CM);
+    CKL();
+    CK(launch_gemm_v(pairg ? V_2CTA_256_6_4 : V_256_4_4, *mx, *mw, *mw, tma_act ? mact : *mx,
+                     ctx->at<GemmSched>(s.s_gp), d.H, ctx->num_sms, st));
+    ctx->gp_done[gpp].layer = layer + 1;
+    ctx->gp_done[gpp].x = x;
+    ctx->gp_done[gpp].T = T;
+    ctx->gp_done[gpp].wn = ctx->gp_wn;
+    ctx->gp_done[gpp].w1 = ctx->gp_w1;
+    ctx->gp_next = -1000;
+  }
   SmallGroups sg{};
   sg.n = 1;
   sg.BN = d.E <= 128 ? 128 : 256;
-  if (fused_gate) {
+  if (gp) {
+    // logits already written by the fused GEMM above
+  } else if (fused_gate) {
     sg.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_TOPK, d.E, d.E, ctx->at<int32_t>(s.ids));
     sg.g[0].topk = d.k;
     sg.g[0].aux = ctx->at<float>(s.gw);
@@ -662,9 +728,12 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   } else {
     sg.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_F32, d.E, d.E, ctx->at<float>(s.logits));
   }
-  k_write_sched<<<1, 32, 0, st>>>(ctx->at<GemmSched>(s.s_gate), sg);
-  CKL();
-  if (f32) {
+  if (!gp) {
+    k_write_sched<<<1, 32, 0, st>>>(ctx->at<GemmSched>(s.s_gate), sg);
+    CKL();
+  }
+  if (gp) {
+  } else if (f32) {
     CK(launch_sgemm(ctx, ctx->at<GemmSched>(s.s_gate), x, w_router, w_router, d.H, st));
   } else {
     const CUtensorMap* mr = ctx->maps.get(w_router, E, H, sg.BN / 2);
@@ -870,7 +939,37 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
   // epilogue top-k keeps neither logits nor per-token sets (NEXT-4 pre-dispatch needs the sets)
   const bool epi_topk = ctx->fused_epi_topk && !pred_logits && !ctx->cfg.predispatch;
   int32_t* pids = ctx->cfg.predispatch ? ctx->at<int32_t>(s.pids[pp]) : nullptr;
-  if (f32) {
+  // stage 1 (prior W_{L+1}·x and a = bf16(SiLU(Ŵ1 x))) already computed by the fused gate GEMM
+  // of probe_moe_forward(next_layer-1) for exactly these operands?
+  const auto& gd = ctx->gp_done[pp];
+  const bool gp = ctx->cfg.fuse_gate_predictor && fused && !f32 && gd.layer == next_layer && gd.x == x &&
+                  gd.T == T && gd.wn == w_router_next && gd.w1 == w_res1;
+  if (gp) {
+    // stage 2: l̂ = prior + Ŵ2·a (EPI_F32_ACC on the 1-CTA kernel, K = h, out of place), then the
+    // top-k select adds b and writes n̂ (Eq. (P), R9)
+    float* prior = ctx->at<float>(s.gprior[pp]);
+    float* lhat = prior;
+    if (w_res1) {
+      const int BN = d.E <= 128 ? 128 : 256;
+      const CUtensorMap* ma = ctx->maps.get(ctx->scratch + s.gact[pp], GL * T, h, 128);
+      const CUtensorMap* m2 = ctx->maps.get(w_res2, E, h, BN / 2);
+      if (!ma || !m2) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
+      SmallGroups s2{};
+      s2.BN = BN;
+      s2.n = 1;
+      lhat = ctx->at<float>(s.pprior);
+      s2.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_F32_ACC, d.E, d.E, lhat);
+      s2.g[0].aux = prior;
+      k_write_sched<<<1, 32, 0, st>>>(ctx->at<GemmSched>(s.s_p2), s2);
+      CKL();
+      CK(launch_gemm_v(BN == 128 ? V_128_6_4 : V_256_4_4, *ma, *m2, *m2, *ma, ctx->at<GemmSched>(s.s_p2), d.h,
+                       ctx->aux_sms, st));
+      ++ctx->launches;
+    }
+    CK(launch_select<true>(d, T, nchunks, st, lhat, b_router_next, nullptr, nullptr, nullptr, nullptr,
+                           ctx->at<int32_t>(s.pred_local), pred_logits, pids));
+    ++ctx->launches;
+  } else if (f32) {
     // fp32 parity path: prior x·W_{L+1}ᵀ and z = x·Ŵ1ᵀ → a = bf16(SiLU(z)) (R8) in one grouped
     // SIMT launch, residual a·Ŵ2ᵀ, then the warp top-k sums prior + b + residual (Eq. (P))
     SmallGroups sg{};
@@ -996,6 +1095,20 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
   CK(ev_record(ctx, ctx->ev_pred[pp], st));
   ctx->pred_layer[pp] = next_layer;
   ctx->pred_T[pp] = (pids && fused && !f32) ? T : 0;   // per-token sets exist only on the select path
+  return PROBE_OK;
+}
+
+probe_status probe_predict_prepare(probe_ctx ctx, int32_t next_layer, const void* w_router_next,
+                                   const void* w_res1) {
+  if (!ctx) return fail(nullptr, PROBE_EINVAL, "null ctx");
+  if (!ctx->cfg.fuse_gate_predictor)
+    return fail(ctx, PROBE_ESTATE, "probe_predict_prepare: probe_config.fuse_gate_predictor is 0");
+  if (!w_router_next) return fail(ctx, PROBE_EINVAL, "probe_predict_prepare: null w_router_next");
+  if (w_res1 && ctx->cfg.res_hidden <= 0) return fail(ctx, PROBE_ESHAPE, "residual given but res_hidden == 0");
+  if (next_layer < 1) return fail(ctx, PROBE_EINVAL, "next_layer %d < 1 (layer 0 is not predicted, R29)", next_layer);
+  ctx->gp_next = next_layer;
+  ctx->gp_wn = w_router_next;
+  ctx->gp_w1 = w_res1;
   return PROBE_OK;
 }
 

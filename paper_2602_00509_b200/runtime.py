@@ -38,6 +38,7 @@ class ProbeConfig:
     dtype: str = "bf16"            # "bf16" (product path, tcgen05) or "fp32" (parity path, SIMT fp32 GEMMs)
     dedup_wire: bool = False       # one wire row per unique (token, dest) + R25 partial-sum combine
     predispatch: bool = False      # NEXT-4: pre-dispatch to predicted experts' home ranks during the gate
+    fuse_gate_predictor: bool = False  # gate GEMM also computes the next layer's prior and Ŵ1 activation
 
     def __post_init__(self):
         if self.local_ranks == 0:
@@ -52,7 +53,8 @@ class ProbeConfig:
     def to_c(self) -> probe_config:
         return probe_config(self.G, self.rank_begin, self.local_ranks, self.E, self.k, self.H, self.F, self.h,
                             self.T, self.recv_capacity, self.replica_budget, self.kmax, self.n_sat,
-                            _lib.DTYPES[self.dtype], int(self.dedup_wire), int(self.predispatch), self.alpha_ps, self.beta_ps,
+                            _lib.DTYPES[self.dtype], int(self.dedup_wire), int(self.predispatch),
+                            int(self.fuse_gate_predictor), self.alpha_ps, self.beta_ps,
                             self.bw_bytes_per_us, self.expert_bytes)
 
     @property
@@ -147,6 +149,10 @@ class ProbeRuntime:
         st = self.lib.probe_predict(self.ctx, next_layer, _ptr(x), T, _ptr(w_router_next), _ptr(b_router_next),
                                     _ptr(w_res1), _ptr(w_res2), _ptr(pred_counts), _ptr(pred_logits), s)
         check("probe_predict", st, self.ctx)
+
+    def predict_prepare(self, next_layer: int, w_router_next, w_res1=None):
+        st = self.lib.probe_predict_prepare(self.ctx, next_layer, _ptr(w_router_next), _ptr(w_res1))
+        check("probe_predict_prepare", st, self.ctx)
 
     def plan(self, next_layer: int, window_ns, pred_counts=None, replicas=None, quota=None, stats=None,
              stream=None):

@@ -42,6 +42,7 @@ class CaseCfg:
     residual_kind: str = "bounded"  # "relabel": exact residual that changes the predicted sets (n̂)
     dedup_wire: bool = False        # one wire row per unique (token, dest) + R25 partial-sum combine
     predispatch: bool = False       # NEXT-4: pre-dispatch to predicted experts' home ranks during the gate
+    fuse_gate_predictor: bool = False  # gate GEMM of layer 0 also computes layer 1's prior + Ŵ1 activation
 
     @property
     def es(self) -> int:
@@ -73,7 +74,8 @@ def run_gpu(case: CaseCfg):
                       replica_budget=case.replica_budget, alpha_ps=case.alpha_ps, beta_ps=case.beta_ps,
                       n_sat=case.n_sat, capacity_factor=case.capacity_factor,
                       bw_bytes_per_us=case.bw_bytes_per_us, dtype=case.dtype,
-                      dedup_wire=case.dedup_wire or case.predispatch, predispatch=case.predispatch)
+                      dedup_wire=case.dedup_wire or case.predispatch, predispatch=case.predispatch,
+                      fuse_gate_predictor=case.fuse_gate_predictor)
     rt = ProbeRuntime(cfg)
     if case.ep_emulation:
         from paper_2602_00509_b200._lib import OPT_EP_EMULATION
@@ -122,6 +124,8 @@ def run_gpu(case: CaseCfg):
     stats = torch.empty(8, dtype=torch.int64, device=dev)
     win = torch.full((G,), case.window_ns, dtype=torch.int64, device=dev)
     res = {}
+    if case.fuse_gate_predictor:        # layer 0's gate GEMM also computes stage 1 of layer 1's predictor
+        rt.predict_prepare(1, W[1], r1)
     rt.forward(0, L0.x, W[0], b[0], w13[0], w2[0], out[0], use_plan=False, topk_ids=ids[0], topk_w=gw[0])
     if os.environ.get("PROBE_TEST_SYNC_L0"):      # debugging aid: serialise layer 0 before the aux track
         torch.cuda.synchronize()

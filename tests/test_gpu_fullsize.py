@@ -27,7 +27,10 @@ def bench_case(shape, zipf_s=1.0, sample=4096, cap=4.0, out_fp32=True, **kw):
 
 
 CASES = {
-    "C1-bench": bench_case(pi.C1),
+    # bench.py's default (--gate-fuse auto with 8 ranks on one GPU): layer 0's gate GEMM also
+    # computes layer 1's prior logits and predictor activation
+    "C1-bench": bench_case(pi.C1, fuse_gate_predictor=True),
+    "C1-unfused-gate": bench_case(pi.C1, sample=1024),
     "C1-s1.5": bench_case(pi.C1, zipf_s=1.5),
     "C1-bf16-out": bench_case(pi.C1, sample=1024, out_fp32=False),
     # a residual that changes n̂ (exact relabelling of the designed prediction)
@@ -36,8 +39,8 @@ CASES = {
     "C1-natural-T1024": bench_case(pi.C1.with_(T=1024), zipf_s=1.2, sample=0, gen="natural", residual=False),
     "C1-dedup-wire": bench_case(pi.C1, sample=1024, dedup_wire=True),
     "C1-predispatch": bench_case(pi.C1, sample=1024, predispatch=True),
-    "C2-decode": bench_case(pi.C2, sample=0),
-    "C3-T2048": bench_case(pi.C3.with_(T=2048), sample=0, cap=3.0),
+    "C2-decode": bench_case(pi.C2, sample=0, fuse_gate_predictor=True),
+    "C3-T2048": bench_case(pi.C3.with_(T=2048), sample=0, cap=3.0, fuse_gate_predictor=True),
 }
 
 

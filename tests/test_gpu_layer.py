@@ -94,6 +94,25 @@ CASES = {
                                    bias=True),
     "predictor-pair-gemm-relabel": CaseCfg(pi.C0.with_(name="ppr", E=64, k=8, H=1536, F=256, T=200, G=4),
                                            zipf_s=1.2, residual_kind="relabel"),
+    # fused gate + predictor stage 1 (probe_config.fuse_gate_predictor): layer 0's gate GEMM over
+    # [W_0 ; W_1 ; Ŵ1] (row-chunk interleaved groups, split fp32 epilogue, TMA bf16 activation),
+    # then layer 1's predictor runs only Ŵ2·a (out-of-place accumulate) + select
+    "gate-fused-predictor": CaseCfg(pi.C0.with_(name="gfp", E=32, k=4, H=512, F=256, T=300, G=4), zipf_s=1.2,
+                                    fuse_gate_predictor=True),
+    "gate-fused-predictor-relabel-bias": CaseCfg(pi.C0.with_(name="gfr", E=64, k=8, H=1536, F=256, T=200, G=4),
+                                                 zipf_s=1.2, residual_kind="relabel", bias=True,
+                                                 fuse_gate_predictor=True),
+    "gate-fused-predictor-one-cta": CaseCfg(pi.C0.with_(name="gf1", E=32, k=4, H=256, F=256, T=50, G=2),
+                                            zipf_s=1.3, fuse_gate_predictor=True),
+    "gate-fused-prior-only": CaseCfg(pi.C0.with_(name="gfn", E=32, k=4, H=512, F=256, T=300, G=4), zipf_s=1.2,
+                                     residual=False, fuse_gate_predictor=True),
+    "gate-fused-ragged-h": CaseCfg(pi.C0.with_(name="gfh", E=32, k=4, H=320, F=320, T=300, G=4), zipf_s=1.3,
+                                   bias=True, fuse_gate_predictor=True),    # h = 80: manual bf16 stores
+    "gate-fused-E256": CaseCfg(pi.C0.with_(name="gfe", E=256, k=8, H=1024, F=128, T=64, G=8), zipf_s=1.0,
+                               residual_kind="relabel", fuse_gate_predictor=True),
+    "gate-fused-natural-predispatch": CaseCfg(pi.C0.with_(name="gfpd", E=64, k=8, H=512, F=256, T=300, G=4),
+                                              zipf_s=1.2, gen="natural", residual=False, predispatch=True,
+                                              fuse_gate_predictor=True),
     # the layer call runs with T below the context's max_tokens (workspaces sized for 4x more)
     "T-below-capacity": CaseCfg(pi.C0.with_(name="tbc", E=16, k=4, H=256, F=256, T=77, G=4), zipf_s=1.3,
                                 max_tokens=300),

@@ -55,6 +55,28 @@ def test_workspace_and_validation(lib):
     assert lib.probe_init(C.byref(bad), arr, C.c_void_p(1024), C.byref(C.c_void_p())) == 1
 
 
+def test_fuse_gate_predictor_config(lib):
+    """probe_config.fuse_gate_predictor: its double-buffered prior / activation and the
+    concatenated [W_L ; W_{L+1} ; Ŵ1] operand enlarge the scratch; unsupported shapes and
+    dtypes are rejected at init; probe_predict_prepare checks its arguments on the host."""
+    from paper_2602_00509_b200 import ProbeConfig, workspace_sizes
+    base = ProbeConfig(G=8, E=128, k=8, H=2048, F=768, T=8192, h=512, capacity_factor=4.0)
+    fused = ProbeConfig(G=8, E=128, k=8, H=2048, F=768, T=8192, h=512, capacity_factor=4.0,
+                        fuse_gate_predictor=True)
+    extra = workspace_sizes(fused)[_lib.BUF_SCRATCH] - workspace_sizes(base)[_lib.BUF_SCRATCH]
+    M = 8 * 8192
+    need = 2 * (M * 128 * 4 + M * 512 * 2) + (2 * 128 + 512) * 2048 * 2
+    assert need <= extra <= need + 8 * 1024 * 1024     # + one GemmSched and alignment
+    arr = (C.c_uint64 * 7)()
+    for kw in (dict(E=16), dict(dtype="fp32"), dict(k=9)):
+        c = dict(G=2, E=32, k=4, H=256, F=256, T=64, h=64, fuse_gate_predictor=True)
+        c.update(kw)
+        bad = ProbeConfig(**c).to_c()
+        assert lib.probe_init(C.byref(bad), arr, C.c_void_p(1024), C.byref(C.c_void_p())) == 2, kw
+        assert b"fuse_gate_predictor" in lib.probe_last_error(None)
+    assert lib.probe_predict_prepare(None, 1, C.c_void_p(256), None) == 1
+
+
 def test_fp32_workspace(lib):
     """dtype = PROBE_FP32 (parity path): receive rows, Y and replica slots are fp32, and
     𝒲 = 3·H·F·4 is the checked expert size."""
