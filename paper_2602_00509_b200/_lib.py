@@ -100,6 +100,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "probe_profile_read": (i32, [vp, vp, C.POINTER(C.c_int32)]),
     }
     for name, (res, args) in sig.items():
+        if path != LIB_PATH and not hasattr(lib, name):     # an older build under A/B (tools only)
+            continue
         f = getattr(lib, name)
         f.restype = res
         f.argtypes = args

@@ -505,39 +505,54 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     int qs = 0;
     uint32_t qph = 0;
     int raw_next = lane == 0 ? claim_raw(sched, -1) : 0;
-    while (true) {
-      int tile = 0;
+    // tile ids one tile ahead, as in the CTA-pair kernel (the group search and the descriptor's
+    // global loads overlap the current tile's TMA loads)
+    auto next_tile = [&]() -> int {
+      int t = 0;
       if (lane == 0) {
-        tile = claim_finish(sched, -1, raw_next);
-        if (tile >= 0) raw_next = claim_raw(sched, -1);   // next tile's claim in flight during this tile
+        t = claim_finish(sched, -1, raw_next);
+        if (t >= 0) raw_next = claim_raw(sched, -1);   // next tile's claim in flight during this tile
         ptx::mbar_wait(&qempty[qs], qph ^ 1);
-        tq[qs] = tile;
+        tq[qs] = t;
         ptx::mbar_arrive(&qfull[qs]);
       }
-      tile = __shfl_sync(0xffffffffu, tile, 0);
+      t = __shfl_sync(0xffffffffu, t, 0);
       if (++qs == kTileQ) { qs = 0; qph ^= 1; }
-      if (tile < 0) break;
-      const int gi = gemm_find_group(ts, ng, tile);
-      const GemmGroup& G = sched->g[gi];
-      const int nt = gemm_ntiles_n(G, BN);
-      const int tin = tile - ts[gi];
-      const int mb = tin / nt, nb = tin % nt;
-      const int arow = G.a_row + mb * 128;
+      return t;
+    };
+    struct Desc { int tin, a_row, b_row, mode, n, k_off, b_sel; };
+    auto load_desc = [&](int t) -> Desc {
+      Desc d;
+      const int gi = gemm_find_group(ts, ng, t);
+      const GemmGroup* G = &sched->g[gi];
+      d.tin = t - ts[gi];
+      d.a_row = G->a_row; d.b_row = G->b_row; d.mode = G->mode; d.n = G->n; d.k_off = G->k_off; d.b_sel = G->b_sel;
+      return d;
+    };
+    int tile = next_tile();
+    Desc nd{};
+    if (tile >= 0) nd = load_desc(tile);
+    while (tile >= 0) {
+      const Desc cd = nd;
+      const int bno = cd.mode == EPI_SWIGLU ? BN / 2 : BN;
+      const int nt = (cd.n + bno - 1) / bno;
+      const int mb = cd.tin / nt, nb = cd.tin % nt;
+      const int arow = cd.a_row + mb * 128;
       int brow0, brow1;
-      if (G.mode == EPI_SWIGLU) {
-        brow0 = G.b_row + nb * (BN / 2);
-        brow1 = brow0 + G.n;
+      if (cd.mode == EPI_SWIGLU) {
+        brow0 = cd.b_row + nb * (BN / 2);
+        brow1 = brow0 + cd.n;
       } else {
-        brow0 = G.b_row + nb * BN;
+        brow0 = cd.b_row + nb * BN;
         brow1 = brow0 + BN / 2;
       }
-      const int koff = G.k_off;
-      const bool bsel = G.b_sel != 0;
+      const bool bsel = cd.b_sel != 0;
+      int nxt = -1;
       for (int kb = 0; kb < num_kb; ++kb) {
         const bool second = kb >= kb1;
         const CUtensorMap* ta = second ? &tmA2 : &tmA;
         const CUtensorMap* tb = (second || bsel) ? &tmB1 : &tmB0;
-        const int kc = second ? (kb - kb1) * 64 : koff + kb * 64;
+        const int kc = second ? (kb - kb1) * 64 : cd.k_off + kb * 64;
         if (lane == 0) {
           GEMM_TIMED_WAIT(&empty[stage], phase ^ 1, 0);
           ptx::mbar_arrive_expect_tx(&full[stage], L::A_BYTES + L::B_BYTES);
@@ -547,7 +562,16 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        if (kb == 0) {
+          nxt = next_tile();
+          if (nxt >= 0) nd = load_desc(nxt);
+        }
       }
+      if (num_kb == 0) {
+        nxt = next_tile();
+        if (nxt >= 0) nd = load_desc(nxt);
+      }
+      tile = nxt;
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer

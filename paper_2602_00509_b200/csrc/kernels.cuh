@@ -824,12 +824,12 @@ __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o
     GemmGroup g1;
     g1.a_row = arow; g1.m = m; g1.b_row = wslot * 2 * d.F; g1.b_sel = is_rep; g1.mode = EPI_SWIGLU;
     g1.n = d.F; g1.ldc = d.F; g1.tile_start = 0; g1.out_row = arow; g1.tma_out = !in.f32;   // bf16 act by TMA
-    g1.topk = 0; g1.rows_per_rank = 1; g1.k_off = 0; g1.aux = nullptr; g1.bias = nullptr;
+    g1.topk = 0; g1.rows_per_rank = 1; g1.k_off = 0; g1.n_split = 0; g1.aux = nullptr; g1.bias = nullptr;
     g1.out = static_cast<uint8_t*>(in.act) + static_cast<size_t>(arow) * d.F * (in.f32 ? 4 : 2);
     GemmGroup g2;
     g2.a_row = arow; g2.m = m; g2.b_row = wslot * d.H; g2.b_sel = is_rep; g2.mode = in.f32 ? EPI_F32 : EPI_F16;
     g2.n = d.H; g2.ldc = d.H; g2.tile_start = 0; g2.out_row = arow; g2.tma_out = !in.f32 && (d.H % 32 == 0);
-    g2.topk = 0; g2.rows_per_rank = 1; g2.k_off = 0; g2.aux = o.err; g2.bias = nullptr;
+    g2.topk = 0; g2.rows_per_rank = 1; g2.k_off = 0; g2.n_split = 0; g2.aux = o.err; g2.bias = nullptr;
     g2.out = static_cast<uint8_t*>(in.y_local) + static_cast<size_t>(arow) * d.H * (in.f32 ? 4 : 2);
     o.s1->g[i] = g1;
     o.s2->g[i] = g2;
@@ -1552,11 +1552,19 @@ __global__ void k_write_sched(GemmSched* s, SmallGroups sg) {
 // same time share their A rows — x streams from HBM once and the other weight blocks' tiles of
 // the chunk hit L2.  One block; thread i writes group i, thread 0 then forms the tile prefix.
 __global__ void k_write_sched_chunked(GemmSched* s, SmallGroups sg, int M, int CM) {
+  const int TM = sg.TM ? sg.TM : 128;
   const int nc = (M + CM - 1) / CM;
   const int ng = nc * sg.n;
+  // tile prefix in closed form (every chunk but the last has CM rows): a serial prefix over
+  // 512 groups read back from global memory cost ~0.15 ms on the critical path
+  int nt[2], full = 0;
+  for (int j = 0; j < sg.n; ++j) {
+    nt[j] = gemm_ntiles_n(sg.g[j], sg.BN);
+    full += (CM / TM) * nt[j];
+  }
   for (int i = threadIdx.x; i < ng; i += blockDim.x) {
-    const int c = i / sg.n;
-    GemmGroup g = sg.g[i % sg.n];
+    const int c = i / sg.n, j = i % sg.n;
+    GemmGroup g = sg.g[j];
     const int r0 = c * CM;
     const size_t es = (g.mode == EPI_F32 || g.mode == EPI_F32_ACC) ? 4 : 2;
     g.a_row += r0;
@@ -1564,12 +1572,21 @@ __global__ void k_write_sched_chunked(GemmSched* s, SmallGroups sg, int M, int C
     g.out_row += r0;
     g.out = static_cast<uint8_t*>(g.out) + static_cast<size_t>(r0) * g.ldc * es;
     if (g.n_split > 0) g.aux = static_cast<uint8_t*>(g.aux) + static_cast<size_t>(r0) * g.ldc * es;
+    int ts = c * full;
+    for (int q = 0; q < j; ++q) ts += ((g.m + TM - 1) / TM) * nt[q];
+    g.tile_start = ts;
     s->g[i] = g;
   }
-  __syncthreads();
   if (threadIdx.x == 0) {
+    const int mlast = M - (nc - 1) * CM;
+    int last = 0;
+    for (int j = 0; j < sg.n; ++j) last += ((mlast + TM - 1) / TM) * nt[j];
     s->num_groups = ng;
-    gemm_finalize_sched(s, sg.BN, sg.TM ? sg.TM : 128);
+    s->nparts = 0;
+    s->tile_m = TM;
+    s->stats = nullptr;
+    sched_reset_counters(s);
+    s->total_tiles = (nc - 1) * full + last;
   }
 }
 

@@ -12,7 +12,7 @@ import torch
 
 import oracle as O
 import probe_inputs as pi
-from layer_harness import CaseCfg, compare, run_gpu, run_oracle
+from layer_harness import CaseCfg, compare, f64, run_gpu, run_oracle
 
 pytestmark = pytest.mark.gpu
 
@@ -113,6 +113,8 @@ CASES = {
     "gate-fused-natural-predispatch": CaseCfg(pi.C0.with_(name="gfpd", E=64, k=8, H=512, F=256, T=300, G=4),
                                               zipf_s=1.2, gen="natural", residual=False, predispatch=True,
                                               fuse_gate_predictor=True),
+    "predispatch-natural": CaseCfg(pi.C0.with_(name="gfpd", E=64, k=8, H=512, F=256, T=300, G=4), zipf_s=1.2,
+                                   gen="natural", residual=False, predispatch=True),
     # the layer call runs with T below the context's max_tokens (workspaces sized for 4x more)
     "T-below-capacity": CaseCfg(pi.C0.with_(name="tbc", E=16, k=4, H=256, F=256, T=77, G=4), zipf_s=1.3,
                                 max_tokens=300),
@@ -218,7 +220,44 @@ def test_boundary_errors():
         rt.forward(3, li.x, W, None, w13, w2, out, use_plan=True)
     with pytest.raises(ProbeError, match="INVAL"):
         rt.forward(0, li.x, W, None, w13, None, out)
+    with pytest.raises(ProbeError, match="STATE"):   # fuse_gate_predictor is off in this config
+        rt.predict_prepare(1, W)
     rt.forward(0, li.x, W, None, w13, w2, out)      # still usable
     rt.check()
     assert torch.isfinite(out).all()
+    rt.close()
+
+
+def test_fused_gate_prediction_falls_back_on_other_operands():
+    """probe_predict_prepare arms the gate of ONE forward; probe_predict then reuses its stage 1
+    only for exactly the armed operands.  A predict with another x (or weights) recomputes stage 1
+    itself, so n̂ never depends on the arming."""
+    import torch
+    from paper_2602_00509_b200 import ProbeConfig, ProbeRuntime
+    sh = pi.C0.with_(name="gff", E=32, k=4, H=512, F=256, T=128, G=4)
+    rt = ProbeRuntime(ProbeConfig(G=sh.G, E=sh.E, k=sh.k, H=sh.H, F=sh.F, T=sh.T, h=sh.h,
+                                  fuse_gate_predictor=True))
+    L0 = pi.layer_inputs(sh, 0, 0, 1.2, device="cuda")
+    L1 = pi.layer_inputs(sh, 0, 1, 1.2, device="cuda")
+    W = [pi.router_weight(sh, p, device="cuda") for p in (0, 1)]
+    w13, w2 = pi.expert_weights(sh, 0, device="cuda")
+    r1, r2 = pi.predictor_residual_relabel(sh, 1, device="cuda")
+    out = torch.empty(sh.G, sh.T, sh.H, device="cuda")
+    pcs = [torch.empty(sh.G, sh.E, dtype=torch.int32, device="cuda") for _ in range(3)]
+    rt.predict_prepare(1, W[1], r1)
+    rt.forward(0, L0.x, W[0], None, w13, w2, out)
+    rt.predict(1, L0.x, W[1], None, r1, r2, pred_counts=pcs[0])     # reuses the fused stage 1
+    rt.predict(1, L1.x, W[1], None, r1, r2, pred_counts=pcs[1])     # other x: recomputed
+    rt.predict(1, L0.x, W[1], None, r1, r2, pred_counts=pcs[2])     # back to the armed x: reused again
+    rt.check()
+    torch.cuda.synchronize()
+    x0 = [f64(L0.x[r]) for r in range(sh.G)]
+    x1 = [f64(L1.x[r]) for r in range(sh.G)]
+    W1, a, b = f64(W[1]), f64(r1), f64(r2)
+    exp0 = np.stack([O.predict_counts(x0[r], W1, None, a, b, sh.k)[0] for r in range(sh.G)])
+    exp1 = np.stack([O.predict_counts(x1[r], W1, None, a, b, sh.k)[0] for r in range(sh.G)])
+    assert np.array_equal(pcs[0].cpu().numpy(), exp0)
+    assert np.array_equal(pcs[1].cpu().numpy(), exp1)
+    assert np.array_equal(pcs[2].cpu().numpy(), exp0)
+    assert not np.array_equal(exp0, exp1)
     rt.close()

@@ -23,13 +23,13 @@ pytestmark = pytest.mark.gpu
 POOL = 4
 
 
-@pytest.mark.parametrize("dedup", [False, True])
-def test_graph_layer_loop_every_layer_matches_oracle(dedup):
+@pytest.mark.parametrize("dedup,fused", [(False, False), (True, False), (False, True)])
+def test_graph_layer_loop_every_layer_matches_oracle(dedup, fused):
     from paper_2602_00509_b200 import ProbeConfig, ProbeRuntime
     sh = pi.C0.with_(name="loop", E=32, k=4, H=256, F=256, T=128, G=4)
     G, E, k, H, T = sh.G, sh.E, sh.k, sh.H, sh.T
     cfg = ProbeConfig(G=G, E=E, k=k, H=H, F=sh.F, T=T, h=sh.h, alpha_ps=1, beta_ps=0, dedup_wire=dedup,
-                      predispatch=dedup)
+                      predispatch=dedup, fuse_gate_predictor=fused)
     rt = ProbeRuntime(cfg)
     dev = "cuda"
     pool = [pi.layer_inputs(sh, 0, i, 1.3, device=dev, wrap=POOL) for i in range(POOL)]
@@ -60,6 +60,8 @@ def test_graph_layer_loop_every_layer_matches_oracle(dedup):
         for L in range(L0, L0 + POOL):
             i, p, q = L % POOL, L % 2, (L + 1) % 2
             attention(pool[i].x)
+            if fused:        # layer L's gate GEMM also computes stage 1 of layer L+1's predictor
+                rt.predict_prepare(L + 1, W[q], res[q][0])
             rt.forward(L, pool[i].x, W[p], None, ex[p][0], ex[p][1], outs[i], use_plan=L > 0, topk_ids=ids[i],
                        topk_w=gws[i], stream=s)
             rt.predict(L + 1, pool[i].x, W[q], None, res[q][0], res[q][1])

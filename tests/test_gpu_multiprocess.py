@@ -29,6 +29,9 @@ CASES = {
     "G8-dedup-predispatch": dict(shape=G8, zipf=1.2, dedup=True),
     "G8-graph-replay": dict(shape=G8, zipf=1.2, graph=True),
     "G8-graph-replay-dedup": dict(shape=G8, zipf=1.2, graph=True, dedup=True),
+    # the gate GEMM of layer 0 also computes layer 1's predictor stage 1 (4 ranks per process)
+    "G8-fused-gate-predictor": dict(shape=G8, zipf=1.2, fused=True),
+    "G8-graph-replay-fused-gate-predictor": dict(shape=G8, zipf=1.2, graph=True, fused=True),
 }
 
 
@@ -59,7 +62,8 @@ def _worker(rank, world, port, q, spec):
     R0 = rank * gl
     ranks = list(range(R0, R0 + gl))
     cfg = ProbeConfig(G=G, E=E, k=k, H=H, F=F, T=T, h=sh.h, rank_begin=R0, local_ranks=gl, replica_budget=3,
-                      alpha_ps=1, beta_ps=0, n_sat=0, dtype=dtype, dedup_wire=dedup, predispatch=dedup)
+                      alpha_ps=1, beta_ps=0, n_sat=0, dtype=dtype, dedup_wire=dedup, predispatch=dedup,
+                      fuse_gate_predictor=spec.get("fused", False))
     rt = make_runtime_distributed(cfg, dev)
     L = [pi.layer_inputs(sh, 0, i, zipf, ranks=ranks, device=dev) for i in (0, 1)]
     W = [pi.router_weight(sh, p, device=dev) for p in (0, 1)]
@@ -80,6 +84,9 @@ def _worker(rank, world, port, q, spec):
     quota = torch.empty(G, E, G, dtype=torch.int32, device=dev)
     pc = torch.empty(G, E, dtype=torch.int32, device=dev)
     win = torch.full((G,), 10 ** 9, dtype=torch.int64, device=dev)
+    fused = spec.get("fused", False)
+    if fused:
+        rt.predict_prepare(1, W[1], r1)
     rt.forward(0, xs[0], W[0], None, w13[0], w2[0], out[0], topk_ids=ids[0])
     rt.predict(1, xs[0], W[1], None, r1, r2, pred_counts=pc)
     rt.plan(1, win, replicas=reps, quota=quota)
@@ -94,6 +101,8 @@ def _worker(rank, world, port, q, spec):
         s = torch.cuda.Stream()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=s):
+            if fused:
+                rt.predict_prepare(2, W[0], r1)
             rt.forward(1, xs[1], W[1], None, w13[1], w2[1], out[1], use_plan=True, topk_ids=ids[1], stream=s)
             rt.predict(2, xs[1], W[0], None, r1, r2)
             rt.plan(2, win)
