@@ -232,6 +232,9 @@ def measure(shape, args, env, light=False, dedup=None, predispatch=False):
     if args.l2hint:
         from paper_2602_00509_b200._lib import OPT_L2_HINTS
         rt.set_option(OPT_L2_HINTS, args.l2hint)
+    if args.epi_topk:
+        from paper_2602_00509_b200._lib import OPT_FUSED_EPILOGUE_TOPK
+        rt.set_option(OPT_FUSED_EPILOGUE_TOPK, 1)
     if args.pred_maxreg:
         from paper_2602_00509_b200._lib import OPT_PRED_MAXREG
         rt.set_option(OPT_PRED_MAXREG, args.pred_maxreg)
@@ -813,6 +816,7 @@ def parse_args(argv=None):
                     help="predictor Ŵ1·x GEMM on CTA pairs (library default 1)")
     ap.add_argument("--l2hint", type=lambda v: int(v, 0), default=0, help="expert-GEMM TMA L2 hint mask (probe.h)")
     ap.add_argument("--cpu-tokens", type=int, default=1024, help="oracle expert-FFN sample, tokens per rank")
+    ap.add_argument("--epi-topk", type=int, default=0, help="1: router/predictor top-k in the GEMM epilogue")
     ap.add_argument("--gate-fuse", default="auto", choices=["auto", "0", "1"],
                     help="gate GEMM also computes the next layer's prior + predictor activation "
                          "(auto: when several logical ranks share the GPU)")

@@ -31,9 +31,7 @@ enum : int {
   EPI_NONE = 3,        // timing experiments: no stores
   EPI_TOPK = 4,        // router: per-row top-k (logit ↓, id ↑) + softmax over the k → ids, weights (a1)
   EPI_TOPK_COUNT = 5,  // predictor: per-row top-k → atomic per-(rank, expert) counts n̂ (a2, R9)
-  EPI_F16 = 6,         // fp16 C (expert output Y, D2): |y| > 65504 raises kErrYRange in *aux
-  EPI_F32_ACC = 7      // fp32 C = accumulator + aux (same layout): the predictor residual added onto
-                       // the prior logits (Eq. (P)); out-of-place, so a repeated call gives the same C
+  EPI_F16 = 6          // fp16 C (expert output Y, D2): |y| > 65504 raises kErrYRange in *aux
 };
 constexpr int kErrYRange = 8;   // device error bit (kernels.cuh ERR_Y_RANGE)
 constexpr int kTopkMax = 8;   // fused top-k supports k <= 8 (larger k uses the unfused kernel)
@@ -185,27 +183,19 @@ __device__ __forceinline__ void epi_store_manual(const float* tile, int lane, co
     }
     return;
   }
-  if (G.mode == EPI_F32 || G.mode == EPI_F32_ACC) {
+  if (G.mode == EPI_F32) {
     // fused gate + predictor GEMM (EPI_F32 with n_split): the chunk lands in the second output
     const bool hi = G.n_split > 0 && col0 >= G.n_split;
     float* base = reinterpret_cast<float*>(hi ? G.aux : G.out);
     const int c0 = hi ? col0 - G.n_split : col0;
     const int nlim = hi ? G.n - G.n_split : (G.n_split > 0 ? G.n_split : G.n);
-    const bool accum = G.mode == EPI_F32_ACC;
 #pragma unroll
     for (int it = 0; it < 8; ++it) {
       const int rl = it * 4 + (lane >> 3), j = lane & 7;
       const int grow = row0 + rl;
-      if (grow < G.m && c0 + 4 * j < nlim) {
-        float4* dst = reinterpret_cast<float4*>(base + static_cast<size_t>(grow) * G.ldc + c0 + 4 * j);
-        float4 v = *reinterpret_cast<const float4*>(tile + swz(rl, j));
-        if (accum) {
-          const float4 o = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(G.aux) +
-                                                            static_cast<size_t>(grow) * G.ldc + c0 + 4 * j);
-          v.x = o.x + v.x; v.y = o.y + v.y; v.z = o.z + v.z; v.w = o.w + v.w;
-        }
-        *dst = v;
-      }
+      if (grow < G.m && c0 + 4 * j < nlim)
+        *reinterpret_cast<float4*>(base + static_cast<size_t>(grow) * G.ldc + c0 + 4 * j) =
+            *reinterpret_cast<const float4*>(tile + swz(rl, j));
     }
   } else {
 #pragma unroll
@@ -306,43 +296,78 @@ __device__ __forceinline__ void epi_chunk(float* tiles, int& tsel, int lane, con
   tsel = (tsel & ~0xff) | ((slot + 1) % (f16 ? 2 * NB : NB));
 }
 
-// Fused router / predictor top-k (a1, a2): row = token (lane).  The k-element list is
-// sorted by (value ↓, id ↑) (R3, R4) and lives in registers (KK is a compile-time
-// constant so no index is dynamic).  Columns arrive in ascending expert id, so a new value
-// enters only if it beats the current k-th strictly; a displaced (carried) element may tie
-// with a later-id entry and then wins.
+// Top-k by sorting networks (R3, R4): keys ordered by (value ↓, id ↑), a total order, so any
+// correct network gives the lowest-id tie rule.  Each group of 8 logits is sorted with the
+// 19-comparator odd-even merge network, merged into the running top 8 (the element-wise
+// better of top[i] and group[7-i] is bitonic and holds the top 8 of both), and re-sorted
+// with a 12-comparator bitonic cleaner.  Branch-free with independent comparators per
+// stage: the former insertion chain was predicated over every logit (11 K instructions per
+// warp at C1) and latency-bound at 13 warps per SM.
+__device__ __forceinline__ void topk_ce(float& av, int& ae, float& bv, int& be) {
+  const bool s = (bv > av) || (bv == av && be < ae);
+  const float tv = s ? bv : av;
+  const int te = s ? be : ae;
+  bv = s ? av : bv;
+  be = s ? ae : be;
+  av = tv;
+  ae = te;
+}
+__device__ __forceinline__ void topk_sort8(float (&v)[8], int (&e)[8]) {
+#define CE(i, j) topk_ce(v[i], e[i], v[j], e[j])
+  CE(0, 1); CE(2, 3); CE(4, 5); CE(6, 7);
+  CE(0, 2); CE(1, 3); CE(4, 6); CE(5, 7);
+  CE(1, 2); CE(5, 6);
+  CE(0, 4); CE(1, 5); CE(2, 6); CE(3, 7);
+  CE(2, 4); CE(3, 5);
+  CE(1, 2); CE(3, 4); CE(5, 6);
+#undef CE
+}
+__device__ __forceinline__ void topk_merge8(float (&tv)[8], int (&te)[8], const float (&gv)[8], const int (&ge)[8]) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float bv = gv[7 - i];
+    const int be = ge[7 - i];
+    const bool s = (bv > tv[i]) || (bv == tv[i] && be < te[i]);
+    tv[i] = s ? bv : tv[i];
+    te[i] = s ? be : te[i];
+  }
+#define CE(i, j) topk_ce(tv[i], te[i], tv[j], te[j])
+  CE(0, 4); CE(1, 5); CE(2, 6); CE(3, 7);
+  CE(0, 2); CE(1, 3); CE(4, 6); CE(5, 7);
+  CE(0, 1); CE(2, 3); CE(4, 5); CE(6, 7);
+#undef CE
+}
+
+// Fused router / predictor top-k in the GEMM epilogue (a1, a2): row = token (lane).  Each
+// 32-column TMEM load holds 32 logits of this lane's row; they are ranked 8 at a time with
+// the sorting networks above (keys (value ↓, id ↑), R3, R4) — the same selection and the same
+// fp32 softmax as k_select, with compile-time register indices (no staging, no branches).
 template <int KK, int BN>
 __device__ __forceinline__ void epi_topk(uint32_t tb, int lane, const GemmGroup& G, int row0, float* stage) {
-  float tv[KK];
-  int te[KK];
+  (void)stage;
+  float tv[8];
+  int te[8];
 #pragma unroll
-  for (int j = 0; j < KK; ++j) { tv[j] = -INFINITY; te[j] = 0x7fffffff; }
+  for (int j = 0; j < 8; ++j) { tv[j] = -INFINITY; te[j] = 0x7fffffff; }
 #pragma unroll 1
   for (int c = 0; c < BN / 32; ++c) {
     if (c * 32 >= G.n) break;
     uint32_t v32[32];
     ptx::tmem_ld32_wait(tb + c * 32, v32);
-    // stage the row in smem (element i of row r at r·32 + (i ^ r): conflict-free both ways)
-    __syncwarp();
 #pragma unroll
-    for (int i = 0; i < 32; ++i) stage[lane * 32 + (i ^ lane)] = __uint_as_float(v32[i]);
-    __syncwarp();
-    const int nv = min(32, G.n - c * 32);
-#pragma unroll 1
-    for (int i = 0; i < nv; ++i) {
-      int e = c * 32 + i;
-      float x = stage[lane * 32 + (i ^ lane)] + (G.bias ? __ldg(G.bias + e) : 0.f);
-      if (x > tv[KK - 1]) {
+    for (int q = 0; q < 4; ++q) {
+      float gv[8];
+      int ge[8];
 #pragma unroll
-        for (int j = 0; j < KK; ++j) {
-          if (x > tv[j] || (x == tv[j] && e < te[j])) {
-            const float ov = tv[j];
-            const int oe = te[j];
-            tv[j] = x; te[j] = e;
-            x = ov; e = oe;
-          }
-        }
+      for (int i = 0; i < 8; ++i) {
+        const int e = c * 32 + q * 8 + i;
+        float x = __uint_as_float(v32[q * 8 + i]);
+        if (G.bias && e < G.n) x += __ldg(G.bias + e);
+        gv[i] = e < G.n ? x : -INFINITY;      // columns past n never beat a real logit (larger id)
+        ge[i] = e;
       }
+      topk_sort8(gv, ge);
+      topk_merge8(tv, te, gv, ge);
     }
   }
   const int row = row0 + lane;
@@ -505,54 +530,39 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     int qs = 0;
     uint32_t qph = 0;
     int raw_next = lane == 0 ? claim_raw(sched, -1) : 0;
-    // tile ids one tile ahead, as in the CTA-pair kernel (the group search and the descriptor's
-    // global loads overlap the current tile's TMA loads)
-    auto next_tile = [&]() -> int {
-      int t = 0;
+    while (true) {
+      int tile = 0;
       if (lane == 0) {
-        t = claim_finish(sched, -1, raw_next);
-        if (t >= 0) raw_next = claim_raw(sched, -1);   // next tile's claim in flight during this tile
+        tile = claim_finish(sched, -1, raw_next);
+        if (tile >= 0) raw_next = claim_raw(sched, -1);   // next tile's claim in flight during this tile
         ptx::mbar_wait(&qempty[qs], qph ^ 1);
-        tq[qs] = t;
+        tq[qs] = tile;
         ptx::mbar_arrive(&qfull[qs]);
       }
-      t = __shfl_sync(0xffffffffu, t, 0);
+      tile = __shfl_sync(0xffffffffu, tile, 0);
       if (++qs == kTileQ) { qs = 0; qph ^= 1; }
-      return t;
-    };
-    struct Desc { int tin, a_row, b_row, mode, n, k_off, b_sel; };
-    auto load_desc = [&](int t) -> Desc {
-      Desc d;
-      const int gi = gemm_find_group(ts, ng, t);
-      const GemmGroup* G = &sched->g[gi];
-      d.tin = t - ts[gi];
-      d.a_row = G->a_row; d.b_row = G->b_row; d.mode = G->mode; d.n = G->n; d.k_off = G->k_off; d.b_sel = G->b_sel;
-      return d;
-    };
-    int tile = next_tile();
-    Desc nd{};
-    if (tile >= 0) nd = load_desc(tile);
-    while (tile >= 0) {
-      const Desc cd = nd;
-      const int bno = cd.mode == EPI_SWIGLU ? BN / 2 : BN;
-      const int nt = (cd.n + bno - 1) / bno;
-      const int mb = cd.tin / nt, nb = cd.tin % nt;
-      const int arow = cd.a_row + mb * 128;
+      if (tile < 0) break;
+      const int gi = gemm_find_group(ts, ng, tile);
+      const GemmGroup& G = sched->g[gi];
+      const int nt = gemm_ntiles_n(G, BN);
+      const int tin = tile - ts[gi];
+      const int mb = tin / nt, nb = tin % nt;
+      const int arow = G.a_row + mb * 128;
       int brow0, brow1;
-      if (cd.mode == EPI_SWIGLU) {
-        brow0 = cd.b_row + nb * (BN / 2);
-        brow1 = brow0 + cd.n;
+      if (G.mode == EPI_SWIGLU) {
+        brow0 = G.b_row + nb * (BN / 2);
+        brow1 = brow0 + G.n;
       } else {
-        brow0 = cd.b_row + nb * BN;
+        brow0 = G.b_row + nb * BN;
         brow1 = brow0 + BN / 2;
       }
-      const bool bsel = cd.b_sel != 0;
-      int nxt = -1;
+      const int koff = G.k_off;
+      const bool bsel = G.b_sel != 0;
       for (int kb = 0; kb < num_kb; ++kb) {
         const bool second = kb >= kb1;
         const CUtensorMap* ta = second ? &tmA2 : &tmA;
         const CUtensorMap* tb = (second || bsel) ? &tmB1 : &tmB0;
-        const int kc = second ? (kb - kb1) * 64 : cd.k_off + kb * 64;
+        const int kc = second ? (kb - kb1) * 64 : koff + kb * 64;
         if (lane == 0) {
           GEMM_TIMED_WAIT(&empty[stage], phase ^ 1, 0);
           ptx::mbar_arrive_expect_tx(&full[stage], L::A_BYTES + L::B_BYTES);
@@ -562,16 +572,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        if (kb == 0) {
-          nxt = next_tile();
-          if (nxt >= 0) nd = load_desc(nxt);
-        }
       }
-      if (num_kb == 0) {
-        nxt = next_tile();
-        if (nxt >= 0) nd = load_desc(nxt);
-      }
-      tile = nxt;
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
@@ -755,62 +756,43 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
     int qs = 0;
     uint32_t qph = 0;
     int raw_next = (lane == 0 && leader) ? claim_raw(sched, unit) : 0;
-    // Tile ids go through the queue ONE TILE AHEAD: the next tile is claimed / published (leader)
-    // or received (peer) right after the current tile's first k-block is issued, and its group
-    // descriptor is loaded then, so the queue fence, the group search and the descriptor's
-    // global-memory latency overlap the current tile's loads instead of stalling the ring at the
-    // tile boundary (K = 768 tiles are only 12 k-blocks: this boundary cost was ~15% of GEMM2).
-    auto next_tile = [&]() -> int {
-      int t = 0;
+    while (true) {
+      int tile = 0;
       if (lane == 0) {
         if (leader) {
-          t = claim_finish(sched, unit, raw_next);
-          if (t >= 0) raw_next = claim_raw(sched, unit);   // next claim in flight during this tile
+          tile = claim_finish(sched, unit, raw_next);
+          if (tile >= 0) raw_next = claim_raw(sched, unit);   // next claim in flight during this tile
           ptx::mbar_wait(&qempty[qs], qph ^ 1);
-          tq[qs] = t;
-          ptx::st_cluster_u32(ptx::mapa(ptx::smem_u32(const_cast<int*>(&tq[qs])), 1), static_cast<uint32_t>(t));
+          tq[qs] = tile;
+          ptx::st_cluster_u32(ptx::mapa(ptx::smem_u32(const_cast<int*>(&tq[qs])), 1), static_cast<uint32_t>(tile));
           ptx::fence_acq_rel_cluster();          // the DSMEM store before the remote arrive (once per tile)
           ptx::mbar_arrive(&qfull[qs]);
           ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&qfull[qs]), 1));
         } else {
           ptx::mbar_wait_cluster(&qfull[qs], qph);
-          t = tq[qs];
+          tile = tq[qs];
           ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&qempty[qs]), 0));
         }
       }
-      t = __shfl_sync(0xffffffffu, t, 0);
+      tile = __shfl_sync(0xffffffffu, tile, 0);
       if (++qs == kTileQ) { qs = 0; qph ^= 1; }
-      return t;
-    };
-    // raw descriptor fields of a tile (loaded early, used one tile later)
-    struct Desc { int tin, nt, a_row, b_row, mode, n, k_off, b_sel; };
-    auto load_desc = [&](int t) -> Desc {
-      Desc d;
-      const int gi = gemm_find_group(ts, ng, t);
-      const GemmGroup* G = &sched->g[gi];
-      d.tin = t - ts[gi];
-      d.a_row = G->a_row; d.b_row = G->b_row; d.mode = G->mode; d.n = G->n; d.k_off = G->k_off; d.b_sel = G->b_sel;
-      return d;
-    };
-    int tile = next_tile();
-    Desc nd{};
-    if (tile >= 0) nd = load_desc(tile);
-    while (tile >= 0) {
-      const Desc cd = nd;
-      const int bno = cd.mode == EPI_SWIGLU ? BN / 2 : BN;
-      const int nt = (cd.n + bno - 1) / bno;
-      const int mb = cd.tin / nt, nb = cd.tin % nt;
-      const int arow = cd.a_row + mb * 256 + static_cast<int>(rank) * 128;
+      if (tile < 0) break;
+      const int gi = gemm_find_group(ts, ng, tile);
+      const GemmGroup& G = sched->g[gi];
+      const int nt = gemm_ntiles_n(G, BN);
+      const int tin = tile - ts[gi];
+      const int mb = tin / nt, nb = tin % nt;
+      const int arow = G.a_row + mb * 256 + static_cast<int>(rank) * 128;
       int brow;
-      if (cd.mode == EPI_SWIGLU) brow = cd.b_row + (rank ? cd.n : 0) + nb * (BN / 2);
-      else brow = cd.b_row + nb * BN + static_cast<int>(rank) * (BN / 2);
-      const bool bsel = cd.b_sel != 0;
-      int nxt = -1;
+      if (G.mode == EPI_SWIGLU) brow = G.b_row + (rank ? G.n : 0) + nb * (BN / 2);
+      else brow = G.b_row + nb * BN + static_cast<int>(rank) * (BN / 2);
+      const int koff = G.k_off;
+      const bool bsel = G.b_sel != 0;
       for (int kb = 0; kb < num_kb; ++kb) {
         const bool second = kb >= kb1;
         const CUtensorMap* ta = second ? &tmA2 : &tmA;
         const CUtensorMap* tb = (second || bsel) ? &tmB1 : &tmB0;
-        const int kc = second ? (kb - kb1) * 64 : cd.k_off + kb * 64;
+        const int kc = second ? (kb - kb1) * 64 : koff + kb * 64;
         if (lane == 0) {
           GEMM_TIMED_WAIT(&empty[stage], phase ^ 1, 0);
           if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (L::A_BYTES + L::B_BYTES));
@@ -821,16 +803,7 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        if (kb == 0) {
-          nxt = next_tile();
-          if (nxt >= 0) nd = load_desc(nxt);
-        }
       }
-      if (num_kb == 0) {
-        nxt = next_tile();
-        if (nxt >= 0) nd = load_desc(nxt);
-      }
-      tile = nxt;
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader CTA only)

@@ -156,47 +156,7 @@ __global__ void __launch_bounds__(128) k_topk(Dims d, int T, const float* __rest
 // n̂[rank][e] (R9).  grid (ceil(T/128), GL), block 128 (thread = token).  E % 32 == 0
 // or E < 32 handled by masking.
 // =============================================================================
-// Top-k by sorting networks (R3, R4): keys ordered by (value ↓, id ↑), a total order, so any
-// correct network gives the lowest-id tie rule.  Each group of 8 logits is sorted with the
-// 19-comparator odd-even merge network, merged into the running top 8 (the element-wise
-// better of top[i] and group[7-i] is bitonic and holds the top 8 of both), and re-sorted
-// with a 12-comparator bitonic cleaner.  Branch-free with independent comparators per
-// stage: the former insertion chain was predicated over every logit (11 K instructions per
-// warp at C1) and latency-bound at 13 warps per SM.
-__device__ __forceinline__ void topk_ce(float& av, int& ae, float& bv, int& be) {
-  const bool s = (bv > av) || (bv == av && be < ae);
-  const float tv = s ? bv : av;
-  const int te = s ? be : ae;
-  bv = s ? av : bv;
-  be = s ? ae : be;
-  av = tv;
-  ae = te;
-}
-__device__ __forceinline__ void topk_sort8(float (&v)[8], int (&e)[8]) {
-#define CE(i, j) topk_ce(v[i], e[i], v[j], e[j])
-  CE(0, 1); CE(2, 3); CE(4, 5); CE(6, 7);
-  CE(0, 2); CE(1, 3); CE(4, 6); CE(5, 7);
-  CE(1, 2); CE(5, 6);
-  CE(0, 4); CE(1, 5); CE(2, 6); CE(3, 7);
-  CE(2, 4); CE(3, 5);
-  CE(1, 2); CE(3, 4); CE(5, 6);
-#undef CE
-}
-__device__ __forceinline__ void topk_merge8(float (&tv)[8], int (&te)[8], const float (&gv)[8], const int (&ge)[8]) {
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const float bv = gv[7 - i];
-    const int be = ge[7 - i];
-    const bool s = (bv > tv[i]) || (bv == tv[i] && be < te[i]);
-    tv[i] = s ? bv : tv[i];
-    te[i] = s ? be : te[i];
-  }
-#define CE(i, j) topk_ce(tv[i], te[i], tv[j], te[j])
-  CE(0, 4); CE(1, 5); CE(2, 6); CE(3, 7);
-  CE(0, 2); CE(1, 3); CE(4, 6); CE(5, 7);
-  CE(0, 1); CE(2, 3); CE(4, 5); CE(6, 7);
-#undef CE
-}
+// Top-k by sorting networks: topk_sort8 / topk_merge8 (gemm_sm100.cuh, shared with the GEMM-epilogue top-k).
 
 // The predictor instance (PRED) is capped at 64 registers (8 CTAs of 128 threads per SM) and
 // streams 16 logits per step: it must fit beside a persistent expert-GEMM CTA (224 × 256
@@ -209,7 +169,8 @@ __global__ void __launch_bounds__(128, PRED ? 8 : 1) k_select(Dims d, int T, con
                                                 float* __restrict__ gw, int32_t* __restrict__ pos,
                                                 int32_t* __restrict__ hist, int32_t* __restrict__ counts,
                                                 float* __restrict__ logits_out = nullptr,
-                                                int32_t* __restrict__ pred_ids = nullptr) {
+                                                int32_t* __restrict__ pred_ids = nullptr,
+                                                const float* __restrict__ logits2 = nullptr) {
   __shared__ uint32_t mask[kMaxE * 4];
   __shared__ int32_t scount[kMaxE];
   const int E = d.E;
@@ -236,6 +197,20 @@ __global__ void __launch_bounds__(128, PRED ? 8 : 1) k_select(Dims d, int T, con
         } else {
 #pragma unroll
           for (int u = 0; u < 4; ++u) v[4 * q + u] = (c + 4 * q + u < E) ? row[c + 4 * q + u] : -INFINITY;
+        }
+      }
+      if (PRED && logits2) {   // fused predictor (D10): l̂ = prior + residual, both fp32 GEMM outputs
+        const float* row2 = logits2 + (static_cast<size_t>(gl) * T + t) * E;
+#pragma unroll
+        for (int q = 0; q < CW / 4; ++q) {
+          if (c + 4 * q + 3 < E) {
+            const float4 f = __ldg(reinterpret_cast<const float4*>(row2 + c) + q);
+            v[4 * q] += f.x; v[4 * q + 1] += f.y; v[4 * q + 2] += f.z; v[4 * q + 3] += f.w;
+          } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (c + 4 * q + u < E) v[4 * q + u] += row2[c + 4 * q + u];
+          }
         }
       }
       if (bias) {
@@ -1566,7 +1541,7 @@ __global__ void k_write_sched_chunked(GemmSched* s, SmallGroups sg, int M, int C
     const int c = i / sg.n, j = i % sg.n;
     GemmGroup g = sg.g[j];
     const int r0 = c * CM;
-    const size_t es = (g.mode == EPI_F32 || g.mode == EPI_F32_ACC) ? 4 : 2;
+    const size_t es = g.mode == EPI_F32 ? 4 : 2;
     g.a_row += r0;
     g.m = min(CM, M - r0);
     g.out_row += r0;

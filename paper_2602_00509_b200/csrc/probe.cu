@@ -376,12 +376,12 @@ cudaError_t launch_gemm(const CUtensorMap& a, const CUtensorMap& b0, const CUten
 template <bool PRED>
 cudaError_t launch_select(const Dims& d, int T, int nchunks, cudaStream_t st, const float* lg, const float* b,
                           int32_t* ids, float* gw, int32_t* pos, int32_t* hist, int32_t* cnt,
-                          float* lo = nullptr, int32_t* pids = nullptr) {
+                          float* lo = nullptr, int32_t* pids = nullptr, const float* lg2 = nullptr) {
   const size_t smem = 0;
   dim3 grid(nchunks, d.GL);
 #define SEL(KK)                                                                                         \
   case KK: {                                                                                            \
-    k_select<KK, PRED><<<grid, 128, smem, st>>>(d, T, lg, b, ids, gw, pos, hist, cnt, lo, pids);       \
+    k_select<KK, PRED><<<grid, 128, smem, st>>>(d, T, lg, b, ids, gw, pos, hist, cnt, lo, pids, lg2);  \
     break;                                                                                              \
   }
   switch (d.k) {
@@ -728,6 +728,11 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   } else {
     sg.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_F32, d.E, d.E, ctx->at<float>(s.logits));
   }
+  // fp32 logits by TMA tensor stores (full 32-row slabs; measured 60 vs 80 µs at C1 shapes)
+  CUtensorMap mlog_f32;
+  const bool gate_tma = !gp && !fused_gate && !f32 && d.E % 32 == 0 &&
+                        make_map_f32_out(&mlog_f32, ctx->at<float>(s.logits), GL * T, E);
+  if (gate_tma) sg.g[0].tma_out = 1;
   if (!gp) {
     k_write_sched<<<1, 32, 0, st>>>(ctx->at<GemmSched>(s.s_gate), sg);
     CKL();
@@ -738,8 +743,9 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   } else {
     const CUtensorMap* mr = ctx->maps.get(w_router, E, H, sg.BN / 2);
     if (!mr) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
-    CK(launch_gemm_v(sg.BN == 128 ? V_128_6_4 : V_256_4_4, *mx, *mr, *mr, *mx, ctx->at<GemmSched>(s.s_gate), d.H,
-                     ctx->num_sms, st));
+    CUtensorMap mlog = *mx;
+    CK(launch_gemm_v(sg.BN == 128 ? V_128_6_4 : V_256_4_4, *mx, *mr, *mr, gate_tma ? mlog_f32 : mlog,
+                     ctx->at<GemmSched>(s.s_gate), d.H, ctx->num_sms, st));
   }
   ++ctx->launches;
   MARK(1);
@@ -945,29 +951,31 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
   const bool gp = ctx->cfg.fuse_gate_predictor && fused && !f32 && gd.layer == next_layer && gd.x == x &&
                   gd.T == T && gd.wn == w_router_next && gd.w1 == w_res1;
   if (gp) {
-    // stage 2: l̂ = prior + Ŵ2·a (EPI_F32_ACC on the 1-CTA kernel, K = h, out of place), then the
-    // top-k select adds b and writes n̂ (Eq. (P), R9)
-    float* prior = ctx->at<float>(s.gprior[pp]);
-    float* lhat = prior;
+    // stage 2: residual Ŵ2·a (1-CTA kernel, K = h, fp32 by TMA tensor stores), then the top-k
+    // select forms l̂ = prior + residual + b and writes n̂ (Eq. (P), R9)
+    const float* prior = ctx->at<float>(s.gprior[pp]);
+    const float* resid = nullptr;
     if (w_res1) {
       const int BN = d.E <= 128 ? 128 : 256;
       const CUtensorMap* ma = ctx->maps.get(ctx->scratch + s.gact[pp], GL * T, h, 128);
       const CUtensorMap* m2 = ctx->maps.get(w_res2, E, h, BN / 2);
       if (!ma || !m2) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
+      CUtensorMap mres;
+      if (!make_map_f32_out(&mres, ctx->scratch + s.pres, GL * T, E)) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
       SmallGroups s2{};
       s2.BN = BN;
       s2.n = 1;
-      lhat = ctx->at<float>(s.pprior);
-      s2.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_F32_ACC, d.E, d.E, lhat);
-      s2.g[0].aux = prior;
+      s2.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_F32, d.E, d.E, ctx->at<float>(s.pres));
+      s2.g[0].tma_out = 1;                      // E % 32 == 0 (fuse_gate_predictor requires it)
       k_write_sched<<<1, 32, 0, st>>>(ctx->at<GemmSched>(s.s_p2), s2);
       CKL();
-      CK(launch_gemm_v(BN == 128 ? V_128_6_4 : V_256_4_4, *ma, *m2, *m2, *ma, ctx->at<GemmSched>(s.s_p2), d.h,
+      CK(launch_gemm_v(BN == 128 ? V_128_6_4 : V_256_4_4, *ma, *m2, *m2, mres, ctx->at<GemmSched>(s.s_p2), d.h,
                        ctx->aux_sms, st));
       ++ctx->launches;
+      resid = ctx->at<float>(s.pres);
     }
-    CK(launch_select<true>(d, T, nchunks, st, lhat, b_router_next, nullptr, nullptr, nullptr, nullptr,
-                           ctx->at<int32_t>(s.pred_local), pred_logits, pids));
+    CK(launch_select<true>(d, T, nchunks, st, prior, b_router_next, nullptr, nullptr, nullptr, nullptr,
+                           ctx->at<int32_t>(s.pred_local), pred_logits, pids, resid));
     ++ctx->launches;
   } else if (f32) {
     // fp32 parity path: prior x·W_{L+1}ᵀ and z = x·Ŵ1ᵀ → a = bf16(SiLU(z)) (R8) in one grouped
@@ -1042,12 +1050,15 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
     } else {
       s2.g[0] = mk_group(0, static_cast<int>(GL * T), 0, 0, EPI_F32, d.E, d.E, ctx->at<float>(s.pprior));
     }
+    CUtensorMap mpr;
+    const bool pr_tma = !epi_topk && d.E % 32 == 0 && make_map_f32_out(&mpr, ctx->at<float>(s.pprior), GL * T, E);
+    if (pr_tma) s2.g[0].tma_out = 1;
     k_write_sched<<<1, 32, 0, st>>>(ctx->at<GemmSched>(s.s_p2), s2);
     CKL();
     const int v2 = pair2 ? (BN == 128 ? V_2CTA_128_8_4 : V_2CTA_256_6_4)
                          : (BN == 128 ? (ctx->pred_maxreg ? V_128_6_4_R192 : V_128_6_4) : V_256_4_4);
-    CK(launch_gemm_v(v2, *mx, *mw, w_res1 ? *m2 : *mw, *mx, ctx->at<GemmSched>(s.s_p2), d.H, ctx->aux_sms, st,
-                     w_res1 ? ma : nullptr, w_res1 ? d.h : 0));
+    CK(launch_gemm_v(v2, *mx, *mw, w_res1 ? *m2 : *mw, pr_tma ? mpr : *mx, ctx->at<GemmSched>(s.s_p2), d.H,
+                     ctx->aux_sms, st, w_res1 ? ma : nullptr, w_res1 ? d.h : 0));
     ++ctx->launches;
     if (!epi_topk) {
       CK(launch_select<true>(d, T, nchunks, st, ctx->at<float>(s.pprior), b_router_next, nullptr, nullptr, nullptr,
@@ -1285,7 +1296,8 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
     hs->g[i] = mk_group(g[0], g[1], g[2], 0, emode, n_out, n_out, static_cast<uint8_t*>(C) + static_cast<size_t>(g[3]) * n_out * esz);
     hs->g[i].out_row = g[3];
     hs->g[i].tma_out =
-        (emode == EPI_F32 || emode == EPI_F16 || emode == EPI_SWIGLU || emode == EPI_SILU_BF16) && n_out % 32 == 0 ? 1 : 0;
+        (emode == EPI_F32 || emode == EPI_F16 || emode == EPI_SWIGLU || emode == EPI_SILU_BF16) && n_out % 32 == 0 &&
+                !getenv("PROBE_NO_TMA_OUT") ? 1 : 0;      // analysis: coalesced st.global epilogue instead
     if (topk_aux) {   // test hook: k = 8; TOPK writes ids to C, weights to aux; COUNT: counts [64][N]
       hs->g[i].topk = 8;
       hs->g[i].rows_per_rank = static_cast<int>((a_rows + 63) / 64);

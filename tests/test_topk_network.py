@@ -1,5 +1,5 @@
-"""CPU check of the sorting networks the top-k select kernel uses (kernels.cuh topk_sort8 /
-topk_merge8).  The comparator lists are parsed from the CUDA source and simulated here:
+"""CPU check of the sorting networks the top-k select kernel and the GEMM-epilogue top-k use
+(gemm_sm100.cuh topk_sort8 / topk_merge8).  The comparator lists are parsed from the CUDA source and simulated here:
 by the 0-1 principle, a comparator network sorts every input iff it sorts every 0-1 input,
 so sort8 is checked on all 2^8 binary vectors, and the merge (element-wise better of
 top[i] and group[7-i], then the bitonic cleaner) on all pairs of sorted binary lists; plus
@@ -10,7 +10,7 @@ import random
 import re
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SRC = open(os.path.join(ROOT, "paper_2602_00509_b200", "csrc", "kernels.cuh")).read()
+SRC = open(os.path.join(ROOT, "paper_2602_00509_b200", "csrc", "gemm_sm100.cuh")).read()
 
 
 def _pairs(fn):
