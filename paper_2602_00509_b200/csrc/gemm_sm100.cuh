@@ -296,6 +296,58 @@ __device__ __forceinline__ void epi_chunk(float* tiles, int& tsel, int lane, con
   tsel = (tsel & ~0xff) | ((slot + 1) % (f16 ? 2 * NB : NB));
 }
 
+// fp16 Y with 64-column TMA stores (tma_out == 2): the warp's two adjacent 32-column chunks
+// are staged as one 32-row × 128-byte tile (SWIZZLE_128B: 16-byte chunk j of row r at
+// j ^ (r & 7)) and leave in ONE tensor store of full 128-byte row segments — half the TMA
+// store operations (and half-line writes) of two 64-byte-row stores.  The 4 KB staging slot
+// is single-buffered: the previous store must have finished reading it.
+__device__ __forceinline__ void epi_chunk64_f16(float* tiles, int& tsel, int lane, const uint32_t (&va)[32],
+                                                const uint32_t (&vb)[32], const GemmGroup& G,
+                                                const CUtensorMap* tmC, int row0, int col0, uint64_t store_pol) {
+  char* tile = reinterpret_cast<char*>(tiles);
+  if (lane == 0) ptx::bulk_wait_read<0>();
+  __syncwarp();
+  bool big = false;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    uint4 p;
+    uint32_t* pw = reinterpret_cast<uint32_t*>(&p);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float a = __uint_as_float(j < 4 ? va[8 * j + 2 * q] : vb[8 * (j - 4) + 2 * q]);
+      const float b = __uint_as_float(j < 4 ? va[8 * j + 2 * q + 1] : vb[8 * (j - 4) + 2 * q + 1]);
+      big |= fabsf(a) > 65504.f || fabsf(b) > 65504.f;
+      __half2 hh = __floats2half2_rn(a, b);
+      pw[q] = *reinterpret_cast<uint32_t*>(&hh);
+    }
+    *reinterpret_cast<uint4*>(tile + lane * 128 + ((j ^ (lane & 7)) << 4)) = p;
+  }
+  big = big && row0 + lane < G.m && col0 < G.n;
+  if (__any_sync(0xffffffffu, big) && lane == 0 && G.aux) atomicOr(reinterpret_cast<int*>(G.aux), kErrYRange);
+  if (row0 + 31 < G.m && col0 < G.n) {
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      if (store_pol) ptx::tma_store_2d_hint(tmC, tile, col0, G.out_row + row0, store_pol);
+      else ptx::tma_store_2d(tmC, tile, col0, G.out_row + row0);
+      ptx::bulk_commit();
+    }
+  } else {
+    __syncwarp();
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {       // 4 rows × 128 B per warp store
+      const int rl = it * 4 + (lane >> 3), j = lane & 7;
+      const int grow = row0 + rl;
+      if (grow < G.m && col0 + 8 * j < G.n)
+        *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(G.out) + static_cast<size_t>(grow) * G.ldc + col0 + 8 * j) =
+            *reinterpret_cast<const uint4*>(tile + rl * 128 + ((j ^ (rl & 7)) << 4));
+    }
+    if (lane == 0) ptx::bulk_commit();     // an empty group keeps one group per staged tile
+  }
+  __syncwarp();
+  tsel = 0x200;
+}
+
 // Top-k by sorting networks (R3, R4): keys ordered by (value ↓, id ↑), a total order, so any
 // correct network gives the lowest-id tie rule.  Each group of 8 logits is sorted with the
 // 19-comparator odd-even merge network, merged into the running top 8 (the element-wise
@@ -421,11 +473,21 @@ __device__ __forceinline__ void epi_tile(uint32_t tb, int lane, int part, const 
     // A launch may mix 32-bit and 16-bit staging only across groups (the fused gate +
     // predictor GEMM: fp32 logits tiles, then TMA-stored bf16 activation tiles).  The slot
     // rotation assumes one geometry, so a change of kind drains this warp's stores first.
-    const int kind = (G.mode == EPI_F16 || (G.tma_out && G.mode == EPI_SILU_BF16)) ? 0x100 : 0;
-    if ((tsel & 0x100) != kind) {
+    const bool wide = NPART == 1 && G.mode == EPI_F16 && G.tma_out == 2;
+    const int kind = wide ? 0x200 : (G.mode == EPI_F16 || (G.tma_out && G.mode == EPI_SILU_BF16)) ? 0x100 : 0;
+    if ((tsel & 0x300) != kind) {
       if (lane == 0) ptx::bulk_wait_read<0>();
       __syncwarp();
       tsel = kind;
+    }
+    if (wide) {
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; c += 2) {
+        uint32_t va[32], vb[32];
+        ptx::tmem_ld32x2_wait(tb + c * 32, va, tb + (c + 1) * 32, vb);
+        epi_chunk64_f16(tiles, tsel, lane, va, vb, G, tmC, row0, nb * BN + c * 32, store_pol);
+      }
+      return;
     }
 #pragma unroll 1
     for (int c = part; c < BN / 32; c += 2 * NPART) {

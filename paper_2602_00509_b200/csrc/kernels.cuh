@@ -653,6 +653,7 @@ struct LayoutIn {
   void* act;                    // [GL*cap, F] bf16
   void* y_local;                // [GL*cap, H] fp16 (this process's Y region, D2)
   int f32;                      // fp32 parity path: act and Y are fp32, GEMM2 stores EPI_F32
+  int y_wide;                   // fp16 Y by 64-column (128-byte row) TMA stores (epi_chunk64_f16)
   int l2hint;                   // TMA L2 hints: bits 0-2 expert GEMM1, bits 4-6 expert GEMM2 (GemmSched::l2hint)
 };
 
@@ -803,7 +804,7 @@ __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o
     g1.out = static_cast<uint8_t*>(in.act) + static_cast<size_t>(arow) * d.F * (in.f32 ? 4 : 2);
     GemmGroup g2;
     g2.a_row = arow; g2.m = m; g2.b_row = wslot * d.H; g2.b_sel = is_rep; g2.mode = in.f32 ? EPI_F32 : EPI_F16;
-    g2.n = d.H; g2.ldc = d.H; g2.tile_start = 0; g2.out_row = arow; g2.tma_out = !in.f32 && (d.H % 32 == 0);
+    g2.n = d.H; g2.ldc = d.H; g2.tile_start = 0; g2.out_row = arow; g2.tma_out = (!in.f32 && (d.H % 32 == 0)) ? (in.y_wide ? 2 : 1) : 0;
     g2.topk = 0; g2.rows_per_rank = 1; g2.k_off = 0; g2.n_split = 0; g2.aux = o.err; g2.bias = nullptr;
     g2.out = static_cast<uint8_t*>(in.y_local) + static_cast<size_t>(arow) * d.H * (in.f32 ? 4 : 2);
     o.s1->g[i] = g1;

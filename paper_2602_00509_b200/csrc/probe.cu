@@ -71,15 +71,15 @@ bool make_map_f32_out(CUtensorMap* m, const void* base, uint64_t rows, uint64_t 
 }
 
 // fp16 output map for TMA tensor stores: box {32 cols (64 B), 32 rows}, SWIZZLE_64B.
-bool make_map_f16_out(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols) {
+bool make_map_f16_out(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, bool wide = false) {
   if (!load_encode()) return false;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * 2};
-  cuuint32_t box[2] = {32, 32};
+  cuuint32_t box[2] = {wide ? 64u : 32u, 32};   // wide: 128-byte rows (epi_chunk64_f16, tma_out == 2)
   cuuint32_t es[2] = {1, 1};
   return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, wide ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // bf16 output map for TMA tensor stores (the SwiGLU / SiLU activations): box {32 cols (64 B),
@@ -242,6 +242,7 @@ struct probe_ctx_s {
   bool ep_emulation = false;  // partition expert GEMMs by local rank (probe_set_option)
   bool fused_epi_topk = false;  // top-k in the GEMM epilogue instead of k_select (probe_set_option)
   bool pair_gemm = true;        // expert GEMMs on CTA pairs (cta_group::2); option turns it off
+  bool y_wide = true;           // fp16 Y by 64-column TMA stores (PROBE_Y_WIDE=0 at init: 32-column, A/B)
   // distillation workspace (NEXT-1), allocated on the first probe_distill_grad
   uint8_t* dbuf = nullptr;
   size_t dbytes = 0;
@@ -600,11 +601,12 @@ probe_status probe_init(const probe_config* cfg, const uint64_t* peer_ptrs, void
     return fail(nullptr, PROBE_ECUDA, "probe_init: %s", cudaGetErrorString(e));
   }
   const uint64_t GL = c.local_ranks, cap = c.recv_capacity, H = c.hidden, F = c.ffn;
+  if (const char* yw = getenv("PROBE_Y_WIDE")) ctx->y_wide = yw[0] != '0';   // analysis A/B only
   bool ok = make_map(&ctx->map_recv, ctx->local_base[PROBE_BUF_RECV], GL * cap, H, 128) &&
             make_map(&ctx->map_act, ctx->scratch + ctx->sl.act, GL * cap, F, 128) &&
             make_map(&ctx->map_rw13, ctx->local_base[PROBE_BUF_REP_W13], GL * 2 * kMaxRb * 2 * F, H, 128) &&
             make_map(&ctx->map_rw2, ctx->local_base[PROBE_BUF_REP_W2], GL * 2 * kMaxRb * H, F, 128) &&
-            make_map_f16_out(&ctx->map_y, ctx->local_base[PROBE_BUF_Y], GL * cap, H) &&
+            make_map_f16_out(&ctx->map_y, ctx->local_base[PROBE_BUF_Y], GL * cap, H, ctx->y_wide) &&
             (c.dtype == PROBE_FP32 || make_map_bf16_out(&ctx->map_act_out, ctx->scratch + ctx->sl.act, GL * cap, F));
   if (!ok) {
     delete ctx;
@@ -785,6 +787,7 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   li.y_local = ctx->local_base[PROBE_BUF_Y];
   li.f32 = f32;
   li.l2hint = ctx->l2hint;
+  li.y_wide = ctx->y_wide ? 1 : 0;
   LayoutOut lo;
   lo.split_cum = ctx->at<int32_t>(s.split_cum);
   lo.slot_of = ctx->at<int32_t>(s.slot_of);
@@ -1289,6 +1292,8 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
     hs->stats = dstats;
   }
   const size_t esz = emode == EPI_SWIGLU || emode == EPI_SILU_BF16 || emode == EPI_F16 ? 2 : 4;
+  // PROBE_Y_WIDE=0/1: fp16 outputs by 32- or 64-column TMA stores (A/B of epi_chunk64_f16)
+  const bool y_wide = n_out % 64 == 0 && !(getenv("PROBE_Y_WIDE") && getenv("PROBE_Y_WIDE")[0] == '0');
   int acc = 0;
   int64_t c_rows = 1;
   for (int i = 0; i < num_groups; ++i) {
@@ -1298,6 +1303,7 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
     hs->g[i].tma_out =
         (emode == EPI_F32 || emode == EPI_F16 || emode == EPI_SWIGLU || emode == EPI_SILU_BF16) && n_out % 32 == 0 &&
                 !getenv("PROBE_NO_TMA_OUT") ? 1 : 0;      // analysis: coalesced st.global epilogue instead
+    if (y_wide && emode == EPI_F16 && hs->g[i].tma_out) hs->g[i].tma_out = 2;
     if (topk_aux) {   // test hook: k = 8; TOPK writes ids to C, weights to aux; COUNT: counts [64][N]
       hs->g[i].topk = 8;
       hs->g[i].rows_per_rank = static_cast<int>((a_rows + 63) / 64);
@@ -1316,7 +1322,7 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
   if (emode == EPI_F32 && n_out % 32 == 0) {
     if (!make_map_f32_out(&mc, C, c_rows, n_out)) return fail(nullptr, PROBE_ECUDA, "tensor map encode failed");
   } else if (emode == EPI_F16 && n_out % 32 == 0) {
-    if (!make_map_f16_out(&mc, C, c_rows, n_out)) return fail(nullptr, PROBE_ECUDA, "tensor map encode failed");
+    if (!make_map_f16_out(&mc, C, c_rows, n_out, y_wide)) return fail(nullptr, PROBE_ECUDA, "tensor map encode failed");
   } else if ((emode == EPI_SWIGLU || emode == EPI_SILU_BF16) && n_out % 32 == 0) {
     if (!make_map_bf16_out(&mc, C, c_rows, n_out)) return fail(nullptr, PROBE_ECUDA, "tensor map encode failed");
   } else {
