@@ -35,13 +35,15 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--seq", type=int, default=2048, help="attention sequence length (T per rank = batch · seq)")
     ap.add_argument("--zipf", type=float, default=1.0)
+    ap.add_argument("--gate-fuse", type=int, default=1, help="fused gate + predictor stage 1 (bench.py's 1-GPU default)")
     a = ap.parse_args()
     sh = pi.C1
     dev = torch.device("cuda", 0)
     G, T, H, F_, E = sh.G, sh.T, sh.H, sh.F, sh.E
     al, be, ns, bw = cost_model(H, F_)
     rt = ProbeRuntime(ProbeConfig(G=G, E=E, k=sh.k, H=H, F=F_, T=T, h=sh.h, alpha_ps=al, beta_ps=be, n_sat=ns,
-                                  bw_bytes_per_us=bw, capacity_factor=4.0), dev)
+                                  bw_bytes_per_us=bw, capacity_factor=4.0,
+                                  fuse_gate_predictor=bool(a.gate_fuse)), dev)
     POOL = 4
     pool = [pi.layer_inputs(sh, 0, i, a.zipf, device=dev, wrap=POOL) for i in range(POOL)]
     W = [pi.router_weight(sh, p, device=dev) for p in (0, 1)]
@@ -75,6 +77,8 @@ def main():
         if attn:
             attention(li.x)
         if moe:
+            if use_plan and a.gate_fuse:
+                rt.predict_prepare(L + 1, W[q], res[q][0])
             rt.forward(L, li.x, W[p], None, ex[p][0], ex[p][1], out, use_plan=use_plan and L > 0, stream=main_s)
             if use_plan:
                 rt.predict(L + 1, li.x, W[q], None, res[q][0], res[q][1])
@@ -99,7 +103,8 @@ def main():
 
     n = a.layers
     assert n % 4 == 0, "layers per loop must be a multiple of the input-pool period (4) for graph replays"
-    res_out = {"config": {"shape": "C1", "G": G, "T": T, "layers_per_loop": n, "attention": f"{B}x{a.seq} tokens, "
+    res_out = {"config": {"shape": "C1", "G": G, "T": T, "layers_per_loop": n, "gate_fused_predictor": bool(a.gate_fuse),
+                          "attention": f"{B}x{a.seq} tokens, "
                           f"{nq} q heads / {nkv} kv heads / hd {hd}, causal SDPA + projections (torch library)"}}
     state = {"L": 0}
 
