@@ -665,12 +665,10 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   } else if (prof) {
     CK(cudaEventRecord(ctx->pev(PROBE_NPHASE - 1), st));
   }
-  // a1 gate: logits = x W_rᵀ on tcgen05 with the top-k + softmax fused in the epilogue
-  // (fp32 logits never leave TMEM/registers); then per-chunk dispatch ranks.
-  // a1 gate: logits = x W_rᵀ on tcgen05 (fp32 logits, HBM-bound) → thread-per-token select
-  // (top-k + softmax + dispatch ranks).  The GEMM-epilogue top-k (EPI_TOPK) is available via
-  // PROBE_OPT_FUSED_EPILOGUE_TOPK: it saves the 2×33 MB logits round trip but runs the
-  // serial selection at 1 warp per SM sub-partition, which measured slower.
+  // a1 gate: logits = x W_rᵀ on tcgen05 (fp32 logits by TMA stores, HBM-bound) → thread-per-token
+  // select (top-k by sorting networks + softmax + dispatch ranks).  The GEMM-epilogue top-k
+  // (EPI_TOPK, PROBE_OPT_FUSED_EPILOGUE_TOPK) saves the 2×33 MB logits round trip but measured
+  // 20 µs slower at C1.
   const bool sel = d.k <= kTopkMax && d.E <= kMaxE && !ctx->unfused;
   const bool fused_gate = sel && ctx->fused_epi_topk && !f32;
   // fused gate + predictor stage 1 (probe_predict_prepare(layer+1) armed it): one GEMM over x for
