@@ -1527,7 +1527,7 @@ __global__ void k_write_sched(GemmSched* s, SmallGroups sg) {
 // M rows) are repeated for every chunk of CM rows, chunk-major, so the tiles that run at the
 // same time share their A rows — x streams from HBM once and the other weight blocks' tiles of
 // the chunk hit L2.  One block; thread i writes group i, thread 0 then forms the tile prefix.
-__global__ void k_write_sched_chunked(GemmSched* s, SmallGroups sg, int M, int CM) {
+__device__ void write_sched_chunked(GemmSched* s, const SmallGroups& sg, int M, int CM) {
   const int TM = sg.TM ? sg.TM : 128;
   const int nc = (M + CM - 1) / CM;
   const int ng = nc * sg.n;
@@ -1566,9 +1566,13 @@ __global__ void k_write_sched_chunked(GemmSched* s, SmallGroups sg, int M, int C
   }
 }
 
-// [W_L ; W_{L+1} ; Ŵ1] row blocks into one B operand (16-byte copies; byte counts % 16 == 0)
-__global__ void k_concat3(uint4* __restrict__ dst, const uint4* __restrict__ a, int64_t na,
-                          const uint4* __restrict__ b, int64_t nb, const uint4* __restrict__ c, int64_t nc) {
+// One launch before the fused gate GEMM: every block copies the [W_L ; W_{L+1} ; Ŵ1] row blocks
+// into one B operand (16-byte copies; byte counts % 16 == 0), block 0 also writes the
+// row-chunk interleaved schedule.
+__global__ void k_gate_pred_prep(GemmSched* s, SmallGroups sg, int M, int CM, uint4* __restrict__ dst,
+                                 const uint4* __restrict__ a, int64_t na, const uint4* __restrict__ b, int64_t nb,
+                                 const uint4* __restrict__ c, int64_t nc) {
+  if (blockIdx.x == 0) write_sched_chunked(s, sg, M, CM);
   const int64_t n = na + nb + nc;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)

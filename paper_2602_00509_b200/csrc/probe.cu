@@ -680,11 +680,6 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
     const bool res = ctx->gp_w1 != nullptr;
     const uint64_t wrows = 2 * E + (res ? h : 0);
     const int64_t blk = static_cast<int64_t>(E * H * 2 / 16);
-    k_concat3<<<ctx->num_sms, 256, 0, st>>>(ctx->at<uint4>(s.wcat), static_cast<const uint4*>(w_router), blk,
-                                            static_cast<const uint4*>(ctx->gp_wn), blk,
-                                            static_cast<const uint4*>(ctx->gp_w1),
-                                            res ? static_cast<int64_t>(h * H * 2 / 16) : 0);
-    CKL();
     const bool pairg = M >= 256;
     const CUtensorMap* mw = ctx->maps.get(ctx->scratch + s.wcat, wrows, H, 128);
     if (!mw) return fail(ctx, PROBE_ECUDA, "tensor map encode failed");
@@ -704,7 +699,11 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
     // ≤ 256 row chunks (≤ 512 groups), each a whole number of tiles
     const int TM = sg.TM;
     const int CM = static_cast<int>(((M + 255) / 256 + TM - 1) / TM * TM);
-    k_write_sched_chunked<<<1, 256, 0, st>>>(ctx->at<GemmSched>(s.s_gp), sg, static_cast<int>(M), CM);
+    k_gate_pred_prep<<<ctx->num_sms, 256, 0, st>>>(ctx->at<GemmSched>(s.s_gp), sg, static_cast<int>(M), CM,
+                                                   ctx->at<uint4>(s.wcat), static_cast<const uint4*>(w_router), blk,
+                                                   static_cast<const uint4*>(ctx->gp_wn), blk,
+                                                   static_cast<const uint4*>(ctx->gp_w1),
+                                                   res ? static_cast<int64_t>(h * H * 2 / 16) : 0);
     CKL();
     CK(launch_gemm_v(pairg ? V_2CTA_256_6_4 : V_256_4_4, *mx, *mw, *mw, tma_act ? mact : *mx,
                      ctx->at<GemmSched>(s.s_gp), d.H, ctx->num_sms, st));
