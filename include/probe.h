@@ -179,8 +179,9 @@ probe_status probe_predict(probe_ctx ctx, int32_t next_layer, const void* x, int
  * [W_{next_layer-1} ; w_router_next ; w_res1] in one tcgen05 pass (x read once, tiles of the
  * three weight blocks interleaved per row chunk so they share x in L2) and keeps the prior
  * logits W_{next_layer}·x (fp32) and a = bf16(SiLU(Ŵ¹·x)) (R8) for probe_predict(next_layer),
- * which must then be called with the same x, T, w_router_next and w_res1 (otherwise it
- * recomputes both, so the result never depends on the arming).  Eq. (P) is unchanged: only the
+ * which reuses them when called with the same x, T, w_router_next and w_res1 pointers
+ * (otherwise it recomputes both).  Reuse is decided by pointer, so the caller must not change
+ * the CONTENTS of x, W_{next_layer} or Ŵ¹ between that forward and that predict.  Eq. (P) is unchanged: only the
  * place where its two x-side products are computed moves.
  *   w_router_next [E, H] bf16;  w_res1 [h, H] bf16 or NULL (prior only)
  * Host-side only (records pointers; enqueues nothing).  PROBE_ESTATE if the config did not
