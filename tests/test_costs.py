@@ -34,3 +34,25 @@ def test_window_decode_is_weight_streaming_time():
     # cap (Eq. 6 with R15): one 49.8 MB replica fits the window at 770 GB/s, two do not
     cap = w * 770_000 // (6 * H * F * 1000)
     assert cap == 1
+
+
+def test_bench_placement_policies():
+    """bench.py's host-side policies: the dedup wire when ranks span processes (NVLink), and the
+    fused gate + predictor stage 1 when one process hosts several ranks (HBM-bound dispatch);
+    shapes the fused path does not support (E % 32, k > 8) keep the aux-stream predictor."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    import probe_inputs as pi
+    a = bench.parse_args([])
+    assert a.wire == "auto" and a.gate_fuse == "auto"
+    assert not bench._wire_dedup(a, 1) and bench._wire_dedup(a, 8)
+    assert bench._gate_fuse(a, 8, pi.C1) and bench._gate_fuse(a, 4, pi.C3)
+    assert not bench._gate_fuse(a, 1, pi.C1)                       # one rank per GPU: paper's placement
+    assert not bench._gate_fuse(a, 2, pi.C0)                       # E = 8: not a multiple of 32
+    assert not bench._gate_fuse(a, 8, pi.C1.with_(k=9))            # top-k above the fused select's 8
+    assert bench._gate_fuse(bench.parse_args(["--gate-fuse", "1"]), 1, pi.C1)
+    assert not bench._gate_fuse(bench.parse_args(["--gate-fuse", "0"]), 8, pi.C1)
+    with pytest.raises(SystemExit):
+        bench.parse_args(["--warmup", "2"])                        # W >= 3 (timing rules)
