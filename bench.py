@@ -579,7 +579,7 @@ def measure(shape, args, env, light=False, dedup=None, predispatch=False):
                             "planner_iterations": stats[0]}}
     if rank == 0:
         cpu = None
-        if not args.no_cpu:
+        if not args.no_cpu and world == 1:      # the oracle baseline: rank 0 at N = 1 only
             inp = oracle_inputs_cpu(shape, args.zipf)
             cpu = cpu_baseline(inp, (alpha_ps, beta_ps, n_sat, bw_Bpus, gemm_ns), args.cpu_tokens)
             del inp
