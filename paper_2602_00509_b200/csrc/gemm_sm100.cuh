@@ -757,6 +757,11 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                          const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmC,
                          const __grid_constant__ CUtensorMap tmA2, GemmSched* __restrict__ sched, int K, int K2) {
   using L = Gemm2Smem<BN, STAGES, EW, NBUF>;
+  // BN = 512 (wide tile, non-SwiGLU groups only): two N = 256 UMMAs per k-step into the whole
+  // 512-column TMEM, so ONE accumulator (the epilogue no longer overlaps the next tile's
+  // MMAs); each CTA loads two 128-row B boxes per k-block.  Half the A bytes per FLOP.
+  constexpr int NACC = BN >= 512 ? 1 : 2;
+  constexpr int TCOLS = BN >= 512 ? 512 : 2 * BN;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -798,7 +803,7 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
     ptx::tma_prefetch_desc(&tmB1);
     if (K2 > 0) ptx::tma_prefetch_desc(&tmA2);
   }
-  if (warp == 2) ptx::tmem_alloc_cg2<2 * BN>(tmem_slot);
+  if (warp == 2) ptx::tmem_alloc_cg2<TCOLS>(tmem_slot);
   ptx::tc_fence_before();
   ptx::cluster_sync();          // barrier inits visible to the peer, TMEM allocated in both CTAs
   ptx::tc_fence_after();
@@ -860,8 +865,15 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
           if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (L::A_BYTES + L::B_BYTES));
           if (pol_a) ptx::tma_load_2d_cg2_hint(ta, &full[stage], sA + stage * L::A_BYTES, kc, arow, pol_a);
           else ptx::tma_load_2d_cg2(ta, &full[stage], sA + stage * L::A_BYTES, kc, arow);
-          if (pol_b) ptx::tma_load_2d_cg2_hint(tb, &full[stage], sB + stage * L::B_BYTES, kc, brow, pol_b);
-          else ptx::tma_load_2d_cg2(tb, &full[stage], sB + stage * L::B_BYTES, kc, brow);
+          if constexpr (BN >= 512) {
+            // N-rows [i·256, i·256 + 256) of UMMA i split 128 / 128 between the pair's CTAs
+            const int b0r = G.b_row + nb * BN + static_cast<int>(rank) * 128;
+            ptx::tma_load_2d_cg2(tb, &full[stage], sB + stage * L::B_BYTES, kc, b0r);
+            ptx::tma_load_2d_cg2(tb, &full[stage], sB + stage * L::B_BYTES + 128 * 128, kc, b0r + 256);
+          } else {
+            if (pol_b) ptx::tma_load_2d_cg2_hint(tb, &full[stage], sB + stage * L::B_BYTES, kc, brow, pol_b);
+            else ptx::tma_load_2d_cg2(tb, &full[stage], sB + stage * L::B_BYTES, kc, brow);
+          }
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -870,7 +882,7 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader CTA only)
     if (leader) {
-      constexpr uint32_t idesc = ptx::idesc_bf16_f32(256, BN);
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(256, BN >= 512 ? 256 : BN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -894,8 +906,12 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
             const uint64_t a0 = ptx::sdesc_sw128(ptx::smem_u32(sA + stage * L::A_BYTES));
             const uint64_t b0 = ptx::sdesc_sw128(ptx::smem_u32(sB + stage * L::B_BYTES));
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
+            for (int k = 0; k < 4; ++k) {
               ptx::umma_bf16_ss_cg2(d, a0 + 2 * k, b0 + 2 * k, idesc, (kb | k) != 0);
+              if constexpr (BN >= 512) {   // second N = 256 half: B box at +16 KB (1024 16-byte units), TMEM cols +256
+                ptx::umma_bf16_ss_cg2(d + 256, a0 + 2 * k, b0 + 1024 + 2 * k, idesc, (kb | k) != 0);
+              }
+            }
             ptx::umma_commit_cg2(&empty[stage], 0x3);
           }
           __syncwarp();
@@ -903,8 +919,7 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
         }
         if (lane == 0) ptx::umma_commit_cg2(&tfull[acc], 0x3);
         __syncwarp();
-        acc ^= 1;
-        if (acc == 0) aphase ^= 1;
+        if (++acc == NACC) { acc = 0; aphase ^= 1; }
       }
     }
   } else if (warp >= 4) {
@@ -949,8 +964,7 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
         if (leader) ptx::mbar_arrive(&tempty[acc]);
         else ptx::mbar_arrive_cluster(tempty_leader0 + acc * 8);
       }
-      acc ^= 1;
-      if (acc == 0) aphase ^= 1;
+      if (++acc == NACC) { acc = 0; aphase ^= 1; }
     }
     if (lane == 0) ptx::bulk_wait<0>();
   }
@@ -966,7 +980,7 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
   ptx::cluster_sync();          // no remote arrive / DSMEM access after this point
   if (warp == 2) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc_cg2<2 * BN>(tmem_base);
+    ptx::tmem_dealloc_cg2<TCOLS>(tmem_base);
   }
 }
 

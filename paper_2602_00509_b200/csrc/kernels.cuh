@@ -646,6 +646,7 @@ struct LayoutOut {
 struct LayoutIn {
   int nparts;                   // >1: partition the expert GEMMs by local rank (EP emulation)
   int tile_m;                   // 128 (1-CTA expert GEMMs) or 256 (CTA-pair expert GEMMs)
+  int bn2;                      // GEMM2 tile width: 256, or 512 (CTA-pair 256×512 one-accumulator kernel)
   const int32_t* board_actual;  // [G][E]
   const int32_t* quota;         // [G][E][G] or null (static EP)
   const int32_t* replicas;      // [G][3] or null
@@ -810,7 +811,7 @@ __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o
     o.s1->g[i] = g1;
     o.s2->g[i] = g2;
     t1[i] = gemm_ntiles(g1, 256, in.tile_m);
-    t2[i] = gemm_ntiles(g2, 256, in.tile_m);
+    t2[i] = gemm_ntiles(g2, in.bn2, in.tile_m);
   }
   __syncthreads();
   // (7) tile prefix (warp 0: s1, warp 1: s2), warp-parallel exclusive scan in chunks of 32

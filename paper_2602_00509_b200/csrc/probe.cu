@@ -243,6 +243,7 @@ struct probe_ctx_s {
   bool fused_epi_topk = false;  // top-k in the GEMM epilogue instead of k_select (probe_set_option)
   bool pair_gemm = true;        // expert GEMMs on CTA pairs (cta_group::2); option turns it off
   bool y_wide = true;           // fp16 Y by 64-column TMA stores (PROBE_Y_WIDE=0 at init: 32-column, A/B)
+  bool gemm2_512 = true;        // GEMM2 on 256×512 CTA-pair tiles (PROBE_G2_512=0 at init: 256×256, A/B)
   // distillation workspace (NEXT-1), allocated on the first probe_distill_grad
   uint8_t* dbuf = nullptr;
   size_t dbytes = 0;
@@ -292,7 +293,8 @@ probe_status fail(probe_ctx ctx, probe_status st, const char* fmt, ...) {
 // predictor GEMMs (PROBE_OPT_PRED_MAXREG).  The numbering is the probe_bench_gemm `variant`
 // argument; the other numbers were configurations measured slower in round 1 and removed.
 enum GemmVariant { V_128_6_4 = 0, V_256_4_4 = 1, V_2CTA_256_6_4 = 6, V_256_4_4_EXP = 10, V_128_6_4_R192 = 11,
-                   V_2CTA_128_8_4 = 12 /* CTA pair, 256×128 tiles, 8 stages: the predictor's N = E = 128 GEMM */ };
+                   V_2CTA_128_8_4 = 12 /* CTA pair, 256×128 tiles, 8 stages: the predictor's N = E = 128 GEMM */,
+                   V_2CTA_512_4_4 = 13 /* CTA pair, 256×512 tiles (one TMEM accumulator), 4 stages: non-SwiGLU only */ };
 
 // Expert GEMMs leave registers for one 128-thread prefetch CTA per SM (a9 part 1 runs beside them):
 // 256 × 224 + 128 × 48 = 62 K.  Splits that fill exactly 64 K (240 + 32, 232 + 48) did not
@@ -355,17 +357,20 @@ cudaError_t launch_gemm_v(int v, const CUtensorMap& a, const CUtensorMap& b0, co
     case V_128_6_4: return launch_gemm_t<128, 6, 4>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_256_4_4: return launch_gemm_t<256, 4, 4>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_2CTA_256_6_4: return launch_gemm_2cta<256, 6, 4, 1, kExpertMaxReg>(a, b0, b1, c, A2, s, K, K2, grid, st);
+    case V_2CTA_512_4_4: return launch_gemm_2cta<512, 4, 4, 1, kExpertMaxReg>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_256_4_4_EXP: return launch_gemm_t<256, 4, 4, 1, PROBE_EXP1_MAXREG>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_128_6_4_R192: return launch_gemm_t<128, 6, 4, 1, 192>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_2CTA_128_8_4: return launch_gemm_2cta<128, 8, 4, 1, kExpertMaxReg>(a, b0, b1, c, A2, s, K, K2, grid, st);
   }
   return cudaErrorInvalidValue;
 }
-int variant_bn(int v) { return (v == V_128_6_4 || v == V_128_6_4_R192 || v == V_2CTA_128_8_4) ? 128 : 256; }
-int variant_tm(int v) { return (v == V_2CTA_256_6_4 || v == V_2CTA_128_8_4) ? 256 : 128; }
+int variant_bn(int v) {
+  return (v == V_128_6_4 || v == V_128_6_4_R192 || v == V_2CTA_128_8_4) ? 128 : (v == V_2CTA_512_4_4 ? 512 : 256);
+}
+int variant_tm(int v) { return (v == V_2CTA_256_6_4 || v == V_2CTA_128_8_4 || v == V_2CTA_512_4_4) ? 256 : 128; }
 bool variant_ok(int v) {
   return v == V_128_6_4 || v == V_256_4_4 || v == V_2CTA_256_6_4 || v == V_256_4_4_EXP || v == V_128_6_4_R192 ||
-         v == V_2CTA_128_8_4;
+         v == V_2CTA_128_8_4 || v == V_2CTA_512_4_4;
 }
 
 template <int BN>
@@ -602,6 +607,7 @@ probe_status probe_init(const probe_config* cfg, const uint64_t* peer_ptrs, void
   }
   const uint64_t GL = c.local_ranks, cap = c.recv_capacity, H = c.hidden, F = c.ffn;
   if (const char* yw = getenv("PROBE_Y_WIDE")) ctx->y_wide = yw[0] != '0';   // analysis A/B only
+  if (const char* g5 = getenv("PROBE_G2_512")) ctx->gemm2_512 = g5[0] != '0';
   bool ok = make_map(&ctx->map_recv, ctx->local_base[PROBE_BUF_RECV], GL * cap, H, 128) &&
             make_map(&ctx->map_act, ctx->scratch + ctx->sl.act, GL * cap, F, 128) &&
             make_map(&ctx->map_rw13, ctx->local_base[PROBE_BUF_REP_W13], GL * 2 * kMaxRb * 2 * F, H, 128) &&
@@ -780,6 +786,8 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   // C2 expert GEMMs 1.45 ms on pairs vs 1.15 ms on single CTAs)
   const bool pair = ctx->pair_gemm && static_cast<int64_t>(T) * d.k * d.G >= 256LL * d.E;
   li.tile_m = pair ? 256 : 128;
+  const bool g2w = pair && !f32 && ctx->gemm2_512;   // GEMM2 on 256×512 tiles (V_2CTA_512_4_4)
+  li.bn2 = g2w ? 512 : 256;
   li.act = ctx->scratch + s.act;
   li.y_local = ctx->local_base[PROBE_BUF_Y];
   li.f32 = f32;
@@ -852,10 +860,11 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   if (f32) {
     CK(launch_sgemm(ctx, lo.s2, ctx->scratch + s.act, w2, ctx->local_base[PROBE_BUF_REP_W2], d.F, st));
   } else {
-    CK(launch_gemm_v(vexp, ctx->map_act, *m2, ctx->map_rw2, ctx->map_y, lo.s2, d.F, ctx->num_sms, st));
+    const int v2 = g2w ? V_2CTA_512_4_4 : vexp;
+    CK(launch_gemm_v(v2, ctx->map_act, *m2, ctx->map_rw2, ctx->map_y, lo.s2, d.F, ctx->num_sms, st));
     if (ctx->dbg_gemm2_repeat && li.nparts == 0) {   // same result again, after a GEMM2 instead of a GEMM1
       CK(cudaMemsetAsync(&lo.s2->counter, 0, sizeof(int32_t), st));
-      CK(launch_gemm_v(vexp, ctx->map_act, *m2, ctx->map_rw2, ctx->map_y, lo.s2, d.F, ctx->num_sms, st));
+      CK(launch_gemm_v(v2, ctx->map_act, *m2, ctx->map_rw2, ctx->map_y, lo.s2, d.F, ctx->num_sms, st));
     }
   }
   ++ctx->launches;
@@ -1314,7 +1323,7 @@ probe_status probe_bench_gemm(const void* A, int64_t a_rows, const void* B, int6
   hs->total_tiles = acc;
   hs->tile_m = TM;
   CUtensorMap ma, mb, mc;
-  if (!make_map(&ma, A, a_rows, K, 128) || !make_map(&mb, B, b_rows, K, BN / 2))
+  if (!make_map(&ma, A, a_rows, K, 128) || !make_map(&mb, B, b_rows, K, BN >= 512 ? 128 : BN / 2))
     return fail(nullptr, PROBE_ECUDA, "tensor map encode failed");
   if (emode == EPI_F32 && n_out % 32 == 0) {
     if (!make_map_f32_out(&mc, C, c_rows, n_out)) return fail(nullptr, PROBE_ECUDA, "tensor map encode failed");
