@@ -757,7 +757,7 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                          const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmC,
                          const __grid_constant__ CUtensorMap tmA2, GemmSched* __restrict__ sched, int K, int K2) {
   using L = Gemm2Smem<BN, STAGES, EW, NBUF>;
-  // BN = 512 (wide tile, non-SwiGLU groups only): two N = 256 UMMAs per k-step into the whole
+  // BN = 512 (wide tile): two N = 256 UMMAs per k-step into the whole
   // 512-column TMEM, so ONE accumulator (the epilogue no longer overlaps the next tile's
   // MMAs); each CTA loads two 128-row B boxes per k-block.  Half the A bytes per FLOP.
   constexpr int NACC = BN >= 512 ? 1 : 2;
@@ -866,10 +866,12 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
           if (pol_a) ptx::tma_load_2d_cg2_hint(ta, &full[stage], sA + stage * L::A_BYTES, kc, arow, pol_a);
           else ptx::tma_load_2d_cg2(ta, &full[stage], sA + stage * L::A_BYTES, kc, arow);
           if constexpr (BN >= 512) {
-            // N-rows [i·256, i·256 + 256) of UMMA i split 128 / 128 between the pair's CTAs
-            const int b0r = G.b_row + nb * BN + static_cast<int>(rank) * 128;
+            // N-rows [i·256, i·256 + 256) of UMMA i split 128 / 128 between the pair's CTAs;
+            // SwiGLU: UMMA 0 = gate rows, UMMA 1 = the matching up rows (F further)
+            const bool sw = G.mode == EPI_SWIGLU;
+            const int b0r = G.b_row + nb * (sw ? BN / 2 : BN) + static_cast<int>(rank) * 128;
             ptx::tma_load_2d_cg2(tb, &full[stage], sB + stage * L::B_BYTES, kc, b0r);
-            ptx::tma_load_2d_cg2(tb, &full[stage], sB + stage * L::B_BYTES + 128 * 128, kc, b0r + 256);
+            ptx::tma_load_2d_cg2(tb, &full[stage], sB + stage * L::B_BYTES + 128 * 128, kc, b0r + (sw ? G.n : 256));
           } else {
             if (pol_b) ptx::tma_load_2d_cg2_hint(tb, &full[stage], sB + stage * L::B_BYTES, kc, brow, pol_b);
             else ptx::tma_load_2d_cg2(tb, &full[stage], sB + stage * L::B_BYTES, kc, brow);

@@ -646,7 +646,7 @@ struct LayoutOut {
 struct LayoutIn {
   int nparts;                   // >1: partition the expert GEMMs by local rank (EP emulation)
   int tile_m;                   // 128 (1-CTA expert GEMMs) or 256 (CTA-pair expert GEMMs)
-  int bn2;                      // GEMM2 tile width: 256, or 512 (CTA-pair 256×512 one-accumulator kernel)
+  int bn1, bn2;                 // GEMM1 / GEMM2 tile widths: 256, or 512 (CTA-pair 256×512 one-accumulator kernel)
   const int32_t* board_actual;  // [G][E]
   const int32_t* quota;         // [G][E][G] or null (static EP)
   const int32_t* replicas;      // [G][3] or null
@@ -810,7 +810,7 @@ __global__ void __launch_bounds__(512) k_layout(Dims d, LayoutIn in, LayoutOut o
     g2.out = static_cast<uint8_t*>(in.y_local) + static_cast<size_t>(arow) * d.H * (in.f32 ? 4 : 2);
     o.s1->g[i] = g1;
     o.s2->g[i] = g2;
-    t1[i] = gemm_ntiles(g1, 256, in.tile_m);
+    t1[i] = gemm_ntiles(g1, in.bn1, in.tile_m);
     t2[i] = gemm_ntiles(g2, in.bn2, in.tile_m);
   }
   __syncthreads();

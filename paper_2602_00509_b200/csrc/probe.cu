@@ -244,6 +244,7 @@ struct probe_ctx_s {
   bool pair_gemm = true;        // expert GEMMs on CTA pairs (cta_group::2); option turns it off
   bool y_wide = true;           // fp16 Y by 64-column TMA stores (PROBE_Y_WIDE=0 at init: 32-column, A/B)
   bool gemm2_512 = true;        // GEMM2 on 256×512 CTA-pair tiles (PROBE_G2_512=0 at init: 256×256, A/B)
+  bool gemm1_512 = false;       // GEMM1 likewise (PROBE_G1_512=1 at init, A/B)
   // distillation workspace (NEXT-1), allocated on the first probe_distill_grad
   uint8_t* dbuf = nullptr;
   size_t dbytes = 0;
@@ -608,6 +609,7 @@ probe_status probe_init(const probe_config* cfg, const uint64_t* peer_ptrs, void
   const uint64_t GL = c.local_ranks, cap = c.recv_capacity, H = c.hidden, F = c.ffn;
   if (const char* yw = getenv("PROBE_Y_WIDE")) ctx->y_wide = yw[0] != '0';   // analysis A/B only
   if (const char* g5 = getenv("PROBE_G2_512")) ctx->gemm2_512 = g5[0] != '0';
+  if (const char* g5 = getenv("PROBE_G1_512")) ctx->gemm1_512 = g5[0] != '0';
   bool ok = make_map(&ctx->map_recv, ctx->local_base[PROBE_BUF_RECV], GL * cap, H, 128) &&
             make_map(&ctx->map_act, ctx->scratch + ctx->sl.act, GL * cap, F, 128) &&
             make_map(&ctx->map_rw13, ctx->local_base[PROBE_BUF_REP_W13], GL * 2 * kMaxRb * 2 * F, H, 128) &&
@@ -787,7 +789,9 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   const bool pair = ctx->pair_gemm && static_cast<int64_t>(T) * d.k * d.G >= 256LL * d.E;
   li.tile_m = pair ? 256 : 128;
   const bool g2w = pair && !f32 && ctx->gemm2_512;   // GEMM2 on 256×512 tiles (V_2CTA_512_4_4)
+  const bool g1w = pair && !f32 && ctx->gemm1_512;   // GEMM1 (SwiGLU) on 256×512 tiles (256 act columns)
   li.bn2 = g2w ? 512 : 256;
+  li.bn1 = g1w ? 512 : 256;
   li.act = ctx->scratch + s.act;
   li.y_local = ctx->local_base[PROBE_BUF_Y];
   li.f32 = f32;
@@ -852,7 +856,8 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   if (f32) {
     CK(launch_sgemm(ctx, lo.s1, ctx->local_base[PROBE_BUF_RECV], w13, ctx->local_base[PROBE_BUF_REP_W13], d.H, st));
   } else {
-    CK(launch_gemm_v(vexp, ctx->map_recv, *m13, ctx->map_rw13, ctx->map_act_out, lo.s1, d.H, ctx->num_sms, st));
+    CK(launch_gemm_v(g1w ? V_2CTA_512_4_4 : vexp, ctx->map_recv, *m13, ctx->map_rw13, ctx->map_act_out, lo.s1, d.H,
+                     ctx->num_sms, st));
   }
   ++ctx->launches;
   if (ctx->dbg_gap_us > 0) k_spin<<<1, 1, 0, st>>>(ctx->dbg_gap_us * 1000ll);

@@ -89,7 +89,7 @@ def test_gemm_multi_tile_per_cta_exact(mode, N, K, rows, variant):
         assert bad.numel() == 0, (mode, N, K, rows, bad[:10].flatten().tolist())
 
 
-@pytest.mark.parametrize("variant", [1, 6, 10])
+@pytest.mark.parametrize("variant", [1, 6, 10, 13])
 def test_gemm_multi_tile_swiglu(variant):
     from paper_2602_00509_b200 import bench_gemm
     F, K, rows = 768, 2048, 20000

@@ -1,7 +1,7 @@
 """Expert-GEMM shapes of the C1 layer through the C-ABI timing hook (probe_bench_gemm):
 GEMM2 (K = F = 768, N = H = 2048, fp16 Y) on the CTA-pair 256×256 kernel (variant 6) and the
 256×512 one-accumulator kernel (variant 13), and GEMM1 (K = H = 2048, SwiGLU over 2F = 1536 →
-bf16 act, variant 6), on 137 uniform groups of the C1 layer's total rows.  PROBE_LIB_PATH
+bf16 act, variants 6 and 13), on 137 uniform groups of the C1 layer's total rows.  PROBE_LIB_PATH
 selects the library build (A/B of two builds).  Prints one JSON line."""
 import json
 import os
@@ -30,6 +30,7 @@ B1 = (torch.randn(slots * 2 * F, H, device=dev) / H ** 0.5).to(torch.bfloat16)
 act = torch.empty(rows, F, dtype=torch.bfloat16, device=dev)
 groups1 = [[i * per, per, (i % slots) * 2 * F, i * per] for i in range(ng)]
 for rep in range(3):
-    ms1 = bench_gemm(A1, B1, groups1, 2 * F, 1, act, variant=6, reps=10)  # mode 1: EPI_SWIGLU
-    out.setdefault("gemm1_TFs", []).append(round(4.0 * per * ng * H * F / ms1 / 1e9, 1))
+    for v in (6, 13):
+        ms1 = bench_gemm(A1, B1, groups1, 2 * F, 1, act, variant=v, reps=10)  # mode 1: EPI_SWIGLU
+        out.setdefault(f"gemm1_v{v}_TFs", []).append(round(4.0 * per * ng * H * F / ms1 / 1e9, 1))
 print(json.dumps(out))
