@@ -108,6 +108,8 @@ CASES = {
                                      residual=False, fuse_gate_predictor=True),
     "gate-fused-ragged-h": CaseCfg(pi.C0.with_(name="gfh", E=32, k=4, H=320, F=320, T=300, G=4), zipf_s=1.3,
                                    bias=True, fuse_gate_predictor=True),    # h = 80: manual bf16 stores
+    "gate-fused-ep-emulation": CaseCfg(pi.C0.with_(name="gfem", E=64, k=8, H=512, F=384, T=300, G=8), zipf_s=1.2,
+                                       ep_emulation=True, fuse_gate_predictor=True),   # the bench's emulated line
     "gate-fused-E256": CaseCfg(pi.C0.with_(name="gfe", E=256, k=8, H=1024, F=128, T=64, G=8), zipf_s=1.0,
                                residual_kind="relabel", fuse_gate_predictor=True),
     # the dedup-natural draw ("dnat") again, with pre-dispatch and the fused gate on top; on
