@@ -301,11 +301,13 @@ __device__ __forceinline__ void epi_chunk(float* tiles, int& tsel, int lane, con
 // j ^ (r & 7)) and leave in ONE tensor store of full 128-byte row segments — half the TMA
 // store operations (and half-line writes) of two 64-byte-row stores.  The 4 KB staging slot
 // is single-buffered: the previous store must have finished reading it.
+template <int NB>
 __device__ __forceinline__ void epi_chunk64_f16(float* tiles, int& tsel, int lane, const uint32_t (&va)[32],
                                                 const uint32_t (&vb)[32], const GemmGroup& G,
                                                 const CUtensorMap* tmC, int row0, int col0, uint64_t store_pol) {
-  char* tile = reinterpret_cast<char*>(tiles);
-  if (lane == 0) ptx::bulk_wait_read<0>();
+  const int slot = NB > 1 ? (tsel & 1) : 0;     // NB = 2: two 4 KB tiles, one store in flight while staging
+  char* tile = reinterpret_cast<char*>(tiles) + slot * 4096;
+  if (lane == 0) ptx::bulk_wait_read<NB - 1>();
   __syncwarp();
   bool big = false;
 #pragma unroll
@@ -345,7 +347,7 @@ __device__ __forceinline__ void epi_chunk64_f16(float* tiles, int& tsel, int lan
     if (lane == 0) ptx::bulk_commit();     // an empty group keeps one group per staged tile
   }
   __syncwarp();
-  tsel = 0x200;
+  tsel = 0x200 | (slot ^ 1);
 }
 
 // Top-k by sorting networks (R3, R4): keys ordered by (value ↓, id ↑), a total order, so any
@@ -485,7 +487,7 @@ __device__ __forceinline__ void epi_tile(uint32_t tb, int lane, int part, const 
       for (int c = 0; c < BN / 32; c += 2) {
         uint32_t va[32], vb[32];
         ptx::tmem_ld32x2_wait(tb + c * 32, va, tb + (c + 1) * 32, vb);
-        epi_chunk64_f16(tiles, tsel, lane, va, vb, G, tmC, row0, nb * BN + c * 32, store_pol);
+        epi_chunk64_f16<NB>(tiles, tsel, lane, va, vb, G, tmC, row0, nb * BN + c * 32, store_pol);
       }
       return;
     }
@@ -746,7 +748,9 @@ struct Gemm2Smem {
   static constexpr int B_BYTES = (BN / 2) * 128;
   static constexpr int BAR_OFF = STAGES * (A_BYTES + B_BYTES);
   static constexpr int TS_OFF = BAR_OFF + (2 * STAGES + 4 + 2 * kTileQ) * 8 + 16 + kTileQ * 4;
-  static constexpr int EPI_OFF = (TS_OFF + (kMaxGroups + 1) * 4 + 1023) / 1024 * 1024;
+  // the 256×512 kernel with double-buffered wide stores fits 227 KB only with a 256-group table
+  static constexpr int TSCAP = (BN >= 512 && NBUF == 2) ? 256 : kMaxGroups;
+  static constexpr int EPI_OFF = (TS_OFF + (TSCAP + 1) * 4 + 1023) / 1024 * 1024;
   static constexpr int NB = NBUF;
   static constexpr int BYTES = EPI_OFF + EW * NB * 4096 + 1024;
 };
@@ -783,6 +787,7 @@ grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
   const int ng = sched->num_groups;
   GEMM_STAT(long long acc_st[7] = {0, 0, 0, 0, 0, 0, 0});
   GEMM_STAT(const long long t_kernel0 = clock64());
+  if (ng > L::TSCAP) __trap();                  // the host picks this instance only for ≤ TSCAP groups
   for (int i = threadIdx.x; i < ng; i += blockDim.x) ts[i] = sched->g[i].tile_start;
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {

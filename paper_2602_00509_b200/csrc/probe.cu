@@ -245,6 +245,7 @@ struct probe_ctx_s {
   bool y_wide = true;           // fp16 Y by 64-column TMA stores (PROBE_Y_WIDE=0 at init: 32-column, A/B)
   bool gemm2_512 = true;        // GEMM2 on 256×512 CTA-pair tiles (PROBE_G2_512=0 at init: 256×256, A/B)
   bool gemm1_512 = false;       // GEMM1 likewise (PROBE_G1_512=1 at init, A/B)
+  bool g2_nb2 = true;           // GEMM2 256×512 with double-buffered wide stores (PROBE_G2_NB2=0 at init, A/B)
   // distillation workspace (NEXT-1), allocated on the first probe_distill_grad
   uint8_t* dbuf = nullptr;
   size_t dbytes = 0;
@@ -295,7 +296,8 @@ probe_status fail(probe_ctx ctx, probe_status st, const char* fmt, ...) {
 // argument; the other numbers were configurations measured slower in round 1 and removed.
 enum GemmVariant { V_128_6_4 = 0, V_256_4_4 = 1, V_2CTA_256_6_4 = 6, V_256_4_4_EXP = 10, V_128_6_4_R192 = 11,
                    V_2CTA_128_8_4 = 12 /* CTA pair, 256×128 tiles, 8 stages: the predictor's N = E = 128 GEMM */,
-                   V_2CTA_512_4_4 = 13 /* CTA pair, 256×512 tiles (one TMEM accumulator), 4 stages: non-SwiGLU only */ };
+                   V_2CTA_512_4_4 = 13 /* CTA pair, 256×512 tiles (one TMEM accumulator), 4 stages */,
+                   V_2CTA_512_4_4_NB2 = 14 /* the same with double-buffered 64-column stores (≤ 256 groups) */ };
 
 // Expert GEMMs leave registers for one 128-thread prefetch CTA per SM (a9 part 1 runs beside them):
 // 256 × 224 + 128 × 48 = 62 K.  Splits that fill exactly 64 K (240 + 32, 232 + 48) did not
@@ -359,6 +361,7 @@ cudaError_t launch_gemm_v(int v, const CUtensorMap& a, const CUtensorMap& b0, co
     case V_256_4_4: return launch_gemm_t<256, 4, 4>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_2CTA_256_6_4: return launch_gemm_2cta<256, 6, 4, 1, kExpertMaxReg>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_2CTA_512_4_4: return launch_gemm_2cta<512, 4, 4, 1, kExpertMaxReg>(a, b0, b1, c, A2, s, K, K2, grid, st);
+    case V_2CTA_512_4_4_NB2: return launch_gemm_2cta<512, 4, 4, 2, kExpertMaxReg>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_256_4_4_EXP: return launch_gemm_t<256, 4, 4, 1, PROBE_EXP1_MAXREG>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_128_6_4_R192: return launch_gemm_t<128, 6, 4, 1, 192>(a, b0, b1, c, A2, s, K, K2, grid, st);
     case V_2CTA_128_8_4: return launch_gemm_2cta<128, 8, 4, 1, kExpertMaxReg>(a, b0, b1, c, A2, s, K, K2, grid, st);
@@ -366,12 +369,16 @@ cudaError_t launch_gemm_v(int v, const CUtensorMap& a, const CUtensorMap& b0, co
   return cudaErrorInvalidValue;
 }
 int variant_bn(int v) {
-  return (v == V_128_6_4 || v == V_128_6_4_R192 || v == V_2CTA_128_8_4) ? 128 : (v == V_2CTA_512_4_4 ? 512 : 256);
+  return (v == V_128_6_4 || v == V_128_6_4_R192 || v == V_2CTA_128_8_4)
+             ? 128
+             : ((v == V_2CTA_512_4_4 || v == V_2CTA_512_4_4_NB2) ? 512 : 256);
 }
-int variant_tm(int v) { return (v == V_2CTA_256_6_4 || v == V_2CTA_128_8_4 || v == V_2CTA_512_4_4) ? 256 : 128; }
+int variant_tm(int v) {
+  return (v == V_2CTA_256_6_4 || v == V_2CTA_128_8_4 || v == V_2CTA_512_4_4 || v == V_2CTA_512_4_4_NB2) ? 256 : 128;
+}
 bool variant_ok(int v) {
   return v == V_128_6_4 || v == V_256_4_4 || v == V_2CTA_256_6_4 || v == V_256_4_4_EXP || v == V_128_6_4_R192 ||
-         v == V_2CTA_128_8_4 || v == V_2CTA_512_4_4;
+         v == V_2CTA_128_8_4 || v == V_2CTA_512_4_4 || v == V_2CTA_512_4_4_NB2;
 }
 
 template <int BN>
@@ -610,6 +617,7 @@ probe_status probe_init(const probe_config* cfg, const uint64_t* peer_ptrs, void
   if (const char* yw = getenv("PROBE_Y_WIDE")) ctx->y_wide = yw[0] != '0';   // analysis A/B only
   if (const char* g5 = getenv("PROBE_G2_512")) ctx->gemm2_512 = g5[0] != '0';
   if (const char* g5 = getenv("PROBE_G1_512")) ctx->gemm1_512 = g5[0] != '0';
+  if (const char* g5 = getenv("PROBE_G2_NB2")) ctx->g2_nb2 = g5[0] != '0';
   bool ok = make_map(&ctx->map_recv, ctx->local_base[PROBE_BUF_RECV], GL * cap, H, 128) &&
             make_map(&ctx->map_act, ctx->scratch + ctx->sl.act, GL * cap, F, 128) &&
             make_map(&ctx->map_rw13, ctx->local_base[PROBE_BUF_REP_W13], GL * 2 * kMaxRb * 2 * F, H, 128) &&
@@ -865,7 +873,8 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   if (f32) {
     CK(launch_sgemm(ctx, lo.s2, ctx->scratch + s.act, w2, ctx->local_base[PROBE_BUF_REP_W2], d.F, st));
   } else {
-    const int v2 = g2w ? V_2CTA_512_4_4 : vexp;
+    // double-buffered wide stores need the 256-group table of the NB2 instance (C1: 8 × 19 groups)
+    const int v2 = !g2w ? vexp : (ctx->g2_nb2 && d.GL * (d.EL + kMaxRb) <= 256 ? V_2CTA_512_4_4_NB2 : V_2CTA_512_4_4);
     CK(launch_gemm_v(v2, ctx->map_act, *m2, ctx->map_rw2, ctx->map_y, lo.s2, d.F, ctx->num_sms, st));
     if (ctx->dbg_gemm2_repeat && li.nparts == 0) {   // same result again, after a GEMM2 instead of a GEMM1
       CK(cudaMemsetAsync(&lo.s2->counter, 0, sizeof(int32_t), st));

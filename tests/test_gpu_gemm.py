@@ -107,7 +107,8 @@ def test_gemm_multi_tile_swiglu(variant):
 
 @pytest.mark.parametrize("N,K,rows,variant", [(256, 256, 3000, 0), (2048, 768, 9000, 10), (2048, 768, 9000, 6),
                                               (512, 768, 30000, 6), (2880, 640, 1000, 6), (2880, 640, 1000, 10),
-                                              (2048, 768, 9000, 13), (2880, 640, 1000, 13), (512, 768, 30000, 13)])
+                                              (2048, 768, 9000, 13), (2880, 640, 1000, 13), (512, 768, 30000, 13),
+                                              (2048, 768, 9000, 14), (2880, 640, 1000, 14)])
 def test_gemm_f16_output_exact(N, K, rows, variant):
     """The expert-output epilogue (fp16 Y, D2): TMA tensor stores in SWIZZLE_64B for full
     32-row slabs, masked row stores for group tails.  Dyadic inputs make the fp32

@@ -1,6 +1,6 @@
 """Expert-GEMM shapes of the C1 layer through the C-ABI timing hook (probe_bench_gemm):
 GEMM2 (K = F = 768, N = H = 2048, fp16 Y) on the CTA-pair 256×256 kernel (variant 6) and the
-256×512 one-accumulator kernel (variant 13), and GEMM1 (K = H = 2048, SwiGLU over 2F = 1536 →
+256×512 one-accumulator kernel (variant 13; 14 with double-buffered stores), and GEMM1 (K = H = 2048, SwiGLU over 2F = 1536 →
 bf16 act, variants 6 and 13), on 137 uniform groups of the C1 layer's total rows.  PROBE_LIB_PATH
 selects the library build (A/B of two builds).  Prints one JSON line."""
 import json
@@ -21,7 +21,7 @@ B2 = (torch.randn(slots * H, F, device=dev) / F ** 0.5).to(torch.bfloat16)
 Y = torch.empty(rows, H, dtype=torch.float16, device=dev)
 out = {"lib": os.environ.get("PROBE_LIB_PATH", "in-tree")}
 for rep in range(3):
-    for v in (6, 13):
+    for v in (6, 13, 14):
         ms2 = bench_gemm(A2, B2, groups2, H, 7, Y, variant=v, reps=10)        # mode 7: EPI_F16
         out.setdefault(f"gemm2_v{v}_TFs", []).append(round(2.0 * per * ng * H * F / ms2 / 1e9, 1))
 del A2, B2, Y
