@@ -748,8 +748,8 @@ struct Gemm2Smem {
   static constexpr int B_BYTES = (BN / 2) * 128;
   static constexpr int BAR_OFF = STAGES * (A_BYTES + B_BYTES);
   static constexpr int TS_OFF = BAR_OFF + (2 * STAGES + 4 + 2 * kTileQ) * 8 + 16 + kTileQ * 4;
-  // the 256×512 kernel with double-buffered wide stores fits 227 KB only with a 256-group table
-  static constexpr int TSCAP = (BN >= 512 && NBUF == 2) ? 256 : kMaxGroups;
+  // the 256×512 kernel with double-buffered wide stores fits 227 KB only with a ≤ 384-group table
+  static constexpr int TSCAP = (BN >= 512 && NBUF == 2) ? 384 : kMaxGroups;
   static constexpr int EPI_OFF = (TS_OFF + (TSCAP + 1) * 4 + 1023) / 1024 * 1024;
   static constexpr int NB = NBUF;
   static constexpr int BYTES = EPI_OFF + EW * NB * 4096 + 1024;

@@ -297,7 +297,7 @@ probe_status fail(probe_ctx ctx, probe_status st, const char* fmt, ...) {
 enum GemmVariant { V_128_6_4 = 0, V_256_4_4 = 1, V_2CTA_256_6_4 = 6, V_256_4_4_EXP = 10, V_128_6_4_R192 = 11,
                    V_2CTA_128_8_4 = 12 /* CTA pair, 256×128 tiles, 8 stages: the predictor's N = E = 128 GEMM */,
                    V_2CTA_512_4_4 = 13 /* CTA pair, 256×512 tiles (one TMEM accumulator), 4 stages */,
-                   V_2CTA_512_4_4_NB2 = 14 /* the same with double-buffered 64-column stores (≤ 256 groups) */ };
+                   V_2CTA_512_4_4_NB2 = 14 /* the same with double-buffered 64-column stores (≤ 384 groups) */ };
 
 // Expert GEMMs leave registers for one 128-thread prefetch CTA per SM (a9 part 1 runs beside them):
 // 256 × 224 + 128 × 48 = 62 K.  Splits that fill exactly 64 K (240 + 32, 232 + 48) did not
@@ -873,8 +873,9 @@ probe_status probe_moe_forward(probe_ctx ctx, int32_t layer, const void* x, int3
   if (f32) {
     CK(launch_sgemm(ctx, lo.s2, ctx->scratch + s.act, w2, ctx->local_base[PROBE_BUF_REP_W2], d.F, st));
   } else {
-    // double-buffered wide stores need the 256-group table of the NB2 instance (C1: 8 × 19 groups)
-    const int v2 = !g2w ? vexp : (ctx->g2_nb2 && d.GL * (d.EL + kMaxRb) <= 256 ? V_2CTA_512_4_4_NB2 : V_2CTA_512_4_4);
+    // double-buffered wide stores need the ≤ 384-group table of the NB2 instance (C1: 8 × 19 groups,
+    // C3: 8 × 35)
+    const int v2 = !g2w ? vexp : (ctx->g2_nb2 && d.GL * (d.EL + kMaxRb) <= 384 ? V_2CTA_512_4_4_NB2 : V_2CTA_512_4_4);
     CK(launch_gemm_v(v2, ctx->map_act, *m2, ctx->map_rw2, ctx->map_y, lo.s2, d.F, ctx->num_sms, st));
     if (ctx->dbg_gemm2_repeat && li.nparts == 0) {   // same result again, after a GEMM2 instead of a GEMM1
       CK(cudaMemsetAsync(&lo.s2->counter, 0, sizeof(int32_t), st));
